@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Benchmark of the PICCS-Krylov CBCT hot path (BASELINE.json metric).
+
+metric: "fwd+back-proj GUPS; seconds per 20-iter PICCS-Krylov recon at 256^3".
+One step = one forward projection A x plus one backprojection A^T y of the
+c3 workload (256^3 volume at 0.5 mm, 384^2 detector at 0.5 mm, 60 views),
+inputs resident in HBM; value = 2 * M * n_angles * steps / time  [GUPS].
+The line also carries the 20-iteration IRN-PICCS reconstruction time at c3
+("recon"), the end-to-end numbers through the C ABI with host buffers ("e2e"),
+the roofline of the dominant kernel and the reference CPU baseline.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+N > 1 runs under torchrun: rank r projects angles r::N (forward) and
+backprojects z-slab r of the volume from all angles (no data-path collective;
+inputs are resident), the device time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M_TAG = "fwd+back-proj GUPS; seconds per 20-iter PICCS-Krylov recon at 256^3"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's own CPU code (oracle/_ref) on host cores
+# ---------------------------------------------------------------------------
+def cpu_reference_gups(n_angles_sample: int, repeats: int, warmup: int = 1, threads: int = 0):
+    """fwd+adj GUPS of the unmodified reference (oracle/_ref) on a c3 angle sample."""
+    import oracle
+    from oracle import Geometry, Grid, Oracle
+    if not os.path.exists(oracle.LIBS["ref"][0]):
+        try:
+            oracle.build("ref")
+        except Exception:
+            pass
+    kind = "reference" if os.path.exists(oracle.LIBS["ref"][0]) else "port"
+    o = Oracle("ref" if kind == "reference" else "ora")
+    if kind == "port":
+        oracle.build("ora")
+    nthreads = threads or os.cpu_count() or 1
+    o.set_threads(nthreads)
+    from paper_2509_08574_b200 import synth
+    cfg = synth.CONFIGS["c3"]
+    sel = synth.angles(cfg.followup_views)[:: max(1, cfg.followup_views // n_angles_sample)][:n_angles_sample]
+    grid = Grid(cfg.n, cfg.n, cfg.n, cfg.voxel, cfg.voxel, cfg.voxel)
+    geom = Geometry(synth.DSO, synth.DSD, cfg.det, cfg.det, cfg.pitch, cfg.pitch, sel)
+    _, prior, _ = synth.study("c3")
+    x = prior.astype(np.float64)
+    times = []
+    y = None
+    for r in range(warmup + repeats):
+        t0 = time.perf_counter()
+        y = o.forward(grid, geom, x)
+        o.adjoint(grid, geom, y)
+        dt = time.perf_counter() - t0
+        if r >= warmup:
+            times.append(dt)
+    m = cfg.n ** 3
+    gups = [2.0 * m * len(sel) / t / 1e9 for t in times]
+    return {"value": float(np.median(gups)), "unit": "GUPS", "cores": nthreads, "kind": kind,
+            "sample": f"c3 256^3/384^2, {len(sel)} of {cfg.followup_views} views, fwd+adj, "
+                      f"float64, median of {repeats} after {warmup} warm-up",
+            "seconds_per_step": float(np.median(times)), "all_gups": gups}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    steps, warmup = args.steps, args.warmup
+    res = cpu_reference_gups(args.ref_angles, steps, warmup)
+    value = res["value"]
+    line = {"impl": "reference", "metric": M_TAG, "value": round(value, 5), "unit": "GUPS",
+            "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
+            "ms_per_step": round(1e3 * res["seconds_per_step"], 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c3: 256^3 @0.5mm, 384^2 @0.5mm, 60 views (angle sample)",
+                       "sample_views": args.ref_angles},
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": round(value, 5), "unit": "GUPS", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import paper_2509_08574_b200 as k
+    from paper_2509_08574_b200 import synth
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = synth.CONFIGS["c3"]
+    M = cfg.n ** 3
+    na = cfg.followup_views
+    geom_all = k.ConeBeamGeometry(synth.DSO, synth.DSD, cfg.det, cfg.det, cfg.pitch, cfg.pitch,
+                                  synth.angles(na))
+    grid = k.GridSpec((cfg.n,) * 3, (cfg.voxel,) * 3)
+    log(f"[bench] rank {rank}/{ws}: generating c3 phantoms")
+    _, prior, follow = synth.study("c3")
+
+    # sharding: forward over angles r::ws, adjoint over z-slab r (all angles)
+    my_angles = np.arange(na)[rank::ws]
+    geom_f = k.ConeBeamGeometry(synth.DSO, synth.DSD, cfg.det, cfg.det, cfg.pitch, cfg.pitch,
+                                geom_all.angles[my_angles])
+    nz_loc = cfg.n // ws
+    z0 = rank * nz_loc
+    grid_b = k.GridSpec((cfg.n, cfg.n, nz_loc), (cfg.voxel,) * 3,
+                        (grid.origin[0], grid.origin[1], grid.origin[2] + z0 * cfg.voxel))
+    A_f = k.ConeBeamProjector(grid, geom_f, device=local)
+    A_b = A_f if ws == 1 else k.ConeBeamProjector(grid_b, geom_all, device=local)
+    nnz_f = A_f.count_nnz()
+    nnz_b = nnz_f if ws == 1 else A_b.count_nnz()
+    Nf = geom_f.ray_count()
+    Nb = geom_all.ray_count()
+    Mb = grid_b.count()
+
+    x_host = torch.from_numpy(prior).to(dev)
+    x = A_f.volume_to_native(x_host)
+    q = torch.empty(Nf, dtype=torch.float32, device=dev)
+    y = torch.rand(Nb, dtype=torch.float32, device=dev, generator=torch.Generator(dev).manual_seed(7))
+    back = torch.empty(Mb, dtype=torch.float32, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        A_f.apply(x, out=q)
+        A_b.apply_adjoint(y, out=back)
+
+    for _ in range(args.warmup):
+        flush.fill_(1.0)
+        step()
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        torch.distributed.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))  # evict L2 between timed steps (not timed)
+            e0, e1, e2 = ev[i]
+            e0.record(stream)
+            A_f.apply(x, out=q)
+            e1.record(stream)
+            A_b.apply_adjoint(y, out=back)
+            e2.record(stream)
+        torch.cuda.synchronize(dev)
+    t_f = [a.elapsed_time(b) * 1e-3 for a, b, _ in ev]
+    t_b = [b.elapsed_time(c) * 1e-3 for _, b, c in ev]
+    t_tot = sum(t_f) + sum(t_b)
+    if ws > 1:
+        tt = torch.tensor([t_tot], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_tot = float(tt.item())
+    gups = 2.0 * M * na * args.steps / t_tot / 1e9
+    mean_f, mean_b = float(np.mean(t_f)), float(np.mean(t_b))
+
+    # roofline of the dominant kernel (SURVEY §8d byte model, per launch)
+    peak, peak_src = measured_peak()
+    bytes_f = 4.0 * nnz_f + 4.0 * Nf
+    bytes_b = 4.0 * nnz_b + 4.0 * Mb
+    if mean_b >= mean_f:
+        dom = ("adjoint (adj_kernel)", bytes_b, mean_b)
+    else:
+        dom = ("forward (fwd_kernel)", bytes_f, mean_f)
+    achieved = dom[1] / dom[2] / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("adj_kernel" if "adj" in dom[0] else "fwd_kernel")
+        except Exception:
+            traffic = None
+
+    out = {"metric": M_TAG, "value": round(gups, 3), "unit": "GUPS", "n_gpus": ws,
+           "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(1e3 * t_tot / args.steps, 4), "higher_is_better": True,
+           "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic (seeded 20-ellipsoid c3 phantom, resident in HBM)",
+           "config": {"workload": "c3: A x + A^T y, 256^3 @0.5mm, 384^2 @0.5mm, 60 views, "
+                                  "DSO 1000 / DSD 1500",
+                      "M": M, "n_angles": na, "nnz": nnz_f if ws == 1 else None,
+                      "l2": "flushed (256 MiB write) between timed steps, flush not timed",
+                      "parallelism": f"angles/z-slabs x{ws}" if ws > 1 else "single GPU"},
+           "kernels_ms": {"forward": round(1e3 * mean_f, 4), "adjoint": round(1e3 * mean_b, 4)},
+           "gups_forward": round(M * len(my_angles) / mean_f / 1e9, 3),
+           "gups_adjoint": round(Mb * na / mean_b / 1e9, 3),
+           "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": round(achieved, 1),
+                        "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                        "traffic": traffic, "peak_source": peak_src,
+                        "algorithmic_bytes_per_launch": dom[1],
+                        "byte_model": "4*nnz + 4*N (A x) / 4*nnz + 4*M (A^T y), nnz = exact "
+                                      "Siddon intersections counted on device"},
+           "gpu_launches": 2 * args.steps, "clocks": clk.summary()}
+
+    # ---- end to end through the C ABI with host buffers (reference layouts) ----
+    if rank == 0 and not args.skip_e2e:
+        vol_h = torch.from_numpy(prior).pin_memory().numpy()
+        proj_h = torch.empty(Nf, dtype=torch.float32).pin_memory().numpy()
+        back_h = torch.empty(M, dtype=torch.float32).pin_memory().numpy()
+        for _ in range(max(1, args.warmup)):
+            A_f.apply(vol_h, out=proj_h)
+            A_f.apply_adjoint(proj_h, out=back_h)
+        te = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            A_f.apply(vol_h, out=proj_h)
+            A_f.apply_adjoint(proj_h, out=back_h)
+            te.append(time.perf_counter() - t0)
+        e2e_gups = 2.0 * M * len(my_angles) / float(np.mean(te)) / 1e9
+        out["e2e"] = {"value": round(e2e_gups, 3), "unit": "GUPS",
+                      "h2d_bytes_per_step": 4 * (M + Nf), "d2h_bytes_per_step": 4 * (Nf + M),
+                      "ms_per_step": round(1e3 * float(np.mean(te)), 3),
+                      "path": "kct_forward + kct_adjoint, pinned host, reference layouts"}
+
+    # ---- 20-iteration IRN-PICCS at c3 (the metric's second half) --------------
+    if rank == 0 and not args.skip_recon:
+        out["recon"] = run_recon(k, synth, cfg, grid, prior, follow, dev, args)
+
+    if rank == 0 and not args.skip_cpu:
+        try:
+            out["cpu_baseline"] = {kk: v for kk, v in cpu_reference_gups(args.ref_angles, 2).items()
+                                   if kk in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # report, do not fail the bench
+            out["cpu_baseline"] = {"value": None, "error": str(e)}
+    if ws > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def run_recon(k, synth, cfg, grid, prior, follow, dev, args):
+    import torch
+    na_p, na_f = cfg.prior_views, cfg.followup_views
+    geom_p = k.ConeBeamGeometry(synth.DSO, synth.DSD, cfg.det, cfg.det, cfg.pitch, cfg.pitch,
+                                synth.angles(na_p))
+    geom_f = k.ConeBeamGeometry(synth.DSO, synth.DSD, cfg.det, cfg.det, cfg.pitch, cfg.pitch,
+                                synth.angles(na_f))
+    Ap = k.ConeBeamProjector(grid, geom_p)
+    Af = k.ConeBeamProjector(grid, geom_f)
+    t0 = time.perf_counter()
+    # prior: 360-view noiseless scan of the prior phantom, 20-iteration CGLS (pinned)
+    xp_n = Ap.volume_to_native(torch.from_numpy(prior).to(dev))
+    bp_n = Ap.apply(xp_n)
+    prior_rec = k.cgls_recon(k.ProjectionSet(geom_p, bp_n), grid, 20, projector=Ap).volume
+    # follow-up: 60 views, Poisson I0 = 5e4 on the transmission
+    xf_n = Af.volume_to_native(torch.from_numpy(follow).to(dev))
+    pf = Af.proj_from_native(Af.apply(xf_n)).cpu().numpy()
+    b = synth.poisson_log(pf, cfg.i0, seed=1003)
+    b_n = Af.proj_to_native(torch.from_numpy(b).to(dev))
+    torch.cuda.synchronize(dev)
+    setup = time.perf_counter() - t0
+    params = k.RegularizationParams(alpha=cfg.alpha, outer_iters=cfg.outer, inner_iters=cfg.inner)
+    proj = k.ProjectionSet(geom_f, b_n)
+    reps = []
+    rep = None
+    for i in range(args.recon_warmup + args.recon_steps):
+        torch.cuda.synchronize(dev)
+        t = time.perf_counter()
+        rep = k.irn_piccs(proj, grid, prior_rec, params, projector=Af)
+        torch.cuda.synchronize(dev)
+        if i >= args.recon_warmup:
+            reps.append(time.perf_counter() - t)
+    x_ref = Af.volume_from_native(rep.volume).cpu().numpy()
+    rel = float(np.linalg.norm(x_ref - follow) / np.linalg.norm(follow))
+    # end to end: host float32 arrays in the reference layouts through kct_irn_piccs
+    prior_h = Af.volume_from_native(prior_rec).cpu().numpy()
+    proj_h = k.ProjectionSet(geom_f, b)
+    t = time.perf_counter()
+    rep_h = k.irn_piccs(proj_h, grid, prior_h, params, projector=Af)
+    e2e = time.perf_counter() - t
+    same = float(np.abs(rep_h.volume - x_ref).max())
+    return {"seconds_per_recon": round(float(np.median(reps)), 4),
+            "all_seconds": [round(r, 4) for r in reps],
+            "solve_seconds_reported": round(rep.solve_seconds, 4),
+            "e2e_seconds": round(e2e, 4), "e2e_h2d_bytes": 4 * (2 * grid.count() + geom_f.ray_count()),
+            "e2e_d2h_bytes": 4 * grid.count(), "e2e_max_abs_diff_vs_device_run": same,
+            "iterations": cfg.outer * cfg.inner, "outer_x_inner": f"{cfg.outer}x{cfg.inner}",
+            "alpha": cfg.alpha, "lambda": cfg.alpha, "tau": rep.tau,
+            "objective_history": [float(v) for v in rep.objective_history],
+            "rel_error_vs_followup_phantom": round(rel, 5),
+            "prior": "20-iter CGLS of a 360-view noiseless scan (computed on device, untimed)",
+            "setup_seconds_untimed": round(setup, 2),
+            "reference_cpu_seconds_survey_box": 329.2}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-angles", type=int, default=4)
+    ap.add_argument("--recon-steps", type=int, default=3)
+    ap.add_argument("--recon-warmup", type=int, default=1)
+    ap.add_argument("--skip-recon", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,161 @@
+/*
+ * kct.h — C ABI of the B200-native PICCS-Krylov CBCT core.
+ *
+ * Drop-in boundary for the hot path of the reference library `kryct`
+ * (header-only C++20, /root/reference/proj/include/kryct).  Every entry point
+ * below replaces one reference interface; the replaced symbol is cited as
+ * file:line next to it.  Plain C: POD structs, raw pointers, sizes and status
+ * codes — no C++ or torch types cross this boundary.
+ *
+ * Data layouts (KCT_LAYOUT_REFERENCE is what the reference uses):
+ *   volume       x-fastest  idx = i + nx*(j + ny*k)          types.hpp:86-88
+ *   projections  u-fastest  idx = iu + nu*(iv + nv*ia)       types.hpp:163-164
+ * KCT_LAYOUT_NATIVE is the device-internal layout the kernels run on:
+ *   volume       z-fastest  idx = k + nz*(i + nx*j)
+ *   projections  v-fastest  idx = iv + nv*(iu + nu*ia)
+ * Values cross the boundary as float32 (the reference promotes float32 files
+ * to double, io.hpp:48-49); reductions and solver scalars are float64.
+ *
+ * Status codes mirror the reference's error taxonomy and CLI exit codes
+ * (types.hpp:16-26, tools/kryct.cpp:120-128):
+ *   KCT_OK 0, KCT_ERR_INTERNAL 1, KCT_ERR_CONFIG 2 (ConfigError),
+ *   KCT_ERR_SOLVER 3 (SolverError), KCT_ERR_CUDA 4 (device failure).
+ * kct_last_error() returns the message of the last failure on this thread.
+ *
+ * Threading: a projector handle is bound to one device and is stream-ordered;
+ * calls on one handle must not run concurrently.  All functions synchronise
+ * the given stream before returning when any pointer is KCT_MEM_HOST.
+ */
+#ifndef KCT_H
+#define KCT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KCT_ABI_VERSION 1
+
+enum kct_status {
+    KCT_OK = 0,
+    KCT_ERR_INTERNAL = 1,
+    KCT_ERR_CONFIG = 2,
+    KCT_ERR_SOLVER = 3,
+    KCT_ERR_CUDA = 4
+};
+
+enum kct_mem { KCT_MEM_HOST = 0, KCT_MEM_DEVICE = 1 };
+enum kct_layout { KCT_LAYOUT_REFERENCE = 0, KCT_LAYOUT_NATIVE = 1 };
+enum kct_kind { KCT_KIND_TV = 0, KCT_KIND_PIPLE = 1, KCT_KIND_PICCS = 2 };
+
+/* GridSpec (types.hpp:56-80): dims, spacing [mm], origin = min corner of voxel (0,0,0). */
+typedef struct kct_grid {
+    int nx, ny, nz;
+    double sx, sy, sz;
+    double ox, oy, oz;
+} kct_grid;
+
+/* ConeBeamGeometry (types.hpp:138-161) + DetectorSpec (types.hpp:125-130).
+ * `angles` (radians, n_angles entries) is copied at handle creation. */
+typedef struct kct_geometry {
+    double dso, dsd;
+    int nu, nv;
+    double pu, pv;
+    double offset_u, offset_v;
+    int n_angles;
+    const double* angles;
+} kct_geometry;
+
+/* RegularizationParams (recon.hpp:37-55).  lambda < 0 means "use alpha";
+ * tau <= 0 resolves from the dynamic range (recon.hpp:60-66). */
+typedef struct kct_reg_params {
+    double alpha;
+    double lambda;
+    double tau;
+    size_t outer_iters;
+    size_t inner_iters;
+    double inner_tolerance;
+    int warm_start;
+} kct_reg_params;
+
+/* ReconReport (recon.hpp:74-83).  The caller owns every array; any pointer may
+ * be NULL to skip that history.  Required capacities:
+ *   objective_history  outer_iters + 1   (irn_*; cgls_recon: iters)
+ *   residual_history   outer_iters * inner_iters   (cgls_recon: iters)
+ *   error_history      same as residual_history (needs ground_truth)
+ *   outer_boundaries   outer_iters       (cgls_recon: 1)
+ *   outer_seconds      outer_iters       (cgls_recon: 1)
+ * The *_count fields are written by the solver. */
+typedef struct kct_report {
+    double* objective_history;  size_t objective_count;
+    double* residual_history;   size_t residual_count;
+    double* error_history;      size_t error_count;
+    uint64_t* outer_boundaries; size_t outer_count;
+    double* outer_seconds;
+    double solve_seconds;
+    double tau;        /* resolved smoothing parameter (irn_*) */
+    int converged;
+    int breakdown;
+} kct_report;
+
+typedef struct kct_projector kct_projector;
+
+/* ---- library ---------------------------------------------------------- */
+const char* kct_last_error(void);
+int kct_abi_version(void);
+
+/* ---- operator: ConeBeamProjector (projector.hpp:264-291) --------------- */
+/* ctor: validate grid + geometry, reject a source inside the volume
+ * (projector.hpp:269-274, :162-168).  device < 0 means the current device. */
+int kct_projector_create(const kct_grid* grid, const kct_geometry* geom, int device,
+                         kct_projector** out);
+int kct_projector_destroy(kct_projector* h);
+/* domain_size() / range_size() (projector.hpp:276-277) */
+int kct_projector_sizes(const kct_projector* h, size_t* domain, size_t* range);
+/* y = A x  — project_forward (projector.hpp:194-204).  vol: M floats, proj: N floats. */
+int kct_forward(kct_projector* h, const float* vol, float* proj, int mem, int layout,
+                void* stream);
+/* x = A^T y — project_adjoint (projector.hpp:226-261); overwrites vol. */
+int kct_adjoint(kct_projector* h, const float* proj, float* vol, int mem, int layout,
+                void* stream);
+/* float64 host spans, reference layouts: LinearMap::apply / apply_adjoint
+ * (linear_map.hpp:33-36) for the C++ shim; values are rounded to float32. */
+int kct_forward_f64(kct_projector* h, const double* vol, double* proj);
+int kct_adjoint_f64(kct_projector* h, const double* proj, double* vol);
+/* Exact Siddon intersection count nnz (number of (ray, voxel) pairs with
+ * positive length) — the algorithmic-bytes unit of the roofline. */
+int kct_count_nnz(kct_projector* h, uint64_t* nnz, void* stream);
+/* Layout conversion on device (reference <-> native), stream-ordered. */
+int kct_volume_to_native(const kct_projector* h, const float* ref, float* native, void* stream);
+int kct_volume_from_native(const kct_projector* h, const float* native, float* ref, void* stream);
+int kct_proj_to_native(const kct_projector* h, const float* ref, float* native, void* stream);
+int kct_proj_from_native(const kct_projector* h, const float* native, float* ref, void* stream);
+
+/* ---- solvers ---------------------------------------------------------- */
+/* cgls_recon (recon.hpp:312-315 -> baseline_solve :274-307 -> cgls krylov.hpp:59-127).
+ * b: N floats, x0: M floats or NULL (zeros), ground_truth: M or NULL,
+ * x_out: M floats.  All arrays share `mem` and `layout`. */
+int kct_cgls_recon(kct_projector* h, const float* b, size_t iters, const float* x0,
+                   const float* ground_truth, double tolerance, float* x_out,
+                   kct_report* report, int mem, int layout, void* stream);
+
+/* irn_tv / irn_piple / irn_piccs (recon.hpp:252-270 -> irn_solve :169-247).
+ * prior: M floats (ignored for KCT_KIND_TV, may be NULL then). */
+int kct_irn(kct_projector* h, int kind, const float* b, const float* prior, const float* x0,
+            const float* ground_truth, const kct_reg_params* params, float* x_out,
+            kct_report* report, int mem, int layout, void* stream);
+
+/* Convenience wrapper with the irn_piccs signature (recon.hpp:267-270). */
+int kct_irn_piccs(kct_projector* h, const float* b, const float* prior, const float* x0,
+                  const float* ground_truth, const kct_reg_params* params, float* x_out,
+                  kct_report* report, int mem, int layout, void* stream);
+
+/* resolve_tau (recon.hpp:60-66) over a float32 host array (NULL/0 = empty). */
+double kct_resolve_tau(double tau, const float* reference, size_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KCT_H */

@@ -1,0 +1,294 @@
+// capi.cu — the C ABI (include/kct.h).  Thin: argument checks, layout and
+// host<->device staging, exception -> status-code mapping.  All compute is in
+// projector.cu / solver.cu.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "projector.cuh"
+#include "solver.cuh"
+
+struct kct_projector {
+    kct::Projector* p;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_err.clear();
+        return KCT_OK;
+    } catch (const kct::ConfigError& e) {
+        g_err = e.what();
+        return KCT_ERR_CONFIG;
+    } catch (const kct::SolverError& e) {
+        g_err = e.what();
+        return KCT_ERR_SOLVER;
+    } catch (const kct::CudaError& e) {
+        g_err = e.what();
+        return KCT_ERR_CUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return KCT_ERR_INTERNAL;
+    } catch (...) {
+        g_err = "unknown error";
+        return KCT_ERR_INTERNAL;
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) KCT_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+kct::Projector& get(kct_projector* h) {
+    if (!h || !h->p) throw kct::ConfigError("null projector handle");
+    return *h->p;
+}
+
+void check_mem_layout(int mem, int layout) {
+    if (mem != KCT_MEM_HOST && mem != KCT_MEM_DEVICE) throw kct::ConfigError("invalid mem kind");
+    if (layout != KCT_LAYOUT_REFERENCE && layout != KCT_LAYOUT_NATIVE)
+        throw kct::ConfigError("invalid layout");
+}
+
+__global__ void sum_counts_kernel(const float* __restrict__ c, size_t n, unsigned long long* out) {
+    unsigned long long local = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        local += (unsigned long long)c[i];
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(out, local);
+}
+
+}  // namespace
+
+namespace kct {
+
+// Stage an input array of `n` floats into a native-layout device buffer.
+// Returns a device pointer (either `src` itself or a scratch buffer).
+const float* stage_in(Projector& P, const float* src, size_t n, bool is_vol, int mem, int layout,
+                      int slot, int tmp_slot, cudaStream_t s) {
+    if (!src) return nullptr;
+    if (mem == KCT_MEM_DEVICE && layout == KCT_LAYOUT_NATIVE) return src;
+    float* dst = P.scratch(slot, n);
+    const float* ref = src;
+    if (mem == KCT_MEM_HOST) {
+        float* tgt = layout == KCT_LAYOUT_NATIVE ? dst : P.scratch(tmp_slot, n);
+        KCT_CUDA(cudaMemcpyAsync(tgt, src, n * sizeof(float), cudaMemcpyHostToDevice, s));
+        if (layout == KCT_LAYOUT_NATIVE) return dst;
+        ref = tgt;
+    }
+    if (is_vol) P.vol_to_native(ref, dst, s);
+    else P.proj_to_native(ref, dst, s);
+    return dst;
+}
+
+// Write a native-layout device array `nat` out to `dst` (mem/layout as given).
+void stage_out(Projector& P, const float* nat, float* dst, size_t n, bool is_vol, int mem,
+               int layout, int tmp_slot, cudaStream_t s) {
+    if (mem == KCT_MEM_DEVICE && layout == KCT_LAYOUT_NATIVE) {
+        if (dst != nat) KCT_CUDA(cudaMemcpyAsync(dst, nat, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    const float* src = nat;
+    if (layout == KCT_LAYOUT_REFERENCE) {
+        float* tgt = mem == KCT_MEM_DEVICE ? dst : P.scratch(tmp_slot, n);
+        if (is_vol) P.vol_from_native(nat, tgt, s);
+        else P.proj_from_native(nat, tgt, s);
+        if (mem == KCT_MEM_DEVICE) return;
+        src = tgt;
+    }
+    KCT_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(float), cudaMemcpyDeviceToHost, s));
+}
+
+}  // namespace kct
+
+extern "C" {
+
+const char* kct_last_error(void) { return g_err.c_str(); }
+int kct_abi_version(void) { return KCT_ABI_VERSION; }
+
+int kct_projector_create(const kct_grid* grid, const kct_geometry* geom, int device,
+                         kct_projector** out) {
+    return guarded([&] {
+        if (!grid || !geom || !out) throw kct::ConfigError("null argument");
+        *out = nullptr;
+        auto* h = new kct_projector{nullptr};
+        try {
+            h->p = new kct::Projector(*grid, *geom, device);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int kct_projector_destroy(kct_projector* h) {
+    return guarded([&] {
+        if (!h) return;
+        delete h->p;
+        delete h;
+    });
+}
+
+int kct_projector_sizes(const kct_projector* h, size_t* domain, size_t* range) {
+    return guarded([&] {
+        if (!h || !h->p) throw kct::ConfigError("null projector handle");
+        if (domain) *domain = h->p->domain_size();
+        if (range) *range = h->p->range_size();
+    });
+}
+
+int kct_forward(kct_projector* h, const float* vol, float* proj, int mem, int layout,
+                void* stream) {
+    return guarded([&] {
+        auto& P = get(h);
+        check_mem_layout(mem, layout);
+        if (!vol || !proj) throw kct::ConfigError("forward: null buffer");
+        DeviceGuard dg(P.device());
+        auto s = static_cast<cudaStream_t>(stream);
+        const size_t M = P.domain_size(), N = P.range_size();
+        const float* v = kct::stage_in(P, vol, M, true, mem, layout, 0, 2, s);
+        float* q = (mem == KCT_MEM_DEVICE && layout == KCT_LAYOUT_NATIVE) ? proj : P.scratch(1, N);
+        P.forward(v, q, s);
+        kct::stage_out(P, q, proj, N, false, mem, layout, 2, s);
+        if (mem == KCT_MEM_HOST) KCT_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int kct_adjoint(kct_projector* h, const float* proj, float* vol, int mem, int layout,
+                void* stream) {
+    return guarded([&] {
+        auto& P = get(h);
+        check_mem_layout(mem, layout);
+        if (!vol || !proj) throw kct::ConfigError("adjoint: null buffer");
+        DeviceGuard dg(P.device());
+        auto s = static_cast<cudaStream_t>(stream);
+        const size_t M = P.domain_size(), N = P.range_size();
+        const float* q = kct::stage_in(P, proj, N, false, mem, layout, 1, 2, s);
+        float* v = (mem == KCT_MEM_DEVICE && layout == KCT_LAYOUT_NATIVE) ? vol : P.scratch(0, M);
+        P.adjoint(q, v, s);
+        kct::stage_out(P, v, vol, M, true, mem, layout, 2, s);
+        if (mem == KCT_MEM_HOST) KCT_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int kct_forward_f64(kct_projector* h, const double* vol, double* proj) {
+    return guarded([&] {
+        auto& P = get(h);
+        if (!vol || !proj) throw kct::ConfigError("forward: null buffer");
+        std::vector<float> v(vol, vol + P.domain_size()), q(P.range_size());
+        if (kct_forward(h, v.data(), q.data(), KCT_MEM_HOST, KCT_LAYOUT_REFERENCE, nullptr))
+            throw kct::CudaError(g_err);
+        for (size_t i = 0; i < q.size(); ++i) proj[i] = q[i];
+    });
+}
+
+int kct_adjoint_f64(kct_projector* h, const double* proj, double* vol) {
+    return guarded([&] {
+        auto& P = get(h);
+        if (!vol || !proj) throw kct::ConfigError("adjoint: null buffer");
+        std::vector<float> q(proj, proj + P.range_size()), v(P.domain_size());
+        if (kct_adjoint(h, q.data(), v.data(), KCT_MEM_HOST, KCT_LAYOUT_REFERENCE, nullptr))
+            throw kct::CudaError(g_err);
+        for (size_t i = 0; i < v.size(); ++i) vol[i] = v[i];
+    });
+}
+
+int kct_count_nnz(kct_projector* h, uint64_t* nnz, void* stream) {
+    return guarded([&] {
+        auto& P = get(h);
+        if (!nnz) throw kct::ConfigError("null output");
+        DeviceGuard dg(P.device());
+        auto s = static_cast<cudaStream_t>(stream);
+        float* c = P.scratch(1, P.range_size());
+        P.count(c, s);
+        unsigned long long* d = reinterpret_cast<unsigned long long*>(P.scratch(3, 2));
+        KCT_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), s));
+        sum_counts_kernel<<<148 * 4, 256, 0, s>>>(c, P.range_size(), d);
+        KCT_CUDA(cudaGetLastError());
+        unsigned long long r = 0;
+        KCT_CUDA(cudaMemcpyAsync(&r, d, sizeof r, cudaMemcpyDeviceToHost, s));
+        KCT_CUDA(cudaStreamSynchronize(s));
+        *nnz = r;
+    });
+}
+
+int kct_volume_to_native(const kct_projector* h, const float* ref, float* native, void* stream) {
+    return guarded([&] {
+        auto& P = get(const_cast<kct_projector*>(h));
+        DeviceGuard dg(P.device());
+        P.vol_to_native(ref, native, static_cast<cudaStream_t>(stream));
+    });
+}
+int kct_volume_from_native(const kct_projector* h, const float* native, float* ref, void* stream) {
+    return guarded([&] {
+        auto& P = get(const_cast<kct_projector*>(h));
+        DeviceGuard dg(P.device());
+        P.vol_from_native(native, ref, static_cast<cudaStream_t>(stream));
+    });
+}
+int kct_proj_to_native(const kct_projector* h, const float* ref, float* native, void* stream) {
+    return guarded([&] {
+        auto& P = get(const_cast<kct_projector*>(h));
+        DeviceGuard dg(P.device());
+        P.proj_to_native(ref, native, static_cast<cudaStream_t>(stream));
+    });
+}
+int kct_proj_from_native(const kct_projector* h, const float* native, float* ref, void* stream) {
+    return guarded([&] {
+        auto& P = get(const_cast<kct_projector*>(h));
+        DeviceGuard dg(P.device());
+        P.proj_from_native(native, ref, static_cast<cudaStream_t>(stream));
+    });
+}
+
+double kct_resolve_tau(double tau, const float* reference, size_t n) {
+    return kct::resolve_tau(tau, reference, n);
+}
+
+int kct_cgls_recon(kct_projector* h, const float* b, size_t iters, const float* x0,
+                   const float* ground_truth, double tolerance, float* x_out,
+                   kct_report* report, int mem, int layout, void* stream) {
+    return guarded([&] {
+        auto& P = get(h);
+        check_mem_layout(mem, layout);
+        DeviceGuard dg(P.device());
+        kct::cgls_recon(P, b, iters, x0, ground_truth, tolerance, x_out, report, mem, layout,
+                        static_cast<cudaStream_t>(stream));
+    });
+}
+
+int kct_irn(kct_projector* h, int kind, const float* b, const float* prior, const float* x0,
+            const float* ground_truth, const kct_reg_params* params, float* x_out,
+            kct_report* report, int mem, int layout, void* stream) {
+    return guarded([&] {
+        auto& P = get(h);
+        check_mem_layout(mem, layout);
+        if (!params) throw kct::ConfigError("null params");
+        DeviceGuard dg(P.device());
+        kct::irn_solve(P, kind, b, prior, x0, ground_truth, *params, x_out, report, mem, layout,
+                       static_cast<cudaStream_t>(stream));
+    });
+}
+
+int kct_irn_piccs(kct_projector* h, const float* b, const float* prior, const float* x0,
+                  const float* ground_truth, const kct_reg_params* params, float* x_out,
+                  kct_report* report, int mem, int layout, void* stream) {
+    return kct_irn(h, KCT_KIND_PICCS, b, prior, x0, ground_truth, params, x_out, report, mem,
+                   layout, stream);
+}
+
+}  // extern "C"

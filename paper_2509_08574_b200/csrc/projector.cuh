@@ -1,0 +1,72 @@
+// projector.cuh — the cone-beam operator pair A / A^T on B200.
+//
+// Replaces ConeBeamProjector / project_forward / project_adjoint /
+// traverse_ray (reference projector.hpp:24-296).  Same model: exact Siddon
+// ray-voxel intersection lengths, nearest-voxel piecewise constant, rays from
+// the source through every detector pixel centre.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "kct_common.cuh"
+
+namespace kct {
+
+class Projector {
+  public:
+    Projector(const kct_grid& grid, const kct_geometry& geom, int device);
+    ~Projector();
+    Projector(const Projector&) = delete;
+    Projector& operator=(const Projector&) = delete;
+
+    size_t domain_size() const { return m_; }
+    size_t range_size() const { return n_; }
+    const kct_grid& grid() const { return grid_; }
+    const DevGeom& dev_geom() const { return dg_; }
+    int device() const { return device_; }
+    int n_angles() const { return dg_.na; }
+
+    // Native-layout, device-resident operators (stream-ordered).
+    void forward(const float* vol, float* proj, cudaStream_t s) const;
+    void adjoint(const float* proj, float* vol, cudaStream_t s) const;
+    // Per-ray count of positive-length Siddon segments (as float) into proj.
+    void count(float* proj, cudaStream_t s) const;
+
+    // Layout conversions (device, stream-ordered).
+    void vol_to_native(const float* ref, float* nat, cudaStream_t s) const;
+    void vol_from_native(const float* nat, float* ref, cudaStream_t s) const;
+    void proj_to_native(const float* ref, float* nat, cudaStream_t s) const;
+    void proj_from_native(const float* nat, float* ref, cudaStream_t s) const;
+
+    // Lazily allocated scratch used by the C-ABI for host / reference-layout calls.
+    float* scratch(int slot, size_t n);
+
+    // Solver workspace cached across calls (owned by solver.cu).
+    std::shared_ptr<void> workspace;
+
+    int fwd_chunks() const { return fwd_c_; }
+    int adj_k() const { return adj_k_; }
+
+  private:
+    void build_tables(const kct_geometry& geom);
+
+    kct_grid grid_;
+    DevGeom dg_{};
+    int device_ = 0;
+    size_t m_ = 0, n_ = 0;
+    std::vector<float2> cs_;          // per-angle (cos, sin)
+    ColParams* d_cols_ = nullptr;     // [na][nu]
+    float* d_dv_ = nullptr;           // [nv] row heights dv(iv)
+    float* d_invdv_ = nullptr;        // [nv] 1/dv (inf at dv == 0)
+    double* d_dvd_ = nullptr;         // [nv] dv in float64
+    int fwd_c_ = 4, fwd_bands_ = 1, adj_k_ = 8;
+    float* scratch_[4] = {nullptr, nullptr, nullptr, nullptr};
+    size_t scratch_n_[4] = {0, 0, 0, 0};
+};
+
+// Validation mirroring the reference (types.hpp:72-77, :152-160;
+// projector.hpp:162-168).  Throws ConfigError.
+void validate_geometry(const kct_grid& grid, const kct_geometry& geom);
+
+}  // namespace kct

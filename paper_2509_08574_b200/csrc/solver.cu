@@ -1,0 +1,782 @@
+// solver.cu — device-resident CGLS on the stacked IRN systems.
+//
+// The reference solves, per outer cycle (recon.hpp:192-242),
+//     min || [A; a*W1*D; l*W2*D] x - [b; 0; l*W2*D*x_p] ||        (PICCS)
+// with cgls (krylov.hpp:59-127) on materialised stacked vectors of length
+// N + 6M.  In exact arithmetic the regulariser blocks of the CGLS residual are
+// always  r1 = -a*W1*D*x  and  r2 = -l*W2*D*(x - x_p)  (block 2 of the rhs is
+// 0, block 3 is l*W2*D*x_p, and x moves by the same steps as r), so this
+// implementation keeps only the projection block r0 (length N) on the
+// recurrence and evaluates the regulariser blocks from x and p in fused
+// stencil kernels:
+//     A~^T r   = A^T r0 - a^2 D^T W1^2 D x - l^2 D^T W2^2 D (x - x_p)
+//     ||A~ p||^2 = ||A p||^2 + a^2 ||W1 D p||^2 + l^2 ||W2 D p||^2
+//     ||r||^2  = ||r0||^2 + a^2 ||W1 D x||^2 + l^2 ||W2 D (x - x_p)||^2
+// PIPLE's l*I block works the same way with D -> I, W2 -> 1.  Vectors are
+// float32; every reduction is float64, deterministic (fixed grid, per-block
+// partials, fixed-order final sum), as the reference's sequential double
+// reductions are (vector_ops.hpp:3-5).  The CGLS scalars (gamma, delta, a,
+// beta) live on the device so the host never waits inside a cycle.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "solver.cuh"
+
+namespace kct {
+
+namespace {
+
+constexpr int kGrid = 148 * 8;  // fixed grid -> deterministic partial sums
+constexpr int kBlock = 256;
+constexpr int kSlots = 8;
+
+struct Ctl {
+    double gamma, a, beta, stop_tol;
+    double r2, e2, gt2, ref2;
+    double alpha2, lambda2;
+    double tv1, tv2, data;
+    int stop, converged, breakdown, error;
+    int iters, x_nonzero, pad0, pad1;
+};
+
+enum ScalarMode {
+    S_DATA = 0,    // data = sum slot0
+    S_TV = 1,      // tv1 = slot1, tv2 = slot2
+    S_INIT = 2,    // gamma = slot0 (reset flags, tolerance)
+    S_DELTA = 3,   // delta = slot0 + a2*slot1 + l2*slot2 -> a
+    S_GAMMA = 4,   // gamma' = slot0; residual from r2(slot4), reg slot1/2; err slot5
+    S_REF = 5,     // ref2 = slot0, x_nonzero = slot3 > 0
+    S_GT2 = 6,     // gt2 = slot0
+    S_OBJ = 7,     // obj_out[idx] = data + ...
+};
+
+// Regulariser configuration shared by the stencil kernels.
+struct RegCfg {
+    int nx, ny, nz;
+    int use_w1;      // a != 0: TV block present
+    int mode2;       // 0 none, 1 PICCS (W2 D block), 2 PIPLE (I block)
+    float alpha2, lambda2;
+    float tau2;
+};
+
+__device__ __forceinline__ void decode(size_t v, const RegCfg& c, int& k, int& i, int& j) {
+    const unsigned p = (unsigned)(v / (unsigned)c.nz);
+    k = (int)(v - (size_t)p * c.nz);
+    i = (int)(p % (unsigned)c.nx);
+    j = (int)(p / (unsigned)c.nx);
+}
+
+// forward differences of f at v (zero at the far face, diffreg.hpp:34-49)
+__device__ __forceinline__ void fdiff(const float* __restrict__ f, size_t v, int k, int i, int j,
+                                      const RegCfg& c, size_t si, size_t sj, float fv, float& gx,
+                                      float& gy, float& gz) {
+    gx = i + 1 < c.nx ? f[v + si] - fv : 0.f;
+    gy = j + 1 < c.ny ? f[v + sj] - fv : 0.f;
+    gz = k + 1 < c.nz ? f[v + 1] - fv : 0.f;
+}
+
+__device__ __forceinline__ void write_partials(double* part, int slot, double v, double* sm) {
+    const double t = block_sum(v, sm);
+    if (threadIdx.x == 0) part[slot * kGrid + blockIdx.x] = t;
+}
+
+// ---- weights + smoothed-TV sums (tv_weights diffreg.hpp:142-156; ----------
+// smoothed_tv :118-126; the PIPLE quadratic of recon.hpp:107-114) ----------
+__global__ void __launch_bounds__(kBlock) k_weights(const float* __restrict__ x,
+                                                    const float* __restrict__ xp,
+                                                    float* __restrict__ w1, float* __restrict__ w2,
+                                                    RegCfg c, int write_w, double* part) {
+    __shared__ double sm[32];
+    const size_t m = (size_t)c.nx * c.ny * c.nz, si = c.nz, sj = (size_t)c.nz * c.nx;
+    double t1 = 0.0, t2 = 0.0;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < m;
+         v += (size_t)gridDim.x * blockDim.x) {
+        int k, i, j;
+        decode(v, c, k, i, j);
+        const float xv = x[v];
+        if (c.use_w1) {
+            float gx, gy, gz;
+            fdiff(x, v, k, i, j, c, si, sj, xv, gx, gy, gz);
+            const float m2 = gx * gx + gy * gy + gz * gz + c.tau2;
+            const float r = sqrtf(m2);
+            t1 += (double)r;
+            if (write_w) w1[v] = 1.f / sqrtf(r);
+        }
+        if (c.mode2 == 1) {
+            const float dv = xv - xp[v];
+            const float gx = i + 1 < c.nx ? (x[v + si] - xp[v + si]) - dv : 0.f;
+            const float gy = j + 1 < c.ny ? (x[v + sj] - xp[v + sj]) - dv : 0.f;
+            const float gz = k + 1 < c.nz ? (x[v + 1] - xp[v + 1]) - dv : 0.f;
+            const float r = sqrtf(gx * gx + gy * gy + gz * gz + c.tau2);
+            t2 += (double)r;
+            if (write_w) w2[v] = 1.f / sqrtf(r);
+        } else if (c.mode2 == 2) {
+            const double d = (double)xv - (double)xp[v];
+            t2 += d * d;
+        }
+    }
+    write_partials(part, 1, t1, sm);
+    write_partials(part, 2, t2, sm);
+}
+
+// ---- r = b - q (q == nullptr: r = b); slot0 = ||r||^2 ---------------------
+__global__ void __launch_bounds__(kBlock) k_resid(const float* __restrict__ b,
+                                                  const float* __restrict__ q,
+                                                  float* __restrict__ r, size_t n, double* part,
+                                                  int slot) {
+    __shared__ double sm[32];
+    double t = 0.0;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n;
+         v += (size_t)gridDim.x * blockDim.x) {
+        const float rv = q ? b[v] - q[v] : b[v];
+        if (r) r[v] = rv;
+        t += (double)rv * (double)rv;
+    }
+    write_partials(part, slot, t, sm);
+}
+
+// ---- s = A^T r0 - a^2 D^T W1^2 D x - l^2 D^T W2^2 D (x - x_p) --------------
+// slot0 = ||s||^2, slot1 = ||W1 D x||^2, slot2 = ||W2 D (x-x_p)||^2 (or ||x-x_p||^2)
+// x == nullptr means x = 0 (the right-hand-side adjoint for the tolerance ref).
+__global__ void __launch_bounds__(kBlock) k_reggrad(const float* __restrict__ sA,
+                                                    const float* __restrict__ x,
+                                                    const float* __restrict__ xp,
+                                                    const float* __restrict__ w1,
+                                                    const float* __restrict__ w2,
+                                                    float* __restrict__ s, RegCfg c, double* part) {
+    __shared__ double sm[32];
+    const size_t m = (size_t)c.nx * c.ny * c.nz, si = c.nz, sj = (size_t)c.nz * c.nx;
+    double ts = 0.0, t1 = 0.0, t2 = 0.0;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < m;
+         v += (size_t)gridDim.x * blockDim.x) {
+        int k, i, j;
+        decode(v, c, k, i, j);
+        float sv = sA[v];
+        const float xv = x ? x[v] : 0.f;
+        if (c.use_w1 && x) {
+            float gx, gy, gz;
+            fdiff(x, v, k, i, j, c, si, sj, xv, gx, gy, gz);
+            const float wv = w1[v], wv2 = wv * wv;
+            float g = -wv2 * (gx + gy + gz);
+            if (i > 0) { const float w = w1[v - si]; g += w * w * (xv - x[v - si]); }
+            if (j > 0) { const float w = w1[v - sj]; g += w * w * (xv - x[v - sj]); }
+            if (k > 0) { const float w = w1[v - 1]; g += w * w * (xv - x[v - 1]); }
+            sv -= c.alpha2 * g;
+            t1 += (double)(wv2 * (gx * gx + gy * gy + gz * gz));
+        }
+        if (c.mode2 == 1) {
+            auto d = [&](size_t u) { return (x ? x[u] : 0.f) - xp[u]; };
+            const float dv = d(v);
+            const float gx = i + 1 < c.nx ? d(v + si) - dv : 0.f;
+            const float gy = j + 1 < c.ny ? d(v + sj) - dv : 0.f;
+            const float gz = k + 1 < c.nz ? d(v + 1) - dv : 0.f;
+            const float wv = w2[v], wv2 = wv * wv;
+            float g = -wv2 * (gx + gy + gz);
+            if (i > 0) { const float w = w2[v - si]; g += w * w * (dv - d(v - si)); }
+            if (j > 0) { const float w = w2[v - sj]; g += w * w * (dv - d(v - sj)); }
+            if (k > 0) { const float w = w2[v - 1]; g += w * w * (dv - d(v - 1)); }
+            sv -= c.lambda2 * g;
+            t2 += (double)(wv2 * (gx * gx + gy * gy + gz * gz));
+        } else if (c.mode2 == 2) {
+            const float dv = xv - xp[v];
+            sv -= c.lambda2 * dv;
+            t2 += (double)dv * (double)dv;
+        }
+        s[v] = sv;
+        ts += (double)sv * (double)sv;
+    }
+    write_partials(part, 0, ts, sm);
+    write_partials(part, 1, t1, sm);
+    write_partials(part, 2, t2, sm);
+}
+
+// ---- slot0 = ||q||^2 (N); slot1 = ||W1 D p||^2, slot2 = ||W2 D p||^2 (M) ---
+__global__ void __launch_bounds__(kBlock) k_normq(const float* __restrict__ q, size_t n,
+                                                  const float* __restrict__ p,
+                                                  const float* __restrict__ w1,
+                                                  const float* __restrict__ w2, RegCfg c,
+                                                  const Ctl* ctl, double* part) {
+    if (ctl->stop) return;
+    __shared__ double sm[32];
+    double tq = 0.0, t1 = 0.0, t2 = 0.0;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n; v += stride) {
+        const double qv = q[v];
+        tq += qv * qv;
+    }
+    if (c.use_w1 || c.mode2) {
+        const size_t m = (size_t)c.nx * c.ny * c.nz, si = c.nz, sj = (size_t)c.nz * c.nx;
+        for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < m; v += stride) {
+            int k, i, j;
+            decode(v, c, k, i, j);
+            const float pv = p[v];
+            if (c.mode2 == 2) t2 += (double)pv * (double)pv;
+            if (c.use_w1 || c.mode2 == 1) {
+                float gx, gy, gz;
+                fdiff(p, v, k, i, j, c, si, sj, pv, gx, gy, gz);
+                const float g2 = gx * gx + gy * gy + gz * gz;
+                if (c.use_w1) { const float w = w1[v]; t1 += (double)(w * w * g2); }
+                if (c.mode2 == 1) { const float w = w2[v]; t2 += (double)(w * w * g2); }
+            }
+        }
+    }
+    write_partials(part, 0, tq, sm);
+    write_partials(part, 1, t1, sm);
+    write_partials(part, 2, t2, sm);
+}
+
+// ---- x += a p ; r0 -= a q ; slot4 = ||r0||^2, slot5 = ||x - gt||^2 ---------
+__global__ void __launch_bounds__(kBlock) k_update_xr(float* __restrict__ x,
+                                                      const float* __restrict__ p, size_t m,
+                                                      float* __restrict__ r,
+                                                      const float* __restrict__ q, size_t n,
+                                                      const float* __restrict__ gt,
+                                                      const Ctl* ctl, double* part) {
+    if (ctl->stop) return;
+    __shared__ double sm[32];
+    const float a = (float)ctl->a;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    double tr = 0.0, te = 0.0;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < m; v += stride) {
+        const float xv = fmaf(a, p[v], x[v]);
+        x[v] = xv;
+        if (gt) { const double d = (double)xv - (double)gt[v]; te += d * d; }
+    }
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n; v += stride) {
+        const float rv = fmaf(-a, q[v], r[v]);
+        r[v] = rv;
+        tr += (double)rv * (double)rv;
+    }
+    write_partials(part, 4, tr, sm);
+    write_partials(part, 5, te, sm);
+}
+
+// ---- p = s + beta p (init: p = s) ----------------------------------------
+__global__ void __launch_bounds__(kBlock) k_update_p(float* __restrict__ p,
+                                                     const float* __restrict__ s, size_t m,
+                                                     const Ctl* ctl, int init) {
+    if (ctl->stop) return;
+    const float beta = (float)ctl->beta;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < m;
+         v += (size_t)gridDim.x * blockDim.x)
+        p[v] = init ? s[v] : fmaf(beta, p[v], s[v]);
+}
+
+// ---- misc reductions -------------------------------------------------------
+__global__ void __launch_bounds__(kBlock) k_stats(const float* __restrict__ f, size_t n,
+                                                  double* part) {
+    // slot0 = sum f^2, slot3 = count(f != 0), slot6 = min, slot7 = max
+    __shared__ double sm[32];
+    double t = 0.0, nz = 0.0;
+    float lo = __builtin_huge_valf(), hi = -__builtin_huge_valf();
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n;
+         v += (size_t)gridDim.x * blockDim.x) {
+        const float fv = f[v];
+        t += (double)fv * (double)fv;
+        nz += fv != 0.f ? 1.0 : 0.0;
+        lo = fminf(lo, fv);
+        hi = fmaxf(hi, fv);
+    }
+    write_partials(part, 0, t, sm);
+    write_partials(part, 3, nz, sm);
+    // min / max: reuse the block reduction tree on warp-level min/max
+    __shared__ float smin[32], smax[32];
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fminf(lo, __shfl_down_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_down_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) { smin[threadIdx.x >> 5] = lo; smax[threadIdx.x >> 5] = hi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { lo = fminf(lo, smin[w]); hi = fmaxf(hi, smax[w]); }
+        part[6 * kGrid + blockIdx.x] = lo;
+        part[7 * kGrid + blockIdx.x] = hi;
+    }
+}
+
+__device__ __forceinline__ double slot_sum(const double* part, int slot, double* sm) {
+    double t = 0.0;
+    for (int b = threadIdx.x; b < kGrid; b += blockDim.x) t += part[slot * kGrid + b];
+    const double r = block_sum(t, sm);
+    __syncthreads();
+    return r;  // valid in thread 0
+}
+
+// One-block scalar step: reduces the partials of the preceding kernel(s) in a
+// fixed order and runs the CGLS scalar recurrence (krylov.hpp:68-125).
+__global__ void __launch_bounds__(kBlock) k_scalar(Ctl* ctl, const double* part, int mode,
+                                                   double tol, double* res_hist, double* err_hist,
+                                                   double* obj_out, int obj_kind) {
+    __shared__ double sm[32];
+    const double s0 = slot_sum(part, 0, sm);
+    double s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0, s5 = 0.0;
+    if (mode == S_TV || mode == S_DELTA || mode == S_GAMMA) {
+        s1 = slot_sum(part, 1, sm);
+        s2 = slot_sum(part, 2, sm);
+    }
+    if (mode == S_REF) s3 = slot_sum(part, 3, sm);
+    if (mode == S_GAMMA) {
+        s4 = slot_sum(part, 4, sm);
+        s5 = slot_sum(part, 5, sm);
+    }
+    if (threadIdx.x != 0) return;
+    Ctl& c = *ctl;
+    switch (mode) {
+    case S_DATA: c.data = s0; break;
+    case S_TV: c.tv1 = s1; c.tv2 = s2; break;
+    case S_GT2: c.gt2 = s0; break;
+    case S_REF:
+        c.ref2 = s0;
+        break;
+    case S_INIT: {
+        c.stop = c.converged = c.breakdown = c.error = 0;
+        c.iters = 0;
+        c.gamma = s0;
+        if (!isfinite(s0)) { c.error = 1; c.stop = 1; break; }
+        if (s0 == 0.0) { c.converged = 1; c.stop = 1; break; }
+        c.stop_tol = 0.0;
+        if (tol > 0.0) {
+            const double ref2 = c.x_nonzero ? c.ref2 : s0;
+            c.stop_tol = tol * sqrt(ref2);
+            if (sqrt(s0) <= c.stop_tol) { c.converged = 1; c.stop = 1; }
+        }
+        break;
+    }
+    case S_DELTA: {
+        if (c.stop) break;
+        const double delta = s0 + c.alpha2 * s1 + c.lambda2 * s2;
+        if (!isfinite(delta)) { c.error = 2; c.stop = 1; break; }
+        if (delta == 0.0) { c.breakdown = 1; c.stop = 1; break; }
+        c.a = c.gamma / delta;
+        break;
+    }
+    case S_GAMMA: {
+        if (c.stop) break;
+        const double g = s0;
+        if (!isfinite(g)) { c.error = 2; c.stop = 1; break; }
+        c.r2 = s4;
+        const double res2 = s4 + c.alpha2 * s1 + c.lambda2 * s2;
+        if (res_hist) res_hist[c.iters] = sqrt(res2);
+        if (err_hist) err_hist[c.iters] = c.gt2 > 0.0 ? sqrt(s5 / c.gt2) : sqrt(s5);
+        c.iters += 1;
+        if (sqrt(g) <= c.stop_tol) { c.converged = 1; c.stop = 1; break; }
+        c.beta = g / c.gamma;
+        c.gamma = g;
+        break;
+    }
+    case S_OBJ: {
+        // recon.hpp:93-120; obj_kind: 0 tv, 1 piple, 2 piccs; alpha2/lambda2 as doubles
+        double obj = c.data;
+        if (c.alpha2 != 0.0) obj += 2.0 * c.alpha2 * c.tv1;
+        if (obj_kind == KCT_KIND_PIPLE && c.lambda2 != 0.0) obj += c.lambda2 * c.tv2;
+        if (obj_kind == KCT_KIND_PICCS && c.lambda2 != 0.0) obj += 2.0 * c.lambda2 * c.tv2;
+        *obj_out = obj;
+        break;
+    }
+    }
+}
+
+__global__ void k_minmax_final(const double* part, double* out) {
+    __shared__ double slo[kBlock], shi[kBlock];
+    double lo = INFINITY, hi = -INFINITY;
+    for (int b = threadIdx.x; b < kGrid; b += blockDim.x) {
+        lo = fmin(lo, part[6 * kGrid + b]);
+        hi = fmax(hi, part[7 * kGrid + b]);
+    }
+    slo[threadIdx.x] = lo;
+    shi[threadIdx.x] = hi;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int t = 1; t < (int)blockDim.x; ++t) { lo = fmin(lo, slo[t]); hi = fmax(hi, shi[t]); }
+        out[0] = lo;
+        out[1] = hi;
+    }
+}
+
+// ---- workspace -----------------------------------------------------------------
+struct Workspace {
+    size_t m = 0, n = 0;
+    float *b = nullptr, *r = nullptr, *q = nullptr;
+    float *x = nullptr, *p = nullptr, *s = nullptr, *prior = nullptr, *w1 = nullptr,
+          *w2 = nullptr, *gt = nullptr;
+    double* part = nullptr;
+    Ctl* ctl = nullptr;
+    double* hist = nullptr;  // [2][cap]: residual, error
+    double* obj = nullptr;   // [cap_obj]
+    double* scal = nullptr;  // misc scalars
+    size_t cap = 0, cap_obj = 0;
+
+    ~Workspace() {
+        for (void* ptr : {(void*)b, (void*)r, (void*)q, (void*)x, (void*)p, (void*)s,
+                          (void*)prior, (void*)w1, (void*)w2, (void*)gt, (void*)part,
+                          (void*)ctl, (void*)hist, (void*)obj, (void*)scal})
+            cudaFree(ptr);
+    }
+};
+
+template <class T>
+void ensure(T*& ptr, size_t n) {
+    if (!ptr) KCT_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
+}
+
+Workspace& workspace(Projector& P, size_t hist_cap, size_t obj_cap) {
+    auto ws = std::static_pointer_cast<Workspace>(P.workspace);
+    if (!ws) {
+        ws = std::make_shared<Workspace>();
+        ws->m = P.domain_size();
+        ws->n = P.range_size();
+        P.workspace = ws;
+    }
+    Workspace& w = *ws;
+    const size_t m = w.m, n = w.n;
+    ensure(w.b, n); ensure(w.r, n); ensure(w.q, n);
+    ensure(w.x, m); ensure(w.p, m); ensure(w.s, m);
+    ensure(w.part, (size_t)kSlots * kGrid);
+    ensure(w.ctl, 1);
+    ensure(w.scal, 8);
+    if (w.cap < hist_cap) {
+        cudaFree(w.hist);
+        w.hist = nullptr;
+        KCT_CUDA(cudaMalloc(&w.hist, 2 * hist_cap * sizeof(double)));
+        w.cap = hist_cap;
+    }
+    if (w.cap_obj < obj_cap) {
+        cudaFree(w.obj);
+        w.obj = nullptr;
+        KCT_CUDA(cudaMalloc(&w.obj, obj_cap * sizeof(double)));
+        w.cap_obj = obj_cap;
+    }
+    return w;
+}
+
+// Copy an input (host/device, reference/native layout) into a native device buffer.
+void load(Projector& P, float* dst, const float* src, size_t n, bool is_vol, int mem, int layout,
+          cudaStream_t s) {
+    if (mem == KCT_MEM_DEVICE && layout == KCT_LAYOUT_NATIVE) {
+        KCT_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    const float* nat = stage_in(P, src, n, is_vol, mem, layout, is_vol ? 0 : 1, 2, s);
+    KCT_CUDA(cudaMemcpyAsync(dst, nat, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+}
+
+void launch_scalar(Workspace& w, int mode, cudaStream_t s, double tol = 0.0,
+                   double* res = nullptr, double* err = nullptr, double* obj = nullptr,
+                   int kind = 0) {
+    k_scalar<<<1, kBlock, 0, s>>>(w.ctl, w.part, mode, tol, res, err, obj, kind);
+    KCT_CUDA(cudaGetLastError());
+}
+
+#define KCT_LAUNCH(kernel, ...)                                \
+    do {                                                       \
+        kernel<<<kGrid, kBlock, 0, stream>>>(__VA_ARGS__);     \
+        KCT_CUDA(cudaGetLastError());                          \
+    } while (0)
+
+
+__global__ void k_set_nonzero(Ctl* ctl, const double* part) {
+    __shared__ double sm[32];
+    double t = 0.0;
+    for (int b = threadIdx.x; b < kGrid; b += blockDim.x) t += part[3 * kGrid + b];
+    t = block_sum(t, sm);
+    if (threadIdx.x == 0) ctl->x_nonzero = t > 0.0 ? 1 : 0;
+}
+
+struct Engine {
+    Projector& P;
+    Workspace& w;
+    cudaStream_t stream;
+    RegCfg rc{};
+    int kind = KCT_KIND_TV;
+
+    // weights (optional) and smoothed-TV / quadratic sums of the objective at w.x
+    void weights(bool write) {
+        if (!rc.use_w1 && !rc.mode2) {
+            KCT_CUDA(cudaMemsetAsync(w.part + 1 * kGrid, 0, 2 * kGrid * sizeof(double), stream));
+        } else {
+            KCT_LAUNCH(k_weights, w.x, w.prior, w.w1, w.w2, rc, write ? 1 : 0, w.part);
+        }
+        launch_scalar(w, S_TV, stream);
+    }
+
+    // objective(x) (recon.hpp:93-120) into w.obj[idx]; the TV sums must be current
+    void objective(bool x_is_zero, int idx) {
+        if (x_is_zero) {
+            KCT_LAUNCH(k_resid, w.b, nullptr, nullptr, w.n, w.part, 0);
+        } else {
+            P.forward(w.x, w.q, stream);
+            KCT_LAUNCH(k_resid, w.b, w.q, nullptr, w.n, w.part, 0);
+        }
+        launch_scalar(w, S_DATA, stream);
+        launch_scalar(w, S_OBJ, stream, 0.0, nullptr, nullptr, w.obj + idx, kind);
+    }
+
+    // CGLS start (krylov.hpp:66-96) from w.x.  When obj_idx >= 0 the data term
+    // ||b - A x||^2 of this residual also completes objective[obj_idx].
+    void start(bool x_is_zero, double tol, int obj_idx) {
+        if (tol > 0.0 && !x_is_zero) {
+            // ||A~^T b~||^2, the tolerance reference of a warm start (krylov.hpp:81-88)
+            KCT_LAUNCH(k_stats, w.x, w.m, w.part);
+            k_set_nonzero<<<1, kBlock, 0, stream>>>(w.ctl, w.part);
+            KCT_CUDA(cudaGetLastError());
+            P.adjoint(w.b, w.p, stream);
+            KCT_LAUNCH(k_reggrad, w.p, nullptr, w.prior, w.w1, w.w2, w.p, rc, w.part);
+            launch_scalar(w, S_REF, stream);
+        } else {
+            KCT_CUDA(cudaMemsetAsync(&w.ctl->x_nonzero, 0, sizeof(int), stream));
+        }
+        if (x_is_zero) {
+            KCT_LAUNCH(k_resid, w.b, nullptr, w.r, w.n, w.part, 0);
+        } else {
+            P.forward(w.x, w.q, stream);
+            KCT_LAUNCH(k_resid, w.b, w.q, w.r, w.n, w.part, 0);
+        }
+        if (obj_idx >= 0) {
+            launch_scalar(w, S_DATA, stream);
+            launch_scalar(w, S_OBJ, stream, 0.0, nullptr, nullptr, w.obj + obj_idx, kind);
+        }
+        P.adjoint(w.r, w.s, stream);
+        KCT_LAUNCH(k_reggrad, w.s, x_is_zero ? nullptr : w.x, w.prior, w.w1, w.w2, w.s, rc,
+                   w.part);
+        launch_scalar(w, S_INIT, stream, tol);
+        KCT_LAUNCH(k_update_p, w.p, w.s, w.m, w.ctl, 1);
+    }
+
+    // One CGLS iteration (krylov.hpp:98-125).
+    void iterate(double* res, double* err, bool with_gt) {
+        P.forward(w.p, w.q, stream);
+        KCT_LAUNCH(k_normq, w.q, w.n, w.p, w.w1, w.w2, rc, w.ctl, w.part);
+        launch_scalar(w, S_DELTA, stream);
+        KCT_LAUNCH(k_update_xr, w.x, w.p, w.m, w.r, w.q, w.n, with_gt ? w.gt : nullptr, w.ctl,
+                   w.part);
+        P.adjoint(w.r, w.s, stream);
+        KCT_LAUNCH(k_reggrad, w.s, w.x, w.prior, w.w1, w.w2, w.s, rc, w.part);
+        launch_scalar(w, S_GAMMA, stream, 0.0, res, err);
+        KCT_LAUNCH(k_update_p, w.p, w.s, w.m, w.ctl, 0);
+    }
+
+    void ground_truth_norm() {
+        KCT_LAUNCH(k_stats, w.gt, w.m, w.part);
+        launch_scalar(w, S_GT2, stream);
+    }
+};
+
+Ctl read_ctl(Workspace& w, cudaStream_t s) {
+    Ctl c;
+    KCT_CUDA(cudaMemcpyAsync(&c, w.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+    KCT_CUDA(cudaStreamSynchronize(s));
+    return c;
+}
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+void init_ctl(Workspace& w, double alpha2, double lambda2, cudaStream_t s) {
+    Ctl c{};
+    c.alpha2 = alpha2;
+    c.lambda2 = lambda2;
+    KCT_CUDA(cudaMemcpyAsync(w.ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice, s));
+}
+
+void throw_solver(const Ctl& c) {
+    if (c.error == 1) throw SolverError("cgls: non-finite normal residual");
+    if (c.error) throw SolverError("cgls: non-finite iterate");
+}
+
+// device (min, max) of a native buffer -> resolve_tau semantics (recon.hpp:60-66)
+double device_tau(Workspace& w, const float* ref, size_t n, double tau, cudaStream_t stream) {
+    if (tau > 0.0) return tau;
+    if (!ref || n == 0) return 1e-4;
+    KCT_LAUNCH(k_stats, ref, n, w.part);
+    k_minmax_final<<<1, kBlock, 0, stream>>>(w.part, w.scal);
+    KCT_CUDA(cudaGetLastError());
+    double mm[2];
+    KCT_CUDA(cudaMemcpyAsync(mm, w.scal, sizeof mm, cudaMemcpyDeviceToHost, stream));
+    KCT_CUDA(cudaStreamSynchronize(stream));
+    const double range = mm[1] - mm[0];
+    return range > 0.0 ? std::max(1e-8, 1e-4 * range) : 1e-4;
+}
+
+void copy_hist(double* dst, const double* src, size_t n, cudaStream_t s) {
+    if (dst && n) KCT_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+}
+
+void reset_report(kct_report* rep) {
+    if (!rep) return;
+    rep->objective_count = rep->residual_count = rep->error_count = rep->outer_count = 0;
+    rep->solve_seconds = 0.0;
+    rep->tau = 0.0;
+    rep->converged = rep->breakdown = 0;
+}
+
+}  // namespace
+
+double resolve_tau(double tau, const float* ref, size_t n) {
+    if (tau > 0.0) return tau;
+    if (!ref || n == 0) return 1e-4;
+    float lo = ref[0], hi = ref[0];
+    for (size_t i = 1; i < n; ++i) {
+        lo = std::min(lo, ref[i]);
+        hi = std::max(hi, ref[i]);
+    }
+    const double range = (double)hi - (double)lo;
+    return range > 0.0 ? std::max(1e-8, 1e-4 * range) : 1e-4;
+}
+
+// cgls_recon / baseline_solve (recon.hpp:274-315)
+void cgls_recon(Projector& P, const float* b, size_t iters, const float* x0, const float* gt,
+                double tol, float* x_out, kct_report* rep, int mem, int layout,
+                cudaStream_t stream) {
+    if (!b || !x_out) throw ConfigError("cgls_recon: null buffer");
+    if (iters < 1) throw ConfigError("reconstruction needs at least one iteration");
+    reset_report(rep);
+    Workspace& w = workspace(P, iters, 1);
+    if (gt) ensure(w.gt, w.m);
+    load(P, w.b, b, w.n, false, mem, layout, stream);
+    if (x0) load(P, w.x, x0, w.m, true, mem, layout, stream);
+    else KCT_CUDA(cudaMemsetAsync(w.x, 0, w.m * sizeof(float), stream));
+    if (gt) load(P, w.gt, gt, w.m, true, mem, layout, stream);
+    init_ctl(w, 0.0, 0.0, stream);
+    Engine e{P, w, stream};
+    e.rc.nx = P.grid().nx; e.rc.ny = P.grid().ny; e.rc.nz = P.grid().nz;
+    if (gt) e.ground_truth_norm();
+    KCT_CUDA(cudaStreamSynchronize(stream));
+
+    const double t0 = now_s();
+    e.start(x0 == nullptr, tol, -1);
+    for (size_t it = 0; it < iters; ++it) e.iterate(w.hist, w.hist + w.cap, gt != nullptr);
+    const Ctl c = read_ctl(w, stream);
+    const double secs = now_s() - t0;
+    throw_solver(c);
+    stage_out(P, w.x, x_out, w.m, true, mem, layout, 2, stream);
+    if (rep) {
+        const size_t n = (size_t)c.iters;
+        copy_hist(rep->residual_history, w.hist, n, stream);
+        if (gt) copy_hist(rep->error_history, w.hist + w.cap, n, stream);
+        KCT_CUDA(cudaStreamSynchronize(stream));
+        rep->residual_count = n;
+        rep->error_count = gt ? n : 0;
+        if (rep->objective_history && rep->residual_history)
+            for (size_t i = 0; i < n; ++i)
+                rep->objective_history[i] = rep->residual_history[i] * rep->residual_history[i];
+        rep->objective_count = n;
+        if (rep->outer_boundaries) rep->outer_boundaries[0] = n;
+        if (rep->outer_seconds) rep->outer_seconds[0] = secs;
+        rep->outer_count = 1;
+        rep->solve_seconds = secs;
+        rep->converged = c.converged;
+        rep->breakdown = c.breakdown;
+    }
+    KCT_CUDA(cudaStreamSynchronize(stream));
+}
+
+// irn_setup + irn_solve (recon.hpp:141-247)
+void irn_solve(Projector& P, int kind, const float* b, const float* prior, const float* x0,
+               const float* gt, const kct_reg_params& p, float* x_out, kct_report* rep, int mem,
+               int layout, cudaStream_t stream) {
+    if (kind != KCT_KIND_TV && kind != KCT_KIND_PIPLE && kind != KCT_KIND_PICCS)
+        throw ConfigError("unknown reconstruction kind");
+    if (!b || !x_out) throw ConfigError("irn: null buffer");
+    if (p.outer_iters < 1 || p.inner_iters < 1)
+        throw ConfigError("reconstruction needs at least one outer and one inner iteration");
+    if (p.alpha < 0.0) throw ConfigError("alpha must be non-negative");
+    if (!std::isfinite(p.alpha) || !std::isfinite(p.lambda) || !std::isfinite(p.tau))
+        throw ConfigError("regularisation parameters must be finite");
+    if (kind != KCT_KIND_TV && !prior) throw ConfigError("prior volume required");
+    const double alpha = p.alpha;
+    const double lambda = p.lambda < 0.0 ? alpha : p.lambda;
+    const size_t outer = p.outer_iters, inner = p.inner_iters;
+    reset_report(rep);
+
+    Workspace& w = workspace(P, outer * inner, outer + 1);
+    const bool use_prior = kind != KCT_KIND_TV;
+    if (use_prior) ensure(w.prior, w.m);
+    if (alpha != 0.0) ensure(w.w1, w.m);
+    if (kind == KCT_KIND_PICCS && lambda != 0.0) ensure(w.w2, w.m);
+    if (gt) ensure(w.gt, w.m);
+    load(P, w.b, b, w.n, false, mem, layout, stream);
+    if (use_prior) load(P, w.prior, prior, w.m, true, mem, layout, stream);
+    if (x0) load(P, w.x, x0, w.m, true, mem, layout, stream);
+    else KCT_CUDA(cudaMemsetAsync(w.x, 0, w.m * sizeof(float), stream));
+    if (gt) load(P, w.gt, gt, w.m, true, mem, layout, stream);
+
+    // tau from the initial image, else the prior when the prior term is active
+    const float* tau_ref = x0 ? w.x : ((use_prior && lambda != 0.0) ? w.prior : nullptr);
+    const double tau = device_tau(w, tau_ref, w.m, p.tau, stream);
+
+    Engine e{P, w, stream};
+    e.kind = kind;
+    e.rc.nx = P.grid().nx; e.rc.ny = P.grid().ny; e.rc.nz = P.grid().nz;
+    e.rc.use_w1 = alpha != 0.0;
+    e.rc.mode2 = lambda == 0.0 ? 0 : (kind == KCT_KIND_PICCS ? 1 : (kind == KCT_KIND_PIPLE ? 2 : 0));
+    e.rc.alpha2 = (float)(alpha * alpha);
+    e.rc.lambda2 = (float)(lambda * lambda);
+    e.rc.tau2 = (float)(tau * tau);
+    init_ctl(w, alpha * alpha, e.rc.mode2 ? lambda * lambda : 0.0, stream);
+    if (gt) e.ground_truth_norm();
+    KCT_CUDA(cudaStreamSynchronize(stream));
+
+    std::vector<uint64_t> bounds;
+    std::vector<double> secs;
+    size_t n_res = 0;
+    bool x_zero = x0 == nullptr;
+    int converged = 0, breakdown = 0;
+    const double t_start = now_s();
+    for (size_t cycle = 0; cycle < outer; ++cycle) {
+        const double t_cycle = now_s();
+        e.weights(true);
+        if (p.warm_start) {
+            e.start(x_zero, p.inner_tolerance, (int)cycle);
+        } else {
+            if (cycle == 0) e.objective(x_zero, 0);
+            KCT_CUDA(cudaMemsetAsync(w.x, 0, w.m * sizeof(float), stream));
+            e.start(true, p.inner_tolerance, -1);
+        }
+        x_zero = false;
+        for (size_t it = 0; it < inner; ++it)
+            e.iterate(w.hist + n_res, w.hist + w.cap + n_res, gt != nullptr);
+        if (!p.warm_start) {
+            e.weights(false);
+            e.objective(false, (int)cycle + 1);
+        }
+        const Ctl c = read_ctl(w, stream);
+        throw_solver(c);
+        n_res += (size_t)c.iters;
+        converged = c.converged;
+        breakdown = c.breakdown;
+        bounds.push_back(n_res);
+        secs.push_back(now_s() - t_cycle);
+    }
+    if (p.warm_start) {
+        e.weights(false);
+        e.objective(false, (int)outer);
+    }
+    KCT_CUDA(cudaStreamSynchronize(stream));
+    const double solve = now_s() - t_start;
+    stage_out(P, w.x, x_out, w.m, true, mem, layout, 2, stream);
+    if (rep) {
+        copy_hist(rep->objective_history, w.obj, outer + 1, stream);
+        copy_hist(rep->residual_history, w.hist, n_res, stream);
+        if (gt) copy_hist(rep->error_history, w.hist + w.cap, n_res, stream);
+        rep->objective_count = outer + 1;
+        rep->residual_count = n_res;
+        rep->error_count = gt ? n_res : 0;
+        rep->outer_count = outer;
+        for (size_t c = 0; c < outer; ++c) {
+            if (rep->outer_boundaries) rep->outer_boundaries[c] = bounds[c];
+            if (rep->outer_seconds) rep->outer_seconds[c] = secs[c];
+        }
+        rep->solve_seconds = solve;
+        rep->tau = tau;
+        rep->converged = converged;
+        rep->breakdown = breakdown;
+    }
+    KCT_CUDA(cudaStreamSynchronize(stream));
+}
+
+}  // namespace kct

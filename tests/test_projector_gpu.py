@@ -1,0 +1,133 @@
+"""GPU parity of the CUDA projector pair against the reference / oracle.
+
+Bar (BASELINE.json north_star): projections and backprojections within 1e-4
+relative L2 of the float64 reference on identical float32 inputs.  Restates
+proj/tests/test_projector.cpp properties (adjoint pair, exact transpose,
+uniform-volume chords, bit-identical reruns, size checks) on the CUDA path.
+"""
+import numpy as np
+import pytest
+
+import paper_2509_08574_b200 as k
+from oracle import Oracle
+from tests._util import (baseline_geometry, geom_from, grid_from, load_golden, rel_l2,
+                         tiny_geometry, tiny_grid, to_pkg)
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def ora():
+    import oracle
+    oracle.build("ora")
+    return Oracle("ora")
+
+
+def projector(grid, geom):
+    gs, ge = to_pkg(grid, geom)
+    return k.ConeBeamProjector(gs, ge)
+
+
+@pytest.mark.parametrize("case", ["op_tiny", "op_tiny_odd", "op_c1_small"])
+def test_golden_operator_parity(case):
+    d = load_golden(case)
+    A = projector(grid_from(d), geom_from(d))
+    assert rel_l2(A.apply(d["x"]), d["ax"]) < TOL
+    assert rel_l2(A.apply_adjoint(d["y"]), d["aty"]) < TOL
+    assert rel_l2(A.apply(np.full(A.domain_size(), 2.5)), d["ax_uniform"]) < TOL
+    # exact Siddon nnz, up to rounding-level degenerate (corner) segments
+    assert abs(A.count_nnz() - int(d["nnz"])) <= max(2, 1e-3 * int(d["nnz"]))
+
+
+def test_uniform_volume_gives_chords(ora):
+    """test_projector.cpp:54-69: A * 2.5 = 2.5 * chord per ray."""
+    grid, geom = tiny_grid(6, 6, 6), tiny_geometry(4, 8, 8)
+    A = projector(grid, geom)
+    got = A.apply(np.full(grid.count, 2.5, dtype=np.float32))
+    want = ora.forward(grid, geom, np.full(grid.count, 2.5))
+    np.testing.assert_allclose(got, want, rtol=2e-6, atol=2e-6)
+
+
+def test_exact_transpose_matricised():
+    """test_projector.cpp:77-85 on the CUDA pair: dense A from apply() equals dense
+    A^T from apply_adjoint() (float32 rounding), non-negative, non-trivial."""
+    grid, geom = tiny_grid(), tiny_geometry(3, 6, 5)
+    A = projector(grid, geom)
+    m, n = grid.count, geom.ray_count
+    fwd = np.stack([A.apply(np.eye(m, dtype=np.float32)[j]) for j in range(m)], axis=1)
+    adj = np.stack([A.apply_adjoint(np.eye(n, dtype=np.float32)[i]) for i in range(n)], axis=0)
+    assert np.abs(fwd - adj).max() <= 1e-6 * np.abs(fwd).max()
+    assert fwd.min() >= 0 and fwd.max() > 0
+    ref = Oracle("ora")
+    dense_ref = np.stack([ref.forward(grid, geom, np.eye(m)[j]) for j in range(m)], axis=1)
+    assert np.abs(fwd - dense_ref).max() <= 1e-5 * np.abs(dense_ref).max()
+    assert np.array_equal(fwd > 0, adj > 0)
+
+
+def test_adjoint_identity():
+    """test_projector.cpp:71-75 (<Ax,y> = <x,A^T y>), float32 pair."""
+    grid, geom = tiny_grid(5, 6, 4), tiny_geometry(7, 9, 8)
+    A = projector(grid, geom)
+    rng = np.random.default_rng(22)
+    for _ in range(5):
+        x = rng.uniform(-1, 1, grid.count).astype(np.float32)
+        y = rng.uniform(-1, 1, geom.ray_count).astype(np.float32)
+        lhs = np.dot(A.apply(x).astype(np.float64), y)
+        rhs = np.dot(x.astype(np.float64), A.apply_adjoint(y))
+        assert abs(lhs - rhs) / abs(lhs) < 1e-5
+
+
+def test_bit_identical_reruns():
+    """test_projector.cpp:100-111."""
+    grid, geom = tiny_grid(6, 5, 6), tiny_geometry(5)
+    A = projector(grid, geom)
+    rng = np.random.default_rng(23)
+    x = rng.uniform(-1, 1, grid.count).astype(np.float32)
+    y = rng.uniform(-1, 1, geom.ray_count).astype(np.float32)
+    ax, aty = A.apply(x), A.apply_adjoint(y)
+    for _ in range(3):
+        assert np.array_equal(A.apply(x), ax)
+        assert np.array_equal(A.apply_adjoint(y), aty)
+
+
+def test_size_mismatch():
+    """test_projector.cpp:143-147."""
+    A = projector(tiny_grid(), tiny_geometry(2))
+    with pytest.raises(k.ConfigError):
+        A.apply(np.zeros(A.domain_size() + 1, dtype=np.float32))
+
+
+@pytest.mark.parametrize("cfg,n_angles", [(1, 64), (2, 8), (3, 3), (4, 1), (5, 2)])
+def test_baseline_geometry_parity(ora, cfg, n_angles):
+    """Full-size BASELINE volumes/detectors, angle subsets the oracle finishes in seconds."""
+    grid, geom = baseline_geometry(cfg, n_angles=n_angles)
+    rng = np.random.default_rng(cfg)
+    # smooth-ish positive volume plus noise, like attenuation maps
+    x = rng.uniform(0.0, 0.04, grid.count).astype(np.float32)
+    A = projector(grid, geom)
+    ax = A.apply(x)
+    ref = ora.forward(grid, geom, x)
+    assert rel_l2(ax, ref) < TOL
+    y = rng.uniform(0.0, 1.0, geom.ray_count).astype(np.float32)
+    assert rel_l2(A.apply_adjoint(y), ora.adjoint(grid, geom, y)) < TOL
+
+
+def test_device_native_matches_host_reference():
+    """Native-layout device tensors and reference-layout host arrays agree."""
+    import torch
+    grid, geom = baseline_geometry(1, n_angles=16)
+    A = projector(grid, geom)
+    rng = np.random.default_rng(3)
+    x = rng.uniform(0, 1, grid.count).astype(np.float32)
+    host = A.apply(x)
+    xd = torch.from_numpy(x).cuda()
+    xn = A.volume_to_native(xd)
+    yn = A.apply(xn)  # native in, native out
+    yr = A.proj_from_native(yn)
+    assert np.array_equal(yr.cpu().numpy(), host)
+    yref_dev = A.apply(xd, layout="reference")
+    assert np.array_equal(yref_dev.cpu().numpy(), host)
+    back = A.apply_adjoint(yn)
+    back_host = A.apply_adjoint(host)
+    assert np.array_equal(A.volume_from_native(back).cpu().numpy(), back_host)

@@ -1,0 +1,196 @@
+"""GPU parity of the device-resident CGLS / IRN drivers against the reference.
+
+Bar (north_star): reconstructions after a fixed iteration count within 1e-3
+relative L2 of the float64 reference iterate.  Also restates the reference's
+solver unit tests (proj/tests/test_krylov.cpp, test_recon.cpp).
+"""
+import numpy as np
+import pytest
+
+import paper_2509_08574_b200 as k
+from oracle import KIND_PICCS, Grid, Oracle
+from tests._util import (baseline_geometry, geom_from, grid_from, load_golden, recon_geometry,
+                         rel_l2, to_pkg)
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def ora():
+    import oracle
+    oracle.build("ora")
+    return Oracle("ora")
+
+
+@pytest.fixture(scope="module")
+def small():
+    d = load_golden("recon_small")
+    gs, ge = to_pkg(grid_from(d), geom_from(d))
+    return d, gs, ge, k.ConeBeamProjector(gs, ge)
+
+
+def test_cgls_recon_golden(small):
+    d, gs, ge, A = small
+    rep = k.cgls_recon(k.ProjectionSet(ge, d["b"]), gs, 8,
+                       k.ReconOptions(ground_truth=d["truth"]), projector=A)
+    assert rel_l2(rep.volume, d["cgls_x"]) < RTOL
+    np.testing.assert_allclose(rep.residual_history, d["cgls_res"], rtol=RTOL)
+    np.testing.assert_allclose(rep.error_history, d["cgls_err"], rtol=RTOL)
+    np.testing.assert_allclose(rep.objective_history, d["cgls_res"] ** 2, rtol=2 * RTOL)
+    assert list(rep.outer_boundaries) == [8]
+
+
+@pytest.mark.parametrize("tag,fn", [("tv", "irn_tv"), ("piple", "irn_piple"), ("piccs", "irn_piccs")])
+def test_irn_golden(small, tag, fn):
+    d, gs, ge, A = small
+    params = k.RegularizationParams(alpha=0.3, tau=1e-3, outer_iters=3, inner_iters=4)
+    opts = k.ReconOptions(ground_truth=d["truth"])
+    proj = k.ProjectionSet(ge, d["b"])
+    if tag == "tv":
+        rep = k.irn_tv(proj, gs, params, opts, projector=A)
+    else:
+        rep = getattr(k, fn)(proj, gs, d["prior"], params, opts, projector=A)
+    assert rel_l2(rep.volume, d[f"{tag}_x"]) < RTOL
+    np.testing.assert_allclose(rep.objective_history, d[f"{tag}_obj"], rtol=RTOL)
+    np.testing.assert_allclose(rep.residual_history, d[f"{tag}_res"], rtol=RTOL)
+    np.testing.assert_allclose(rep.error_history, d[f"{tag}_err"], rtol=RTOL)
+    assert list(rep.outer_boundaries) == [4, 8, 12]
+    assert len(rep.outer_seconds) == 3
+
+
+def test_irn_piccs_auto_tau(small):
+    d, gs, ge, A = small
+    params = k.RegularizationParams(alpha=0.2, lambda_=0.4, outer_iters=2, inner_iters=5)
+    rep = k.irn_piccs(k.ProjectionSet(ge, d["b"]), gs, d["prior"], params, projector=A)
+    assert rep.tau == pytest.approx(float(d["piccs_auto_tau"]), rel=1e-12)
+    assert rel_l2(rep.volume, d["piccs_auto_x"]) < RTOL
+    np.testing.assert_allclose(rep.objective_history, d["piccs_auto_obj"], rtol=RTOL)
+
+
+def _sphere_problem(n=8, n_angles=6):
+    grid = Grid(n, n, n)
+    geom = recon_geometry(n_angles)
+    gs, ge = to_pkg(grid, geom)
+    x = -1 + 2 * (np.arange(n) + 0.5) / n
+    Z, Y, X = np.meshgrid(x, x, x, indexing="ij")
+    truth = np.where(X * X + Y * Y + Z * Z <= 0.36, 0.8, 0.0).astype(np.float32).reshape(-1)
+    A = k.ConeBeamProjector(gs, ge)
+    b = A.apply(truth)
+    return gs, ge, A, truth, b
+
+
+def test_alpha_zero_is_plain_cgls():
+    """test_recon.cpp:178-201: irn_tv(alpha=0) == cgls bit for bit; cycles == warm restarts."""
+    gs, ge, A, truth, b = _sphere_problem()
+    proj = k.ProjectionSet(ge, b)
+    reg = k.irn_tv(proj, gs, k.RegularizationParams(alpha=0.0, lambda_=0.0, outer_iters=1,
+                                                    inner_iters=8), projector=A)
+    plain = k.cgls_recon(proj, gs, 8, projector=A)
+    assert np.array_equal(reg.volume, plain.volume)
+    cyc = k.irn_tv(proj, gs, k.RegularizationParams(alpha=0.0, lambda_=0.0, outer_iters=3,
+                                                    inner_iters=4), projector=A)
+    x = None
+    for _ in range(3):
+        x = k.cgls_recon(proj, gs, 4, k.ReconOptions(initial=x), projector=A).volume
+    assert np.array_equal(cyc.volume, x)
+
+
+def test_lambda_zero_collapses_onto_tv():
+    """test_recon.cpp:238-275: lambda = 0 -> PICCS / PIPLE reproduce irn_tv bitwise."""
+    gs, ge, A, truth, b = _sphere_problem(7, 5)
+    proj = k.ProjectionSet(ge, b)
+    p = k.RegularizationParams(alpha=0.25, lambda_=0.0, outer_iters=3, inner_iters=5)
+    prior = 0.9 * truth
+    r_tv = k.irn_tv(proj, gs, p, projector=A)
+    r_pc = k.irn_piccs(proj, gs, prior, p, projector=A)
+    r_pl = k.irn_piple(proj, gs, prior, p, projector=A)
+    assert np.array_equal(r_tv.volume, r_pc.volume)
+    assert np.array_equal(r_tv.volume, r_pl.volume)
+
+
+def test_objective_descent():
+    """test_recon.cpp:203-236: majorise-minimise never increases the objective."""
+    gs, ge, A, truth, b = _sphere_problem()
+    rng = np.random.default_rng(99)
+    b = (b + 0.02 * np.linalg.norm(b) / np.sqrt(b.size) * rng.standard_normal(b.size)).astype(np.float32)
+    proj = k.ProjectionSet(ge, b)
+    p = k.RegularizationParams(alpha=0.3, tau=1e-3, outer_iters=4, inner_iters=6)
+    opts = k.ReconOptions(ground_truth=truth)
+    for rep in (k.irn_tv(proj, gs, p, opts, projector=A),
+                k.irn_piple(proj, gs, truth, p, opts, projector=A),
+                k.irn_piccs(proj, gs, truth, p, opts, projector=A)):
+        h = rep.objective_history
+        assert len(h) == 5
+        assert np.all(h[1:] <= h[:-1] * (1 + 1e-6))
+        assert len(rep.error_history) == len(rep.residual_history) == 24
+        assert np.all(np.isfinite(rep.volume))
+
+
+def test_warm_start_tolerance_converges():
+    """test_krylov.cpp:90-118: tolerance stop and warm restarts."""
+    gs, ge, A, truth, b = _sphere_problem()
+    proj = k.ProjectionSet(ge, b)
+    first = k.cgls_recon(proj, gs, 6, projector=A)
+    second = k.cgls_recon(proj, gs, 6, k.ReconOptions(initial=first.volume), projector=A)
+    assert second.residual_history[-1] < first.residual_history[-1]
+    done = k.cgls_recon(proj, gs, 200, tolerance=1e-3, projector=A)
+    assert done.converged and len(done.residual_history) < 200
+
+
+def test_nonfinite_data_is_solver_error():
+    """test_krylov.cpp:146-152."""
+    gs, ge, A, truth, b = _sphere_problem()
+    bad = b.copy()
+    bad[ge.nu // 2 + ge.nu * (ge.nv // 2)] = np.inf  # a ray through the volume
+    with pytest.raises(k.SolverError):
+        k.cgls_recon(k.ProjectionSet(ge, bad), gs, 3, projector=A)
+
+
+def test_parameter_validation():
+    """test_recon.cpp:88-120."""
+    gs, ge, A, truth, b = _sphere_problem(6, 4)
+    proj = k.ProjectionSet(ge, b)
+    with pytest.raises(k.ConfigError):
+        k.irn_tv(proj, gs, k.RegularizationParams(outer_iters=0), projector=A)
+    with pytest.raises(k.ConfigError):
+        k.irn_tv(proj, gs, k.RegularizationParams(alpha=-0.1), projector=A)
+    with pytest.raises(k.ConfigError):
+        k.irn_tv(proj, gs, k.RegularizationParams(tau=np.inf), projector=A)
+    with pytest.raises(k.ConfigError):
+        k.cgls_recon(proj, gs, 0, projector=A)
+    with pytest.raises(k.ConfigError):
+        k.irn_piccs(proj, gs, np.zeros(5, dtype=np.float32), projector=A)
+
+
+def test_c1_cgls_parity(ora):
+    """BASELINE config 1: 64^3, 96^2, 64 views, 20 CGLS iterations from zero."""
+    grid, geom = baseline_geometry(1)
+    gs, ge = to_pkg(grid, geom)
+    rng = np.random.default_rng(11)
+    truth = rng.uniform(0, 0.04, grid.count).astype(np.float32)
+    A = k.ConeBeamProjector(gs, ge)
+    b = A.apply(truth)
+    x_ref, r_ref = ora.cgls_recon(grid, geom, b.astype(np.float64), 20)
+    rep = k.cgls_recon(k.ProjectionSet(ge, b), gs, 20, projector=A)
+    assert rel_l2(rep.volume, x_ref) < RTOL
+    np.testing.assert_allclose(rep.residual_history, r_ref["residual_history"], rtol=RTOL)
+
+
+@pytest.mark.slow
+def test_c2_piccs_parity(ora):
+    """BASELINE config 2 geometry (128^3, 192^2, 45 views), PICCS 2x3, alpha=0.5."""
+    grid, geom = baseline_geometry(2)
+    gs, ge = to_pkg(grid, geom)
+    rng = np.random.default_rng(12)
+    prior = rng.uniform(0, 0.04, grid.count).astype(np.float32)
+    truth = prior.copy()
+    truth[grid.count // 2: grid.count // 2 + 2000] += 0.01
+    A = k.ConeBeamProjector(gs, ge)
+    b = A.apply(truth)
+    p = dict(alpha=0.5, outer_iters=2, inner_iters=3)
+    x_ref, r_ref = ora.irn(grid, geom, KIND_PICCS, b.astype(np.float64), prior, p)
+    rep = k.irn_piccs(k.ProjectionSet(ge, b), gs, prior,
+                      k.RegularizationParams(alpha=0.5, outer_iters=2, inner_iters=3), projector=A)
+    assert rel_l2(rep.volume, x_ref) < RTOL
+    np.testing.assert_allclose(rep.objective_history, r_ref["objective_history"], rtol=RTOL)
