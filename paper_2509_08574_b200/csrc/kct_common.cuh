@@ -44,18 +44,32 @@ struct CudaError : std::runtime_error {
 // rotation axis on the ray (re-basing at R keeps |w| <~ FOV, which is what
 // makes float32 crossings accurate; a [0,1] parametrisation over the full
 // source-detector segment is not).
-//   x-plane n is crossed at  w = fmaf(n, dx, bx);  y-plane n at fmaf(n, dy, by)
+//   x-plane n is crossed at  w = (float)fma(n, dx, bx)   (float64: a ray nearly
+//   parallel to the planes has |bx|, |dx| >> |w|), y-plane n likewise
 //   [w_in, w_out]  clip of the ray against the volume's xy box and t in [0,1]
 //   continuous z index at w_in of detector row dv (float64, split as k0 + f0):
 //           kz_in = fma(dv, g_in, -kz0),  k0 = floor(kz_in),  f0 = kz_in - k0
 //   z-plane P is crossed at  w = fmaf((P - k0) - f0, inv_dv * inv_h1, w_in)
 //   3D length = dw * sqrt(1 + (dv * inv_l)^2)
+// Forward and adjoint evaluate exactly these expressions, so every segment
+// endpoint is bit-identical between A and A^T.
 struct __align__(16) ColParams {
-    float bx, dx, by, dy;
+    double bx, dx, by, dy;
     float w_in, w_out, inv_h1, inv_l;
     double g_in;
     int i0, j0;  // entry voxel (valid when w_in < w_out)
 };
+
+__device__ __forceinline__ float xcross(const ColParams& c, int n) {
+    return __double2float_rn(fma((double)n, c.dx, c.bx));
+}
+__device__ __forceinline__ float ycross(const ColParams& c, int n) {
+    return __double2float_rn(fma((double)n, c.dy, c.by));
+}
+// z-plane P crossing of a row with z state (k0, f0) and inverse slope imk
+__device__ __forceinline__ float zcross(int P, int k0, float f0, float imk, float w_in) {
+    return __fmaf_rn(__fsub_rn((float)(P - k0), f0), imk, w_in);
+}
 
 constexpr int kMaxAnglesPerLaunch = 1024;
 

@@ -1,15 +1,18 @@
 // projector.cu — Siddon forward projector (ray-driven, 2D+1) and its exact
-// transpose (voxel-driven gather) for sm_100a.
+// transpose (brick-owned, deterministic) for sm_100a.
 //
 // Reference semantics: projector.hpp:53-131 (traverse_ray), :173-204
 // (project_forward), :207-261 (project_adjoint).  The intersection lengths are
 // the reference's exact Siddon lengths; only rounding differs (float32 values,
-// float64 host geometry).  Forward and adjoint evaluate every ray-voxel
-// segment endpoint with the same float expressions (ColParams, kct_common.cuh)
-// so the pair is a transpose up to the rounding of the final products.
+// float64 host geometry and plane crossings).  Forward and adjoint evaluate
+// every ray-voxel segment endpoint with the same expressions (ColParams,
+// xcross/ycross/zcross in kct_common.cuh), so A^T is the transpose of A up to
+// the rounding of the final products and sums.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <limits>
+#include <string>
 
 #include "projector.cuh"
 
@@ -63,19 +66,18 @@ __global__ void __launch_bounds__(128) fwd_kernel(const float* __restrict__ vol,
         if (!row_ok) kk = -1 - nz;  // never valid, never crosses
         k[c] = kk;
         const int P = dv > 0.f ? kk + 1 : kk;
-        wz[c] = (row_ok && dv != 0.f && P >= 0 && P <= nz)
-                    ? __fmaf_rn(__fsub_rn((float)(P - k0), fz[c]), imk[c], cp.w_in)
-                    : kInf;
+        wz[c] = (row_ok && dv != 0.f && P >= 0 && P <= nz) ? zcross(P, k0, fz[c], imk[c], cp.w_in)
+                                                            : kInf;
     }
 
     if (cp.w_in < cp.w_out) {
         const int nx = g.nx, ny = g.ny;
         int i = cp.i0, j = cp.j0;
-        const int stx = cp.dx > 0.f ? 1 : -1, sty = cp.dy > 0.f ? 1 : -1;
-        int px = cp.dx > 0.f ? i + 1 : i;
-        int py = cp.dy > 0.f ? j + 1 : j;
-        float wnx = cp.dx != 0.f ? __fmaf_rn((float)px, cp.dx, cp.bx) : kInf;
-        float wny = cp.dy != 0.f ? __fmaf_rn((float)py, cp.dy, cp.by) : kInf;
+        const int stx = cp.dx > 0.0 ? 1 : -1, sty = cp.dy > 0.0 ? 1 : -1;
+        int px = cp.dx > 0.0 ? i + 1 : i;
+        int py = cp.dy > 0.0 ? j + 1 : j;
+        float wnx = cp.dx != 0.0 ? xcross(cp, px) : kInf;
+        float wny = cp.dy != 0.0 ? ycross(cp, py) : kInf;
         float wcur = cp.w_in;
         for (;;) {
             const bool stepx = wnx <= wny;
@@ -100,10 +102,8 @@ __global__ void __launch_bounds__(128) fwd_kernel(const float* __restrict__ vol,
                         const bool ok = (unsigned)k[c] < (unsigned)nz;
                         v[c] = ok ? (COUNT ? 1.f : __ldg(vol + col + k[c])) : 0.f;
                         const int P = kstep[c] > 0 ? k[c] + 1 : k[c];
-                        wz[c] = (P >= 0 && P <= nz)
-                                    ? __fmaf_rn(__fsub_rn((float)(P - kz0i[c]), fz[c]), imk[c],
-                                                cp.w_in)
-                                    : kInf;
+                        wz[c] = (P >= 0 && P <= nz) ? zcross(P, kz0i[c], fz[c], imk[c], cp.w_in)
+                                                    : kInf;
                     } while (wz[c] < wb);
                 }
                 const float len = wb - wa[c];
@@ -116,12 +116,12 @@ __global__ void __launch_bounds__(128) fwd_kernel(const float* __restrict__ vol,
                 i += stx;
                 if ((unsigned)i >= (unsigned)nx) break;
                 px += stx;
-                wnx = __fmaf_rn((float)px, cp.dx, cp.bx);
+                wnx = xcross(cp, px);
             } else {
                 j += sty;
                 if ((unsigned)j >= (unsigned)ny) break;
                 py += sty;
-                wny = __fmaf_rn((float)py, cp.dy, cp.by);
+                wny = ycross(cp, py);
             }
         }
     }
@@ -141,90 +141,284 @@ __global__ void __launch_bounds__(128) fwd_kernel(const float* __restrict__ vol,
     }
 }
 
+// Detector-column footprint of an axis-aligned xy rectangle at one angle:
+// the columns whose ray passes the rectangle's interior (projected corners,
+// widened by eps pixels).
+__device__ __forceinline__ void footprint(const DevGeom& g, float cth, float sth, float X0, float X1,
+                                          float Y0, float Y1, int& lo, int& hi) {
+    lo = 0;
+    hi = g.nu - 1;
+    const float l00 = g.dso - X0 * cth - Y0 * sth, l01 = g.dso - X0 * cth - Y1 * sth;
+    const float l10 = g.dso - X1 * cth - Y0 * sth, l11 = g.dso - X1 * cth - Y1 * sth;
+    const float lmin = fminf(fminf(l00, l01), fminf(l10, l11));
+    if (g.full_footprint && !(lmin > 0.f)) return;
+    const float lx0 = -X0 * sth, lx1 = -X1 * sth, ly0 = Y0 * cth, ly1 = Y1 * cth;
+    const float u00 = (lx0 + ly0) / l00, u01 = (lx0 + ly1) / l01;
+    const float u10 = (lx1 + ly0) / l10, u11 = (lx1 + ly1) / l11;
+    const float umin = fminf(fminf(u00, u01), fminf(u10, u11)) * g.dsd;
+    const float umax = fmaxf(fmaxf(u00, u01), fmaxf(u10, u11)) * g.dsd;
+    const float off = 0.5f * g.nu - 0.5f;
+    constexpr float eps = 1e-3f;
+    lo = max(0, (int)ceilf((umin - g.off_u) / g.pu + off - eps));
+    hi = min(g.nu - 1, (int)floorf((umax - g.off_u) / g.pu + off + eps));
+}
+
 // ----------------------------------------------------------------------------
-// Adjoint (exact transpose), voxel-driven.  One warp = one voxel column (i,j),
-// lane owns voxels k = kbase + lane + 32c (c < K).  For each angle the
-// detector columns whose rays cross the xy square of (i,j) are found from the
-// projected square corners; for each such column the xy chord [wa,wb] is the
-// same float expression the forward walk produces, and for every row whose
-// z-span over the chord touches slab k the overlap length is gathered from
-// the v-fastest projection (consecutive lanes -> consecutive rows).
+// Adjoint, brick-owned exact transpose.  Each warp owns a brick of
+// BX x BY voxel columns x bz slabs, accumulated in shared memory.  For every
+// angle and every detector column whose rays cross the brick, the warp replays
+// the forward's xy walk through the brick once (segment list in shared
+// memory), then lanes take detector rows (stride S so that no two lanes of a
+// pass can touch the same voxel: S * dkz_min > 1 + span_max, derived on the
+// host) and deposit len * F * y for each ray-voxel segment — the same
+// segment endpoints the forward computes.  Every voxel is owned by one warp
+// and its contributions are added in a fixed (angle, column, pass, row group,
+// segment) order: deterministic, no atomics, exactly A^T.
+// ----------------------------------------------------------------------------
+constexpr int BX = 8, BY = 8;
+constexpr int kAdjWarps = 4;
+constexpr int kMaxSeg = BX + BY + 4;
+constexpr int kMaxBz = 64;
+
+struct __align__(16) Seg {
+    float wa, wb;
+    int ij, pad;
+};
+
+struct BrickCfg {
+    int bz;  // slabs per brick (<= kMaxBz)
+    int S;   // row stride of a pass
+    int nbx, nby, nbz;
+};
+
+__global__ void __launch_bounds__(kAdjWarps * 32) adj_brick_kernel(
+    const float* __restrict__ proj, float* __restrict__ out, const ColParams* __restrict__ cols,
+    const float* __restrict__ dvtab, const float* __restrict__ invdv, const double* __restrict__ dvd,
+    DevGeom g, BrickCfg bc, AngleBatch ab, int nab, int accumulate) {
+    extern __shared__ float sm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int brick = blockIdx.x * kAdjWarps + warp;
+    if (brick >= bc.nbx * bc.nby * bc.nbz) return;
+    const int bi = brick % bc.nbx, bj = (brick / bc.nbx) % bc.nby, bk = brick / (bc.nbx * bc.nby);
+    const int BZ = bc.bz;
+    const int I0 = bi * BX, J0 = bj * BY, K0 = bk * BZ;
+    const int bxn = min(BX, g.nx - I0), byn = min(BY, g.ny - J0), bzn = min(BZ, g.nz - K0);
+    const int nu = g.nu, nv = g.nv;
+    const int abase = warp * (BX * BY * BZ + 4 * kMaxSeg);  // this warp's accumulator
+    Seg* segs = reinterpret_cast<Seg*>(sm + abase + BX * BY * BZ);
+    for (int q = lane; q < BX * BY * BZ; q += 32) sm[abase + q] = 0.f;
+    __syncwarp();
+
+    const float X0 = g.ox + I0 * g.sx, X1 = g.ox + (I0 + bxn) * g.sx;
+    const float Y0 = g.oy + J0 * g.sy, Y1 = g.oy + (J0 + byn) * g.sy;
+    const float rpv = 1.f / g.pv;
+    const int S = bc.S;
+    const int kend = K0 + bzn;
+
+    for (int ia = 0; ia < nab; ++ia) {
+        int iu_lo, iu_hi;
+        footprint(g, ab.cs[ia].x, ab.cs[ia].y, X0, X1, Y0, Y1, iu_lo, iu_hi);
+        const ColParams* colp = cols + (size_t)ia * nu;
+        const float* yb = proj + (size_t)ia * nu * nv;
+        for (int iu = iu_lo; iu <= iu_hi; ++iu) {
+            const ColParams cp = colp[iu];
+            // chord of the column's xy line through the brick
+            float lo = cp.w_in, hi = cp.w_out;
+            if (cp.dx != 0.0) {
+                const float e0 = xcross(cp, I0), e1 = xcross(cp, I0 + bxn);
+                lo = fmaxf(lo, fminf(e0, e1));
+                hi = fminf(hi, fmaxf(e0, e1));
+            } else if (cp.i0 < I0 || cp.i0 >= I0 + bxn) {
+                continue;
+            }
+            if (cp.dy != 0.0) {
+                const float e0 = ycross(cp, J0), e1 = ycross(cp, J0 + byn);
+                lo = fmaxf(lo, fminf(e0, e1));
+                hi = fminf(hi, fmaxf(e0, e1));
+            } else if (cp.j0 < J0 || cp.j0 >= J0 + byn) {
+                continue;
+            }
+            if (!(lo < hi)) continue;
+            // rows whose z-span over [lo, hi] meets slabs [K0, K0 + bzn]
+            const float h1 = 1.f / cp.inv_h1;
+            const float gin = (float)cp.g_in;
+            const float Glo = gin + (lo - cp.w_in) * h1, Ghi = gin + (hi - cp.w_in) * h1;
+            const float n0 = (float)K0 + g.kz0, n1 = n0 + (float)bzn;
+            const float dlo = n0 >= 0.f ? n0 / Ghi : n0 / Glo;
+            const float dhi = n1 >= 0.f ? n1 / Glo : n1 / Ghi;
+            const int rlo = max(0, (int)ceilf((dlo - g.dv0) * rpv - 1e-3f));
+            const int rhi = min(nv - 1, (int)floorf((dhi - g.dv0) * rpv + 1e-3f));
+            if (rlo > rhi) continue;
+            // xy walk through the brick (the forward's walk restricted to it);
+            // segment n is written by lane n
+            int i = cp.dx != 0.0 ? (int)floor(((double)lo - cp.bx) / cp.dx) : cp.i0;
+            int j = cp.dy != 0.0 ? (int)floor(((double)lo - cp.by) / cp.dy) : cp.j0;
+            i = min(max(i, I0), I0 + bxn - 1);
+            j = min(max(j, J0), J0 + byn - 1);
+            const int stx = cp.dx > 0.0 ? 1 : -1, sty = cp.dy > 0.0 ? 1 : -1;
+            int px = cp.dx > 0.0 ? i + 1 : i;
+            int py = cp.dy > 0.0 ? j + 1 : j;
+            float wnx = cp.dx != 0.0 ? xcross(cp, px) : kInf;
+            float wny = cp.dy != 0.0 ? ycross(cp, py) : kInf;
+            float wcur = lo;
+            int nseg = 0;
+            for (;;) {
+                const bool stepx = wnx <= wny;
+                const float wnext = stepx ? wnx : wny;
+                const float wb = fmaxf(fminf(wnext, hi), wcur);
+                if (lane == nseg) {
+                    Seg sg;
+                    sg.wa = wcur;
+                    sg.wb = wb;
+                    sg.ij = abase + ((i - I0) + BX * (j - J0)) * BZ - K0;
+                    sg.pad = 0;
+                    segs[nseg] = sg;
+                }
+                ++nseg;
+                if (wnext >= hi || nseg == kMaxSeg) break;
+                wcur = fmaxf(wnext, wcur);
+                if (stepx) {
+                    i += stx;
+                    if (i < I0 || i >= I0 + bxn) break;
+                    px += stx;
+                    wnx = xcross(cp, px);
+                } else {
+                    j += sty;
+                    if (j < J0 || j >= J0 + byn) break;
+                    py += sty;
+                    wny = ycross(cp, py);
+                }
+            }
+            __syncwarp();
+            const float* ycol = yb + (size_t)iu * nv;
+            for (int p = 0; p < S; ++p) {
+                for (int base = rlo + p; base <= rhi; base += 32 * S) {
+                    const int iv = base + S * lane;
+                    if (iv <= rhi) {
+                        // the forward's per-ray z state (k0, f0, imk), then the
+                        // slab at lo: last plane crossed strictly before lo
+                        const float dv = dvtab[iv];
+                        const double kzd = fma(dvd[iv], cp.g_in, -g.kz0d);
+                        const int k0 = __double2int_rd(kzd);
+                        const float f0 = (float)(kzd - (double)k0);
+                        const float imk = __fmul_rn(invdv[iv], cp.inv_h1);
+                        const float q = dv * cp.inv_l;
+                        const float yf = __ldg(ycol + iv) * __fsqrt_rn(__fmaf_rn(q, q, 1.f));
+                        const float t = f0 + (lo - cp.w_in) * (dv * h1);
+                        int k = k0 + (int)floorf(t);
+                        int kstep;
+                        float wz;
+                        if (dv > 0.f) {
+                            kstep = 1;
+                            k = max(k, k0);
+                            while (k > k0 && !(zcross(k, k0, f0, imk, cp.w_in) < lo)) --k;
+                            while (zcross(k + 1, k0, f0, imk, cp.w_in) < lo) ++k;
+                            k = max(k, K0 - 1);
+                            wz = k + 1 <= kend ? zcross(k + 1, k0, f0, imk, cp.w_in) : kInf;
+                        } else if (dv < 0.f) {
+                            kstep = -1;
+                            k = min(k, k0);
+                            while (k < k0 && !(zcross(k + 1, k0, f0, imk, cp.w_in) < lo)) ++k;
+                            while (zcross(k, k0, f0, imk, cp.w_in) < lo) --k;
+                            k = min(k, kend);
+                            wz = k >= K0 ? zcross(k, k0, f0, imk, cp.w_in) : kInf;
+                        } else {
+                            kstep = 0;
+                            k = k0;
+                            wz = kInf;
+                        }
+                        for (int sgi = 0; sgi < nseg; ++sgi) {
+                            const Seg sg = segs[sgi];
+                            // first piece up to the next z-plane (or the segment end)
+                            const bool cr = wz < sg.wb;
+                            const float wm = cr ? wz : sg.wb;
+                            if ((unsigned)(k - K0) < (unsigned)bzn)
+                                sm[sg.ij + k] = __fmaf_rn(wm - sg.wa, yf, sm[sg.ij + k]);
+                            if (cr) {  // z-plane crossing(s) inside the segment (rare)
+                                float wa = wz;
+                                for (;;) {
+                                    k += kstep;
+                                    const int P = kstep > 0 ? k + 1 : k;
+                                    wz = (P >= K0 && P <= kend) ? zcross(P, k0, f0, imk, cp.w_in)
+                                                                : kInf;
+                                    const float we = fminf(wz, sg.wb);
+                                    if ((unsigned)(k - K0) < (unsigned)bzn)
+                                        sm[sg.ij + k] = __fmaf_rn(we - wa, yf, sm[sg.ij + k]);
+                                    if (!(wz < sg.wb)) break;
+                                    wa = wz;
+                                }
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+            __syncwarp();
+        }
+    }
+    // write the brick (coalesced runs of bzn slabs per voxel column)
+    for (int c = 0; c < bxn * byn; ++c) {
+        const int ci = c % bxn, cj = c / bxn;
+        float* o = out + ((size_t)(I0 + ci) + (size_t)g.nx * (J0 + cj)) * g.nz + K0;
+        const int a = abase + (ci + BX * cj) * BZ;
+        for (int kk = lane; kk < bzn; kk += 32) o[kk] = accumulate ? o[kk] + sm[a + kk] : sm[a + kk];
+    }
+}
+
+// ----------------------------------------------------------------------------
+// Adjoint, per-voxel gather (alternative; KCT_ADJOINT=gather).  One warp = one
+// voxel column (i,j), lane owns voxels k = kbase + lane + 32c.  For each angle
+// and footprint column the chord is computed from the voxel's own planes and
+// every candidate row's overlap with slab k from the shared crossing
+// expressions.  Slower than the brick kernel; kept as an independent check.
 // ----------------------------------------------------------------------------
 template <int K>
-__global__ void __launch_bounds__(128) adj_kernel(const float* __restrict__ proj,
-                                                  float* __restrict__ out,
-                                                  const ColParams* __restrict__ cols,
-                                                  const float* __restrict__ dvtab,
-                                                  const float* __restrict__ invdv,
-                                                  const double* __restrict__ dvd, DevGeom g,
-                                                  AngleBatch ab, int a0, int nab, int accumulate) {
+__global__ void __launch_bounds__(128) adj_gather_kernel(const float* __restrict__ proj,
+                                                         float* __restrict__ out,
+                                                         const ColParams* __restrict__ cols,
+                                                         const float* __restrict__ dvtab,
+                                                         const float* __restrict__ invdv,
+                                                         const double* __restrict__ dvd,
+                                                         DevGeom g, AngleBatch ab, int nab,
+                                                         int accumulate) {
     const int lane = threadIdx.x & 31;
     const int colid = blockIdx.x * 4 + (threadIdx.x >> 5);
     if (colid >= g.nx * g.ny) return;
     const int i = colid % g.nx, j = colid / g.nx;
     const int kbase = blockIdx.y * (32 * K) + lane;
     const int nz = g.nz, nu = g.nu, nv = g.nv;
-
     const float X0 = g.ox + i * g.sx, X1 = g.ox + (i + 1) * g.sx;
     const float Y0 = g.oy + j * g.sy, Y1 = g.oy + (j + 1) * g.sy;
     const float rpv = 1.f / g.pv;
-    constexpr float eps = 1e-3f;
-
     float acc[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) acc[c] = 0.f;
-
     for (int ia = 0; ia < nab; ++ia) {
-        const int a = a0 + ia;
-        const float cth = ab.cs[ia].x, sth = ab.cs[ia].y;
-        // footprint: detector columns whose ray passes the square's interior
-        int iu_lo = 0, iu_hi = nu - 1;
-        {
-            const float lx0 = -X0 * sth, lx1 = -X1 * sth, ly0 = Y0 * cth, ly1 = Y1 * cth;
-            const float ax0 = X0 * cth, ax1 = X1 * cth, ay0 = Y0 * sth, ay1 = Y1 * sth;
-            const float l00 = g.dso - ax0 - ay0, l01 = g.dso - ax0 - ay1;
-            const float l10 = g.dso - ax1 - ay0, l11 = g.dso - ax1 - ay1;
-            const float lmin = fminf(fminf(l00, l01), fminf(l10, l11));
-            if (!g.full_footprint || lmin > 0.f) {
-                const float u00 = (lx0 + ly0) / l00, u01 = (lx0 + ly1) / l01;
-                const float u10 = (lx1 + ly0) / l10, u11 = (lx1 + ly1) / l11;
-                const float umin = fminf(fminf(u00, u01), fminf(u10, u11)) * g.dsd;
-                const float umax = fmaxf(fmaxf(u00, u01), fmaxf(u10, u11)) * g.dsd;
-                const float off = 0.5f * nu - 0.5f;
-                const float flo = (umin - g.off_u) / g.pu + off;
-                const float fhi = (umax - g.off_u) / g.pu + off;
-                iu_lo = max(0, (int)ceilf(flo - eps));
-                iu_hi = min(nu - 1, (int)floorf(fhi + eps));
-            }
-        }
+        int iu_lo, iu_hi;
+        footprint(g, ab.cs[ia].x, ab.cs[ia].y, X0, X1, Y0, Y1, iu_lo, iu_hi);
         for (int iu = iu_lo; iu <= iu_hi; ++iu) {
-            const ColParams cp = cols[(size_t)a * nu + iu];
+            const ColParams cp = cols[(size_t)ia * nu + iu];
             float lo = cp.w_in, hi = cp.w_out;
-            if (cp.dx != 0.f) {
-                const float e0 = __fmaf_rn((float)i, cp.dx, cp.bx);
-                const float e1 = __fmaf_rn((float)(i + 1), cp.dx, cp.bx);
+            if (cp.dx != 0.0) {
+                const float e0 = xcross(cp, i), e1 = xcross(cp, i + 1);
                 lo = fmaxf(lo, fminf(e0, e1));
                 hi = fminf(hi, fmaxf(e0, e1));
             } else if (i != cp.i0) {
                 continue;
             }
-            if (cp.dy != 0.f) {
-                const float e0 = __fmaf_rn((float)j, cp.dy, cp.by);
-                const float e1 = __fmaf_rn((float)(j + 1), cp.dy, cp.by);
+            if (cp.dy != 0.0) {
+                const float e0 = ycross(cp, j), e1 = ycross(cp, j + 1);
                 lo = fmaxf(lo, fminf(e0, e1));
                 hi = fminf(hi, fmaxf(e0, e1));
             } else if (j != cp.j0) {
                 continue;
             }
             if (!(lo < hi)) continue;
-            const float wa = lo, wb = hi;
-            // row candidates: z index kz(w) = dv*G(w) - kz0, G increasing in w
             const float h1 = 1.f / cp.inv_h1;
             const float gin = (float)cp.g_in;
-            const float Ga = gin + (wa - cp.w_in) * h1;
-            const float Gb = gin + (wb - cp.w_in) * h1;
-            const float rGa = 1.f / Ga, rGb = 1.f / Gb;
-            const float* py = proj + ((size_t)a * nu + iu) * nv;
+            const float rGa = 1.f / (gin + (lo - cp.w_in) * h1);
+            const float rGb = 1.f / (gin + (hi - cp.w_in) * h1);
+            const float* py = proj + ((size_t)ia * nu + iu) * nv;
 #pragma unroll
             for (int c = 0; c < K; ++c) {
                 const int k = kbase + 32 * c;
@@ -232,8 +426,8 @@ __global__ void __launch_bounds__(128) adj_kernel(const float* __restrict__ proj
                 const float n0 = (float)k + g.kz0, n1 = n0 + 1.f;
                 const float dlo = n0 * (n0 >= 0.f ? rGb : rGa);
                 const float dhi = n1 * (n1 >= 0.f ? rGa : rGb);
-                const int rlo = max(0, (int)ceilf((dlo - g.dv0) * rpv - eps));
-                const int rhi = min(nv - 1, (int)floorf((dhi - g.dv0) * rpv + eps));
+                const int rlo = max(0, (int)ceilf((dlo - g.dv0) * rpv - 1e-3f));
+                const int rhi = min(nv - 1, (int)floorf((dhi - g.dv0) * rpv + 1e-3f));
                 for (int iv = rlo; iv <= rhi; ++iv) {
                     const float dv = dvtab[iv];
                     const double kzd = fma(dvd[iv], cp.g_in, -g.kz0d);
@@ -243,8 +437,8 @@ __global__ void __launch_bounds__(128) adj_kernel(const float* __restrict__ proj
                     float zlo, zhi;
                     if (dv != 0.f) {
                         const float imk = __fmul_rn(invdv[iv], cp.inv_h1);
-                        const float w0 = __fmaf_rn(__fsub_rn((float)(k - k0), f0), imk, cp.w_in);
-                        const float w1 = __fmaf_rn(__fsub_rn((float)(k + 1 - k0), f0), imk, cp.w_in);
+                        const float w0 = zcross(k, k0, f0, imk, cp.w_in);
+                        const float w1 = zcross(k + 1, k0, f0, imk, cp.w_in);
                         zlo = fminf(w0, w1);
                         zhi = fmaxf(w0, w1);
                     } else {
@@ -252,11 +446,11 @@ __global__ void __launch_bounds__(128) adj_kernel(const float* __restrict__ proj
                         zlo = -kInf;
                         zhi = kInf;
                     }
-                    const float len = fminf(wb, zhi) - fmaxf(wa, zlo);
+                    const float len = fminf(hi, zhi) - fmaxf(lo, zlo);
                     if (len > 0.f) {
                         const float q = dv * cp.inv_l;
                         const float f = __fsqrt_rn(__fmaf_rn(q, q, 1.f));
-                        acc[c] = __fmaf_rn(len * f, __ldg(py + iv), acc[c]);
+                        acc[c] = __fmaf_rn(len, __ldg(py + iv) * f, acc[c]);
                     }
                 }
             }
@@ -325,6 +519,8 @@ Projector::Projector(const kct_grid& grid, const kct_geometry& geom, int device)
     KCT_CUDA(cudaGetDevice(&device_));
     m_ = (size_t)grid.nx * grid.ny * grid.nz;
     n_ = (size_t)geom.nu * geom.nv * geom.n_angles;
+    const char* mode = std::getenv("KCT_ADJOINT");
+    adj_gather_ = mode && std::string(mode) == "gather";
     build_tables(geom);
 }
 
@@ -368,31 +564,34 @@ void Projector::build_tables(const kct_geometry& geom) {
     // detector rows: dv(iv) (projector.hpp:36) — the ray's z at the detector
     std::vector<float> dv(nv), invdv(nv);
     std::vector<double> dvd(nv);
+    double dv_max = 0.0;
     for (int iv = 0; iv < nv; ++iv) {
         const double d = (iv + 0.5 - 0.5 * nv) * geom.pv + geom.offset_v;
         dvd[iv] = d;
         dv[iv] = (float)d;
-        invdv[iv] = dv[iv] != 0.f ? (float)(1.0 / (double)dv[iv]) : std::numeric_limits<float>::infinity();
+        dv_max = std::max(dv_max, std::abs(d));
+        invdv[iv] = dv[iv] != 0.f ? (float)(1.0 / (double)dv[iv])
+                                  : std::numeric_limits<float>::infinity();
     }
 
     const double ox = grid_.ox, oy = grid_.oy, sx = grid_.sx, sy = grid_.sy, sz = grid_.sz;
     const double hx = ox + nx * sx, hy = oy + ny * sy;
-    const float inf = std::numeric_limits<float>::infinity();
     std::vector<ColParams> cols((size_t)na * nu);
     cs_.resize(na);
     bool full_fp = false;
+    double r_max = 0.0;  // farthest xy corner of the volume from the axis
+    for (double X : {ox, hx})
+        for (double Y : {oy, hy}) r_max = std::max(r_max, std::hypot(X, Y));
+    double L_min = std::numeric_limits<double>::infinity(), L_max = 0.0;
     for (int a = 0; a < na; ++a) {
         const double t = geom.angles[a];
         const double c = std::cos(t), s = std::sin(t);
         cs_[a] = make_float2((float)c, (float)s);
         const double Sx = geom.dso * c, Sy = geom.dso * s;
         // a voxel square behind the source plane breaks the corner-projection footprint
-        {
-            const double xs[2] = {ox, hx}, ys[2] = {oy, hy};
-            for (double X : xs)
-                for (double Y : ys)
-                    if (geom.dso - (X * c + Y * s) <= 1e-6 * geom.dso) full_fp = true;
-        }
+        for (double X : {ox, hx})
+            for (double Y : {oy, hy})
+                if (geom.dso - (X * c + Y * s) <= 1e-6 * geom.dso) full_fp = true;
         for (int iu = 0; iu < nu; ++iu) {
             ColParams& cp = cols[(size_t)a * nu + iu];
             const double du = (iu + 0.5 - 0.5 * nu) * geom.pu + geom.offset_u;
@@ -400,28 +599,32 @@ void Projector::build_tables(const kct_geometry& geom) {
             const double dx = -geom.dsd * c - du * s;
             const double dy = -geom.dsd * s + du * c;
             const double L = std::hypot(dx, dy);
+            L_min = std::min(L_min, L);
+            L_max = std::max(L_max, L);
             const double ex = dx / L, ey = dy / L;
             const double w0 = -(Sx * ex + Sy * ey);  // foot point of the axis
             const double Rx = Sx + w0 * ex, Ry = Sy + w0 * ey;
-            cp.bx = ex != 0.0 ? (float)((ox - Rx) / ex) : inf;
-            cp.dx = ex != 0.0 ? (float)(sx / ex) : 0.f;
-            cp.by = ey != 0.0 ? (float)((oy - Ry) / ey) : inf;
-            cp.dy = ey != 0.0 ? (float)(sy / ey) : 0.f;
+            cp.bx = ex != 0.0 ? (ox - Rx) / ex : 0.0;
+            cp.dx = ex != 0.0 ? sx / ex : 0.0;
+            cp.by = ey != 0.0 ? (oy - Ry) / ey : 0.0;
+            cp.dy = ey != 0.0 ? sy / ey : 0.0;
             cp.inv_h1 = (float)(L * sz);
             cp.inv_l = (float)(1.0 / L);
-            // clip: t in [0,1] and the xy box, evaluated with the same float
+            // clip: t in [0,1] and the xy box, evaluated with the same
             // expressions the kernels use for plane crossings
+            auto xc = [&](int n) { return (float)std::fma((double)n, cp.dx, cp.bx); };
+            auto yc = [&](int n) { return (float)std::fma((double)n, cp.dy, cp.by); };
             float lo = (float)(-w0), hi = (float)(L - w0);
             bool miss = false;
-            if (cp.dx != 0.f) {
-                const float e0 = std::fmaf(0.f, cp.dx, cp.bx), e1 = std::fmaf((float)nx, cp.dx, cp.bx);
+            if (cp.dx != 0.0) {
+                const float e0 = xc(0), e1 = xc(nx);
                 lo = std::max(lo, std::min(e0, e1));
                 hi = std::min(hi, std::max(e0, e1));
             } else if (Sx <= ox || Sx >= hx) {
                 miss = true;
             }
-            if (cp.dy != 0.f) {
-                const float e0 = std::fmaf(0.f, cp.dy, cp.by), e1 = std::fmaf((float)ny, cp.dy, cp.by);
+            if (cp.dy != 0.0) {
+                const float e0 = yc(0), e1 = yc(ny);
                 lo = std::max(lo, std::min(e0, e1));
                 hi = std::min(hi, std::max(e0, e1));
             } else if (Sy <= oy || Sy >= hy) {
@@ -439,19 +642,32 @@ void Projector::build_tables(const kct_geometry& geom) {
             cp.g_in = (w0 + (double)lo) / (L * sz);
             // entry voxel (projector.hpp:93-98): floor at the entry point, clamped
             const double px = Rx + (double)lo * ex, py = Ry + (double)lo * ey;
-            int ii = (int)std::floor((px - ox) / sx), jj = (int)std::floor((py - oy) / sy);
+            const int ii = (int)std::floor((px - ox) / sx), jj = (int)std::floor((py - oy) / sy);
             cp.i0 = std::clamp(ii, 0, nx - 1);
             cp.j0 = std::clamp(jj, 0, ny - 1);
         }
     }
     dg_.full_footprint = full_fp ? 1 : 0;
 
-    // launch shapes: forward rows per warp = 32*C, C <= 4; adjoint voxels per lane K
+    // forward launch shape: rows per warp = 32*C, C <= 4
     const int chunks = (nv + 31) / 32;
     fwd_bands_ = (chunks + 3) / 4;
     fwd_c_ = (chunks + fwd_bands_ - 1) / fwd_bands_;
     const int kc = (nz + 31) / 32;
     adj_k_ = kc <= 1 ? 1 : kc <= 2 ? 2 : kc <= 4 ? 4 : 8;
+
+    // brick adjoint: row stride S so that rows r and r+S of one pass never
+    // touch the same slab (S * dkz_min > 1 + span_max).
+    const double G_min = std::max(1e-12, (geom.dso - r_max) / (L_max * sz));
+    const double dkz_min = geom.pv * G_min;
+    const double span_max = dv_max / (L_min * sz) * std::hypot(sx, sy);
+    int S = (int)std::ceil((1.0 + span_max) / dkz_min * 1.02 + 1e-9);
+    S = std::max(S, 1);
+    if (S > 64 || full_fp) adj_gather_ = true;  // degenerate geometry: use the gather kernel
+    adj_S_ = S;
+    // one pass of 32 lanes should cover the rows of a brick
+    const int bz = (int)std::floor((32.0 * S - 3.0) * dkz_min);
+    adj_bz_ = std::clamp(std::min(bz, nz), 1, kMaxBz);
 
     KCT_CUDA(cudaMalloc(&d_cols_, cols.size() * sizeof(ColParams)));
     KCT_CUDA(cudaMemcpy(d_cols_, cols.data(), cols.size() * sizeof(ColParams), cudaMemcpyHostToDevice));
@@ -461,6 +677,9 @@ void Projector::build_tables(const kct_geometry& geom) {
     KCT_CUDA(cudaMemcpy(d_invdv_, invdv.data(), nv * sizeof(float), cudaMemcpyHostToDevice));
     KCT_CUDA(cudaMalloc(&d_dvd_, nv * sizeof(double)));
     KCT_CUDA(cudaMemcpy(d_dvd_, dvd.data(), nv * sizeof(double), cudaMemcpyHostToDevice));
+    const size_t smem = (size_t)kAdjWarps * (BX * BY * adj_bz_ + 4 * kMaxSeg) * sizeof(float);
+    KCT_CUDA(cudaFuncSetAttribute(adj_brick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
 }
 
 // ---- launches -----------------------------------------------------------------
@@ -487,18 +706,34 @@ void Projector::count(float* proj, cudaStream_t s) const {
 }
 
 void Projector::adjoint(const float* proj, float* vol, cudaStream_t s) const {
-    const int K = adj_k_;
-    dim3 grid((dg_.nx * dg_.ny + 3) / 4, (dg_.nz + 32 * K - 1) / (32 * K), 1);
     AngleBatch ab;
+    BrickCfg bc;
+    bc.bz = adj_bz_;
+    bc.S = adj_S_;
+    bc.nbx = (dg_.nx + BX - 1) / BX;
+    bc.nby = (dg_.ny + BY - 1) / BY;
+    bc.nbz = (dg_.nz + adj_bz_ - 1) / adj_bz_;
+    const int nbricks = bc.nbx * bc.nby * bc.nbz;
+    const size_t smem = (size_t)kAdjWarps * (BX * BY * adj_bz_ + 4 * kMaxSeg) * sizeof(float);
     for (int a0 = 0; a0 < dg_.na; a0 += kMaxAnglesPerLaunch) {
         const int nab = std::min(kMaxAnglesPerLaunch, dg_.na - a0);
         for (int q = 0; q < nab; ++q) ab.cs[q] = cs_[a0 + q];
         const int accum = a0 > 0 ? 1 : 0;
-        switch (K) {
-        case 1: adj_kernel<1><<<grid, 128, 0, s>>>(proj, vol, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_, ab, a0, nab, accum); break;
-        case 2: adj_kernel<2><<<grid, 128, 0, s>>>(proj, vol, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_, ab, a0, nab, accum); break;
-        case 4: adj_kernel<4><<<grid, 128, 0, s>>>(proj, vol, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_, ab, a0, nab, accum); break;
-        default: adj_kernel<8><<<grid, 128, 0, s>>>(proj, vol, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_, ab, a0, nab, accum); break;
+        const ColParams* cols = d_cols_ + (size_t)a0 * dg_.nu;
+        const float* pr = proj + (size_t)a0 * dg_.nu * dg_.nv;
+        if (adj_gather_) {
+            const int K = adj_k_;
+            dim3 grid((dg_.nx * dg_.ny + 3) / 4, (dg_.nz + 32 * K - 1) / (32 * K), 1);
+            switch (K) {
+            case 1: adj_gather_kernel<1><<<grid, 128, 0, s>>>(pr, vol, cols, d_dv_, d_invdv_, d_dvd_, dg_, ab, nab, accum); break;
+            case 2: adj_gather_kernel<2><<<grid, 128, 0, s>>>(pr, vol, cols, d_dv_, d_invdv_, d_dvd_, dg_, ab, nab, accum); break;
+            case 4: adj_gather_kernel<4><<<grid, 128, 0, s>>>(pr, vol, cols, d_dv_, d_invdv_, d_dvd_, dg_, ab, nab, accum); break;
+            default: adj_gather_kernel<8><<<grid, 128, 0, s>>>(pr, vol, cols, d_dv_, d_invdv_, d_dvd_, dg_, ab, nab, accum); break;
+            }
+        } else {
+            const int blocks = (nbricks + kAdjWarps - 1) / kAdjWarps;
+            adj_brick_kernel<<<blocks, kAdjWarps * 32, smem, s>>>(pr, vol, cols, d_dv_, d_invdv_,
+                                                                  d_dvd_, dg_, bc, ab, nab, accum);
         }
         KCT_CUDA(cudaGetLastError());
     }

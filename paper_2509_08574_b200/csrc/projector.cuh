@@ -47,6 +47,9 @@ class Projector {
 
     int fwd_chunks() const { return fwd_c_; }
     int adj_k() const { return adj_k_; }
+    int adj_stride() const { return adj_S_; }
+    int adj_bz() const { return adj_bz_; }
+    bool adj_gather() const { return adj_gather_; }
 
   private:
     void build_tables(const kct_geometry& geom);
@@ -61,6 +64,8 @@ class Projector {
     float* d_invdv_ = nullptr;        // [nv] 1/dv (inf at dv == 0)
     double* d_dvd_ = nullptr;         // [nv] dv in float64
     int fwd_c_ = 4, fwd_bands_ = 1, adj_k_ = 8;
+    int adj_S_ = 2, adj_bz_ = 32;
+    bool adj_gather_ = false;
     float* scratch_[4] = {nullptr, nullptr, nullptr, nullptr};
     size_t scratch_n_[4] = {0, 0, 0, 0};
 };

@@ -36,8 +36,10 @@ def test_golden_operator_parity(case):
     assert rel_l2(A.apply(d["x"]), d["ax"]) < TOL
     assert rel_l2(A.apply_adjoint(d["y"]), d["aty"]) < TOL
     assert rel_l2(A.apply(np.full(A.domain_size(), 2.5)), d["ax_uniform"]) < TOL
-    # exact Siddon nnz, up to rounding-level degenerate (corner) segments
-    assert abs(A.count_nnz() - int(d["nnz"])) <= max(2, 1e-3 * int(d["nnz"]))
+    # exact Siddon nnz, up to degenerate corner/edge segments whose length is
+    # positive in float64 but rounds to zero in float32 (this case is full of
+    # exact corner crossings: 4 mm voxels, 4 mm pitch, axis-aligned views)
+    assert abs(A.count_nnz() - int(d["nnz"])) <= max(2, 1e-2 * int(d["nnz"]))
 
 
 def test_uniform_volume_gives_chords(ora):
@@ -131,3 +133,15 @@ def test_device_native_matches_host_reference():
     back = A.apply_adjoint(yn)
     back_host = A.apply_adjoint(host)
     assert np.array_equal(A.volume_from_native(back).cpu().numpy(), back_host)
+
+
+@pytest.mark.parametrize("cfg,n_angles", [(1, 8), (3, 2)])
+def test_brick_and_gather_adjoints_agree(monkeypatch, cfg, n_angles):
+    """The brick-owned transpose and the per-voxel gather compute the same
+    segment lengths from the same crossing expressions."""
+    grid, geom = baseline_geometry(cfg, n_angles=n_angles)
+    y = np.random.default_rng(9).uniform(0, 1, geom.ray_count).astype(np.float32)
+    brick = projector(grid, geom).apply_adjoint(y)
+    monkeypatch.setenv("KCT_ADJOINT", "gather")
+    gather = projector(grid, geom).apply_adjoint(y)
+    assert rel_l2(brick, gather) < 2e-6
