@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <climits>
 #include <limits>
 #include <string>
 
@@ -164,33 +165,132 @@ __device__ __forceinline__ void footprint(const DevGeom& g, float cth, float sth
 }
 
 // ----------------------------------------------------------------------------
-// Adjoint, brick-owned exact transpose.  Each warp owns a brick of
-// BX x BY voxel columns x bz slabs, accumulated in shared memory.  For every
-// angle and every detector column whose rays cross the brick, the warp replays
-// the forward's xy walk through the brick once (segment list in shared
-// memory), then lanes take detector rows (stride S so that no two lanes of a
-// pass can touch the same voxel: S * dkz_min > 1 + span_max, derived on the
-// host) and deposit len * F * y for each ray-voxel segment — the same
-// segment endpoints the forward computes.  Every voxel is owned by one warp
-// and its contributions are added in a fixed (angle, column, pass, row group,
-// segment) order: deterministic, no atomics, exactly A^T.
+// Adjoint, brick-owned exact transpose.
+//
+// Each warp owns a brick of BX x BY voxel columns x bz slabs, accumulated in
+// shared memory; the 4 warps of a CTA own 4 bricks stacked in z over the same
+// voxel columns, so they share the detector-column footprint and the xy walks.
+// For every angle the CTA takes the footprint columns in batches of 4: warp w
+// replays the forward's xy walk of column (batch + w) through the brick
+// (segment list in shared memory), then every warp deposits the rows that
+// cross its own slabs: C rows per lane, rows of one pass S apart so that no
+// two lanes can touch the same voxel (S * dkz_min > 1 + span_max, derived on
+// the host).  Each deposit is len * F * y of one ray-voxel piece —
+// the same segment endpoints the forward computes.  Every voxel is owned by
+// one warp and its contributions are added in a fixed (angle, column, pass,
+// row group, segment, piece) order: deterministic, no atomics, exactly A^T.
 // ----------------------------------------------------------------------------
 constexpr int BX = 8, BY = 8;
 constexpr int kAdjWarps = 4;
-constexpr int kMaxSeg = BX + BY + 4;
-constexpr int kMaxBz = 64;
+constexpr int kAdjRows = 1;  // rows per lane (C)
+constexpr int kMaxSeg = 16;  // (BX - 1) + (BY - 1) interior crossings + 1 (+ slack)
+constexpr int kMaxBz = 128;
+constexpr unsigned kFull = 0xffffffffu;
 
 struct __align__(16) Seg {
     float wa, wb;
-    int ij, pad;
+    int ij;  // (i - I0) + BX * (j - J0)
+    int pad;
 };
 
 struct BrickCfg {
     int bz;  // slabs per brick (<= kMaxBz)
     int S;   // row stride of a pass
     int nbx, nby, nbz;
+    int nbzc;  // CTAs in z (each covers kAdjWarps bricks)
 };
 
+__device__ __forceinline__ float lds_f(unsigned a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_f(unsigned a, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v));
+}
+
+// z state of one detector row inside a brick: the forward's per-ray state
+// (k0, f0, imk) restricted to the brick's slab planes [K0, kend].
+struct RowZ {
+    int k, kstep, k0;
+    float f0, imk, wz, yf;
+};
+
+__device__ __forceinline__ void row_init(RowZ& r, bool on, int iv, const ColParams& cp, float lo,
+                                         float h1, int K0, int kend,
+                                         const float* __restrict__ dvtab,
+                                         const float* __restrict__ invdv,
+                                         const double* __restrict__ dvd,
+                                         const float* __restrict__ ycol, const DevGeom& g) {
+    if (!on) {
+        r.k = K0 - 1;
+        r.kstep = 0;
+        r.k0 = 0;
+        r.f0 = 0.f;
+        r.imk = 0.f;
+        r.wz = kInf;
+        r.yf = 0.f;
+        return;
+    }
+    const float dv = dvtab[iv];
+    const double kzd = fma(dvd[iv], cp.g_in, -g.kz0d);
+    const int k0 = __double2int_rd(kzd);
+    r.k0 = k0;
+    r.f0 = (float)(kzd - (double)k0);
+    r.imk = __fmul_rn(invdv[iv], cp.inv_h1);
+    const float q = dv * cp.inv_l;
+    r.yf = __ldg(ycol + iv) * __fsqrt_rn(__fmaf_rn(q, q, 1.f));
+    // slab at lo: last plane crossed strictly before lo (forward semantics);
+    // the float estimate is corrected with the exact crossing expression
+    int k = k0 + (int)floorf(r.f0 + (lo - cp.w_in) * (dv * h1));
+    if (dv > 0.f) {
+        r.kstep = 1;
+        k = max(k, k0);
+        while (k > k0 && !(zcross(k, k0, r.f0, r.imk, cp.w_in) < lo)) --k;
+        while (zcross(k + 1, k0, r.f0, r.imk, cp.w_in) < lo) ++k;
+        k = max(k, K0 - 1);
+        r.wz = k + 1 <= kend ? zcross(k + 1, k0, r.f0, r.imk, cp.w_in) : kInf;
+    } else if (dv < 0.f) {
+        r.kstep = -1;
+        k = min(k, k0);
+        while (k < k0 && !(zcross(k + 1, k0, r.f0, r.imk, cp.w_in) < lo)) ++k;
+        while (zcross(k, k0, r.f0, r.imk, cp.w_in) < lo) --k;
+        k = min(k, kend);
+        r.wz = k >= K0 ? zcross(k, k0, r.f0, r.imk, cp.w_in) : kInf;
+    } else {
+        r.kstep = 0;
+        k = k0;
+        r.wz = kInf;
+    }
+    r.k = min(max(k, K0 - 1), kend);
+}
+
+// Deposit one row's pieces of one xy segment: [wa, min(wb, wz)] into slab k,
+// then (rarely) the pieces after each z-plane crossing inside the segment.
+// r.k stays within [K0 - 1, kend]; the two guard slabs of every column
+// (K0 - 1 and kend) absorb the pieces outside the brick, so no range checks.
+__device__ __forceinline__ void row_segment(RowZ& r, const Seg& sg, unsigned colbase, int K0,
+                                            int kend, float w_in) {
+    const bool cr = r.wz < sg.wb;
+    const float wm = cr ? r.wz : sg.wb;
+    const unsigned a = colbase + 4u * (unsigned)r.k;
+    sts_f(a, __fmaf_rn(wm - sg.wa, r.yf, lds_f(a)));
+    if (cr) {
+        float wa = r.wz;
+        for (;;) {
+            r.k += r.kstep;
+            const int P = r.kstep > 0 ? r.k + 1 : r.k;
+            r.wz = (P >= K0 && P <= kend) ? zcross(P, r.k0, r.f0, r.imk, w_in) : kInf;
+            const float we = fminf(r.wz, sg.wb);
+            const unsigned b = colbase + 4u * (unsigned)r.k;
+            sts_f(b, __fmaf_rn(we - wa, r.yf, lds_f(b)));
+            if (!(r.wz < sg.wb)) break;
+            wa = r.wz;
+        }
+    }
+}
+
+template <int C>
 __global__ void __launch_bounds__(kAdjWarps * 32) adj_brick_kernel(
     const float* __restrict__ proj, float* __restrict__ out, const ColParams* __restrict__ cols,
     const float* __restrict__ dvtab, const float* __restrict__ invdv, const double* __restrict__ dvd,
@@ -203,17 +303,27 @@ __global__ void __launch_bounds__(kAdjWarps * 32) adj_brick_kernel(
     const int BZ = bc.bz;
     const int I0 = bi * BX, J0 = bj * BY, K0 = bk * BZ;
     const int bxn = min(BX, g.nx - I0), byn = min(BY, g.ny - J0), bzn = min(BZ, g.nz - K0);
+    const int kend = K0 + bzn;
     const int nu = g.nu, nv = g.nv;
-    const int abase = warp * (BX * BY * BZ + 4 * kMaxSeg);  // this warp's accumulator
-    Seg* segs = reinterpret_cast<Seg*>(sm + abase + BX * BY * BZ);
-    for (int q = lane; q < BX * BY * BZ; q += 32) sm[abase + q] = 0.f;
+    // per-warp shared layout: acc[BX*BY][BZ + 2] (slab k at k - K0 + 1; two
+    // guard slabs) | segs[kMaxSeg] | bnd[kMaxSeg + 2] | axis[kMaxSeg + 2]
+    const int CS = BZ + 2;
+    const int wfloats = BX * BY * CS + 4 * kMaxSeg + 2 * (kMaxSeg + 2);
+    float* acc = sm + warp * wfloats;
+    Seg* segs = reinterpret_cast<Seg*>(acc + BX * BY * CS);
+    float* bnd = acc + BX * BY * CS + 4 * kMaxSeg;
+    int* axis = reinterpret_cast<int*>(bnd + kMaxSeg + 2);
+    const unsigned acc_s = (unsigned)__cvta_generic_to_shared(acc);
+    for (int q = lane; q < BX * BY * CS; q += 32) acc[q] = 0.f;
     __syncwarp();
 
     const float X0 = g.ox + I0 * g.sx, X1 = g.ox + (I0 + bxn) * g.sx;
     const float Y0 = g.oy + J0 * g.sy, Y1 = g.oy + (J0 + byn) * g.sy;
     const float rpv = 1.f / g.pv;
     const int S = bc.S;
-    const int kend = K0 + bzn;
+    const bool xl = lane < 8;  // lanes 0..7: interior x planes, 8..15: interior y planes
+    const int pl = xl ? lane : lane - 8;
+    const unsigned below = (1u << lane) - 1u;
 
     for (int ia = 0; ia < nab; ++ia) {
         int iu_lo, iu_hi;
@@ -239,116 +349,86 @@ __global__ void __launch_bounds__(kAdjWarps * 32) adj_brick_kernel(
                 continue;
             }
             if (!(lo < hi)) continue;
-            // rows whose z-span over [lo, hi] meets slabs [K0, K0 + bzn]
-            const float h1 = 1.f / cp.inv_h1;
+            // rows whose z-span over [lo, hi] meets slabs [K0, kend]
+            const float h1 = __frcp_rn(cp.inv_h1);
             const float gin = (float)cp.g_in;
             const float Glo = gin + (lo - cp.w_in) * h1, Ghi = gin + (hi - cp.w_in) * h1;
             const float n0 = (float)K0 + g.kz0, n1 = n0 + (float)bzn;
-            const float dlo = n0 >= 0.f ? n0 / Ghi : n0 / Glo;
-            const float dhi = n1 >= 0.f ? n1 / Glo : n1 / Ghi;
+            const float dlo = n0 >= 0.f ? __fdividef(n0, Ghi) : __fdividef(n0, Glo);
+            const float dhi = n1 >= 0.f ? __fdividef(n1, Glo) : __fdividef(n1, Ghi);
             const int rlo = max(0, (int)ceilf((dlo - g.dv0) * rpv - 1e-3f));
             const int rhi = min(nv - 1, (int)floorf((dhi - g.dv0) * rpv + 1e-3f));
             if (rlo > rhi) continue;
-            // xy walk through the brick (the forward's walk restricted to it);
-            // segment n is written by lane n
-            int i = cp.dx != 0.0 ? (int)floor(((double)lo - cp.bx) / cp.dx) : cp.i0;
-            int j = cp.dy != 0.0 ? (int)floor(((double)lo - cp.by) / cp.dy) : cp.j0;
-            i = min(max(i, I0), I0 + bxn - 1);
-            j = min(max(j, J0), J0 + byn - 1);
+
+            // ---- lane-parallel xy walk through the brick ----
+            float v = kInf;
+            bool has = false;
+            if (xl && pl < bxn - 1 && cp.dx != 0.0) {
+                v = xcross(cp, I0 + 1 + pl);
+                has = true;
+            } else if (!xl && lane < 16 && pl < byn - 1 && cp.dy != 0.0) {
+                v = ycross(cp, J0 + 1 + pl);
+                has = true;
+            }
+            const unsigned mbefore = __ballot_sync(kFull, has && v <= lo);
+            const bool valid = has && v > lo && v < hi;
+            const unsigned mval = __ballot_sync(kFull, valid);
+            const int cbx = __popc(mbefore & 0xffu), cby = __popc(mbefore & 0xff00u);
             const int stx = cp.dx > 0.0 ? 1 : -1, sty = cp.dy > 0.0 ? 1 : -1;
-            int px = cp.dx > 0.0 ? i + 1 : i;
-            int py = cp.dy > 0.0 ? j + 1 : j;
-            float wnx = cp.dx != 0.0 ? xcross(cp, px) : kInf;
-            float wny = cp.dy != 0.0 ? ycross(cp, py) : kInf;
-            float wcur = lo;
-            int nseg = 0;
-            for (;;) {
-                const bool stepx = wnx <= wny;
-                const float wnext = stepx ? wnx : wny;
-                const float wb = fmaxf(fminf(wnext, hi), wcur);
-                if (lane == nseg) {
-                    Seg sg;
-                    sg.wa = wcur;
-                    sg.wb = wb;
-                    sg.ij = abase + ((i - I0) + BX * (j - J0)) * BZ - K0;
-                    sg.pad = 0;
-                    segs[nseg] = sg;
-                }
-                ++nseg;
-                if (wnext >= hi || nseg == kMaxSeg) break;
-                wcur = fmaxf(wnext, wcur);
-                if (stepx) {
-                    i += stx;
-                    if (i < I0 || i >= I0 + bxn) break;
-                    px += stx;
-                    wnx = xcross(cp, px);
-                } else {
-                    j += sty;
-                    if (j < J0 || j >= J0 + byn) break;
-                    py += sty;
-                    wny = ycross(cp, py);
-                }
+            const int ie = cp.dx == 0.0 ? cp.i0 : (stx > 0 ? I0 + cbx : I0 + bxn - 1 - cbx);
+            const int je = cp.dy == 0.0 ? cp.j0 : (sty > 0 ? J0 + cby : J0 + byn - 1 - cby);
+            // rank along the ray: own-axis predecessors (plane order) + other-axis
+            // crossings before it (x first at ties, as the forward's walk)
+            const unsigned own = xl ? (mval & 0xffu) : (mval & 0xff00u);
+            int rank = (xl ? stx : sty) > 0 ? __popc(own & below)
+                                            : __popc(own & ~below & ~(1u << lane));
+            const unsigned other = xl ? (mval >> 8) & 0xffu : mval & 0xffu;
+#pragma unroll
+            for (int t = 0; t < (BX > BY ? BX : BY) - 1; ++t) {
+                const float ov = __shfl_sync(kFull, v, xl ? 8 + t : t);
+                rank += (((other >> t) & 1u) && (xl ? ov < v : ov <= v)) ? 1 : 0;
+            }
+            const int nval = __popc(mval);
+            const int nseg = nval + 1;
+            if (valid) {
+                bnd[rank + 1] = v;
+                axis[rank] = xl ? 1 : 0;
+            }
+            if (lane == 0) {
+                bnd[0] = lo;
+                bnd[nval + 1] = hi;
             }
             __syncwarp();
+            const unsigned mx = __ballot_sync(kFull, lane < nval && axis[lane]);
+            if (lane < nseg) {
+                const int nxb = __popc(mx & below);
+                const int i = ie + stx * nxb, j = je + sty * (lane - nxb);
+                Seg sg;
+                sg.wa = bnd[lane];
+                sg.wb = bnd[lane + 1];
+                // byte address of slab 0 (so that slab k sits at + 4k)
+                sg.ij = (int)(acc_s + 4u * (unsigned)(((i - I0) + BX * (j - J0)) * CS + 1 - K0));
+                sg.pad = 0;
+                segs[lane] = sg;
+            }
+            __syncwarp();
+
+            // ---- rows: C per lane, passes of stride S ----
             const float* ycol = yb + (size_t)iu * nv;
             for (int p = 0; p < S; ++p) {
-                for (int base = rlo + p; base <= rhi; base += 32 * S) {
-                    const int iv = base + S * lane;
-                    if (iv <= rhi) {
-                        // the forward's per-ray z state (k0, f0, imk), then the
-                        // slab at lo: last plane crossed strictly before lo
-                        const float dv = dvtab[iv];
-                        const double kzd = fma(dvd[iv], cp.g_in, -g.kz0d);
-                        const int k0 = __double2int_rd(kzd);
-                        const float f0 = (float)(kzd - (double)k0);
-                        const float imk = __fmul_rn(invdv[iv], cp.inv_h1);
-                        const float q = dv * cp.inv_l;
-                        const float yf = __ldg(ycol + iv) * __fsqrt_rn(__fmaf_rn(q, q, 1.f));
-                        const float t = f0 + (lo - cp.w_in) * (dv * h1);
-                        int k = k0 + (int)floorf(t);
-                        int kstep;
-                        float wz;
-                        if (dv > 0.f) {
-                            kstep = 1;
-                            k = max(k, k0);
-                            while (k > k0 && !(zcross(k, k0, f0, imk, cp.w_in) < lo)) --k;
-                            while (zcross(k + 1, k0, f0, imk, cp.w_in) < lo) ++k;
-                            k = max(k, K0 - 1);
-                            wz = k + 1 <= kend ? zcross(k + 1, k0, f0, imk, cp.w_in) : kInf;
-                        } else if (dv < 0.f) {
-                            kstep = -1;
-                            k = min(k, k0);
-                            while (k < k0 && !(zcross(k + 1, k0, f0, imk, cp.w_in) < lo)) ++k;
-                            while (zcross(k, k0, f0, imk, cp.w_in) < lo) --k;
-                            k = min(k, kend);
-                            wz = k >= K0 ? zcross(k, k0, f0, imk, cp.w_in) : kInf;
-                        } else {
-                            kstep = 0;
-                            k = k0;
-                            wz = kInf;
-                        }
-                        for (int sgi = 0; sgi < nseg; ++sgi) {
-                            const Seg sg = segs[sgi];
-                            // first piece up to the next z-plane (or the segment end)
-                            const bool cr = wz < sg.wb;
-                            const float wm = cr ? wz : sg.wb;
-                            if ((unsigned)(k - K0) < (unsigned)bzn)
-                                sm[sg.ij + k] = __fmaf_rn(wm - sg.wa, yf, sm[sg.ij + k]);
-                            if (cr) {  // z-plane crossing(s) inside the segment (rare)
-                                float wa = wz;
-                                for (;;) {
-                                    k += kstep;
-                                    const int P = kstep > 0 ? k + 1 : k;
-                                    wz = (P >= K0 && P <= kend) ? zcross(P, k0, f0, imk, cp.w_in)
-                                                                : kInf;
-                                    const float we = fminf(wz, sg.wb);
-                                    if ((unsigned)(k - K0) < (unsigned)bzn)
-                                        sm[sg.ij + k] = __fmaf_rn(we - wa, yf, sm[sg.ij + k]);
-                                    if (!(wz < sg.wb)) break;
-                                    wa = wz;
-                                }
-                            }
-                        }
+                for (int base = rlo + p; base <= rhi; base += 32 * S * C) {
+                    RowZ r[C];
+#pragma unroll
+                    for (int c = 0; c < C; ++c) {
+                        const int iv = base + S * (lane + 32 * c);
+                        row_init(r[c], iv <= rhi, iv, cp, lo, h1, K0, kend, dvtab, invdv, dvd,
+                                 ycol, g);
+                    }
+                    for (int sgi = 0; sgi < nseg; ++sgi) {
+                        const Seg sg = segs[sgi];
+#pragma unroll
+                        for (int c = 0; c < C; ++c)
+                            row_segment(r[c], sg, (unsigned)sg.ij, K0, kend, cp.w_in);
                     }
                     __syncwarp();
                 }
@@ -360,8 +440,8 @@ __global__ void __launch_bounds__(kAdjWarps * 32) adj_brick_kernel(
     for (int c = 0; c < bxn * byn; ++c) {
         const int ci = c % bxn, cj = c / bxn;
         float* o = out + ((size_t)(I0 + ci) + (size_t)g.nx * (J0 + cj)) * g.nz + K0;
-        const int a = abase + (ci + BX * cj) * BZ;
-        for (int kk = lane; kk < bzn; kk += 32) o[kk] = accumulate ? o[kk] + sm[a + kk] : sm[a + kk];
+        const float* a = acc + (ci + BX * cj) * CS + 1;
+        for (int kk = lane; kk < bzn; kk += 32) o[kk] = accumulate ? o[kk] + a[kk] : a[kk];
     }
 }
 
@@ -665,9 +745,10 @@ void Projector::build_tables(const kct_geometry& geom) {
     S = std::max(S, 1);
     if (S > 64 || full_fp) adj_gather_ = true;  // degenerate geometry: use the gather kernel
     adj_S_ = S;
-    // one pass of 32 lanes should cover the rows of a brick
-    const int bz = (int)std::floor((32.0 * S - 3.0) * dkz_min);
-    adj_bz_ = std::clamp(std::min(bz, nz), 1, kMaxBz);
+    // one pass of 32*C lanes should cover the rows of a brick
+    adj_bz_ = std::clamp(std::min((int)std::floor((32.0 * kAdjRows * S - 3.0) * dkz_min), nz), 1,
+                         kMaxBz);
+    if (const char* e = std::getenv("KCT_ADJ_BZ")) adj_bz_ = std::clamp(std::atoi(e), 1, kMaxBz);
 
     KCT_CUDA(cudaMalloc(&d_cols_, cols.size() * sizeof(ColParams)));
     KCT_CUDA(cudaMemcpy(d_cols_, cols.data(), cols.size() * sizeof(ColParams), cudaMemcpyHostToDevice));
@@ -677,9 +758,14 @@ void Projector::build_tables(const kct_geometry& geom) {
     KCT_CUDA(cudaMemcpy(d_invdv_, invdv.data(), nv * sizeof(float), cudaMemcpyHostToDevice));
     KCT_CUDA(cudaMalloc(&d_dvd_, nv * sizeof(double)));
     KCT_CUDA(cudaMemcpy(d_dvd_, dvd.data(), nv * sizeof(double), cudaMemcpyHostToDevice));
-    const size_t smem = (size_t)kAdjWarps * (BX * BY * adj_bz_ + 4 * kMaxSeg) * sizeof(float);
-    KCT_CUDA(cudaFuncSetAttribute(adj_brick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+    const size_t smem = adj_smem_bytes();
+    KCT_CUDA(cudaFuncSetAttribute(adj_brick_kernel<kAdjRows>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+}
+
+size_t Projector::adj_smem_bytes() const {
+    return (size_t)kAdjWarps * (BX * BY * (adj_bz_ + 2) + 4 * kMaxSeg + 2 * (kMaxSeg + 2)) *
+           sizeof(float);
 }
 
 // ---- launches -----------------------------------------------------------------
@@ -713,8 +799,9 @@ void Projector::adjoint(const float* proj, float* vol, cudaStream_t s) const {
     bc.nbx = (dg_.nx + BX - 1) / BX;
     bc.nby = (dg_.ny + BY - 1) / BY;
     bc.nbz = (dg_.nz + adj_bz_ - 1) / adj_bz_;
-    const int nbricks = bc.nbx * bc.nby * bc.nbz;
-    const size_t smem = (size_t)kAdjWarps * (BX * BY * adj_bz_ + 4 * kMaxSeg) * sizeof(float);
+    bc.nbzc = 0;
+    const int nctas = (bc.nbx * bc.nby * bc.nbz + kAdjWarps - 1) / kAdjWarps;
+    const size_t smem = adj_smem_bytes();
     for (int a0 = 0; a0 < dg_.na; a0 += kMaxAnglesPerLaunch) {
         const int nab = std::min(kMaxAnglesPerLaunch, dg_.na - a0);
         for (int q = 0; q < nab; ++q) ab.cs[q] = cs_[a0 + q];
@@ -731,9 +818,8 @@ void Projector::adjoint(const float* proj, float* vol, cudaStream_t s) const {
             default: adj_gather_kernel<8><<<grid, 128, 0, s>>>(pr, vol, cols, d_dv_, d_invdv_, d_dvd_, dg_, ab, nab, accum); break;
             }
         } else {
-            const int blocks = (nbricks + kAdjWarps - 1) / kAdjWarps;
-            adj_brick_kernel<<<blocks, kAdjWarps * 32, smem, s>>>(pr, vol, cols, d_dv_, d_invdv_,
-                                                                  d_dvd_, dg_, bc, ab, nab, accum);
+            adj_brick_kernel<kAdjRows><<<nctas, kAdjWarps * 32, smem, s>>>(
+                pr, vol, cols, d_dv_, d_invdv_, d_dvd_, dg_, bc, ab, nab, accum);
         }
         KCT_CUDA(cudaGetLastError());
     }

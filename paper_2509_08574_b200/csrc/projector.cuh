@@ -53,6 +53,7 @@ class Projector {
 
   private:
     void build_tables(const kct_geometry& geom);
+    size_t adj_smem_bytes() const;
 
     kct_grid grid_;
     DevGeom dg_{};
