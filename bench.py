@@ -244,7 +244,7 @@ def run_ours(args):
     bytes_f = 4.0 * nnz_f + 4.0 * Nf
     bytes_b = 4.0 * nnz_b + 4.0 * Mb
     if mean_b >= mean_f:
-        dom = ("adjoint (adj_kernel)", bytes_b, mean_b)
+        dom = ("adjoint (adj_brick_kernel)", bytes_b, mean_b)
     else:
         dom = ("forward (fwd_kernel)", bytes_f, mean_f)
     achieved = dom[1] / dom[2] / 1e9
@@ -253,7 +253,7 @@ def run_ours(args):
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get("adj_kernel" if "adj" in dom[0] else "fwd_kernel")
+                traffic = json.load(f).get("adj_brick_kernel" if "adj" in dom[0] else "fwd_kernel")
         except Exception:
             traffic = None
 
@@ -376,7 +376,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-angles", type=int, default=4)
+    ap.add_argument("--ref-angles", type=int, default=16)
     ap.add_argument("--recon-steps", type=int, default=3)
     ap.add_argument("--recon-warmup", type=int, default=1)
     ap.add_argument("--skip-recon", action="store_true")
