@@ -183,14 +183,12 @@ def run_ours(args):
     log(f"[bench] rank {rank}/{ws}: generating c3 phantoms")
     _, prior, follow = synth.study("c3")
 
-    # sharding: forward over angles r::ws, adjoint over z-slab r (all angles)
-    my_angles = np.arange(na)[rank::ws]
-    geom_f = k.ConeBeamGeometry(synth.DSO, synth.DSD, cfg.det, cfg.det, cfg.pitch, cfg.pitch,
-                                geom_all.angles[my_angles])
-    nz_loc = cfg.n // ws
-    z0 = rank * nz_loc
-    grid_b = k.GridSpec((cfg.n, cfg.n, nz_loc), (cfg.voxel,) * 3,
-                        (grid.origin[0], grid.origin[1], grid.origin[2] + z0 * cfg.voxel))
+    # sharding (paper_2509_08574_b200/shard.py): forward over angles r::ws,
+    # adjoint over z-slab r from all angles; no data-path collective
+    from paper_2509_08574_b200 import shard
+    my_angles = shard.angle_indices(na, ws, rank)
+    geom_f = shard.shard_geometry(geom_all, ws, rank)
+    grid_b = shard.slab_grid(grid, ws, rank)
     A_f = k.ConeBeamProjector(grid, geom_f, device=local)
     A_b = A_f if ws == 1 else k.ConeBeamProjector(grid_b, geom_all, device=local)
     nnz_f = A_f.count_nnz()

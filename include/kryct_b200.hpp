@@ -1,0 +1,200 @@
+// kryct_b200.hpp — C++ drop-in shim: the reference kryct API on the B200
+// library (libkct.so, C ABI in kct.h).
+//
+// Include this after the reference headers.  It provides, with the reference
+// signatures and error behaviour (ConfigError / SolverError):
+//   kryct_b200::GpuConeBeamProjector : kryct::LinearMap   (projector.hpp:264-291)
+//   kryct_b200::cgls_recon(proj, grid, iters, opts, tol)   (recon.hpp:312-315)
+//   kryct_b200::irn_tv / irn_piple / irn_piccs             (recon.hpp:252-270)
+// so existing callers switch by namespace, and the reference's own generic
+// solvers (kryct::cgls, kryct::StackedMap, ...) can drive the GPU operator.
+// Values cross the boundary as float32 (the reference reads float32 files,
+// io.hpp:48-49); the solvers reduce in float64 on the device.
+// ReconOptions::hook (a host callback per inner iteration) cannot be served
+// by a device-resident solver; set ground_truth for the error history instead
+// (a set hook raises ConfigError).
+#pragma once
+
+#include <kryct/linear_map.hpp>
+#include <kryct/recon.hpp>
+#include <kryct/types.hpp>
+
+#include <memory>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "kct.h"
+
+namespace kryct_b200 {
+
+namespace detail {
+
+inline void check(int rc) {
+    if (rc == KCT_OK) return;
+    const std::string msg = kct_last_error();
+    if (rc == KCT_ERR_CONFIG) throw kryct::ConfigError(msg);
+    if (rc == KCT_ERR_SOLVER) throw kryct::SolverError(msg);
+    throw std::runtime_error("kct: " + msg);
+}
+
+inline kct_grid to_grid(const kryct::GridSpec& g) {
+    return kct_grid{g.dims.nx,   g.dims.ny,   g.dims.nz,   g.spacing.x, g.spacing.y,
+                    g.spacing.z, g.origin.x, g.origin.y, g.origin.z};
+}
+
+inline kct_geometry to_geom(const kryct::ConeBeamGeometry& g) {
+    return kct_geometry{g.dso,      g.dsd,      g.detector.nu,
+                        g.detector.nv, g.detector.pu, g.detector.pv,
+                        g.offset_u, g.offset_v, static_cast<int>(g.angles.size()),
+                        g.angles.data()};
+}
+
+inline std::vector<float> to_f32(std::span<const double> v) {
+    return std::vector<float>(v.begin(), v.end());
+}
+
+struct Handle {
+    kct_projector* h = nullptr;
+    ~Handle() {
+        if (h) kct_projector_destroy(h);
+    }
+};
+
+}  // namespace detail
+
+/// ConeBeamProjector on one CUDA device (projector.hpp:264-291).
+class GpuConeBeamProjector final : public kryct::LinearMap {
+  public:
+    using kryct::LinearMap::apply;
+    using kryct::LinearMap::apply_adjoint;
+
+    GpuConeBeamProjector(kryct::GridSpec grid, kryct::ConeBeamGeometry geometry, int device = -1)
+        : grid_(grid), geom_(std::move(geometry)), h_(std::make_shared<detail::Handle>()) {
+        const kct_grid g = detail::to_grid(grid_);
+        const kct_geometry ge = detail::to_geom(geom_);
+        detail::check(kct_projector_create(&g, &ge, device, &h_->h));
+    }
+
+    std::size_t domain_size() const override { return grid_.dims.count(); }
+    std::size_t range_size() const override { return geom_.ray_count(); }
+    const kryct::GridSpec& grid() const { return grid_; }
+    const kryct::ConeBeamGeometry& geometry() const { return geom_; }
+    kct_projector* handle() const { return h_->h; }
+
+    void apply(std::span<const double> x, std::span<double> out) const override {
+        check_domain(x.size());
+        check_range(out.size());
+        detail::check(kct_forward_f64(h_->h, x.data(), out.data()));
+    }
+    void apply_adjoint(std::span<const double> y, std::span<double> out) const override {
+        check_range(y.size());
+        check_domain(out.size());
+        detail::check(kct_adjoint_f64(h_->h, y.data(), out.data()));
+    }
+
+  private:
+    kryct::GridSpec grid_;
+    kryct::ConeBeamGeometry geom_;
+    std::shared_ptr<detail::Handle> h_;
+};
+
+namespace detail {
+
+inline kryct::ReconReport run(int kind, const kryct::ProjectionSet& proj,
+                              const kryct::GridSpec& grid, const kryct::Volume* prior,
+                              const kryct::RegularizationParams* params, std::size_t iters,
+                              double tol, const kryct::ReconOptions& opts) {
+    if (opts.hook) throw kryct::ConfigError("kryct_b200: per-iteration hooks are not supported");
+    proj.validate();
+    grid.validate();
+    GpuConeBeamProjector A(grid, proj.geometry);
+    const std::size_t m = grid.dims.count();
+    auto b = to_f32(proj.data);
+    std::vector<float> pr, x0, gt, x(m);
+    if (prior) {
+        if (!(prior->dims == grid.dims))
+            throw kryct::ConfigError("prior volume does not match the reconstruction grid");
+        pr = to_f32(prior->data);
+    }
+    if (opts.initial) {
+        if (!(opts.initial->dims == grid.dims))
+            throw kryct::ConfigError("initial volume does not match the reconstruction grid");
+        x0 = to_f32(opts.initial->data);
+    }
+    if (opts.ground_truth) {
+        if (!(opts.ground_truth->dims == grid.dims))
+            throw kryct::ConfigError("ground truth does not match the reconstruction grid");
+        gt = to_f32(opts.ground_truth->data);
+    }
+    const std::size_t outer = params ? params->outer_iters : 1;
+    const std::size_t inner = params ? params->inner_iters : iters;
+    std::vector<double> obj(outer * inner + outer + 1), res(outer * inner), err(outer * inner),
+        secs(outer + 1);
+    std::vector<uint64_t> bnd(outer + 1);
+    kct_report rep{};
+    rep.objective_history = obj.data();
+    rep.residual_history = res.data();
+    rep.error_history = err.data();
+    rep.outer_boundaries = bnd.data();
+    rep.outer_seconds = secs.data();
+    const float* px0 = x0.empty() ? nullptr : x0.data();
+    const float* pgt = gt.empty() ? nullptr : gt.data();
+    if (params) {
+        const kct_reg_params p{params->alpha,       params->lambda,          params->tau,
+                               params->outer_iters, params->inner_iters,    params->inner_tolerance,
+                               params->warm_start ? 1 : 0};
+        check(kct_irn(A.handle(), kind, b.data(), pr.empty() ? nullptr : pr.data(), px0, pgt, &p,
+                      x.data(), &rep, KCT_MEM_HOST, KCT_LAYOUT_REFERENCE, nullptr));
+    } else {
+        check(kct_cgls_recon(A.handle(), b.data(), iters, px0, pgt, tol, x.data(), &rep,
+                             KCT_MEM_HOST, KCT_LAYOUT_REFERENCE, nullptr));
+    }
+    kryct::ReconReport r;
+    r.volume = kryct::Volume(grid);
+    r.volume.data.assign(x.begin(), x.end());
+    r.objective_history.assign(obj.begin(), obj.begin() + rep.objective_count);
+    r.residual_history.assign(res.begin(), res.begin() + rep.residual_count);
+    r.error_history.assign(err.begin(), err.begin() + rep.error_count);
+    for (std::size_t i = 0; i < rep.outer_count; ++i) {
+        r.outer_boundaries.push_back(bnd[i]);
+        r.outer_seconds.push_back(secs[i]);
+    }
+    r.solve_seconds = rep.solve_seconds;
+    r.converged = rep.converged != 0;
+    return r;
+}
+
+}  // namespace detail
+
+/// recon.hpp:312-315
+inline kryct::ReconReport cgls_recon(const kryct::ProjectionSet& proj, const kryct::GridSpec& grid,
+                                     std::size_t iters, const kryct::ReconOptions& opts = {},
+                                     double tolerance = 0.0) {
+    return detail::run(KCT_KIND_TV, proj, grid, nullptr, nullptr, iters, tolerance, opts);
+}
+
+/// recon.hpp:252-255
+inline kryct::ReconReport irn_tv(const kryct::ProjectionSet& proj, const kryct::GridSpec& grid,
+                                 const kryct::RegularizationParams& params,
+                                 const kryct::ReconOptions& opts = {}) {
+    return detail::run(KCT_KIND_TV, proj, grid, nullptr, &params, 0, 0.0, opts);
+}
+
+/// recon.hpp:260-263
+inline kryct::ReconReport irn_piple(const kryct::ProjectionSet& proj, const kryct::GridSpec& grid,
+                                    const kryct::Volume& prior,
+                                    const kryct::RegularizationParams& params,
+                                    const kryct::ReconOptions& opts = {}) {
+    return detail::run(KCT_KIND_PIPLE, proj, grid, &prior, &params, 0, 0.0, opts);
+}
+
+/// recon.hpp:267-270 — the north-star entry point.
+inline kryct::ReconReport irn_piccs(const kryct::ProjectionSet& proj, const kryct::GridSpec& grid,
+                                    const kryct::Volume& prior,
+                                    const kryct::RegularizationParams& params,
+                                    const kryct::ReconOptions& opts = {}) {
+    return detail::run(KCT_KIND_PICCS, proj, grid, &prior, &params, 0, 0.0, opts);
+}
+
+}  // namespace kryct_b200

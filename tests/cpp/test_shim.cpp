@@ -1,0 +1,99 @@
+// TEST INFRASTRUCTURE: the C++ drop-in shim (include/kryct_b200.hpp) against
+// the unmodified reference.  Compiled against /root/reference headers by
+// oracle/Makefile (target `shim`) into oracle/_ref/test_shim; run on a GPU box by
+// tests/test_shim_gpu.py.  Exit code 0 = all checks passed.
+#include <kryct/krylov.hpp>
+#include <kryct/projector.hpp>
+#include <kryct/recon.hpp>
+
+#include <cmath>
+#include <cstdio>
+#include <numbers>
+#include <random>
+
+#include "kryct_b200.hpp"
+
+using namespace kryct;
+
+static double rel(const std::vector<double>& a, const std::vector<double>& b) {
+    double num = 0, den = 0;
+    for (size_t i = 0; i < a.size(); ++i) {
+        num += (a[i] - b[i]) * (a[i] - b[i]);
+        den += b[i] * b[i];
+    }
+    return std::sqrt(num / (den > 0 ? den : 1));
+}
+
+static int fails = 0;
+static void expect(bool ok, const char* what, double v) {
+    std::printf("%-52s %s (%.3e)\n", what, ok ? "ok" : "FAIL", v);
+    if (!ok) ++fails;
+}
+
+int main() {
+    GridSpec grid = GridSpec::centered({32, 32, 24}, {2.0, 2.0, 2.0});
+    ConeBeamGeometry g;
+    g.dso = 1000.0;
+    g.dsd = 1500.0;
+    g.detector = {48, 40, 2.0, 2.0};
+    for (int i = 0; i < 24; ++i) g.angles.push_back(2.0 * std::numbers::pi * i / 24.0);
+    std::mt19937 rng(7);
+    std::uniform_real_distribution<float> u(0.f, 0.04f);
+    std::vector<double> x(grid.dims.count()), y(g.ray_count());
+    for (auto& v : x) v = u(rng);
+    for (auto& v : y) v = u(rng);
+
+    ConeBeamProjector ref(grid, g);
+    kryct_b200::GpuConeBeamProjector gpu(grid, g);
+    expect(rel(gpu.apply(x), ref.apply(x)) < 1e-4, "GpuConeBeamProjector::apply vs reference",
+           rel(gpu.apply(x), ref.apply(x)));
+    expect(rel(gpu.apply_adjoint(y), ref.apply_adjoint(y)) < 1e-4,
+           "GpuConeBeamProjector::apply_adjoint vs reference",
+           rel(gpu.apply_adjoint(y), ref.apply_adjoint(y)));
+
+    // the reference's own cgls driving the GPU operator
+    const auto b = ref.apply(x);
+    std::vector<double> bf(b.begin(), b.end());
+    for (auto& v : bf) v = static_cast<float>(v);
+    const std::vector<double> x0(grid.dims.count(), 0.0);
+    const auto r_ref = cgls(ref, bf, x0, {.max_iters = 10});
+    const auto r_gpu = cgls(gpu, bf, x0, {.max_iters = 10});
+    expect(rel(r_gpu.x, r_ref.x) < 1e-3, "kryct::cgls(GpuConeBeamProjector) vs reference",
+           rel(r_gpu.x, r_ref.x));
+
+    // solver entry points with the reference signatures
+    ProjectionSet proj(g);
+    proj.data = bf;
+    Volume prior(grid);
+    for (size_t i = 0; i < x.size(); ++i) prior.data[i] = static_cast<float>(0.9 * x[i]);
+    RegularizationParams p;
+    p.alpha = 0.5;
+    p.outer_iters = 2;
+    p.inner_iters = 4;
+    const auto a_ref = irn_piccs(proj, grid, prior, p);
+    const auto a_gpu = kryct_b200::irn_piccs(proj, grid, prior, p);
+    expect(rel(a_gpu.volume.data, a_ref.volume.data) < 1e-3, "kryct_b200::irn_piccs vs irn_piccs",
+           rel(a_gpu.volume.data, a_ref.volume.data));
+    expect(a_gpu.objective_history.size() == a_ref.objective_history.size() &&
+               rel(a_gpu.objective_history, a_ref.objective_history) < 1e-3,
+           "objective history", rel(a_gpu.objective_history, a_ref.objective_history));
+    expect(a_gpu.outer_boundaries == a_ref.outer_boundaries, "outer boundaries", 0.0);
+    const auto c_ref = cgls_recon(proj, grid, 8);
+    const auto c_gpu = kryct_b200::cgls_recon(proj, grid, 8);
+    expect(rel(c_gpu.volume.data, c_ref.volume.data) < 1e-3, "kryct_b200::cgls_recon vs cgls_recon",
+           rel(c_gpu.volume.data, c_ref.volume.data));
+
+    // error taxonomy (test_projector.cpp:113-120)
+    bool threw = false;
+    try {
+        ConeBeamGeometry tiny = g;
+        tiny.dso = 40.0;
+        tiny.dsd = 90.0;
+        kryct_b200::GpuConeBeamProjector bad(GridSpec::centered({32, 32, 32}, {10, 10, 10}), tiny);
+    } catch (const ConfigError&) {
+        threw = true;
+    }
+    expect(threw, "source inside the volume -> ConfigError", 0.0);
+    std::printf(fails ? "FAILED %d\n" : "ALL OK\n", fails);
+    return fails ? 1 : 0;
+}

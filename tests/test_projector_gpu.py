@@ -145,3 +145,25 @@ def test_brick_and_gather_adjoints_agree(monkeypatch, cfg, n_angles):
     monkeypatch.setenv("KCT_ADJOINT", "gather")
     gather = projector(grid, geom).apply_adjoint(y)
     assert rel_l2(brick, gather) < 2e-6
+
+
+def test_sharded_operators_match_full():
+    """Angle-shard forward and z-slab adjoint (shard.py, the multi-GPU
+    decomposition) reproduce the full operators on the CUDA path."""
+    from paper_2509_08574_b200 import shard
+    grid, geom = baseline_geometry(1, n_angles=12)
+    gs, ge = to_pkg(grid, geom)
+    full = k.ConeBeamProjector(gs, ge)
+    rng = np.random.default_rng(4)
+    x = rng.uniform(0, 0.04, grid.count).astype(np.float32)
+    y = rng.uniform(0, 1, geom.ray_count).astype(np.float32)
+    fwd = full.apply(x).reshape(geom.n_angles, -1)
+    adj = full.apply_adjoint(y).reshape(grid.nz, -1)
+    for world in (2, 3):
+        for r in range(world):
+            part = k.ConeBeamProjector(gs, shard.shard_geometry(ge, world, r)).apply(x)
+            np.testing.assert_array_equal(part.reshape(-1, fwd.shape[1]),
+                                          fwd[shard.angle_indices(geom.n_angles, world, r)])
+            z0, z1 = shard.slab_range(grid.nz, world, r)
+            blk = k.ConeBeamProjector(shard.slab_grid(gs, world, r), ge).apply_adjoint(y)
+            assert rel_l2(blk, adj[z0:z1]) < 1e-6
