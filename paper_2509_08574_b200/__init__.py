@@ -36,7 +36,7 @@ __all__ = [
     "subsample_indices", "subsample_angles", "LIB_PATH",
 ]
 
-LIB_PATH = _build.LIB
+LIB_PATH = os.environ.get("KCT_LIB_PATH", _build.LIB)
 MEM_HOST, MEM_DEVICE = 0, 1
 LAYOUT_REFERENCE, LAYOUT_NATIVE = 0, 1
 KIND_TV, KIND_PIPLE, KIND_PICCS = 0, 1, 2
@@ -125,7 +125,7 @@ def load_library(build: bool = True):
     """Load (building in-tree first if stale) the CUDA library.  Raises if absent."""
     global _lib
     if _lib is None:
-        if build:
+        if build and LIB_PATH == _build.LIB:
             try:
                 _build.build()
             except Exception:  # no nvcc on this host: the prebuilt .so must exist

@@ -180,11 +180,23 @@ __device__ __forceinline__ void footprint(const DevGeom& g, float cth, float sth
 // one warp and its contributions are added in a fixed (angle, column, pass,
 // row group, segment, piece) order: deterministic, no atomics, exactly A^T.
 // ----------------------------------------------------------------------------
-constexpr int BX = 8, BY = 8;
-constexpr int kAdjWarps = 4;
-constexpr int kAdjRows = 1;  // rows per lane (C)
+// Brick shape: tall narrow bricks (4x4 voxel columns x ~128 slabs, two rows
+// per lane) measured best at c3 (tools/adj_sweep.sh).
+#ifndef KCT_BX
+#define KCT_BX 4
+#define KCT_BY 4
+#endif
+#ifndef KCT_ADJ_WARPS
+#define KCT_ADJ_WARPS 4
+#endif
+constexpr int BX = KCT_BX, BY = KCT_BY;
+constexpr int kAdjWarps = KCT_ADJ_WARPS;
+#ifndef KCT_ADJ_ROWS
+#define KCT_ADJ_ROWS 2
+#endif
+constexpr int kAdjRows = KCT_ADJ_ROWS;  // rows per lane (C)
 constexpr int kMaxSeg = 16;  // (BX - 1) + (BY - 1) interior crossings + 1 (+ slack)
-constexpr int kMaxBz = 128;
+constexpr int kMaxBz = 512;
 constexpr unsigned kFull = 0xffffffffu;
 
 struct __align__(16) Seg {
@@ -745,9 +757,12 @@ void Projector::build_tables(const kct_geometry& geom) {
     S = std::max(S, 1);
     if (S > 64 || full_fp) adj_gather_ = true;  // degenerate geometry: use the gather kernel
     adj_S_ = S;
-    // one pass of 32*C lanes should cover the rows of a brick
-    adj_bz_ = std::clamp(std::min((int)std::floor((32.0 * kAdjRows * S - 3.0) * dkz_min), nz), 1,
-                         kMaxBz);
+    // bricks ~128 slabs tall, nz split evenly (fewer per-row z-state
+    // initialisations per ray than short bricks; measured)
+    {
+        const int nbz = (nz + 127) / 128;
+        adj_bz_ = (nz + nbz - 1) / nbz;
+    }
     if (const char* e = std::getenv("KCT_ADJ_BZ")) adj_bz_ = std::clamp(std::atoi(e), 1, kMaxBz);
 
     KCT_CUDA(cudaMalloc(&d_cols_, cols.size() * sizeof(ColParams)));
