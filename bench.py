@@ -169,11 +169,19 @@ def run_ours(args):
     from paper_2509_08574_b200 import synth
 
     ws, rank, local = dist_env()
+    ndev = torch.cuda.device_count()
+    # one process per GPU; if fewer GPUs than ranks (functional check only),
+    # ranks share devices and synchronise over gloo (host barriers only)
+    shared = ws > ndev
+    local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg = synth.CONFIGS["c3"]
     M = cfg.n ** 3
     na = cfg.followup_views
@@ -231,7 +239,7 @@ def run_ours(args):
     t_b = [b.elapsed_time(c) * 1e-3 for _, b, c in ev]
     t_tot = sum(t_f) + sum(t_b)
     if ws > 1:
-        tt = torch.tensor([t_tot], device=dev, dtype=torch.float64)
+        tt = torch.tensor([t_tot], device="cpu" if shared else dev, dtype=torch.float64)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_tot = float(tt.item())
     gups = 2.0 * M * na * args.steps / t_tot / 1e9
@@ -264,7 +272,8 @@ def run_ours(args):
                                   "DSO 1000 / DSD 1500",
                       "M": M, "n_angles": na, "nnz": nnz_f if ws == 1 else None,
                       "l2": "flushed (256 MiB write) between timed steps, flush not timed",
-                      "parallelism": f"angles/z-slabs x{ws}" if ws > 1 else "single GPU"},
+                      "parallelism": f"angles/z-slabs x{ws}" if ws > 1 else "single GPU",
+                      **({"shared_devices": "functional check: more ranks than GPUs"} if shared else {})},
            "kernels_ms": {"forward": round(1e3 * mean_f, 4), "adjoint": round(1e3 * mean_b, 4)},
            "gups_forward": round(M * len(my_angles) / mean_f / 1e9, 3),
            "gups_adjoint": round(Mb * na / mean_b / 1e9, 3),
