@@ -31,8 +31,11 @@ constexpr float kInf = __builtin_huge_valf();
 // A CTA holds 4 adjacent columns of the same angle and row band so their
 // overlapping voxel columns are served from L1.
 // ----------------------------------------------------------------------------
+#ifndef KCT_FWD_MINB
+#define KCT_FWD_MINB 1
+#endif
 template <int C, bool COUNT>
-__global__ void __launch_bounds__(128) fwd_kernel(const float* __restrict__ vol,
+__global__ void __launch_bounds__(128, KCT_FWD_MINB) fwd_kernel(const float* __restrict__ vol,
                                                   float* __restrict__ out,
                                                   const ColParams* __restrict__ cols,
                                                   const float* __restrict__ dvtab,
@@ -46,8 +49,10 @@ __global__ void __launch_bounds__(128) fwd_kernel(const float* __restrict__ vol,
     const int iv0 = blockIdx.y * (32 * C) + lane;
     const int nz = g.nz;
 
+    // per ray: slab k, next crossing wz of plane P (kept as pk = P - k0),
+    // remaining crossings nrem of planes inside [0, nz]
     float acc[C], wz[C], fz[C], imk[C], dvv[C];
-    int k[C], kstep[C], kz0i[C];
+    int k[C], kstep[C], pk[C], nrem[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
         const int iv = iv0 + 32 * c;
@@ -59,16 +64,19 @@ __global__ void __launch_bounds__(128) fwd_kernel(const float* __restrict__ vol,
         const double kzd = fma(row_ok ? dvd[iv] : 0.0, cp.g_in, -g.kz0d);
         const double fl = floor(kzd);
         const int k0 = (int)fmax(fmin(fl, 1.0e9), -1.0e9);
-        kz0i[c] = k0;
         fz[c] = (float)(kzd - fl);
         imk[c] = row_ok ? __fmul_rn(invdv[iv], cp.inv_h1) : 0.f;
         int kk = min(max(k0, -1), nz);
-        kstep[c] = dv > 0.f ? 1 : -1;
-        if (!row_ok) kk = -1 - nz;  // never valid, never crosses
+        const int ks = dv > 0.f ? 1 : -1;
+        kstep[c] = ks;
+        const int P = ks > 0 ? kk + 1 : kk;
+        int n = ks > 0 ? nz - kk : kk + 1;  // planes P, P+ks, ... inside [0, nz]
+        if (!row_ok || dv == 0.f) n = 0;
+        if (!row_ok) kk = -1 - nz;  // never valid
         k[c] = kk;
-        const int P = dv > 0.f ? kk + 1 : kk;
-        wz[c] = (row_ok && dv != 0.f && P >= 0 && P <= nz) ? zcross(P, k0, fz[c], imk[c], cp.w_in)
-                                                            : kInf;
+        pk[c] = P - k0;
+        nrem[c] = max(n, 0);
+        wz[c] = nrem[c] > 0 ? __fmaf_rn(__fsub_rn((float)pk[c], fz[c]), imk[c], cp.w_in) : kInf;
     }
 
     if (cp.w_in < cp.w_out) {
@@ -84,12 +92,12 @@ __global__ void __launch_bounds__(128) fwd_kernel(const float* __restrict__ vol,
             const bool stepx = wnx <= wny;
             const float wnext = stepx ? wnx : wny;
             const float wb = fmaxf(fminf(wnext, cp.w_out), wcur);
-            const int col = (i + nx * j) * nz;
+            const unsigned col = (unsigned)(i + nx * j) * (unsigned)nz;
             float v[C], wa[C];
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 wa[c] = wcur;
-                v[c] = (unsigned)k[c] < (unsigned)nz ? (COUNT ? 1.f : __ldg(vol + col + k[c])) : 0.f;
+                v[c] = (unsigned)k[c] < (unsigned)nz ? (COUNT ? 1.f : __ldg(vol + (col + (unsigned)k[c]))) : 0.f;
             }
 #pragma unroll
             for (int c = 0; c < C; ++c) {
@@ -101,10 +109,12 @@ __global__ void __launch_bounds__(128) fwd_kernel(const float* __restrict__ vol,
                         wa[c] = wz[c];
                         k[c] += kstep[c];
                         const bool ok = (unsigned)k[c] < (unsigned)nz;
-                        v[c] = ok ? (COUNT ? 1.f : __ldg(vol + col + k[c])) : 0.f;
-                        const int P = kstep[c] > 0 ? k[c] + 1 : k[c];
-                        wz[c] = (P >= 0 && P <= nz) ? zcross(P, kz0i[c], fz[c], imk[c], cp.w_in)
-                                                    : kInf;
+                        v[c] = ok ? (COUNT ? 1.f : __ldg(vol + (col + (unsigned)k[c]))) : 0.f;
+                        pk[c] += kstep[c];
+                        nrem[c] -= 1;
+                        wz[c] = nrem[c] > 0
+                                    ? __fmaf_rn(__fsub_rn((float)pk[c], fz[c]), imk[c], cp.w_in)
+                                    : kInf;
                     } while (wz[c] < wb);
                 }
                 const float len = wb - wa[c];
@@ -743,7 +753,9 @@ void Projector::build_tables(const kct_geometry& geom) {
 
     // forward launch shape: rows per warp = 32*C, C <= 4
     const int chunks = (nv + 31) / 32;
-    fwd_bands_ = (chunks + 3) / 4;
+    int cmax = 4;
+    if (const char* e = std::getenv("KCT_FWD_C")) cmax = std::clamp(std::atoi(e), 1, 4);
+    fwd_bands_ = (chunks + cmax - 1) / cmax;
     fwd_c_ = (chunks + fwd_bands_ - 1) / fwd_bands_;
     const int kc = (nz + 31) / 32;
     adj_k_ = kc <= 1 ? 1 : kc <= 2 ? 2 : kc <= 4 ? 4 : 8;
