@@ -133,6 +133,18 @@ int kct_volume_from_native(const kct_projector* h, const float* native, float* r
 int kct_proj_to_native(const kct_projector* h, const float* ref, float* native, void* stream);
 int kct_proj_from_native(const kct_projector* h, const float* native, float* ref, void* stream);
 
+/* ---- multi-process solves ------------------------------------------------ */
+/* Collective hook: sum `count` elements (dtype 0 = float32, 1 = float64) of
+ * the device buffer `buf` over all ranks, in place, ordered on `stream`;
+ * return 0 on success.  Installing a hook puts the handle in angle-sharded
+ * mode: its geometry holds this rank's projection angles, solver inputs `b`
+ * are this rank's readings, the volume-domain state is replicated, and the
+ * solvers sum A^T partial volumes and projection-domain reductions over the
+ * ranks (the "partial-volume reductions and Krylov scalar all-reduces" of the
+ * north star).  NULL restores single-process mode. */
+typedef int (*kct_allreduce_fn)(void* ctx, void* buf, size_t count, int dtype, void* stream);
+int kct_set_allreduce(kct_projector* h, kct_allreduce_fn fn, void* ctx);
+
 /* ---- solvers ---------------------------------------------------------- */
 /* cgls_recon (recon.hpp:312-315 -> baseline_solve :274-307 -> cgls krylov.hpp:59-127).
  * b: N floats, x0: M floats or NULL (zeros), ground_truth: M or NULL,

@@ -33,7 +33,7 @@ __all__ = [
     "ConfigError", "SolverError", "KctError", "GridSpec", "ConeBeamGeometry", "ProjectionSet",
     "ConeBeamProjector", "RegularizationParams", "ReconOptions", "ReconReport", "cgls_recon",
     "irn_tv", "irn_piple", "irn_piccs", "resolve_tau", "uniform_angles", "load_library",
-    "subsample_indices", "subsample_angles", "LIB_PATH",
+    "subsample_indices", "subsample_angles", "LIB_PATH", "shard",
 ]
 
 LIB_PATH = os.environ.get("KCT_LIB_PATH", _build.LIB)
@@ -116,6 +116,7 @@ _SIGS = {
     "kct_irn_piccs": ([_P, _P, _P, _P, _P, C.POINTER(_Reg), _P, C.POINTER(_Report), C.c_int,
                        C.c_int, _P], C.c_int),
     "kct_resolve_tau": ([C.c_double, _P, C.c_size_t], C.c_double),
+    "kct_set_allreduce": ([_P, _P, _P], C.c_int),  # typed by distributed.install_allreduce
 }
 
 _lib = None
@@ -530,3 +531,6 @@ def resolve_tau(tau: float, reference=None) -> float:
         return float(lib.kct_resolve_tau(tau, None, 0))
     r = np.ascontiguousarray(np.asarray(reference, dtype=np.float32).reshape(-1))
     return float(lib.kct_resolve_tau(tau, r.ctypes.data, r.size))
+
+
+from . import shard  # noqa: E402  (depends on the types above)

@@ -255,6 +255,14 @@ int kct_proj_from_native(const kct_projector* h, const float* native, float* ref
     });
 }
 
+int kct_set_allreduce(kct_projector* h, kct_allreduce_fn fn, void* ctx) {
+    return guarded([&] {
+        auto& P = get(h);
+        P.comm_fn = fn;
+        P.comm_ctx = ctx;
+    });
+}
+
 double kct_resolve_tau(double tau, const float* reference, size_t n) {
     return kct::resolve_tau(tau, reference, n);
 }

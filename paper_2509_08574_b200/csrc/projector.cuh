@@ -44,6 +44,9 @@ class Projector {
 
     // Solver workspace cached across calls (owned by solver.cu).
     std::shared_ptr<void> workspace;
+    // Angle-sharded multi-process mode (kct_set_allreduce).
+    kct_allreduce_fn comm_fn = nullptr;
+    void* comm_ctx = nullptr;
 
     int fwd_chunks() const { return fwd_c_; }
     int adj_k() const { return adj_k_; }

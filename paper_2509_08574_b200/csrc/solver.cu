@@ -485,12 +485,44 @@ __global__ void k_set_nonzero(Ctl* ctl, const double* part) {
     if (threadIdx.x == 0) ctl->x_nonzero = t > 0.0 ? 1 : 0;
 }
 
+// Fold the block partials of one slot into element 0 (fixed order), so a
+// single double carries the slot to a cross-rank all-reduce.
+__global__ void k_fold(double* part, int slot) {
+    __shared__ double sm[32];
+    double t = 0.0;
+    for (int b = threadIdx.x; b < kGrid; b += blockDim.x) t += part[slot * kGrid + b];
+    t = block_sum(t, sm);
+    __syncthreads();
+    for (int b = threadIdx.x; b < kGrid; b += blockDim.x) part[slot * kGrid + b] = 0.0;
+    __syncthreads();
+    if (threadIdx.x == 0) part[slot * kGrid] = t;
+}
+
 struct Engine {
     Projector& P;
     Workspace& w;
     cudaStream_t stream;
     RegCfg rc{};
     int kind = KCT_KIND_TV;
+
+    // angle-sharded mode: sum A^T partial volumes and projection-domain
+    // reductions over the ranks (no-ops in single-process mode)
+    void reduce_volume(float* v) {
+        if (!P.comm_fn) return;
+        if (P.comm_fn(P.comm_ctx, v, w.m, 0, stream) != 0)
+            throw CudaError("allreduce hook failed (volume)");
+    }
+    void reduce_slot(int slot) {
+        if (!P.comm_fn) return;
+        k_fold<<<1, kBlock, 0, stream>>>(w.part, slot);
+        KCT_CUDA(cudaGetLastError());
+        if (P.comm_fn(P.comm_ctx, w.part + slot * kGrid, 1, 1, stream) != 0)
+            throw CudaError("allreduce hook failed (scalar)");
+    }
+    void adjoint(const float* y, float* v) {
+        P.adjoint(y, v, stream);
+        reduce_volume(v);
+    }
 
     // weights (optional) and smoothed-TV / quadratic sums of the objective at w.x
     void weights(bool write) {
@@ -510,6 +542,7 @@ struct Engine {
             P.forward(w.x, w.q, stream);
             KCT_LAUNCH(k_resid, w.b, w.q, nullptr, w.n, w.part, 0);
         }
+        reduce_slot(0);
         launch_scalar(w, S_DATA, stream);
         launch_scalar(w, S_OBJ, stream, 0.0, nullptr, nullptr, w.obj + idx, kind);
     }
@@ -522,7 +555,7 @@ struct Engine {
             KCT_LAUNCH(k_stats, w.x, w.m, w.part);
             k_set_nonzero<<<1, kBlock, 0, stream>>>(w.ctl, w.part);
             KCT_CUDA(cudaGetLastError());
-            P.adjoint(w.b, w.p, stream);
+            adjoint(w.b, w.p);
             KCT_LAUNCH(k_reggrad, w.p, nullptr, w.prior, w.w1, w.w2, w.p, rc, w.part);
             launch_scalar(w, S_REF, stream);
         } else {
@@ -534,11 +567,12 @@ struct Engine {
             P.forward(w.x, w.q, stream);
             KCT_LAUNCH(k_resid, w.b, w.q, w.r, w.n, w.part, 0);
         }
+        reduce_slot(0);
         if (obj_idx >= 0) {
             launch_scalar(w, S_DATA, stream);
             launch_scalar(w, S_OBJ, stream, 0.0, nullptr, nullptr, w.obj + obj_idx, kind);
         }
-        P.adjoint(w.r, w.s, stream);
+        adjoint(w.r, w.s);
         KCT_LAUNCH(k_reggrad, w.s, x_is_zero ? nullptr : w.x, w.prior, w.w1, w.w2, w.s, rc,
                    w.part);
         launch_scalar(w, S_INIT, stream, tol);
@@ -549,10 +583,12 @@ struct Engine {
     void iterate(double* res, double* err, bool with_gt) {
         P.forward(w.p, w.q, stream);
         KCT_LAUNCH(k_normq, w.q, w.n, w.p, w.w1, w.w2, rc, w.ctl, w.part);
+        reduce_slot(0);
         launch_scalar(w, S_DELTA, stream);
         KCT_LAUNCH(k_update_xr, w.x, w.p, w.m, w.r, w.q, w.n, with_gt ? w.gt : nullptr, w.ctl,
                    w.part);
-        P.adjoint(w.r, w.s, stream);
+        reduce_slot(4);
+        adjoint(w.r, w.s);
         KCT_LAUNCH(k_reggrad, w.s, w.x, w.prior, w.w1, w.w2, w.s, rc, w.part);
         launch_scalar(w, S_GAMMA, stream, 0.0, res, err);
         KCT_LAUNCH(k_update_p, w.p, w.s, w.m, w.ctl, 0);

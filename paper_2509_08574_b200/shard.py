@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import ConeBeamGeometry, GridSpec
+from . import ConeBeamGeometry, GridSpec  # noqa: F401  (circular-safe: defined first)
 
 
 def angle_indices(n_angles: int, world: int, rank: int) -> np.ndarray:
