@@ -34,15 +34,19 @@ constexpr float kInf = __builtin_huge_valf();
 #ifndef KCT_FWD_MINB
 #define KCT_FWD_MINB 1
 #endif
+#ifndef KCT_FWD_WARPS
+#define KCT_FWD_WARPS 4  // adjacent detector columns per CTA (shared voxel columns in L1)
+#endif
+constexpr int kFwdWarps = KCT_FWD_WARPS;
 template <int C, bool COUNT>
-__global__ void __launch_bounds__(128, KCT_FWD_MINB) fwd_kernel(const float* __restrict__ vol,
+__global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const float* __restrict__ vol,
                                                   float* __restrict__ out,
                                                   const ColParams* __restrict__ cols,
                                                   const float* __restrict__ dvtab,
                                                   const float* __restrict__ invdv,
                                                   const double* __restrict__ dvd, DevGeom g) {
     const int lane = threadIdx.x & 31;
-    const int iu = blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int iu = blockIdx.x * kFwdWarps + (threadIdx.x >> 5);
     const int a = blockIdx.z;
     if (iu >= g.nu) return;
     const ColParams cp = cols[(size_t)a * g.nu + iu];
@@ -800,12 +804,13 @@ template <bool COUNT>
 static void launch_fwd(int C, int bands, const float* vol, float* out, const ColParams* cols,
                        const float* dv, const float* invdv, const double* dvd, const DevGeom& g,
                        cudaStream_t s) {
-    dim3 grid((g.nu + 3) / 4, bands, g.na);
+    dim3 grid((g.nu + kFwdWarps - 1) / kFwdWarps, bands, g.na);
+    const int th = kFwdWarps * 32;
     switch (C) {
-    case 1: fwd_kernel<1, COUNT><<<grid, 128, 0, s>>>(vol, out, cols, dv, invdv, dvd, g); break;
-    case 2: fwd_kernel<2, COUNT><<<grid, 128, 0, s>>>(vol, out, cols, dv, invdv, dvd, g); break;
-    case 3: fwd_kernel<3, COUNT><<<grid, 128, 0, s>>>(vol, out, cols, dv, invdv, dvd, g); break;
-    default: fwd_kernel<4, COUNT><<<grid, 128, 0, s>>>(vol, out, cols, dv, invdv, dvd, g); break;
+    case 1: fwd_kernel<1, COUNT><<<grid, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, g); break;
+    case 2: fwd_kernel<2, COUNT><<<grid, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, g); break;
+    case 3: fwd_kernel<3, COUNT><<<grid, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, g); break;
+    default: fwd_kernel<4, COUNT><<<grid, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, g); break;
     }
     KCT_CUDA(cudaGetLastError());
 }
