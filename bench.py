@@ -285,6 +285,18 @@ def run_ours(args):
                                       "Siddon intersections counted on device"},
            "gpu_launches": 2 * args.steps, "clocks": clk.summary()}
 
+    # ---- FDK (fdk.hpp:50-139) of the c3 follow-up geometry, device resident ----
+    if rank == 0 and ws == 1:
+        fdk_out = torch.empty(M, dtype=torch.float32, device=dev)
+        A_f.fdk(q, out=fdk_out)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(3):
+            A_f.fdk(q, out=fdk_out)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        out["fdk_ms"] = round(e0.elapsed_time(e1) / 3, 4)
+
     # ---- end to end through the C ABI with host buffers (reference layouts) ----
     if rank == 0 and not args.skip_e2e:
         vol_h = torch.from_numpy(prior).pin_memory().numpy()

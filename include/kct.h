@@ -133,6 +133,11 @@ int kct_volume_from_native(const kct_projector* h, const float* native, float* r
 int kct_proj_to_native(const kct_projector* h, const float* ref, float* native, void* stream);
 int kct_proj_from_native(const kct_projector* h, const float* native, float* ref, void* stream);
 
+/* Feldkamp-Davis-Kress reconstruction — fdk (fdk.hpp:50-139): cosine
+ * weighting, Ram-Lak ramp filter, distance-weighted bilinear backprojection.
+ * Needs >= 2 angles over a full circle (short scans are not compensated). */
+int kct_fdk(kct_projector* h, const float* proj, float* vol, int mem, int layout, void* stream);
+
 /* ---- multi-process solves ------------------------------------------------ */
 /* Collective hook: sum `count` elements (dtype 0 = float32, 1 = float64) of
  * the device buffer `buf` over all ranks, in place, ordered on `stream`;

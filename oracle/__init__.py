@@ -170,6 +170,7 @@ class Oracle:
         self._obj.argtypes = [gp, gg, C.c_int, P(C.c_double), P(C.c_double), P(C.c_double),
                               C.c_double, C.c_double, C.c_double]
         self._obj.restype = C.c_double
+        self._fdk = g("fdk"); self._fdk.argtypes = [gp, gg, P(C.c_double), P(C.c_double)]
         self._cgls = g("cgls_recon")
         self._cgls.argtypes = [gp, gg, P(C.c_double), C.c_size_t, P(C.c_double), P(C.c_double),
                                C.c_double, P(C.c_double), P(KctReport)]
@@ -203,6 +204,13 @@ class Oracle:
         out = np.zeros(grid.count)
         gc, ge = grid.c(), geom.c()
         self._check(self._adj(C.byref(gc), C.byref(ge), _dp(p), _dp(out)))
+        return out
+
+    def fdk(self, grid: Grid, geom: Geometry, proj) -> np.ndarray:
+        p = self._f64(proj, geom.ray_count)
+        out = np.zeros(grid.count)
+        gc, ge = grid.c(), geom.c()
+        self._check(self._fdk(C.byref(gc), C.byref(ge), _dp(p), _dp(out)))
         return out
 
     def count_nnz(self, grid: Grid, geom: Geometry) -> int:

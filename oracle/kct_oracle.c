@@ -677,3 +677,113 @@ int ora_irn(const kct_grid* grid, const kct_geometry* g, int kind, const double*
     free(w1); free(w2); free(tmp3); free(tmpm); free(rhs); free(start);
     return rc;
 }
+
+/* ---- FDK: fdk.hpp:50-139 with detail/fft.hpp:23-49 -------------------- */
+typedef struct { double re, im; } cpx;
+
+static void fft_inplace(cpx* a, size_t n, int inverse) { /* fft.hpp:23-49 */
+    for (size_t i = 1, j = 0; i < n; ++i) {
+        size_t bit = n >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j ^= bit;
+        if (i < j) { cpx t = a[i]; a[i] = a[j]; a[j] = t; }
+    }
+    for (size_t len = 2; len <= n; len <<= 1) {
+        const double ang = (inverse ? 2.0 : -2.0) * M_PI / (double)len;
+        const cpx wl = {cos(ang), sin(ang)};
+        for (size_t i = 0; i < n; i += len) {
+            cpx w = {1.0, 0.0};
+            for (size_t k = 0; k < len / 2; ++k) {
+                const cpx u = a[i + k], x = a[i + k + len / 2];
+                const cpx v = {x.re * w.re - x.im * w.im, x.re * w.im + x.im * w.re};
+                a[i + k] = (cpx){u.re + v.re, u.im + v.im};
+                a[i + k + len / 2] = (cpx){u.re - v.re, u.im - v.im};
+                const cpx nw = {w.re * wl.re - w.im * wl.im, w.re * wl.im + w.im * wl.re};
+                w = nw;
+            }
+        }
+    }
+    if (inverse)
+        for (size_t i = 0; i < n; ++i) { a[i].re /= (double)n; a[i].im /= (double)n; }
+}
+
+int ora_fdk(const kct_grid* grid, const kct_geometry* g, const double* proj, double* vol) {
+    int rc = validate(grid, g);
+    if (rc) return rc;
+    if (g->n_angles < 2) return fail(2, "fdk needs at least two projection angles");
+    const int nu = g->nu, nv = g->nv, na = g->n_angles;
+    const size_t per = (size_t)nu * nv;
+    const double mag = g->dso / g->dsd;
+    const double du = g->pu * mag, dv = g->pv * mag;
+    const double u0 = (0.5 - 0.5 * nu) * du + g->offset_u * mag;
+    const double v0 = (0.5 - 0.5 * nv) * dv + g->offset_v * mag;
+    size_t pad = 1;
+    while (pad < 2 * (size_t)nu) pad <<= 1;
+    cpx* ramp = (cpx*)calloc(pad, sizeof(cpx)); /* ramlak_response fdk.hpp:30-42 */
+    const double inv = 1.0 / (du * du);
+    ramp[0].re = 0.25 * inv;
+    for (size_t k = 1; k < pad / 2; k += 2) {
+        const double v = -inv / (M_PI * M_PI * (double)k * (double)k);
+        ramp[k].re = v;
+        ramp[pad - k].re = v;
+    }
+    fft_inplace(ramp, pad, 0);
+    double* filtered = (double*)malloc((size_t)na * per * sizeof(double));
+#pragma omp parallel num_threads(nthreads())
+    {
+        cpx* row = (cpx*)malloc(pad * sizeof(cpx));
+#pragma omp for schedule(static)
+        for (long r = 0; r < (long)na * nv; ++r) {
+            const int ia = (int)(r / nv), iv = (int)(r % nv);
+            const double v = v0 + iv * dv;
+            memset(row, 0, pad * sizeof(cpx));
+            const size_t base = ia * per + (size_t)iv * nu;
+            for (int iu = 0; iu < nu; ++iu) {
+                const double u = u0 + iu * du;
+                const double cosw = g->dso / sqrt(g->dso * g->dso + u * u + v * v);
+                row[iu].re = proj[base + iu] * cosw;
+            }
+            fft_inplace(row, pad, 0);
+            for (size_t i = 0; i < pad; ++i) {
+                const cpx a = row[i], b = ramp[i];
+                row[i] = (cpx){a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+            }
+            fft_inplace(row, pad, 1);
+            for (int iu = 0; iu < nu; ++iu) filtered[base + iu] = row[iu].re * du;
+        }
+        free(row);
+    }
+    const double scale = 0.5 * (2.0 * M_PI / (double)na);
+#pragma omp parallel for schedule(static) num_threads(nthreads())
+    for (int k = 0; k < grid->nz; ++k) {
+        const double z = grid->oz + (k + 0.5) * grid->sz;
+        for (int j = 0; j < grid->ny; ++j) {
+            const double y = grid->oy + (j + 0.5) * grid->sy;
+            for (int i = 0; i < grid->nx; ++i) {
+                const double x = grid->ox + (i + 0.5) * grid->sx;
+                double acc = 0.0;
+                for (int ia = 0; ia < na; ++ia) {
+                    const double c = cos(g->angles[ia]), s = sin(g->angles[ia]);
+                    const double ss = x * c + y * s, t = -x * s + y * c;
+                    const double L = g->dso - ss;
+                    if (L <= 1e-6 * g->dso) continue;
+                    const double u = t * g->dso / L, v = z * g->dso / L;
+                    const double fu = (u - u0) / du, fv = (v - v0) / dv;
+                    const int ju = (int)floor(fu), jv = (int)floor(fv);
+                    if (ju < -1 || ju > nu - 1 || jv < -1 || jv > nv - 1) continue;
+                    const double au = fu - ju, av = fv - jv;
+                    const double* f = filtered + (size_t)ia * per;
+#define S_(uu, vv) (((uu) < 0 || (uu) >= nu || (vv) < 0 || (vv) >= nv) ? 0.0 : f[(size_t)(vv) * nu + (uu)])
+                    const double val = (1.0 - au) * (1.0 - av) * S_(ju, jv) + au * (1.0 - av) * S_(ju + 1, jv) +
+                                       (1.0 - au) * av * S_(ju, jv + 1) + au * av * S_(ju + 1, jv + 1);
+#undef S_
+                    acc += (g->dso * g->dso) / (L * L) * val;
+                }
+                vol[(size_t)i + (size_t)grid->nx * ((size_t)j + (size_t)grid->ny * k)] = scale * acc;
+            }
+        }
+    }
+    free(ramp);
+    free(filtered);
+    return 0;
+}

@@ -58,6 +58,9 @@ int ora_irn(const kct_grid* grid, const kct_geometry* g, int kind, const double*
             const double* prior, const double* x0, const double* ground_truth,
             const kct_reg_params* p, double* x_out, kct_report* rep);
 
+/* fdk.hpp:50-139 (FFT ramp filter detail/fft.hpp:23-49) */
+int ora_fdk(const kct_grid* grid, const kct_geometry* g, const double* proj, double* vol);
+
 /* recon.hpp:93-120 */
 double ora_objective(const kct_grid* grid, const kct_geometry* g, int kind, const double* b,
                      const double* x, const double* prior, double alpha, double lambda,

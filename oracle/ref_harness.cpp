@@ -7,6 +7,7 @@
 // as kct_oracle.h (prefix ref_ instead of ora_).  Only the hot-path headers
 // are included (io.hpp / experiment.hpp need a vendor/ tree that is absent).
 #include <kryct/diffreg.hpp>
+#include <kryct/fdk.hpp>
 #include <kryct/krylov.hpp>
 #include <kryct/linear_map.hpp>
 #include <kryct/projector.hpp>
@@ -212,6 +213,16 @@ double ref_objective(const kct_grid* grid, const kct_geometry* g, int kind, cons
             std::span<const double>(prior, prior ? m : 0), a.grid().dims, alpha, lambda, tau);
     });
     return obj;
+}
+
+// fdk (fdk.hpp:50-139)
+int ref_fdk(const kct_grid* grid, const kct_geometry* g, const double* proj, double* vol) {
+    return guarded([&] {
+        kryct::ProjectionSet p(to_geom(g));
+        std::memcpy(p.data.data(), proj, p.data.size() * sizeof(double));
+        const auto v = kryct::fdk(p, to_grid(grid));
+        std::memcpy(vol, v.data.data(), v.data.size() * sizeof(double));
+    });
 }
 
 // cgls_recon (recon.hpp:312-315)

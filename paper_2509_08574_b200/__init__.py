@@ -32,7 +32,7 @@ from . import _build
 __all__ = [
     "ConfigError", "SolverError", "KctError", "GridSpec", "ConeBeamGeometry", "ProjectionSet",
     "ConeBeamProjector", "RegularizationParams", "ReconOptions", "ReconReport", "cgls_recon",
-    "irn_tv", "irn_piple", "irn_piccs", "resolve_tau", "uniform_angles", "load_library",
+    "irn_tv", "irn_piple", "irn_piccs", "fdk", "resolve_tau", "uniform_angles", "load_library",
     "subsample_indices", "subsample_angles", "LIB_PATH", "shard",
 ]
 
@@ -117,6 +117,7 @@ _SIGS = {
                        C.c_int, _P], C.c_int),
     "kct_resolve_tau": ([C.c_double, _P, C.c_size_t], C.c_double),
     "kct_set_allreduce": ([_P, _P, _P], C.c_int),  # typed by distributed.install_allreduce
+    "kct_fdk": ([_P, _P, _P, C.c_int, C.c_int, _P], C.c_int),
 }
 
 _lib = None
@@ -392,6 +393,14 @@ class ConeBeamProjector:
                                 _stream_of(ya.mem, self._dev_index(ya))))
         return x
 
+    def fdk(self, proj, out=None, layout=None):
+        """FDK reconstruction (fdk.hpp:50-139) of a full-circle scan on this geometry."""
+        pa = _Arg(proj, self.range_size(), "fdk: projections")
+        x = out if out is not None else _alloc_like(pa, self.domain_size())
+        _check(_lib.kct_fdk(self._h, pa.ptr, _ptr(x), pa.mem, _layout_code(layout, pa.mem),
+                            _stream_of(pa.mem, self._dev_index(pa))))
+        return x
+
     def count_nnz(self) -> int:
         n = C.c_uint64()
         _check(_lib.kct_count_nnz(self._h, C.byref(n), None))
@@ -522,6 +531,13 @@ def irn_piple(proj, grid, prior, params=None, opts=None, projector=None, layout=
 def irn_piccs(proj, grid, prior, params=None, opts=None, projector=None, layout=None):
     """recon.hpp:267-270 — the north-star entry point."""
     return _irn(KIND_PICCS, proj, grid, prior, params, opts, projector, layout)
+
+
+def fdk(proj: ProjectionSet, grid: GridSpec, projector: ConeBeamProjector | None = None,
+        layout=None):
+    """fdk (fdk.hpp:50-139)."""
+    A = _projector_for(proj, grid, projector)
+    return A.fdk(proj.data, layout=layout)
 
 
 def resolve_tau(tau: float, reference=None) -> float:

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libkct.so")
 BUILD = os.path.join(ROOT, "build", "kct")
-SOURCES = ["projector.cu", "solver.cu", "capi.cu"]
+SOURCES = ["projector.cu", "solver.cu", "fdk.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-diag-suppress", "550"]

@@ -255,6 +255,22 @@ int kct_proj_from_native(const kct_projector* h, const float* native, float* ref
     });
 }
 
+int kct_fdk(kct_projector* h, const float* proj, float* vol, int mem, int layout, void* stream) {
+    return guarded([&] {
+        auto& P = get(h);
+        check_mem_layout(mem, layout);
+        if (!vol || !proj) throw kct::ConfigError("fdk: null buffer");
+        DeviceGuard dg(P.device());
+        auto s = static_cast<cudaStream_t>(stream);
+        const size_t M = P.domain_size(), N = P.range_size();
+        const float* q = kct::stage_in(P, proj, N, false, mem, layout, 1, 2, s);
+        float* v = (mem == KCT_MEM_DEVICE && layout == KCT_LAYOUT_NATIVE) ? vol : P.scratch(0, M);
+        P.fdk(q, v, P.scratch(3, N), s);
+        kct::stage_out(P, v, vol, M, true, mem, layout, 2, s);
+        if (mem == KCT_MEM_HOST) KCT_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 int kct_set_allreduce(kct_projector* h, kct_allreduce_fn fn, void* ctx) {
     return guarded([&] {
         auto& P = get(h);

@@ -625,6 +625,12 @@ Projector::Projector(const kct_grid& grid, const kct_geometry& geom, int device)
     KCT_CUDA(cudaGetDevice(&device_));
     m_ = (size_t)grid.nx * grid.ny * grid.nz;
     n_ = (size_t)geom.nu * geom.nv * geom.n_angles;
+    dso_d_ = geom.dso;
+    dsd_d_ = geom.dsd;
+    pu_d_ = geom.pu;
+    pv_d_ = geom.pv;
+    offu_d_ = geom.offset_u;
+    offv_d_ = geom.offset_v;
     const char* mode = std::getenv("KCT_ADJOINT");
     adj_gather_ = mode && std::string(mode) == "gather";
     build_tables(geom);

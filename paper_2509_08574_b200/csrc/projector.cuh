@@ -32,6 +32,8 @@ class Projector {
     void adjoint(const float* proj, float* vol, cudaStream_t s) const;
     // Per-ray count of positive-length Siddon segments (as float) into proj.
     void count(float* proj, cudaStream_t s) const;
+    // FDK (fdk.hpp:50-139), native layouts; `filt` is N floats of scratch.
+    void fdk(const float* proj, float* vol, float* filt, cudaStream_t s) const;
 
     // Layout conversions (device, stream-ordered).
     void vol_to_native(const float* ref, float* nat, cudaStream_t s) const;
@@ -60,6 +62,8 @@ class Projector {
 
     kct_grid grid_;
     DevGeom dg_{};
+    // geometry as given, float64 (FDK weights)
+    double dso_d_ = 0, dsd_d_ = 0, pu_d_ = 0, pv_d_ = 0, offu_d_ = 0, offv_d_ = 0;
     int device_ = 0;
     size_t m_ = 0, n_ = 0;
     std::vector<float2> cs_;          // per-angle (cos, sin)

@@ -87,6 +87,16 @@ def recon_case(ref, name, grid, geom, seed):
                         **grid_dict(grid), **geom_dict(geom))
 
 
+def fdk_case(ref, name, grid, geom, seed):
+    """fdk.hpp:50-139 on a projected ellipsoid phantom."""
+    rng = np.random.default_rng(seed)
+    truth = f32(sphere(grid, 0.55, 0.02) + 0.005 * rng.uniform(0, 1, grid.count))
+    proj = f32(ref.forward(grid, geom, truth))
+    vol = ref.fdk(grid, geom, proj)
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), truth=truth, proj=proj, fdk=vol,
+                        **grid_dict(grid), **geom_dict(geom))
+
+
 def main():
     ref = Oracle("ref")
     op_case(ref, "op_tiny", Grid(4, 4, 4, 1.0, 1.1, 0.9), tiny_geometry(8, 10, 9), 101)
@@ -94,6 +104,8 @@ def main():
     op_case(ref, "op_c1_small", Grid(16, 16, 16, 4.0, 4.0, 4.0),
             Geometry(1000.0, 1500.0, 24, 24, 4.0, 4.0, uniform_angles(16)), 103)
     recon_case(ref, "recon_small", Grid(8, 8, 8), recon_geometry(6), 104)
+    fdk_case(ref, "fdk_small", Grid(24, 24, 16, 2.0, 2.0, 2.0),
+             Geometry(1000.0, 1500.0, 48, 32, 2.0, 2.0, uniform_angles(36), 0.5, -0.7), 105)
     print("golden fixtures written to", OUT)
 
 

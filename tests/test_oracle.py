@@ -57,6 +57,13 @@ def test_recon_golden(ora):
     assert rel_l2(x, d["piccs_auto_x"]) < 1e-12
 
 
+def test_fdk_golden(ora):
+    """fdk.hpp:50-139 restated (radix-2 FFT ramp filter) reproduces the reference."""
+    d = load_golden("fdk_small")
+    np.testing.assert_allclose(ora.fdk(grid_from(d), geom_from(d), d["proj"]), d["fdk"],
+                               rtol=0, atol=1e-12)
+
+
 @pytest.mark.skipif(not HAVE_REF, reason="reference not compiled (make -C oracle ref)")
 def test_oracle_equals_reference_c1():
     """Our restatement reproduces the reference bit for bit at c1 geometry."""
