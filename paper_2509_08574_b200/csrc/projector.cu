@@ -22,6 +22,7 @@ namespace kct {
 namespace {
 
 constexpr float kInf = __builtin_huge_valf();
+constexpr unsigned kFull = 0xffffffffu;
 
 // ----------------------------------------------------------------------------
 // Forward projector.  One warp = one detector column iu of one angle, C row
@@ -211,7 +212,6 @@ constexpr int kAdjWarps = KCT_ADJ_WARPS;
 constexpr int kAdjRows = KCT_ADJ_ROWS;  // rows per lane (C)
 constexpr int kMaxSeg = 16;  // (BX - 1) + (BY - 1) interior crossings + 1 (+ slack)
 constexpr int kMaxBz = 512;
-constexpr unsigned kFull = 0xffffffffu;
 
 struct __align__(16) Seg {
     float wa, wb;
@@ -316,20 +316,19 @@ __device__ __forceinline__ void row_segment(RowZ& r, const Seg& sg, unsigned col
     }
 }
 
+#ifndef KCT_ADJ_MINB
+#define KCT_ADJ_MINB 6  // caps registers at ~64: 8 CTAs of 4 warps per SM (measured)
+#endif
 template <int C>
-__global__ void __launch_bounds__(kAdjWarps * 32) adj_brick_kernel(
+__global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel(
     const float* __restrict__ proj, float* __restrict__ out, const ColParams* __restrict__ cols,
     const float* __restrict__ dvtab, const float* __restrict__ invdv, const double* __restrict__ dvd,
-    DevGeom g, BrickCfg bc, AngleBatch ab, int nab, int accumulate) {
+    DevGeom g, BrickCfg bc, AngleBatch ab, int nab, int accumulate,
+    const int* __restrict__ order, int* queue) {
     extern __shared__ float sm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int brick = blockIdx.x * kAdjWarps + warp;
-    if (brick >= bc.nbx * bc.nby * bc.nbz) return;
-    const int bi = brick % bc.nbx, bj = (brick / bc.nbx) % bc.nby, bk = brick / (bc.nbx * bc.nby);
+    const int nbricks = bc.nbx * bc.nby * bc.nbz;
     const int BZ = bc.bz;
-    const int I0 = bi * BX, J0 = bj * BY, K0 = bk * BZ;
-    const int bxn = min(BX, g.nx - I0), byn = min(BY, g.ny - J0), bzn = min(BZ, g.nz - K0);
-    const int kend = K0 + bzn;
     const int nu = g.nu, nv = g.nv;
     // per-warp shared layout: acc[BX*BY][BZ + 2] (slab k at k - K0 + 1; two
     // guard slabs) | segs[kMaxSeg] | bnd[kMaxSeg + 2] | axis[kMaxSeg + 2]
@@ -340,16 +339,39 @@ __global__ void __launch_bounds__(kAdjWarps * 32) adj_brick_kernel(
     float* bnd = acc + BX * BY * CS + 4 * kMaxSeg;
     int* axis = reinterpret_cast<int*>(bnd + kMaxSeg + 2);
     const unsigned acc_s = (unsigned)__cvta_generic_to_shared(acc);
+    const bool xl = lane < 8;  // lanes 0..7: interior x planes, 8..15: interior y planes
+    const int pl = xl ? lane : lane - 8;
+    const unsigned below = (1u << lane) - 1u;
+    const float rpv = 1.f / g.pv;
+    const int S = bc.S;
+
+    // Bricks are handed out to warps by a queue (heaviest first, `order`), so
+    // the uneven per-brick work does not leave a partial last wave; without a
+    // queue every warp takes one brick.  Each brick is still computed by one
+    // warp in a fixed order: the result does not depend on the schedule.
+    int ticket = queue ? 0 : blockIdx.x * kAdjWarps + warp;
+    for (;;) {
+    int brick;
+    if (queue) {
+        int tk = 0;
+        if (lane == 0) tk = atomicAdd(queue, 1);
+        tk = __shfl_sync(kFull, tk, 0);
+        if (tk >= nbricks) break;
+        brick = order[tk];
+    } else {
+        if (ticket >= nbricks) break;
+        brick = ticket;
+        ticket = nbricks;
+    }
+    const int bi = brick % bc.nbx, bj = (brick / bc.nbx) % bc.nby, bk = brick / (bc.nbx * bc.nby);
+    const int I0 = bi * BX, J0 = bj * BY, K0 = bk * BZ;
+    const int bxn = min(BX, g.nx - I0), byn = min(BY, g.ny - J0), bzn = min(BZ, g.nz - K0);
+    const int kend = K0 + bzn;
     for (int q = lane; q < BX * BY * CS; q += 32) acc[q] = 0.f;
     __syncwarp();
 
     const float X0 = g.ox + I0 * g.sx, X1 = g.ox + (I0 + bxn) * g.sx;
     const float Y0 = g.oy + J0 * g.sy, Y1 = g.oy + (J0 + byn) * g.sy;
-    const float rpv = 1.f / g.pv;
-    const int S = bc.S;
-    const bool xl = lane < 8;  // lanes 0..7: interior x planes, 8..15: interior y planes
-    const int pl = xl ? lane : lane - 8;
-    const unsigned below = (1u << lane) - 1u;
 
     for (int ia = 0; ia < nab; ++ia) {
         int iu_lo, iu_hi;
@@ -468,6 +490,8 @@ __global__ void __launch_bounds__(kAdjWarps * 32) adj_brick_kernel(
         float* o = out + ((size_t)(I0 + ci) + (size_t)g.nx * (J0 + cj)) * g.nz + K0;
         const float* a = acc + (ci + BX * cj) * CS + 1;
         for (int kk = lane; kk < bzn; kk += 32) o[kk] = accumulate ? o[kk] + a[kk] : a[kk];
+    }
+    __syncwarp();
     }
 }
 
@@ -645,6 +669,8 @@ Projector::~Projector() {
     cudaFree(d_dv_);
     cudaFree(d_invdv_);
     cudaFree(d_dvd_);
+    cudaFree(d_border_);
+    cudaFree(d_queue_);
     for (auto* p : scratch_) cudaFree(p);
     if (cur >= 0) cudaSetDevice(cur);
 }
@@ -779,10 +805,11 @@ void Projector::build_tables(const kct_geometry& geom) {
     S = std::max(S, 1);
     if (S > 64 || full_fp) adj_gather_ = true;  // degenerate geometry: use the gather kernel
     adj_S_ = S;
-    // bricks ~128 slabs tall, nz split evenly (fewer per-row z-state
-    // initialisations per ray than short bricks; measured)
+    // bricks <= 96 slabs tall, nz split evenly (c3: 3 x 86; measured against
+    // 52..192 with the brick queue: shorter bricks pay more per-row z-state
+    // initialisations per ray, taller ones cost occupancy and balance)
     {
-        const int nbz = (nz + 127) / 128;
+        const int nbz = (nz + 95) / 96;
         adj_bz_ = (nz + nbz - 1) / nbz;
     }
     if (const char* e = std::getenv("KCT_ADJ_BZ")) adj_bz_ = std::clamp(std::atoi(e), 1, kMaxBz);
@@ -798,6 +825,34 @@ void Projector::build_tables(const kct_geometry& geom) {
     const size_t smem = adj_smem_bytes();
     KCT_CUDA(cudaFuncSetAttribute(adj_brick_kernel<kAdjRows>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+
+    // brick queue: persistent grid of resident CTAs, bricks heaviest first
+    // (by xy distance of the brick centre from the rotation axis, then by z
+    // distance from the mid-plane: central bricks are crossed by the most rays)
+    const char* sched = std::getenv("KCT_ADJ_SCHED");
+    if (!adj_gather_ && !(sched && std::string(sched) == "static")) {
+        const int nbx = (nx + BX - 1) / BX, nby = (ny + BY - 1) / BY;
+        const int nbz = (nz + adj_bz_ - 1) / adj_bz_;
+        const int nb = nbx * nby * nbz;
+        std::vector<std::pair<double, int>> key(nb);
+        for (int b = 0; b < nb; ++b) {
+            const int bi = b % nbx, bj = (b / nbx) % nby, bk = b / (nbx * nby);
+            const double cx = ox + (bi + 0.5) * BX * sx, cy = oy + (bj + 0.5) * BY * sy;
+            const double cz = grid_.oz + (bk + 0.5) * adj_bz_ * sz;
+            key[b] = {std::hypot(cx, cy) + 1e-3 * std::fabs(cz), b};
+        }
+        std::stable_sort(key.begin(), key.end());
+        std::vector<int> order(nb);
+        for (int b = 0; b < nb; ++b) order[b] = key[b].second;
+        KCT_CUDA(cudaMalloc(&d_border_, nb * sizeof(int)));
+        KCT_CUDA(cudaMemcpy(d_border_, order.data(), nb * sizeof(int), cudaMemcpyHostToDevice));
+        KCT_CUDA(cudaMalloc(&d_queue_, sizeof(int)));
+        int per_sm = 0, sms = 0;
+        KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_brick_kernel<kAdjRows>,
+                                                               kAdjWarps * 32, smem));
+        KCT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+        adj_ctas_ = std::max(1, per_sm) * std::max(1, sms);
+    }
 }
 
 size_t Projector::adj_smem_bytes() const {
@@ -856,8 +911,11 @@ void Projector::adjoint(const float* proj, float* vol, cudaStream_t s) const {
             default: adj_gather_kernel<8><<<grid, 128, 0, s>>>(pr, vol, cols, d_dv_, d_invdv_, d_dvd_, dg_, ab, nab, accum); break;
             }
         } else {
-            adj_brick_kernel<kAdjRows><<<nctas, kAdjWarps * 32, smem, s>>>(
-                pr, vol, cols, d_dv_, d_invdv_, d_dvd_, dg_, bc, ab, nab, accum);
+            if (d_queue_) KCT_CUDA(cudaMemsetAsync(d_queue_, 0, sizeof(int), s));
+            adj_brick_kernel<kAdjRows><<<d_queue_ ? std::min(nctas, adj_ctas_) : nctas,
+                                         kAdjWarps * 32, smem, s>>>(
+                pr, vol, cols, d_dv_, d_invdv_, d_dvd_, dg_, bc, ab, nab, accum, d_border_,
+                d_queue_);
         }
         KCT_CUDA(cudaGetLastError());
     }

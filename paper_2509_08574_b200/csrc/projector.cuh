@@ -74,6 +74,9 @@ class Projector {
     int fwd_c_ = 4, fwd_bands_ = 1, adj_k_ = 8;
     int adj_S_ = 2, adj_bz_ = 32;
     bool adj_gather_ = false;
+    int* d_border_ = nullptr;         // brick order of the adjoint queue
+    int* d_queue_ = nullptr;          // adjoint brick queue counter
+    int adj_ctas_ = 0;                // resident CTAs of the persistent adjoint grid
     float* scratch_[4] = {nullptr, nullptr, nullptr, nullptr};
     size_t scratch_n_[4] = {0, 0, 0, 0};
 };

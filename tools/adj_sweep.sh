@@ -1,7 +1,9 @@
-for lib in build/libkct_*.so; do
-  for bz in 96 128 192 256; do
-    if [ $bz = 0 ]; then unset KCT_ADJ_BZ; else export KCT_ADJ_BZ=$bz; fi
-    r=$(KCT_LIB_PATH=$lib timeout 120 python tools/kprof.py --reps 2 2>&1 | tail -1)
+# A/B sweep of adjoint variants (tools/build_variant.sh) over brick heights.
+#   BZS="64 96 128" tools/adj_sweep.sh build/libkct_a*.so
+BZS=${BZS:-"96 128 192 256"}
+for lib in "$@"; do
+  for bz in $BZS; do
+    r=$(KCT_ADJ_BZ=$bz KCT_LIB_PATH=$lib timeout 120 python tools/kprof.py --reps 3 2>&1 | tail -1)
     echo "$lib bz=$bz $r"
   done
 done
