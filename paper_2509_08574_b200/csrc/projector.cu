@@ -223,7 +223,8 @@ struct BrickCfg {
     int bz;  // slabs per brick (<= kMaxBz)
     int S;   // row stride of a pass
     int nbx, nby, nbz;
-    int nbzc;  // CTAs in z (each covers kAdjWarps bricks)
+    int ngrp;      // angle groups: work item = (brick, group of the batch's angles)
+    size_t gstride;  // floats between the partial volumes of groups 1.. (group 0 -> out)
 };
 
 __device__ __forceinline__ float lds_f(unsigned a) {
@@ -324,7 +325,7 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
     const float* __restrict__ proj, float* __restrict__ out, const ColParams* __restrict__ cols,
     const float* __restrict__ dvtab, const float* __restrict__ invdv, const double* __restrict__ dvd,
     DevGeom g, BrickCfg bc, AngleBatch ab, int nab, int accumulate,
-    const int* __restrict__ order, int* queue) {
+    const int* __restrict__ order, int* queue, float* __restrict__ out_part) {
     extern __shared__ float sm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nbricks = bc.nbx * bc.nby * bc.nbz;
@@ -349,20 +350,30 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
     // the uneven per-brick work does not leave a partial last wave; without a
     // queue every warp takes one brick.  Each brick is still computed by one
     // warp in a fixed order: the result does not depend on the schedule.
+    // Small problems have too few bricks to fill the GPU: the angles of the
+    // batch are then split into ngrp groups, group g accumulating into its own
+    // partial volume (g = 0: `out`), summed in group order afterwards.
+    const int nitems = nbricks * bc.ngrp;
     int ticket = queue ? 0 : blockIdx.x * kAdjWarps + warp;
     for (;;) {
-    int brick;
+    int item;
     if (queue) {
         int tk = 0;
         if (lane == 0) tk = atomicAdd(queue, 1);
         tk = __shfl_sync(kFull, tk, 0);
-        if (tk >= nbricks) break;
-        brick = order[tk];
+        if (tk >= nitems) break;
+        item = tk;
     } else {
-        if (ticket >= nbricks) break;
-        brick = ticket;
-        ticket = nbricks;
+        if (ticket >= nitems) break;
+        item = ticket;
+        ticket = nitems;
     }
+    const int grp = item % bc.ngrp;
+    const int brick = queue ? order[item / bc.ngrp] : item / bc.ngrp;
+    const int a_lo = (int)((long long)nab * grp / bc.ngrp);
+    const int a_hi = (int)((long long)nab * (grp + 1) / bc.ngrp);
+    float* const dst = grp == 0 ? out : out_part + (size_t)(grp - 1) * bc.gstride;
+    const int acc_in = grp == 0 ? accumulate : 0;
     const int bi = brick % bc.nbx, bj = (brick / bc.nbx) % bc.nby, bk = brick / (bc.nbx * bc.nby);
     const int I0 = bi * BX, J0 = bj * BY, K0 = bk * BZ;
     const int bxn = min(BX, g.nx - I0), byn = min(BY, g.ny - J0), bzn = min(BZ, g.nz - K0);
@@ -373,7 +384,7 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
     const float X0 = g.ox + I0 * g.sx, X1 = g.ox + (I0 + bxn) * g.sx;
     const float Y0 = g.oy + J0 * g.sy, Y1 = g.oy + (J0 + byn) * g.sy;
 
-    for (int ia = 0; ia < nab; ++ia) {
+    for (int ia = a_lo; ia < a_hi; ++ia) {
         int iu_lo, iu_hi;
         footprint(g, ab.cs[ia].x, ab.cs[ia].y, X0, X1, Y0, Y1, iu_lo, iu_hi);
         const ColParams* colp = cols + (size_t)ia * nu;
@@ -487,9 +498,9 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
     // write the brick (coalesced runs of bzn slabs per voxel column)
     for (int c = 0; c < bxn * byn; ++c) {
         const int ci = c % bxn, cj = c / bxn;
-        float* o = out + ((size_t)(I0 + ci) + (size_t)g.nx * (J0 + cj)) * g.nz + K0;
+        float* o = dst + ((size_t)(I0 + ci) + (size_t)g.nx * (J0 + cj)) * g.nz + K0;
         const float* a = acc + (ci + BX * cj) * CS + 1;
-        for (int kk = lane; kk < bzn; kk += 32) o[kk] = accumulate ? o[kk] + a[kk] : a[kk];
+        for (int kk = lane; kk < bzn; kk += 32) o[kk] = acc_in ? o[kk] + a[kk] : a[kk];
     }
     __syncwarp();
     }
@@ -671,6 +682,7 @@ Projector::~Projector() {
     cudaFree(d_dvd_);
     cudaFree(d_border_);
     cudaFree(d_queue_);
+    cudaFree(d_part_);
     for (auto* p : scratch_) cudaFree(p);
     if (cur >= 0) cudaSetDevice(cur);
 }
@@ -826,6 +838,21 @@ void Projector::build_tables(const kct_geometry& geom) {
     KCT_CUDA(cudaFuncSetAttribute(adj_brick_kernel<kAdjRows>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 
+    // angle groups for problems with few bricks (see adj_brick_kernel); a
+    // function of the problem size only, so results do not depend on the device
+    {
+        const long nb = (long)((nx + BX - 1) / BX) * ((ny + BY - 1) / BY) * ((nz + adj_bz_ - 1) / adj_bz_);
+        const int amax = std::min(na, kMaxAnglesPerLaunch);
+        int G = (int)std::min<long>(16, (16384 + nb - 1) / nb);
+        if (const char* e = std::getenv("KCT_ADJ_GROUPS")) G = std::max(1, std::atoi(e));
+        G = std::max(1, std::min(G, amax));
+        // partial volumes: (G - 1) x M floats, capped at 2 GiB
+        while (G > 1 && (size_t)(G - 1) * m_ * sizeof(float) > (2ull << 30)) --G;
+        if (adj_gather_) G = 1;
+        adj_groups_ = G;
+        if (G > 1) KCT_CUDA(cudaMalloc(&d_part_, (size_t)(G - 1) * m_ * sizeof(float)));
+    }
+
     // brick queue: persistent grid of resident CTAs, bricks heaviest first
     // (by xy distance of the brick centre from the rotation axis, then by z
     // distance from the mid-plane: central bricks are crossed by the most rays)
@@ -860,6 +887,18 @@ size_t Projector::adj_smem_bytes() const {
            sizeof(float);
 }
 
+// out += part[0] + part[1] + ... (fixed order: deterministic)
+__global__ void __launch_bounds__(256) adj_group_sum(float* __restrict__ out,
+                                                     const float* __restrict__ part, int nparts,
+                                                     size_t m, size_t stride) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < m;
+         i += (size_t)gridDim.x * blockDim.x) {
+        float v = out[i];
+        for (int g = 0; g < nparts; ++g) v += part[(size_t)g * stride + i];
+        out[i] = v;
+    }
+}
+
 // ---- launches -----------------------------------------------------------------
 template <bool COUNT>
 static void launch_fwd(int C, int bands, const float* vol, float* out, const ColParams* cols,
@@ -892,8 +931,9 @@ void Projector::adjoint(const float* proj, float* vol, cudaStream_t s) const {
     bc.nbx = (dg_.nx + BX - 1) / BX;
     bc.nby = (dg_.ny + BY - 1) / BY;
     bc.nbz = (dg_.nz + adj_bz_ - 1) / adj_bz_;
-    bc.nbzc = 0;
-    const int nctas = (bc.nbx * bc.nby * bc.nbz + kAdjWarps - 1) / kAdjWarps;
+    bc.ngrp = adj_groups_;
+    bc.gstride = m_;
+    const int nctas = (bc.nbx * bc.nby * bc.nbz * bc.ngrp + kAdjWarps - 1) / kAdjWarps;
     const size_t smem = adj_smem_bytes();
     for (int a0 = 0; a0 < dg_.na; a0 += kMaxAnglesPerLaunch) {
         const int nab = std::min(kMaxAnglesPerLaunch, dg_.na - a0);
@@ -915,7 +955,11 @@ void Projector::adjoint(const float* proj, float* vol, cudaStream_t s) const {
             adj_brick_kernel<kAdjRows><<<d_queue_ ? std::min(nctas, adj_ctas_) : nctas,
                                          kAdjWarps * 32, smem, s>>>(
                 pr, vol, cols, d_dv_, d_invdv_, d_dvd_, dg_, bc, ab, nab, accum, d_border_,
-                d_queue_);
+                d_queue_, d_part_);
+            if (bc.ngrp > 1) {
+                KCT_CUDA(cudaGetLastError());
+                adj_group_sum<<<1184, 256, 0, s>>>(vol, d_part_, bc.ngrp - 1, m_, m_);
+            }
         }
         KCT_CUDA(cudaGetLastError());
     }

@@ -55,6 +55,7 @@ class Projector {
     int adj_stride() const { return adj_S_; }
     int adj_bz() const { return adj_bz_; }
     bool adj_gather() const { return adj_gather_; }
+    int adj_groups() const { return adj_groups_; }
 
   private:
     void build_tables(const kct_geometry& geom);
@@ -77,6 +78,8 @@ class Projector {
     int* d_border_ = nullptr;         // brick order of the adjoint queue
     int* d_queue_ = nullptr;          // adjoint brick queue counter
     int adj_ctas_ = 0;                // resident CTAs of the persistent adjoint grid
+    int adj_groups_ = 1;              // angle groups of the adjoint (small problems)
+    float* d_part_ = nullptr;         // (adj_groups_ - 1) partial volumes
     float* scratch_[4] = {nullptr, nullptr, nullptr, nullptr};
     size_t scratch_n_[4] = {0, 0, 0, 0};
 };

@@ -147,6 +147,36 @@ def test_brick_and_gather_adjoints_agree(monkeypatch, cfg, n_angles):
     assert rel_l2(brick, gather) < 2e-6
 
 
+@pytest.mark.parametrize("env", [{"KCT_ADJ_GROUPS": "1"}, {"KCT_ADJ_GROUPS": "5"},
+                                 {"KCT_ADJ_SCHED": "static"}])
+def test_adjoint_schedule_independent(monkeypatch, ora, env):
+    """Angle groups (partial volumes summed in group order) and the brick
+    queue change only the summation order: same result to rounding, each
+    schedule bit-reproducible."""
+    grid, geom = baseline_geometry(1, n_angles=64)
+    y = np.random.default_rng(4).uniform(0, 1, geom.ray_count).astype(np.float32)
+    A = projector(grid, geom)
+    base = A.apply_adjoint(y)
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    B = projector(grid, geom)
+    other = B.apply_adjoint(y)
+    assert rel_l2(other, base) < 2e-6
+    assert np.array_equal(B.apply_adjoint(y), other)
+    assert rel_l2(other, ora.adjoint(grid, geom, y)) < TOL
+
+
+def test_more_than_one_angle_batch(ora):
+    """> 1024 angles: several launches accumulate (angle batches in param space)."""
+    grid, geom = tiny_grid(6, 5, 6), tiny_geometry(1100)
+    rng = np.random.default_rng(31)
+    x = rng.uniform(0, 1, grid.count).astype(np.float32)
+    y = rng.uniform(0, 1, geom.ray_count).astype(np.float32)
+    A = projector(grid, geom)
+    assert rel_l2(A.apply(x), ora.forward(grid, geom, x)) < TOL
+    assert rel_l2(A.apply_adjoint(y), ora.adjoint(grid, geom, y)) < TOL
+
+
 def test_sharded_operators_match_full():
     """Angle-shard forward and z-slab adjoint (shard.py, the multi-GPU
     decomposition) reproduce the full operators on the CUDA path."""
