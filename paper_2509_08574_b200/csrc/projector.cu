@@ -22,6 +22,9 @@ namespace kct {
 namespace {
 
 constexpr float kInf = __builtin_huge_valf();
+#ifndef KCT_ADJ_PREWEIGHT
+#define KCT_ADJ_PREWEIGHT 1  // adjoint input pre-scaled per ray (adj_weight_kernel)
+#endif
 constexpr unsigned kFull = 0xffffffffu;
 
 // ----------------------------------------------------------------------------
@@ -265,8 +268,12 @@ __device__ __forceinline__ void row_init(RowZ& r, bool on, int iv, const ColPara
     r.k0 = k0;
     r.f0 = (float)(kzd - (double)k0);
     r.imk = __fmul_rn(invdv[iv], cp.inv_h1);
+#if KCT_ADJ_PREWEIGHT
+    r.yf = __ldg(ycol + iv);  // y * sqrt(1 + (dv inv_l)^2), adj_weight_kernel
+#else
     const float q = dv * cp.inv_l;
     r.yf = __ldg(ycol + iv) * __fsqrt_rn(__fmaf_rn(q, q, 1.f));
+#endif
     // slab at lo: last plane crossed strictly before lo (forward semantics);
     // the float estimate is corrected with the exact crossing expression
     int k = k0 + (int)floorf(r.f0 + (lo - cp.w_in) * (dv * h1));
@@ -683,6 +690,7 @@ Projector::~Projector() {
     cudaFree(d_border_);
     cudaFree(d_queue_);
     cudaFree(d_part_);
+    cudaFree(d_yw_);
     for (auto* p : scratch_) cudaFree(p);
     if (cur >= 0) cudaSetDevice(cur);
 }
@@ -853,6 +861,11 @@ void Projector::build_tables(const kct_geometry& geom) {
         if (G > 1) KCT_CUDA(cudaMalloc(&d_part_, (size_t)(G - 1) * m_ * sizeof(float)));
     }
 
+#if KCT_ADJ_PREWEIGHT
+    if (!adj_gather_)
+        KCT_CUDA(cudaMalloc(&d_yw_, (size_t)std::min(na, kMaxAnglesPerLaunch) * nu * nv * sizeof(float)));
+#endif
+
     // brick queue: persistent grid of resident CTAs, bricks heaviest first
     // (by xy distance of the brick centre from the rotation axis, then by z
     // distance from the mid-plane: central bricks are crossed by the most rays)
@@ -885,6 +898,22 @@ void Projector::build_tables(const kct_geometry& geom) {
 size_t Projector::adj_smem_bytes() const {
     return (size_t)kAdjWarps * (BX * BY * (adj_bz_ + 2) + 4 * kMaxSeg + 2 * (kMaxSeg + 2)) *
            sizeof(float);
+}
+
+// Adjoint input weighting: yw = y * sqrt(1 + (dv * inv_l)^2), the 3D length
+// factor of each ray (the forward's final scale), applied once per ray instead
+// of once per (ray, brick).  Native layout, one warp-row of 32 detector rows.
+__global__ void __launch_bounds__(256) adj_weight_kernel(const float* __restrict__ y,
+                                                         float* __restrict__ yw,
+                                                         const ColParams* __restrict__ cols,
+                                                         const float* __restrict__ dvtab, int nv,
+                                                         size_t ncols) {
+    const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    const size_t col = t / (size_t)nv;
+    if (col >= ncols) return;
+    const int iv = (int)(t - col * (size_t)nv);
+    const float q = dvtab[iv] * cols[col].inv_l;
+    yw[t] = y[t] * __fsqrt_rn(__fmaf_rn(q, q, 1.f));
 }
 
 // out += part[0] + part[1] + ... (fixed order: deterministic)
@@ -941,6 +970,15 @@ void Projector::adjoint(const float* proj, float* vol, cudaStream_t s) const {
         const int accum = a0 > 0 ? 1 : 0;
         const ColParams* cols = d_cols_ + (size_t)a0 * dg_.nu;
         const float* pr = proj + (size_t)a0 * dg_.nu * dg_.nv;
+#if KCT_ADJ_PREWEIGHT
+        if (!adj_gather_) {
+            const size_t nb = (size_t)nab * dg_.nu * dg_.nv;
+            adj_weight_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(
+                pr, d_yw_, cols, d_dv_, dg_.nv, (size_t)nab * dg_.nu);
+            KCT_CUDA(cudaGetLastError());
+            pr = d_yw_;
+        }
+#endif
         if (adj_gather_) {
             const int K = adj_k_;
             dim3 grid((dg_.nx * dg_.ny + 3) / 4, (dg_.nz + 32 * K - 1) / (32 * K), 1);

@@ -80,6 +80,7 @@ class Projector {
     int adj_ctas_ = 0;                // resident CTAs of the persistent adjoint grid
     int adj_groups_ = 1;              // angle groups of the adjoint (small problems)
     float* d_part_ = nullptr;         // (adj_groups_ - 1) partial volumes
+    float* d_yw_ = nullptr;           // length-weighted adjoint input (one angle batch)
     float* scratch_[4] = {nullptr, nullptr, nullptr, nullptr};
     size_t scratch_n_[4] = {0, 0, 0, 0};
 };
