@@ -230,6 +230,12 @@ struct BrickCfg {
     size_t gstride;  // floats between the partial volumes of groups 1.. (group 0 -> out)
 };
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 __device__ __forceinline__ float lds_f(unsigned a) {
     float v;
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
@@ -416,12 +422,15 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
             }
             if (!(lo < hi)) continue;
             // rows whose z-span over [lo, hi] meets slabs [K0, kend]
-            const float h1 = __frcp_rn(cp.inv_h1);
+            // (approximate reciprocals: h1 only feeds estimates, the row range
+            // carries a 1e-3-row margin >> their 2^-22 relative error)
+            const float h1 = rcp_approx(cp.inv_h1);
             const float gin = (float)cp.g_in;
             const float Glo = gin + (lo - cp.w_in) * h1, Ghi = gin + (hi - cp.w_in) * h1;
+            const float rGlo = rcp_approx(Glo), rGhi = rcp_approx(Ghi);
             const float n0 = (float)K0 + g.kz0, n1 = n0 + (float)bzn;
-            const float dlo = n0 >= 0.f ? __fdividef(n0, Ghi) : __fdividef(n0, Glo);
-            const float dhi = n1 >= 0.f ? __fdividef(n1, Glo) : __fdividef(n1, Ghi);
+            const float dlo = n0 * (n0 >= 0.f ? rGhi : rGlo);
+            const float dhi = n1 * (n1 >= 0.f ? rGlo : rGhi);
             const int rlo = max(0, (int)ceilf((dlo - g.dv0) * rpv - 1e-3f));
             const int rhi = min(nv - 1, (int)floorf((dhi - g.dv0) * rpv + 1e-3f));
             if (rlo > rhi) continue;
