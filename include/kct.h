@@ -105,6 +105,9 @@ typedef struct kct_projector kct_projector;
 /* ---- library ---------------------------------------------------------- */
 const char* kct_last_error(void);
 int kct_abi_version(void);
+/* Number of CUDA kernels the library has launched in this process (all
+ * handles, all devices) — lets a caller verify which work ran on the GPU. */
+unsigned long long kct_launch_count(void);
 
 /* ---- operator: ConeBeamProjector (projector.hpp:264-291) --------------- */
 /* ctor: validate grid + geometry, reject a source inside the volume

@@ -97,6 +97,7 @@ _P = C.c_void_p
 _SIGS = {
     "kct_last_error": ([], C.c_char_p),
     "kct_abi_version": ([], C.c_int),
+    "kct_launch_count": ([], C.c_ulonglong),
     "kct_projector_create": ([C.POINTER(_Grid), C.POINTER(_Geom), C.c_int, C.POINTER(_P)], C.c_int),
     "kct_projector_destroy": ([_P], C.c_int),
     "kct_projector_sizes": ([_P, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)], C.c_int),
@@ -142,6 +143,11 @@ def load_library(build: bool = True):
             fn.restype = res
         _lib = lib
     return _lib
+
+
+def launch_count() -> int:
+    """Kernels the CUDA library has launched in this process (kct_launch_count)."""
+    return int(load_library().kct_launch_count())
 
 
 def _check(rc: int) -> None:

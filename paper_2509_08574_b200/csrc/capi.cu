@@ -1,6 +1,7 @@
 // capi.cu — the C ABI (include/kct.h).  Thin: argument checks, layout and
 // host<->device staging, exception -> status-code mapping.  All compute is in
 // projector.cu / solver.cu.
+#include <atomic>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -75,6 +76,9 @@ __global__ void sum_counts_kernel(const float* __restrict__ c, size_t n, unsigne
 
 namespace kct {
 
+std::atomic<unsigned long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 // Stage an input array of `n` floats into a native-layout device buffer.
 // Returns a device pointer (either `src` itself or a scratch buffer).
 const float* stage_in(Projector& P, const float* src, size_t n, bool is_vol, int mem, int layout,
@@ -118,6 +122,8 @@ extern "C" {
 
 const char* kct_last_error(void) { return g_err.c_str(); }
 int kct_abi_version(void) { return KCT_ABI_VERSION; }
+
+unsigned long long kct_launch_count(void) { return kct::g_launches.load(std::memory_order_relaxed); }
 
 int kct_projector_create(const kct_grid* grid, const kct_geometry* geom, int device,
                          kct_projector** out) {
@@ -218,7 +224,7 @@ int kct_count_nnz(kct_projector* h, uint64_t* nnz, void* stream) {
         unsigned long long* d = reinterpret_cast<unsigned long long*>(P.scratch(3, 2));
         KCT_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), s));
         sum_counts_kernel<<<148 * 4, 256, 0, s>>>(c, P.range_size(), d);
-        KCT_CUDA(cudaGetLastError());
+        KCT_LAUNCHED();
         unsigned long long r = 0;
         KCT_CUDA(cudaMemcpyAsync(&r, d, sizeof r, cudaMemcpyDeviceToHost, s));
         KCT_CUDA(cudaStreamSynchronize(s));

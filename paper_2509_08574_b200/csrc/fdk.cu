@@ -64,43 +64,75 @@ __global__ void __launch_bounds__(256) k_fdk_filter(const float* __restrict__ pr
     }
 }
 
-// Stage 3 (fdk.hpp:88-138): one thread per voxel (native z-fastest layout, a
-// warp = 32 consecutive slabs of one voxel column), each voxel sums its own
-// angle loop (deterministic).
+// Stage 3 (fdk.hpp:88-138): a warp owns 32*KZ consecutive slabs of one voxel
+// column (native z-fastest layout), lane = slab k = kbase + lane + 32 q.  The
+// per-(column, angle) projection (u coordinate, magnification, distance
+// weight) is warp-uniform; per slab only the v coordinate changes, so the
+// detector reads of a warp are consecutive rows of one or two detector
+// columns (coalesced).  Float32 positions: |error| ~1e-5 pixel, far inside the
+// 1e-4 bar, with the bilinear interpolation continuous across pixel and
+// detector edges.  Each voxel sums its own angle loop (deterministic).
+constexpr int kFdkKZ = 4;
 __global__ void __launch_bounds__(256) k_fdk_backproject(const float* __restrict__ filt,
                                                          float* __restrict__ vol, FdkGeom f,
                                                          AngleBatch ab, int a0, int nab,
                                                          int accumulate) {
-    const size_t m = (size_t)f.nx * f.ny * f.nz;
-    const size_t vidx = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-    if (vidx >= m) return;
-    const int k = (int)(vidx % f.nz);
-    const int p = (int)(vidx / f.nz);
-    const int i = p % f.nx, j = p / f.nx;
-    const double x = f.ox + (i + 0.5) * f.sx, y = f.oy + (j + 0.5) * f.sy;
-    const double z = f.oz + (k + 0.5) * f.sz;
-    float acc = 0.f;
-    for (int q = 0; q < nab; ++q) {
-        const double c = ab.cs[q].x, s = ab.cs[q].y;
-        const double ss = x * c + y * s, t = -x * s + y * c;
-        const double L = f.dso - ss;
-        if (L <= 1e-6 * f.dso) continue;
-        const double fu = (t * f.dso / L - f.u0) / f.du;
-        const double fv = (z * f.dso / L - f.v0) / f.dv;
-        const int ju = (int)floor(fu), jv = (int)floor(fv);
-        if (ju < -1 || ju > f.nu - 1 || jv < -1 || jv > f.nv - 1) continue;
-        const float au = (float)(fu - ju), av = (float)(fv - jv);
-        const float* fa = filt + (size_t)(a0 + q) * f.nu * f.nv;
-        auto sample = [&](int uu, int vv) -> float {
-            return (uu < 0 || uu >= f.nu || vv < 0 || vv >= f.nv) ? 0.f
-                                                                   : __ldg(fa + (size_t)uu * f.nv + vv);
-        };
-        const float val = (1.f - au) * (1.f - av) * sample(ju, jv) + au * (1.f - av) * sample(ju + 1, jv) +
-                          (1.f - au) * av * sample(ju, jv + 1) + au * av * sample(ju + 1, jv + 1);
-        acc = fmaf((float)((f.dso * f.dso) / (L * L)), val, acc);
+    const int lane = threadIdx.x & 31;
+    const size_t wid = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+    const int kchunks = (f.nz + 32 * kFdkKZ - 1) / (32 * kFdkKZ);
+    const size_t col = wid / kchunks;
+    if (col >= (size_t)f.nx * f.ny) return;
+    const int kbase = (int)(wid - col * kchunks) * 32 * kFdkKZ + lane;
+    const int i = (int)(col % f.nx), j = (int)(col / f.nx);
+    const float x = (float)(f.ox + (i + 0.5) * f.sx), y = (float)(f.oy + (j + 0.5) * f.sy);
+    const float dso = (float)f.dso;
+    const float inv_du = (float)(1.0 / f.du), inv_dv = (float)(1.0 / f.dv);
+    const float u0 = (float)f.u0, v0 = (float)f.v0;
+    float zq[kFdkKZ], acc[kFdkKZ];
+#pragma unroll
+    for (int q = 0; q < kFdkKZ; ++q) {
+        zq[q] = (float)(f.oz + (kbase + 32 * q + 0.5) * f.sz);
+        acc[q] = 0.f;
     }
-    const float r = f.scale * acc;
-    vol[vidx] = accumulate ? vol[vidx] + r : r;
+    for (int a = 0; a < nab; ++a) {
+        const float c = ab.cs[a].x, s = ab.cs[a].y;
+        const float ss = fmaf(x, c, y * s), t = fmaf(-x, s, y * c);
+        const float L = dso - ss;
+        if (!(L > 1e-6f * dso)) continue;
+        const float mag = __fdiv_rn(dso, L);
+        const float fu = (t * mag - u0) * inv_du;
+        const int ju = (int)floorf(fu);
+        if (ju < -1 || ju > f.nu - 1) continue;
+        const float au = fu - (float)ju;
+        const float wgt = mag * mag;
+        const float* fa = filt + (size_t)(a0 + a) * f.nu * f.nv;
+        const float* c0 = ju >= 0 ? fa + (size_t)ju * f.nv : nullptr;
+        const float* c1 = ju + 1 < f.nu ? fa + (size_t)(ju + 1) * f.nv : nullptr;
+#pragma unroll
+        for (int q = 0; q < kFdkKZ; ++q) {
+            const float fv = (zq[q] * mag - v0) * inv_dv;
+            const int jv = (int)floorf(fv);
+            if (jv < -1 || jv > f.nv - 1) continue;
+            const float av = fv - (float)jv;
+            const bool r0 = jv >= 0, r1 = jv + 1 < f.nv;
+            const float s00 = (c0 && r0) ? __ldg(c0 + jv) : 0.f;
+            const float s01 = (c0 && r1) ? __ldg(c0 + jv + 1) : 0.f;
+            const float s10 = (c1 && r0) ? __ldg(c1 + jv) : 0.f;
+            const float s11 = (c1 && r1) ? __ldg(c1 + jv + 1) : 0.f;
+            const float val = (1.f - au) * ((1.f - av) * s00 + av * s01) +
+                              au * ((1.f - av) * s10 + av * s11);
+            acc[q] = fmaf(wgt, val, acc[q]);
+        }
+    }
+    float* o = vol + col * f.nz;
+#pragma unroll
+    for (int q = 0; q < kFdkKZ; ++q) {
+        const int k = kbase + 32 * q;
+        if (k < f.nz) {
+            const float r = f.scale * acc[q];
+            o[k] = accumulate ? o[k] + r : r;
+        }
+    }
 }
 
 }  // namespace
@@ -123,15 +155,15 @@ void Projector::fdk(const float* proj, float* vol, float* filt, cudaStream_t s) 
     KCT_CUDA(cudaFuncSetAttribute(k_fdk_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 g1((f.nv + 31) / 32, f.na);
     k_fdk_filter<<<g1, 256, smem, s>>>(proj, filt, f);
-    KCT_CUDA(cudaGetLastError());
+    KCT_LAUNCHED();
     AngleBatch ab;
-    const size_t m = domain_size();
-    const unsigned blocks = (unsigned)((m + 255) / 256);
+    const size_t warps = (size_t)f.nx * f.ny * ((f.nz + 32 * kFdkKZ - 1) / (32 * kFdkKZ));
+    const unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
     for (int a0 = 0; a0 < f.na; a0 += kMaxAnglesPerLaunch) {
         const int nab = std::min(kMaxAnglesPerLaunch, f.na - a0);
         for (int q = 0; q < nab; ++q) ab.cs[q] = cs_[a0 + q];
         k_fdk_backproject<<<blocks, 256, 0, s>>>(filt, vol, f, ab, a0, nab, a0 > 0 ? 1 : 0);
-        KCT_CUDA(cudaGetLastError());
+        KCT_LAUNCHED();
     }
 }
 

@@ -38,6 +38,15 @@ struct CudaError : std::runtime_error {
             throw ::kct::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
+// Every kernel launch of the library is counted (kct_launch_count): evidence
+// of which work ran on the device, read by bench.py around its timed region.
+void note_launch();
+#define KCT_LAUNCHED()                          \
+    do {                                        \
+        ::kct::note_launch();                   \
+        KCT_CUDA(cudaGetLastError());           \
+    } while (0)
+
 // Per (angle, detector column) parameters of the shared xy ray path, computed
 // on the host in double and stored as float.  w is the signed xy distance
 // along the column's unit direction, measured from the foot point R of the

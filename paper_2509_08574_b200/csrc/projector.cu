@@ -641,7 +641,7 @@ __global__ void transpose_kernel(const float* __restrict__ in, float* __restrict
 void launch_transpose(const float* in, float* out, int B, int R, int Cc, cudaStream_t s) {
     dim3 grid((Cc + 31) / 32, (R + 31) / 32, B);
     transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(in, out, R, Cc);
-    KCT_CUDA(cudaGetLastError());
+    KCT_LAUNCHED();
 }
 
 }  // namespace
@@ -950,7 +950,7 @@ static void launch_fwd(int C, int bands, const float* vol, float* out, const Col
     case 3: fwd_kernel<3, COUNT><<<grid, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, g); break;
     default: fwd_kernel<4, COUNT><<<grid, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, g); break;
     }
-    KCT_CUDA(cudaGetLastError());
+    KCT_LAUNCHED();
 }
 
 void Projector::forward(const float* vol, float* proj, cudaStream_t s) const {
@@ -984,7 +984,7 @@ void Projector::adjoint(const float* proj, float* vol, cudaStream_t s) const {
             const size_t nb = (size_t)nab * dg_.nu * dg_.nv;
             adj_weight_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(
                 pr, d_yw_, cols, d_dv_, dg_.nv, (size_t)nab * dg_.nu);
-            KCT_CUDA(cudaGetLastError());
+            KCT_LAUNCHED();
             pr = d_yw_;
         }
 #endif
@@ -1004,11 +1004,11 @@ void Projector::adjoint(const float* proj, float* vol, cudaStream_t s) const {
                 pr, vol, cols, d_dv_, d_invdv_, d_dvd_, dg_, bc, ab, nab, accum, d_border_,
                 d_queue_, d_part_);
             if (bc.ngrp > 1) {
-                KCT_CUDA(cudaGetLastError());
+                KCT_LAUNCHED();
                 adj_group_sum<<<1184, 256, 0, s>>>(vol, d_part_, bc.ngrp - 1, m_, m_);
             }
         }
-        KCT_CUDA(cudaGetLastError());
+        KCT_LAUNCHED();
     }
 }
 

@@ -467,13 +467,13 @@ void launch_scalar(Workspace& w, int mode, cudaStream_t s, double tol = 0.0,
                    double* res = nullptr, double* err = nullptr, double* obj = nullptr,
                    int kind = 0) {
     k_scalar<<<1, kBlock, 0, s>>>(w.ctl, w.part, mode, tol, res, err, obj, kind);
-    KCT_CUDA(cudaGetLastError());
+    KCT_LAUNCHED();
 }
 
 #define KCT_LAUNCH(kernel, ...)                                \
     do {                                                       \
         kernel<<<kGrid, kBlock, 0, stream>>>(__VA_ARGS__);     \
-        KCT_CUDA(cudaGetLastError());                          \
+        KCT_LAUNCHED();                          \
     } while (0)
 
 
@@ -515,7 +515,7 @@ struct Engine {
     void reduce_slot(int slot) {
         if (!P.comm_fn) return;
         k_fold<<<1, kBlock, 0, stream>>>(w.part, slot);
-        KCT_CUDA(cudaGetLastError());
+        KCT_LAUNCHED();
         if (P.comm_fn(P.comm_ctx, w.part + slot * kGrid, 1, 1, stream) != 0)
             throw CudaError("allreduce hook failed (scalar)");
     }
@@ -554,7 +554,7 @@ struct Engine {
             // ||A~^T b~||^2, the tolerance reference of a warm start (krylov.hpp:81-88)
             KCT_LAUNCH(k_stats, w.x, w.m, w.part);
             k_set_nonzero<<<1, kBlock, 0, stream>>>(w.ctl, w.part);
-            KCT_CUDA(cudaGetLastError());
+            KCT_LAUNCHED();
             adjoint(w.b, w.p);
             KCT_LAUNCH(k_reggrad, w.p, nullptr, w.prior, w.w1, w.w2, w.p, rc, w.part);
             launch_scalar(w, S_REF, stream);
@@ -630,7 +630,7 @@ double device_tau(Workspace& w, const float* ref, size_t n, double tau, cudaStre
     if (!ref || n == 0) return 1e-4;
     KCT_LAUNCH(k_stats, ref, n, w.part);
     k_minmax_final<<<1, kBlock, 0, stream>>>(w.part, w.scal);
-    KCT_CUDA(cudaGetLastError());
+    KCT_LAUNCHED();
     double mm[2];
     KCT_CUDA(cudaMemcpyAsync(mm, w.scal, sizeof mm, cudaMemcpyDeviceToHost, stream));
     KCT_CUDA(cudaStreamSynchronize(stream));

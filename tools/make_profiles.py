@@ -39,7 +39,7 @@ def launches(tag, path):
     tot = sum(sum(v) for v in agg.values())
     lines = [f"# ncu launch list ({tag}): gpu__time_duration.sum, --clock-control none,",
              "# cold-cache serialised launches of `bench.py --steps 2 --warmup 3 --skip-recon",
-             "# --skip-cpu --skip-e2e` (shares, not absolutes, are comparable to the bench)",
+             "# --skip-cpu --skip-e2e --skip-fdk` (shares, not absolutes, are comparable to the bench)",
              f"{'kernel':70s} {'n':>4s} {'total_ms':>10s} {'mean_ms':>9s} {'share':>6s}"]
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"{k[:70]:70s} {len(v):4d} {sum(v):10.3f} {sum(v) / len(v):9.3f} "
