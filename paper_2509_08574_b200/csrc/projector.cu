@@ -330,15 +330,212 @@ __device__ __forceinline__ void row_segment(RowZ& r, const Seg& sg, unsigned col
     }
 }
 
+// ---- the xy part of one (brick, detector column): chord, row range, walk ----
+// Fills bnd[0..nseg] (segment boundaries, shared memory) and, for lanes
+// < nseg, the segment's voxel column `ij` = (i - I0) + BX (j - J0).  Returns
+// nseg, 0 when the column's rays miss the brick.  Used on the fly by the
+// adjoint and by the walk-table builder (bit-identical entries).
+struct BrickGeo {
+    int I0, J0, K0, bxn, byn, bzn;
+};
+
+__device__ __forceinline__ int brick_walk(const ColParams& cp, const DevGeom& g, const BrickGeo& B,
+                                          int lane, float* bnd, int* axis, float& lo_out,
+                                          int& rlo_out, int& rhi_out, int& ij_out) {
+    const int I0 = B.I0, J0 = B.J0, bxn = B.bxn, byn = B.byn;
+    // chord of the column's xy line through the brick
+    float lo = cp.w_in, hi = cp.w_out;
+    if (cp.dx != 0.0) {
+        const float e0 = xcross(cp, I0), e1 = xcross(cp, I0 + bxn);
+        lo = fmaxf(lo, fminf(e0, e1));
+        hi = fminf(hi, fmaxf(e0, e1));
+    } else if (cp.i0 < I0 || cp.i0 >= I0 + bxn) {
+        return 0;
+    }
+    if (cp.dy != 0.0) {
+        const float e0 = ycross(cp, J0), e1 = ycross(cp, J0 + byn);
+        lo = fmaxf(lo, fminf(e0, e1));
+        hi = fminf(hi, fmaxf(e0, e1));
+    } else if (cp.j0 < J0 || cp.j0 >= J0 + byn) {
+        return 0;
+    }
+    if (!(lo < hi)) return 0;
+    // rows whose z-span over [lo, hi] meets slabs [K0, K0 + bzn]
+    // (approximate reciprocals: the row range carries a 1e-3-row margin >>
+    // their 2^-22 relative error)
+    const float h1 = rcp_approx(cp.inv_h1);
+    const float gin = (float)cp.g_in;
+    const float Glo = gin + (lo - cp.w_in) * h1, Ghi = gin + (hi - cp.w_in) * h1;
+    const float rGlo = rcp_approx(Glo), rGhi = rcp_approx(Ghi);
+    const float n0 = (float)B.K0 + g.kz0, n1 = n0 + (float)B.bzn;
+    const float dlo = n0 * (n0 >= 0.f ? rGhi : rGlo);
+    const float dhi = n1 * (n1 >= 0.f ? rGlo : rGhi);
+    const float rpv = 1.f / g.pv;
+    const int rlo = max(0, (int)ceilf((dlo - g.dv0) * rpv - 1e-3f));
+    const int rhi = min(g.nv - 1, (int)floorf((dhi - g.dv0) * rpv + 1e-3f));
+    if (rlo > rhi) return 0;
+
+    // lane-parallel walk: lanes 0..7 take the interior x planes, 8..15 the y planes
+    const bool xl = lane < 8;
+    const int pl = xl ? lane : lane - 8;
+    const unsigned below = (1u << lane) - 1u;
+    float v = kInf;
+    bool has = false;
+    if (xl && pl < bxn - 1 && cp.dx != 0.0) {
+        v = xcross(cp, I0 + 1 + pl);
+        has = true;
+    } else if (!xl && lane < 16 && pl < byn - 1 && cp.dy != 0.0) {
+        v = ycross(cp, J0 + 1 + pl);
+        has = true;
+    }
+    const unsigned mbefore = __ballot_sync(kFull, has && v <= lo);
+    const bool valid = has && v > lo && v < hi;
+    const unsigned mval = __ballot_sync(kFull, valid);
+    const int cbx = __popc(mbefore & 0xffu), cby = __popc(mbefore & 0xff00u);
+    const int stx = cp.dx > 0.0 ? 1 : -1, sty = cp.dy > 0.0 ? 1 : -1;
+    const int ie = cp.dx == 0.0 ? cp.i0 : (stx > 0 ? I0 + cbx : I0 + bxn - 1 - cbx);
+    const int je = cp.dy == 0.0 ? cp.j0 : (sty > 0 ? J0 + cby : J0 + byn - 1 - cby);
+    // rank along the ray: own-axis predecessors (plane order) + other-axis
+    // crossings before it (x first at ties, as the forward's walk)
+    const unsigned own = xl ? (mval & 0xffu) : (mval & 0xff00u);
+    int rank = (xl ? stx : sty) > 0 ? __popc(own & below) : __popc(own & ~below & ~(1u << lane));
+    const unsigned other = xl ? (mval >> 8) & 0xffu : mval & 0xffu;
+#pragma unroll
+    for (int t = 0; t < (BX > BY ? BX : BY) - 1; ++t) {
+        const float ov = __shfl_sync(kFull, v, xl ? 8 + t : t);
+        rank += (((other >> t) & 1u) && (xl ? ov < v : ov <= v)) ? 1 : 0;
+    }
+    const int nval = __popc(mval);
+    if (valid) {
+        bnd[rank + 1] = v;
+        axis[rank] = xl ? 1 : 0;
+    }
+    if (lane == 0) {
+        bnd[0] = lo;
+        bnd[nval + 1] = hi;
+    }
+    __syncwarp();
+    const unsigned mx = __ballot_sync(kFull, lane < nval && axis[lane]);
+    const int nxb = __popc(mx & below);
+    ij_out = (ie + stx * nxb - I0) + BX * (je + sty * (lane - nxb) - J0);
+    lo_out = lo;
+    rlo_out = rlo;
+    rhi_out = rhi;
+    return nval + 1;
+}
+
+// ---- the rows of one (brick, detector column): C per lane, passes of stride S ----
+template <int C>
+__device__ __forceinline__ void brick_rows(const Seg* segs, int nseg, const ColParams& cp, float lo,
+                                           int rlo, int rhi, int S, int K0, int kend, int lane,
+                                           const float* __restrict__ dvtab,
+                                           const float* __restrict__ invdv,
+                                           const double* __restrict__ dvd,
+                                           const float* __restrict__ ycol, const DevGeom& g) {
+    const float h1 = rcp_approx(cp.inv_h1);
+    for (int p = 0; p < S; ++p) {
+        for (int base = rlo + p; base <= rhi; base += 32 * S * C) {
+            RowZ r[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const int iv = base + S * (lane + 32 * c);
+                row_init(r[c], iv <= rhi, iv, cp, lo, h1, K0, kend, dvtab, invdv, dvd, ycol, g);
+            }
+            for (int sgi = 0; sgi < nseg; ++sgi) {
+                const Seg sg = segs[sgi];
+#pragma unroll
+                for (int c = 0; c < C; ++c) row_segment(r[c], sg, (unsigned)sg.ij, K0, kend, cp.w_in);
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// ---- walk table: the xy part of every (brick, angle, column), built once per
+// projector (geometry-only) and streamed by the adjoint instead of recomputed
+// for every application.  64 bytes per entry. ----
+struct __align__(16) WalkEntry {
+    float bnd[8];            // segment boundaries, lo = bnd[0] .. hi = bnd[nseg]
+    unsigned char ij[8];     // per segment: (i - I0) + BX (j - J0)
+    unsigned short ia, iu;   // angle (global index), detector column
+    unsigned short rlo, rhi; // detector rows crossing the brick
+    int nseg;
+    int pad[3];
+};
+static_assert(sizeof(WalkEntry) == 64, "WalkEntry layout");
+constexpr int kTabMaxSeg = 8;
+constexpr bool kTabOk = BX + BY - 1 <= kTabMaxSeg && BX * BY <= 256;
+
+__device__ __forceinline__ BrickGeo brick_geo(int brick, const BrickCfg& bc, const DevGeom& g) {
+    const int bi = brick % bc.nbx, bj = (brick / bc.nbx) % bc.nby, bk = brick / (bc.nbx * bc.nby);
+    BrickGeo B;
+    B.I0 = bi * BX;
+    B.J0 = bj * BY;
+    B.K0 = bk * bc.bz;
+    B.bxn = min(BX, g.nx - B.I0);
+    B.byn = min(BY, g.ny - B.J0);
+    B.bzn = min(bc.bz, g.nz - B.K0);
+    return B;
+}
+
+// FILL = false: count entries per (brick, angle) into off[b (na + 1) + a];
+// FILL = true: write them from off[] (exclusive prefix sums).  One warp per brick.
+template <bool FILL>
+__global__ void __launch_bounds__(128) adj_walk_build(const ColParams* __restrict__ cols,
+                                                      const float2* __restrict__ cs, DevGeom g,
+                                                      BrickCfg bc,
+                                                      unsigned long long* __restrict__ off,
+                                                      WalkEntry* __restrict__ tab) {
+    __shared__ float sbnd[4][kMaxSeg + 2];
+    __shared__ int saxis[4][kMaxSeg + 2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int brick = blockIdx.x * 4 + warp;
+    if (brick >= bc.nbx * bc.nby * bc.nbz) return;
+    const BrickGeo B = brick_geo(brick, bc, g);
+    const float X0 = g.ox + B.I0 * g.sx, X1 = g.ox + (B.I0 + B.bxn) * g.sx;
+    const float Y0 = g.oy + B.J0 * g.sy, Y1 = g.oy + (B.J0 + B.byn) * g.sy;
+    unsigned long long* ob = off + (size_t)brick * (g.na + 1);
+    for (int ia = 0; ia < g.na; ++ia) {
+        int iu_lo, iu_hi;
+        footprint(g, cs[ia].x, cs[ia].y, X0, X1, Y0, Y1, iu_lo, iu_hi);
+        unsigned long long e = FILL ? ob[ia] : 0ull;
+        for (int iu = iu_lo; iu <= iu_hi; ++iu) {
+            const ColParams cp = cols[(size_t)ia * g.nu + iu];
+            float lo;
+            int rlo, rhi, ij;
+            const int nseg = brick_walk(cp, g, B, lane, sbnd[warp], saxis[warp], lo, rlo, rhi, ij);
+            if (nseg == 0) continue;
+            if (FILL) {
+                WalkEntry* E = tab + e;
+                if (lane <= nseg) E->bnd[lane] = sbnd[warp][lane];
+                if (lane < nseg) E->ij[lane] = (unsigned char)ij;
+                if (lane == 0) {
+                    E->ia = (unsigned short)ia;
+                    E->iu = (unsigned short)iu;
+                    E->rlo = (unsigned short)rlo;
+                    E->rhi = (unsigned short)rhi;
+                    E->nseg = nseg;
+                }
+            }
+            ++e;
+            __syncwarp();
+        }
+        if (!FILL && lane == 0) ob[ia] = e;
+    }
+}
+
 #ifndef KCT_ADJ_MINB
 #define KCT_ADJ_MINB 6  // caps registers at ~64: 8 CTAs of 4 warps per SM (measured)
 #endif
-template <int C>
+// TAB: the xy walks come from the walk table (tab, off) instead of being
+// recomputed; identical values either way.
+template <int C, bool TAB>
 __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel(
     const float* __restrict__ proj, float* __restrict__ out, const ColParams* __restrict__ cols,
     const float* __restrict__ dvtab, const float* __restrict__ invdv, const double* __restrict__ dvd,
-    DevGeom g, BrickCfg bc, AngleBatch ab, int nab, int accumulate,
-    const int* __restrict__ order, int* queue, float* __restrict__ out_part) {
+    DevGeom g, BrickCfg bc, AngleBatch ab, int a0, int nab, int accumulate,
+    const int* __restrict__ order, int* queue, float* __restrict__ out_part,
+    const WalkEntry* __restrict__ tab, const unsigned long long* __restrict__ off) {
     extern __shared__ float sm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nbricks = bc.nbx * bc.nby * bc.nbz;
@@ -353,10 +550,6 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
     float* bnd = acc + BX * BY * CS + 4 * kMaxSeg;
     int* axis = reinterpret_cast<int*>(bnd + kMaxSeg + 2);
     const unsigned acc_s = (unsigned)__cvta_generic_to_shared(acc);
-    const bool xl = lane < 8;  // lanes 0..7: interior x planes, 8..15: interior y planes
-    const int pl = xl ? lane : lane - 8;
-    const unsigned below = (1u << lane) - 1u;
-    const float rpv = 1.f / g.pv;
     const int S = bc.S;
 
     // Bricks are handed out to warps by a queue (heaviest first, `order`), so
@@ -387,136 +580,77 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
     const int a_hi = (int)((long long)nab * (grp + 1) / bc.ngrp);
     float* const dst = grp == 0 ? out : out_part + (size_t)(grp - 1) * bc.gstride;
     const int acc_in = grp == 0 ? accumulate : 0;
-    const int bi = brick % bc.nbx, bj = (brick / bc.nbx) % bc.nby, bk = brick / (bc.nbx * bc.nby);
-    const int I0 = bi * BX, J0 = bj * BY, K0 = bk * BZ;
-    const int bxn = min(BX, g.nx - I0), byn = min(BY, g.ny - J0), bzn = min(BZ, g.nz - K0);
-    const int kend = K0 + bzn;
+    const BrickGeo B = brick_geo(brick, bc, g);
+    const int K0 = B.K0, kend = B.K0 + B.bzn;
     for (int q = lane; q < BX * BY * CS; q += 32) acc[q] = 0.f;
     __syncwarp();
+    // byte address of slab 0 of voxel column ij (so that slab k sits at + 4k)
+    const unsigned seg_base = acc_s + 4u * (unsigned)(1 - K0);
 
-    const float X0 = g.ox + I0 * g.sx, X1 = g.ox + (I0 + bxn) * g.sx;
-    const float Y0 = g.oy + J0 * g.sy, Y1 = g.oy + (J0 + byn) * g.sy;
-
-    for (int ia = a_lo; ia < a_hi; ++ia) {
-        int iu_lo, iu_hi;
-        footprint(g, ab.cs[ia].x, ab.cs[ia].y, X0, X1, Y0, Y1, iu_lo, iu_hi);
-        const ColParams* colp = cols + (size_t)ia * nu;
-        const float* yb = proj + (size_t)ia * nu * nv;
-        for (int iu = iu_lo; iu <= iu_hi; ++iu) {
-            const ColParams cp = colp[iu];
-            // chord of the column's xy line through the brick
-            float lo = cp.w_in, hi = cp.w_out;
-            if (cp.dx != 0.0) {
-                const float e0 = xcross(cp, I0), e1 = xcross(cp, I0 + bxn);
-                lo = fmaxf(lo, fminf(e0, e1));
-                hi = fminf(hi, fmaxf(e0, e1));
-            } else if (cp.i0 < I0 || cp.i0 >= I0 + bxn) {
-                continue;
-            }
-            if (cp.dy != 0.0) {
-                const float e0 = ycross(cp, J0), e1 = ycross(cp, J0 + byn);
-                lo = fmaxf(lo, fminf(e0, e1));
-                hi = fminf(hi, fmaxf(e0, e1));
-            } else if (cp.j0 < J0 || cp.j0 >= J0 + byn) {
-                continue;
-            }
-            if (!(lo < hi)) continue;
-            // rows whose z-span over [lo, hi] meets slabs [K0, kend]
-            // (approximate reciprocals: h1 only feeds estimates, the row range
-            // carries a 1e-3-row margin >> their 2^-22 relative error)
-            const float h1 = rcp_approx(cp.inv_h1);
-            const float gin = (float)cp.g_in;
-            const float Glo = gin + (lo - cp.w_in) * h1, Ghi = gin + (hi - cp.w_in) * h1;
-            const float rGlo = rcp_approx(Glo), rGhi = rcp_approx(Ghi);
-            const float n0 = (float)K0 + g.kz0, n1 = n0 + (float)bzn;
-            const float dlo = n0 * (n0 >= 0.f ? rGhi : rGlo);
-            const float dhi = n1 * (n1 >= 0.f ? rGlo : rGhi);
-            const int rlo = max(0, (int)ceilf((dlo - g.dv0) * rpv - 1e-3f));
-            const int rhi = min(nv - 1, (int)floorf((dhi - g.dv0) * rpv + 1e-3f));
-            if (rlo > rhi) continue;
-
-            // ---- lane-parallel xy walk through the brick ----
-            float v = kInf;
-            bool has = false;
-            if (xl && pl < bxn - 1 && cp.dx != 0.0) {
-                v = xcross(cp, I0 + 1 + pl);
-                has = true;
-            } else if (!xl && lane < 16 && pl < byn - 1 && cp.dy != 0.0) {
-                v = ycross(cp, J0 + 1 + pl);
-                has = true;
-            }
-            const unsigned mbefore = __ballot_sync(kFull, has && v <= lo);
-            const bool valid = has && v > lo && v < hi;
-            const unsigned mval = __ballot_sync(kFull, valid);
-            const int cbx = __popc(mbefore & 0xffu), cby = __popc(mbefore & 0xff00u);
-            const int stx = cp.dx > 0.0 ? 1 : -1, sty = cp.dy > 0.0 ? 1 : -1;
-            const int ie = cp.dx == 0.0 ? cp.i0 : (stx > 0 ? I0 + cbx : I0 + bxn - 1 - cbx);
-            const int je = cp.dy == 0.0 ? cp.j0 : (sty > 0 ? J0 + cby : J0 + byn - 1 - cby);
-            // rank along the ray: own-axis predecessors (plane order) + other-axis
-            // crossings before it (x first at ties, as the forward's walk)
-            const unsigned own = xl ? (mval & 0xffu) : (mval & 0xff00u);
-            int rank = (xl ? stx : sty) > 0 ? __popc(own & below)
-                                            : __popc(own & ~below & ~(1u << lane));
-            const unsigned other = xl ? (mval >> 8) & 0xffu : mval & 0xffu;
-#pragma unroll
-            for (int t = 0; t < (BX > BY ? BX : BY) - 1; ++t) {
-                const float ov = __shfl_sync(kFull, v, xl ? 8 + t : t);
-                rank += (((other >> t) & 1u) && (xl ? ov < v : ov <= v)) ? 1 : 0;
-            }
-            const int nval = __popc(mval);
-            const int nseg = nval + 1;
-            if (valid) {
-                bnd[rank + 1] = v;
-                axis[rank] = xl ? 1 : 0;
-            }
-            if (lane == 0) {
-                bnd[0] = lo;
-                bnd[nval + 1] = hi;
-            }
-            __syncwarp();
-            const unsigned mx = __ballot_sync(kFull, lane < nval && axis[lane]);
+    if (TAB) {
+        const unsigned long long* ob = off + (size_t)brick * (g.na + 1);
+        const unsigned long long e0 = ob[a0 + a_lo], e1 = ob[a0 + a_hi];
+        const unsigned* tw = reinterpret_cast<const unsigned*>(tab);
+        for (unsigned long long e = e0; e < e1; ++e) {
+            // lanes 0..15 fetch the 64-byte entry, shuffles distribute it
+            const unsigned w = lane < 16 ? __ldg(tw + e * 16 + lane) : 0u;
+            const int nseg = (int)__shfl_sync(kFull, w, 12);
+            const unsigned aiu = __shfl_sync(kFull, w, 10), rr = __shfl_sync(kFull, w, 11);
+            const float wa = __uint_as_float(__shfl_sync(kFull, w, lane & 7));
+            const float wb = __uint_as_float(__shfl_sync(kFull, w, (lane + 1) & 7));
+            const unsigned ijw = __shfl_sync(kFull, w, 8 + ((lane >> 2) & 1));
+            const float lo = __uint_as_float(__shfl_sync(kFull, w, 0));
             if (lane < nseg) {
-                const int nxb = __popc(mx & below);
-                const int i = ie + stx * nxb, j = je + sty * (lane - nxb);
+                const unsigned ij = (ijw >> (8 * (lane & 3))) & 0xffu;
                 Seg sg;
-                sg.wa = bnd[lane];
-                sg.wb = bnd[lane + 1];
-                // byte address of slab 0 (so that slab k sits at + 4k)
-                sg.ij = (int)(acc_s + 4u * (unsigned)(((i - I0) + BX * (j - J0)) * CS + 1 - K0));
+                sg.wa = wa;
+                sg.wb = wb;
+                sg.ij = (int)(seg_base + 4u * ij * (unsigned)CS);
                 sg.pad = 0;
                 segs[lane] = sg;
             }
             __syncwarp();
-
-            // ---- rows: C per lane, passes of stride S ----
-            const float* ycol = yb + (size_t)iu * nv;
-            for (int p = 0; p < S; ++p) {
-                for (int base = rlo + p; base <= rhi; base += 32 * S * C) {
-                    RowZ r[C];
-#pragma unroll
-                    for (int c = 0; c < C; ++c) {
-                        const int iv = base + S * (lane + 32 * c);
-                        row_init(r[c], iv <= rhi, iv, cp, lo, h1, K0, kend, dvtab, invdv, dvd,
-                                 ycol, g);
-                    }
-                    for (int sgi = 0; sgi < nseg; ++sgi) {
-                        const Seg sg = segs[sgi];
-#pragma unroll
-                        for (int c = 0; c < C; ++c)
-                            row_segment(r[c], sg, (unsigned)sg.ij, K0, kend, cp.w_in);
-                    }
-                    __syncwarp();
-                }
-            }
+            const size_t cidx = (size_t)((int)(aiu & 0xffffu) - a0) * nu + (aiu >> 16);
+            const ColParams cp = cols[cidx];
+            brick_rows<C>(segs, nseg, cp, lo, (int)(rr & 0xffffu), (int)(rr >> 16), S, K0, kend,
+                          lane, dvtab, invdv, dvd, proj + cidx * nv, g);
             __syncwarp();
+        }
+    } else {
+        const float X0 = g.ox + B.I0 * g.sx, X1 = g.ox + (B.I0 + B.bxn) * g.sx;
+        const float Y0 = g.oy + B.J0 * g.sy, Y1 = g.oy + (B.J0 + B.byn) * g.sy;
+        for (int ia = a_lo; ia < a_hi; ++ia) {
+            int iu_lo, iu_hi;
+            footprint(g, ab.cs[ia].x, ab.cs[ia].y, X0, X1, Y0, Y1, iu_lo, iu_hi);
+            const ColParams* colp = cols + (size_t)ia * nu;
+            const float* yb = proj + (size_t)ia * nu * nv;
+            for (int iu = iu_lo; iu <= iu_hi; ++iu) {
+                const ColParams cp = colp[iu];
+                float lo;
+                int rlo, rhi, ij;
+                const int nseg = brick_walk(cp, g, B, lane, bnd, axis, lo, rlo, rhi, ij);
+                if (nseg == 0) continue;
+                if (lane < nseg) {
+                    Seg sg;
+                    sg.wa = bnd[lane];
+                    sg.wb = bnd[lane + 1];
+                    sg.ij = (int)(seg_base + 4u * (unsigned)(ij * CS));
+                    sg.pad = 0;
+                    segs[lane] = sg;
+                }
+                __syncwarp();
+                brick_rows<C>(segs, nseg, cp, lo, rlo, rhi, S, K0, kend, lane, dvtab, invdv, dvd,
+                              yb + (size_t)iu * nv, g);
+                __syncwarp();
+            }
         }
     }
     // write the brick (coalesced runs of bzn slabs per voxel column)
-    for (int c = 0; c < bxn * byn; ++c) {
-        const int ci = c % bxn, cj = c / bxn;
-        float* o = dst + ((size_t)(I0 + ci) + (size_t)g.nx * (J0 + cj)) * g.nz + K0;
+    for (int c = 0; c < B.bxn * B.byn; ++c) {
+        const int ci = c % B.bxn, cj = c / B.bxn;
+        float* o = dst + ((size_t)(B.I0 + ci) + (size_t)g.nx * (B.J0 + cj)) * g.nz + K0;
         const float* a = acc + (ci + BX * cj) * CS + 1;
-        for (int kk = lane; kk < bzn; kk += 32) o[kk] = acc_in ? o[kk] + a[kk] : a[kk];
+        for (int kk = lane; kk < B.bzn; kk += 32) o[kk] = acc_in ? o[kk] + a[kk] : a[kk];
     }
     __syncwarp();
     }
@@ -700,6 +834,8 @@ Projector::~Projector() {
     cudaFree(d_queue_);
     cudaFree(d_part_);
     cudaFree(d_yw_);
+    cudaFree(d_tab_);
+    cudaFree(d_off_);
     for (auto* p : scratch_) cudaFree(p);
     if (cur >= 0) cudaSetDevice(cur);
 }
@@ -852,7 +988,9 @@ void Projector::build_tables(const kct_geometry& geom) {
     KCT_CUDA(cudaMalloc(&d_dvd_, nv * sizeof(double)));
     KCT_CUDA(cudaMemcpy(d_dvd_, dvd.data(), nv * sizeof(double), cudaMemcpyHostToDevice));
     const size_t smem = adj_smem_bytes();
-    KCT_CUDA(cudaFuncSetAttribute(adj_brick_kernel<kAdjRows>,
+    KCT_CUDA(cudaFuncSetAttribute(adj_brick_kernel<kAdjRows, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    KCT_CUDA(cudaFuncSetAttribute(adj_brick_kernel<kAdjRows, true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 
     // angle groups for problems with few bricks (see adj_brick_kernel); a
@@ -897,11 +1035,69 @@ void Projector::build_tables(const kct_geometry& geom) {
         KCT_CUDA(cudaMemcpy(d_border_, order.data(), nb * sizeof(int), cudaMemcpyHostToDevice));
         KCT_CUDA(cudaMalloc(&d_queue_, sizeof(int)));
         int per_sm = 0, sms = 0;
-        KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_brick_kernel<kAdjRows>,
+        KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_brick_kernel<kAdjRows, true>,
                                                                kAdjWarps * 32, smem));
         KCT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
         adj_ctas_ = std::max(1, per_sm) * std::max(1, sms);
     }
+
+    build_walk_table();
+}
+
+// Walk table (adj_walk_build): the xy part of every (brick, angle, column) of
+// the adjoint, 64 bytes each, built once per projector.  Skipped (the adjoint
+// then recomputes the walks) when disabled (KCT_ADJ_TABLE=0), when an index
+// does not fit the entry, or above the memory budget (KCT_ADJ_TABLE_MB,
+// default 8192).
+void Projector::build_walk_table() {
+    const char* en = std::getenv("KCT_ADJ_TABLE");
+    if (adj_gather_ || !kTabOk || (en && std::string(en) == "0")) return;
+    if (dg_.na > 65535 || dg_.nu > 65535 || dg_.nv > 65535) return;
+    size_t budget = 8192ull << 20;
+    if (const char* e = std::getenv("KCT_ADJ_TABLE_MB")) budget = (size_t)std::atoll(e) << 20;
+    BrickCfg bc{};
+    bc.bz = adj_bz_;
+    bc.S = adj_S_;
+    bc.nbx = (dg_.nx + BX - 1) / BX;
+    bc.nby = (dg_.ny + BY - 1) / BY;
+    bc.nbz = (dg_.nz + adj_bz_ - 1) / adj_bz_;
+    bc.ngrp = 1;
+    const size_t nb = (size_t)bc.nbx * bc.nby * bc.nbz;
+    const size_t noff = nb * (dg_.na + 1);
+    float2* d_cs = nullptr;
+    KCT_CUDA(cudaMalloc(&d_cs, cs_.size() * sizeof(float2)));
+    KCT_CUDA(cudaMemcpy(d_cs, cs_.data(), cs_.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    KCT_CUDA(cudaMalloc(&d_off_, noff * sizeof(unsigned long long)));
+    const unsigned blocks = (unsigned)((nb + 3) / 4);
+    adj_walk_build<false><<<blocks, 128>>>(d_cols_, d_cs, dg_, bc, d_off_, nullptr);
+    KCT_LAUNCHED();
+    std::vector<unsigned long long> off(noff);
+    KCT_CUDA(cudaMemcpy(off.data(), d_off_, noff * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    // per brick: counts per angle -> exclusive prefix over (brick, angle)
+    unsigned long long tot = 0;
+    for (size_t b = 0; b < nb; ++b) {
+        unsigned long long* ob = off.data() + b * (dg_.na + 1);
+        for (int a = 0; a < dg_.na; ++a) {
+            const unsigned long long c = ob[a];
+            ob[a] = tot;
+            tot += c;
+        }
+        ob[dg_.na] = tot;
+    }
+    if (tot == 0 || tot * sizeof(WalkEntry) > budget) {
+        cudaFree(d_cs);
+        cudaFree(d_off_);
+        d_off_ = nullptr;
+        return;
+    }
+    KCT_CUDA(cudaMemcpy(d_off_, off.data(), noff * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    KCT_CUDA(cudaMalloc(&d_tab_, tot * sizeof(WalkEntry)));
+    adj_walk_build<true><<<blocks, 128>>>(d_cols_, d_cs, dg_, bc, d_off_,
+                                          static_cast<WalkEntry*>(d_tab_));
+    KCT_LAUNCHED();
+    KCT_CUDA(cudaDeviceSynchronize());
+    cudaFree(d_cs);
+    tab_entries_ = tot;
 }
 
 size_t Projector::adj_smem_bytes() const {
@@ -999,10 +1195,15 @@ void Projector::adjoint(const float* proj, float* vol, cudaStream_t s) const {
             }
         } else {
             if (d_queue_) KCT_CUDA(cudaMemsetAsync(d_queue_, 0, sizeof(int), s));
-            adj_brick_kernel<kAdjRows><<<d_queue_ ? std::min(nctas, adj_ctas_) : nctas,
-                                         kAdjWarps * 32, smem, s>>>(
-                pr, vol, cols, d_dv_, d_invdv_, d_dvd_, dg_, bc, ab, nab, accum, d_border_,
-                d_queue_, d_part_);
+            const unsigned grid = d_queue_ ? std::min(nctas, adj_ctas_) : nctas;
+            if (d_tab_)
+                adj_brick_kernel<kAdjRows, true><<<grid, kAdjWarps * 32, smem, s>>>(
+                    pr, vol, cols, d_dv_, d_invdv_, d_dvd_, dg_, bc, ab, a0, nab, accum, d_border_,
+                    d_queue_, d_part_, static_cast<const WalkEntry*>(d_tab_), d_off_);
+            else
+                adj_brick_kernel<kAdjRows, false><<<grid, kAdjWarps * 32, smem, s>>>(
+                    pr, vol, cols, d_dv_, d_invdv_, d_dvd_, dg_, bc, ab, a0, nab, accum, d_border_,
+                    d_queue_, d_part_, nullptr, nullptr);
             if (bc.ngrp > 1) {
                 KCT_LAUNCHED();
                 adj_group_sum<<<1184, 256, 0, s>>>(vol, d_part_, bc.ngrp - 1, m_, m_);

@@ -56,10 +56,12 @@ class Projector {
     int adj_bz() const { return adj_bz_; }
     bool adj_gather() const { return adj_gather_; }
     int adj_groups() const { return adj_groups_; }
+    unsigned long long walk_entries() const { return tab_entries_; }
 
   private:
     void build_tables(const kct_geometry& geom);
     size_t adj_smem_bytes() const;
+    void build_walk_table();
 
     kct_grid grid_;
     DevGeom dg_{};
@@ -81,6 +83,9 @@ class Projector {
     int adj_groups_ = 1;              // angle groups of the adjoint (small problems)
     float* d_part_ = nullptr;         // (adj_groups_ - 1) partial volumes
     float* d_yw_ = nullptr;           // length-weighted adjoint input (one angle batch)
+    void* d_tab_ = nullptr;           // adjoint walk table (WalkEntry, projector.cu)
+    unsigned long long* d_off_ = nullptr;  // walk-table offsets [brick][angle + 1]
+    unsigned long long tab_entries_ = 0;
     float* scratch_[4] = {nullptr, nullptr, nullptr, nullptr};
     size_t scratch_n_[4] = {0, 0, 0, 0};
 };
