@@ -22,6 +22,9 @@ namespace kct {
 namespace {
 
 constexpr float kInf = __builtin_huge_valf();
+#ifndef KCT_ROW_VERIFY
+#define KCT_ROW_VERIFY 1  // adjoint row z-state: verify the estimate, search only on failure
+#endif
 #ifndef KCT_ADJ_PREWEIGHT
 #define KCT_ADJ_PREWEIGHT 1  // adjoint input pre-scaled per ray (adj_weight_kernel)
 #endif
@@ -283,6 +286,28 @@ __device__ __forceinline__ void row_init(RowZ& r, bool on, int iv, const ColPara
     // slab at lo: last plane crossed strictly before lo (forward semantics);
     // the float estimate is corrected with the exact crossing expression
     int k = k0 + (int)floorf(r.f0 + (lo - cp.w_in) * (dv * h1));
+#if KCT_ROW_VERIFY
+    // Sign-generic fast path: the estimate is right unless z(lo) sits within
+    // rounding of a plane; verify it with the two bounding planes (the next
+    // one is also the first crossing) and search only when that fails.
+    if (dv != 0.f) {
+        const int sg = dv > 0.f ? 1 : -1;
+        k = sg > 0 ? max(k, k0) : min(k, k0);
+        const int pn = sg > 0 ? k + 1 : k;      // next plane
+        const int pp = sg > 0 ? k : k + 1;      // plane crossed entering slab k
+        const float zn = zcross(pn, k0, r.f0, r.imk, cp.w_in);
+        const float zp = k != k0 ? zcross(pp, k0, r.f0, r.imk, cp.w_in) : -kInf;
+        if (zp < lo && !(zn < lo)) {
+            r.kstep = sg;
+            const int kc = sg > 0 ? max(k, K0 - 1) : min(k, kend);
+            const int pc = sg > 0 ? kc + 1 : kc;
+            r.wz = (pc >= K0 && pc <= kend) ? (kc == k ? zn : zcross(pc, k0, r.f0, r.imk, cp.w_in))
+                                            : kInf;
+            r.k = min(max(kc, K0 - 1), kend);
+            return;
+        }
+    }
+#endif
     if (dv > 0.f) {
         r.kstep = 1;
         k = max(k, k0);
