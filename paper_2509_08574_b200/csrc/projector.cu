@@ -1013,10 +1013,14 @@ void Projector::build_tables(const kct_geometry& geom) {
     KCT_CUDA(cudaMalloc(&d_dvd_, nv * sizeof(double)));
     KCT_CUDA(cudaMemcpy(d_dvd_, dvd.data(), nv * sizeof(double), cudaMemcpyHostToDevice));
     const size_t smem = adj_smem_bytes();
+    // the attribute is per function, not per handle: set it to the largest
+    // brick any projector can use, so handles with taller bricks coexist
+    const int smem_max = (int)((size_t)kAdjWarps *
+                               (BX * BY * (kMaxBz + 2) + 4 * kMaxSeg + 2 * (kMaxSeg + 2)) * sizeof(float));
     KCT_CUDA(cudaFuncSetAttribute(adj_brick_kernel<kAdjRows, false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
     KCT_CUDA(cudaFuncSetAttribute(adj_brick_kernel<kAdjRows, true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
 
     // angle groups for problems with few bricks (see adj_brick_kernel); a
     // function of the problem size only, so results do not depend on the device

@@ -3,10 +3,13 @@
 Rays are independent in A x (projector.hpp:192-193) and voxels are
 independent in the voxel-owned A^T y, so the operator pair shards without any
 reduction: rank r projects the angle subset r::world of the full volume, and
-backprojects its z-slab of the volume from all angles.  Slab
-boundaries are z-planes, so the slab grid's Siddon segments are exactly the
-full grid's segments inside the slab: the slab adjoint equals the slab of the
-full adjoint.  These helpers are pure host logic (tested on CPU with gloo);
+backprojects its slab of the volume from all angles.  Slab
+boundaries are grid planes, so the slab grid's Siddon segments are the full
+grid's segments inside the slab: the slab adjoint equals the slab of the full
+adjoint (to float rounding of the re-based plane coefficients).  Slabs can be
+cut along z (contiguous in the reference layout) or y (contiguous in the
+native z-fastest layout, and the brick adjoint keeps full-height bricks: the
+bench's choice, tools/shard_time.py).  These helpers are pure host logic (tested on CPU with gloo);
 the CUDA operators are built per rank from the returned geometry / grid.
 """
 from __future__ import annotations
@@ -24,7 +27,8 @@ def angle_indices(n_angles: int, world: int, rank: int) -> np.ndarray:
 
 
 def slab_range(nz: int, world: int, rank: int) -> tuple[int, int]:
-    """[z0, z1) slab of `rank` (balanced, contiguous, covers 0..nz)."""
+    """[z0, z1) slab of `rank` along an axis of nz planes (balanced,
+    contiguous, covers 0..nz)."""
     if not 0 <= rank < world:
         raise ValueError("rank out of range")
     base, extra = divmod(nz, world)
@@ -38,9 +42,15 @@ def shard_geometry(geom: ConeBeamGeometry, world: int, rank: int) -> ConeBeamGeo
                             geom.angles[idx], geom.offset_u, geom.offset_v)
 
 
-def slab_grid(grid: GridSpec, world: int, rank: int) -> GridSpec:
-    z0, z1 = slab_range(grid.dims[2], world, rank)
-    if z1 <= z0:
+def slab_grid(grid: GridSpec, world: int, rank: int, axis: str = "z") -> GridSpec:
+    """The grid of `rank`'s slab along `axis` ("z": contiguous in the
+    reference layout; "y": contiguous in the native z-fastest layout)."""
+    ax = {"x": 0, "y": 1, "z": 2}[axis]
+    a0, a1 = slab_range(grid.dims[ax], world, rank)
+    if a1 <= a0:
         raise ValueError("more ranks than slabs")
-    return GridSpec((grid.dims[0], grid.dims[1], z1 - z0), grid.spacing,
-                    (grid.origin[0], grid.origin[1], grid.origin[2] + z0 * grid.spacing[2]))
+    dims = list(grid.dims)
+    origin = list(grid.origin)
+    dims[ax] = a1 - a0
+    origin[ax] = grid.origin[ax] + a0 * grid.spacing[ax]
+    return GridSpec(tuple(dims), grid.spacing, tuple(origin))

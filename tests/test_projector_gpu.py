@@ -166,6 +166,19 @@ def test_adjoint_schedule_independent(monkeypatch, ora, env):
     assert rel_l2(other, ora.adjoint(grid, geom, y)) < TOL
 
 
+def test_handles_with_different_bricks_coexist(ora):
+    """Kernel attributes are per function: a handle created later with shorter
+    bricks must not break an earlier handle with taller ones."""
+    from tests._util import Grid
+    geom = tiny_geometry(4, nu=12, nv=40)
+    tall, short = Grid(8, 8, 192, 0.5, 0.5, 0.25), Grid(8, 8, 16, 0.5, 0.5, 0.25)
+    A = projector(tall, geom)
+    B = projector(short, geom)
+    y = np.random.default_rng(5).uniform(0, 1, geom.ray_count).astype(np.float32)
+    assert rel_l2(A.apply_adjoint(y), ora.adjoint(tall, geom, y)) < TOL
+    assert rel_l2(B.apply_adjoint(y), ora.adjoint(short, geom, y)) < TOL
+
+
 def test_more_than_one_angle_batch(ora):
     """> 1024 angles: several launches accumulate (angle batches in param space)."""
     grid, geom = tiny_grid(6, 5, 6), tiny_geometry(1100)
@@ -178,7 +191,7 @@ def test_more_than_one_angle_batch(ora):
 
 
 def test_sharded_operators_match_full():
-    """Angle-shard forward and z-slab adjoint (shard.py, the multi-GPU
+    """Angle-shard forward and z- / y-slab adjoints (shard.py, the multi-GPU
     decomposition) reproduce the full operators on the CUDA path."""
     from paper_2509_08574_b200 import shard
     grid, geom = baseline_geometry(1, n_angles=12)
@@ -197,3 +210,7 @@ def test_sharded_operators_match_full():
             z0, z1 = shard.slab_range(grid.nz, world, r)
             blk = k.ConeBeamProjector(shard.slab_grid(gs, world, r), ge).apply_adjoint(y)
             assert rel_l2(blk, adj[z0:z1]) < 1e-6
+            y0, y1 = shard.slab_range(grid.ny, world, r)
+            blk = k.ConeBeamProjector(shard.slab_grid(gs, world, r, axis="y"), ge).apply_adjoint(y)
+            ref = adj.reshape(grid.nz, grid.ny, grid.nx)[:, y0:y1, :]
+            assert rel_l2(blk, ref) < 1e-6

@@ -105,3 +105,9 @@ def test_decomposition_is_exact_float64():
         z0, z1 = shard.slab_range(grid.nz, world, r)
         blk = ora.adjoint(osl, geom, y).reshape(z1 - z0, -1)
         np.testing.assert_allclose(blk, full_adj[z0:z1], rtol=1e-12, atol=1e-12)
+        sl = shard.slab_grid(kg, world, r, axis="y")
+        osl = Grid(*sl.dims, *sl.spacing, *sl.origin)
+        y0, y1 = shard.slab_range(grid.ny, world, r)
+        blk = ora.adjoint(osl, geom, y).reshape(grid.nz, y1 - y0, grid.nx)
+        ref = full_adj.reshape(grid.nz, grid.ny, grid.nx)[:, y0:y1, :]
+        np.testing.assert_allclose(blk, ref, rtol=1e-12, atol=1e-12)
