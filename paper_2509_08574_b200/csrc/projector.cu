@@ -51,13 +51,20 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
                                                   const ColParams* __restrict__ cols,
                                                   const float* __restrict__ dvtab,
                                                   const float* __restrict__ invdv,
-                                                  const double* __restrict__ dvd, DevGeom g) {
+                                                  const double* __restrict__ dvd, DevGeom g,
+                                                  const int* __restrict__ order) {
+    // blocks are dispatched in index order; `order` maps them to (angle, row
+    // band, column quad) items longest-chord first, so the last wave holds
+    // the shortest rays (no long tail, notably with few angles per GPU)
+    const int nq = (g.nu + kFwdWarps - 1) / kFwdWarps;
+    const int item = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
+    const int quad = item % nq, rest = item / nq;
+    const int band = rest % g.fwd_bands, a = rest / g.fwd_bands;
     const int lane = threadIdx.x & 31;
-    const int iu = blockIdx.x * kFwdWarps + (threadIdx.x >> 5);
-    const int a = blockIdx.z;
+    const int iu = quad * kFwdWarps + (threadIdx.x >> 5);
     if (iu >= g.nu) return;
     const ColParams cp = cols[(size_t)a * g.nu + iu];
-    const int iv0 = blockIdx.y * (32 * C) + lane;
+    const int iv0 = band * (32 * C) + lane;
     const int nz = g.nz;
 
     // per ray: slab k, next crossing wz of plane P (kept as pk = P - k0),
@@ -856,6 +863,7 @@ Projector::~Projector() {
     cudaFree(d_invdv_);
     cudaFree(d_dvd_);
     cudaFree(d_border_);
+    cudaFree(d_forder_);
     cudaFree(d_queue_);
     cudaFree(d_part_);
     cudaFree(d_yw_);
@@ -983,6 +991,31 @@ void Projector::build_tables(const kct_geometry& geom) {
     if (const char* e = std::getenv("KCT_FWD_C")) cmax = std::clamp(std::atoi(e), 1, 4);
     fwd_bands_ = (chunks + cmax - 1) / cmax;
     fwd_c_ = (chunks + fwd_bands_ - 1) / fwd_bands_;
+    dg_.fwd_bands = fwd_bands_;
+    // forward block order: (angle, band, column quad) items by decreasing
+    // xy chord of the quad (ray length ~ work), stable
+    {
+        const int nq = (nu + kFwdWarps - 1) / kFwdWarps;
+        const size_t nitems = (size_t)nq * fwd_bands_ * na;
+        std::vector<std::pair<float, int>> key(nitems);
+        for (size_t t = 0; t < nitems; ++t) {
+            const int quad = (int)(t % nq), a = (int)(t / ((size_t)nq * fwd_bands_));
+            float len = 0.f;
+            for (int w = 0; w < kFwdWarps && quad * kFwdWarps + w < nu; ++w) {
+                const ColParams& cp = cols[(size_t)a * nu + quad * kFwdWarps + w];
+                len += std::max(0.f, cp.w_out - cp.w_in);
+            }
+            key[t] = {-len, (int)t};
+        }
+        std::stable_sort(key.begin(), key.end());
+        std::vector<int> order(nitems);
+        for (size_t t = 0; t < nitems; ++t) order[t] = key[t].second;
+        const char* fo = std::getenv("KCT_FWD_ORDER");
+        if (!(fo && std::string(fo) == "0")) {
+            KCT_CUDA(cudaMalloc(&d_forder_, nitems * sizeof(int)));
+            KCT_CUDA(cudaMemcpy(d_forder_, order.data(), nitems * sizeof(int), cudaMemcpyHostToDevice));
+        }
+    }
     const int kc = (nz + 31) / 32;
     adj_k_ = kc <= 1 ? 1 : kc <= 2 ? 2 : kc <= 4 ? 4 : 8;
 
@@ -1166,24 +1199,30 @@ __global__ void __launch_bounds__(256) adj_group_sum(float* __restrict__ out,
 template <bool COUNT>
 static void launch_fwd(int C, int bands, const float* vol, float* out, const ColParams* cols,
                        const float* dv, const float* invdv, const double* dvd, const DevGeom& g,
-                       cudaStream_t s) {
-    dim3 grid((g.nu + kFwdWarps - 1) / kFwdWarps, bands, g.na);
+                       const int* order, cudaStream_t s) {
+    // 1D grid over (angle, band, column quad) items
+    const unsigned nq = (unsigned)((g.nu + kFwdWarps - 1) / kFwdWarps);
+    const dim3 g1(nq * (unsigned)bands * (unsigned)g.na, 1, 1);
     const int th = kFwdWarps * 32;
+    DevGeom gg = g;
+    gg.fwd_bands = bands;
     switch (C) {
-    case 1: fwd_kernel<1, COUNT><<<grid, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, g); break;
-    case 2: fwd_kernel<2, COUNT><<<grid, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, g); break;
-    case 3: fwd_kernel<3, COUNT><<<grid, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, g); break;
-    default: fwd_kernel<4, COUNT><<<grid, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, g); break;
+    case 1: fwd_kernel<1, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order); break;
+    case 2: fwd_kernel<2, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order); break;
+    case 3: fwd_kernel<3, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order); break;
+    default: fwd_kernel<4, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order); break;
     }
     KCT_LAUNCHED();
 }
 
 void Projector::forward(const float* vol, float* proj, cudaStream_t s) const {
-    launch_fwd<false>(fwd_c_, fwd_bands_, vol, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_, s);
+    launch_fwd<false>(fwd_c_, fwd_bands_, vol, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_,
+                      d_forder_, s);
 }
 
 void Projector::count(float* proj, cudaStream_t s) const {
-    launch_fwd<true>(fwd_c_, fwd_bands_, nullptr, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_, s);
+    launch_fwd<true>(fwd_c_, fwd_bands_, nullptr, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_,
+                     d_forder_, s);
 }
 
 void Projector::adjoint(const float* proj, float* vol, cudaStream_t s) const {

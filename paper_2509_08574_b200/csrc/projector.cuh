@@ -78,6 +78,7 @@ class Projector {
     int adj_S_ = 2, adj_bz_ = 32;
     bool adj_gather_ = false;
     int* d_border_ = nullptr;         // brick order of the adjoint queue
+    int* d_forder_ = nullptr;         // forward block -> item order (longest chords first)
     int* d_queue_ = nullptr;          // adjoint brick queue counter
     int adj_ctas_ = 0;                // resident CTAs of the persistent adjoint grid
     int adj_groups_ = 1;              // angle groups of the adjoint (small problems)
