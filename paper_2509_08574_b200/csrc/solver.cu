@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -189,6 +190,239 @@ __global__ void __launch_bounds__(kBlock) k_reggrad(const float* __restrict__ sA
         ts += (double)sv * (double)sv;
     }
     write_partials(part, 0, ts, sm);
+    write_partials(part, 1, t1, sm);
+    write_partials(part, 2, t2, sm);
+}
+
+// ---- float4 versions of the three stencil kernels (nz % 4 == 0) ----------
+// A lane owns 4 consecutive slabs of one voxel column (one float4); the k-1 /
+// k+4 neighbours come from the adjacent lanes by shuffle (lanes 0 / 31 load
+// them), the i / j neighbours are float4 loads — 4x fewer load instructions
+// and all of a lane's loads independent, so the (L2 / DRAM latency bound)
+// scalar kernels become bandwidth bound.  Same arithmetic per voxel as the
+// scalar kernels; the partial sums add the 4 voxels of a lane in k order.
+struct Nb4 {
+    float f[6];           // f[0] = slab k-1, f[1..4] = slabs k..k+3, f[5] = slab k+4
+    float4 ip, im, jp, jm;  // columns i+1, i-1, j+1, j-1 (0 outside the grid)
+};
+
+__device__ __forceinline__ float4 ld4(const float* __restrict__ f, size_t v) {
+    return __ldg(reinterpret_cast<const float4*>(f + v));
+}
+__device__ __forceinline__ float q4(const float4& a, int q) {
+    return q == 0 ? a.x : (q == 1 ? a.y : (q == 2 ? a.z : a.w));
+}
+
+// All lanes must call (shuffles); `ok` false lanes pass v = 0 and get zeros.
+template <bool MINUS_I, bool MINUS_J>
+__device__ __forceinline__ void load_nb(const float* __restrict__ f, size_t v, int k, int i, int j,
+                                        const RegCfg& c, bool ok, int lane, Nb4& n) {
+    const size_t si = c.nz, sj = (size_t)c.nz * c.nx;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 a = (ok && f) ? ld4(f, v) : z4;
+    n.f[1] = a.x; n.f[2] = a.y; n.f[3] = a.z; n.f[4] = a.w;
+    const float up = __shfl_up_sync(0xffffffffu, a.w, 1);
+    const float dn = __shfl_down_sync(0xffffffffu, a.x, 1);
+    n.f[0] = (ok && f && k > 0) ? (lane > 0 ? up : f[v - 1]) : 0.f;
+    n.f[5] = (ok && f && k + 4 < c.nz) ? (lane < 31 ? dn : f[v + 4]) : 0.f;
+    n.ip = (ok && f && i + 1 < c.nx) ? ld4(f, v + si) : z4;
+    n.jp = (ok && f && j + 1 < c.ny) ? ld4(f, v + sj) : z4;
+    n.im = (MINUS_I && ok && f && i > 0) ? ld4(f, v - si) : z4;
+    n.jm = (MINUS_J && ok && f && j > 0) ? ld4(f, v - sj) : z4;
+}
+
+__device__ __forceinline__ void decode4(size_t base, int lane, size_t m4, const RegCfg& c, bool& ok,
+                                        size_t& v, int& k, int& i, int& j) {
+    const size_t e = base + lane;
+    ok = e < m4;
+    v = ok ? 4 * e : 0;
+    decode(v, c, k, i, j);
+}
+
+__global__ void __launch_bounds__(kBlock) k_weights4(const float* __restrict__ x,
+                                                     const float* __restrict__ xp,
+                                                     float* __restrict__ w1, float* __restrict__ w2,
+                                                     RegCfg c, int write_w, double* part) {
+    __shared__ double sm[32];
+    const int lane = threadIdx.x & 31;
+    const size_t m4 = (size_t)c.nx * c.ny * c.nz / 4, stride = (size_t)gridDim.x * blockDim.x;
+    double t1 = 0.0, t2 = 0.0;
+    for (size_t base = blockIdx.x * (size_t)blockDim.x + (threadIdx.x & ~31u); base < m4;
+         base += stride) {
+        bool ok;
+        size_t v;
+        int k, i, j;
+        decode4(base, lane, m4, c, ok, v, k, i, j);
+        Nb4 X, P;
+        load_nb<false, false>(x, v, k, i, j, c, ok, lane, X);
+        if (c.mode2) load_nb<false, false>(xp, v, k, i, j, c, ok, lane, P);
+        float o1[4], o2[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float xv = X.f[q + 1];
+            if (c.use_w1) {
+                const float gx = i + 1 < c.nx ? q4(X.ip, q) - xv : 0.f;
+                const float gy = j + 1 < c.ny ? q4(X.jp, q) - xv : 0.f;
+                const float gz = k + q + 1 < c.nz ? X.f[q + 2] - xv : 0.f;
+                const float r = sqrtf(gx * gx + gy * gy + gz * gz + c.tau2);
+                if (ok) t1 += (double)r;
+                o1[q] = 1.f / sqrtf(r);
+            }
+            if (c.mode2 == 1) {
+                const float dv = xv - P.f[q + 1];
+                const float gx = i + 1 < c.nx ? (q4(X.ip, q) - q4(P.ip, q)) - dv : 0.f;
+                const float gy = j + 1 < c.ny ? (q4(X.jp, q) - q4(P.jp, q)) - dv : 0.f;
+                const float gz = k + q + 1 < c.nz ? (X.f[q + 2] - P.f[q + 2]) - dv : 0.f;
+                const float r = sqrtf(gx * gx + gy * gy + gz * gz + c.tau2);
+                if (ok) t2 += (double)r;
+                o2[q] = 1.f / sqrtf(r);
+            } else if (c.mode2 == 2) {
+                const double d = (double)xv - (double)P.f[q + 1];
+                if (ok) t2 += d * d;
+            }
+        }
+        if (ok && write_w) {
+            if (c.use_w1) *reinterpret_cast<float4*>(w1 + v) = make_float4(o1[0], o1[1], o1[2], o1[3]);
+            if (c.mode2 == 1) *reinterpret_cast<float4*>(w2 + v) = make_float4(o2[0], o2[1], o2[2], o2[3]);
+        }
+    }
+    write_partials(part, 1, t1, sm);
+    write_partials(part, 2, t2, sm);
+}
+
+// D^T W^2 D f at the 4 voxels of a lane, from f's and w's neighbourhoods
+__device__ __forceinline__ void dtwd(const Nb4& F, const Nb4& W, int k, int i, int j,
+                                     const RegCfg& c, float g[4], float g2[4]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const float fv = F.f[q + 1];
+        const float gx = i + 1 < c.nx ? q4(F.ip, q) - fv : 0.f;
+        const float gy = j + 1 < c.ny ? q4(F.jp, q) - fv : 0.f;
+        const float gz = k + q + 1 < c.nz ? F.f[q + 2] - fv : 0.f;
+        const float wv = W.f[q + 1], wv2 = wv * wv;
+        float t = -wv2 * (gx + gy + gz);
+        if (i > 0) { const float w = q4(W.im, q); t += w * w * (fv - q4(F.im, q)); }
+        if (j > 0) { const float w = q4(W.jm, q); t += w * w * (fv - q4(F.jm, q)); }
+        if (k + q > 0) { const float w = W.f[q]; t += w * w * (fv - F.f[q]); }
+        g[q] = t;
+        g2[q] = wv2 * (gx * gx + gy * gy + gz * gz);
+    }
+}
+
+__device__ __forceinline__ void nb_sub(Nb4& a, const Nb4& b) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) a.f[q] -= b.f[q];
+    a.ip.x -= b.ip.x; a.ip.y -= b.ip.y; a.ip.z -= b.ip.z; a.ip.w -= b.ip.w;
+    a.im.x -= b.im.x; a.im.y -= b.im.y; a.im.z -= b.im.z; a.im.w -= b.im.w;
+    a.jp.x -= b.jp.x; a.jp.y -= b.jp.y; a.jp.z -= b.jp.z; a.jp.w -= b.jp.w;
+    a.jm.x -= b.jm.x; a.jm.y -= b.jm.y; a.jm.z -= b.jm.z; a.jm.w -= b.jm.w;
+}
+
+__global__ void __launch_bounds__(kBlock) k_reggrad4(const float* __restrict__ sA,
+                                                     const float* __restrict__ x,
+                                                     const float* __restrict__ xp,
+                                                     const float* __restrict__ w1,
+                                                     const float* __restrict__ w2,
+                                                     float* __restrict__ s, RegCfg c, double* part) {
+    __shared__ double sm[32];
+    const int lane = threadIdx.x & 31;
+    const size_t m4 = (size_t)c.nx * c.ny * c.nz / 4, stride = (size_t)gridDim.x * blockDim.x;
+    double ts = 0.0, t1 = 0.0, t2 = 0.0;
+    for (size_t base = blockIdx.x * (size_t)blockDim.x + (threadIdx.x & ~31u); base < m4;
+         base += stride) {
+        bool ok;
+        size_t v;
+        int k, i, j;
+        decode4(base, lane, m4, c, ok, v, k, i, j);
+        const float4 a = ok ? ld4(sA, v) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float sv[4] = {a.x, a.y, a.z, a.w};
+        float g[4], gg[4];
+        Nb4 X, W;
+        if (c.use_w1 && x) {
+            load_nb<true, true>(x, v, k, i, j, c, ok, lane, X);
+            load_nb<true, true>(w1, v, k, i, j, c, ok, lane, W);
+            dtwd(X, W, k, i, j, c, g, gg);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                sv[q] -= c.alpha2 * g[q];
+                if (ok) t1 += (double)gg[q];
+            }
+        }
+        if (c.mode2 == 1) {
+            Nb4 D, P;
+            load_nb<true, true>(x, v, k, i, j, c, ok, lane, D);  // x == nullptr -> zeros
+            load_nb<true, true>(xp, v, k, i, j, c, ok, lane, P);
+            nb_sub(D, P);
+            load_nb<true, true>(w2, v, k, i, j, c, ok, lane, W);
+            dtwd(D, W, k, i, j, c, g, gg);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                sv[q] -= c.lambda2 * g[q];
+                if (ok) t2 += (double)gg[q];
+            }
+        } else if (c.mode2 == 2) {
+            const float4 xv = (ok && x) ? ld4(x, v) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 pv = ok ? ld4(xp, v) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float dv = q4(xv, q) - q4(pv, q);
+                sv[q] -= c.lambda2 * dv;
+                if (ok) t2 += (double)dv * (double)dv;
+            }
+        }
+        if (ok) {
+            *reinterpret_cast<float4*>(s + v) = make_float4(sv[0], sv[1], sv[2], sv[3]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) ts += (double)sv[q] * (double)sv[q];
+        }
+    }
+    write_partials(part, 0, ts, sm);
+    write_partials(part, 1, t1, sm);
+    write_partials(part, 2, t2, sm);
+}
+
+__global__ void __launch_bounds__(kBlock) k_normq4(const float* __restrict__ q, size_t n,
+                                                   const float* __restrict__ p,
+                                                   const float* __restrict__ w1,
+                                                   const float* __restrict__ w2, RegCfg c,
+                                                   const Ctl* ctl, double* part) {
+    if (ctl->stop) return;
+    __shared__ double sm[32];
+    const int lane = threadIdx.x & 31;
+    double tq = 0.0, t1 = 0.0, t2 = 0.0;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n; v += stride) {
+        const double qv = q[v];
+        tq += qv * qv;
+    }
+    if (c.use_w1 || c.mode2) {
+        const size_t m4 = (size_t)c.nx * c.ny * c.nz / 4;
+        for (size_t base = blockIdx.x * (size_t)blockDim.x + (threadIdx.x & ~31u); base < m4;
+             base += stride) {
+            bool ok;
+            size_t v;
+            int k, i, j;
+            decode4(base, lane, m4, c, ok, v, k, i, j);
+            Nb4 Pn;
+            load_nb<false, false>(p, v, k, i, j, c, ok, lane, Pn);
+            const float4 a1 = (ok && c.use_w1) ? ld4(w1, v) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 a2 = (ok && c.mode2 == 1) ? ld4(w2, v) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                const float pv = Pn.f[qq + 1];
+                if (c.mode2 == 2 && ok) t2 += (double)pv * (double)pv;
+                if (c.use_w1 || c.mode2 == 1) {
+                    const float gx = i + 1 < c.nx ? q4(Pn.ip, qq) - pv : 0.f;
+                    const float gy = j + 1 < c.ny ? q4(Pn.jp, qq) - pv : 0.f;
+                    const float gz = k + qq + 1 < c.nz ? Pn.f[qq + 2] - pv : 0.f;
+                    const float g2 = gx * gx + gy * gy + gz * gz;
+                    if (c.use_w1 && ok) { const float w = q4(a1, qq); t1 += (double)(w * w * g2); }
+                    if (c.mode2 == 1 && ok) { const float w = q4(a2, qq); t2 += (double)(w * w * g2); }
+                }
+            }
+        }
+    }
+    write_partials(part, 0, tq, sm);
     write_partials(part, 1, t1, sm);
     write_partials(part, 2, t2, sm);
 }
@@ -529,7 +763,8 @@ struct Engine {
         if (!rc.use_w1 && !rc.mode2) {
             KCT_CUDA(cudaMemsetAsync(w.part + 1 * kGrid, 0, 2 * kGrid * sizeof(double), stream));
         } else {
-            KCT_LAUNCH(k_weights, w.x, w.prior, w.w1, w.w2, rc, write ? 1 : 0, w.part);
+            if (use4()) KCT_LAUNCH(k_weights4, w.x, w.prior, w.w1, w.w2, rc, write ? 1 : 0, w.part);
+            else KCT_LAUNCH(k_weights, w.x, w.prior, w.w1, w.w2, rc, write ? 1 : 0, w.part);
         }
         launch_scalar(w, S_TV, stream);
     }
@@ -556,7 +791,7 @@ struct Engine {
             k_set_nonzero<<<1, kBlock, 0, stream>>>(w.ctl, w.part);
             KCT_LAUNCHED();
             adjoint(w.b, w.p);
-            KCT_LAUNCH(k_reggrad, w.p, nullptr, w.prior, w.w1, w.w2, w.p, rc, w.part);
+            reggrad(w.p, nullptr);
             launch_scalar(w, S_REF, stream);
         } else {
             KCT_CUDA(cudaMemsetAsync(&w.ctl->x_nonzero, 0, sizeof(int), stream));
@@ -573,23 +808,35 @@ struct Engine {
             launch_scalar(w, S_OBJ, stream, 0.0, nullptr, nullptr, w.obj + obj_idx, kind);
         }
         adjoint(w.r, w.s);
-        KCT_LAUNCH(k_reggrad, w.s, x_is_zero ? nullptr : w.x, w.prior, w.w1, w.w2, w.s, rc,
-                   w.part);
+        reggrad(w.s, x_is_zero ? nullptr : w.x);
         launch_scalar(w, S_INIT, stream, tol);
         KCT_LAUNCH(k_update_p, w.p, w.s, w.m, w.ctl, 1);
+    }
+
+    // float4 stencil kernels when the slab count allows (KCT_SCALAR_STENCILS=1: scalar)
+    bool use4() const {
+        const char* e = std::getenv("KCT_SCALAR_STENCILS");
+        return rc.nz % 4 == 0 && !(e && e[0] == '1');
+    }
+
+    // s <- s - regulariser gradient (in place), norms into slots 0..2
+    void reggrad(float* sv, const float* xv) {
+        if (use4()) KCT_LAUNCH(k_reggrad4, sv, xv, w.prior, w.w1, w.w2, sv, rc, w.part);
+        else KCT_LAUNCH(k_reggrad, sv, xv, w.prior, w.w1, w.w2, sv, rc, w.part);
     }
 
     // One CGLS iteration (krylov.hpp:98-125).
     void iterate(double* res, double* err, bool with_gt) {
         P.forward(w.p, w.q, stream);
-        KCT_LAUNCH(k_normq, w.q, w.n, w.p, w.w1, w.w2, rc, w.ctl, w.part);
+        if (use4()) KCT_LAUNCH(k_normq4, w.q, w.n, w.p, w.w1, w.w2, rc, w.ctl, w.part);
+        else KCT_LAUNCH(k_normq, w.q, w.n, w.p, w.w1, w.w2, rc, w.ctl, w.part);
         reduce_slot(0);
         launch_scalar(w, S_DELTA, stream);
         KCT_LAUNCH(k_update_xr, w.x, w.p, w.m, w.r, w.q, w.n, with_gt ? w.gt : nullptr, w.ctl,
                    w.part);
         reduce_slot(4);
         adjoint(w.r, w.s);
-        KCT_LAUNCH(k_reggrad, w.s, w.x, w.prior, w.w1, w.w2, w.s, rc, w.part);
+        reggrad(w.s, w.x);
         launch_scalar(w, S_GAMMA, stream, 0.0, res, err);
         KCT_LAUNCH(k_update_p, w.p, w.s, w.m, w.ctl, 0);
     }
