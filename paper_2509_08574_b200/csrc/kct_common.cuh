@@ -80,6 +80,22 @@ __device__ __forceinline__ float zcross(int P, int k0, float f0, float imk, floa
     return __fmaf_rn(__fsub_rn((float)(P - k0), f0), imk, w_in);
 }
 
+// Per detector row: dv in float64 and float32 and 1/dv (inf at dv == 0), the
+// row's z slope data, packed for one 16-byte load.
+struct __align__(16) RowTab {
+    double dvd;
+    float dv, invdv;
+};
+__device__ __forceinline__ RowTab ld_row(const RowTab* __restrict__ rows, int iv) {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(rows) + iv);
+    RowTab r;
+    r.dvd = t.x;
+    const float2 f = *reinterpret_cast<const float2*>(&t.y);
+    r.dv = f.x;
+    r.invdv = f.y;
+    return r;
+}
+
 constexpr int kMaxAnglesPerLaunch = 1024;
 
 // Per-angle cos/sin, passed by value in the kernel parameter space (constant

@@ -264,9 +264,7 @@ struct RowZ {
 
 __device__ __forceinline__ void row_init(RowZ& r, bool on, int iv, const ColParams& cp, float lo,
                                          float h1, int K0, int kend,
-                                         const float* __restrict__ dvtab,
-                                         const float* __restrict__ invdv,
-                                         const double* __restrict__ dvd,
+                                         const RowTab* __restrict__ rows,
                                          const float* __restrict__ ycol, const DevGeom& g) {
     if (!on) {
         r.k = K0 - 1;
@@ -278,12 +276,13 @@ __device__ __forceinline__ void row_init(RowZ& r, bool on, int iv, const ColPara
         r.yf = 0.f;
         return;
     }
-    const float dv = dvtab[iv];
-    const double kzd = fma(dvd[iv], cp.g_in, -g.kz0d);
+    const RowTab rt = ld_row(rows, iv);  // one 16-byte load: dv (f64, f32), 1/dv
+    const float dv = rt.dv;
+    const double kzd = fma(rt.dvd, cp.g_in, -g.kz0d);
     const int k0 = __double2int_rd(kzd);
     r.k0 = k0;
     r.f0 = (float)(kzd - (double)k0);
-    r.imk = __fmul_rn(invdv[iv], cp.inv_h1);
+    r.imk = __fmul_rn(rt.invdv, cp.inv_h1);
 #if KCT_ADJ_PREWEIGHT
     r.yf = __ldg(ycol + iv);  // y * sqrt(1 + (dv inv_l)^2), adj_weight_kernel
 #else
@@ -460,9 +459,7 @@ __device__ __forceinline__ int brick_walk(const ColParams& cp, const DevGeom& g,
 template <int C>
 __device__ __forceinline__ void brick_rows(const Seg* segs, int nseg, const ColParams& cp, float lo,
                                            int rlo, int rhi, int S, int K0, int kend, int lane,
-                                           const float* __restrict__ dvtab,
-                                           const float* __restrict__ invdv,
-                                           const double* __restrict__ dvd,
+                                           const RowTab* __restrict__ rows,
                                            const float* __restrict__ ycol, const DevGeom& g) {
     const float h1 = rcp_approx(cp.inv_h1);
     for (int p = 0; p < S; ++p) {
@@ -471,7 +468,7 @@ __device__ __forceinline__ void brick_rows(const Seg* segs, int nseg, const ColP
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 const int iv = base + S * (lane + 32 * c);
-                row_init(r[c], iv <= rhi, iv, cp, lo, h1, K0, kend, dvtab, invdv, dvd, ycol, g);
+                row_init(r[c], iv <= rhi, iv, cp, lo, h1, K0, kend, rows, ycol, g);
             }
             for (int sgi = 0; sgi < nseg; ++sgi) {
                 const Seg sg = segs[sgi];
@@ -564,7 +561,7 @@ __global__ void __launch_bounds__(128) adj_walk_build(const ColParams* __restric
 template <int C, bool TAB>
 __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel(
     const float* __restrict__ proj, float* __restrict__ out, const ColParams* __restrict__ cols,
-    const float* __restrict__ dvtab, const float* __restrict__ invdv, const double* __restrict__ dvd,
+    const RowTab* __restrict__ rows,
     DevGeom g, BrickCfg bc, AngleBatch ab, int a0, int nab, int accumulate,
     const int* __restrict__ order, int* queue, float* __restrict__ out_part,
     const WalkEntry* __restrict__ tab, const unsigned long long* __restrict__ off) {
@@ -645,7 +642,7 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
             const size_t cidx = (size_t)((int)(aiu & 0xffffu) - a0) * nu + (aiu >> 16);
             const ColParams cp = cols[cidx];
             brick_rows<C>(segs, nseg, cp, lo, (int)(rr & 0xffffu), (int)(rr >> 16), S, K0, kend,
-                          lane, dvtab, invdv, dvd, proj + cidx * nv, g);
+                          lane, rows, proj + cidx * nv, g);
             __syncwarp();
         }
     } else {
@@ -671,7 +668,7 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
                     segs[lane] = sg;
                 }
                 __syncwarp();
-                brick_rows<C>(segs, nseg, cp, lo, rlo, rhi, S, K0, kend, lane, dvtab, invdv, dvd,
+                brick_rows<C>(segs, nseg, cp, lo, rlo, rhi, S, K0, kend, lane, rows,
                               yb + (size_t)iu * nv, g);
                 __syncwarp();
             }
@@ -862,6 +859,7 @@ Projector::~Projector() {
     cudaFree(d_dv_);
     cudaFree(d_invdv_);
     cudaFree(d_dvd_);
+    cudaFree(d_rows_);
     cudaFree(d_border_);
     cudaFree(d_forder_);
     cudaFree(d_queue_);
@@ -1045,6 +1043,12 @@ void Projector::build_tables(const kct_geometry& geom) {
     KCT_CUDA(cudaMemcpy(d_invdv_, invdv.data(), nv * sizeof(float), cudaMemcpyHostToDevice));
     KCT_CUDA(cudaMalloc(&d_dvd_, nv * sizeof(double)));
     KCT_CUDA(cudaMemcpy(d_dvd_, dvd.data(), nv * sizeof(double), cudaMemcpyHostToDevice));
+    {
+        std::vector<RowTab> rt(nv);
+        for (int iv = 0; iv < nv; ++iv) rt[iv] = RowTab{dvd[iv], dv[iv], invdv[iv]};
+        KCT_CUDA(cudaMalloc(&d_rows_, nv * sizeof(RowTab)));
+        KCT_CUDA(cudaMemcpy(d_rows_, rt.data(), nv * sizeof(RowTab), cudaMemcpyHostToDevice));
+    }
     const size_t smem = adj_smem_bytes();
     // the attribute is per function, not per handle: set it to the largest
     // brick any projector can use, so handles with taller bricks coexist
@@ -1266,11 +1270,11 @@ void Projector::adjoint(const float* proj, float* vol, cudaStream_t s) const {
             const unsigned grid = d_queue_ ? std::min(nctas, adj_ctas_) : nctas;
             if (d_tab_)
                 adj_brick_kernel<kAdjRows, true><<<grid, kAdjWarps * 32, smem, s>>>(
-                    pr, vol, cols, d_dv_, d_invdv_, d_dvd_, dg_, bc, ab, a0, nab, accum, d_border_,
+                    pr, vol, cols, d_rows_, dg_, bc, ab, a0, nab, accum, d_border_,
                     d_queue_, d_part_, static_cast<const WalkEntry*>(d_tab_), d_off_);
             else
                 adj_brick_kernel<kAdjRows, false><<<grid, kAdjWarps * 32, smem, s>>>(
-                    pr, vol, cols, d_dv_, d_invdv_, d_dvd_, dg_, bc, ab, a0, nab, accum, d_border_,
+                    pr, vol, cols, d_rows_, dg_, bc, ab, a0, nab, accum, d_border_,
                     d_queue_, d_part_, nullptr, nullptr);
             if (bc.ngrp > 1) {
                 KCT_LAUNCHED();

@@ -74,6 +74,7 @@ class Projector {
     float* d_dv_ = nullptr;           // [nv] row heights dv(iv)
     float* d_invdv_ = nullptr;        // [nv] 1/dv (inf at dv == 0)
     double* d_dvd_ = nullptr;         // [nv] dv in float64
+    RowTab* d_rows_ = nullptr;        // [nv] packed (dvd, dv, 1/dv) for the adjoint
     int fwd_c_ = 4, fwd_bands_ = 1, adj_k_ = 8;
     int adj_S_ = 2, adj_bz_ = 32;
     bool adj_gather_ = false;
