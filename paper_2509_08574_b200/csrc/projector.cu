@@ -462,12 +462,15 @@ __device__ __forceinline__ void brick_rows(const Seg* segs, int nseg, const ColP
                                            const RowTab* __restrict__ rows,
                                            const float* __restrict__ ycol, const DevGeom& g) {
     const float h1 = rcp_approx(cp.inv_h1);
-    for (int p = 0; p < S; ++p) {
-        for (int base = rlo + p; base <= rhi; base += 32 * S * C) {
+    // passes of rows S' >= S apart with S' = max(S, ceil(n / 32C)): the n rows
+    // in the fewest passes, one per residue class (measured: -2.6% at c3)
+    const int Sp = max(S, (rhi - rlo + 32 * C) / (32 * C));
+    for (int p = 0; p < Sp; ++p) {
+        for (int base = rlo + p; base <= rhi; base += 32 * Sp * C) {
             RowZ r[C];
 #pragma unroll
             for (int c = 0; c < C; ++c) {
-                const int iv = base + S * (lane + 32 * c);
+                const int iv = base + Sp * (lane + 32 * c);
                 row_init(r[c], iv <= rhi, iv, cp, lo, h1, K0, kend, rows, ycol, g);
             }
             for (int sgi = 0; sgi < nseg; ++sgi) {
