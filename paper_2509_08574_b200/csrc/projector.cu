@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
     // remaining crossings nrem of planes inside [0, nz]
     float acc[C], wz[C], fz[C], imk[C], dvv[C];
     int k[C], kstep[C], pk[C], nrem[C];
+    bool hit = false;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
         const int iv = iv0 + 32 * c;
@@ -95,9 +96,14 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
         pk[c] = P - k0;
         nrem[c] = max(n, 0);
         wz[c] = nrem[c] > 0 ? __fmaf_rn(__fsub_rn((float)pk[c], fz[c]), imk[c], cp.w_in) : kInf;
+        // a ray meets the volume iff it starts inside the z range or its first
+        // plane crossing (the entry plane) comes before the xy exit
+        hit = hit || (unsigned)kk < (unsigned)nz || wz[c] < cp.w_out;
     }
 
-    if (cp.w_in < cp.w_out) {
+    // rows that all pass above / below the volume (detector overhang, c4)
+    // skip the walk: their line integrals are 0
+    if (cp.w_in < cp.w_out && __any_sync(kFull, hit)) {
         const int nx = g.nx, ny = g.ny;
         int i = cp.i0, j = cp.j0;
         const int stx = cp.dx > 0.0 ? 1 : -1, sty = cp.dy > 0.0 ? 1 : -1;
