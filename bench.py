@@ -343,8 +343,10 @@ def run_ours(args):
 
 
 def run_recon(k, synth, cfg, grid, prior, follow, dev, args, ws=1, rank=0, shared=False):
-    """20-iteration IRN-PICCS at c3.  With ws > 1 every rank holds the angles
-    r::ws of the follow-up scan (distributed.py: partial-volume and scalar
+    """20-iteration IRN-PICCS at c3.  With ws > 1 (distributed.py) either every
+    rank holds y planes [j0, j1) of the volume vectors and all projections
+    (--recon-split yslab: partial-projection and scalar all-reduces, halo
+    planes) or the angles r::ws (angles: partial-volume and scalar
     all-reduces); the reported time is the max over ranks."""
     import torch
     na_p, na_f = cfg.prior_views, cfg.followup_views
@@ -364,7 +366,19 @@ def run_recon(k, synth, cfg, grid, prior, follow, dev, args, ws=1, rank=0, share
     pf = Af.proj_from_native(Af.apply(xf_n)).cpu().numpy()
     b = synth.poisson_log(pf, cfg.i0, seed=1003)
     del Ap, xp_n, bp_n, xf_n
-    if ws > 1:
+    slab = ws > 1 and args.recon_split == "yslab"
+    grid_s, prior_s, follow_s = grid, prior_rec, follow
+    if slab:
+        # y-slab-sharded state (distributed.irn_piccs_slab): this rank's volume
+        # planes [j0, j1) with halos, all projections, partial-projection sums
+        from paper_2509_08574_b200 import distributed, shard
+        proj_h = k.ProjectionSet(geom_f, b)
+        A, j0, j1 = distributed.slab_projector(grid, geom_f, ws, rank)
+        grid_s = shard.slab_grid(grid, ws, rank, axis="y")
+        plane = grid.dims[0] * grid.dims[2]
+        prior_s = prior_rec[j0 * plane:j1 * plane].contiguous()  # native y-slab
+        follow_s = distributed.y_slab(follow, grid, j0, j1)
+    elif ws > 1:
         from paper_2509_08574_b200 import distributed
         proj_h = distributed.shard_projections(k.ProjectionSet(geom_f, b), ws, rank)
         A = distributed.sharded_projector(proj_h, grid)
@@ -376,6 +390,14 @@ def run_recon(k, synth, cfg, grid, prior, follow, dev, args, ws=1, rank=0, share
     setup = time.perf_counter() - t0
     params = k.RegularizationParams(alpha=cfg.alpha, outer_iters=cfg.outer, inner_iters=cfg.inner)
     proj = k.ProjectionSet(proj_h.geometry, b_n)
+
+    def rsum(vals, op="sum"):
+        if ws == 1:
+            return vals
+        t = torch.tensor(vals, dtype=torch.float64, device="cpu" if shared else dev)
+        torch.distributed.all_reduce(
+            t, op=torch.distributed.ReduceOp.SUM if op == "sum" else torch.distributed.ReduceOp.MAX)
+        return t.tolist()
 
     def timed(fn):
         if ws > 1:
@@ -394,31 +416,35 @@ def run_recon(k, synth, cfg, grid, prior, follow, dev, args, ws=1, rank=0, share
     reps = []
     rep = None
     for i in range(args.recon_warmup + args.recon_steps):
-        rep, dt = timed(lambda: k.irn_piccs(proj, grid, prior_rec, params, projector=A))
+        rep, dt = timed(lambda: k.irn_piccs(proj, grid_s, prior_s, params, projector=A))
         if i >= args.recon_warmup:
             reps.append(dt)
-    x_ref = Af.volume_from_native(rep.volume).cpu().numpy()
-    rel = float(np.linalg.norm(x_ref - follow) / np.linalg.norm(follow))
+    x_ref = A.volume_from_native(rep.volume).cpu().numpy()
+    e2, f2 = rsum([float(np.sum((x_ref.astype(np.float64) - follow_s) ** 2)),
+                   float(np.sum(np.asarray(follow_s, dtype=np.float64) ** 2))])
+    rel = float(np.sqrt(e2 / f2))
     # end to end: host float32 arrays in the reference layouts through kct_irn_piccs
     # (pinned host buffers; one untimed warm-up of the host-buffer path)
-    prior_h = Af.volume_from_native(prior_rec).cpu().pin_memory().numpy()
+    prior_h = A.volume_from_native(prior_s).cpu().pin_memory().numpy()
     b_h = torch.from_numpy(np.ascontiguousarray(proj_h.data, dtype=np.float32)).pin_memory().numpy()
     proj_hp = k.ProjectionSet(proj_h.geometry, b_h)
-    k.irn_piccs(proj_hp, grid, prior_h, params, projector=A)
-    rep_h, e2e = timed(lambda: k.irn_piccs(proj_hp, grid, prior_h, params, projector=A))
-    same = float(np.abs(rep_h.volume - x_ref).max())
+    k.irn_piccs(proj_hp, grid_s, prior_h, params, projector=A)
+    rep_h, e2e = timed(lambda: k.irn_piccs(proj_hp, grid_s, prior_h, params, projector=A))
+    same = rsum([float(np.abs(rep_h.volume - x_ref).max())], op="max")[0]
     return {"seconds_per_recon": round(float(np.median(reps)), 4),
             "all_seconds": [round(r, 4) for r in reps],
             "solve_seconds_reported": round(rep.solve_seconds, 4),
             "e2e_seconds": round(e2e, 4),
-            "e2e_h2d_bytes": 4 * (2 * grid.count() + proj_h.geometry.ray_count()),
-            "e2e_d2h_bytes": 4 * grid.count(), "e2e_max_abs_diff_vs_device_run": same,
+            "e2e_h2d_bytes": 4 * (2 * grid_s.count() + proj_h.geometry.ray_count()),
+            "e2e_d2h_bytes": 4 * grid_s.count(), "e2e_max_abs_diff_vs_device_run": same,
             "iterations": cfg.outer * cfg.inner, "outer_x_inner": f"{cfg.outer}x{cfg.inner}",
             "alpha": cfg.alpha, "lambda": cfg.alpha, "tau": rep.tau,
             "objective_history": [float(v) for v in rep.objective_history],
             "rel_error_vs_followup_phantom": round(rel, 5),
             "prior": "20-iter CGLS of a 360-view noiseless scan (computed on device, untimed)",
-            "parallelism": (f"angle-sharded x{ws}: partial-volume + scalar all-reduces"
+            "parallelism": (f"y-slab-sharded x{ws}: partial-projection + scalar all-reduces, "
+                            "halo planes" if slab else
+                            f"angle-sharded x{ws}: partial-volume + scalar all-reduces"
                             if ws > 1 else "single GPU"),
             "setup_seconds_untimed": round(setup, 2),
             "reference_cpu_seconds_survey_box": 329.2}
@@ -437,6 +463,8 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-fdk", action="store_true")
+    ap.add_argument("--recon-split", default="yslab", choices=["yslab", "angles"],
+                    help="multi-GPU PICCS decomposition (N > 1)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -153,6 +153,23 @@ int kct_fdk(kct_projector* h, const float* proj, float* vol, int mem, int layout
 typedef int (*kct_allreduce_fn)(void* ctx, void* buf, size_t count, int dtype, void* stream);
 int kct_set_allreduce(kct_projector* h, kct_allreduce_fn fn, void* ctx);
 
+/* y-slab-sharded solves (the volume-partitioned variant).  The
+ * handle's grid is planes [j0, j0 + ny) of a grid with ny_global y planes
+ * (e.g. shard.slab_grid(..., axis="y")); every rank holds all projections.
+ * The solver then keeps its volume vectors slab-local with one halo plane on
+ * each side, sums the partial forward projections and the volume-domain
+ * reductions with the all-reduce hook (kct_set_allreduce, required), and
+ * exchanges halo planes through `fn`: send this rank's first / last interior
+ * y plane (lo_plane / hi_plane, `count` floats each) and receive the
+ * neighbouring ranks' adjacent planes into lo_halo (from rank - 1) /
+ * hi_halo (from rank + 1); buffers without a neighbour are left untouched.
+ * fn = NULL leaves slab mode.  Not part of the reference (the reference is
+ * single-process). */
+typedef int (*kct_halo_fn)(void* ctx, const void* lo_plane, const void* hi_plane, void* lo_halo,
+                           void* hi_halo, size_t count, void* stream);
+int kct_set_slab(kct_projector* h, int rank, int world, int j0, int ny_global, kct_halo_fn fn,
+                 void* ctx);
+
 /* ---- solvers ---------------------------------------------------------- */
 /* cgls_recon (recon.hpp:312-315 -> baseline_solve :274-307 -> cgls krylov.hpp:59-127).
  * b: N floats, x0: M floats or NULL (zeros), ground_truth: M or NULL,

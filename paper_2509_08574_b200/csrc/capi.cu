@@ -285,6 +285,26 @@ int kct_set_allreduce(kct_projector* h, kct_allreduce_fn fn, void* ctx) {
     });
 }
 
+int kct_set_slab(kct_projector* h, int rank, int world, int j0, int ny_global, kct_halo_fn fn,
+                 void* ctx) {
+    return guarded([&] {
+        auto& P = get(h);
+        if (fn) {
+            if (world < 1 || rank < 0 || rank >= world)
+                throw kct::ConfigError("slab: rank out of range");
+            if (j0 < 0 || ny_global < j0 + P.grid().ny)
+                throw kct::ConfigError("slab: plane range outside the global grid");
+        }
+        P.slab_rank = fn ? rank : -1;
+        P.slab_world = fn ? world : 0;
+        P.slab_j0 = fn ? j0 : 0;
+        P.slab_nyg = fn ? ny_global : 0;
+        P.halo_fn = fn;
+        P.halo_ctx = ctx;
+        P.workspace.reset();  // volume buffers change shape (halo planes)
+    });
+}
+
 double kct_resolve_tau(double tau, const float* reference, size_t n) {
     return kct::resolve_tau(tau, reference, n);
 }

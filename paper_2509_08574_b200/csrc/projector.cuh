@@ -49,6 +49,12 @@ class Projector {
     // Angle-sharded multi-process mode (kct_set_allreduce).
     kct_allreduce_fn comm_fn = nullptr;
     void* comm_ctx = nullptr;
+    // y-slab-sharded multi-process mode (kct_set_slab): this grid is planes
+    // [slab_j0, slab_j0 + ny) of a grid with slab_nyg y planes.
+    int slab_rank = -1, slab_world = 0, slab_j0 = 0, slab_nyg = 0;
+    kct_halo_fn halo_fn = nullptr;
+    void* halo_ctx = nullptr;
+    bool slab_mode() const { return halo_fn != nullptr; }
 
     int fwd_chunks() const { return fwd_c_; }
     int adj_k() const { return adj_k_; }

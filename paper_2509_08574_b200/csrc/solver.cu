@@ -22,6 +22,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <initializer_list>
+#include <string>
 #include <vector>
 
 #include "solver.cuh"
@@ -56,7 +58,8 @@ enum ScalarMode {
 
 // Regulariser configuration shared by the stencil kernels.
 struct RegCfg {
-    int nx, ny, nz;
+    int nx, ny, nz;  // this rank's grid (the whole grid unless y-slab sharded)
+    int j0, nyg;     // y-slab: global index of local plane 0, global plane count
     int use_w1;      // a != 0: TV block present
     int mode2;       // 0 none, 1 PICCS (W2 D block), 2 PIPLE (I block)
     float alpha2, lambda2;
@@ -75,7 +78,7 @@ __device__ __forceinline__ void fdiff(const float* __restrict__ f, size_t v, int
                                       const RegCfg& c, size_t si, size_t sj, float fv, float& gx,
                                       float& gy, float& gz) {
     gx = i + 1 < c.nx ? f[v + si] - fv : 0.f;
-    gy = j + 1 < c.ny ? f[v + sj] - fv : 0.f;
+    gy = j + c.j0 + 1 < c.nyg ? f[v + sj] - fv : 0.f;
     gz = k + 1 < c.nz ? f[v + 1] - fv : 0.f;
 }
 
@@ -109,7 +112,7 @@ __global__ void __launch_bounds__(kBlock) k_weights(const float* __restrict__ x,
         if (c.mode2 == 1) {
             const float dv = xv - xp[v];
             const float gx = i + 1 < c.nx ? (x[v + si] - xp[v + si]) - dv : 0.f;
-            const float gy = j + 1 < c.ny ? (x[v + sj] - xp[v + sj]) - dv : 0.f;
+            const float gy = j + c.j0 + 1 < c.nyg ? (x[v + sj] - xp[v + sj]) - dv : 0.f;
             const float gz = k + 1 < c.nz ? (x[v + 1] - xp[v + 1]) - dv : 0.f;
             const float r = sqrtf(gx * gx + gy * gy + gz * gz + c.tau2);
             t2 += (double)r;
@@ -163,7 +166,7 @@ __global__ void __launch_bounds__(kBlock) k_reggrad(const float* __restrict__ sA
             const float wv = w1[v], wv2 = wv * wv;
             float g = -wv2 * (gx + gy + gz);
             if (i > 0) { const float w = w1[v - si]; g += w * w * (xv - x[v - si]); }
-            if (j > 0) { const float w = w1[v - sj]; g += w * w * (xv - x[v - sj]); }
+            if (j + c.j0 > 0) { const float w = w1[v - sj]; g += w * w * (xv - x[v - sj]); }
             if (k > 0) { const float w = w1[v - 1]; g += w * w * (xv - x[v - 1]); }
             sv -= c.alpha2 * g;
             t1 += (double)(wv2 * (gx * gx + gy * gy + gz * gz));
@@ -172,12 +175,12 @@ __global__ void __launch_bounds__(kBlock) k_reggrad(const float* __restrict__ sA
             auto d = [&](size_t u) { return (x ? x[u] : 0.f) - xp[u]; };
             const float dv = d(v);
             const float gx = i + 1 < c.nx ? d(v + si) - dv : 0.f;
-            const float gy = j + 1 < c.ny ? d(v + sj) - dv : 0.f;
+            const float gy = j + c.j0 + 1 < c.nyg ? d(v + sj) - dv : 0.f;
             const float gz = k + 1 < c.nz ? d(v + 1) - dv : 0.f;
             const float wv = w2[v], wv2 = wv * wv;
             float g = -wv2 * (gx + gy + gz);
             if (i > 0) { const float w = w2[v - si]; g += w * w * (dv - d(v - si)); }
-            if (j > 0) { const float w = w2[v - sj]; g += w * w * (dv - d(v - sj)); }
+            if (j + c.j0 > 0) { const float w = w2[v - sj]; g += w * w * (dv - d(v - sj)); }
             if (k > 0) { const float w = w2[v - 1]; g += w * w * (dv - d(v - 1)); }
             sv -= c.lambda2 * g;
             t2 += (double)(wv2 * (gx * gx + gy * gy + gz * gz));
@@ -226,9 +229,9 @@ __device__ __forceinline__ void load_nb(const float* __restrict__ f, size_t v, i
     n.f[0] = (ok && f && k > 0) ? (lane > 0 ? up : f[v - 1]) : 0.f;
     n.f[5] = (ok && f && k + 4 < c.nz) ? (lane < 31 ? dn : f[v + 4]) : 0.f;
     n.ip = (ok && f && i + 1 < c.nx) ? ld4(f, v + si) : z4;
-    n.jp = (ok && f && j + 1 < c.ny) ? ld4(f, v + sj) : z4;
+    n.jp = (ok && f && j + c.j0 + 1 < c.nyg) ? ld4(f, v + sj) : z4;
     n.im = (MINUS_I && ok && f && i > 0) ? ld4(f, v - si) : z4;
-    n.jm = (MINUS_J && ok && f && j > 0) ? ld4(f, v - sj) : z4;
+    n.jm = (MINUS_J && ok && f && j + c.j0 > 0) ? ld4(f, v - sj) : z4;
 }
 
 __device__ __forceinline__ void decode4(size_t base, int lane, size_t m4, const RegCfg& c, bool& ok,
@@ -262,7 +265,7 @@ __global__ void __launch_bounds__(kBlock) k_weights4(const float* __restrict__ x
             const float xv = X.f[q + 1];
             if (c.use_w1) {
                 const float gx = i + 1 < c.nx ? q4(X.ip, q) - xv : 0.f;
-                const float gy = j + 1 < c.ny ? q4(X.jp, q) - xv : 0.f;
+                const float gy = j + c.j0 + 1 < c.nyg ? q4(X.jp, q) - xv : 0.f;
                 const float gz = k + q + 1 < c.nz ? X.f[q + 2] - xv : 0.f;
                 const float r = sqrtf(gx * gx + gy * gy + gz * gz + c.tau2);
                 if (ok) t1 += (double)r;
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(kBlock) k_weights4(const float* __restrict__ x
             if (c.mode2 == 1) {
                 const float dv = xv - P.f[q + 1];
                 const float gx = i + 1 < c.nx ? (q4(X.ip, q) - q4(P.ip, q)) - dv : 0.f;
-                const float gy = j + 1 < c.ny ? (q4(X.jp, q) - q4(P.jp, q)) - dv : 0.f;
+                const float gy = j + c.j0 + 1 < c.nyg ? (q4(X.jp, q) - q4(P.jp, q)) - dv : 0.f;
                 const float gz = k + q + 1 < c.nz ? (X.f[q + 2] - P.f[q + 2]) - dv : 0.f;
                 const float r = sqrtf(gx * gx + gy * gy + gz * gz + c.tau2);
                 if (ok) t2 += (double)r;
@@ -297,12 +300,12 @@ __device__ __forceinline__ void dtwd(const Nb4& F, const Nb4& W, int k, int i, i
     for (int q = 0; q < 4; ++q) {
         const float fv = F.f[q + 1];
         const float gx = i + 1 < c.nx ? q4(F.ip, q) - fv : 0.f;
-        const float gy = j + 1 < c.ny ? q4(F.jp, q) - fv : 0.f;
+        const float gy = j + c.j0 + 1 < c.nyg ? q4(F.jp, q) - fv : 0.f;
         const float gz = k + q + 1 < c.nz ? F.f[q + 2] - fv : 0.f;
         const float wv = W.f[q + 1], wv2 = wv * wv;
         float t = -wv2 * (gx + gy + gz);
         if (i > 0) { const float w = q4(W.im, q); t += w * w * (fv - q4(F.im, q)); }
-        if (j > 0) { const float w = q4(W.jm, q); t += w * w * (fv - q4(F.jm, q)); }
+        if (j + c.j0 > 0) { const float w = q4(W.jm, q); t += w * w * (fv - q4(F.jm, q)); }
         if (k + q > 0) { const float w = W.f[q]; t += w * w * (fv - F.f[q]); }
         g[q] = t;
         g2[q] = wv2 * (gx * gx + gy * gy + gz * gz);
@@ -413,7 +416,7 @@ __global__ void __launch_bounds__(kBlock) k_normq4(const float* __restrict__ q, 
                 if (c.mode2 == 2 && ok) t2 += (double)pv * (double)pv;
                 if (c.use_w1 || c.mode2 == 1) {
                     const float gx = i + 1 < c.nx ? q4(Pn.ip, qq) - pv : 0.f;
-                    const float gy = j + 1 < c.ny ? q4(Pn.jp, qq) - pv : 0.f;
+                    const float gy = j + c.j0 + 1 < c.nyg ? q4(Pn.jp, qq) - pv : 0.f;
                     const float gz = k + qq + 1 < c.nz ? Pn.f[qq + 2] - pv : 0.f;
                     const float g2 = gx * gx + gy * gy + gz * gz;
                     if (c.use_w1 && ok) { const float w = q4(a1, qq); t1 += (double)(w * w * g2); }
@@ -633,6 +636,7 @@ __global__ void k_minmax_final(const double* part, double* out) {
 // ---- workspace -----------------------------------------------------------------
 struct Workspace {
     size_t m = 0, n = 0;
+    size_t halo = 0;  // y-slab mode: floats of one y plane kept on each side of volume vectors
     float *b = nullptr, *r = nullptr, *q = nullptr;
     float *x = nullptr, *p = nullptr, *s = nullptr, *prior = nullptr, *w1 = nullptr,
           *w2 = nullptr, *gt = nullptr;
@@ -641,19 +645,34 @@ struct Workspace {
     double* hist = nullptr;  // [2][cap]: residual, error
     double* obj = nullptr;   // [cap_obj]
     double* scal = nullptr;  // misc scalars
+    double* gath = nullptr;  // y-slab mode: [2 * world] gather-by-sum buffer
     size_t cap = 0, cap_obj = 0;
+    std::vector<void*> allocs;
 
     ~Workspace() {
-        for (void* ptr : {(void*)b, (void*)r, (void*)q, (void*)x, (void*)p, (void*)s,
-                          (void*)prior, (void*)w1, (void*)w2, (void*)gt, (void*)part,
-                          (void*)ctl, (void*)hist, (void*)obj, (void*)scal})
-            cudaFree(ptr);
+        for (void* ptr : allocs) cudaFree(ptr);
+        for (void* ptr : {(void*)hist, (void*)obj}) cudaFree(ptr);
     }
 };
 
 template <class T>
-void ensure(T*& ptr, size_t n) {
-    if (!ptr) KCT_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
+void ensure(Workspace& w, T*& ptr, size_t n) {
+    if (!ptr) {
+        KCT_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
+        w.allocs.push_back(ptr);
+    }
+}
+
+// volume vectors: `halo` floats (one y plane) of zeros before and after
+void ensure_vol(Workspace& w, float*& ptr) {
+    if (!ptr) {
+        float* base = nullptr;
+        const size_t tot = w.m + 2 * w.halo;
+        KCT_CUDA(cudaMalloc(&base, tot * sizeof(float)));
+        KCT_CUDA(cudaMemset(base, 0, tot * sizeof(float)));
+        w.allocs.push_back(base);
+        ptr = base + w.halo;
+    }
 }
 
 Workspace& workspace(Projector& P, size_t hist_cap, size_t obj_cap) {
@@ -662,15 +681,17 @@ Workspace& workspace(Projector& P, size_t hist_cap, size_t obj_cap) {
         ws = std::make_shared<Workspace>();
         ws->m = P.domain_size();
         ws->n = P.range_size();
+        ws->halo = P.slab_mode() ? (size_t)P.grid().nx * P.grid().nz : 0;
         P.workspace = ws;
     }
     Workspace& w = *ws;
-    const size_t m = w.m, n = w.n;
-    ensure(w.b, n); ensure(w.r, n); ensure(w.q, n);
-    ensure(w.x, m); ensure(w.p, m); ensure(w.s, m);
-    ensure(w.part, (size_t)kSlots * kGrid);
-    ensure(w.ctl, 1);
-    ensure(w.scal, 8);
+    const size_t n = w.n;
+    ensure(w, w.b, n); ensure(w, w.r, n); ensure(w, w.q, n);
+    ensure_vol(w, w.x); ensure_vol(w, w.p); ensure_vol(w, w.s);
+    ensure(w, w.part, (size_t)kSlots * kGrid);
+    ensure(w, w.ctl, 1);
+    ensure(w, w.scal, 8);
+    if (P.slab_mode()) ensure(w, w.gath, (size_t)2 * P.slab_world);
     if (w.cap < hist_cap) {
         cudaFree(w.hist);
         w.hist = nullptr;
@@ -739,23 +760,41 @@ struct Engine {
     RegCfg rc{};
     int kind = KCT_KIND_TV;
 
-    // angle-sharded mode: sum A^T partial volumes and projection-domain
-    // reductions over the ranks (no-ops in single-process mode)
-    void reduce_volume(float* v) {
-        if (!P.comm_fn) return;
-        if (P.comm_fn(P.comm_ctx, v, w.m, 0, stream) != 0)
-            throw CudaError("allreduce hook failed (volume)");
+    // Multi-process modes (no-ops in a single process):
+    //  * angle-sharded (kct_set_allreduce): rank-local rays; sum the partial
+    //    A^T volumes and the projection-domain reductions;
+    //  * y-slab-sharded (kct_set_slab): rank-local volume slab with halo
+    //    planes; sum the partial forward projections and the volume-domain
+    //    reductions, exchange halos after every update of a stencil operand.
+    bool slab() const { return P.slab_mode(); }
+    void allreduce(void* buf, size_t count, int dtype, const char* what) {
+        if (P.comm_fn(P.comm_ctx, buf, count, dtype, stream) != 0)
+            throw CudaError(std::string("allreduce hook failed (") + what + ")");
     }
-    void reduce_slot(int slot) {
+    void reduce_slots(std::initializer_list<int> slots) {
         if (!P.comm_fn) return;
-        k_fold<<<1, kBlock, 0, stream>>>(w.part, slot);
-        KCT_LAUNCHED();
-        if (P.comm_fn(P.comm_ctx, w.part + slot * kGrid, 1, 1, stream) != 0)
-            throw CudaError("allreduce hook failed (scalar)");
+        for (int slot : slots) {
+            k_fold<<<1, kBlock, 0, stream>>>(w.part, slot);
+            KCT_LAUNCHED();
+            allreduce(w.part + slot * kGrid, 1, 1, "scalar");
+        }
+    }
+    void proj_slots(std::initializer_list<int> slots) { if (!slab()) reduce_slots(slots); }
+    void vol_slots(std::initializer_list<int> slots) { if (slab()) reduce_slots(slots); }
+    void forward(const float* v, float* q) {
+        P.forward(v, q, stream);
+        if (slab()) allreduce(q, w.n, 0, "projections");
     }
     void adjoint(const float* y, float* v) {
         P.adjoint(y, v, stream);
-        reduce_volume(v);
+        if (!slab() && P.comm_fn) allreduce(v, w.m, 0, "volume");
+    }
+    void halo(float* v) {
+        if (!slab() || !v) return;
+        const size_t pl = w.halo;
+        const size_t ny = (size_t)P.grid().ny;
+        if (P.halo_fn(P.halo_ctx, v, v + (ny - 1) * pl, v - pl, v + ny * pl, pl, stream) != 0)
+            throw CudaError("halo exchange hook failed");
     }
 
     // weights (optional) and smoothed-TV / quadratic sums of the objective at w.x
@@ -765,6 +804,11 @@ struct Engine {
         } else {
             if (use4()) KCT_LAUNCH(k_weights4, w.x, w.prior, w.w1, w.w2, rc, write ? 1 : 0, w.part);
             else KCT_LAUNCH(k_weights, w.x, w.prior, w.w1, w.w2, rc, write ? 1 : 0, w.part);
+            vol_slots({1, 2});
+            if (write) {
+                if (rc.use_w1) halo(w.w1);
+                if (rc.mode2 == 1) halo(w.w2);
+            }
         }
         launch_scalar(w, S_TV, stream);
     }
@@ -774,10 +818,10 @@ struct Engine {
         if (x_is_zero) {
             KCT_LAUNCH(k_resid, w.b, nullptr, nullptr, w.n, w.part, 0);
         } else {
-            P.forward(w.x, w.q, stream);
+            forward(w.x, w.q);
             KCT_LAUNCH(k_resid, w.b, w.q, nullptr, w.n, w.part, 0);
         }
-        reduce_slot(0);
+        proj_slots({0});
         launch_scalar(w, S_DATA, stream);
         launch_scalar(w, S_OBJ, stream, 0.0, nullptr, nullptr, w.obj + idx, kind);
     }
@@ -788,6 +832,7 @@ struct Engine {
         if (tol > 0.0 && !x_is_zero) {
             // ||A~^T b~||^2, the tolerance reference of a warm start (krylov.hpp:81-88)
             KCT_LAUNCH(k_stats, w.x, w.m, w.part);
+            vol_slots({3});
             k_set_nonzero<<<1, kBlock, 0, stream>>>(w.ctl, w.part);
             KCT_LAUNCHED();
             adjoint(w.b, w.p);
@@ -799,10 +844,10 @@ struct Engine {
         if (x_is_zero) {
             KCT_LAUNCH(k_resid, w.b, nullptr, w.r, w.n, w.part, 0);
         } else {
-            P.forward(w.x, w.q, stream);
+            forward(w.x, w.q);
             KCT_LAUNCH(k_resid, w.b, w.q, w.r, w.n, w.part, 0);
         }
-        reduce_slot(0);
+        proj_slots({0});
         if (obj_idx >= 0) {
             launch_scalar(w, S_DATA, stream);
             launch_scalar(w, S_OBJ, stream, 0.0, nullptr, nullptr, w.obj + obj_idx, kind);
@@ -811,6 +856,7 @@ struct Engine {
         reggrad(w.s, x_is_zero ? nullptr : w.x);
         launch_scalar(w, S_INIT, stream, tol);
         KCT_LAUNCH(k_update_p, w.p, w.s, w.m, w.ctl, 1);
+        halo(w.p);
     }
 
     // float4 stencil kernels when the slab count allows (KCT_SCALAR_STENCILS=1: scalar)
@@ -823,26 +869,32 @@ struct Engine {
     void reggrad(float* sv, const float* xv) {
         if (use4()) KCT_LAUNCH(k_reggrad4, sv, xv, w.prior, w.w1, w.w2, sv, rc, w.part);
         else KCT_LAUNCH(k_reggrad, sv, xv, w.prior, w.w1, w.w2, sv, rc, w.part);
+        vol_slots({0, 1, 2});
     }
 
     // One CGLS iteration (krylov.hpp:98-125).
     void iterate(double* res, double* err, bool with_gt) {
-        P.forward(w.p, w.q, stream);
+        forward(w.p, w.q);
         if (use4()) KCT_LAUNCH(k_normq4, w.q, w.n, w.p, w.w1, w.w2, rc, w.ctl, w.part);
         else KCT_LAUNCH(k_normq, w.q, w.n, w.p, w.w1, w.w2, rc, w.ctl, w.part);
-        reduce_slot(0);
+        proj_slots({0});
+        vol_slots({1, 2});
         launch_scalar(w, S_DELTA, stream);
         KCT_LAUNCH(k_update_xr, w.x, w.p, w.m, w.r, w.q, w.n, with_gt ? w.gt : nullptr, w.ctl,
                    w.part);
-        reduce_slot(4);
+        proj_slots({4});
+        vol_slots({5});
+        halo(w.x);
         adjoint(w.r, w.s);
         reggrad(w.s, w.x);
         launch_scalar(w, S_GAMMA, stream, 0.0, res, err);
         KCT_LAUNCH(k_update_p, w.p, w.s, w.m, w.ctl, 0);
+        halo(w.p);
     }
 
     void ground_truth_norm() {
         KCT_LAUNCH(k_stats, w.gt, w.m, w.part);
+        vol_slots({0});
         launch_scalar(w, S_GT2, stream);
     }
 };
@@ -872,17 +924,51 @@ void throw_solver(const Ctl& c) {
 }
 
 // device (min, max) of a native buffer -> resolve_tau semantics (recon.hpp:60-66)
-double device_tau(Workspace& w, const float* ref, size_t n, double tau, cudaStream_t stream) {
+double device_tau(Projector& P, Workspace& w, const float* ref, size_t n, double tau,
+                  cudaStream_t stream) {
     if (tau > 0.0) return tau;
     if (!ref || n == 0) return 1e-4;
     KCT_LAUNCH(k_stats, ref, n, w.part);
     k_minmax_final<<<1, kBlock, 0, stream>>>(w.part, w.scal);
     KCT_LAUNCHED();
     double mm[2];
-    KCT_CUDA(cudaMemcpyAsync(mm, w.scal, sizeof mm, cudaMemcpyDeviceToHost, stream));
-    KCT_CUDA(cudaStreamSynchronize(stream));
+    if (P.slab_mode()) {
+        // global (min, max) over the slabs: gather by sum into [2 * world]
+        const int W = P.slab_world;
+        KCT_CUDA(cudaMemsetAsync(w.gath, 0, 2 * W * sizeof(double), stream));
+        KCT_CUDA(cudaMemcpyAsync(w.gath + 2 * P.slab_rank, w.scal, 2 * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, stream));
+        if (P.comm_fn(P.comm_ctx, w.gath, 2 * W, 1, stream) != 0)
+            throw CudaError("allreduce hook failed (tau)");
+        std::vector<double> g(2 * W);
+        KCT_CUDA(cudaMemcpyAsync(g.data(), w.gath, 2 * W * sizeof(double), cudaMemcpyDeviceToHost,
+                                 stream));
+        KCT_CUDA(cudaStreamSynchronize(stream));
+        mm[0] = g[0];
+        mm[1] = g[1];
+        for (int r = 1; r < W; ++r) {
+            mm[0] = std::min(mm[0], g[2 * r]);
+            mm[1] = std::max(mm[1], g[2 * r + 1]);
+        }
+    } else {
+        KCT_CUDA(cudaMemcpyAsync(mm, w.scal, sizeof mm, cudaMemcpyDeviceToHost, stream));
+        KCT_CUDA(cudaStreamSynchronize(stream));
+    }
     const double range = mm[1] - mm[0];
     return range > 0.0 ? std::max(1e-8, 1e-4 * range) : 1e-4;
+}
+
+void check_slab(Projector& P) {
+    if (P.slab_mode() && !P.comm_fn)
+        throw ConfigError("y-slab mode needs the all-reduce hook (kct_set_allreduce)");
+}
+
+void set_grid(RegCfg& rc, Projector& P) {
+    rc.nx = P.grid().nx;
+    rc.ny = P.grid().ny;
+    rc.nz = P.grid().nz;
+    rc.j0 = P.slab_mode() ? P.slab_j0 : 0;
+    rc.nyg = P.slab_mode() ? P.slab_nyg : rc.ny;
 }
 
 void copy_hist(double* dst, const double* src, size_t n, cudaStream_t s) {
@@ -918,15 +1004,17 @@ void cgls_recon(Projector& P, const float* b, size_t iters, const float* x0, con
     if (!b || !x_out) throw ConfigError("cgls_recon: null buffer");
     if (iters < 1) throw ConfigError("reconstruction needs at least one iteration");
     reset_report(rep);
+    check_slab(P);
     Workspace& w = workspace(P, iters, 1);
-    if (gt) ensure(w.gt, w.m);
+    if (gt) ensure_vol(w, w.gt);
     load(P, w.b, b, w.n, false, mem, layout, stream);
     if (x0) load(P, w.x, x0, w.m, true, mem, layout, stream);
     else KCT_CUDA(cudaMemsetAsync(w.x, 0, w.m * sizeof(float), stream));
     if (gt) load(P, w.gt, gt, w.m, true, mem, layout, stream);
     init_ctl(w, 0.0, 0.0, stream);
     Engine e{P, w, stream};
-    e.rc.nx = P.grid().nx; e.rc.ny = P.grid().ny; e.rc.nz = P.grid().nz;
+    set_grid(e.rc, P);
+    e.halo(w.x);
     if (gt) e.ground_truth_norm();
     KCT_CUDA(cudaStreamSynchronize(stream));
 
@@ -975,13 +1063,14 @@ void irn_solve(Projector& P, int kind, const float* b, const float* prior, const
     const double lambda = p.lambda < 0.0 ? alpha : p.lambda;
     const size_t outer = p.outer_iters, inner = p.inner_iters;
     reset_report(rep);
+    check_slab(P);
 
     Workspace& w = workspace(P, outer * inner, outer + 1);
     const bool use_prior = kind != KCT_KIND_TV;
-    if (use_prior) ensure(w.prior, w.m);
-    if (alpha != 0.0) ensure(w.w1, w.m);
-    if (kind == KCT_KIND_PICCS && lambda != 0.0) ensure(w.w2, w.m);
-    if (gt) ensure(w.gt, w.m);
+    if (use_prior) ensure_vol(w, w.prior);
+    if (alpha != 0.0) ensure_vol(w, w.w1);
+    if (kind == KCT_KIND_PICCS && lambda != 0.0) ensure_vol(w, w.w2);
+    if (gt) ensure_vol(w, w.gt);
     load(P, w.b, b, w.n, false, mem, layout, stream);
     if (use_prior) load(P, w.prior, prior, w.m, true, mem, layout, stream);
     if (x0) load(P, w.x, x0, w.m, true, mem, layout, stream);
@@ -990,11 +1079,13 @@ void irn_solve(Projector& P, int kind, const float* b, const float* prior, const
 
     // tau from the initial image, else the prior when the prior term is active
     const float* tau_ref = x0 ? w.x : ((use_prior && lambda != 0.0) ? w.prior : nullptr);
-    const double tau = device_tau(w, tau_ref, w.m, p.tau, stream);
+    const double tau = device_tau(P, w, tau_ref, w.m, p.tau, stream);
 
     Engine e{P, w, stream};
     e.kind = kind;
-    e.rc.nx = P.grid().nx; e.rc.ny = P.grid().ny; e.rc.nz = P.grid().nz;
+    set_grid(e.rc, P);
+    e.halo(w.x);
+    if (use_prior) e.halo(w.prior);
     e.rc.use_w1 = alpha != 0.0;
     e.rc.mode2 = lambda == 0.0 ? 0 : (kind == KCT_KIND_PICCS ? 1 : (kind == KCT_KIND_PIPLE ? 2 : 0));
     e.rc.alpha2 = (float)(alpha * alpha);
@@ -1018,6 +1109,7 @@ void irn_solve(Projector& P, int kind, const float* b, const float* prior, const
         } else {
             if (cycle == 0) e.objective(x_zero, 0);
             KCT_CUDA(cudaMemsetAsync(w.x, 0, w.m * sizeof(float), stream));
+            e.halo(w.x);
             e.start(true, p.inner_tolerance, -1);
         }
         x_zero = false;

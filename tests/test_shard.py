@@ -111,3 +111,22 @@ def test_decomposition_is_exact_float64():
         blk = ora.adjoint(osl, geom, y).reshape(grid.nz, y1 - y0, grid.nx)
         ref = full_adj.reshape(grid.nz, grid.ny, grid.nx)[:, y0:y1, :]
         np.testing.assert_allclose(blk, ref, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 5])
+def test_y_slab_split_and_assemble_round_trip(world):
+    """distributed.y_slab / assemble_y_slabs (reference layout, x-fastest)."""
+    from paper_2509_08574_b200 import distributed
+    grid = k.GridSpec((5, 11, 4), (1.0, 1.0, 1.0))
+    vol = np.arange(grid.count(), dtype=np.float32)
+    parts = []
+    for r in range(world):
+        j0, j1 = shard.slab_range(grid.dims[1], world, r)
+        sl = distributed.y_slab(vol, grid, j0, j1)
+        assert sl.size == 5 * (j1 - j0) * 4
+        parts.append(sl)
+    np.testing.assert_array_equal(distributed.assemble_y_slabs(parts, grid), vol)
+    sg = shard.slab_grid(grid, world, world - 1, axis="y")
+    j0, j1 = shard.slab_range(grid.dims[1], world, world - 1)
+    assert sg.dims == (5, j1 - j0, 4)
+    assert sg.origin[1] == pytest.approx(grid.origin[1] + j0 * grid.spacing[1])

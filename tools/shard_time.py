@@ -30,18 +30,25 @@ geom = k.ConeBeamGeometry(synth.DSO, synth.DSD, cfg.det, cfg.det, cfg.pitch, cfg
 y = torch.rand(geom.ray_count(), device="cuda")
 x = torch.rand(grid.count(), device="cuda")
 for N in [int(a) for a in sys.argv[1:]] or [1, 2, 4, 8]:
-    tf, tz, ty = [], [], []
+    tf, tz, ty, tfy, ta = [], [], [], [], []
     for r in range(N):
         Af = k.ConeBeamProjector(grid, shard.shard_geometry(geom, N, r))
         q = torch.empty(Af.range_size(), device="cuda")
         tf.append(t_op(lambda: Af.apply(x, out=q)))
+        vb = torch.empty(Af.domain_size(), device="cuda")
+        qa = torch.rand(Af.range_size(), device="cuda")
+        ta.append(t_op(lambda: Af.apply_adjoint(qa, out=vb)))  # angle-sharded solver's adjoint
         del Af
         for axis, acc in (("z", tz), ("y", ty)):
             g = shard.slab_grid(grid, N, r, axis=axis)
             Ab = k.ConeBeamProjector(g, geom)
             b = torch.empty(Ab.domain_size(), device="cuda")
             acc.append(t_op(lambda: Ab.apply_adjoint(y, out=b)))
+            if axis == "y":  # the slab solver's forward: this slab's share of every ray
+                xs = torch.rand(Ab.domain_size(), device="cuda")
+                qs = torch.empty(Ab.range_size(), device="cuda")
+                tfy.append(t_op(lambda: Ab.apply(xs, out=qs)))
             del Ab
-    print(f"N={N} fwd max {max(tf):.3f} ms | adj z-slab max {max(tz):.3f} "
+    print(f"N={N} fwd max {max(tf):.3f} ms | adj angle-shard max {max(ta):.3f} | adj z-slab max {max(tz):.3f} "
           f"[{' '.join(f'{t:.2f}' for t in tz)}] | adj y-slab max {max(ty):.3f} "
-          f"[{' '.join(f'{t:.2f}' for t in ty)}]", flush=True)
+          f"[{' '.join(f'{t:.2f}' for t in ty)}] | fwd y-slab max {max(tfy):.3f}", flush=True)
