@@ -871,6 +871,11 @@ Projector::~Projector() {
     cudaFree(d_rows_);
     cudaFree(d_border_);
     cudaFree(d_forder_);
+    cudaFree(d_fpipe_);
+    if (pipe_stream_) {
+        for (auto e : pipe_ev_) cudaEventDestroy(e);
+        cudaStreamDestroy(pipe_stream_);
+    }
     cudaFree(d_queue_);
     cudaFree(d_part_);
     cudaFree(d_yw_);
@@ -1021,6 +1026,27 @@ void Projector::build_tables(const kct_geometry& geom) {
         if (!(fo && std::string(fo) == "0")) {
             KCT_CUDA(cudaMalloc(&d_forder_, nitems * sizeof(int)));
             KCT_CUDA(cudaMemcpy(d_forder_, order.data(), nitems * sizeof(int), cudaMemcpyHostToDevice));
+            // the same order restricted to each host-path pipeline chunk of angles
+            // (items re-indexed relative to the chunk's first angle)
+            pipe_chunks_ = na >= 4 * kPipeMinAngles ? kPipeChunks : 1;
+            if (pipe_chunks_ > 1) {
+                std::vector<int> pord;
+                pipe_off_.assign(pipe_chunks_ + 1, 0);
+                const size_t per_angle = (size_t)nq * fwd_bands_;
+                for (int c = 0; c < pipe_chunks_; ++c) {
+                    const int a0 = pipe_angle(c), a1 = pipe_angle(c + 1);
+                    pipe_off_[c] = (int)pord.size();
+                    for (size_t t = 0; t < nitems; ++t) {
+                        const int it = key[t].second;
+                        const int a = (int)(it / per_angle);
+                        if (a >= a0 && a < a1) pord.push_back(it - (int)(a0 * per_angle));
+                    }
+                }
+                pipe_off_[pipe_chunks_] = (int)pord.size();
+                KCT_CUDA(cudaMalloc(&d_fpipe_, pord.size() * sizeof(int)));
+                KCT_CUDA(cudaMemcpy(d_fpipe_, pord.data(), pord.size() * sizeof(int),
+                                    cudaMemcpyHostToDevice));
+            }
         }
     }
     const int kc = (nz + 31) / 32;
@@ -1237,12 +1263,39 @@ void Projector::forward(const float* vol, float* proj, cudaStream_t s) const {
                       d_forder_, s);
 }
 
+void Projector::forward_range(const float* vol, float* proj, int a_begin, int a_end,
+                              cudaStream_t s) const {
+    if (a_begin == 0 && a_end == dg_.na) return forward(vol, proj, s);
+    DevGeom g = dg_;
+    g.na = a_end - a_begin;
+    // the block order of a pipeline chunk when the range is one (else natural order)
+    const int* order = nullptr;
+    for (int c = 0; c < pipe_chunks_; ++c)
+        if (pipe_angle(c) == a_begin && pipe_angle(c + 1) == a_end && d_fpipe_)
+            order = d_fpipe_ + pipe_off_[c];
+    launch_fwd<false>(fwd_c_, fwd_bands_, vol, proj + (size_t)a_begin * dg_.nu * dg_.nv,
+                      d_cols_ + (size_t)a_begin * dg_.nu, d_dv_, d_invdv_, d_dvd_, g, order, s);
+}
+
+cudaStream_t Projector::pipe_stream() {
+    if (!pipe_stream_) {
+        KCT_CUDA(cudaStreamCreateWithFlags(&pipe_stream_, cudaStreamNonBlocking));
+        for (auto& e : pipe_ev_) KCT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    return pipe_stream_;
+}
+
 void Projector::count(float* proj, cudaStream_t s) const {
     launch_fwd<true>(fwd_c_, fwd_bands_, nullptr, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_,
                      d_forder_, s);
 }
 
 void Projector::adjoint(const float* proj, float* vol, cudaStream_t s) const {
+    adjoint_range(proj, vol, 0, dg_.na, false, s);
+}
+
+void Projector::adjoint_range(const float* proj, float* vol, int a_begin, int a_end,
+                              bool accumulate, cudaStream_t s) const {
     AngleBatch ab;
     BrickCfg bc;
     bc.bz = adj_bz_;
@@ -1254,10 +1307,10 @@ void Projector::adjoint(const float* proj, float* vol, cudaStream_t s) const {
     bc.gstride = m_;
     const int nctas = (bc.nbx * bc.nby * bc.nbz * bc.ngrp + kAdjWarps - 1) / kAdjWarps;
     const size_t smem = adj_smem_bytes();
-    for (int a0 = 0; a0 < dg_.na; a0 += kMaxAnglesPerLaunch) {
-        const int nab = std::min(kMaxAnglesPerLaunch, dg_.na - a0);
+    for (int a0 = a_begin; a0 < a_end; a0 += kMaxAnglesPerLaunch) {
+        const int nab = std::min(kMaxAnglesPerLaunch, a_end - a0);
         for (int q = 0; q < nab; ++q) ab.cs[q] = cs_[a0 + q];
-        const int accum = a0 > 0 ? 1 : 0;
+        const int accum = (a0 > a_begin || accumulate) ? 1 : 0;
         const ColParams* cols = d_cols_ + (size_t)a0 * dg_.nu;
         const float* pr = proj + (size_t)a0 * dg_.nu * dg_.nv;
 #if KCT_ADJ_PREWEIGHT
@@ -1311,6 +1364,16 @@ void Projector::proj_to_native(const float* ref, float* nat, cudaStream_t s) con
 }
 void Projector::proj_from_native(const float* nat, float* ref, cudaStream_t s) const {
     launch_transpose(nat, ref, dg_.na, dg_.nu, dg_.nv, s);
+}
+void Projector::proj_to_native_range(const float* ref, float* nat, int a0, int a1,
+                                     cudaStream_t s) const {
+    const size_t off = (size_t)a0 * dg_.nu * dg_.nv;
+    launch_transpose(ref + off, nat + off, a1 - a0, dg_.nv, dg_.nu, s);
+}
+void Projector::proj_from_native_range(const float* nat, float* ref, int a0, int a1,
+                                       cudaStream_t s) const {
+    const size_t off = (size_t)a0 * dg_.nu * dg_.nv;
+    launch_transpose(nat + off, ref + off, a1 - a0, dg_.nu, dg_.nv, s);
 }
 
 }  // namespace kct

@@ -30,6 +30,18 @@ class Projector {
     // Native-layout, device-resident operators (stream-ordered).
     void forward(const float* vol, float* proj, cudaStream_t s) const;
     void adjoint(const float* proj, float* vol, cudaStream_t s) const;
+    // Angle sub-ranges [a_begin, a_end) (full-size native buffers; the
+    // adjoint adds into `vol` when accumulate).
+    void forward_range(const float* vol, float* proj, int a_begin, int a_end,
+                       cudaStream_t s) const;
+    void adjoint_range(const float* proj, float* vol, int a_begin, int a_end, bool accumulate,
+                       cudaStream_t s) const;
+    // Host-buffer pipeline (capi.cu): angle chunks, a copy stream and events.
+    static constexpr int kPipeChunks = 4, kPipeMinAngles = 4;
+    int pipe_chunks() const { return pipe_chunks_; }
+    int pipe_angle(int c) const { return (int)((long long)dg_.na * c / pipe_chunks_); }
+    cudaStream_t pipe_stream();
+    cudaEvent_t pipe_event(int i) const { return pipe_ev_[i]; }
     // Per-ray count of positive-length Siddon segments (as float) into proj.
     void count(float* proj, cudaStream_t s) const;
     // FDK (fdk.hpp:50-139), native layouts; `filt` is N floats of scratch.
@@ -40,6 +52,8 @@ class Projector {
     void vol_from_native(const float* nat, float* ref, cudaStream_t s) const;
     void proj_to_native(const float* ref, float* nat, cudaStream_t s) const;
     void proj_from_native(const float* nat, float* ref, cudaStream_t s) const;
+    void proj_to_native_range(const float* ref, float* nat, int a0, int a1, cudaStream_t s) const;
+    void proj_from_native_range(const float* nat, float* ref, int a0, int a1, cudaStream_t s) const;
 
     // Lazily allocated scratch used by the C-ABI for host / reference-layout calls.
     float* scratch(int slot, size_t n);
@@ -86,6 +100,11 @@ class Projector {
     bool adj_gather_ = false;
     int* d_border_ = nullptr;         // brick order of the adjoint queue
     int* d_forder_ = nullptr;         // forward block -> item order (longest chords first)
+    int* d_fpipe_ = nullptr;          // the same per pipeline chunk (offsets pipe_off_)
+    std::vector<int> pipe_off_;
+    int pipe_chunks_ = 1;
+    cudaStream_t pipe_stream_ = nullptr;
+    cudaEvent_t pipe_ev_[kPipeChunks] = {};
     int* d_queue_ = nullptr;          // adjoint brick queue counter
     int adj_ctas_ = 0;                // resident CTAs of the persistent adjoint grid
     int adj_groups_ = 1;              // angle groups of the adjoint (small problems)

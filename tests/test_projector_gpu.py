@@ -179,6 +179,17 @@ def test_handles_with_different_bricks_coexist(ora):
     assert rel_l2(B.apply_adjoint(y), ora.adjoint(short, geom, y)) < TOL
 
 
+def test_host_pipeline_is_bitwise(monkeypatch):
+    """kct_forward with host buffers runs in angle chunks whose projections
+    leave the device while the next chunk is computed: same bits."""
+    grid, geom = baseline_geometry(1, n_angles=64)
+    x = np.random.default_rng(12).uniform(0, 0.04, grid.count).astype(np.float32)
+    piped = projector(grid, geom).apply(x)
+    monkeypatch.setenv("KCT_HOST_PIPELINE", "0")
+    plain = projector(grid, geom).apply(x)
+    assert np.array_equal(piped, plain)
+
+
 def test_more_than_one_angle_batch(ora):
     """> 1024 angles: several launches accumulate (angle batches in param space)."""
     grid, geom = tiny_grid(6, 5, 6), tiny_geometry(1100)
