@@ -25,9 +25,6 @@ constexpr float kInf = __builtin_huge_valf();
 #ifndef KCT_ROW_VERIFY
 #define KCT_ROW_VERIFY 1  // adjoint row z-state: verify the estimate, search only on failure
 #endif
-#ifndef KCT_ADJ_PREWEIGHT
-#define KCT_ADJ_PREWEIGHT 1  // adjoint input pre-scaled per ray (adj_weight_kernel)
-#endif
 constexpr unsigned kFull = 0xffffffffu;
 
 // ----------------------------------------------------------------------------
@@ -268,7 +265,21 @@ struct RowZ {
     float f0, imk, wz, yf;
 };
 
-__device__ __forceinline__ void row_init(RowZ& r, bool on, int iv, const ColParams& cp, float lo,
+// The per-(angle, column) values the row z-state needs (a ColParams subset;
+// carried in the walk-table entries so the adjoint never loads ColParams).
+struct RowCol {
+    float w_in, inv_h1;
+    double g_in;
+};
+__device__ __forceinline__ RowCol row_col(const ColParams& cp) {
+    RowCol r;
+    r.w_in = cp.w_in;
+    r.inv_h1 = cp.inv_h1;
+    r.g_in = cp.g_in;
+    return r;
+}
+
+__device__ __forceinline__ void row_init(RowZ& r, bool on, int iv, const RowCol& cp, float lo,
                                          float h1, int K0, int kend,
                                          const RowTab* __restrict__ rows,
                                          const float* __restrict__ ycol, const DevGeom& g) {
@@ -289,12 +300,7 @@ __device__ __forceinline__ void row_init(RowZ& r, bool on, int iv, const ColPara
     r.k0 = k0;
     r.f0 = (float)(kzd - (double)k0);
     r.imk = __fmul_rn(rt.invdv, cp.inv_h1);
-#if KCT_ADJ_PREWEIGHT
     r.yf = __ldg(ycol + iv);  // y * sqrt(1 + (dv inv_l)^2), adj_weight_kernel
-#else
-    const float q = dv * cp.inv_l;
-    r.yf = __ldg(ycol + iv) * __fsqrt_rn(__fmaf_rn(q, q, 1.f));
-#endif
     // slab at lo: last plane crossed strictly before lo (forward semantics);
     // the float estimate is corrected with the exact crossing expression
     int k = k0 + (int)floorf(r.f0 + (lo - cp.w_in) * (dv * h1));
@@ -463,7 +469,7 @@ __device__ __forceinline__ int brick_walk(const ColParams& cp, const DevGeom& g,
 
 // ---- the rows of one (brick, detector column): C per lane, passes of stride S ----
 template <int C>
-__device__ __forceinline__ void brick_rows(const Seg* segs, int nseg, const ColParams& cp, float lo,
+__device__ __forceinline__ void brick_rows(const Seg* segs, int nseg, const RowCol& cp, float lo,
                                            int rlo, int rhi, int S, int K0, int kend, int lane,
                                            const RowTab* __restrict__ rows,
                                            const float* __restrict__ ycol, const DevGeom& g) {
@@ -494,14 +500,13 @@ __device__ __forceinline__ void brick_rows(const Seg* segs, int nseg, const ColP
 // for every application.  64 bytes per entry. ----
 struct __align__(16) WalkEntry {
     float bnd[8];            // segment boundaries, lo = bnd[0] .. hi = bnd[nseg]
-    unsigned char ij[8];     // per segment: (i - I0) + BX (j - J0)
+    unsigned char ij[8];     // per segment: (i - I0) + BX (j - J0); ij[7] = nseg
     unsigned short ia, iu;   // angle (global index), detector column
     unsigned short rlo, rhi; // detector rows crossing the brick
-    int nseg;
-    int pad[3];
+    RowCol rc;               // the column's row z-state inputs
 };
 static_assert(sizeof(WalkEntry) == 64, "WalkEntry layout");
-constexpr int kTabMaxSeg = 8;
+constexpr int kTabMaxSeg = 7;
 constexpr bool kTabOk = BX + BY - 1 <= kTabMaxSeg && BX * BY <= 256;
 
 __device__ __forceinline__ BrickGeo brick_geo(int brick, const BrickCfg& bc, const DevGeom& g) {
@@ -548,11 +553,12 @@ __global__ void __launch_bounds__(128) adj_walk_build(const ColParams* __restric
                 if (lane <= nseg) E->bnd[lane] = sbnd[warp][lane];
                 if (lane < nseg) E->ij[lane] = (unsigned char)ij;
                 if (lane == 0) {
+                    E->ij[7] = (unsigned char)nseg;
                     E->ia = (unsigned short)ia;
                     E->iu = (unsigned short)iu;
                     E->rlo = (unsigned short)rlo;
                     E->rhi = (unsigned short)rhi;
-                    E->nseg = nseg;
+                    E->rc = row_col(cp);
                 }
             }
             ++e;
@@ -629,15 +635,22 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
         const unsigned long long* ob = off + (size_t)brick * (g.na + 1);
         const unsigned long long e0 = ob[a0 + a_lo], e1 = ob[a0 + a_hi];
         const unsigned* tw = reinterpret_cast<const unsigned*>(tab);
+        // lanes 0..15 hold one 64-byte entry; the next one is fetched while
+        // the current one's rows run
+        unsigned w = (e0 < e1 && lane < 16) ? __ldg(tw + e0 * 16 + lane) : 0u;
         for (unsigned long long e = e0; e < e1; ++e) {
-            // lanes 0..15 fetch the 64-byte entry, shuffles distribute it
-            const unsigned w = lane < 16 ? __ldg(tw + e * 16 + lane) : 0u;
-            const int nseg = (int)__shfl_sync(kFull, w, 12);
-            const unsigned aiu = __shfl_sync(kFull, w, 10), rr = __shfl_sync(kFull, w, 11);
+            const unsigned ijw1 = __shfl_sync(kFull, w, 9);
+            const int nseg = (int)(ijw1 >> 24);
+            const unsigned rr = __shfl_sync(kFull, w, 11);
             const float wa = __uint_as_float(__shfl_sync(kFull, w, lane & 7));
             const float wb = __uint_as_float(__shfl_sync(kFull, w, (lane + 1) & 7));
             const unsigned ijw = __shfl_sync(kFull, w, 8 + ((lane >> 2) & 1));
             const float lo = __uint_as_float(__shfl_sync(kFull, w, 0));
+            const unsigned aiu = __shfl_sync(kFull, w, 10);
+            RowCol rcp;
+            rcp.w_in = __uint_as_float(__shfl_sync(kFull, w, 12));
+            rcp.inv_h1 = __uint_as_float(__shfl_sync(kFull, w, 13));
+            rcp.g_in = __hiloint2double((int)__shfl_sync(kFull, w, 15), (int)__shfl_sync(kFull, w, 14));
             if (lane < nseg) {
                 const unsigned ij = (ijw >> (8 * (lane & 3))) & 0xffu;
                 Seg sg;
@@ -647,10 +660,10 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
                 sg.pad = 0;
                 segs[lane] = sg;
             }
+            w = (e + 1 < e1 && lane < 16) ? __ldg(tw + (e + 1) * 16 + lane) : 0u;
             __syncwarp();
             const size_t cidx = (size_t)((int)(aiu & 0xffffu) - a0) * nu + (aiu >> 16);
-            const ColParams cp = cols[cidx];
-            brick_rows<C>(segs, nseg, cp, lo, (int)(rr & 0xffffu), (int)(rr >> 16), S, K0, kend,
+            brick_rows<C>(segs, nseg, rcp, lo, (int)(rr & 0xffffu), (int)(rr >> 16), S, K0, kend,
                           lane, rows, proj + cidx * nv, g);
             __syncwarp();
         }
@@ -677,7 +690,7 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
                     segs[lane] = sg;
                 }
                 __syncwarp();
-                brick_rows<C>(segs, nseg, cp, lo, rlo, rhi, S, K0, kend, lane, rows,
+                brick_rows<C>(segs, nseg, row_col(cp), lo, rlo, rhi, S, K0, kend, lane, rows,
                               yb + (size_t)iu * nv, g);
                 __syncwarp();
             }
@@ -1113,10 +1126,8 @@ void Projector::build_tables(const kct_geometry& geom) {
         if (G > 1) KCT_CUDA(cudaMalloc(&d_part_, (size_t)(G - 1) * m_ * sizeof(float)));
     }
 
-#if KCT_ADJ_PREWEIGHT
     if (!adj_gather_)
         KCT_CUDA(cudaMalloc(&d_yw_, (size_t)std::min(na, kMaxAnglesPerLaunch) * nu * nv * sizeof(float)));
-#endif
 
     // brick queue: persistent grid of resident CTAs, bricks heaviest first
     // (by xy distance of the brick centre from the rotation axis, then by z
@@ -1313,7 +1324,6 @@ void Projector::adjoint_range(const float* proj, float* vol, int a_begin, int a_
         const int accum = (a0 > a_begin || accumulate) ? 1 : 0;
         const ColParams* cols = d_cols_ + (size_t)a0 * dg_.nu;
         const float* pr = proj + (size_t)a0 * dg_.nu * dg_.nv;
-#if KCT_ADJ_PREWEIGHT
         if (!adj_gather_) {
             const size_t nb = (size_t)nab * dg_.nu * dg_.nv;
             adj_weight_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(
@@ -1321,7 +1331,6 @@ void Projector::adjoint_range(const float* proj, float* vol, int a_begin, int a_
             KCT_LAUNCHED();
             pr = d_yw_;
         }
-#endif
         if (adj_gather_) {
             const int K = adj_k_;
             dim3 grid((dg_.nx * dg_.ny + 3) / 4, (dg_.nz + 32 * K - 1) / (32 * K), 1);
