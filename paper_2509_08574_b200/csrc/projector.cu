@@ -1164,12 +1164,16 @@ void Projector::build_tables(const kct_geometry& geom) {
 // the adjoint, 64 bytes each, built once per projector.  Skipped (the adjoint
 // then recomputes the walks) when disabled (KCT_ADJ_TABLE=0), when an index
 // does not fit the entry, or above the memory budget (KCT_ADJ_TABLE_MB,
-// default 8192).
+// default a quarter of the free device memory).
 void Projector::build_walk_table() {
     const char* en = std::getenv("KCT_ADJ_TABLE");
     if (adj_gather_ || !kTabOk || (en && std::string(en) == "0")) return;
     if (dg_.na > 65535 || dg_.nu > 65535 || dg_.nv > 65535) return;
-    size_t budget = 8192ull << 20;
+    // budget: a quarter of the free device memory (B200: ~45 GB, enough for
+    // c4's 720-view prior, 28 GB), or KCT_ADJ_TABLE_MB
+    size_t free_b = 0, total_b = 0;
+    KCT_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    size_t budget = free_b / 4;
     if (const char* e = std::getenv("KCT_ADJ_TABLE_MB")) budget = (size_t)std::atoll(e) << 20;
     BrickCfg bc{};
     bc.bz = adj_bz_;
