@@ -44,6 +44,16 @@ def launches(tag, path):
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"{k[:70]:70s} {len(v):4d} {sum(v):10.3f} {sum(v) / len(v):9.3f} "
                      f"{100 * sum(v) / tot:5.1f}%")
+    # the step's own kernels: launched once per warm-up / timed step (the
+    # most frequent count); setup kernels (nnz count, walk table) excluded
+    counts = collections.Counter(len(v) for v in agg.values())
+    per_step = counts.most_common(1)[0][0]
+    step = {k: v for k, v in agg.items() if len(v) == per_step}
+    st = sum(sum(v) for v in step.values())
+    lines += ["", f"# per bench step (kernels launched {per_step}x = once per step):",
+              f"{'kernel':70s} {'mean_ms':>9s} {'share':>6s}"]
+    for k, v in sorted(step.items(), key=lambda kv: -sum(kv[1])):
+        lines.append(f"{k[:70]:70s} {sum(v) / len(v):9.3f} {100 * sum(v) / st:5.1f}%")
     open(os.path.join(PROF, f"{tag}_launches.txt"), "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
