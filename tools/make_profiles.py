@@ -44,10 +44,10 @@ def launches(tag, path):
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"{k[:70]:70s} {len(v):4d} {sum(v):10.3f} {sum(v) / len(v):9.3f} "
                      f"{100 * sum(v) / tot:5.1f}%")
-    # the step's own kernels: launched once per warm-up / timed step (the
-    # most frequent count); setup kernels (nnz count, walk table) excluded
-    counts = collections.Counter(len(v) for v in agg.values())
-    per_step = counts.most_common(1)[0][0]
+    # the step's own kernels: launched as often as the dominant kernel (once
+    # per warm-up / timed step); setup kernels (nnz count, walk table) excluded
+    top = max(agg.items(), key=lambda kv: sum(kv[1]))
+    per_step = len(top[1])
     step = {k: v for k, v in agg.items() if len(v) == per_step}
     st = sum(sum(v) for v in step.values())
     lines += ["", f"# per bench step (kernels launched {per_step}x = once per step):",
