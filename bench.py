@@ -428,8 +428,10 @@ def run_recon(k, synth, cfg, grid, prior, follow, dev, args, ws=1, rank=0, share
     prior_h = A.volume_from_native(prior_s).cpu().pin_memory().numpy()
     b_h = torch.from_numpy(np.ascontiguousarray(proj_h.data, dtype=np.float32)).pin_memory().numpy()
     proj_hp = k.ProjectionSet(proj_h.geometry, b_h)
-    k.irn_piccs(proj_hp, grid_s, prior_h, params, projector=A)
-    rep_h, e2e = timed(lambda: k.irn_piccs(proj_hp, grid_s, prior_h, params, projector=A))
+    x_h = torch.empty(grid_s.count(), dtype=torch.float32).pin_memory().numpy()
+    k.irn_piccs(proj_hp, grid_s, prior_h, params, projector=A, out=x_h)
+    rep_h, e2e = timed(lambda: k.irn_piccs(proj_hp, grid_s, prior_h, params, projector=A,
+                                           out=x_h))
     same = rsum([float(np.abs(rep_h.volume - x_ref).max())], op="max")[0]
     return {"seconds_per_recon": round(float(np.median(reps)), 4),
             "all_seconds": [round(r, 4) for r in reps],

@@ -484,10 +484,20 @@ def _same_mem(args):
     return mems.pop() if mems else MEM_HOST
 
 
+def _out_for(arg: _Arg, m: int, out):
+    """The caller's output buffer (e.g. pinned host memory) or a new one."""
+    if out is None:
+        return _alloc_like(arg, m)
+    if (out.numel() if _is_torch(out) else np.asarray(out).size) != m:
+        raise ConfigError("output size mismatch")
+    return out
+
+
 def cgls_recon(proj: ProjectionSet, grid: GridSpec, iters: int, opts: ReconOptions | None = None,
                tolerance: float = 0.0, projector: ConeBeamProjector | None = None,
-               layout=None) -> ReconReport:
-    """Unregularised least squares from zero (recon.hpp:312-315)."""
+               layout=None, out=None) -> ReconReport:
+    """Unregularised least squares from zero (recon.hpp:312-315).  `out`: an
+    optional caller buffer for the volume (same memory kind as the data)."""
     opts = opts or ReconOptions()
     A = _projector_for(proj, grid, projector)
     m, n = A.domain_size(), A.range_size()
@@ -495,7 +505,7 @@ def cgls_recon(proj: ProjectionSet, grid: GridSpec, iters: int, opts: ReconOptio
     x0 = _Arg(opts.initial, m, "initial") if opts.initial is not None else None
     gt = _Arg(opts.ground_truth, m, "ground truth") if opts.ground_truth is not None else None
     mem = _same_mem([b, x0, gt])
-    out = _alloc_like(b, m)
+    out = _out_for(b, m, out)
     rep, bufs = _report_buffers(iters, iters, 1)
     _check(_lib.kct_cgls_recon(A.handle, b.ptr, int(iters), x0.ptr if x0 else None,
                                gt.ptr if gt else None, float(tolerance), _ptr(out), C.byref(rep),
@@ -504,7 +514,7 @@ def cgls_recon(proj: ProjectionSet, grid: GridSpec, iters: int, opts: ReconOptio
     return _unpack(rep, bufs, out)
 
 
-def _irn(kind, proj, grid, prior, params, opts, projector, layout):
+def _irn(kind, proj, grid, prior, params, opts, projector, layout, out=None):
     params = params or RegularizationParams()
     opts = opts or ReconOptions()
     A = _projector_for(proj, grid, projector)
@@ -514,7 +524,7 @@ def _irn(kind, proj, grid, prior, params, opts, projector, layout):
     x0 = _Arg(opts.initial, m, "initial") if opts.initial is not None else None
     gt = _Arg(opts.ground_truth, m, "ground truth") if opts.ground_truth is not None else None
     mem = _same_mem([b, pr, x0, gt])
-    out = _alloc_like(b, m)
+    out = _out_for(b, m, out)
     o, i = int(params.outer_iters), int(params.inner_iters)
     rep, bufs = _report_buffers(o + 1, o * i, o)
     p = params._c()
@@ -525,19 +535,21 @@ def _irn(kind, proj, grid, prior, params, opts, projector, layout):
     return _unpack(rep, bufs, out)
 
 
-def irn_tv(proj, grid, params=None, opts=None, projector=None, layout=None) -> ReconReport:
+def irn_tv(proj, grid, params=None, opts=None, projector=None, layout=None,
+           out=None) -> ReconReport:
     """recon.hpp:252-255."""
-    return _irn(KIND_TV, proj, grid, None, params, opts, projector, layout)
+    return _irn(KIND_TV, proj, grid, None, params, opts, projector, layout, out)
 
 
-def irn_piple(proj, grid, prior, params=None, opts=None, projector=None, layout=None):
+def irn_piple(proj, grid, prior, params=None, opts=None, projector=None, layout=None, out=None):
     """recon.hpp:260-263."""
-    return _irn(KIND_PIPLE, proj, grid, prior, params, opts, projector, layout)
+    return _irn(KIND_PIPLE, proj, grid, prior, params, opts, projector, layout, out)
 
 
-def irn_piccs(proj, grid, prior, params=None, opts=None, projector=None, layout=None):
-    """recon.hpp:267-270 — the north-star entry point."""
-    return _irn(KIND_PICCS, proj, grid, prior, params, opts, projector, layout)
+def irn_piccs(proj, grid, prior, params=None, opts=None, projector=None, layout=None, out=None):
+    """recon.hpp:267-270 — the north-star entry point.  `out`: optional caller
+    buffer for the volume (e.g. pinned host memory for fast copies)."""
+    return _irn(KIND_PICCS, proj, grid, prior, params, opts, projector, layout, out)
 
 
 def fdk(proj: ProjectionSet, grid: GridSpec, projector: ConeBeamProjector | None = None,
