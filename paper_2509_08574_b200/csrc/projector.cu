@@ -1023,6 +1023,10 @@ void Projector::build_tables(const kct_geometry& geom) {
         const int nq = (nu + kFwdWarps - 1) / kFwdWarps;
         const size_t nitems = (size_t)nq * fwd_bands_ * na;
         std::vector<std::pair<float, int>> key(nitems);
+        // bands in turn, longest chords first within a band: the volume's z
+        // range a band's rays touch stays in L2 (c4: 24.0 -> 20.6 ms; c3 +-0)
+        const char* fob = std::getenv("KCT_FWD_ORDER");
+        const bool band_major = !(fob && std::string(fob) == "chord");
         for (size_t t = 0; t < nitems; ++t) {
             const int quad = (int)(t % nq), a = (int)(t / ((size_t)nq * fwd_bands_));
             float len = 0.f;
@@ -1031,6 +1035,10 @@ void Projector::build_tables(const kct_geometry& geom) {
                 len += std::max(0.f, cp.w_out - cp.w_in);
             }
             key[t] = {-len, (int)t};
+            if (band_major) {  // bands in turn: each band's z range of the volume stays in L2
+                const int band = (int)((t / nq) % fwd_bands_);
+                key[t].first = (float)band * 1e9f - len;
+            }
         }
         std::stable_sort(key.begin(), key.end());
         std::vector<int> order(nitems);
@@ -1138,11 +1146,15 @@ void Projector::build_tables(const kct_geometry& geom) {
         const int nbz = (nz + adj_bz_ - 1) / adj_bz_;
         const int nb = nbx * nby * nbz;
         std::vector<std::pair<double, int>> key(nb);
+        const char* zo = std::getenv("KCT_ADJ_ORDER");
+        const bool z_major = !(zo && std::string(zo) == "radius");
         for (int b = 0; b < nb; ++b) {
             const int bi = b % nbx, bj = (b / nbx) % nby, bk = b / (nbx * nby);
             const double cx = ox + (bi + 0.5) * BX * sx, cy = oy + (bj + 0.5) * BY * sy;
             const double cz = grid_.oz + (bk + 0.5) * adj_bz_ * sz;
             key[b] = {std::hypot(cx, cy) + 1e-3 * std::fabs(cz), b};
+            // z levels in turn: the detector rows they read stay in L2 (c4 -1%)
+            if (z_major) key[b].first += 1e6 * bk;
         }
         std::stable_sort(key.begin(), key.end());
         std::vector<int> order(nb);
