@@ -204,6 +204,9 @@ __global__ void __launch_bounds__(kBlock) k_reggrad(const float* __restrict__ sA
 // and all of a lane's loads independent, so the (L2 / DRAM latency bound)
 // scalar kernels become bandwidth bound.  Same arithmetic per voxel as the
 // scalar kernels; the partial sums add the 4 voxels of a lane in k order.
+#ifndef KCT_STENCIL_MINB
+#define KCT_STENCIL_MINB 4  // k_reggrad4: cap registers at 64 (2x the warps of the uncapped 118)
+#endif
 struct Nb4 {
     float f[6];           // f[0] = slab k-1, f[1..4] = slabs k..k+3, f[5] = slab k+4
     float4 ip, im, jp, jm;  // columns i+1, i-1, j+1, j-1 (0 outside the grid)
@@ -321,7 +324,7 @@ __device__ __forceinline__ void nb_sub(Nb4& a, const Nb4& b) {
     a.jm.x -= b.jm.x; a.jm.y -= b.jm.y; a.jm.z -= b.jm.z; a.jm.w -= b.jm.w;
 }
 
-__global__ void __launch_bounds__(kBlock) k_reggrad4(const float* __restrict__ sA,
+__global__ void __launch_bounds__(kBlock, KCT_STENCIL_MINB) k_reggrad4(const float* __restrict__ sA,
                                                      const float* __restrict__ x,
                                                      const float* __restrict__ xp,
                                                      const float* __restrict__ w1,
