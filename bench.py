@@ -304,24 +304,38 @@ def run_ours(args):
         out["fdk_ms"] = round(e0.elapsed_time(e1) / 3, 4)
 
     # ---- end to end through the C ABI with host buffers (reference layouts) ----
-    if rank == 0 and not args.skip_e2e:
+    # every rank: its forward (host volume in, host projections out) and its
+    # adjoint (host projections in, host volume slab out); whole-job rate over
+    # the slowest rank
+    if not args.skip_e2e:
         vol_h = torch.from_numpy(prior).pin_memory().numpy()
         proj_h = torch.empty(Nf, dtype=torch.float32).pin_memory().numpy()
-        back_h = torch.empty(M, dtype=torch.float32).pin_memory().numpy()
+        yb_h = proj_h if ws == 1 else y.cpu().pin_memory().numpy()
+        back_h = torch.empty(Mb, dtype=torch.float32).pin_memory().numpy()
+
+        def e2e_step():
+            A_f.apply(vol_h, out=proj_h)
+            A_b.apply_adjoint(yb_h, out=back_h)
+
         for _ in range(max(1, args.warmup)):
-            A_f.apply(vol_h, out=proj_h)
-            A_f.apply_adjoint(proj_h, out=back_h)
-        te = []
+            e2e_step()
+        if ws > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
         for _ in range(args.steps):
-            t0 = time.perf_counter()
-            A_f.apply(vol_h, out=proj_h)
-            A_f.apply_adjoint(proj_h, out=back_h)
-            te.append(time.perf_counter() - t0)
-        e2e_gups = 2.0 * M * len(my_angles) / float(np.mean(te)) / 1e9
+            e2e_step()
+        te = time.perf_counter() - t0
+        if ws > 1:
+            tt = torch.tensor([te], device="cpu" if shared else dev, dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e_gups = 2.0 * M * na * args.steps / te / 1e9
         out["e2e"] = {"value": round(e2e_gups, 3), "unit": "GUPS",
-                      "h2d_bytes_per_step": 4 * (M + Nf), "d2h_bytes_per_step": 4 * (Nf + M),
-                      "ms_per_step": round(1e3 * float(np.mean(te)), 3),
-                      "path": "kct_forward + kct_adjoint, pinned host, reference layouts"}
+                      "h2d_bytes_per_step": 4 * (M + (Nf if ws == 1 else Nb)),
+                      "d2h_bytes_per_step": 4 * (Nf + Mb),
+                      "ms_per_step": round(1e3 * te / args.steps, 3),
+                      "path": "kct_forward + kct_adjoint, pinned host, reference layouts"
+                              + ("" if ws == 1 else "; bytes per rank, time = slowest rank")}
 
     # ---- 20-iteration IRN-PICCS at c3 (the metric's second half) --------------
     if not args.skip_recon:
