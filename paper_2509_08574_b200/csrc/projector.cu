@@ -222,12 +222,8 @@ __device__ __forceinline__ void footprint(const DevGeom& g, float cth, float sth
 #endif
 constexpr int BX = KCT_BX, BY = KCT_BY;
 constexpr int kAdjWarps = KCT_ADJ_WARPS;
-#ifndef KCT_ADJ_ROWS
-#define KCT_ADJ_ROWS 2
-#endif
-constexpr int kAdjRows = KCT_ADJ_ROWS;  // rows per lane (C)
 constexpr int kMaxSeg = 16;  // (BX - 1) + (BY - 1) interior crossings + 1 (+ slack)
-constexpr int kMaxBz = 512;
+constexpr int kMaxBz = 512 * 16 / (BX * BY);  // brick smem stays below 227 KB per CTA
 
 struct __align__(16) Seg {
     float wa, wb;
@@ -240,6 +236,7 @@ struct BrickCfg {
     int S;   // row stride of a pass
     int nbx, nby, nbz;
     int ngrp;      // angle groups: work item = (brick, group of the batch's angles)
+    int slab;      // slab-lane deposits (brick_rows_slab): 0 off, 1 on, 2 on with slot-conflict detection
     size_t gstride;  // floats between the partial volumes of groups 1.. (group 0 -> out)
 };
 
@@ -257,12 +254,34 @@ __device__ __forceinline__ float lds_f(unsigned a) {
 __device__ __forceinline__ void sts_f(unsigned a, float v) {
     asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v));
 }
+__device__ __forceinline__ float4 lds_f4(unsigned a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_f4(unsigned a, float4 v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w));
+}
+__device__ __forceinline__ float2 lds_f2(unsigned a) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_f2(unsigned a, float2 v) {
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y));
+}
 
 // z state of one detector row inside a brick: the forward's per-ray state
-// (k0, f0, imk) restricted to the brick's slab planes [K0, kend].
+// (k0, f0, imk) restricted to the brick's slab planes [K0, kend].  wz is the
+// next z-plane crossing, wz2 the one after it when that lies beyond the
+// entry's chord (then the row crosses at most once more inside the entry and
+// the crossing takes the short path), else -inf (general path).
 struct RowZ {
     int k, kstep, k0;
-    float f0, imk, wz, yf;
+    float f0, imk, wz, wz2, yf;
 };
 
 // The per-(angle, column) values the row z-state needs (a ColParams subset;
@@ -279,10 +298,14 @@ __device__ __forceinline__ RowCol row_col(const ColParams& cp) {
     return r;
 }
 
-__device__ __forceinline__ void row_init(RowZ& r, bool on, int iv, const RowCol& cp, float lo,
+// Per-ray adjoint record, written once per application by adj_weight_kernel
+// (native layout, one float4 per ray): x = y * sqrt(1 + (dv inv_l)^2) (the
+// forward's 3D length factor), y = f0, z = imk, w = bits of 4 k0 + kstep + 1
+// — the forward's z state of the ray (fwd_kernel: k0, f0, imk), so the
+// per-(row, brick) set-up is one 16-byte load instead of a float64 split.
+__device__ __forceinline__ void row_init(RowZ& r, bool on, int iv, float w_in, float lo, float hi,
                                          float h1, int K0, int kend,
-                                         const RowTab* __restrict__ rows,
-                                         const float* __restrict__ ycol, const DevGeom& g) {
+                                         const float4* __restrict__ rec, const DevGeom& g) {
     if (!on) {
         r.k = K0 - 1;
         r.kstep = 0;
@@ -290,62 +313,58 @@ __device__ __forceinline__ void row_init(RowZ& r, bool on, int iv, const RowCol&
         r.f0 = 0.f;
         r.imk = 0.f;
         r.wz = kInf;
+        r.wz2 = kInf;
         r.yf = 0.f;
         return;
     }
-    const RowTab rt = ld_row(rows, iv);  // one 16-byte load: dv (f64, f32), 1/dv
-    const float dv = rt.dv;
-    const double kzd = fma(rt.dvd, cp.g_in, -g.kz0d);
-    const int k0 = __double2int_rd(kzd);
+    const float4 q = __ldg(rec + iv);
+    r.yf = q.x;
+    r.f0 = q.y;
+    r.imk = q.z;
+    const int code = __float_as_int(q.w);
+    const int k0 = code >> 2, sg = (code & 3) - 1;
     r.k0 = k0;
-    r.f0 = (float)(kzd - (double)k0);
-    r.imk = __fmul_rn(rt.invdv, cp.inv_h1);
-    r.yf = __ldg(ycol + iv);  // y * sqrt(1 + (dv inv_l)^2), adj_weight_kernel
+    r.kstep = sg;
     // slab at lo: last plane crossed strictly before lo (forward semantics);
-    // the float estimate is corrected with the exact crossing expression
-    int k = k0 + (int)floorf(r.f0 + (lo - cp.w_in) * (dv * h1));
-#if KCT_ROW_VERIFY
-    // Sign-generic fast path: the estimate is right unless z(lo) sits within
-    // rounding of a plane; verify it with the two bounding planes (the next
-    // one is also the first crossing) and search only when that fails.
-    if (dv != 0.f) {
-        const int sg = dv > 0.f ? 1 : -1;
-        k = sg > 0 ? max(k, k0) : min(k, k0);
-        const int pn = sg > 0 ? k + 1 : k;      // next plane
-        const int pp = sg > 0 ? k : k + 1;      // plane crossed entering slab k
-        const float zn = zcross(pn, k0, r.f0, r.imk, cp.w_in);
-        const float zp = k != k0 ? zcross(pp, k0, r.f0, r.imk, cp.w_in) : -kInf;
-        if (zp < lo && !(zn < lo)) {
-            r.kstep = sg;
-            const int kc = sg > 0 ? max(k, K0 - 1) : min(k, kend);
-            const int pc = sg > 0 ? kc + 1 : kc;
-            r.wz = (pc >= K0 && pc <= kend) ? (kc == k ? zn : zcross(pc, k0, r.f0, r.imk, cp.w_in))
-                                            : kInf;
-            r.k = min(max(kc, K0 - 1), kend);
-            return;
-        }
-    }
-#endif
-    if (dv > 0.f) {
-        r.kstep = 1;
-        k = max(k, k0);
-        while (k > k0 && !(zcross(k, k0, r.f0, r.imk, cp.w_in) < lo)) --k;
-        while (zcross(k + 1, k0, r.f0, r.imk, cp.w_in) < lo) ++k;
-        k = max(k, K0 - 1);
-        r.wz = k + 1 <= kend ? zcross(k + 1, k0, r.f0, r.imk, cp.w_in) : kInf;
-    } else if (dv < 0.f) {
-        r.kstep = -1;
-        k = min(k, k0);
-        while (k < k0 && !(zcross(k + 1, k0, r.f0, r.imk, cp.w_in) < lo)) ++k;
-        while (zcross(k, k0, r.f0, r.imk, cp.w_in) < lo) --k;
-        k = min(k, kend);
-        r.wz = k >= K0 ? zcross(k, k0, r.f0, r.imk, cp.w_in) : kInf;
-    } else {
-        r.kstep = 0;
-        k = k0;
+    // the float estimate (dv from the row index) is corrected with the exact
+    // crossing expression
+    const float dvh = __fmul_rn(__fmaf_rn((float)iv, g.pv, g.dv0), h1);
+    int k = k0 + __float2int_rd(__fmaf_rn(lo - w_in, dvh, r.f0));
+    if (sg == 0) {
         r.wz = kInf;
+        r.wz2 = kInf;
+        r.k = min(max(k0, K0 - 1), kend);
+        return;
     }
-    r.k = min(max(k, K0 - 1), kend);
+    k = sg > 0 ? max(k, k0) : min(k, k0);
+    int pn = sg > 0 ? k + 1 : k;      // next plane
+    const int pp = sg > 0 ? k : k + 1;  // plane crossed entering slab k
+    float zn = zcross(pn, k0, r.f0, r.imk, w_in);
+    const float zp = k != k0 ? zcross(pp, k0, r.f0, r.imk, w_in) : -kInf;
+    if (!(zp < lo && !(zn < lo))) {
+        // z(lo) within rounding of a plane: search
+        if (sg > 0) {
+            while (k > k0 && !(zcross(k, k0, r.f0, r.imk, w_in) < lo)) --k;
+            while (zcross(k + 1, k0, r.f0, r.imk, w_in) < lo) ++k;
+            pn = k + 1;
+        } else {
+            while (k < k0 && !(zcross(k + 1, k0, r.f0, r.imk, w_in) < lo)) ++k;
+            while (zcross(k, k0, r.f0, r.imk, w_in) < lo) --k;
+            pn = k;
+        }
+        zn = zcross(pn, k0, r.f0, r.imk, w_in);
+    }
+    // rows entering the brick from below / above start in a guard slab and
+    // cross the brick's first plane next
+    const int kc = sg > 0 ? max(k, K0 - 1) : min(k, kend);
+    const int pc = sg > 0 ? kc + 1 : kc;
+    r.wz = (pc >= K0 && pc <= kend) ? (kc == k ? zn : zcross(pc, k0, r.f0, r.imk, w_in)) : kInf;
+    const int pc2 = pc + sg;
+    const float z2 = (pc >= K0 && pc <= kend && pc2 >= K0 && pc2 <= kend)
+                         ? zcross(pc2, k0, r.f0, r.imk, w_in)
+                         : kInf;
+    r.wz2 = z2 < hi ? -kInf : z2;
+    r.k = min(max(kc, K0 - 1), kend);
 }
 
 // Deposit one row's pieces of one xy segment: [wa, min(wb, wz)] into slab k,
@@ -359,16 +378,26 @@ __device__ __forceinline__ void row_segment(RowZ& r, const Seg& sg, unsigned col
     const unsigned a = colbase + 4u * (unsigned)r.k;
     sts_f(a, __fmaf_rn(wm - sg.wa, r.yf, lds_f(a)));
     if (cr) {
-        float wa = r.wz;
-        for (;;) {
+        if (!(r.wz2 < sg.wb)) {
+            // the row's last crossing inside this entry: [wz, wb] into the
+            // next slab (the general path below computes the same values:
+            // the next crossing wz2 lies beyond wb)
             r.k += r.kstep;
-            const int P = r.kstep > 0 ? r.k + 1 : r.k;
-            r.wz = (P >= K0 && P <= kend) ? zcross(P, r.k0, r.f0, r.imk, w_in) : kInf;
-            const float we = fminf(r.wz, sg.wb);
             const unsigned b = colbase + 4u * (unsigned)r.k;
-            sts_f(b, __fmaf_rn(we - wa, r.yf, lds_f(b)));
-            if (!(r.wz < sg.wb)) break;
-            wa = r.wz;
+            sts_f(b, __fmaf_rn(sg.wb - r.wz, r.yf, lds_f(b)));
+            r.wz = r.wz2;
+        } else {
+            float wa = r.wz;
+            for (;;) {
+                r.k += r.kstep;
+                const int P = r.kstep > 0 ? r.k + 1 : r.k;
+                r.wz = (P >= K0 && P <= kend) ? zcross(P, r.k0, r.f0, r.imk, w_in) : kInf;
+                const float we = fminf(r.wz, sg.wb);
+                const unsigned b = colbase + 4u * (unsigned)r.k;
+                sts_f(b, __fmaf_rn(we - wa, r.yf, lds_f(b)));
+                if (!(r.wz < sg.wb)) break;
+                wa = r.wz;
+            }
         }
     }
 }
@@ -467,46 +496,229 @@ __device__ __forceinline__ int brick_walk(const ColParams& cp, const DevGeom& g,
     return nval + 1;
 }
 
-// ---- the rows of one (brick, detector column): C per lane, passes of stride S ----
+// ---- the rows of one (brick, detector column) ----
+// The n rows go in Sp = max(S, ceil(n / 32)) residue classes of rows Sp apart
+// (one lane per row: no two lanes of a class touch the same voxel, since
+// Sp * dkz_min > 1 + span_max), two classes at a time: lane l takes rows
+// base + Sp l (c = 0) and base + 1 + Sp l (c = 1), deposited by separate
+// warp-converged instructions (__syncwarp between them), so only the rows of
+// one class need the spacing.  An odd last class runs alone.
 template <int C>
-__device__ __forceinline__ void brick_rows(const Seg* segs, int nseg, const RowCol& cp, float lo,
-                                           int rlo, int rhi, int S, int K0, int kend, int lane,
-                                           const RowTab* __restrict__ rows,
-                                           const float* __restrict__ ycol, const DevGeom& g) {
-    const float h1 = rcp_approx(cp.inv_h1);
-    // passes of rows S' >= S apart with S' = max(S, ceil(n / 32C)): the n rows
-    // in the fewest passes, one per residue class (measured: -2.6% at c3)
-    const int Sp = max(S, (rhi - rlo + 32 * C) / (32 * C));
-    for (int p = 0; p < Sp; ++p) {
-        for (int base = rlo + p; base <= rhi; base += 32 * Sp * C) {
-            RowZ r[C];
+__device__ __forceinline__ void row_chunks(const Seg* segs, int nseg, const RowCol& cp, float lo,
+                                           float hi, float h1, int base, int rhi, int Sp, int K0,
+                                           int kend, int lane, const float4* __restrict__ rec,
+                                           const DevGeom& g) {
+    RowZ r[C];
 #pragma unroll
-            for (int c = 0; c < C; ++c) {
-                const int iv = base + Sp * (lane + 32 * c);
-                row_init(r[c], iv <= rhi, iv, cp, lo, h1, K0, kend, rows, ycol, g);
-            }
-            for (int sgi = 0; sgi < nseg; ++sgi) {
-                const Seg sg = segs[sgi];
-#pragma unroll
-                for (int c = 0; c < C; ++c) row_segment(r[c], sg, (unsigned)sg.ij, K0, kend, cp.w_in);
-            }
+    for (int c = 0; c < C; ++c) {
+        const int iv = base + c + Sp * lane;
+        row_init(r[c], iv <= rhi, iv, cp.w_in, lo, hi, h1, K0, kend, rec, g);
+    }
+    for (int sgi = 0; sgi < nseg; ++sgi) {
+        const Seg sg = segs[sgi];
+        row_segment(r[0], sg, (unsigned)sg.ij, K0, kend, cp.w_in);
+        if (C == 2) {
             __syncwarp();
+            row_segment(r[C - 1], sg, (unsigned)sg.ij, K0, kend, cp.w_in);
         }
     }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void brick_rows(const Seg* segs, int nseg, const RowCol& cp, float lo,
+                                           int rlo, int rhi, int S, int K0, int kend, int lane,
+                                           const float4* __restrict__ rec, const DevGeom& g) {
+    const float h1 = rcp_approx(cp.inv_h1);
+    const float hi = segs[nseg - 1].wb;
+    const int Sp = max(S, (rhi - rlo + 32) >> 5);
+    int q = 0;
+    for (; q + 1 < Sp; q += 2)
+        row_chunks<2>(segs, nseg, cp, lo, hi, h1, rlo + q, rhi, Sp, K0, kend, lane, rec, g);
+    if (q < Sp) row_chunks<1>(segs, nseg, cp, lo, hi, h1, rlo + q, rhi, Sp, K0, kend, lane, rec, g);
+}
+
+// ---- slab-lane deposits (the common case) ----
+// When a row's z-span over a brick chord is below one slab and below the row
+// spacing, and rows two apart are more than one slab apart (host-checked:
+// Projector::adj_slab_), every row of an entry either stays in one slab over
+// the whole chord ("simple") or crosses exactly one z-plane, and a slab is
+// left / entered by at most one row.  The rows of the entry are classified
+// once (lanes = consecutive rows) into per-slab tables — H[k]: the sum of the
+// simple rows' weights, Xb[k]: (crossing, weight) of the row leaving slab k,
+// Xa[k]: the row entering it — and the deposits run with lanes = slabs:
+//   acc[ij][k] += (wb - wa) H[k] + (clamp(Xb.w) - wa) Xb.y + (wb - clamp(Xa.w)) Xa.y
+// with clamp(w) = min(max(w, wa), wb): per segment exactly the forward's piece
+// lengths ([wa, wz] / [wz, wb] in the crossing segment, 0 or wb - wa
+// elsewhere).  Each row's crossing is the forward's zcross of one of the two
+// planes bounding its slab at the chord's midpoint.  A detected slot conflict
+// (not expected under the host condition) returns false and the entry takes
+// the row-wise path.  Fixed summation order: deterministic.
+constexpr int kSlabChunks = 4;  // slab table slots (bz + 2) <= 32 * kSlabChunks
+
+// floats of one warp's shared memory in adj_brick_kernel (16-byte multiple)
+__host__ __device__ constexpr int adj_warp_floats(int bz) {
+    return (BX * BY * (bz + 2) + 4 * kMaxSeg + 2 * (kMaxSeg + 2) + 6 * (bz + 2) + 3) & ~3;
+}
+
+// Row classification of one entry into the slab tables.  tA[j] = {H, -,
+// Xb.w, Xb.y} (16 B), tB[j] = {Xa.w, Xa.y} (8 B), slot j = slab K0 - 1 + j,
+// j < NS; the tables are all-zero on entry (cleared by slab_deposits).
+// Returns false when two rows claim one crossing slot (only possible for a
+// falling and a rising row around dv = 0 when the row spacing can reach one
+// slab: detect = true).
+__device__ __forceinline__ bool slab_classify(const float4* __restrict__ p, int nrows, int rlo,
+                                              float lo, float hi, float w_in, float h1, int K0,
+                                              int NS, int lane, bool detect, const DevGeom& g,
+                                              unsigned tA, unsigned tB) {
+    const float mid = 0.5f * (lo + hi) - w_in;
+    const unsigned tA0 = tA + 16u * (unsigned)(1 - K0), tB0 = tB + 8u * (unsigned)(1 - K0);
+    const int km = K0 - 1;
+    p += lane;
+    float ivf = (float)(rlo + lane);
+    float4 q = lane < nrows ? __ldg(p) : make_float4(0.f, 0.f, 0.f, 0.f);
+    bool bad = false;
+    unsigned prev_fall = 0u;
+    for (int b = lane; b < nrows + lane; b += 32) {
+        const float4 qc = q;
+        p += 32;
+        if (b + 32 < nrows) q = __ldg(p);  // next chunk
+        const bool valid = b < nrows;
+        const int code = __float_as_int(qc.w);
+        const int k0 = code >> 2, ks = (code & 3) - 1;
+        const float dvh = __fmul_rn(__fmaf_rn(ivf, g.pv, g.dv0), h1);
+        ivf += 32.f;
+        int k = k0 + __float2int_rd(__fmaf_rn(mid, dvh, qc.y));
+        k = ks != 0 ? k : k0;
+        const float z1 = zcross(k, k0, qc.y, qc.z, w_in);
+        const float z2 = zcross(k + 1, k0, qc.y, qc.z, w_in);
+        const float wen = fminf(z1, z2), wlv = fmaxf(z1, z2);
+        const bool enter = ks != 0 && wen > lo;
+        const bool leave = ks != 0 && wlv < hi;
+        const bool simple = valid && !enter && !leave;
+        const bool cx = valid && (enter || leave);
+        const float yf = qc.x;
+        // H: a run of simple rows in one slab is <= 2 adjacent rows; its first
+        // row adds both (a run split across chunks adds in chunk order)
+        const int kn = __shfl_down_sync(kFull, k, 1), kp = __shfl_up_sync(kFull, k, 1);
+        const float yn = __shfl_down_sync(kFull, yf, 1);
+        const unsigned sm = __ballot_sync(kFull, simple);
+        const bool sn = (((sm >> 1) >> lane) & 1u) && kn == k;
+        const bool sp = (((sm << 1) >> lane) & 1u) && kp == k;
+        const bool in_k = (unsigned)(k - km) < (unsigned)NS;
+        if (simple && !sp && in_k) {
+            const unsigned a = tA0 + 16u * (unsigned)k;
+            sts_f(a, lds_f(a) + (sn ? yf + yn : yf));
+        }
+        // crossing rows: the row leaves slab kb / enters slab ka at wc
+        if (cx) {
+            const float wc = enter ? wen : wlv;
+            const int kb = enter ? k - ks : k, ka = enter ? k : k + ks;
+            if ((unsigned)(kb - km) < (unsigned)NS) sts_f2(tA0 + 16u * (unsigned)kb + 8u, make_float2(wc, yf));
+            if ((unsigned)(ka - km) < (unsigned)NS) sts_f2(tB0 + 8u * (unsigned)ka, make_float2(wc, yf));
+        }
+        if (detect) {
+            const unsigned fall = __ballot_sync(kFull, cx && ks < 0);
+            const unsigned pf = ((fall << 1) | prev_fall) >> lane;
+            bad |= cx && ks > 0 && (pf & 1u);
+            prev_fall = fall >> 31;
+        }
+        __syncwarp();
+    }
+    return !(detect && __any_sync(kFull, bad));
+}
+
+// Deposits of one entry with lanes = slabs (slot j = lane + 32 r; slots past
+// the brick deposit 0 into the upper guard slab); clears the tables.
+template <int RC>
+__device__ __forceinline__ void slab_deposits(const Seg* segs, int nseg, int K0, int NS, int lane,
+                                              unsigned tA, unsigned tB) {
+    float H[RC], bw[RC], by[RC], aw[RC], ay[RC];
+    unsigned off[RC];
+    bool xs[RC];
+#pragma unroll
+    for (int r = 0; r < RC; ++r) {
+        const int j = lane + 32 * r;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        float2 b = make_float2(0.f, 0.f);
+        if (j < NS) {
+            a = lds_f4(tA + 16u * j);
+            b = lds_f2(tB + 8u * j);
+            sts_f4(tA + 16u * j, make_float4(0.f, 0.f, 0.f, 0.f));
+            sts_f2(tB + 8u * j, make_float2(0.f, 0.f));
+        }
+        H[r] = a.x;
+        bw[r] = a.z;
+        by[r] = a.w;
+        aw[r] = b.x;
+        ay[r] = b.y;
+        off[r] = 4u * (unsigned)(K0 - 1 + min(j, NS - 1));
+        xs[r] = __any_sync(kFull, a.w != 0.f || b.y != 0.f);
+    }
+    for (int sgi = 0; sgi < nseg; ++sgi) {
+        const Seg sg = segs[sgi];
+        const float d = sg.wb - sg.wa;
+#pragma unroll
+        for (int r = 0; r < RC; ++r) {
+            float dep;
+            if (xs[r]) {
+                const float cb = fminf(fmaxf(bw[r], sg.wa), sg.wb);
+                const float ca = fminf(fmaxf(aw[r], sg.wa), sg.wb);
+                dep = __fmaf_rn(d, H[r], __fmaf_rn(cb - sg.wa, by[r], (sg.wb - ca) * ay[r]));
+            } else {
+                dep = __fmul_rn(d, H[r]);
+            }
+            const unsigned a = (unsigned)sg.ij + off[r];
+            sts_f(a, lds_f(a) + dep);
+        }
+    }
+    __syncwarp();
+}
+
+// The slab-lane path for one entry; false: take the row-wise path (the
+// tables are left clean either way).
+__device__ __forceinline__ bool brick_rows_slab(const Seg* segs, int nseg, float w_in, float inv_h1,
+                                                float lo, float hi, int rlo, int rhi, int K0,
+                                                int kend, int lane, bool detect,
+                                                const float4* __restrict__ rec, const DevGeom& g,
+                                                unsigned tA, unsigned tB) {
+    const int NS = kend - K0 + 2;
+    const bool ok = slab_classify(rec + rlo, rhi - rlo + 1, rlo, lo, hi, w_in, rcp_approx(inv_h1),
+                                  K0, NS, lane, detect, g, tA, tB);
+    if (!ok) {
+        for (int j = lane; j < NS; j += 32) {
+            sts_f4(tA + 16u * j, make_float4(0.f, 0.f, 0.f, 0.f));
+            sts_f2(tB + 8u * j, make_float2(0.f, 0.f));
+        }
+        __syncwarp();
+        return false;
+    }
+    switch ((NS + 31) >> 5) {
+    case 1: slab_deposits<1>(segs, nseg, K0, NS, lane, tA, tB); break;
+    case 2: slab_deposits<2>(segs, nseg, K0, NS, lane, tA, tB); break;
+    case 3: slab_deposits<3>(segs, nseg, K0, NS, lane, tA, tB); break;
+    default: slab_deposits<4>(segs, nseg, K0, NS, lane, tA, tB); break;
+    }
+    return true;
 }
 
 // ---- walk table: the xy part of every (brick, angle, column), built once per
 // projector (geometry-only) and streamed by the adjoint instead of recomputed
 // for every application.  64 bytes per entry. ----
-struct __align__(16) WalkEntry {
-    float bnd[8];            // segment boundaries, lo = bnd[0] .. hi = bnd[nseg]
-    unsigned char ij[8];     // per segment: (i - I0) + BX (j - J0); ij[7] = nseg
+// kEW 32-bit words per entry: segment boundaries (kNB words), segment voxel
+// columns (one byte each, kNB / 4 words; the last byte holds nseg), then
+// angle | column << 16, rlo | rhi << 16, and the RowCol values.  64 bytes for
+// bricks with <= 7 segments (4x4), 128 bytes for <= 15 (8x4, 8x8).
+constexpr int kEW = BX + BY - 1 <= 7 ? 16 : 32;
+constexpr int kNB = kEW / 2;
+constexpr int kTabMaxSeg = kNB - 1;
+struct alignas(4 * kEW) WalkEntry {
+    float bnd[kNB];          // segment boundaries, lo = bnd[0] .. hi = bnd[nseg]
+    unsigned char ij[kNB];   // per segment: (i - I0) + BX (j - J0); ij[kNB - 1] = nseg
     unsigned short ia, iu;   // angle (global index), detector column
     unsigned short rlo, rhi; // detector rows crossing the brick
     RowCol rc;               // the column's row z-state inputs
 };
-static_assert(sizeof(WalkEntry) == 64, "WalkEntry layout");
-constexpr int kTabMaxSeg = 7;
+static_assert(sizeof(WalkEntry) == 4 * kEW, "WalkEntry layout");
 constexpr bool kTabOk = BX + BY - 1 <= kTabMaxSeg && BX * BY <= 256;
 
 __device__ __forceinline__ BrickGeo brick_geo(int brick, const BrickCfg& bc, const DevGeom& g) {
@@ -553,7 +765,7 @@ __global__ void __launch_bounds__(128) adj_walk_build(const ColParams* __restric
                 if (lane <= nseg) E->bnd[lane] = sbnd[warp][lane];
                 if (lane < nseg) E->ij[lane] = (unsigned char)ij;
                 if (lane == 0) {
-                    E->ij[7] = (unsigned char)nseg;
+                    E->ij[kNB - 1] = (unsigned char)nseg;
                     E->ia = (unsigned short)ia;
                     E->iu = (unsigned short)iu;
                     E->rlo = (unsigned short)rlo;
@@ -573,10 +785,9 @@ __global__ void __launch_bounds__(128) adj_walk_build(const ColParams* __restric
 #endif
 // TAB: the xy walks come from the walk table (tab, off) instead of being
 // recomputed; identical values either way.
-template <int C, bool TAB>
+template <bool TAB>
 __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel(
-    const float* __restrict__ proj, float* __restrict__ out, const ColParams* __restrict__ cols,
-    const RowTab* __restrict__ rows,
+    const float4* __restrict__ rec, float* __restrict__ out, const ColParams* __restrict__ cols,
     DevGeom g, BrickCfg bc, AngleBatch ab, int a0, int nab, int accumulate,
     const int* __restrict__ order, int* queue, float* __restrict__ out_part,
     const WalkEntry* __restrict__ tab, const unsigned long long* __restrict__ off) {
@@ -585,14 +796,17 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
     const int nbricks = bc.nbx * bc.nby * bc.nbz;
     const int BZ = bc.bz;
     const int nu = g.nu, nv = g.nv;
-    // per-warp shared layout: acc[BX*BY][BZ + 2] (slab k at k - K0 + 1; two
-    // guard slabs) | segs[kMaxSeg] | bnd[kMaxSeg + 2] | axis[kMaxSeg + 2]
+    // per-warp shared layout (adj_warp_floats): acc[BX*BY][BZ + 2] (slab k at
+    // k - K0 + 1; two guard slabs) | segs[kMaxSeg] | bnd[kMaxSeg + 2] |
+    // axis[kMaxSeg + 2] | slab tables tA[BZ + 2] (float4), tB[BZ + 2] (float2)
     const int CS = BZ + 2;
-    const int wfloats = BX * BY * CS + 4 * kMaxSeg + 2 * (kMaxSeg + 2);
+    const int wfloats = adj_warp_floats(BZ);
     float* acc = sm + warp * wfloats;
     Seg* segs = reinterpret_cast<Seg*>(acc + BX * BY * CS);
     float* bnd = acc + BX * BY * CS + 4 * kMaxSeg;
     int* axis = reinterpret_cast<int*>(bnd + kMaxSeg + 2);
+    const unsigned tA = (unsigned)__cvta_generic_to_shared(bnd + 2 * (kMaxSeg + 2));
+    const unsigned tB = tA + 16u * (unsigned)CS;
     const unsigned acc_s = (unsigned)__cvta_generic_to_shared(acc);
     const int S = bc.S;
 
@@ -627,6 +841,11 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
     const BrickGeo B = brick_geo(brick, bc, g);
     const int K0 = B.K0, kend = B.K0 + B.bzn;
     for (int q = lane; q < BX * BY * CS; q += 32) acc[q] = 0.f;
+    if (bc.slab)
+        for (int j = lane; j < CS; j += 32) {
+            sts_f4(tA + 16u * j, make_float4(0.f, 0.f, 0.f, 0.f));
+            sts_f2(tB + 8u * j, make_float2(0.f, 0.f));
+        }
     __syncwarp();
     // byte address of slab 0 of voxel column ij (so that slab k sits at + 4k)
     const unsigned seg_base = acc_s + 4u * (unsigned)(1 - K0);
@@ -635,22 +854,24 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
         const unsigned long long* ob = off + (size_t)brick * (g.na + 1);
         const unsigned long long e0 = ob[a0 + a_lo], e1 = ob[a0 + a_hi];
         const unsigned* tw = reinterpret_cast<const unsigned*>(tab);
-        // lanes 0..15 hold one 64-byte entry; the next one is fetched while
-        // the current one's rows run
-        unsigned w = (e0 < e1 && lane < 16) ? __ldg(tw + e0 * 16 + lane) : 0u;
+        // lanes 0..kEW-1 hold one entry; the next one is fetched while the
+        // current one's rows run
+        unsigned w = (e0 < e1 && lane < kEW) ? __ldg(tw + e0 * kEW + lane) : 0u;
         for (unsigned long long e = e0; e < e1; ++e) {
-            const unsigned ijw1 = __shfl_sync(kFull, w, 9);
+            constexpr int M = kNB + kNB / 4;  // first meta word
+            const unsigned ijw1 = __shfl_sync(kFull, w, M - 1);
             const int nseg = (int)(ijw1 >> 24);
-            const unsigned rr = __shfl_sync(kFull, w, 11);
-            const float wa = __uint_as_float(__shfl_sync(kFull, w, lane & 7));
-            const float wb = __uint_as_float(__shfl_sync(kFull, w, (lane + 1) & 7));
-            const unsigned ijw = __shfl_sync(kFull, w, 8 + ((lane >> 2) & 1));
+            const unsigned rr = __shfl_sync(kFull, w, M + 1);
+            const float wa = __uint_as_float(__shfl_sync(kFull, w, lane & (kNB - 1)));
+            const float wb = __uint_as_float(__shfl_sync(kFull, w, (lane + 1) & (kNB - 1)));
+            const unsigned ijw = __shfl_sync(kFull, w, kNB + ((lane >> 2) & (kNB / 4 - 1)));
             const float lo = __uint_as_float(__shfl_sync(kFull, w, 0));
-            const unsigned aiu = __shfl_sync(kFull, w, 10);
+            const float hi = __uint_as_float(__shfl_sync(kFull, w, nseg & (kNB - 1)));
+            const unsigned aiu = __shfl_sync(kFull, w, M);
             RowCol rcp;
-            rcp.w_in = __uint_as_float(__shfl_sync(kFull, w, 12));
-            rcp.inv_h1 = __uint_as_float(__shfl_sync(kFull, w, 13));
-            rcp.g_in = __hiloint2double((int)__shfl_sync(kFull, w, 15), (int)__shfl_sync(kFull, w, 14));
+            rcp.w_in = __uint_as_float(__shfl_sync(kFull, w, M + 2));
+            rcp.inv_h1 = __uint_as_float(__shfl_sync(kFull, w, M + 3));
+            rcp.g_in = __hiloint2double((int)__shfl_sync(kFull, w, M + 5), (int)__shfl_sync(kFull, w, M + 4));
             if (lane < nseg) {
                 const unsigned ij = (ijw >> (8 * (lane & 3))) & 0xffu;
                 Seg sg;
@@ -660,11 +881,14 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
                 sg.pad = 0;
                 segs[lane] = sg;
             }
-            w = (e + 1 < e1 && lane < 16) ? __ldg(tw + (e + 1) * 16 + lane) : 0u;
+            w = (e + 1 < e1 && lane < kEW) ? __ldg(tw + (e + 1) * kEW + lane) : 0u;
             __syncwarp();
             const size_t cidx = (size_t)((int)(aiu & 0xffffu) - a0) * nu + (aiu >> 16);
-            brick_rows<C>(segs, nseg, rcp, lo, (int)(rr & 0xffffu), (int)(rr >> 16), S, K0, kend,
-                          lane, rows, proj + cidx * nv, g);
+            const int rlo = (int)(rr & 0xffffu), rhi = (int)(rr >> 16);
+            if (!(bc.slab && brick_rows_slab(segs, nseg, rcp.w_in, rcp.inv_h1, lo, hi, rlo, rhi,
+                                             K0, kend, lane, bc.slab > 1, rec + cidx * nv, g,
+                                             tA, tB)))
+                brick_rows(segs, nseg, rcp, lo, rlo, rhi, S, K0, kend, lane, rec + cidx * nv, g);
             __syncwarp();
         }
     } else {
@@ -674,7 +898,7 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
             int iu_lo, iu_hi;
             footprint(g, ab.cs[ia].x, ab.cs[ia].y, X0, X1, Y0, Y1, iu_lo, iu_hi);
             const ColParams* colp = cols + (size_t)ia * nu;
-            const float* yb = proj + (size_t)ia * nu * nv;
+            const float4* yb = rec + (size_t)ia * nu * nv;
             for (int iu = iu_lo; iu <= iu_hi; ++iu) {
                 const ColParams cp = colp[iu];
                 float lo;
@@ -690,8 +914,12 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
                     segs[lane] = sg;
                 }
                 __syncwarp();
-                brick_rows<C>(segs, nseg, row_col(cp), lo, rlo, rhi, S, K0, kend, lane, rows,
-                              yb + (size_t)iu * nv, g);
+                const RowCol rcp = row_col(cp);
+                if (!(bc.slab && brick_rows_slab(segs, nseg, cp.w_in, cp.inv_h1, lo, bnd[nseg],
+                                                 rlo, rhi, K0, kend, lane, bc.slab > 1,
+                                                 yb + (size_t)iu * nv, g, tA, tB)))
+                    brick_rows(segs, nseg, rcp, lo, rlo, rhi, S, K0, kend, lane,
+                               yb + (size_t)iu * nv, g);
                 __syncwarp();
             }
         }
@@ -1090,6 +1318,22 @@ void Projector::build_tables(const kct_geometry& geom) {
         adj_bz_ = (nz + nbz - 1) / nbz;
     }
     if (const char* e = std::getenv("KCT_ADJ_BZ")) adj_bz_ = std::clamp(std::atoi(e), 1, kMaxBz);
+    // slab-lane deposits (brick_rows_slab): a row's z-span over a brick chord
+    // below one slab and below the row spacing, rows two apart more than one
+    // slab apart (c1-c5: spans 0.18-0.58, spacings 0.61-0.97 slabs)
+    {
+        const double span_brick = dv_max / (L_min * sz) * std::hypot(BX * sx, BY * sy);
+        adj_slab_ = span_brick < 0.9 && span_brick < 0.9 * dkz_min && dkz_min > 0.55 &&
+                    adj_bz_ + 2 <= 32 * kSlabChunks;
+        // a falling and a rising row next to each other (around dv = 0) can
+        // claim one crossing slot only if the row spacing can reach one slab
+        const double G_max = (geom.dso + r_max) / (L_min * sz);
+        adj_slab_detect_ = geom.pv * G_max > 0.98;
+        const char* e = std::getenv("KCT_ADJ_SLAB");
+        if (e && std::string(e) == "0") adj_slab_ = false;
+        if (e && std::string(e) == "force" && !adj_slab_)
+            throw ConfigError("KCT_ADJ_SLAB=force: slab-lane adjoint not valid for this geometry");
+    }
 
     KCT_CUDA(cudaMalloc(&d_cols_, cols.size() * sizeof(ColParams)));
     KCT_CUDA(cudaMemcpy(d_cols_, cols.data(), cols.size() * sizeof(ColParams), cudaMemcpyHostToDevice));
@@ -1108,11 +1352,10 @@ void Projector::build_tables(const kct_geometry& geom) {
     const size_t smem = adj_smem_bytes();
     // the attribute is per function, not per handle: set it to the largest
     // brick any projector can use, so handles with taller bricks coexist
-    const int smem_max = (int)((size_t)kAdjWarps *
-                               (BX * BY * (kMaxBz + 2) + 4 * kMaxSeg + 2 * (kMaxSeg + 2)) * sizeof(float));
-    KCT_CUDA(cudaFuncSetAttribute(adj_brick_kernel<kAdjRows, false>,
+    const int smem_max = (int)((size_t)kAdjWarps * adj_warp_floats(kMaxBz) * sizeof(float));
+    KCT_CUDA(cudaFuncSetAttribute(adj_brick_kernel<false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
-    KCT_CUDA(cudaFuncSetAttribute(adj_brick_kernel<kAdjRows, true>,
+    KCT_CUDA(cudaFuncSetAttribute(adj_brick_kernel<true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
 
     // angle groups for problems with few bricks (see adj_brick_kernel); a
@@ -1135,7 +1378,7 @@ void Projector::build_tables(const kct_geometry& geom) {
     }
 
     if (!adj_gather_)
-        KCT_CUDA(cudaMalloc(&d_yw_, (size_t)std::min(na, kMaxAnglesPerLaunch) * nu * nv * sizeof(float)));
+        KCT_CUDA(cudaMalloc(&d_yw_, (size_t)std::min(na, kMaxAnglesPerLaunch) * nu * nv * sizeof(float4)));
 
     // brick queue: persistent grid of resident CTAs, bricks heaviest first
     // (by xy distance of the brick centre from the rotation axis, then by z
@@ -1163,7 +1406,7 @@ void Projector::build_tables(const kct_geometry& geom) {
         KCT_CUDA(cudaMemcpy(d_border_, order.data(), nb * sizeof(int), cudaMemcpyHostToDevice));
         KCT_CUDA(cudaMalloc(&d_queue_, sizeof(int)));
         int per_sm = 0, sms = 0;
-        KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_brick_kernel<kAdjRows, true>,
+        KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_brick_kernel<true>,
                                                                kAdjWarps * 32, smem));
         KCT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
         adj_ctas_ = std::max(1, per_sm) * std::max(1, sms);
@@ -1190,6 +1433,7 @@ void Projector::build_walk_table() {
     BrickCfg bc{};
     bc.bz = adj_bz_;
     bc.S = adj_S_;
+    bc.slab = adj_slab_ ? (adj_slab_detect_ ? 2 : 1) : 0;
     bc.nbx = (dg_.nx + BX - 1) / BX;
     bc.nby = (dg_.ny + BY - 1) / BY;
     bc.nbz = (dg_.nz + adj_bz_ - 1) / adj_bz_;
@@ -1233,24 +1477,37 @@ void Projector::build_walk_table() {
 }
 
 size_t Projector::adj_smem_bytes() const {
-    return (size_t)kAdjWarps * (BX * BY * (adj_bz_ + 2) + 4 * kMaxSeg + 2 * (kMaxSeg + 2)) *
-           sizeof(float);
+    return (size_t)kAdjWarps * adj_warp_floats(adj_bz_) * sizeof(float);
 }
 
-// Adjoint input weighting: yw = y * sqrt(1 + (dv * inv_l)^2), the 3D length
-// factor of each ray (the forward's final scale), applied once per ray instead
-// of once per (ray, brick).  Native layout, one warp-row of 32 detector rows.
+// Adjoint per-ray records (row_init): yw = y * sqrt(1 + (dv * inv_l)^2), the
+// 3D length factor of each ray (the forward's final scale), applied once per
+// ray instead of once per (ray, brick), and the ray's z state (k0, f0, imk)
+// evaluated exactly as fwd_kernel does.  Native layout, one thread per ray.
 __global__ void __launch_bounds__(256) adj_weight_kernel(const float* __restrict__ y,
-                                                         float* __restrict__ yw,
+                                                         float4* __restrict__ rec,
                                                          const ColParams* __restrict__ cols,
-                                                         const float* __restrict__ dvtab, int nv,
+                                                         const RowTab* __restrict__ rows, DevGeom g,
                                                          size_t ncols) {
     const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    const int nv = g.nv;
     const size_t col = t / (size_t)nv;
     if (col >= ncols) return;
     const int iv = (int)(t - col * (size_t)nv);
-    const float q = dvtab[iv] * cols[col].inv_l;
-    yw[t] = y[t] * __fsqrt_rn(__fmaf_rn(q, q, 1.f));
+    const RowTab rt = ld_row(rows, iv);
+    const float inv_l = cols[col].inv_l, inv_h1 = cols[col].inv_h1;
+    const double g_in = cols[col].g_in;
+    const float q = rt.dv * inv_l;
+    const double kzd = fma(rt.dvd, g_in, -g.kz0d);
+    const double fl = floor(kzd);
+    const int k0 = (int)fmax(fmin(fl, (double)(1 << 28)), -(double)(1 << 28));
+    const int ks = rt.dv > 0.f ? 1 : rt.dv < 0.f ? -1 : 0;
+    float4 r;
+    r.x = y[t] * __fsqrt_rn(__fmaf_rn(q, q, 1.f));
+    r.y = (float)(kzd - fl);
+    r.z = __fmul_rn(rt.invdv, inv_h1);
+    r.w = __int_as_float(k0 * 4 + ks + 1);
+    rec[t] = r;
 }
 
 // out += part[0] + part[1] + ... (fixed order: deterministic)
@@ -1327,6 +1584,7 @@ void Projector::adjoint_range(const float* proj, float* vol, int a_begin, int a_
     BrickCfg bc;
     bc.bz = adj_bz_;
     bc.S = adj_S_;
+    bc.slab = adj_slab_ ? (adj_slab_detect_ ? 2 : 1) : 0;
     bc.nbx = (dg_.nx + BX - 1) / BX;
     bc.nby = (dg_.ny + BY - 1) / BY;
     bc.nbz = (dg_.nz + adj_bz_ - 1) / adj_bz_;
@@ -1343,9 +1601,8 @@ void Projector::adjoint_range(const float* proj, float* vol, int a_begin, int a_
         if (!adj_gather_) {
             const size_t nb = (size_t)nab * dg_.nu * dg_.nv;
             adj_weight_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(
-                pr, d_yw_, cols, d_dv_, dg_.nv, (size_t)nab * dg_.nu);
+                pr, reinterpret_cast<float4*>(d_yw_), cols, d_rows_, dg_, (size_t)nab * dg_.nu);
             KCT_LAUNCHED();
-            pr = d_yw_;
         }
         if (adj_gather_) {
             const int K = adj_k_;
@@ -1360,12 +1617,12 @@ void Projector::adjoint_range(const float* proj, float* vol, int a_begin, int a_
             if (d_queue_) KCT_CUDA(cudaMemsetAsync(d_queue_, 0, sizeof(int), s));
             const unsigned grid = d_queue_ ? std::min(nctas, adj_ctas_) : nctas;
             if (d_tab_)
-                adj_brick_kernel<kAdjRows, true><<<grid, kAdjWarps * 32, smem, s>>>(
-                    pr, vol, cols, d_rows_, dg_, bc, ab, a0, nab, accum, d_border_,
+                adj_brick_kernel<true><<<grid, kAdjWarps * 32, smem, s>>>(
+                    reinterpret_cast<const float4*>(d_yw_), vol, cols, dg_, bc, ab, a0, nab, accum, d_border_,
                     d_queue_, d_part_, static_cast<const WalkEntry*>(d_tab_), d_off_);
             else
-                adj_brick_kernel<kAdjRows, false><<<grid, kAdjWarps * 32, smem, s>>>(
-                    pr, vol, cols, d_rows_, dg_, bc, ab, a0, nab, accum, d_border_,
+                adj_brick_kernel<false><<<grid, kAdjWarps * 32, smem, s>>>(
+                    reinterpret_cast<const float4*>(d_yw_), vol, cols, dg_, bc, ab, a0, nab, accum, d_border_,
                     d_queue_, d_part_, nullptr, nullptr);
             if (bc.ngrp > 1) {
                 KCT_LAUNCHED();

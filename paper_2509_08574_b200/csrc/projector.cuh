@@ -75,6 +75,7 @@ class Projector {
     int adj_stride() const { return adj_S_; }
     int adj_bz() const { return adj_bz_; }
     bool adj_gather() const { return adj_gather_; }
+    bool adj_slab() const { return adj_slab_; }
     int adj_groups() const { return adj_groups_; }
     unsigned long long walk_entries() const { return tab_entries_; }
 
@@ -98,6 +99,8 @@ class Projector {
     int fwd_c_ = 4, fwd_bands_ = 1, adj_k_ = 8;
     int adj_S_ = 2, adj_bz_ = 32;
     bool adj_gather_ = false;
+    bool adj_slab_ = false;           // slab-lane adjoint deposits valid (brick_rows_slab)
+    bool adj_slab_detect_ = false;    // ... with crossing-slot conflict detection
     int* d_border_ = nullptr;         // brick order of the adjoint queue
     int* d_forder_ = nullptr;         // forward block -> item order (longest chords first)
     int* d_fpipe_ = nullptr;          // the same per pipeline chunk (offsets pipe_off_)
@@ -109,7 +112,7 @@ class Projector {
     int adj_ctas_ = 0;                // resident CTAs of the persistent adjoint grid
     int adj_groups_ = 1;              // angle groups of the adjoint (small problems)
     float* d_part_ = nullptr;         // (adj_groups_ - 1) partial volumes
-    float* d_yw_ = nullptr;           // length-weighted adjoint input (one angle batch)
+    float* d_yw_ = nullptr;           // adjoint per-ray records (float4, one angle batch)
     void* d_tab_ = nullptr;           // adjoint walk table (WalkEntry, projector.cu)
     unsigned long long* d_off_ = nullptr;  // walk-table offsets [brick][angle + 1]
     unsigned long long tab_entries_ = 0;

@@ -225,3 +225,44 @@ def test_sharded_operators_match_full():
             blk = k.ConeBeamProjector(shard.slab_grid(gs, world, r, axis="y"), ge).apply_adjoint(y)
             ref = adj.reshape(grid.nz, grid.ny, grid.nx)[:, y0:y1, :]
             assert rel_l2(blk, ref) < 1e-6
+
+
+def slab_geometry(n_angles=3, nu=12, nv=12):
+    """A small geometry inside the slab-lane adjoint's validity range
+    (projector.cu brick_rows_slab: z-span over a brick chord < row spacing)."""
+    from tests._util import Geometry, Grid, uniform_angles
+    return Grid(8, 8, 8, 1.0, 1.0, 1.0), Geometry(100.0, 150.0, nu, nv, 1.0, 1.0,
+                                                  uniform_angles(n_angles))
+
+
+def test_slab_adjoint_exact_transpose(monkeypatch):
+    """test_projector.cpp:77-85 on the slab-lane adjoint path: dense A^T from
+    apply_adjoint() equals the dense A from apply() (float32 rounding), same
+    sparsity."""
+    monkeypatch.setenv("KCT_ADJ_SLAB", "force")
+    grid, geom = slab_geometry()
+    A = projector(grid, geom)
+    m, n = grid.count, geom.ray_count
+    fwd = np.stack([A.apply(np.eye(m, dtype=np.float32)[j]) for j in range(m)], axis=1)
+    adj = np.stack([A.apply_adjoint(np.eye(n, dtype=np.float32)[i]) for i in range(n)], axis=0)
+    assert fwd.max() > 0
+    assert np.abs(fwd - adj).max() <= 1e-6 * np.abs(fwd).max()
+    assert np.array_equal(fwd > 0, adj > 0)
+
+
+@pytest.mark.parametrize("cfg,n_angles", [(1, 16), (2, 6), (3, 3), (4, 1)])
+def test_slab_and_row_adjoints_agree(monkeypatch, ora, cfg, n_angles):
+    """The slab-lane deposits and the row-wise deposits compute the same piece
+    lengths (summation order differs); both bit-reproducible; BASELINE
+    geometries are inside the slab path's validity range."""
+    grid, geom = baseline_geometry(cfg, n_angles=n_angles)
+    y = np.random.default_rng(31).uniform(0, 1, geom.ray_count).astype(np.float32)
+    monkeypatch.setenv("KCT_ADJ_SLAB", "force")
+    A = projector(grid, geom)
+    slab = A.apply_adjoint(y)
+    assert np.array_equal(A.apply_adjoint(y), slab)
+    monkeypatch.setenv("KCT_ADJ_SLAB", "0")
+    row = projector(grid, geom).apply_adjoint(y)
+    assert rel_l2(slab, row) < 1e-6
+    if cfg <= 2:
+        assert rel_l2(slab, ora.adjoint(grid, geom, y)) < TOL
