@@ -265,11 +265,6 @@ __device__ __forceinline__ void sts_f4(unsigned a, float4 v) {
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
                  "f"(v.w));
 }
-__device__ __forceinline__ float2 lds_f2(unsigned a) {
-    float2 v;
-    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
-    return v;
-}
 __device__ __forceinline__ void sts_f2(unsigned a, float2 v) {
     asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y));
 }
@@ -557,25 +552,26 @@ constexpr int kSlabChunks = 4;  // slab table slots (bz + 2) <= 32 * kSlabChunks
 
 // floats of one warp's shared memory in adj_brick_kernel (16-byte multiple)
 __host__ __device__ constexpr int adj_warp_floats(int bz) {
-    return (BX * BY * (bz + 2) + 4 * kMaxSeg + 2 * (kMaxSeg + 2) + 6 * (bz + 2) + 3) & ~3;
+    return (BX * BY * (bz + 2) + 4 * kMaxSeg + 2 * (kMaxSeg + 2) + 5 * (bz + 2) + 3) & ~3;
 }
 
-// Row classification of one entry into the slab tables.  tA[j] = {H, -,
-// Xb.w, Xb.y} (16 B), tB[j] = {Xa.w, Xa.y} (8 B), slot j = slab K0 - 1 + j,
-// j < NS; the tables are all-zero on entry (cleared by slab_deposits).
-// Returns false when two rows claim one crossing slot (only possible for a
-// falling and a rising row around dv = 0 when the row spacing can reach one
-// slab: detect = true).
-__device__ __forceinline__ bool slab_classify(const float4* __restrict__ p, int nrows, int rlo,
-                                              float lo, float hi, float w_in, float h1, int K0,
-                                              int NS, int lane, bool detect, const DevGeom& g,
-                                              unsigned tA, unsigned tB) {
+// Row classification of one entry into the slab tables: tH[j] = H (4 B),
+// tX[j] = {Xb.w, Xb.y, Xa.w, Xa.y} (16 B), slot j = slab K0 - 1 + j, j < NS;
+// all-zero on entry (cleared by slab_deposits).  Simple rows add
+// their weight to H; a crossing row leaving slab kb / entering ka at wc
+// writes Xb[kb] and Xa[ka] (one writer per slot: row z-intervals are
+// disjoint).  Returns false when two rows could claim one slot (only
+// possible for a falling and a rising row around dv = 0 when the row spacing
+// can reach one slab: detect = true).
+__device__ __forceinline__ bool slab_classify(const float4* __restrict__ p, float4 q, int nrows,
+                                              int rlo, float lo, float hi, float w_in, float h1,
+                                              int K0, int NS, int lane, bool detect,
+                                              const DevGeom& g, unsigned tH, unsigned tX) {
     const float mid = 0.5f * (lo + hi) - w_in;
-    const unsigned tA0 = tA + 16u * (unsigned)(1 - K0), tB0 = tB + 8u * (unsigned)(1 - K0);
+    const unsigned tH0 = tH + 4u * (unsigned)(1 - K0), tX0 = tX + 16u * (unsigned)(1 - K0);
     const int km = K0 - 1;
     p += lane;
     float ivf = (float)(rlo + lane);
-    float4 q = lane < nrows ? __ldg(p) : make_float4(0.f, 0.f, 0.f, 0.f);
     bool bad = false;
     unsigned prev_fall = 0u;
     for (int b = lane; b < nrows + lane; b += 32) {
@@ -594,27 +590,20 @@ __device__ __forceinline__ bool slab_classify(const float4* __restrict__ p, int 
         const float wen = fminf(z1, z2), wlv = fmaxf(z1, z2);
         const bool enter = ks != 0 && wen > lo;
         const bool leave = ks != 0 && wlv < hi;
-        const bool simple = valid && !enter && !leave;
         const bool cx = valid && (enter || leave);
         const float yf = qc.x;
-        // H: a run of simple rows in one slab is <= 2 adjacent rows; its first
-        // row adds both (a run split across chunks adds in chunk order)
-        const int kn = __shfl_down_sync(kFull, k, 1), kp = __shfl_up_sync(kFull, k, 1);
-        const float yn = __shfl_down_sync(kFull, yf, 1);
-        const unsigned sm = __ballot_sync(kFull, simple);
-        const bool sn = (((sm >> 1) >> lane) & 1u) && kn == k;
-        const bool sp = (((sm << 1) >> lane) & 1u) && kp == k;
-        const bool in_k = (unsigned)(k - km) < (unsigned)NS;
-        if (simple && !sp && in_k) {
-            const unsigned a = tA0 + 16u * (unsigned)k;
-            sts_f(a, lds_f(a) + (sn ? yf + yn : yf));
-        }
-        // crossing rows: the row leaves slab kb / enters slab ka at wc
+        // H: rows two apart never share a slab; two parity passes (a run of
+        // two rows adds in the same order either way: 0 + a + b)
+        const bool hw = valid && !cx && (unsigned)(k - km) < (unsigned)NS;
+        const unsigned ha = tH0 + 4u * (unsigned)k;
+        if (hw && !(lane & 1)) sts_f(ha, lds_f(ha) + yf);
+        __syncwarp();
+        if (hw && (lane & 1)) sts_f(ha, lds_f(ha) + yf);
         if (cx) {
-            const float wc = enter ? wen : wlv;
             const int kb = enter ? k - ks : k, ka = enter ? k : k + ks;
-            if ((unsigned)(kb - km) < (unsigned)NS) sts_f2(tA0 + 16u * (unsigned)kb + 8u, make_float2(wc, yf));
-            if ((unsigned)(ka - km) < (unsigned)NS) sts_f2(tB0 + 8u * (unsigned)ka, make_float2(wc, yf));
+            const float wc = enter ? wen : wlv;
+            if ((unsigned)(kb - km) < (unsigned)NS) sts_f2(tX0 + 16u * (unsigned)kb, make_float2(wc, yf));
+            if ((unsigned)(ka - km) < (unsigned)NS) sts_f2(tX0 + 16u * (unsigned)ka + 8u, make_float2(wc, yf));
         }
         if (detect) {
             const unsigned fall = __ballot_sync(kFull, cx && ks < 0);
@@ -631,32 +620,36 @@ __device__ __forceinline__ bool slab_classify(const float4* __restrict__ p, int 
 // the brick deposit 0 into the upper guard slab); clears the tables.
 template <int RC>
 __device__ __forceinline__ void slab_deposits(const Seg* segs, int nseg, int K0, int NS, int lane,
-                                              unsigned tA, unsigned tB) {
+                                              unsigned tH, unsigned tX) {
     float H[RC], bw[RC], by[RC], aw[RC], ay[RC];
     unsigned off[RC];
     bool xs[RC];
 #pragma unroll
     for (int r = 0; r < RC; ++r) {
         const int j = lane + 32 * r;
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-        float2 b = make_float2(0.f, 0.f);
+        float h = 0.f;
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
         if (j < NS) {
-            a = lds_f4(tA + 16u * j);
-            b = lds_f2(tB + 8u * j);
-            sts_f4(tA + 16u * j, make_float4(0.f, 0.f, 0.f, 0.f));
-            sts_f2(tB + 8u * j, make_float2(0.f, 0.f));
+            h = lds_f(tH + 4u * j);
+            x = lds_f4(tX + 16u * j);
+            sts_f(tH + 4u * j, 0.f);
+            sts_f4(tX + 16u * j, make_float4(0.f, 0.f, 0.f, 0.f));
         }
-        H[r] = a.x;
-        bw[r] = a.z;
-        by[r] = a.w;
-        aw[r] = b.x;
-        ay[r] = b.y;
+        H[r] = h;
+        bw[r] = x.x;
+        by[r] = x.y;
+        aw[r] = x.z;
+        ay[r] = x.w;
         off[r] = 4u * (unsigned)(K0 - 1 + min(j, NS - 1));
-        xs[r] = __any_sync(kFull, a.w != 0.f || b.y != 0.f);
+        xs[r] = __any_sync(kFull, x.y != 0.f || x.w != 0.f);
     }
     for (int sgi = 0; sgi < nseg; ++sgi) {
         const Seg sg = segs[sgi];
         const float d = sg.wb - sg.wa;
+        // the chunks' slabs are distinct: all loads first, then the stores
+        float v[RC];
+#pragma unroll
+        for (int r = 0; r < RC; ++r) v[r] = lds_f((unsigned)sg.ij + off[r]);
 #pragma unroll
         for (int r = 0; r < RC; ++r) {
             float dep;
@@ -667,36 +660,37 @@ __device__ __forceinline__ void slab_deposits(const Seg* segs, int nseg, int K0,
             } else {
                 dep = __fmul_rn(d, H[r]);
             }
-            const unsigned a = (unsigned)sg.ij + off[r];
-            sts_f(a, lds_f(a) + dep);
+            v[r] += dep;
         }
+#pragma unroll
+        for (int r = 0; r < RC; ++r) sts_f((unsigned)sg.ij + off[r], v[r]);
     }
     __syncwarp();
 }
 
-// The slab-lane path for one entry; false: take the row-wise path (the
-// tables are left clean either way).
+// The slab-lane path for one entry (q: the first row chunk's records,
+// prefetched by the caller); false: take the row-wise path (the tables are
+// left clean either way).
 __device__ __forceinline__ bool brick_rows_slab(const Seg* segs, int nseg, float w_in, float inv_h1,
                                                 float lo, float hi, int rlo, int rhi, int K0,
                                                 int kend, int lane, bool detect,
-                                                const float4* __restrict__ rec, const DevGeom& g,
-                                                unsigned tA, unsigned tB) {
+                                                const float4* __restrict__ rec, float4 q,
+                                                const DevGeom& g, unsigned tH, unsigned tX) {
     const int NS = kend - K0 + 2;
-    const bool ok = slab_classify(rec + rlo, rhi - rlo + 1, rlo, lo, hi, w_in, rcp_approx(inv_h1),
-                                  K0, NS, lane, detect, g, tA, tB);
-    if (!ok) {
+    if (!slab_classify(rec + rlo, q, rhi - rlo + 1, rlo, lo, hi, w_in, rcp_approx(inv_h1), K0, NS,
+                       lane, detect, g, tH, tX)) {
         for (int j = lane; j < NS; j += 32) {
-            sts_f4(tA + 16u * j, make_float4(0.f, 0.f, 0.f, 0.f));
-            sts_f2(tB + 8u * j, make_float2(0.f, 0.f));
+            sts_f(tH + 4u * j, 0.f);
+            sts_f4(tX + 16u * j, make_float4(0.f, 0.f, 0.f, 0.f));
         }
         __syncwarp();
         return false;
     }
     switch ((NS + 31) >> 5) {
-    case 1: slab_deposits<1>(segs, nseg, K0, NS, lane, tA, tB); break;
-    case 2: slab_deposits<2>(segs, nseg, K0, NS, lane, tA, tB); break;
-    case 3: slab_deposits<3>(segs, nseg, K0, NS, lane, tA, tB); break;
-    default: slab_deposits<4>(segs, nseg, K0, NS, lane, tA, tB); break;
+    case 1: slab_deposits<1>(segs, nseg, K0, NS, lane, tH, tX); break;
+    case 2: slab_deposits<2>(segs, nseg, K0, NS, lane, tH, tX); break;
+    case 3: slab_deposits<3>(segs, nseg, K0, NS, lane, tH, tX); break;
+    default: slab_deposits<4>(segs, nseg, K0, NS, lane, tH, tX); break;
     }
     return true;
 }
@@ -798,15 +792,15 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
     const int nu = g.nu, nv = g.nv;
     // per-warp shared layout (adj_warp_floats): acc[BX*BY][BZ + 2] (slab k at
     // k - K0 + 1; two guard slabs) | segs[kMaxSeg] | bnd[kMaxSeg + 2] |
-    // axis[kMaxSeg + 2] | slab tables tA[BZ + 2] (float4), tB[BZ + 2] (float2)
+    // axis[kMaxSeg + 2] | slab tables tX[BZ + 2] (float4), tH[BZ + 2] (float)
     const int CS = BZ + 2;
     const int wfloats = adj_warp_floats(BZ);
     float* acc = sm + warp * wfloats;
     Seg* segs = reinterpret_cast<Seg*>(acc + BX * BY * CS);
     float* bnd = acc + BX * BY * CS + 4 * kMaxSeg;
     int* axis = reinterpret_cast<int*>(bnd + kMaxSeg + 2);
-    const unsigned tA = (unsigned)__cvta_generic_to_shared(bnd + 2 * (kMaxSeg + 2));
-    const unsigned tB = tA + 16u * (unsigned)CS;
+    const unsigned tX = (unsigned)__cvta_generic_to_shared(bnd + 2 * (kMaxSeg + 2));
+    const unsigned tH = tX + 16u * (unsigned)CS;
     const unsigned acc_s = (unsigned)__cvta_generic_to_shared(acc);
     const int S = bc.S;
 
@@ -843,8 +837,8 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
     for (int q = lane; q < BX * BY * CS; q += 32) acc[q] = 0.f;
     if (bc.slab)
         for (int j = lane; j < CS; j += 32) {
-            sts_f4(tA + 16u * j, make_float4(0.f, 0.f, 0.f, 0.f));
-            sts_f2(tB + 8u * j, make_float2(0.f, 0.f));
+            sts_f(tH + 4u * j, 0.f);
+            sts_f4(tX + 16u * j, make_float4(0.f, 0.f, 0.f, 0.f));
         }
     __syncwarp();
     // byte address of slab 0 of voxel column ij (so that slab k sits at + 4k)
@@ -854,11 +848,23 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
         const unsigned long long* ob = off + (size_t)brick * (g.na + 1);
         const unsigned long long e0 = ob[a0 + a_lo], e1 = ob[a0 + a_hi];
         const unsigned* tw = reinterpret_cast<const unsigned*>(tab);
-        // lanes 0..kEW-1 hold one entry; the next one is fetched while the
+        // lanes 0..kEW-1 hold one entry; two entries ahead are in flight, and
+        // the next entry's first row chunk of records is fetched while the
         // current one's rows run
-        unsigned w = (e0 < e1 && lane < kEW) ? __ldg(tw + e0 * kEW + lane) : 0u;
+        constexpr int M = kNB + kNB / 4;  // first meta word
+        auto ld_entry = [&](unsigned long long e) {
+            return (e < e1 && lane < kEW) ? __ldg(tw + e * kEW + lane) : 0u;
+        };
+        auto first_chunk = [&](unsigned we, unsigned long long e) {
+            const unsigned a = __shfl_sync(kFull, we, M), r = __shfl_sync(kFull, we, M + 1);
+            const int rl = (int)(r & 0xffffu), n = (int)(r >> 16) - rl + 1;
+            const size_t ci = (size_t)((int)(a & 0xffffu) - a0) * nu + (a >> 16);
+            return (e < e1 && bc.slab && lane < n) ? __ldg(rec + ci * nv + rl + lane)
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+        };
+        unsigned w = ld_entry(e0), w1 = ld_entry(e0 + 1);
+        float4 q = first_chunk(w, e0);
         for (unsigned long long e = e0; e < e1; ++e) {
-            constexpr int M = kNB + kNB / 4;  // first meta word
             const unsigned ijw1 = __shfl_sync(kFull, w, M - 1);
             const int nseg = (int)(ijw1 >> 24);
             const unsigned rr = __shfl_sync(kFull, w, M + 1);
@@ -881,15 +887,19 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
                 sg.pad = 0;
                 segs[lane] = sg;
             }
-            w = (e + 1 < e1 && lane < kEW) ? __ldg(tw + (e + 1) * kEW + lane) : 0u;
+            const unsigned w2 = ld_entry(e + 2);
+            const float4 q1 = first_chunk(w1, e + 1);
             __syncwarp();
             const size_t cidx = (size_t)((int)(aiu & 0xffffu) - a0) * nu + (aiu >> 16);
             const int rlo = (int)(rr & 0xffffu), rhi = (int)(rr >> 16);
             if (!(bc.slab && brick_rows_slab(segs, nseg, rcp.w_in, rcp.inv_h1, lo, hi, rlo, rhi,
-                                             K0, kend, lane, bc.slab > 1, rec + cidx * nv, g,
-                                             tA, tB)))
+                                             K0, kend, lane, bc.slab > 1, rec + cidx * nv, q, g,
+                                             tH, tX)))
                 brick_rows(segs, nseg, rcp, lo, rlo, rhi, S, K0, kend, lane, rec + cidx * nv, g);
             __syncwarp();
+            w = w1;
+            w1 = w2;
+            q = q1;
         }
     } else {
         const float X0 = g.ox + B.I0 * g.sx, X1 = g.ox + (B.I0 + B.bxn) * g.sx;
@@ -915,9 +925,12 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
                 }
                 __syncwarp();
                 const RowCol rcp = row_col(cp);
+                const float4* ry = yb + (size_t)iu * nv;
+                const float4 q = lane <= rhi - rlo ? __ldg(ry + rlo + lane)
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
                 if (!(bc.slab && brick_rows_slab(segs, nseg, cp.w_in, cp.inv_h1, lo, bnd[nseg],
-                                                 rlo, rhi, K0, kend, lane, bc.slab > 1,
-                                                 yb + (size_t)iu * nv, g, tA, tB)))
+                                                 rlo, rhi, K0, kend, lane, bc.slab > 1, ry, q, g,
+                                                 tH, tX)))
                     brick_rows(segs, nseg, rcp, lo, rlo, rhi, S, K0, kend, lane,
                                yb + (size_t)iu * nv, g);
                 __syncwarp();
