@@ -708,7 +708,7 @@ constexpr int kTabMaxSeg = kNB - 1;
 struct alignas(4 * kEW) WalkEntry {
     float bnd[kNB];          // segment boundaries, lo = bnd[0] .. hi = bnd[nseg]
     unsigned char ij[kNB];   // per segment: (i - I0) + BX (j - J0); ij[kNB - 1] = nseg
-    unsigned short ia, iu;   // angle (global index), detector column
+    unsigned roff;           // first ray of the column: (angle * nu + column) * nv (global)
     unsigned short rlo, rhi; // detector rows crossing the brick
     RowCol rc;               // the column's row z-state inputs
 };
@@ -760,8 +760,7 @@ __global__ void __launch_bounds__(128) adj_walk_build(const ColParams* __restric
                 if (lane < nseg) E->ij[lane] = (unsigned char)ij;
                 if (lane == 0) {
                     E->ij[kNB - 1] = (unsigned char)nseg;
-                    E->ia = (unsigned short)ia;
-                    E->iu = (unsigned short)iu;
+                    E->roff = ((unsigned)ia * (unsigned)g.nu + (unsigned)iu) * (unsigned)g.nv;
                     E->rlo = (unsigned short)rlo;
                     E->rhi = (unsigned short)rhi;
                     E->rc = row_col(cp);
@@ -799,9 +798,9 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
     Seg* segs = reinterpret_cast<Seg*>(acc + BX * BY * CS);
     float* bnd = acc + BX * BY * CS + 4 * kMaxSeg;
     int* axis = reinterpret_cast<int*>(bnd + kMaxSeg + 2);
-    const unsigned tX = (unsigned)__cvta_generic_to_shared(bnd + 2 * (kMaxSeg + 2));
-    const unsigned tH = tX + 16u * (unsigned)CS;
     const unsigned acc_s = (unsigned)__cvta_generic_to_shared(acc);
+    const unsigned tX = acc_s + 4u * (unsigned)(BX * BY * CS + 4 * kMaxSeg + 2 * (kMaxSeg + 2));
+    const unsigned tH = tX + 16u * (unsigned)CS;
     const int S = bc.S;
 
     // Bricks are handed out to warps by a queue (heaviest first, `order`), so
@@ -855,11 +854,12 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
         auto ld_entry = [&](unsigned long long e) {
             return (e < e1 && lane < kEW) ? __ldg(tw + e * kEW + lane) : 0u;
         };
+        // records of this angle batch start at ray a0 * nu * nv
+        const unsigned boff = (unsigned)a0 * (unsigned)nu * (unsigned)nv;
         auto first_chunk = [&](unsigned we, unsigned long long e) {
-            const unsigned a = __shfl_sync(kFull, we, M), r = __shfl_sync(kFull, we, M + 1);
+            const unsigned ro = __shfl_sync(kFull, we, M), r = __shfl_sync(kFull, we, M + 1);
             const int rl = (int)(r & 0xffffu), n = (int)(r >> 16) - rl + 1;
-            const size_t ci = (size_t)((int)(a & 0xffffu) - a0) * nu + (a >> 16);
-            return (e < e1 && bc.slab && lane < n) ? __ldg(rec + ci * nv + rl + lane)
+            return (e < e1 && bc.slab && lane < n) ? __ldg(rec + (ro - boff + (unsigned)(rl + lane)))
                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
         };
         unsigned w = ld_entry(e0), w1 = ld_entry(e0 + 1);
@@ -873,11 +873,9 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
             const unsigned ijw = __shfl_sync(kFull, w, kNB + ((lane >> 2) & (kNB / 4 - 1)));
             const float lo = __uint_as_float(__shfl_sync(kFull, w, 0));
             const float hi = __uint_as_float(__shfl_sync(kFull, w, nseg & (kNB - 1)));
-            const unsigned aiu = __shfl_sync(kFull, w, M);
-            RowCol rcp;
-            rcp.w_in = __uint_as_float(__shfl_sync(kFull, w, M + 2));
-            rcp.inv_h1 = __uint_as_float(__shfl_sync(kFull, w, M + 3));
-            rcp.g_in = __hiloint2double((int)__shfl_sync(kFull, w, M + 5), (int)__shfl_sync(kFull, w, M + 4));
+            const unsigned ro = __shfl_sync(kFull, w, M);
+            const float w_in = __uint_as_float(__shfl_sync(kFull, w, M + 2));
+            const float inv_h1 = __uint_as_float(__shfl_sync(kFull, w, M + 3));
             if (lane < nseg) {
                 const unsigned ij = (ijw >> (8 * (lane & 3))) & 0xffu;
                 Seg sg;
@@ -890,12 +888,17 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
             const unsigned w2 = ld_entry(e + 2);
             const float4 q1 = first_chunk(w1, e + 1);
             __syncwarp();
-            const size_t cidx = (size_t)((int)(aiu & 0xffffu) - a0) * nu + (aiu >> 16);
             const int rlo = (int)(rr & 0xffffu), rhi = (int)(rr >> 16);
-            if (!(bc.slab && brick_rows_slab(segs, nseg, rcp.w_in, rcp.inv_h1, lo, hi, rlo, rhi,
-                                             K0, kend, lane, bc.slab > 1, rec + cidx * nv, q, g,
-                                             tH, tX)))
-                brick_rows(segs, nseg, rcp, lo, rlo, rhi, S, K0, kend, lane, rec + cidx * nv, g);
+            const float4* rc = rec + (ro - boff);
+            if (!(bc.slab && brick_rows_slab(segs, nseg, w_in, inv_h1, lo, hi, rlo, rhi, K0, kend,
+                                             lane, bc.slab > 1, rc, q, g, tH, tX))) {
+                RowCol rcp;
+                rcp.w_in = w_in;
+                rcp.inv_h1 = inv_h1;
+                rcp.g_in = __hiloint2double((int)__shfl_sync(kFull, w, M + 5),
+                                            (int)__shfl_sync(kFull, w, M + 4));
+                brick_rows(segs, nseg, rcp, lo, rlo, rhi, S, K0, kend, lane, rc, g);
+            }
             __syncwarp();
             w = w1;
             w1 = w2;
@@ -1336,7 +1339,7 @@ void Projector::build_tables(const kct_geometry& geom) {
     // slab apart (c1-c5: spans 0.18-0.58, spacings 0.61-0.97 slabs)
     {
         const double span_brick = dv_max / (L_min * sz) * std::hypot(BX * sx, BY * sy);
-        adj_slab_ = span_brick < 0.9 && span_brick < 0.9 * dkz_min && dkz_min > 0.55 &&
+        adj_slab_ = span_brick < 0.9 && span_brick < 0.97 * dkz_min && dkz_min > 0.55 &&
                     adj_bz_ + 2 <= 32 * kSlabChunks;
         // a falling and a rising row next to each other (around dv = 0) can
         // claim one crossing slot only if the row spacing can reach one slab
