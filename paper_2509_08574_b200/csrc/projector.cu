@@ -15,6 +15,8 @@
 #include <limits>
 #include <string>
 
+#include <cuda.h>
+
 #include "projector.cuh"
 
 namespace kct {
@@ -238,6 +240,8 @@ struct BrickCfg {
     int ngrp;      // angle groups: work item = (brick, group of the batch's angles)
     int slab;      // slab-lane deposits (brick_rows_slab): 0 off, 1 on, 2 on with slot-conflict detection
     size_t gstride;  // floats between the partial volumes of groups 1.. (group 0 -> out)
+    int out_ref;     // 1: write `out` in the reference layout (x fastest) ...
+    unsigned* level_done;  // ... and count finished bricks per z level (adjoint_host_ref)
 };
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -940,14 +944,31 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
             }
         }
     }
-    // write the brick (coalesced runs of bzn slabs per voxel column)
-    for (int c = 0; c < B.bxn * B.byn; ++c) {
-        const int ci = c % B.bxn, cj = c / B.bxn;
-        float* o = dst + ((size_t)(B.I0 + ci) + (size_t)g.nx * (B.J0 + cj)) * g.nz + K0;
-        const float* a = acc + (ci + BX * cj) * CS + 1;
-        for (int kk = lane; kk < B.bzn; kk += 32) o[kk] = acc_in ? o[kk] + a[kk] : a[kk];
+    if (!bc.out_ref) {
+        // write the brick (coalesced runs of bzn slabs per voxel column)
+        for (int c = 0; c < B.bxn * B.byn; ++c) {
+            const int ci = c % B.bxn, cj = c / B.bxn;
+            float* o = dst + ((size_t)(B.I0 + ci) + (size_t)g.nx * (B.J0 + cj)) * g.nz + K0;
+            const float* a = acc + (ci + BX * cj) * CS + 1;
+            for (int kk = lane; kk < B.bzn; kk += 32) o[kk] = acc_in ? o[kk] + a[kk] : a[kk];
+        }
+        __syncwarp();
+    } else {
+        // reference layout (x fastest): lanes over the brick's voxel columns
+        // (runs of BX floats in x), then slabs; the z level's counter tells
+        // the host copy stream when the level's slabs are final
+        const int ncol = BX * BY;
+        for (int t = lane; t < ncol * B.bzn; t += 32) {
+            const int c = t % ncol, kk = t / ncol;
+            const int ci = c % BX, cj = c / BX;
+            if (ci < B.bxn && cj < B.byn)
+                dst[(size_t)(B.I0 + ci) + (size_t)g.nx * ((size_t)(B.J0 + cj) + (size_t)g.ny * (K0 + kk))] =
+                    acc[c * CS + 1 + kk];
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(bc.level_done + brick / (bc.nbx * bc.nby), 1u);
     }
-    __syncwarp();
     }
 }
 
@@ -1138,6 +1159,7 @@ Projector::~Projector() {
     cudaFree(d_yw_);
     cudaFree(d_tab_);
     cudaFree(d_off_);
+    cudaFree(d_level_);
     for (auto* p : scratch_) cudaFree(p);
     if (cur >= 0) cudaSetDevice(cur);
 }
@@ -1596,6 +1618,11 @@ void Projector::adjoint(const float* proj, float* vol, cudaStream_t s) const {
 
 void Projector::adjoint_range(const float* proj, float* vol, int a_begin, int a_end,
                               bool accumulate, cudaStream_t s) const {
+    adjoint_impl(proj, vol, a_begin, a_end, accumulate, nullptr, s);
+}
+
+void Projector::adjoint_impl(const float* proj, float* vol, int a_begin, int a_end,
+                             bool accumulate, unsigned* level_done, cudaStream_t s) const {
     AngleBatch ab;
     BrickCfg bc;
     bc.bz = adj_bz_;
@@ -1606,6 +1633,8 @@ void Projector::adjoint_range(const float* proj, float* vol, int a_begin, int a_
     bc.nbz = (dg_.nz + adj_bz_ - 1) / adj_bz_;
     bc.ngrp = adj_groups_;
     bc.gstride = m_;
+    bc.out_ref = level_done ? 1 : 0;
+    bc.level_done = level_done;
     const int nctas = (bc.nbx * bc.nby * bc.nbz * bc.ngrp + kAdjWarps - 1) / kAdjWarps;
     const size_t smem = adj_smem_bytes();
     for (int a0 = a_begin; a0 < a_end; a0 += kMaxAnglesPerLaunch) {
@@ -1647,6 +1676,63 @@ void Projector::adjoint_range(const float* proj, float* vol, int a_begin, int a_
         }
         KCT_LAUNCHED();
     }
+}
+
+// cuStreamWaitValue32 (driver API, MemOp v2: supported by default since CUDA
+// 11.7), resolved at run time through the runtime's entry-point query.
+using WaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static WaitValue32Fn wait_value32() {
+    static const WaitValue32Fn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<WaitValue32Fn>(p);
+    }();
+    return fn;
+}
+
+// Host-buffer adjoint in the reference layout with the result leaving the
+// device z level by z level: the brick kernel writes the reference layout
+// directly (a z level's slabs are contiguous there) and counts finished
+// bricks per level; the copy stream waits on each level's counter
+// (cuStreamWaitValue32) and copies the level to the host while the next
+// levels are computed.  Same kernel arithmetic as adjoint(); false when the
+// configuration does not allow it (gather kernel, angle groups, several
+// angle batches, no brick queue, no stream-wait support).
+bool Projector::adjoint_host_ref(const float* proj, float* host, cudaStream_t s) {
+    const char* e = std::getenv("KCT_ADJ_PROGRESSIVE");
+    if (e && e[0] == '0') return false;
+    if (adj_gather_ || adj_groups_ > 1 || dg_.na > kMaxAnglesPerLaunch || !d_queue_ || !wait_value32())
+        return false;
+    const int nbz = (dg_.nz + adj_bz_ - 1) / adj_bz_;
+    const unsigned per_level =
+        (unsigned)(((dg_.nx + BX - 1) / BX) * ((dg_.ny + BY - 1) / BY));
+    if (!d_level_) KCT_CUDA(cudaMalloc(&d_level_, (size_t)nbz * sizeof(unsigned)));
+    float* dev = scratch(0, m_);
+    KCT_CUDA(cudaMemsetAsync(d_level_, 0, (size_t)nbz * sizeof(unsigned), s));
+    cudaStream_t sc = pipe_stream();
+    KCT_CUDA(cudaEventRecord(pipe_ev_[0], s));  // the copy stream sees the reset counters
+    KCT_CUDA(cudaStreamWaitEvent(sc, pipe_ev_[0], 0));
+    adjoint_impl(proj, dev, 0, dg_.na, false, d_level_, s);
+    const size_t plane = (size_t)dg_.nx * dg_.ny;
+    for (int L = 0; L < nbz; ++L) {
+        const CUresult r = wait_value32()((CUstream)sc, (CUdeviceptr)(d_level_ + L), per_level,
+                                          CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) {  // fall back: whole volume after the kernel
+            KCT_CUDA(cudaStreamSynchronize(s));
+            KCT_CUDA(cudaStreamSynchronize(sc));
+            KCT_CUDA(cudaMemcpy(host, dev, m_ * sizeof(float), cudaMemcpyDeviceToHost));
+            return true;
+        }
+        const size_t k0 = (size_t)L * adj_bz_, k1 = std::min((size_t)dg_.nz, k0 + adj_bz_);
+        KCT_CUDA(cudaMemcpyAsync(host + k0 * plane, dev + k0 * plane, (k1 - k0) * plane * sizeof(float),
+                                 cudaMemcpyDeviceToHost, sc));
+    }
+    KCT_CUDA(cudaStreamSynchronize(sc));
+    KCT_CUDA(cudaStreamSynchronize(s));
+    return true;
 }
 
 void Projector::vol_to_native(const float* ref, float* nat, cudaStream_t s) const {

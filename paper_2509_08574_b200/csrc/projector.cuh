@@ -36,6 +36,10 @@ class Projector {
                        cudaStream_t s) const;
     void adjoint_range(const float* proj, float* vol, int a_begin, int a_end, bool accumulate,
                        cudaStream_t s) const;
+    // Adjoint of native device projections into a HOST volume in the
+    // reference layout, copied out z level by z level while the kernel runs
+    // (synchronous).  false: not available for this handle (use adjoint()).
+    bool adjoint_host_ref(const float* proj, float* host, cudaStream_t s);
     // Host-buffer pipeline (capi.cu): angle chunks, a copy stream and events.
     static constexpr int kPipeChunks = 4, kPipeMinAngles = 4;
     int pipe_chunks() const { return pipe_chunks_; }
@@ -83,6 +87,8 @@ class Projector {
     void build_tables(const kct_geometry& geom);
     size_t adj_smem_bytes() const;
     void build_walk_table();
+    void adjoint_impl(const float* proj, float* vol, int a_begin, int a_end, bool accumulate,
+                      unsigned* level_done, cudaStream_t s) const;
 
     kct_grid grid_;
     DevGeom dg_{};
@@ -116,6 +122,7 @@ class Projector {
     void* d_tab_ = nullptr;           // adjoint walk table (WalkEntry, projector.cu)
     unsigned long long* d_off_ = nullptr;  // walk-table offsets [brick][angle + 1]
     unsigned long long tab_entries_ = 0;
+    unsigned* d_level_ = nullptr;     // finished bricks per z level (adjoint_host_ref)
     float* scratch_[4] = {nullptr, nullptr, nullptr, nullptr};
     size_t scratch_n_[4] = {0, 0, 0, 0};
 };
