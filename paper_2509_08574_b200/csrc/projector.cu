@@ -220,7 +220,7 @@ __device__ __forceinline__ void footprint(const DevGeom& g, float cth, float sth
 #define KCT_BY 4
 #endif
 #ifndef KCT_ADJ_WARPS
-#define KCT_ADJ_WARPS 4
+#define KCT_ADJ_WARPS 1  // one-warp CTAs: the warp's shared-memory base is CTA-uniform (uniform registers)
 #endif
 constexpr int BX = KCT_BX, BY = KCT_BY;
 constexpr int kAdjWarps = KCT_ADJ_WARPS;
@@ -778,7 +778,7 @@ __global__ void __launch_bounds__(128) adj_walk_build(const ColParams* __restric
 }
 
 #ifndef KCT_ADJ_MINB
-#define KCT_ADJ_MINB 6  // caps registers at ~64: 8 CTAs of 4 warps per SM (measured)
+#define KCT_ADJ_MINB (24 / KCT_ADJ_WARPS)  // 24 warps per SM: caps registers at 85 (measured best)
 #endif
 // TAB: the xy walks come from the walk table (tab, off) instead of being
 // recomputed; identical values either way.
