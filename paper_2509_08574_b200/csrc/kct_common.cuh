@@ -114,7 +114,8 @@ struct DevGeom {
     float pu, off_u;       // fu = (du - off_u)/pu + nu/2 - 1/2
     float pv, dv0;         // dv(iv) = fmaf(iv, pv, dv0)
     int full_footprint;    // 1: some voxel square is not fully in front of a source
-    int fwd_bands;         // forward row bands (32*C rows each)
+    int fwd_bands;         // forward row bands (32*C rows each) in this launch
+    int fwd_band0;         // first row band of this launch
 };
 
 // ---- deterministic fp64 block reduction ----------------------------------

@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
     const int nq = (g.nu + kFwdWarps - 1) / kFwdWarps;
     const int item = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
     const int quad = item % nq, rest = item / nq;
-    const int band = rest % g.fwd_bands, a = rest / g.fwd_bands;
+    const int band = g.fwd_band0 + rest % g.fwd_bands, a = rest / g.fwd_bands;
     const int lane = threadIdx.x & 31;
     const int iu = quad * kFwdWarps + (threadIdx.x >> 5);
     if (iu >= g.nu) return;
@@ -1073,9 +1073,10 @@ __global__ void __launch_bounds__(128) adj_gather_kernel(const float* __restrict
 
 // Batched 2D transpose: in[b][r][c] -> out[b][c][r].
 __global__ void transpose_kernel(const float* __restrict__ in, float* __restrict__ out, int R,
-                                 int Cc) {
+                                 int Cc, int ldo) {
     __shared__ float tile[32][33];
     const size_t boff = (size_t)blockIdx.z * R * Cc;
+    const size_t ooff = (size_t)blockIdx.z * ldo * Cc;
     const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
     for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
         const int r = r0 + dy, c = c0 + threadIdx.x;
@@ -1084,13 +1085,15 @@ __global__ void transpose_kernel(const float* __restrict__ in, float* __restrict
     __syncthreads();
     for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
         const int c = c0 + dy, r = r0 + threadIdx.x;
-        if (r < R && c < Cc) out[boff + (size_t)c * R + r] = tile[threadIdx.x][dy];
+        if (r < R && c < Cc) out[ooff + (size_t)c * ldo + r] = tile[threadIdx.x][dy];
     }
 }
 
-void launch_transpose(const float* in, float* out, int B, int R, int Cc, cudaStream_t s) {
+// in[b][r][c] -> out[b][c][r] (row stride of out: ldo >= R)
+void launch_transpose(const float* in, float* out, int B, int R, int Cc, cudaStream_t s,
+                      int ldo = 0) {
     dim3 grid((Cc + 31) / 32, (R + 31) / 32, B);
-    transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(in, out, R, Cc);
+    transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(in, out, R, Cc, ldo ? ldo : R);
     KCT_LAUNCHED();
 }
 
@@ -1150,8 +1153,11 @@ Projector::~Projector() {
     cudaFree(d_border_);
     cudaFree(d_forder_);
     cudaFree(d_fpipe_);
+    cudaFree(d_flo_);
+    cudaFree(d_fhi_);
     if (pipe_stream_) {
         for (auto e : pipe_ev_) cudaEventDestroy(e);
+        cudaEventDestroy(up_ev_);
         cudaStreamDestroy(pipe_stream_);
     }
     cudaFree(d_queue_);
@@ -1333,6 +1339,45 @@ void Projector::build_tables(const kct_geometry& geom) {
                 KCT_CUDA(cudaMalloc(&d_fpipe_, pord.size() * sizeof(int)));
                 KCT_CUDA(cudaMemcpy(d_fpipe_, pord.data(), pord.size() * sizeof(int),
                                     cudaMemcpyHostToDevice));
+                // split upload of a host volume: the rays of row band 0 stay
+                // below slab Z (largest continuous z index over every column's
+                // clip, row band 0's top row; + 2 slabs of margin), so band 0
+                // can run once slabs [0, Z) are on the device
+                double kmax = -1e30;
+                const int r1 = std::min(nv, 32 * fwd_c_) - 1;
+                for (const ColParams& cp : cols) {
+                    if (!(cp.w_in < cp.w_out)) continue;
+                    const double Gin = cp.g_in, Gout = cp.g_in + (double)(cp.w_out - cp.w_in) / cp.inv_h1;
+                    kmax = std::max(kmax, std::max(dvd[r1] * Gin, dvd[r1] * Gout) - grid_.oz / grid_.sz);
+                }
+                const int Z = (int)std::floor(kmax) + 3;
+                const char* sp = std::getenv("KCT_FWD_SPLIT");
+                if (fwd_bands_ >= 2 && Z >= 1 && Z <= (nz * 6) / 10 && !(sp && sp[0] == '0')) {
+                    fwd_split_z_ = Z;
+                    std::vector<int> lo, hi;
+                    const int B = fwd_bands_;
+                    for (size_t t = 0; t < nitems; ++t) {
+                        const int it = key[t].second;
+                        const int quad = it % nq, band = (it / nq) % B, a = it / (nq * B);
+                        if (band == 0) lo.push_back(quad + nq * a);
+                    }
+                    fhi_off_.assign(pipe_chunks_ + 1, 0);
+                    for (int c = 0; c < pipe_chunks_; ++c) {
+                        const int a0 = pipe_angle(c), a1 = pipe_angle(c + 1);
+                        fhi_off_[c] = (int)hi.size();
+                        for (size_t t = 0; t < nitems; ++t) {
+                            const int it = key[t].second;
+                            const int quad = it % nq, band = (it / nq) % B, a = it / (nq * B);
+                            if (band > 0 && a >= a0 && a < a1)
+                                hi.push_back(quad + nq * ((band - 1) + (B - 1) * (a - a0)));
+                        }
+                    }
+                    fhi_off_[pipe_chunks_] = (int)hi.size();
+                    KCT_CUDA(cudaMalloc(&d_flo_, lo.size() * sizeof(int)));
+                    KCT_CUDA(cudaMemcpy(d_flo_, lo.data(), lo.size() * sizeof(int), cudaMemcpyHostToDevice));
+                    KCT_CUDA(cudaMalloc(&d_fhi_, hi.size() * sizeof(int)));
+                    KCT_CUDA(cudaMemcpy(d_fhi_, hi.data(), hi.size() * sizeof(int), cudaMemcpyHostToDevice));
+                }
             }
         }
     }
@@ -1562,7 +1607,7 @@ __global__ void __launch_bounds__(256) adj_group_sum(float* __restrict__ out,
 
 // ---- launches -----------------------------------------------------------------
 template <bool COUNT>
-static void launch_fwd(int C, int bands, const float* vol, float* out, const ColParams* cols,
+static void launch_fwd(int C, int bands, int band0, const float* vol, float* out, const ColParams* cols,
                        const float* dv, const float* invdv, const double* dvd, const DevGeom& g,
                        const int* order, cudaStream_t s) {
     // 1D grid over (angle, band, column quad) items
@@ -1571,6 +1616,7 @@ static void launch_fwd(int C, int bands, const float* vol, float* out, const Col
     const int th = kFwdWarps * 32;
     DevGeom gg = g;
     gg.fwd_bands = bands;
+    gg.fwd_band0 = band0;
     switch (C) {
     case 1: fwd_kernel<1, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order); break;
     case 2: fwd_kernel<2, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order); break;
@@ -1581,7 +1627,7 @@ static void launch_fwd(int C, int bands, const float* vol, float* out, const Col
 }
 
 void Projector::forward(const float* vol, float* proj, cudaStream_t s) const {
-    launch_fwd<false>(fwd_c_, fwd_bands_, vol, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_,
+    launch_fwd<false>(fwd_c_, fwd_bands_, 0, vol, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_,
                       d_forder_, s);
 }
 
@@ -1595,20 +1641,40 @@ void Projector::forward_range(const float* vol, float* proj, int a_begin, int a_
     for (int c = 0; c < pipe_chunks_; ++c)
         if (pipe_angle(c) == a_begin && pipe_angle(c + 1) == a_end && d_fpipe_)
             order = d_fpipe_ + pipe_off_[c];
-    launch_fwd<false>(fwd_c_, fwd_bands_, vol, proj + (size_t)a_begin * dg_.nu * dg_.nv,
+    launch_fwd<false>(fwd_c_, fwd_bands_, 0, vol, proj + (size_t)a_begin * dg_.nu * dg_.nv,
                       d_cols_ + (size_t)a_begin * dg_.nu, d_dv_, d_invdv_, d_dvd_, g, order, s);
+}
+
+// Split-upload forward (capi.cu forward_host_pipelined): band 0 (its rays
+// stay below slab fwd_split_z_) for all angles, or bands 1.. for angles
+// [a_begin, a_end) — with the block orders built for these launches.
+void Projector::forward_split_lo(const float* vol, float* proj, cudaStream_t s) const {
+    launch_fwd<false>(fwd_c_, 1, 0, vol, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_, d_flo_, s);
+}
+void Projector::forward_split_hi(const float* vol, float* proj, int c, cudaStream_t s) const {
+    const int a0 = pipe_angle(c), a1 = pipe_angle(c + 1);
+    DevGeom g = dg_;
+    g.na = a1 - a0;
+    launch_fwd<false>(fwd_c_, fwd_bands_ - 1, 1, vol, proj + (size_t)a0 * dg_.nu * dg_.nv,
+                      d_cols_ + (size_t)a0 * dg_.nu, d_dv_, d_invdv_, d_dvd_, g,
+                      d_fhi_ + fhi_off_[c], s);
+}
+void Projector::vol_to_native_z(const float* ref, float* nat, int z0, int z1, cudaStream_t s) const {
+    const size_t plane = (size_t)dg_.nx * dg_.ny;
+    launch_transpose(ref + (size_t)z0 * plane, nat + z0, 1, z1 - z0, (int)plane, s, dg_.nz);
 }
 
 cudaStream_t Projector::pipe_stream() {
     if (!pipe_stream_) {
         KCT_CUDA(cudaStreamCreateWithFlags(&pipe_stream_, cudaStreamNonBlocking));
         for (auto& e : pipe_ev_) KCT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        KCT_CUDA(cudaEventCreateWithFlags(&up_ev_, cudaEventDisableTiming));
     }
     return pipe_stream_;
 }
 
 void Projector::count(float* proj, cudaStream_t s) const {
-    launch_fwd<true>(fwd_c_, fwd_bands_, nullptr, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_,
+    launch_fwd<true>(fwd_c_, fwd_bands_, 0, nullptr, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_,
                      d_forder_, s);
 }
 

@@ -46,6 +46,13 @@ class Projector {
     int pipe_angle(int c) const { return (int)((long long)dg_.na * c / pipe_chunks_); }
     cudaStream_t pipe_stream();
     cudaEvent_t pipe_event(int i) const { return pipe_ev_[i]; }
+    cudaEvent_t upload_event() const { return up_ev_; }
+    // Split upload of a host volume (forward_host_pipelined): row band 0's
+    // rays stay below slab fwd_split_z() (0: no split).
+    int fwd_split_z() const { return fwd_split_z_; }
+    void forward_split_lo(const float* vol, float* proj, cudaStream_t s) const;
+    void forward_split_hi(const float* vol, float* proj, int chunk, cudaStream_t s) const;
+    void vol_to_native_z(const float* ref, float* nat, int z0, int z1, cudaStream_t s) const;
     // Per-ray count of positive-length Siddon segments (as float) into proj.
     void count(float* proj, cudaStream_t s) const;
     // FDK (fdk.hpp:50-139), native layouts; `filt` is N floats of scratch.
@@ -114,6 +121,11 @@ class Projector {
     int pipe_chunks_ = 1;
     cudaStream_t pipe_stream_ = nullptr;
     cudaEvent_t pipe_ev_[kPipeChunks] = {};
+    cudaEvent_t up_ev_ = nullptr;
+    int fwd_split_z_ = 0;
+    int* d_flo_ = nullptr;            // block order of the split forward's band 0 (all angles)
+    int* d_fhi_ = nullptr;            // ... of its bands 1.. per pipeline chunk (offsets fhi_off_)
+    std::vector<int> fhi_off_;
     int* d_queue_ = nullptr;          // adjoint brick queue counter
     int adj_ctas_ = 0;                // resident CTAs of the persistent adjoint grid
     int adj_groups_ = 1;              // angle groups of the adjoint (small problems)
