@@ -289,7 +289,11 @@ def run_ours(args):
                                       "Siddon intersections counted on device"},
            "gpu_launches": launches, "clocks": clk.summary(),
            "launches_per_step": {"forward": "fwd_kernel", "adjoint": "adj_weight_kernel + "
-                                 "adj_brick_kernel (+ adj_group_sum when angle groups > 1)"}}
+                                 "adj_brick_kernel (+ adj_group_sum when angle groups > 1)"},
+           # which code paths the handles run (kct_projector_info)
+           "paths": {key: A_b.info(key) for key in ("adj_slab", "adj_bz", "adj_groups",
+                                                      "adj_walk_entries")}
+           | {key: A_f.info(key) for key in ("fwd_rows_per_warp", "fwd_bands", "fwd_split_z")}}
 
     # ---- FDK (fdk.hpp:50-139) of the c3 follow-up geometry, device resident ----
     if rank == 0 and ws == 1 and not args.skip_fdk:

@@ -130,6 +130,13 @@ int kct_adjoint_f64(kct_projector* h, const double* proj, double* vol);
 /* Exact Siddon intersection count nnz (number of (ray, voxel) pairs with
  * positive length) — the algorithmic-bytes unit of the roofline. */
 int kct_count_nnz(kct_projector* h, uint64_t* nnz, void* stream);
+/* Which code paths this handle runs (no reference counterpart; evidence for
+ * tests and benchmarks).  key: "adj_slab" (1: slab-lane adjoint deposits),
+ * "adj_slab_detect", "adj_bz" (brick height), "adj_stride" (row-wise pass
+ * stride S), "adj_groups" (angle groups), "adj_gather", "adj_walk_entries",
+ * "fwd_rows_per_warp", "fwd_bands", "fwd_split_z" (host forward split upload:
+ * slabs below it first, 0 = off).  Unknown key: ConfigError. */
+int kct_projector_info(const kct_projector* h, const char* key, double* value);
 /* Layout conversion on device (reference <-> native), stream-ordered. */
 int kct_volume_to_native(const kct_projector* h, const float* ref, float* native, void* stream);
 int kct_volume_from_native(const kct_projector* h, const float* native, float* ref, void* stream);

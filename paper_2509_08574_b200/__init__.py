@@ -107,6 +107,7 @@ _SIGS = {
     "kct_forward_f64": ([_P, _P, _P], C.c_int),
     "kct_adjoint_f64": ([_P, _P, _P], C.c_int),
     "kct_count_nnz": ([_P, C.POINTER(C.c_uint64), _P], C.c_int),
+    "kct_projector_info": ([_P, C.c_char_p, C.POINTER(C.c_double)], C.c_int),
     "kct_volume_to_native": ([_P, _P, _P, _P], C.c_int),
     "kct_volume_from_native": ([_P, _P, _P, _P], C.c_int),
     "kct_proj_to_native": ([_P, _P, _P, _P], C.c_int),
@@ -412,6 +413,13 @@ class ConeBeamProjector:
         n = C.c_uint64()
         _check(_lib.kct_count_nnz(self._h, C.byref(n), None))
         return int(n.value)
+
+    def info(self, key: str) -> float:
+        """Which code path the handle runs (kct_projector_info): adj_slab,
+        adj_bz, adj_groups, fwd_split_z, ..."""
+        v = C.c_double()
+        _check(_lib.kct_projector_info(self._h, key.encode(), C.byref(v)))
+        return v.value
 
     # layout conversions of device tensors
     def volume_to_native(self, ref, out=None):

@@ -285,6 +285,26 @@ int kct_adjoint_f64(kct_projector* h, const double* proj, double* vol) {
     });
 }
 
+int kct_projector_info(const kct_projector* h, const char* key, double* value) {
+    return guarded([&] {
+        if (!h || !h->p) throw kct::ConfigError("null projector handle");
+        if (!key || !value) throw kct::ConfigError("null argument");
+        const kct::Projector& P = *h->p;
+        const std::string k(key);
+        if (k == "adj_slab") *value = P.adj_slab() ? 1 : 0;
+        else if (k == "adj_slab_detect") *value = P.adj_slab_detect() ? 1 : 0;
+        else if (k == "adj_bz") *value = P.adj_bz();
+        else if (k == "adj_stride") *value = P.adj_stride();
+        else if (k == "adj_groups") *value = P.adj_groups();
+        else if (k == "adj_gather") *value = P.adj_gather() ? 1 : 0;
+        else if (k == "adj_walk_entries") *value = (double)P.walk_entries();
+        else if (k == "fwd_rows_per_warp") *value = 32 * P.fwd_chunks();
+        else if (k == "fwd_bands") *value = P.dev_geom().fwd_bands;
+        else if (k == "fwd_split_z") *value = P.fwd_split_z();
+        else throw kct::ConfigError("kct_projector_info: unknown key '" + k + "'");
+    });
+}
+
 int kct_count_nnz(kct_projector* h, uint64_t* nnz, void* stream) {
     return guarded([&] {
         auto& P = get(h);

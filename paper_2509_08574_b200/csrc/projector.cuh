@@ -87,6 +87,7 @@ class Projector {
     int adj_bz() const { return adj_bz_; }
     bool adj_gather() const { return adj_gather_; }
     bool adj_slab() const { return adj_slab_; }
+    bool adj_slab_detect() const { return adj_slab_detect_; }
     int adj_groups() const { return adj_groups_; }
     unsigned long long walk_entries() const { return tab_entries_; }
 

@@ -284,3 +284,17 @@ def test_split_upload_forward_is_bitwise(monkeypatch):
     monkeypatch.setenv("KCT_HOST_PIPELINE", "0")
     plain = projector(grid, geom).apply(x2)
     assert np.array_equal(split, plain)
+
+
+def test_projector_info_reports_paths():
+    """kct_projector_info: BASELINE c3 runs the slab-lane adjoint and the split
+    host upload; c1 (one row band) has no split; unknown keys are ConfigError."""
+    A = projector(*baseline_geometry(3, n_angles=16))
+    assert A.info("adj_slab") == 1 and A.info("adj_gather") == 0
+    assert A.info("adj_bz") == 86 and A.info("fwd_rows_per_warp") == 128
+    assert 0 < A.info("fwd_split_z") < 256
+    assert A.info("adj_walk_entries") > 0
+    B = projector(*baseline_geometry(1, n_angles=8))
+    assert B.info("adj_slab") == 1 and B.info("fwd_split_z") == 0
+    with pytest.raises(k.ConfigError):
+        A.info("no_such_key")
