@@ -171,35 +171,36 @@ void forward_host_pipelined(kct::Projector& P, const float* vol, float* proj, in
     // first, row band 0 (whose rays stay below Z) runs while the rest of the
     // volume is uploaded on the copy stream.
     const int Z = layout == KCT_LAYOUT_REFERENCE ? P.fwd_split_z() : 0;
-    const float* v;
     if (Z > 0) {
         const kct_grid& gr = P.grid();
         const size_t plane = (size_t)gr.nx * gr.ny, lo = (size_t)Z * plane;
         float* tmp = P.scratch(2, M);
-        float* nat = P.scratch(0, M);
         KCT_CUDA(cudaMemcpyAsync(tmp, vol, lo * sizeof(float), cudaMemcpyHostToDevice, s));
         KCT_CUDA(cudaEventRecord(P.upload_event(), s));  // the copy stream starts after this call's
         KCT_CUDA(cudaStreamWaitEvent(sc, P.upload_event(), 0));  // earlier work on s
         KCT_CUDA(cudaMemcpyAsync(tmp + lo, vol + lo, (M - lo) * sizeof(float), cudaMemcpyHostToDevice, sc));
-        P.vol_to_native_z(tmp, nat, 0, Z, s);
-        v = nat;
+        P.vol_to_padded_z(tmp, 0, Z, s);
+    } else if (layout == KCT_LAYOUT_REFERENCE) {
+        float* tmp = P.scratch(2, M);
+        KCT_CUDA(cudaMemcpyAsync(tmp, vol, M * sizeof(float), cudaMemcpyHostToDevice, s));
+        P.vol_to_padded_z(tmp, 0, P.grid().nz, s);
     } else {
-        v = kct::stage_in(P, vol, M, true, KCT_MEM_HOST, layout, 0, 2, s);
+        P.pad_volume(kct::stage_in(P, vol, M, true, KCT_MEM_HOST, layout, 0, 2, s), s);
     }
     float* q = P.scratch(1, N);
     float* qr = layout == KCT_LAYOUT_REFERENCE ? P.scratch(3, N) : nullptr;
     const int K = P.pipe_chunks();
     const size_t per = N / (size_t)P.n_angles();
     if (Z > 0) {
-        P.forward_split_lo(v, q, s);
+        P.forward_split_lo(q, s);
         KCT_CUDA(cudaEventRecord(P.upload_event(), sc));
         KCT_CUDA(cudaStreamWaitEvent(s, P.upload_event(), 0));
-        P.vol_to_native_z(P.scratch(2, M), P.scratch(0, M), Z, P.grid().nz, s);
+        P.vol_to_padded_z(P.scratch(2, M), Z, P.grid().nz, s);
     }
     for (int c = 0; c < K; ++c) {
         const int a0 = P.pipe_angle(c), a1 = P.pipe_angle(c + 1);
-        if (Z > 0) P.forward_split_hi(v, q, c, s);
-        else P.forward_range(v, q, a0, a1, s);
+        if (Z > 0) P.forward_split_hi(q, c, s);
+        else P.forward_padded(q, a0, a1, s);
         KCT_CUDA(cudaEventRecord(P.pipe_event(c), s));
         KCT_CUDA(cudaStreamWaitEvent(sc, P.pipe_event(c), 0));
         const float* src = q + a0 * per;

@@ -38,12 +38,14 @@ constexpr unsigned kFull = 0xffffffffu;
 // overlapping voxel columns are served from L1.
 // ----------------------------------------------------------------------------
 #ifndef KCT_FWD_MINB
-#define KCT_FWD_MINB 1
+#define KCT_FWD_MINB 6  // <= 80 registers: 6 CTAs of 4 warps per SM
 #endif
 #ifndef KCT_FWD_WARPS
 #define KCT_FWD_WARPS 4  // adjacent detector columns per CTA (shared voxel columns in L1)
 #endif
 constexpr int kFwdWarps = KCT_FWD_WARPS;
+// vol: slab 0 of voxel column 0 of the padded native volume (column stride
+// nz + 2, zero slabs at -1 and nz; Projector::pad_volume).
 template <int C, bool COUNT>
 __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const float* __restrict__ vol,
                                                   float* __restrict__ out,
@@ -90,14 +92,14 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
         const int P = ks > 0 ? kk + 1 : kk;
         int n = ks > 0 ? nz - kk : kk + 1;  // planes P, P+ks, ... inside [0, nz]
         if (!row_ok || dv == 0.f) n = 0;
-        if (!row_ok) kk = -1 - nz;  // never valid
+        if (!row_ok) kk = -1;  // reads the zero pad, never crosses
         k[c] = kk;
         pk[c] = P - k0;
         nrem[c] = max(n, 0);
         wz[c] = nrem[c] > 0 ? __fmaf_rn(__fsub_rn((float)pk[c], fz[c]), imk[c], cp.w_in) : kInf;
         // a ray meets the volume iff it starts inside the z range or its first
         // plane crossing (the entry plane) comes before the xy exit
-        hit = hit || (unsigned)kk < (unsigned)nz || wz[c] < cp.w_out;
+        hit = hit || (row_ok && (unsigned)kk < (unsigned)nz) || wz[c] < cp.w_out;
     }
 
     // rows that all pass above / below the volume (detector overhang, c4)
@@ -115,12 +117,14 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
             const bool stepx = wnx <= wny;
             const float wnext = stepx ? wnx : wny;
             const float wb = fmaxf(fminf(wnext, cp.w_out), wcur);
-            const unsigned col = (unsigned)(i + nx * j) * (unsigned)nz;
+            // the column's slab 0 in the padded volume (zero slabs at -1 and
+            // nz: slabs k in [-1, nz] need no range check)
+            const float* colp = vol + (unsigned)(i + nx * j) * (unsigned)(nz + 2);
             float v[C], wa[C];
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 wa[c] = wcur;
-                v[c] = (unsigned)k[c] < (unsigned)nz ? (COUNT ? 1.f : __ldg(vol + (col + (unsigned)k[c]))) : 0.f;
+                v[c] = COUNT ? ((unsigned)k[c] < (unsigned)nz ? 1.f : 0.f) : __ldg(colp + k[c]);
             }
 #pragma unroll
             for (int c = 0; c < C; ++c) {
@@ -131,8 +135,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
                         else acc[c] = __fmaf_rn(len, v[c], acc[c]);
                         wa[c] = wz[c];
                         k[c] += kstep[c];
-                        const bool ok = (unsigned)k[c] < (unsigned)nz;
-                        v[c] = ok ? (COUNT ? 1.f : __ldg(vol + (col + (unsigned)k[c]))) : 0.f;
+                        v[c] = COUNT ? ((unsigned)k[c] < (unsigned)nz ? 1.f : 0.f) : __ldg(colp + k[c]);
                         pk[c] += kstep[c];
                         nrem[c] -= 1;
                         wz[c] = nrem[c] > 0
@@ -1138,6 +1141,9 @@ Projector::Projector(const kct_grid& grid, const kct_geometry& geom, int device)
     const char* mode = std::getenv("KCT_ADJOINT");
     adj_gather_ = mode && std::string(mode) == "gather";
     build_tables(geom);
+    // padded native volume of the forward (zero slabs at -1 and nz)
+    KCT_CUDA(cudaMalloc(&d_vpad_, (size_t)grid.nx * grid.ny * (grid.nz + 2) * sizeof(float)));
+    KCT_CUDA(cudaMemset(d_vpad_, 0, (size_t)grid.nx * grid.ny * (grid.nz + 2) * sizeof(float)));
 }
 
 Projector::~Projector() {
@@ -1154,6 +1160,7 @@ Projector::~Projector() {
     cudaFree(d_forder_);
     cudaFree(d_fpipe_);
     cudaFree(d_flo_);
+    cudaFree(d_vpad_);
     cudaFree(d_fhi_);
     if (pipe_stream_) {
         for (auto e : pipe_ev_) cudaEventDestroy(e);
@@ -1627,41 +1634,65 @@ static void launch_fwd(int C, int bands, int band0, const float* vol, float* out
 }
 
 void Projector::forward(const float* vol, float* proj, cudaStream_t s) const {
-    launch_fwd<false>(fwd_c_, fwd_bands_, 0, vol, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_,
-                      d_forder_, s);
+    pad_volume(vol, s);
+    forward_padded(proj, 0, dg_.na, s);
 }
 
 void Projector::forward_range(const float* vol, float* proj, int a_begin, int a_end,
                               cudaStream_t s) const {
-    if (a_begin == 0 && a_end == dg_.na) return forward(vol, proj, s);
-    DevGeom g = dg_;
-    g.na = a_end - a_begin;
-    // the block order of a pipeline chunk when the range is one (else natural order)
-    const int* order = nullptr;
-    for (int c = 0; c < pipe_chunks_; ++c)
-        if (pipe_angle(c) == a_begin && pipe_angle(c + 1) == a_end && d_fpipe_)
-            order = d_fpipe_ + pipe_off_[c];
-    launch_fwd<false>(fwd_c_, fwd_bands_, 0, vol, proj + (size_t)a_begin * dg_.nu * dg_.nv,
-                      d_cols_ + (size_t)a_begin * dg_.nu, d_dv_, d_invdv_, d_dvd_, g, order, s);
+    pad_volume(vol, s);
+    forward_padded(proj, a_begin, a_end, s);
 }
 
 // Split-upload forward (capi.cu forward_host_pipelined): band 0 (its rays
 // stay below slab fwd_split_z_) for all angles, or bands 1.. for angles
 // [a_begin, a_end) — with the block orders built for these launches.
-void Projector::forward_split_lo(const float* vol, float* proj, cudaStream_t s) const {
-    launch_fwd<false>(fwd_c_, 1, 0, vol, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_, d_flo_, s);
+void Projector::forward_split_lo(float* proj, cudaStream_t s) const {
+    launch_fwd<false>(fwd_c_, 1, 0, d_vpad_ + 1, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_, d_flo_, s);
 }
-void Projector::forward_split_hi(const float* vol, float* proj, int c, cudaStream_t s) const {
+void Projector::forward_split_hi(float* proj, int c, cudaStream_t s) const {
     const int a0 = pipe_angle(c), a1 = pipe_angle(c + 1);
     DevGeom g = dg_;
     g.na = a1 - a0;
-    launch_fwd<false>(fwd_c_, fwd_bands_ - 1, 1, vol, proj + (size_t)a0 * dg_.nu * dg_.nv,
+    launch_fwd<false>(fwd_c_, fwd_bands_ - 1, 1, d_vpad_ + 1, proj + (size_t)a0 * dg_.nu * dg_.nv,
                       d_cols_ + (size_t)a0 * dg_.nu, d_dv_, d_invdv_, d_dvd_, g,
                       d_fhi_ + fhi_off_[c], s);
 }
-void Projector::vol_to_native_z(const float* ref, float* nat, int z0, int z1, cudaStream_t s) const {
+// reference-layout slabs [z0, z1) straight into the padded native volume
+void Projector::vol_to_padded_z(const float* ref, int z0, int z1, cudaStream_t s) const {
     const size_t plane = (size_t)dg_.nx * dg_.ny;
-    launch_transpose(ref + (size_t)z0 * plane, nat + z0, 1, z1 - z0, (int)plane, s, dg_.nz);
+    launch_transpose(ref + (size_t)z0 * plane, d_vpad_ + 1 + z0, 1, z1 - z0, (int)plane, s,
+                     dg_.nz + 2);
+}
+
+// native volume -> padded copy (column stride nz + 2; the pad slabs stay 0)
+__global__ void __launch_bounds__(256) pad_kernel(const float* __restrict__ nat,
+                                                  float* __restrict__ pad, int nz, size_t m) {
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < m;
+         t += (size_t)gridDim.x * blockDim.x) {
+        const size_t p = t / (unsigned)nz, kk = t - p * (unsigned)nz;
+        pad[p * (nz + 2) + 1 + kk] = nat[t];
+    }
+}
+
+void Projector::pad_volume(const float* nat, cudaStream_t s) const {
+    pad_kernel<<<148 * 8, 256, 0, s>>>(nat, d_vpad_, dg_.nz, m_);
+    KCT_LAUNCHED();
+}
+
+void Projector::forward_padded(float* proj, int a_begin, int a_end, cudaStream_t s) const {
+    const int* order = nullptr;
+    if (a_begin == 0 && a_end == dg_.na) {
+        order = d_forder_;
+    } else {
+        for (int c = 0; c < pipe_chunks_; ++c)
+            if (pipe_angle(c) == a_begin && pipe_angle(c + 1) == a_end && d_fpipe_)
+                order = d_fpipe_ + pipe_off_[c];
+    }
+    DevGeom g = dg_;
+    g.na = a_end - a_begin;
+    launch_fwd<false>(fwd_c_, fwd_bands_, 0, d_vpad_ + 1, proj + (size_t)a_begin * dg_.nu * dg_.nv,
+                      d_cols_ + (size_t)a_begin * dg_.nu, d_dv_, d_invdv_, d_dvd_, g, order, s);
 }
 
 cudaStream_t Projector::pipe_stream() {

@@ -50,9 +50,14 @@ class Projector {
     // Split upload of a host volume (forward_host_pipelined): row band 0's
     // rays stay below slab fwd_split_z() (0: no split).
     int fwd_split_z() const { return fwd_split_z_; }
-    void forward_split_lo(const float* vol, float* proj, cudaStream_t s) const;
-    void forward_split_hi(const float* vol, float* proj, int chunk, cudaStream_t s) const;
-    void vol_to_native_z(const float* ref, float* nat, int z0, int z1, cudaStream_t s) const;
+    void forward_split_lo(float* proj, cudaStream_t s) const;
+    void forward_split_hi(float* proj, int chunk, cudaStream_t s) const;
+    // The forward reads a padded copy of the native volume (column stride
+    // nz + 2, zero slabs at -1 and nz: no per-load range checks).
+    void pad_volume(const float* nat, cudaStream_t s) const;
+    void vol_to_padded_z(const float* ref, int z0, int z1, cudaStream_t s) const;
+    // forward of angles [a_begin, a_end) from the padded volume as it stands
+    void forward_padded(float* proj, int a_begin, int a_end, cudaStream_t s) const;
     // Per-ray count of positive-length Siddon segments (as float) into proj.
     void count(float* proj, cudaStream_t s) const;
     // FDK (fdk.hpp:50-139), native layouts; `filt` is N floats of scratch.
@@ -124,6 +129,7 @@ class Projector {
     cudaEvent_t pipe_ev_[kPipeChunks] = {};
     cudaEvent_t up_ev_ = nullptr;
     int fwd_split_z_ = 0;
+    float* d_vpad_ = nullptr;         // padded native volume read by the forward
     int* d_flo_ = nullptr;            // block order of the split forward's band 0 (all angles)
     int* d_fhi_ = nullptr;            // ... of its bands 1.. per pipeline chunk (offsets fhi_off_)
     std::vector<int> fhi_off_;
