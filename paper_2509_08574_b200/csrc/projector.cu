@@ -44,6 +44,15 @@ constexpr unsigned kFull = 0xffffffffu;
 #define KCT_FWD_WARPS 4  // adjacent detector columns per CTA (shared voxel columns in L1)
 #endif
 constexpr int kFwdWarps = KCT_FWD_WARPS;
+#ifndef KCT_VPAD_ALIGN
+#define KCT_VPAD_ALIGN 0
+#endif
+// padded forward volume: slab 0 of a column at offset kVOff, column stride
+// vpad_stride(nz) (zero slabs at -1 and nz)
+constexpr int kVOff = KCT_VPAD_ALIGN ? 16 : 1;
+__host__ __device__ constexpr int vpad_stride(int nz) {
+    return KCT_VPAD_ALIGN ? (kVOff + nz + 1 + 31) / 32 * 32 : nz + 2;  // (aligned: measured +-0)
+}
 // vol: slab 0 of voxel column 0 of the padded native volume (column stride
 // nz + 2, zero slabs at -1 and nz; Projector::pad_volume).
 template <int C, bool COUNT>
@@ -119,7 +128,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
             const float wb = fmaxf(fminf(wnext, cp.w_out), wcur);
             // the column's slab 0 in the padded volume (zero slabs at -1 and
             // nz: slabs k in [-1, nz] need no range check)
-            const float* colp = vol + (unsigned)(i + nx * j) * (unsigned)(nz + 2);
+            const float* colp = vol + (unsigned)(i + nx * j) * (unsigned)vpad_stride(nz);
             float v[C], wa[C];
 #pragma unroll
             for (int c = 0; c < C; ++c) {
@@ -1142,8 +1151,8 @@ Projector::Projector(const kct_grid& grid, const kct_geometry& geom, int device)
     adj_gather_ = mode && std::string(mode) == "gather";
     build_tables(geom);
     // padded native volume of the forward (zero slabs at -1 and nz)
-    KCT_CUDA(cudaMalloc(&d_vpad_, (size_t)grid.nx * grid.ny * (grid.nz + 2) * sizeof(float)));
-    KCT_CUDA(cudaMemset(d_vpad_, 0, (size_t)grid.nx * grid.ny * (grid.nz + 2) * sizeof(float)));
+    KCT_CUDA(cudaMalloc(&d_vpad_, (size_t)grid.nx * grid.ny * vpad_stride(grid.nz) * sizeof(float)));
+    KCT_CUDA(cudaMemset(d_vpad_, 0, (size_t)grid.nx * grid.ny * vpad_stride(grid.nz) * sizeof(float)));
 }
 
 Projector::~Projector() {
@@ -1648,21 +1657,21 @@ void Projector::forward_range(const float* vol, float* proj, int a_begin, int a_
 // stay below slab fwd_split_z_) for all angles, or bands 1.. for angles
 // [a_begin, a_end) — with the block orders built for these launches.
 void Projector::forward_split_lo(float* proj, cudaStream_t s) const {
-    launch_fwd<false>(fwd_c_, 1, 0, d_vpad_ + 1, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_, d_flo_, s);
+    launch_fwd<false>(fwd_c_, 1, 0, d_vpad_ + kVOff, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_, d_flo_, s);
 }
 void Projector::forward_split_hi(float* proj, int c, cudaStream_t s) const {
     const int a0 = pipe_angle(c), a1 = pipe_angle(c + 1);
     DevGeom g = dg_;
     g.na = a1 - a0;
-    launch_fwd<false>(fwd_c_, fwd_bands_ - 1, 1, d_vpad_ + 1, proj + (size_t)a0 * dg_.nu * dg_.nv,
+    launch_fwd<false>(fwd_c_, fwd_bands_ - 1, 1, d_vpad_ + kVOff, proj + (size_t)a0 * dg_.nu * dg_.nv,
                       d_cols_ + (size_t)a0 * dg_.nu, d_dv_, d_invdv_, d_dvd_, g,
                       d_fhi_ + fhi_off_[c], s);
 }
 // reference-layout slabs [z0, z1) straight into the padded native volume
 void Projector::vol_to_padded_z(const float* ref, int z0, int z1, cudaStream_t s) const {
     const size_t plane = (size_t)dg_.nx * dg_.ny;
-    launch_transpose(ref + (size_t)z0 * plane, d_vpad_ + 1 + z0, 1, z1 - z0, (int)plane, s,
-                     dg_.nz + 2);
+    launch_transpose(ref + (size_t)z0 * plane, d_vpad_ + kVOff + z0, 1, z1 - z0, (int)plane, s,
+                     vpad_stride(dg_.nz));
 }
 
 // native volume -> padded copy (column stride nz + 2; the pad slabs stay 0)
@@ -1671,7 +1680,7 @@ __global__ void __launch_bounds__(256) pad_kernel(const float* __restrict__ nat,
     for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < m;
          t += (size_t)gridDim.x * blockDim.x) {
         const size_t p = t / (unsigned)nz, kk = t - p * (unsigned)nz;
-        pad[p * (nz + 2) + 1 + kk] = nat[t];
+        pad[p * vpad_stride(nz) + kVOff + kk] = nat[t];
     }
 }
 
@@ -1691,7 +1700,7 @@ void Projector::forward_padded(float* proj, int a_begin, int a_end, cudaStream_t
     }
     DevGeom g = dg_;
     g.na = a_end - a_begin;
-    launch_fwd<false>(fwd_c_, fwd_bands_, 0, d_vpad_ + 1, proj + (size_t)a_begin * dg_.nu * dg_.nv,
+    launch_fwd<false>(fwd_c_, fwd_bands_, 0, d_vpad_ + kVOff, proj + (size_t)a_begin * dg_.nu * dg_.nv,
                       d_cols_ + (size_t)a_begin * dg_.nu, d_dv_, d_invdv_, d_dvd_, g, order, s);
 }
 
