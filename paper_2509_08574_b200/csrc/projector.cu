@@ -128,12 +128,13 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
             const float wb = fmaxf(fminf(wnext, cp.w_out), wcur);
             // the column's slab 0 in the padded volume (zero slabs at -1 and
             // nz: slabs k in [-1, nz] need no range check)
-            const float* colp = vol + (unsigned)(i + nx * j) * (unsigned)vpad_stride(nz);
+            // (32-bit element index: one IMAD.WIDE per load)
+            const int col = (i + nx * j) * vpad_stride(nz);
             float v[C], wa[C];
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 wa[c] = wcur;
-                v[c] = COUNT ? ((unsigned)k[c] < (unsigned)nz ? 1.f : 0.f) : __ldg(colp + k[c]);
+                v[c] = COUNT ? ((unsigned)k[c] < (unsigned)nz ? 1.f : 0.f) : __ldg(vol + (col + k[c]));
             }
 #pragma unroll
             for (int c = 0; c < C; ++c) {
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
                         else acc[c] = __fmaf_rn(len, v[c], acc[c]);
                         wa[c] = wz[c];
                         k[c] += kstep[c];
-                        v[c] = COUNT ? ((unsigned)k[c] < (unsigned)nz ? 1.f : 0.f) : __ldg(colp + k[c]);
+                        v[c] = COUNT ? ((unsigned)k[c] < (unsigned)nz ? 1.f : 0.f) : __ldg(vol + (col + k[c]));
                         pk[c] += kstep[c];
                         nrem[c] -= 1;
                         wz[c] = nrem[c] > 0
