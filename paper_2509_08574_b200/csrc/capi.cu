@@ -252,11 +252,11 @@ int kct_adjoint(kct_projector* h, const float* proj, float* vol, int mem, int la
         DeviceGuard dg(P.device());
         auto s = static_cast<cudaStream_t>(stream);
         const size_t M = P.domain_size(), N = P.range_size();
-        const float* q = kct::stage_in(P, proj, N, false, mem, layout, 1, 2, s);
-        // host volume in the reference layout: leaves the device z level by
-        // z level while the adjoint runs (Projector::adjoint_host_ref)
-        if (mem == KCT_MEM_HOST && layout == KCT_LAYOUT_REFERENCE && P.adjoint_host_ref(q, vol, s))
+        // host buffers, reference layouts: upload in angle halves, volume out
+        // z level by z level while the adjoint runs (Projector::adjoint_host_ref)
+        if (mem == KCT_MEM_HOST && layout == KCT_LAYOUT_REFERENCE && P.adjoint_host_ref(proj, vol, s))
             return;
+        const float* q = kct::stage_in(P, proj, N, false, mem, layout, 1, 2, s);
         float* v = (mem == KCT_MEM_DEVICE && layout == KCT_LAYOUT_NATIVE) ? vol : P.scratch(0, M);
         P.adjoint(q, v, s);
         kct::stage_out(P, v, vol, M, true, mem, layout, 2, s);

@@ -974,13 +974,17 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
         for (int t = lane; t < ncol * B.bzn; t += 32) {
             const int c = t % ncol, kk = t / ncol;
             const int ci = c % BX, cj = c / BX;
-            if (ci < B.bxn && cj < B.byn)
-                dst[(size_t)(B.I0 + ci) + (size_t)g.nx * ((size_t)(B.J0 + cj) + (size_t)g.ny * (K0 + kk))] =
-                    acc[c * CS + 1 + kk];
+            if (ci < B.bxn && cj < B.byn) {
+                float* o = dst + (size_t)(B.I0 + ci) +
+                           (size_t)g.nx * ((size_t)(B.J0 + cj) + (size_t)g.ny * (K0 + kk));
+                *o = acc_in ? *o + acc[c * CS + 1 + kk] : acc[c * CS + 1 + kk];
+            }
         }
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) atomicAdd(bc.level_done + brick / (bc.nbx * bc.nby), 1u);
+        if (bc.level_done) {
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicAdd(bc.level_done + brick / (bc.nbx * bc.nby), 1u);
+        }
     }
     }
 }
@@ -1725,11 +1729,12 @@ void Projector::adjoint(const float* proj, float* vol, cudaStream_t s) const {
 
 void Projector::adjoint_range(const float* proj, float* vol, int a_begin, int a_end,
                               bool accumulate, cudaStream_t s) const {
-    adjoint_impl(proj, vol, a_begin, a_end, accumulate, nullptr, s);
+    adjoint_impl(proj, vol, a_begin, a_end, accumulate, false, nullptr, s);
 }
 
 void Projector::adjoint_impl(const float* proj, float* vol, int a_begin, int a_end,
-                             bool accumulate, unsigned* level_done, cudaStream_t s) const {
+                             bool accumulate, bool out_ref, unsigned* level_done,
+                             cudaStream_t s) const {
     AngleBatch ab;
     BrickCfg bc;
     bc.bz = adj_bz_;
@@ -1740,7 +1745,7 @@ void Projector::adjoint_impl(const float* proj, float* vol, int a_begin, int a_e
     bc.nbz = (dg_.nz + adj_bz_ - 1) / adj_bz_;
     bc.ngrp = adj_groups_;
     bc.gstride = m_;
-    bc.out_ref = level_done ? 1 : 0;
+    bc.out_ref = out_ref ? 1 : 0;
     bc.level_done = level_done;
     const int nctas = (bc.nbx * bc.nby * bc.nbz * bc.ngrp + kAdjWarps - 1) / kAdjWarps;
     const size_t smem = adj_smem_bytes();
@@ -1800,15 +1805,18 @@ static WaitValue32Fn wait_value32() {
     return fn;
 }
 
-// Host-buffer adjoint in the reference layout with the result leaving the
-// device z level by z level: the brick kernel writes the reference layout
-// directly (a z level's slabs are contiguous there) and counts finished
-// bricks per level; the copy stream waits on each level's counter
+// Host-buffer adjoint, reference layouts: the projections arrive in two
+// angle halves (the second half's upload overlaps the first half's adjoint,
+// which the second launch accumulates onto), and the volume leaves the device
+// z level by z level: the brick kernel writes the reference layout directly
+// (a z level's slabs are contiguous there) and its last launch counts
+// finished bricks per level; the copy stream waits on each level's counter
 // (cuStreamWaitValue32) and copies the level to the host while the next
-// levels are computed.  Same kernel arithmetic as adjoint(); false when the
-// configuration does not allow it (gather kernel, angle groups, several
-// angle batches, no brick queue, no stream-wait support).
-bool Projector::adjoint_host_ref(const float* proj, float* host, cudaStream_t s) {
+// levels are computed.  Same per-brick arithmetic as adjoint() (the two
+// launches add the halves' partial sums); false when the configuration does
+// not allow it (gather kernel, angle groups, several angle batches, no brick
+// queue, no stream-wait support).
+bool Projector::adjoint_host_ref(const float* host_proj, float* host, cudaStream_t s) {
     const char* e = std::getenv("KCT_ADJ_PROGRESSIVE");
     if (e && e[0] == '0') return false;
     if (adj_gather_ || adj_groups_ > 1 || dg_.na > kMaxAnglesPerLaunch || !d_queue_ || !wait_value32())
@@ -1817,12 +1825,28 @@ bool Projector::adjoint_host_ref(const float* proj, float* host, cudaStream_t s)
     const unsigned per_level =
         (unsigned)(((dg_.nx + BX - 1) / BX) * ((dg_.ny + BY - 1) / BY));
     if (!d_level_) KCT_CUDA(cudaMalloc(&d_level_, (size_t)nbz * sizeof(unsigned)));
-    float* dev = scratch(0, m_);
-    KCT_CUDA(cudaMemsetAsync(d_level_, 0, (size_t)nbz * sizeof(unsigned), s));
+    const size_t per = (size_t)dg_.nu * dg_.nv;
+    float* tmp = scratch(2, n_);  // reference-layout projections
+    float* q = scratch(1, n_);    // native projections
+    float* dev = scratch(0, m_);  // reference-layout volume
     cudaStream_t sc = pipe_stream();
-    KCT_CUDA(cudaEventRecord(pipe_ev_[0], s));  // the copy stream sees the reset counters
-    KCT_CUDA(cudaStreamWaitEvent(sc, pipe_ev_[0], 0));
-    adjoint_impl(proj, dev, 0, dg_.na, false, d_level_, s);
+    const char* sp = std::getenv("KCT_ADJ_SPLIT");
+    const int H = (dg_.na >= 4 * kPipeMinAngles && !(sp && sp[0] == '0')) ? dg_.na / 2 : dg_.na;
+    KCT_CUDA(cudaMemcpyAsync(tmp, host_proj, H * per * sizeof(float), cudaMemcpyHostToDevice, s));
+    KCT_CUDA(cudaMemsetAsync(d_level_, 0, (size_t)nbz * sizeof(unsigned), s));
+    KCT_CUDA(cudaEventRecord(pipe_ev_[0], s));  // copy stream: after this call's earlier work
+    KCT_CUDA(cudaStreamWaitEvent(sc, pipe_ev_[0], 0));  // and sees the reset counters
+    if (H < dg_.na)
+        KCT_CUDA(cudaMemcpyAsync(tmp + H * per, host_proj + H * per, (dg_.na - H) * per * sizeof(float),
+                                 cudaMemcpyHostToDevice, sc));
+    KCT_CUDA(cudaEventRecord(up_ev_, sc));
+    proj_to_native_range(tmp, q, 0, H, s);
+    if (H < dg_.na) {
+        adjoint_impl(q, dev, 0, H, false, true, nullptr, s);
+        KCT_CUDA(cudaStreamWaitEvent(s, up_ev_, 0));
+        proj_to_native_range(tmp, q, H, dg_.na, s);
+    }
+    adjoint_impl(q, dev, H < dg_.na ? H : 0, dg_.na, H < dg_.na, true, d_level_, s);
     const size_t plane = (size_t)dg_.nx * dg_.ny;
     for (int L = 0; L < nbz; ++L) {
         const CUresult r = wait_value32()((CUstream)sc, (CUdeviceptr)(d_level_ + L), per_level,

@@ -36,10 +36,11 @@ class Projector {
                        cudaStream_t s) const;
     void adjoint_range(const float* proj, float* vol, int a_begin, int a_end, bool accumulate,
                        cudaStream_t s) const;
-    // Adjoint of native device projections into a HOST volume in the
-    // reference layout, copied out z level by z level while the kernel runs
-    // (synchronous).  false: not available for this handle (use adjoint()).
-    bool adjoint_host_ref(const float* proj, float* host, cudaStream_t s);
+    // Adjoint of HOST projections into a HOST volume, reference layouts:
+    // uploads in two angle halves, copies the volume out z level by z level
+    // while the kernel runs (synchronous).  false: not available for this
+    // handle (stage the data and use adjoint()).
+    bool adjoint_host_ref(const float* host_proj, float* host, cudaStream_t s);
     // Host-buffer pipeline (capi.cu): angle chunks, a copy stream and events.
     static constexpr int kPipeChunks = 4, kPipeMinAngles = 4;
     int pipe_chunks() const { return pipe_chunks_; }
@@ -101,7 +102,7 @@ class Projector {
     size_t adj_smem_bytes() const;
     void build_walk_table();
     void adjoint_impl(const float* proj, float* vol, int a_begin, int a_end, bool accumulate,
-                      unsigned* level_done, cudaStream_t s) const;
+                      bool out_ref, unsigned* level_done, cudaStream_t s) const;
 
     kct_grid grid_;
     DevGeom dg_{};
