@@ -1679,18 +1679,32 @@ void Projector::vol_to_padded_z(const float* ref, int z0, int z1, cudaStream_t s
                      vpad_stride(dg_.nz));
 }
 
-// native volume -> padded copy (column stride nz + 2; the pad slabs stay 0)
+// native volume -> padded copy (column stride vpad_stride(nz); the pad slabs
+// stay 0): one warp per voxel column, float4 reads when nz % 4 == 0
 __global__ void __launch_bounds__(256) pad_kernel(const float* __restrict__ nat,
-                                                  float* __restrict__ pad, int nz, size_t m) {
-    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < m;
-         t += (size_t)gridDim.x * blockDim.x) {
-        const size_t p = t / (unsigned)nz, kk = t - p * (unsigned)nz;
-        pad[p * vpad_stride(nz) + kVOff + kk] = nat[t];
+                                                  float* __restrict__ pad, int nz, int ncols) {
+    const int lane = threadIdx.x & 31;
+    const int stride = vpad_stride(nz);
+    for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < ncols;
+         p += (gridDim.x * blockDim.x) >> 5) {
+        const float* src = nat + (size_t)p * nz;
+        float* dst = pad + (size_t)p * stride + kVOff;
+        if ((nz & 3) == 0) {
+            for (int q = lane; q < nz / 4; q += 32) {
+                const float4 v = __ldg(reinterpret_cast<const float4*>(src) + q);
+                dst[4 * q] = v.x;
+                dst[4 * q + 1] = v.y;
+                dst[4 * q + 2] = v.z;
+                dst[4 * q + 3] = v.w;
+            }
+        } else {
+            for (int q = lane; q < nz; q += 32) dst[q] = __ldg(src + q);
+        }
     }
 }
 
 void Projector::pad_volume(const float* nat, cudaStream_t s) const {
-    pad_kernel<<<148 * 8, 256, 0, s>>>(nat, d_vpad_, dg_.nz, m_);
+    pad_kernel<<<148 * 16, 256, 0, s>>>(nat, d_vpad_, dg_.nz, dg_.nx * dg_.ny);
     KCT_LAUNCHED();
 }
 
