@@ -42,7 +42,10 @@ class Projector {
     // handle (stage the data and use adjoint()).
     bool adjoint_host_ref(const float* host_proj, float* host, cudaStream_t s);
     // Host-buffer pipeline (capi.cu): angle chunks, a copy stream and events.
-    static constexpr int kPipeChunks = 4, kPipeMinAngles = 4;
+#ifndef KCT_PIPE_CHUNKS
+#define KCT_PIPE_CHUNKS 4
+#endif
+    static constexpr int kPipeChunks = KCT_PIPE_CHUNKS, kPipeMinAngles = 4;
     int pipe_chunks() const { return pipe_chunks_; }
     int pipe_angle(int c) const { return (int)((long long)dg_.na * c / pipe_chunks_); }
     cudaStream_t pipe_stream();
