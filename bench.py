@@ -215,7 +215,8 @@ def run_ours(args):
     from paper_2509_08574_b200 import shard
     my_angles = shard.angle_indices(na, ws, rank)
     geom_f = shard.shard_geometry(geom_all, ws, rank)
-    grid_b = shard.slab_grid(grid, ws, rank, axis="y")
+    from paper_2509_08574_b200 import distributed as _dist
+    grid_b = shard.slab_grid(grid, ws, rank, "y", _dist.slab_bounds(grid, geom_all, ws))
     A_f = k.ConeBeamProjector(grid, geom_f, device=local)
     A_b = A_f if ws == 1 else k.ConeBeamProjector(grid_b, geom_all, device=local)
     nnz_f = A_f.count_nnz()
@@ -409,7 +410,7 @@ def run_recon(k, synth, cfg, grid, prior, follow, dev, args, ws=1, rank=0, share
         from paper_2509_08574_b200 import distributed, shard
         proj_h = k.ProjectionSet(geom_f, b)
         A, j0, j1 = distributed.slab_projector(grid, geom_f, ws, rank)
-        grid_s = shard.slab_grid(grid, ws, rank, axis="y")
+        grid_s = A.grid
         plane = grid.dims[0] * grid.dims[2]
         prior_s = prior_rec[j0 * plane:j1 * plane].contiguous()  # native y-slab
         follow_s = distributed.y_slab(follow, grid, j0, j1)

@@ -140,11 +140,25 @@ def install_slab(projector: ConeBeamProjector, rank: int, world: int, j0: int, n
     _check(lib.kct_set_slab(projector.handle, rank, world, j0, ny_global, cb, None))
 
 
+def slab_bounds(grid, geometry, world: int) -> list:
+    """y-slab boundaries of all ranks, balanced by backprojection work
+    (shard.coverage_weights of a full circle of 64 views with this system's
+    source, detector and offsets — not of the scan's own angles, so every scan
+    of one system (prior and follow-ups) gets the same slabs); the same on
+    every rank."""
+    from . import ConeBeamGeometry
+    circle = ConeBeamGeometry(geometry.dso, geometry.dsd, geometry.nu, geometry.nv, geometry.pu,
+                              geometry.pv, 2.0 * np.pi * np.arange(64) / 64, geometry.offset_u,
+                              geometry.offset_v)
+    return shard.balanced_bounds(shard.coverage_weights(grid, circle, "y"), world)
+
+
 def slab_projector(grid, geometry, world: int, rank: int, group=None, device=None):
-    """This rank's projector on its y-slab of `grid`, in slab mode; returns
-    (projector, j0, j1)."""
-    j0, j1 = shard.slab_range(grid.dims[1], world, rank)
-    A = ConeBeamProjector(shard.slab_grid(grid, world, rank, axis="y"), geometry, device)
+    """This rank's projector on its (work-balanced) y-slab of `grid`, in slab
+    mode; returns (projector, j0, j1)."""
+    bounds = slab_bounds(grid, geometry, world)
+    j0, j1 = bounds[rank], bounds[rank + 1]
+    A = ConeBeamProjector(shard.slab_grid(grid, world, rank, "y", bounds), geometry, device)
     install_slab(A, rank, world, j0, grid.dims[1], group)
     return A, j0, j1
 
@@ -178,7 +192,7 @@ def irn_piccs_slab(proj, grid, prior, params=None, opts=None, group=None) -> Rec
     import torch.distributed as dist
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     A, j0, j1 = slab_projector(grid, proj.geometry, world, rank, group)
-    g = shard.slab_grid(grid, world, rank, axis="y")
+    g = A.grid
     return irn_piccs(proj, g, y_slab(prior, grid, j0, j1), params, _slab_opts(opts, grid, j0, j1),
                      projector=A)
 
@@ -187,7 +201,7 @@ def irn_tv_slab(proj, grid, params=None, opts=None, group=None) -> ReconReport:
     import torch.distributed as dist
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     A, j0, j1 = slab_projector(grid, proj.geometry, world, rank, group)
-    g = shard.slab_grid(grid, world, rank, axis="y")
+    g = A.grid
     return irn_tv(proj, g, params, _slab_opts(opts, grid, j0, j1), projector=A)
 
 
@@ -195,5 +209,5 @@ def cgls_recon_slab(proj, grid, iters, opts=None, tolerance=0.0, group=None) -> 
     import torch.distributed as dist
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     A, j0, j1 = slab_projector(grid, proj.geometry, world, rank, group)
-    g = shard.slab_grid(grid, world, rank, axis="y")
+    g = A.grid
     return cgls_recon(proj, g, iters, _slab_opts(opts, grid, j0, j1), tolerance, projector=A)

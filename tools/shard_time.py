@@ -8,7 +8,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_2509_08574_b200 as k  # noqa: E402
-from paper_2509_08574_b200 import shard, synth  # noqa: E402
+from paper_2509_08574_b200 import distributed, shard, synth  # noqa: E402
 
 
 def t_op(fn, reps=3):
@@ -39,8 +39,11 @@ for N in [int(a) for a in sys.argv[1:]] or [1, 2, 4, 8]:
         qa = torch.rand(Af.range_size(), device="cuda")
         ta.append(t_op(lambda: Af.apply_adjoint(qa, out=vb)))  # angle-sharded solver's adjoint
         del Af
+        # y-slabs balanced by backprojection work (distributed.slab_bounds),
+        # as the bench and the slab solver cut them
+        yb = distributed.slab_bounds(grid, geom, N)
         for axis, acc in (("z", tz), ("y", ty)):
-            g = shard.slab_grid(grid, N, r, axis=axis)
+            g = shard.slab_grid(grid, N, r, axis, yb if axis == "y" else None)
             Ab = k.ConeBeamProjector(g, geom)
             b = torch.empty(Ab.domain_size(), device="cuda")
             acc.append(t_op(lambda: Ab.apply_adjoint(y, out=b)))
