@@ -130,3 +130,37 @@ def test_y_slab_split_and_assemble_round_trip(world):
     j0, j1 = shard.slab_range(grid.dims[1], world, world - 1)
     assert sg.dims == (5, j1 - j0, 4)
     assert sg.origin[1] == pytest.approx(grid.origin[1] + j0 * grid.spacing[1])
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_balanced_bounds(world):
+    """shard.balanced_bounds: contiguous, covering, non-empty slabs on 4-plane
+    boundaries, equal totals for uniform weights, thinner slabs where the
+    weight is larger."""
+    bounds = shard.balanced_bounds(np.ones(64), world)
+    assert bounds[0] == 0 and bounds[-1] == 64 and len(bounds) == world + 1
+    assert all(b1 > b0 for b0, b1 in zip(bounds, bounds[1:]))
+    assert all(b % 4 == 0 for b in bounds)
+    sizes = np.diff(bounds)
+    assert sizes.max() - sizes.min() <= 4
+    w = np.concatenate([np.ones(32), 3 * np.ones(32)])
+    b2 = shard.balanced_bounds(w, 2)
+    assert b2[1] > 32  # the heavy half gets the thinner slab
+
+
+def test_slab_bounds_same_for_every_scan_of_a_system():
+    """distributed.slab_bounds depends on the system (source, detector), not on
+    the scan's angles: prior and follow-up projectors get the same y-slabs;
+    the corners of a cube outside the field of view make the outer slabs
+    thicker."""
+    from paper_2509_08574_b200 import distributed, synth
+    cfg = synth.CONFIGS["c3"]
+    grid = k.GridSpec((cfg.n,) * 3, (cfg.voxel,) * 3)
+    g60 = k.ConeBeamGeometry(synth.DSO, synth.DSD, cfg.det, cfg.det, cfg.pitch, cfg.pitch,
+                             synth.angles(60))
+    g360 = k.ConeBeamGeometry(synth.DSO, synth.DSD, cfg.det, cfg.det, cfg.pitch, cfg.pitch,
+                              synth.angles(360))
+    b = distributed.slab_bounds(grid, g60, 8)
+    assert b == distributed.slab_bounds(grid, g360, 8)
+    sizes = np.diff(b)
+    assert sizes[0] > sizes[3] and sizes[-1] > sizes[4]
