@@ -1725,7 +1725,13 @@ void Projector::forward_padded(float* proj, int a_begin, int a_end, cudaStream_t
 
 cudaStream_t Projector::pipe_stream() {
     if (!pipe_stream_) {
-        KCT_CUDA(cudaStreamCreateWithFlags(&pipe_stream_, cudaStreamNonBlocking));
+        // highest priority: the copy stream's small layout-transpose kernels
+        // are dispatched ahead of the pending blocks of the long operator
+        // kernel on the compute stream, so each chunk's copy starts when the
+        // chunk is done (not at the end of the next chunk's launch)
+        int lo = 0, hi = 0;
+        KCT_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        KCT_CUDA(cudaStreamCreateWithPriority(&pipe_stream_, cudaStreamNonBlocking, hi));
         for (auto& e : pipe_ev_) KCT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         KCT_CUDA(cudaEventCreateWithFlags(&up_ev_, cudaEventDisableTiming));
     }
