@@ -24,9 +24,6 @@ namespace kct {
 namespace {
 
 constexpr float kInf = __builtin_huge_valf();
-#ifndef KCT_ROW_VERIFY
-#define KCT_ROW_VERIFY 1  // adjoint row z-state: verify the estimate, search only on failure
-#endif
 constexpr unsigned kFull = 0xffffffffu;
 
 // ----------------------------------------------------------------------------
