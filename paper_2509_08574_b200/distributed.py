@@ -42,6 +42,16 @@ class _DeviceBuffer:
                                          "data": (int(ptr), False), "version": 3}
 
 
+def _on_stream(stream, device):
+    """Context making the library's CUDA stream (a raw handle; None / 0: the
+    legacy default stream) torch's current stream for a hook's collectives."""
+    import contextlib
+    import torch
+    if not stream:
+        return contextlib.nullcontext()
+    return torch.cuda.stream(torch.cuda.ExternalStream(stream, device=device))
+
+
 def install_allreduce(projector: ConeBeamProjector, group=None) -> None:
     """Put `projector` in angle-sharded mode, summing over `group` (torch.distributed)."""
     import torch
@@ -52,7 +62,11 @@ def install_allreduce(projector: ConeBeamProjector, group=None) -> None:
     def hook(ctx, buf, count, dtype, stream):
         try:
             t = torch.as_tensor(_DeviceBuffer(buf, count, dtype), device=device)
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+            # stream-ordered with the library's stream (NCCL waits for the
+            # kernels that produced `buf`, the library's next kernels wait
+            # for the sum)
+            with _on_stream(stream, device):
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
             return 0
         except Exception:  # surfaced as KCT_ERR_CUDA by the library
             return 1
@@ -117,6 +131,13 @@ def install_slab(projector: ConeBeamProjector, rank: int, world: int, j0: int, n
     cpu = dist.get_backend(group) == "gloo"
 
     def halo(ctx, lo_plane, hi_plane, lo_halo, hi_halo, count, stream):
+        try:
+            with _on_stream(stream, device):
+                return _halo(lo_plane, hi_plane, lo_halo, hi_halo, count)
+        except Exception:  # surfaced as KCT_ERR_CUDA by the library
+            return 1
+
+    def _halo(lo_plane, hi_plane, lo_halo, hi_halo, count):
         try:
             lo = torch.as_tensor(_DeviceBuffer(lo_plane, count, 0), device=device)
             hi = torch.as_tensor(_DeviceBuffer(hi_plane, count, 0), device=device)
