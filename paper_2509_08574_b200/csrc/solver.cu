@@ -643,6 +643,7 @@ struct Workspace {
     float *b = nullptr, *r = nullptr, *q = nullptr;
     float *x = nullptr, *p = nullptr, *s = nullptr, *prior = nullptr, *w1 = nullptr,
           *w2 = nullptr, *gt = nullptr;
+    float* atr = nullptr;  // A^T r of the current residual (before the regulariser terms)
     double* part = nullptr;
     Ctl* ctl = nullptr;
     double* hist = nullptr;  // [2][cap]: residual, error
@@ -690,7 +691,7 @@ Workspace& workspace(Projector& P, size_t hist_cap, size_t obj_cap) {
     Workspace& w = *ws;
     const size_t n = w.n;
     ensure(w, w.b, n); ensure(w, w.r, n); ensure(w, w.q, n);
-    ensure_vol(w, w.x); ensure_vol(w, w.p); ensure_vol(w, w.s);
+    ensure_vol(w, w.x); ensure_vol(w, w.p); ensure_vol(w, w.s); ensure_vol(w, w.atr);
     ensure(w, w.part, (size_t)kSlots * kGrid);
     ensure(w, w.ctl, 1);
     ensure(w, w.scal, 8);
@@ -762,6 +763,9 @@ struct Engine {
     cudaStream_t stream;
     RegCfg rc{};
     int kind = KCT_KIND_TV;
+    // w.r == b - A w.x and w.atr == A^T w.r (set by start / iterate; cleared
+    // when x is replaced)
+    bool r_current = false;
 
     // Multi-process modes (no-ops in a single process):
     //  * angle-sharded (kct_set_allreduce): rank-local rays; sum the partial
@@ -820,6 +824,8 @@ struct Engine {
     void objective(bool x_is_zero, int idx) {
         if (x_is_zero) {
             KCT_LAUNCH(k_resid, w.b, nullptr, nullptr, w.n, w.part, 0);
+        } else if (r_current) {
+            KCT_LAUNCH(k_stats, w.r, w.n, w.part);  // ||r||^2, r = b - A x (CGLS recurrence)
         } else {
             forward(w.x, w.q);
             KCT_LAUNCH(k_resid, w.b, w.q, nullptr, w.n, w.part, 0);
@@ -839,13 +845,22 @@ struct Engine {
             k_set_nonzero<<<1, kBlock, 0, stream>>>(w.ctl, w.part);
             KCT_LAUNCHED();
             adjoint(w.b, w.p);
-            reggrad(w.p, nullptr);
+            reggrad(w.p, w.p, nullptr);
             launch_scalar(w, S_REF, stream);
         } else {
             KCT_CUDA(cudaMemsetAsync(&w.ctl->x_nonzero, 0, sizeof(int), stream));
         }
+        // A warm start from the x the previous cycle's iterations ended on
+        // reuses their data residual r = b - A x (the CGLS recurrence keeps it
+        // up to rounding) and its A^T r: the stacked system changes between
+        // cycles only in the regulariser blocks, whose residual parts are
+        // evaluated from x anyway (section 4 of DESIGN.md) — one forward and one
+        // adjoint projection less per cycle.
+        const bool reuse = r_current && !x_is_zero;
         if (x_is_zero) {
             KCT_LAUNCH(k_resid, w.b, nullptr, w.r, w.n, w.part, 0);
+        } else if (reuse) {
+            KCT_LAUNCH(k_stats, w.r, w.n, w.part);
         } else {
             forward(w.x, w.q);
             KCT_LAUNCH(k_resid, w.b, w.q, w.r, w.n, w.part, 0);
@@ -855,11 +870,12 @@ struct Engine {
             launch_scalar(w, S_DATA, stream);
             launch_scalar(w, S_OBJ, stream, 0.0, nullptr, nullptr, w.obj + obj_idx, kind);
         }
-        adjoint(w.r, w.s);
-        reggrad(w.s, x_is_zero ? nullptr : w.x);
+        if (!reuse) adjoint(w.r, w.atr);
+        reggrad(w.atr, w.s, x_is_zero ? nullptr : w.x);
         launch_scalar(w, S_INIT, stream, tol);
         KCT_LAUNCH(k_update_p, w.p, w.s, w.m, w.ctl, 1);
         halo(w.p);
+        r_current = true;
     }
 
     // float4 stencil kernels when the slab count allows (KCT_SCALAR_STENCILS=1: scalar)
@@ -868,10 +884,10 @@ struct Engine {
         return rc.nz % 4 == 0 && !(e && e[0] == '1');
     }
 
-    // s <- s - regulariser gradient (in place), norms into slots 0..2
-    void reggrad(float* sv, const float* xv) {
-        if (use4()) KCT_LAUNCH(k_reggrad4, sv, xv, w.prior, w.w1, w.w2, sv, rc, w.part);
-        else KCT_LAUNCH(k_reggrad, sv, xv, w.prior, w.w1, w.w2, sv, rc, w.part);
+    // out <- in - regulariser gradient (in == out allowed), norms into slots 0..2
+    void reggrad(const float* in, float* out, const float* xv) {
+        if (use4()) KCT_LAUNCH(k_reggrad4, in, xv, w.prior, w.w1, w.w2, out, rc, w.part);
+        else KCT_LAUNCH(k_reggrad, in, xv, w.prior, w.w1, w.w2, out, rc, w.part);
         vol_slots({0, 1, 2});
     }
 
@@ -888,8 +904,8 @@ struct Engine {
         proj_slots({4});
         vol_slots({5});
         halo(w.x);
-        adjoint(w.r, w.s);
-        reggrad(w.s, w.x);
+        adjoint(w.r, w.atr);
+        reggrad(w.atr, w.s, w.x);
         launch_scalar(w, S_GAMMA, stream, 0.0, res, err);
         KCT_LAUNCH(k_update_p, w.p, w.s, w.m, w.ctl, 0);
         halo(w.p);
@@ -1112,6 +1128,7 @@ void irn_solve(Projector& P, int kind, const float* b, const float* prior, const
         } else {
             if (cycle == 0) e.objective(x_zero, 0);
             KCT_CUDA(cudaMemsetAsync(w.x, 0, w.m * sizeof(float), stream));
+            e.r_current = false;
             e.halo(w.x);
             e.start(true, p.inner_tolerance, -1);
         }
