@@ -252,7 +252,7 @@ int kct_adjoint(kct_projector* h, const float* proj, float* vol, int mem, int la
         DeviceGuard dg(P.device());
         auto s = static_cast<cudaStream_t>(stream);
         const size_t M = P.domain_size(), N = P.range_size();
-        // host buffers, reference layouts: upload in angle halves, volume out
+        // host buffers, reference layouts: upload in two angle parts, volume out
         // z level by z level while the adjoint runs (Projector::adjoint_host_ref)
         if (mem == KCT_MEM_HOST && layout == KCT_LAYOUT_REFERENCE && P.adjoint_host_ref(proj, vol, s))
             return;

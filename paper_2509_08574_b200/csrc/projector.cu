@@ -1823,7 +1823,7 @@ static WaitValue32Fn wait_value32() {
 }
 
 // Host-buffer adjoint, reference layouts: the projections arrive in two
-// angle halves (the second half's upload overlaps the first half's adjoint,
+// angle parts (the second part's upload overlaps the first part's adjoint,
 // which the second launch accumulates onto), and the volume leaves the device
 // z level by z level: the brick kernel writes the reference layout directly
 // (a z level's slabs are contiguous there) and its last launch counts

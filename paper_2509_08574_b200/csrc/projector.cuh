@@ -37,7 +37,7 @@ class Projector {
     void adjoint_range(const float* proj, float* vol, int a_begin, int a_end, bool accumulate,
                        cudaStream_t s) const;
     // Adjoint of HOST projections into a HOST volume, reference layouts:
-    // uploads in two angle halves, copies the volume out z level by z level
+    // uploads in two angle parts, copies the volume out z level by z level
     // while the kernel runs (synchronous).  false: not available for this
     // handle (stage the data and use adjoint()).
     bool adjoint_host_ref(const float* host_proj, float* host, cudaStream_t s);
