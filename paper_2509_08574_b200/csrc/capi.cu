@@ -191,13 +191,43 @@ void forward_host_pipelined(kct::Projector& P, const float* vol, float* proj, in
     float* qr = layout == KCT_LAYOUT_REFERENCE ? P.scratch(3, N) : nullptr;
     const int K = P.pipe_chunks();
     const size_t per = N / (size_t)P.n_angles();
+    // one counted launch (chunk-major blocks, finished columns per chunk):
+    // the copy stream waits on each chunk's count (cuStreamWaitValue32)
+    // instead of one launch per chunk — no per-chunk launch tails
+    const char* ce = std::getenv("KCT_FWD_COUNTED");
+    unsigned* done = (ce && ce[0] == '0') ? nullptr : P.fwd_done();
+    if (done) {
+        KCT_CUDA(cudaMemsetAsync(done, 0, K * sizeof(unsigned), s));
+        KCT_CUDA(cudaEventRecord(P.pipe_event(0), s));
+    }
     if (Z > 0) {
         P.forward_split_lo(q, s);
         KCT_CUDA(cudaEventRecord(P.upload_event(), sc));
         KCT_CUDA(cudaStreamWaitEvent(s, P.upload_event(), 0));
         P.vol_to_padded_z(P.scratch(2, M), Z, P.grid().nz, s);
     }
-    for (int c = 0; c < K; ++c) {
+    bool counted = false;
+    if (done) {
+        const int band0 = Z > 0 ? 1 : 0;
+        KCT_CUDA(cudaStreamWaitEvent(sc, P.pipe_event(0), 0));  // sees the reset counts
+        counted = P.stream_wait_geq(sc, done, 0u);  // probe: stream memory ops available
+        if (counted) {
+            P.forward_counted(q, band0, done, s);
+            for (int c = 0; c < K; ++c) {
+                const int a0 = P.pipe_angle(c), a1 = P.pipe_angle(c + 1);
+                if (!P.stream_wait_geq(sc, done + c, P.fwd_chunk_columns(c, band0)))
+                    throw kct::CudaError("forward: stream wait failed");
+                const float* src = q + a0 * per;
+                if (qr) {
+                    P.proj_from_native_range(q, qr, a0, a1, sc);
+                    src = qr + a0 * per;
+                }
+                KCT_CUDA(cudaMemcpyAsync(proj + a0 * per, src, (a1 - a0) * per * sizeof(float),
+                                         cudaMemcpyDeviceToHost, sc));
+            }
+        }
+    }
+    for (int c = 0; !counted && c < K; ++c) {
         const int a0 = P.pipe_angle(c), a1 = P.pipe_angle(c + 1);
         if (Z > 0) P.forward_split_hi(q, c, s);
         else P.forward_padded(q, a0, a1, s);

@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
                                                   const float* __restrict__ dvtab,
                                                   const float* __restrict__ invdv,
                                                   const double* __restrict__ dvd, DevGeom g,
-                                                  const int* __restrict__ order) {
+                                                  const int* __restrict__ order,
+                                                  unsigned* __restrict__ done) {
     // blocks are dispatched in index order; `order` maps them to (angle, row
     // band, column quad) items longest-chord first, so the last wave holds
     // the shortest rays (no long tail, notably with few angles per GPU)
@@ -181,6 +182,15 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
                 const float q = dvv[c] * cp.inv_l;
                 o[iv] = acc[c] * __fsqrt_rn(__fmaf_rn(q, q, 1.f));
             }
+        }
+    }
+    if (done) {  // host pipeline: this column of this band of angle a is out
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+            int ck = 0;
+            while (ck + 1 < g.fwd_nchunks && a >= g.fwd_cb[ck + 1]) ++ck;
+            atomicAdd(done + ck, 1u);
         }
     }
 }
@@ -1171,6 +1181,9 @@ Projector::~Projector() {
     cudaFree(d_forder_);
     cudaFree(d_fpipe_);
     cudaFree(d_flo_);
+    cudaFree(d_fcnt_all_);
+    cudaFree(d_fcnt_hi_);
+    cudaFree(d_fdone_);
     cudaFree(d_vpad_);
     cudaFree(d_fhi_);
     if (pipe_stream_) {
@@ -1357,6 +1370,31 @@ void Projector::build_tables(const kct_geometry& geom) {
                 KCT_CUDA(cudaMalloc(&d_fpipe_, pord.size() * sizeof(int)));
                 KCT_CUDA(cudaMemcpy(d_fpipe_, pord.data(), pord.size() * sizeof(int),
                                     cudaMemcpyHostToDevice));
+                // the same items chunk-major for the single counted launch of
+                // the host pipeline (forward_counted): all bands, and bands 1..
+                {
+                    const int B = fwd_bands_;
+                    std::vector<int> all, hi;
+                    for (int c = 0; c < pipe_chunks_; ++c) {
+                        const int a0 = pipe_angle(c), a1 = pipe_angle(c + 1);
+                        for (size_t t = 0; t < nitems; ++t) {
+                            const int it = key[t].second;
+                            const int quad = it % nq, band = (it / nq) % B, a = it / (nq * B);
+                            if (a < a0 || a >= a1) continue;
+                            all.push_back(it);
+                            if (band > 0) hi.push_back(quad + nq * ((band - 1) + (B - 1) * a));
+                        }
+                    }
+                    KCT_CUDA(cudaMalloc(&d_fcnt_all_, all.size() * sizeof(int)));
+                    KCT_CUDA(cudaMemcpy(d_fcnt_all_, all.data(), all.size() * sizeof(int),
+                                        cudaMemcpyHostToDevice));
+                    if (!hi.empty()) {
+                        KCT_CUDA(cudaMalloc(&d_fcnt_hi_, hi.size() * sizeof(int)));
+                        KCT_CUDA(cudaMemcpy(d_fcnt_hi_, hi.data(), hi.size() * sizeof(int),
+                                            cudaMemcpyHostToDevice));
+                    }
+                    KCT_CUDA(cudaMalloc(&d_fdone_, (size_t)pipe_chunks_ * sizeof(unsigned)));
+                }
                 // split upload of a host volume: the rays of row band 0 stay
                 // below slab Z (largest continuous z index over every column's
                 // clip, row band 0's top row; + 2 slabs of margin), so band 0
@@ -1627,7 +1665,7 @@ __global__ void __launch_bounds__(256) adj_group_sum(float* __restrict__ out,
 template <bool COUNT>
 static void launch_fwd(int C, int bands, int band0, const float* vol, float* out, const ColParams* cols,
                        const float* dv, const float* invdv, const double* dvd, const DevGeom& g,
-                       const int* order, cudaStream_t s) {
+                       const int* order, cudaStream_t s, unsigned* done = nullptr) {
     // 1D grid over (angle, band, column quad) items
     const unsigned nq = (unsigned)((g.nu + kFwdWarps - 1) / kFwdWarps);
     const dim3 g1(nq * (unsigned)bands * (unsigned)g.na, 1, 1);
@@ -1636,10 +1674,10 @@ static void launch_fwd(int C, int bands, int band0, const float* vol, float* out
     gg.fwd_bands = bands;
     gg.fwd_band0 = band0;
     switch (C) {
-    case 1: fwd_kernel<1, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order); break;
-    case 2: fwd_kernel<2, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order); break;
-    case 3: fwd_kernel<3, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order); break;
-    default: fwd_kernel<4, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order); break;
+    case 1: fwd_kernel<1, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, done); break;
+    case 2: fwd_kernel<2, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, done); break;
+    case 3: fwd_kernel<3, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, done); break;
+    default: fwd_kernel<4, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, done); break;
     }
     KCT_LAUNCHED();
 }
@@ -1669,6 +1707,21 @@ void Projector::forward_split_hi(float* proj, int c, cudaStream_t s) const {
                       d_cols_ + (size_t)a0 * dg_.nu, d_dv_, d_invdv_, d_dvd_, g,
                       d_fhi_ + fhi_off_[c], s);
 }
+// Host pipeline, one launch: bands band0.. of every angle in chunk-major
+// block order, counting finished columns per pipeline chunk into `done`
+// (expected counts: fwd_chunk_columns); with the split upload band0 = 1 (band
+// 0 ran before), else 0.
+void Projector::forward_counted(float* proj, int band0, unsigned* done, cudaStream_t s) const {
+    DevGeom g = dg_;
+    g.fwd_nchunks = pipe_chunks_;
+    for (int c = 0; c <= pipe_chunks_; ++c) g.fwd_cb[c] = pipe_angle(c);
+    launch_fwd<false>(fwd_c_, fwd_bands_ - band0, band0, d_vpad_ + kVOff, proj, d_cols_, d_dv_,
+                      d_invdv_, d_dvd_, g, band0 ? d_fcnt_hi_ : d_fcnt_all_, s, done);
+}
+unsigned Projector::fwd_chunk_columns(int c, int band0) const {
+    return (unsigned)((pipe_angle(c + 1) - pipe_angle(c)) * dg_.nu * (fwd_bands_ - band0));
+}
+
 // reference-layout slabs [z0, z1) straight into the padded native volume
 void Projector::vol_to_padded_z(const float* ref, int z0, int z1, cudaStream_t s) const {
     const size_t plane = (size_t)dg_.nx * dg_.ny;
@@ -1820,6 +1873,12 @@ static WaitValue32Fn wait_value32() {
         return reinterpret_cast<WaitValue32Fn>(p);
     }();
     return fn;
+}
+
+bool Projector::stream_wait_geq(cudaStream_t sc, const unsigned* addr, unsigned value) const {
+    if (!wait_value32()) return false;
+    return wait_value32()((CUstream)sc, (CUdeviceptr)addr, value, CU_STREAM_WAIT_VALUE_GEQ) ==
+           CUDA_SUCCESS;
 }
 
 // Host-buffer adjoint, reference layouts: the projections arrive in two

@@ -62,6 +62,15 @@ class Projector {
     void vol_to_padded_z(const float* ref, int z0, int z1, cudaStream_t s) const;
     // forward of angles [a_begin, a_end) from the padded volume as it stands
     void forward_padded(float* proj, int a_begin, int a_end, cudaStream_t s) const;
+    // Host pipeline: one launch of bands band0.. for all angles, chunk-major,
+    // counting finished columns per pipeline chunk (fwd_chunk_columns each)
+    // into fwd_done(); false-free: available when pipe_chunks() > 1.
+    void forward_counted(float* proj, int band0, unsigned* done, cudaStream_t s) const;
+    unsigned fwd_chunk_columns(int chunk, int band0) const;
+    unsigned* fwd_done() const { return d_fdone_; }
+    // enqueue on `sc`: wait until *addr >= value (cuStreamWaitValue32); false
+    // when stream memory operations are unavailable (nothing enqueued)
+    bool stream_wait_geq(cudaStream_t sc, const unsigned* addr, unsigned value) const;
     // Per-ray count of positive-length Siddon segments (as float) into proj.
     void count(float* proj, cudaStream_t s) const;
     // FDK (fdk.hpp:50-139), native layouts; `filt` is N floats of scratch.
@@ -137,6 +146,9 @@ class Projector {
     int* d_flo_ = nullptr;            // block order of the split forward's band 0 (all angles)
     int* d_fhi_ = nullptr;            // ... of its bands 1.. per pipeline chunk (offsets fhi_off_)
     std::vector<int> fhi_off_;
+    int* d_fcnt_all_ = nullptr;       // chunk-major block orders of forward_counted (all bands,
+    int* d_fcnt_hi_ = nullptr;        //   bands 1..)
+    unsigned* d_fdone_ = nullptr;     // finished columns per pipeline chunk
     int* d_queue_ = nullptr;          // adjoint brick queue counter
     int adj_ctas_ = 0;                // resident CTAs of the persistent adjoint grid
     int adj_groups_ = 1;              // angle groups of the adjoint (small problems)
