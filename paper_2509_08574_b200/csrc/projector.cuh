@@ -43,7 +43,7 @@ class Projector {
     bool adjoint_host_ref(const float* host_proj, float* host, cudaStream_t s);
     // Host-buffer pipeline (capi.cu): angle chunks, a copy stream and events.
 #ifndef KCT_PIPE_CHUNKS
-#define KCT_PIPE_CHUNKS 4
+#define KCT_PIPE_CHUNKS 6  // host-forward output chunks (counted launch: 6 measured best of 4 / 6 / 8)
 #endif
     static constexpr int kPipeChunks = KCT_PIPE_CHUNKS, kPipeMinAngles = 4;
     int pipe_chunks() const { return pipe_chunks_; }
