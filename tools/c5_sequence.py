@@ -113,6 +113,7 @@ def main():
                           "followups": a.followups,
                           "seconds_per_followup": [round(s, 4) for s in secs],
                           "mean_seconds_per_followup": round(float(np.mean(secs)), 4),
+                          "median_seconds_per_followup": round(float(np.median(secs)), 4),
                           "total_seconds": round(total, 3), "prior_cgls_seconds": round(t_prior, 3),
                           "rel_error_vs_phantom": [round(e, 4) for e in errs],
                           "taus": [r.tau for r in reps]}), flush=True)
