@@ -116,8 +116,6 @@ struct DevGeom {
     int full_footprint;    // 1: some voxel square is not fully in front of a source
     int fwd_bands;         // forward row bands (32*C rows each) in this launch
     int fwd_band0;         // first row band of this launch
-    int fwd_nchunks;       // host pipeline: angle chunks [fwd_cb[c], fwd_cb[c + 1]) whose
-    int fwd_cb[9];         //   finished columns fwd_kernel counts (fwd_done != nullptr)
 };
 
 // ---- deterministic fp64 block reduction ----------------------------------

@@ -50,9 +50,17 @@ constexpr int kVOff = KCT_VPAD_ALIGN ? 16 : 1;
 __host__ __device__ constexpr int vpad_stride(int nz) {
     return KCT_VPAD_ALIGN ? (kVOff + nz + 1 + 31) / 32 * 32 : nz + 2;  // (aligned: measured +-0)
 }
+// Host pipeline: angle chunks [cb[c], cb[c + 1]) whose finished columns a
+// counted forward launch adds to count[c].
+struct FwdChunks {
+    unsigned* count;
+    int n;
+    int cb[9];
+};
+
 // vol: slab 0 of voxel column 0 of the padded native volume (column stride
 // nz + 2, zero slabs at -1 and nz; Projector::pad_volume).
-template <int C, bool COUNT>
+template <int C, bool COUNT, bool DONE = false>
 __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const float* __restrict__ vol,
                                                   float* __restrict__ out,
                                                   const ColParams* __restrict__ cols,
@@ -60,7 +68,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
                                                   const float* __restrict__ invdv,
                                                   const double* __restrict__ dvd, DevGeom g,
                                                   const int* __restrict__ order,
-                                                  unsigned* __restrict__ done) {
+                                                  FwdChunks done) {
     // blocks are dispatched in index order; `order` maps them to (angle, row
     // band, column quad) items longest-chord first, so the last wave holds
     // the shortest rays (no long tail, notably with few angles per GPU)
@@ -184,13 +192,13 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
             }
         }
     }
-    if (done) {  // host pipeline: this column of this band of angle a is out
+    if (DONE) {  // host pipeline: this column of this band of angle a is out
         __threadfence();
         __syncwarp();
         if (lane == 0) {
             int ck = 0;
-            while (ck + 1 < g.fwd_nchunks && a >= g.fwd_cb[ck + 1]) ++ck;
-            atomicAdd(done + ck, 1u);
+            while (ck + 1 < done.n && a >= done.cb[ck + 1]) ++ck;
+            atomicAdd(done.count + ck, 1u);
         }
     }
 }
@@ -1665,7 +1673,7 @@ __global__ void __launch_bounds__(256) adj_group_sum(float* __restrict__ out,
 template <bool COUNT>
 static void launch_fwd(int C, int bands, int band0, const float* vol, float* out, const ColParams* cols,
                        const float* dv, const float* invdv, const double* dvd, const DevGeom& g,
-                       const int* order, cudaStream_t s, unsigned* done = nullptr) {
+                       const int* order, cudaStream_t s, const FwdChunks* done = nullptr) {
     // 1D grid over (angle, band, column quad) items
     const unsigned nq = (unsigned)((g.nu + kFwdWarps - 1) / kFwdWarps);
     const dim3 g1(nq * (unsigned)bands * (unsigned)g.na, 1, 1);
@@ -1673,11 +1681,23 @@ static void launch_fwd(int C, int bands, int band0, const float* vol, float* out
     DevGeom gg = g;
     gg.fwd_bands = bands;
     gg.fwd_band0 = band0;
+    FwdChunks fc{};
+    if (done) fc = *done;
+    if (!COUNT && done) {  // host pipeline (counted launch)
+        switch (C) {
+        case 1: fwd_kernel<1, false, true><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
+        case 2: fwd_kernel<2, false, true><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
+        case 3: fwd_kernel<3, false, true><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
+        default: fwd_kernel<4, false, true><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
+        }
+        KCT_LAUNCHED();
+        return;
+    }
     switch (C) {
-    case 1: fwd_kernel<1, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, done); break;
-    case 2: fwd_kernel<2, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, done); break;
-    case 3: fwd_kernel<3, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, done); break;
-    default: fwd_kernel<4, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, done); break;
+    case 1: fwd_kernel<1, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
+    case 2: fwd_kernel<2, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
+    case 3: fwd_kernel<3, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
+    default: fwd_kernel<4, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
     }
     KCT_LAUNCHED();
 }
@@ -1712,11 +1732,12 @@ void Projector::forward_split_hi(float* proj, int c, cudaStream_t s) const {
 // (expected counts: fwd_chunk_columns); with the split upload band0 = 1 (band
 // 0 ran before), else 0.
 void Projector::forward_counted(float* proj, int band0, unsigned* done, cudaStream_t s) const {
-    DevGeom g = dg_;
-    g.fwd_nchunks = pipe_chunks_;
-    for (int c = 0; c <= pipe_chunks_; ++c) g.fwd_cb[c] = pipe_angle(c);
+    FwdChunks fc{};
+    fc.count = done;
+    fc.n = pipe_chunks_;
+    for (int c = 0; c <= pipe_chunks_; ++c) fc.cb[c] = pipe_angle(c);
     launch_fwd<false>(fwd_c_, fwd_bands_ - band0, band0, d_vpad_ + kVOff, proj, d_cols_, d_dv_,
-                      d_invdv_, d_dvd_, g, band0 ? d_fcnt_hi_ : d_fcnt_all_, s, done);
+                      d_invdv_, d_dvd_, dg_, band0 ? d_fcnt_hi_ : d_fcnt_all_, s, &fc);
 }
 unsigned Projector::fwd_chunk_columns(int c, int band0) const {
     return (unsigned)((pipe_angle(c + 1) - pipe_angle(c)) * dg_.nu * (fwd_bands_ - band0));
