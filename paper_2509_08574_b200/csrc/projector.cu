@@ -813,7 +813,7 @@ __global__ void __launch_bounds__(128) adj_walk_build(const ColParams* __restric
 template <bool TAB>
 __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel(
     const float4* __restrict__ rec, float* __restrict__ out, const ColParams* __restrict__ cols,
-    DevGeom g, BrickCfg bc, AngleBatch ab, int a0, int nab, int accumulate,
+    DevGeom g, BrickCfg bc, const float2* __restrict__ csb, int a0, int nab, int accumulate,
     const int* __restrict__ order, int* queue, float* __restrict__ out_part,
     const WalkEntry* __restrict__ tab, const unsigned long long* __restrict__ off) {
     extern __shared__ float sm[];
@@ -941,7 +941,8 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
         const float Y0 = g.oy + B.J0 * g.sy, Y1 = g.oy + (B.J0 + B.byn) * g.sy;
         for (int ia = a_lo; ia < a_hi; ++ia) {
             int iu_lo, iu_hi;
-            footprint(g, ab.cs[ia].x, ab.cs[ia].y, X0, X1, Y0, Y1, iu_lo, iu_hi);
+            const float2 csa = __ldg(csb + ia);
+            footprint(g, csa.x, csa.y, X0, X1, Y0, Y1, iu_lo, iu_hi);
             const ColParams* colp = cols + (size_t)ia * nu;
             const float4* yb = rec + (size_t)ia * nu * nv;
             for (int iu = iu_lo; iu <= iu_hi; ++iu) {
@@ -1193,6 +1194,7 @@ Projector::~Projector() {
     cudaFree(d_fcnt_hi_);
     cudaFree(d_fdone_);
     cudaFree(d_vpad_);
+    cudaFree(d_cs_);
     cudaFree(d_fhi_);
     if (pipe_stream_) {
         for (auto e : pipe_ev_) cudaEventDestroy(e);
@@ -1559,6 +1561,8 @@ void Projector::build_tables(const kct_geometry& geom) {
         adj_ctas_ = std::max(1, per_sm) * std::max(1, sms);
     }
 
+    KCT_CUDA(cudaMalloc(&d_cs_, cs_.size() * sizeof(float2)));
+    KCT_CUDA(cudaMemcpy(d_cs_, cs_.data(), cs_.size() * sizeof(float2), cudaMemcpyHostToDevice));
     build_walk_table();
 }
 
@@ -1587,9 +1591,7 @@ void Projector::build_walk_table() {
     bc.ngrp = 1;
     const size_t nb = (size_t)bc.nbx * bc.nby * bc.nbz;
     const size_t noff = nb * (dg_.na + 1);
-    float2* d_cs = nullptr;
-    KCT_CUDA(cudaMalloc(&d_cs, cs_.size() * sizeof(float2)));
-    KCT_CUDA(cudaMemcpy(d_cs, cs_.data(), cs_.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    const float2* d_cs = d_cs_;
     KCT_CUDA(cudaMalloc(&d_off_, noff * sizeof(unsigned long long)));
     const unsigned blocks = (unsigned)((nb + 3) / 4);
     adj_walk_build<false><<<blocks, 128>>>(d_cols_, d_cs, dg_, bc, d_off_, nullptr);
@@ -1608,7 +1610,6 @@ void Projector::build_walk_table() {
         ob[dg_.na] = tot;
     }
     if (tot == 0 || tot * sizeof(WalkEntry) > budget) {
-        cudaFree(d_cs);
         cudaFree(d_off_);
         d_off_ = nullptr;
         return;
@@ -1619,7 +1620,6 @@ void Projector::build_walk_table() {
                                           static_cast<WalkEntry*>(d_tab_));
     KCT_LAUNCHED();
     KCT_CUDA(cudaDeviceSynchronize());
-    cudaFree(d_cs);
     tab_entries_ = tot;
 }
 
@@ -1866,11 +1866,11 @@ void Projector::adjoint_impl(const float* proj, float* vol, int a_begin, int a_e
             const unsigned grid = d_queue_ ? std::min(nctas, adj_ctas_) : nctas;
             if (d_tab_)
                 adj_brick_kernel<true><<<grid, kAdjWarps * 32, smem, s>>>(
-                    reinterpret_cast<const float4*>(d_yw_), vol, cols, dg_, bc, ab, a0, nab, accum, d_border_,
+                    reinterpret_cast<const float4*>(d_yw_), vol, cols, dg_, bc, d_cs_ + a0, a0, nab, accum, d_border_,
                     d_queue_, d_part_, static_cast<const WalkEntry*>(d_tab_), d_off_);
             else
                 adj_brick_kernel<false><<<grid, kAdjWarps * 32, smem, s>>>(
-                    reinterpret_cast<const float4*>(d_yw_), vol, cols, dg_, bc, ab, a0, nab, accum, d_border_,
+                    reinterpret_cast<const float4*>(d_yw_), vol, cols, dg_, bc, d_cs_ + a0, a0, nab, accum, d_border_,
                     d_queue_, d_part_, nullptr, nullptr);
             if (bc.ngrp > 1) {
                 KCT_LAUNCHED();

@@ -143,6 +143,7 @@ class Projector {
     cudaEvent_t up_ev_ = nullptr;
     int fwd_split_z_ = 0;
     float* d_vpad_ = nullptr;         // padded native volume read by the forward
+    float2* d_cs_ = nullptr;          // per-angle (cos, sin) on the device
     int* d_flo_ = nullptr;            // block order of the split forward's band 0 (all angles)
     int* d_fhi_ = nullptr;            // ... of its bands 1.. per pipeline chunk (offsets fhi_off_)
     std::vector<int> fhi_off_;
