@@ -57,6 +57,7 @@ struct FwdChunks {
     int n;
     int cb[9];
 };
+static_assert(Projector::kPipeChunks <= 8, "FwdChunks holds at most 8 pipeline chunks");
 
 // vol: slab 0 of voxel column 0 of the padded native volume (column stride
 // nz + 2, zero slabs at -1 and nz; Projector::pad_volume).
