@@ -504,6 +504,22 @@ def main():
     ap.add_argument("--recon-split", default="yslab", choices=["yslab", "angles"],
                     help="multi-GPU PICCS decomposition (N > 1)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: launch the ranks ourselves (torchrun, rendezvous
+        # on 127.0.0.1) with NCCL's communicator logging on, so the rank count
+        # of every communicator is visible in the log; rank 0 prints the line
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        log(f"[bench] spawning {args.gpus} ranks: {' '.join(cmd)}")
+        sys.exit(subprocess.call(cmd, env=env))
     if args.impl == "reference":
         run_reference(args)
     else:

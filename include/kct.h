@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define KCT_ABI_VERSION 1
+#define KCT_ABI_VERSION 2
 
 enum kct_status {
     KCT_OK = 0,
@@ -98,6 +98,10 @@ typedef struct kct_report {
     double tau;        /* resolved smoothing parameter (irn_*) */
     int converged;
     int breakdown;
+    /* SolveTrace::wall_times (krylov.hpp:40, :115): seconds since the solve
+     * started, one per inner iteration (device event timeline); capacity as
+     * residual_history; NULL skips it.  (ABI 2) */
+    double* wall_times;         size_t wall_count;
 } kct_report;
 
 typedef struct kct_projector kct_projector;
@@ -147,6 +151,30 @@ int kct_proj_from_native(const kct_projector* h, const float* native, float* ref
  * weighting, Ram-Lak ramp filter, distance-weighted bilinear backprojection.
  * Needs >= 2 angles over a full circle (short scans are not compensated). */
 int kct_fdk(kct_projector* h, const float* proj, float* vol, int mem, int layout, void* stream);
+
+/* ---- solver options and the per-iteration hook ------------------------- */
+/* Options of the solvers run on this handle (value as double):
+ *   "solver_restart" 1: the reference's control flow at every CGLS start —
+ *       recompute r = b - A x and A^T r (krylov.hpp:68-75) — and a fresh A x
+ *       for every objective evaluation (recon.hpp:189, :238).  0 (default):
+ *       a warm start continues the data residual the previous cycle's CGLS
+ *       recurrence ended on and its A^T r (one forward and
+ *       one adjoint projection less per outer cycle).  The environment
+ *       variable KCT_SOLVER_RESTART=1 sets the default for new handles.
+ * Unknown key: ConfigError.  kct_projector_info reads options back. */
+int kct_set_option(kct_projector* h, const char* key, double value);
+
+/* IterateHook (krylov.hpp:22-23; ReconOptions::hook recon.hpp:68-72, called
+ * at recon.hpp:223-228 / :291-295): after every inner CGLS iteration the
+ * solver copies the iterate to pinned host memory on a side stream and calls
+ * fn(ctx, iteration, x, m) from a CUDA host callback (iteration is 1-based and
+ * runs across outer cycles, as the reference's global_iter; x is float32 in
+ * the reference layout, valid only during the call; m = domain size of the
+ * handle — a y-slab handle passes its slab).  Calls arrive in iteration order
+ * and all have returned when the solver returns.  The callback must not call
+ * CUDA or this library.  fn = NULL removes the hook (no copies at all). */
+typedef void (*kct_iterate_hook)(void* ctx, size_t iteration, const float* x, size_t m);
+int kct_set_iterate_hook(kct_projector* h, kct_iterate_hook fn, void* ctx);
 
 /* ---- multi-process solves ------------------------------------------------ */
 /* Collective hook: sum `count` elements (dtype 0 = float32, 1 = float64) of

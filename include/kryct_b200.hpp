@@ -10,16 +10,30 @@
 // solvers (kryct::cgls, kryct::StackedMap, ...) can drive the GPU operator.
 // Values cross the boundary as float32 (the reference reads float32 files,
 // io.hpp:48-49); the solvers reduce in float64 on the device.
-// ReconOptions::hook (a host callback per inner iteration) cannot be served
-// by a device-resident solver; set ground_truth for the error history instead
-// (a set hook raises ConfigError).
+// ReconOptions::hook (the reference's per-iteration IterateHook) is served as
+// an opt-in device->host copy of every iterate (kct_set_iterate_hook): the
+// copy overlaps the solve on a side stream and the hook runs on a CUDA host
+// callback thread, in iteration order, all calls done before the solver
+// returns.  The error history against ground_truth needs no hook (device).
+//
+// Handle cache: a projector handle owns device tables (the adjoint walk
+// table: 339 MB at 256^3 / 60 views) and a solver workspace, whose creation
+// costs milliseconds of kernels and allocations.  The reference builds its
+// CPU projector per call (recon.hpp:155, :282), which is cheap there; here the
+// drivers keep the last KRYCT_B200_CACHE (default 2, 0 = off) handles keyed by
+// (grid, geometry) and reuse them.  A handle in use by one call is not handed
+// to a concurrent call (that call builds its own).
 #pragma once
 
 #include <kryct/linear_map.hpp>
 #include <kryct/recon.hpp>
 #include <kryct/types.hpp>
 
+#include <cstdlib>
+#include <exception>
+#include <list>
 #include <memory>
+#include <mutex>
 #include <span>
 #include <string>
 #include <vector>
@@ -101,14 +115,103 @@ class GpuConeBeamProjector final : public kryct::LinearMap {
 
 namespace detail {
 
+// ---- handle cache keyed by (grid, geometry) ---------------------------------
+struct CacheKey {
+    kryct::GridSpec grid;
+    kryct::ConeBeamGeometry geom;
+    bool operator==(const CacheKey& o) const {
+        const auto& a = grid;
+        const auto& b = o.grid;
+        return a.dims == b.dims && a.spacing.x == b.spacing.x && a.spacing.y == b.spacing.y &&
+               a.spacing.z == b.spacing.z && a.origin.x == b.origin.x &&
+               a.origin.y == b.origin.y && a.origin.z == b.origin.z && geom.dso == o.geom.dso &&
+               geom.dsd == o.geom.dsd && geom.detector.nu == o.geom.detector.nu &&
+               geom.detector.nv == o.geom.detector.nv && geom.detector.pu == o.geom.detector.pu &&
+               geom.detector.pv == o.geom.detector.pv && geom.offset_u == o.geom.offset_u &&
+               geom.offset_v == o.geom.offset_v && geom.angles == o.geom.angles;
+    }
+};
+
+struct HandleCache {
+    std::mutex mu;
+    std::list<std::pair<CacheKey, std::shared_ptr<GpuConeBeamProjector>>> idle;  // MRU first
+    std::size_t capacity() const {
+        const char* e = std::getenv("KRYCT_B200_CACHE");
+        return e ? static_cast<std::size_t>(std::strtoul(e, nullptr, 10)) : 2;
+    }
+    // check a handle out (removed from the cache while in use)
+    std::shared_ptr<GpuConeBeamProjector> acquire(const kryct::GridSpec& g,
+                                                  const kryct::ConeBeamGeometry& ge) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            const CacheKey key{g, ge};
+            for (auto it = idle.begin(); it != idle.end(); ++it)
+                if (it->first == key) {
+                    auto h = it->second;
+                    idle.erase(it);
+                    return h;
+                }
+        }
+        return std::make_shared<GpuConeBeamProjector>(g, ge);
+    }
+    void release(std::shared_ptr<GpuConeBeamProjector> h) {
+        const std::size_t cap = capacity();
+        if (cap == 0) return;
+        std::lock_guard<std::mutex> lk(mu);
+        idle.emplace_front(CacheKey{h->grid(), h->geometry()}, std::move(h));
+        while (idle.size() > cap) idle.pop_back();
+    }
+    void clear() {
+        std::lock_guard<std::mutex> lk(mu);
+        idle.clear();
+    }
+};
+
+inline HandleCache& handle_cache() {
+    static HandleCache c;
+    return c;
+}
+
+struct CheckedOut {
+    std::shared_ptr<GpuConeBeamProjector> h;
+    CheckedOut(const kryct::GridSpec& g, const kryct::ConeBeamGeometry& ge)
+        : h(handle_cache().acquire(g, ge)) {}
+    ~CheckedOut() {
+        kct_set_iterate_hook(h->handle(), nullptr, nullptr);
+        handle_cache().release(std::move(h));
+    }
+};
+
+// IterateHook trampoline: float32 reference-layout iterate -> span<const double>.
+// An exception thrown by the hook stops further calls and is rethrown by the
+// solver entry point once the solve has returned.
+struct HookCtx {
+    const kryct::IterateHook* hook;
+    std::exception_ptr err;
+    std::vector<double> xd;
+};
+
+inline void hook_trampoline(void* ctx, std::size_t it, const float* x, std::size_t m) {
+    auto& c = *static_cast<HookCtx*>(ctx);
+    if (c.err) return;
+    try {
+        c.xd.assign(x, x + m);
+        (*c.hook)(it, c.xd);
+    } catch (...) {
+        c.err = std::current_exception();
+    }
+}
+
 inline kryct::ReconReport run(int kind, const kryct::ProjectionSet& proj,
                               const kryct::GridSpec& grid, const kryct::Volume* prior,
                               const kryct::RegularizationParams* params, std::size_t iters,
                               double tol, const kryct::ReconOptions& opts) {
-    if (opts.hook) throw kryct::ConfigError("kryct_b200: per-iteration hooks are not supported");
     proj.validate();
     grid.validate();
-    GpuConeBeamProjector A(grid, proj.geometry);
+    CheckedOut co(grid, proj.geometry);
+    const GpuConeBeamProjector& A = *co.h;
+    HookCtx hc{&opts.hook, nullptr, {}};
+    if (opts.hook) check(kct_set_iterate_hook(A.handle(), hook_trampoline, &hc));
     const std::size_t m = grid.dims.count();
     auto b = to_f32(proj.data);
     std::vector<float> pr, x0, gt, x(m);
@@ -162,10 +265,14 @@ inline kryct::ReconReport run(int kind, const kryct::ProjectionSet& proj,
     }
     r.solve_seconds = rep.solve_seconds;
     r.converged = rep.converged != 0;
+    if (hc.err) std::rethrow_exception(hc.err);
     return r;
 }
 
 }  // namespace detail
+
+/// Drop the cached projector handles (frees their device memory).
+inline void clear_handle_cache() { detail::handle_cache().clear(); }
 
 /// recon.hpp:312-315
 inline kryct::ReconReport cgls_recon(const kryct::ProjectionSet& proj, const kryct::GridSpec& grid,

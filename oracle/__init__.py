@@ -52,7 +52,8 @@ class KctReport(C.Structure):
                 ("outer_boundaries", C.POINTER(C.c_uint64)), ("outer_count", C.c_size_t),
                 ("outer_seconds", C.POINTER(C.c_double)),
                 ("solve_seconds", C.c_double), ("tau", C.c_double),
-                ("converged", C.c_int), ("breakdown", C.c_int)]
+                ("converged", C.c_int), ("breakdown", C.c_int),
+                ("wall_times", C.POINTER(C.c_double)), ("wall_count", C.c_size_t)]
 
 
 @dataclass

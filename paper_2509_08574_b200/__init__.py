@@ -89,8 +89,12 @@ class _Report(C.Structure):
                 ("outer_boundaries", C.POINTER(C.c_uint64)), ("outer_count", C.c_size_t),
                 ("outer_seconds", C.POINTER(C.c_double)),
                 ("solve_seconds", C.c_double), ("tau", C.c_double),
-                ("converged", C.c_int), ("breakdown", C.c_int)]
+                ("converged", C.c_int), ("breakdown", C.c_int),
+                ("wall_times", C.POINTER(C.c_double)), ("wall_count", C.c_size_t)]
 
+
+# kct_iterate_hook(ctx, iteration, x, m)
+_ITER_HOOK = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.POINTER(C.c_float), C.c_size_t)
 
 # Every symbol include/kct.h declares, with its ctypes signature.
 _P = C.c_void_p
@@ -121,6 +125,8 @@ _SIGS = {
     "kct_resolve_tau": ([C.c_double, _P, C.c_size_t], C.c_double),
     "kct_set_allreduce": ([_P, _P, _P], C.c_int),  # typed by distributed.install_allreduce
     "kct_fdk": ([_P, _P, _P, C.c_int, C.c_int, _P], C.c_int),
+    "kct_set_option": ([_P, C.c_char_p, C.c_double], C.c_int),
+    "kct_set_iterate_hook": ([_P, _ITER_HOOK, _P], C.c_int),
 }
 
 _lib = None
@@ -272,10 +278,15 @@ class RegularizationParams:
 
 @dataclass
 class ReconOptions:
-    """recon.hpp:68-72 (the per-iterate hook is not carried over the C ABI;
-    ground_truth drives the error history on the device instead)."""
+    """recon.hpp:68-72.  ``hook(iteration, x)`` is the reference's IterateHook
+    (krylov.hpp:22-23): called after every inner iteration (1-based, across
+    outer cycles) with a float32 copy of the iterate in the reference layout.
+    It is an opt-in device->host copy per iteration (kct_set_iterate_hook,
+    overlapped with the solve on a side stream); the error history against
+    ``ground_truth`` is computed on the device and needs no hook."""
     initial: object = None
     ground_truth: object = None
+    hook: object = None
 
 
 @dataclass
@@ -291,6 +302,7 @@ class ReconReport:
     converged: bool = False
     tau: float = 0.0
     breakdown: bool = False
+    wall_times: np.ndarray = field(default_factory=lambda: np.zeros(0))  # SolveTrace (krylov.hpp:40)
 
 
 # ---------------------------------------------------------------------------
@@ -414,9 +426,15 @@ class ConeBeamProjector:
         _check(_lib.kct_count_nnz(self._h, C.byref(n), None))
         return int(n.value)
 
+    def set_option(self, key: str, value) -> None:
+        """Solver option of this handle (kct_set_option): "solver_restart" = 1
+        runs the reference's control flow at every CGLS start (fresh
+        r = b - A x and A^T r, krylov.hpp:68-75; fresh A x for each objective)."""
+        _check(_lib.kct_set_option(self._h, key.encode(), float(value)))
+
     def info(self, key: str) -> float:
         """Which code path the handle runs (kct_projector_info): adj_slab,
-        adj_bz, adj_groups, fwd_split_z, ..."""
+        adj_bz, adj_groups, fwd_split_z, solver_restart, ..."""
         v = C.c_double()
         _check(_lib.kct_projector_info(self._h, key.encode(), C.byref(v)))
         return v.value
@@ -457,7 +475,7 @@ class ConeBeamProjector:
 def _report_buffers(n_obj, n_res, n_outer):
     bufs = dict(obj=np.zeros(max(n_obj, 1)), res=np.zeros(max(n_res, 1)),
                 err=np.zeros(max(n_res, 1)), bnd=np.zeros(max(n_outer, 1), dtype=np.uint64),
-                sec=np.zeros(max(n_outer, 1)))
+                sec=np.zeros(max(n_outer, 1)), wall=np.zeros(max(n_res, 1)))
     rep = _Report()
     dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
     rep.objective_history = dp(bufs["obj"])
@@ -465,6 +483,7 @@ def _report_buffers(n_obj, n_res, n_outer):
     rep.error_history = dp(bufs["err"])
     rep.outer_boundaries = bufs["bnd"].ctypes.data_as(C.POINTER(C.c_uint64))
     rep.outer_seconds = dp(bufs["sec"])
+    rep.wall_times = dp(bufs["wall"])
     return rep, bufs
 
 
@@ -476,7 +495,36 @@ def _unpack(rep, bufs, volume) -> ReconReport:
                        outer_boundaries=bufs["bnd"][:rep.outer_count].astype(np.int64),
                        outer_seconds=bufs["sec"][:rep.outer_count].copy(),
                        solve_seconds=rep.solve_seconds, converged=bool(rep.converged),
-                       tau=rep.tau, breakdown=bool(rep.breakdown))
+                       tau=rep.tau, breakdown=bool(rep.breakdown),
+                       wall_times=bufs["wall"][:rep.wall_count].copy())
+
+
+class _HookInstall:
+    """ReconOptions.hook installed on the handle for one solve (kct_set_iterate_hook)."""
+
+    def __init__(self, A, hook):
+        self.A, self.hook, self.cb, self.err = A, hook, None, None
+
+    def __enter__(self):
+        if self.hook is not None:
+            def tramp(ctx, it, x, m):
+                if self.err is not None:
+                    return
+                try:
+                    self.hook(int(it), np.ctypeslib.as_array(x, shape=(int(m),)).copy())
+                except BaseException as e:  # re-raised after the solve
+                    self.err = e
+            self.cb = _ITER_HOOK(tramp)
+            _check(_lib.kct_set_iterate_hook(self.A.handle, self.cb, None))
+        return self
+
+    def __exit__(self, *exc):
+        if self.cb is not None:
+            _lib.kct_set_iterate_hook(self.A.handle, _ITER_HOOK(), None)
+            self.cb = None
+        if self.err is not None and exc[0] is None:
+            raise self.err
+        return False
 
 
 def _projector_for(proj: ProjectionSet, grid: GridSpec, projector):
@@ -515,10 +563,11 @@ def cgls_recon(proj: ProjectionSet, grid: GridSpec, iters: int, opts: ReconOptio
     mem = _same_mem([b, x0, gt])
     out = _out_for(b, m, out)
     rep, bufs = _report_buffers(iters, iters, 1)
-    _check(_lib.kct_cgls_recon(A.handle, b.ptr, int(iters), x0.ptr if x0 else None,
-                               gt.ptr if gt else None, float(tolerance), _ptr(out), C.byref(rep),
-                               mem, _layout_code(layout, mem),
-                               _stream_of(mem, b.keep.device.index if mem == MEM_DEVICE else None)))
+    with _HookInstall(A, opts.hook):
+        _check(_lib.kct_cgls_recon(A.handle, b.ptr, int(iters), x0.ptr if x0 else None,
+                                   gt.ptr if gt else None, float(tolerance), _ptr(out),
+                                   C.byref(rep), mem, _layout_code(layout, mem),
+                                   _stream_of(mem, b.keep.device.index if mem == MEM_DEVICE else None)))
     return _unpack(rep, bufs, out)
 
 
@@ -536,10 +585,11 @@ def _irn(kind, proj, grid, prior, params, opts, projector, layout, out=None):
     o, i = int(params.outer_iters), int(params.inner_iters)
     rep, bufs = _report_buffers(o + 1, o * i, o)
     p = params._c()
-    _check(_lib.kct_irn(A.handle, kind, b.ptr, pr.ptr if pr else None, x0.ptr if x0 else None,
-                        gt.ptr if gt else None, C.byref(p), _ptr(out), C.byref(rep), mem,
-                        _layout_code(layout, mem),
-                        _stream_of(mem, b.keep.device.index if mem == MEM_DEVICE else None)))
+    with _HookInstall(A, opts.hook):
+        _check(_lib.kct_irn(A.handle, kind, b.ptr, pr.ptr if pr else None, x0.ptr if x0 else None,
+                            gt.ptr if gt else None, C.byref(p), _ptr(out), C.byref(rep), mem,
+                            _layout_code(layout, mem),
+                            _stream_of(mem, b.keep.device.index if mem == MEM_DEVICE else None)))
     return _unpack(rep, bufs, out)
 
 

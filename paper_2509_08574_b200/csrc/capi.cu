@@ -332,6 +332,7 @@ int kct_projector_info(const kct_projector* h, const char* key, double* value) {
         else if (k == "fwd_rows_per_warp") *value = 32 * P.fwd_chunks();
         else if (k == "fwd_bands") *value = P.dev_geom().fwd_bands;
         else if (k == "fwd_split_z") *value = P.fwd_split_z();
+        else if (k == "solver_restart") *value = P.solver_restart ? 1 : 0;
         else throw kct::ConfigError("kct_projector_info: unknown key '" + k + "'");
     });
 }
@@ -397,6 +398,28 @@ int kct_fdk(kct_projector* h, const float* proj, float* vol, int mem, int layout
         P.fdk(q, v, P.scratch(3, N), s);
         kct::stage_out(P, v, vol, M, true, mem, layout, 2, s);
         if (mem == KCT_MEM_HOST) KCT_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int kct_set_option(kct_projector* h, const char* key, double value) {
+    return guarded([&] {
+        auto& P = get(h);
+        if (!key) throw kct::ConfigError("null option key");
+        const std::string k(key);
+        if (k == "solver_restart") {
+            if (value != 0.0 && value != 1.0) throw kct::ConfigError("solver_restart must be 0 or 1");
+            P.solver_restart = value != 0.0;
+        } else {
+            throw kct::ConfigError("kct_set_option: unknown key '" + k + "'");
+        }
+    });
+}
+
+int kct_set_iterate_hook(kct_projector* h, kct_iterate_hook fn, void* ctx) {
+    return guarded([&] {
+        auto& P = get(h);
+        P.hook_fn = fn;
+        P.hook_ctx = fn ? ctx : nullptr;
     });
 }
 

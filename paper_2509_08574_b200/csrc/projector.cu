@@ -1151,8 +1151,12 @@ void validate_geometry(const kct_grid& grid, const kct_geometry& g) {
         if (sx > grid.ox && sx < hx && sy > grid.oy && sy < hy && sz > grid.oz && sz < hz)
             throw ConfigError("source position lies inside the volume");
     }
-    const double m = (double)grid.nx * grid.ny * grid.nz;
-    if (m > 2147483647.0) throw ConfigError("volume too large for 32-bit voxel indexing");
+    // The forward indexes the padded volume (column stride vpad_stride(nz)) and
+    // the walk table the rays ((angle * nu + column) * nv) with 32-bit integers.
+    const double mpad = (double)grid.nx * grid.ny * vpad_stride(grid.nz);
+    if (mpad > 2147483647.0) throw ConfigError("volume too large for 32-bit voxel indexing");
+    const double rays = (double)g.nu * g.nv * g.n_angles;
+    if (rays > 4294967295.0) throw ConfigError("too many rays for 32-bit ray indexing");
 }
 
 // ---- host-side tables ---------------------------------------------------------
@@ -1169,6 +1173,8 @@ Projector::Projector(const kct_grid& grid, const kct_geometry& geom, int device)
     pv_d_ = geom.pv;
     offu_d_ = geom.offset_u;
     offv_d_ = geom.offset_v;
+    const char* rs = std::getenv("KCT_SOLVER_RESTART");
+    solver_restart = rs && rs[0] == '1';
     const char* mode = std::getenv("KCT_ADJOINT");
     adj_gather_ = mode && std::string(mode) == "gather";
     build_tables(geom);

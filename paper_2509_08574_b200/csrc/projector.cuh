@@ -98,6 +98,10 @@ class Projector {
     kct_halo_fn halo_fn = nullptr;
     void* halo_ctx = nullptr;
     bool slab_mode() const { return halo_fn != nullptr; }
+    // Solver options (kct_set_option) and the per-iteration hook.
+    bool solver_restart = false;  // KCT_SOLVER_RESTART=1 sets it at creation
+    kct_iterate_hook hook_fn = nullptr;
+    void* hook_ctx = nullptr;
 
     int fwd_chunks() const { return fwd_c_; }
     int adj_k() const { return adj_k_; }

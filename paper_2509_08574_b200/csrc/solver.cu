@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <initializer_list>
 #include <string>
 #include <vector>
@@ -650,12 +651,30 @@ struct Workspace {
     double* obj = nullptr;   // [cap_obj]
     double* scal = nullptr;  // misc scalars
     double* gath = nullptr;  // y-slab mode: [2 * world] gather-by-sum buffer
+    double* red = nullptr;   // multi-process: packed fp64 slots of one all-reduce
     size_t cap = 0, cap_obj = 0;
     std::vector<void*> allocs;
+    // per-iteration hook: reference-layout device copy of x, pinned host copy,
+    // side stream, events (x copied / host copy done)
+    float* hook_dev = nullptr;
+    float* hook_host = nullptr;
+    int* hook_stop = nullptr;      // pinned copy of the CGLS stop flag at the copy
+    int* hook_stop_dev = nullptr;  // its snapshot on the solver stream
+    cudaStream_t hook_stream = nullptr;
+    cudaEvent_t hook_ev_x = nullptr, hook_ev_done = nullptr;
+    // wall_times: one event at the solve start + one per inner iteration
+    std::vector<cudaEvent_t> wall_ev;
 
     ~Workspace() {
+        if (hook_stream) cudaStreamSynchronize(hook_stream);
         for (void* ptr : allocs) cudaFree(ptr);
         for (void* ptr : {(void*)hist, (void*)obj}) cudaFree(ptr);
+        if (hook_host) cudaFreeHost(hook_host);
+        if (hook_stop) cudaFreeHost(hook_stop);
+        if (hook_stream) cudaStreamDestroy(hook_stream);
+        for (cudaEvent_t e : {hook_ev_x, hook_ev_done})
+            if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : wall_ev) cudaEventDestroy(e);
     }
 };
 
@@ -696,6 +715,21 @@ Workspace& workspace(Projector& P, size_t hist_cap, size_t obj_cap) {
     ensure(w, w.ctl, 1);
     ensure(w, w.scal, 8);
     if (P.slab_mode()) ensure(w, w.gath, (size_t)2 * P.slab_world);
+    if (P.comm_fn) ensure(w, w.red, (size_t)kSlots);
+    if (P.hook_fn && !w.hook_dev) {
+        ensure(w, w.hook_dev, w.m);
+        ensure(w, w.hook_stop_dev, 1);
+        KCT_CUDA(cudaMallocHost(&w.hook_host, w.m * sizeof(float)));
+        KCT_CUDA(cudaMallocHost(&w.hook_stop, sizeof(int)));
+        KCT_CUDA(cudaStreamCreateWithFlags(&w.hook_stream, cudaStreamNonBlocking));
+        KCT_CUDA(cudaEventCreateWithFlags(&w.hook_ev_x, cudaEventDisableTiming));
+        KCT_CUDA(cudaEventCreateWithFlags(&w.hook_ev_done, cudaEventDisableTiming));
+    }
+    while (w.wall_ev.size() < hist_cap + 1) {
+        cudaEvent_t e;
+        KCT_CUDA(cudaEventCreate(&e));
+        w.wall_ev.push_back(e);
+    }
     if (w.cap < hist_cap) {
         cudaFree(w.hist);
         w.hist = nullptr;
@@ -744,17 +778,50 @@ __global__ void k_set_nonzero(Ctl* ctl, const double* part) {
     if (threadIdx.x == 0) ctl->x_nonzero = t > 0.0 ? 1 : 0;
 }
 
-// Fold the block partials of one slot into element 0 (fixed order), so a
-// single double carries the slot to a cross-rank all-reduce.
-__global__ void k_fold(double* part, int slot) {
+// Fold the block partials of each listed slot (fixed order) into red[idx],
+// so one all-reduce of `count` doubles carries every slot of a phase across
+// the ranks; k_unpack writes the sums back as the slots' only partials.
+struct SlotList {
+    int n;
+    int slot[kSlots];
+};
+
+__global__ void k_fold(double* part, SlotList sl, double* red) {
     __shared__ double sm[32];
-    double t = 0.0;
-    for (int b = threadIdx.x; b < kGrid; b += blockDim.x) t += part[slot * kGrid + b];
-    t = block_sum(t, sm);
-    __syncthreads();
-    for (int b = threadIdx.x; b < kGrid; b += blockDim.x) part[slot * kGrid + b] = 0.0;
-    __syncthreads();
-    if (threadIdx.x == 0) part[slot * kGrid] = t;
+    for (int q = 0; q < sl.n; ++q) {
+        double* row = part + sl.slot[q] * kGrid;
+        double t = 0.0;
+        for (int b = threadIdx.x; b < kGrid; b += blockDim.x) t += row[b];
+        t = block_sum(t, sm);
+        __syncthreads();
+        if (threadIdx.x == 0) red[q] = t;
+    }
+}
+
+__global__ void k_unpack(double* part, SlotList sl, const double* red) {
+    for (int q = 0; q < sl.n; ++q) {
+        double* row = part + sl.slot[q] * kGrid;
+        for (int b = threadIdx.x; b < kGrid; b += blockDim.x) row[b] = b == 0 ? red[q] : 0.0;
+    }
+}
+
+// Host trampoline of the per-iteration hook (cudaLaunchHostFunc on the side stream).
+// The iteration number counts the calls actually made (the reference's
+// global_iter, recon.hpp:223-228): an iteration of a stopped CGLS (breakdown,
+// tolerance reached) changes nothing and, as in the reference, has no call.
+struct HookCall {
+    kct_iterate_hook fn;
+    void* ctx;
+    size_t* counter;
+    const int* stopped;
+    const float* x;
+    size_t m;
+};
+
+void CUDART_CB hook_trampoline(void* arg) {
+    const HookCall* c = static_cast<const HookCall*>(arg);
+    if (*c->stopped) return;
+    c->fn(c->ctx, ++*c->counter, c->x, c->m);
 }
 
 struct Engine {
@@ -774,17 +841,31 @@ struct Engine {
     //    planes; sum the partial forward projections and the volume-domain
     //    reductions, exchange halos after every update of a stencil operand.
     bool slab() const { return P.slab_mode(); }
+    // the reference's control flow at every CGLS start (kct_set_option "solver_restart")
+    bool restart = false;
+    // per-iteration hook state (P.hook_fn): 1-based global iteration counter
+    size_t hook_iter = 0;
+    std::deque<HookCall>* hook_calls = nullptr;  // stable addresses for the host callbacks
+    // wall_times: events recorded so far (index 0 = solve start)
+    size_t n_wall = 0;
+    // scalar all-reduces issued (evidence for the per-iteration collective count)
+    size_t n_scalar_reduce = 0;
+
     void allreduce(void* buf, size_t count, int dtype, const char* what) {
         if (P.comm_fn(P.comm_ctx, buf, count, dtype, stream) != 0)
             throw CudaError(std::string("allreduce hook failed (") + what + ")");
     }
+    // one all-reduce of all listed slots (fixed order)
     void reduce_slots(std::initializer_list<int> slots) {
-        if (!P.comm_fn) return;
-        for (int slot : slots) {
-            k_fold<<<1, kBlock, 0, stream>>>(w.part, slot);
-            KCT_LAUNCHED();
-            allreduce(w.part + slot * kGrid, 1, 1, "scalar");
-        }
+        if (!P.comm_fn || slots.size() == 0) return;
+        SlotList sl{};
+        for (int slot : slots) sl.slot[sl.n++] = slot;
+        k_fold<<<1, kBlock, 0, stream>>>(w.part, sl, w.red);
+        KCT_LAUNCHED();
+        allreduce(w.red, (size_t)sl.n, 1, "scalars");
+        ++n_scalar_reduce;
+        k_unpack<<<1, kBlock, 0, stream>>>(w.part, sl, w.red);
+        KCT_LAUNCHED();
     }
     void proj_slots(std::initializer_list<int> slots) { if (!slab()) reduce_slots(slots); }
     void vol_slots(std::initializer_list<int> slots) { if (slab()) reduce_slots(slots); }
@@ -824,7 +905,7 @@ struct Engine {
     void objective(bool x_is_zero, int idx) {
         if (x_is_zero) {
             KCT_LAUNCH(k_resid, w.b, nullptr, nullptr, w.n, w.part, 0);
-        } else if (r_current) {
+        } else if (r_current && !restart) {
             KCT_LAUNCH(k_stats, w.r, w.n, w.part);  // ||r||^2, r = b - A x (CGLS recurrence)
         } else {
             forward(w.x, w.q);
@@ -856,7 +937,7 @@ struct Engine {
         // cycles only in the regulariser blocks, whose residual parts are
         // evaluated from x anyway (section 4 of DESIGN.md) — one forward and one
         // adjoint projection less per cycle.
-        const bool reuse = r_current && !x_is_zero;
+        const bool reuse = r_current && !x_is_zero && !restart;
         if (x_is_zero) {
             KCT_LAUNCH(k_resid, w.b, nullptr, w.r, w.n, w.part, 0);
         } else if (reuse) {
@@ -885,10 +966,12 @@ struct Engine {
     }
 
     // out <- in - regulariser gradient (in == out allowed), norms into slots 0..2
-    void reggrad(const float* in, float* out, const float* xv) {
+    // (with_err: slot 5 of the preceding k_update_xr joins the same all-reduce)
+    void reggrad(const float* in, float* out, const float* xv, bool with_err = false) {
         if (use4()) KCT_LAUNCH(k_reggrad4, in, xv, w.prior, w.w1, w.w2, out, rc, w.part);
         else KCT_LAUNCH(k_reggrad, in, xv, w.prior, w.w1, w.w2, out, rc, w.part);
-        vol_slots({0, 1, 2});
+        if (with_err) vol_slots({0, 1, 2, 5});
+        else vol_slots({0, 1, 2});
     }
 
     // One CGLS iteration (krylov.hpp:98-125).
@@ -902,13 +985,56 @@ struct Engine {
         KCT_LAUNCH(k_update_xr, w.x, w.p, w.m, w.r, w.q, w.n, with_gt ? w.gt : nullptr, w.ctl,
                    w.part);
         proj_slots({4});
-        vol_slots({5});
         halo(w.x);
+        hook_copy();
         adjoint(w.r, w.atr);
-        reggrad(w.atr, w.s, w.x);
+        reggrad(w.atr, w.s, w.x, with_gt);  // + slot 5 (||x - gt||^2) in slab mode
         launch_scalar(w, S_GAMMA, stream, 0.0, res, err);
         KCT_LAUNCH(k_update_p, w.p, w.s, w.m, w.ctl, 0);
         halo(w.p);
+        if (n_wall < w.wall_ev.size()) KCT_CUDA(cudaEventRecord(w.wall_ev[n_wall++], stream));
+    }
+
+    // solve start on the device timeline (wall_times reference point)
+    void mark_start() {
+        n_wall = 0;
+        KCT_CUDA(cudaEventRecord(w.wall_ev[n_wall++], stream));
+    }
+    // seconds since the start event of the iterations recorded (synchronises)
+    size_t wall_times(double* out) {
+        if (n_wall < 2) return 0;
+        KCT_CUDA(cudaEventSynchronize(w.wall_ev[n_wall - 1]));
+        for (size_t i = 1; i < n_wall; ++i) {
+            float ms = 0.f;
+            KCT_CUDA(cudaEventElapsedTime(&ms, w.wall_ev[0], w.wall_ev[i]));
+            if (out) out[i - 1] = 1e-3 * ms;
+        }
+        return n_wall - 1;
+    }
+
+    // IterateHook (krylov.hpp:116): x (reference layout) -> pinned host on the
+    // side stream, then the caller's callback; the main stream only waits
+    // for the previous iteration's copy before it overwrites the device copy.
+    // A stopped solve (tolerance / breakdown) skips the call, as the
+    // reference's loop exits before its hook.
+    void hook_copy() {
+        if (!P.hook_fn || !hook_calls) return;
+        KCT_CUDA(cudaStreamWaitEvent(stream, w.hook_ev_done, 0));
+        P.vol_from_native(w.x, w.hook_dev, stream);
+        KCT_CUDA(cudaMemcpyAsync(w.hook_stop_dev, &w.ctl->stop, sizeof(int),
+                                 cudaMemcpyDeviceToDevice, stream));
+        KCT_CUDA(cudaEventRecord(w.hook_ev_x, stream));
+        KCT_CUDA(cudaStreamWaitEvent(w.hook_stream, w.hook_ev_x, 0));
+        KCT_CUDA(cudaMemcpyAsync(w.hook_host, w.hook_dev, w.m * sizeof(float),
+                                 cudaMemcpyDeviceToHost, w.hook_stream));
+        KCT_CUDA(cudaMemcpyAsync(w.hook_stop, w.hook_stop_dev, sizeof(int),
+                                 cudaMemcpyDeviceToHost, w.hook_stream));
+        KCT_CUDA(cudaEventRecord(w.hook_ev_done, w.hook_stream));
+        hook_calls->push_back(HookCall{P.hook_fn, P.hook_ctx, &hook_iter, w.hook_stop, w.hook_host, w.m});
+        KCT_CUDA(cudaLaunchHostFunc(w.hook_stream, hook_trampoline, &hook_calls->back()));
+    }
+    void hook_drain() {
+        if (w.hook_stream) KCT_CUDA(cudaStreamSynchronize(w.hook_stream));
     }
 
     void ground_truth_norm() {
@@ -997,9 +1123,27 @@ void copy_hist(double* dst, const double* src, size_t n, cudaStream_t s) {
 void reset_report(kct_report* rep) {
     if (!rep) return;
     rep->objective_count = rep->residual_count = rep->error_count = rep->outer_count = 0;
+    rep->wall_count = 0;
     rep->solve_seconds = 0.0;
     rep->tau = 0.0;
     rep->converged = rep->breakdown = 0;
+}
+
+// Drains the hook stream when a solve ends (normally or by exception), so
+// no host callback outlives the call list it points into.
+struct HookScope {
+    Engine& e;
+    std::deque<HookCall> calls;
+    explicit HookScope(Engine& en) : e(en) { e.hook_calls = &calls; }
+    ~HookScope() {
+        if (e.w.hook_stream) cudaStreamSynchronize(e.w.hook_stream);
+        e.hook_calls = nullptr;
+    }
+};
+
+void write_wall(Engine& e, kct_report* rep) {
+    if (!rep) return;
+    rep->wall_count = e.wall_times(rep->wall_times);
 }
 
 }  // namespace
@@ -1032,16 +1176,20 @@ void cgls_recon(Projector& P, const float* b, size_t iters, const float* x0, con
     if (gt) load(P, w.gt, gt, w.m, true, mem, layout, stream);
     init_ctl(w, 0.0, 0.0, stream);
     Engine e{P, w, stream};
+    e.restart = P.solver_restart;
     set_grid(e.rc, P);
     e.halo(w.x);
     if (gt) e.ground_truth_norm();
     KCT_CUDA(cudaStreamSynchronize(stream));
 
+    HookScope hooks(e);
     const double t0 = now_s();
+    e.mark_start();
     e.start(x0 == nullptr, tol, -1);
     for (size_t it = 0; it < iters; ++it) e.iterate(w.hist, w.hist + w.cap, gt != nullptr);
     const Ctl c = read_ctl(w, stream);
     const double secs = now_s() - t0;
+    e.hook_drain();
     throw_solver(c);
     stage_out(P, w.x, x_out, w.m, true, mem, layout, 2, stream);
     if (rep) {
@@ -1061,6 +1209,8 @@ void cgls_recon(Projector& P, const float* b, size_t iters, const float* x0, con
         rep->solve_seconds = secs;
         rep->converged = c.converged;
         rep->breakdown = c.breakdown;
+        write_wall(e, rep);
+        if (rep->wall_count > n) rep->wall_count = n;
     }
     KCT_CUDA(cudaStreamSynchronize(stream));
 }
@@ -1102,6 +1252,7 @@ void irn_solve(Projector& P, int kind, const float* b, const float* prior, const
 
     Engine e{P, w, stream};
     e.kind = kind;
+    e.restart = P.solver_restart;
     set_grid(e.rc, P);
     e.halo(w.x);
     if (use_prior) e.halo(w.prior);
@@ -1119,7 +1270,10 @@ void irn_solve(Projector& P, int kind, const float* b, const float* prior, const
     size_t n_res = 0;
     bool x_zero = x0 == nullptr;
     int converged = 0, breakdown = 0;
+    HookScope hooks(e);
     const double t_start = now_s();
+    e.mark_start();
+    std::vector<size_t> wall_keep;  // event indices of the iterations that ran
     for (size_t cycle = 0; cycle < outer; ++cycle) {
         const double t_cycle = now_s();
         e.weights(true);
@@ -1140,7 +1294,9 @@ void irn_solve(Projector& P, int kind, const float* b, const float* prior, const
             e.objective(false, (int)cycle + 1);
         }
         const Ctl c = read_ctl(w, stream);
+        e.hook_drain();
         throw_solver(c);
+        for (size_t i = 0; i < (size_t)c.iters; ++i) wall_keep.push_back(e.n_wall - inner + i);
         n_res += (size_t)c.iters;
         converged = c.converged;
         breakdown = c.breakdown;
@@ -1170,6 +1326,15 @@ void irn_solve(Projector& P, int kind, const float* b, const float* prior, const
         rep->tau = tau;
         rep->converged = converged;
         rep->breakdown = breakdown;
+        // wall_times of the iterations that ran (a cycle stopped early keeps its first c.iters)
+        std::vector<double> all(e.n_wall > 0 ? e.n_wall - 1 : 0);
+        e.wall_times(all.data());
+        rep->wall_count = 0;
+        for (size_t idx : wall_keep)
+            if (idx >= 1 && idx - 1 < all.size()) {
+                if (rep->wall_times) rep->wall_times[rep->wall_count] = all[idx - 1];
+                ++rep->wall_count;
+            }
     }
     KCT_CUDA(cudaStreamSynchronize(stream));
 }

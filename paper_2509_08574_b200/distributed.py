@@ -44,11 +44,13 @@ class _DeviceBuffer:
 
 def _on_stream(stream, device):
     """Context making the library's CUDA stream (a raw handle; None / 0: the
-    legacy default stream) torch's current stream for a hook's collectives."""
-    import contextlib
+    legacy default stream, which is torch's default stream) torch's current
+    stream for a hook's collectives, so they are ordered after the kernels that
+    produced the buffer and before the library's next kernels, whatever stream
+    the caller has made current."""
     import torch
     if not stream:
-        return contextlib.nullcontext()
+        return torch.cuda.stream(torch.cuda.default_stream(device))
     return torch.cuda.stream(torch.cuda.ExternalStream(stream, device=device))
 
 
@@ -121,8 +123,8 @@ def cgls_recon_sharded(proj_local, grid, iters, opts=None, tolerance=0.0, group=
 def install_slab(projector: ConeBeamProjector, rank: int, world: int, j0: int, ny_global: int,
                  group=None) -> None:
     """Put `projector` (built on this rank's y-slab grid) in slab mode: the
-    all-reduce hook plus a halo exchange of boundary y planes (all_gather of
-    the two boundary planes of every rank; CPU staging under gloo)."""
+    all-reduce hook plus a neighbour exchange of boundary y planes (P2P
+    send / recv with ranks r - 1 and r + 1; CPU staging under gloo)."""
     import torch
     import torch.distributed as dist
     install_allreduce(projector, group)
@@ -137,19 +139,33 @@ def install_slab(projector: ConeBeamProjector, rank: int, world: int, j0: int, n
         except Exception:  # surfaced as KCT_ERR_CUDA by the library
             return 1
 
+    def peer(r):  # group rank -> global rank (P2P ops address global ranks)
+        return r if group is None else dist.get_global_rank(group, r)
+
     def _halo(lo_plane, hi_plane, lo_halo, hi_halo, count):
+        """Neighbour exchange: send the first / last interior plane to rank - 1 /
+        rank + 1 and receive theirs into the halos (P2P, O(1) traffic per rank)."""
         try:
-            lo = torch.as_tensor(_DeviceBuffer(lo_plane, count, 0), device=device)
-            hi = torch.as_tensor(_DeviceBuffer(hi_plane, count, 0), device=device)
-            send = torch.stack([lo, hi])
-            if cpu:
-                send = send.cpu()
-            got = [torch.empty_like(send) for _ in range(world)]
-            dist.all_gather(got, send, group=group)
-            if rank > 0:
-                torch.as_tensor(_DeviceBuffer(lo_halo, count, 0), device=device).copy_(got[rank - 1][1])
-            if rank + 1 < world:
-                torch.as_tensor(_DeviceBuffer(hi_halo, count, 0), device=device).copy_(got[rank + 1][0])
+            ops, recv = [], []
+            buf = lambda p: torch.as_tensor(_DeviceBuffer(p, count, 0), device=device)  # noqa: E731
+            for nb, plane, halo in ((rank - 1, lo_plane, lo_halo), (rank + 1, hi_plane, hi_halo)):
+                if not 0 <= nb < world:
+                    continue
+                send = buf(plane)
+                dst = buf(halo)
+                if cpu:
+                    send, tmp = send.cpu(), torch.empty(count, dtype=torch.float32)
+                else:
+                    tmp = dst
+                ops.append(dist.P2POp(dist.isend, send, peer(nb), group))
+                ops.append(dist.P2POp(dist.irecv, tmp, peer(nb), group))
+                recv.append((dst, tmp))
+            if ops:
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+            for dst, tmp in recv:
+                if tmp is not dst:
+                    dst.copy_(tmp)
             return 0
         except Exception:  # surfaced as KCT_ERR_CUDA by the library
             return 1

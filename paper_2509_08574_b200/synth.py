@@ -160,3 +160,44 @@ def study(cfg_name: str, seed: int | None = None, followup_step: int = 0):
         grown[0, 1:4] *= 1.15
         follow = render(cfg, grown)
     return cfg, prior, follow
+
+
+def noise_seed(cfg_name: str, followup_step: int = 0) -> int:
+    """Poisson seed of a follow-up scan: 1000 + config id (+ 10 * step for c5)."""
+    return 1000 + int(cfg_name[1]) + 10 * followup_step
+
+
+def scan_inputs(cfg_name: str, followup_step: int = 0, prior_iters: int = 20, device: int = 0,
+                n_followup_views: int | None = None):
+    """The inputs of a BASELINE config's follow-up solve, made on the GPU.
+
+    * prior image: ``prior_iters``-iteration CGLS (``cgls_recon``) of a
+      noiseless ``prior_views`` scan of the prior phantom (SURVEY §8d pins);
+    * follow-up readings b: forward projection of the follow-up phantom at
+      ``followup_views`` (or ``n_followup_views``) angles, Poisson noise at the
+      config's I0, seed ``noise_seed``.
+    Returns a dict of host float32 arrays in the reference layouts (x-fastest
+    volumes, u-fastest projections) plus the package grid / geometries, so the
+    identical values can be fed to the GPU solver and to the CPU reference."""
+    import torch
+    from . import ConeBeamGeometry, ConeBeamProjector, GridSpec, ProjectionSet, cgls_recon
+    cfg = CONFIGS[cfg_name]
+    dev = torch.device("cuda", device)
+    grid = GridSpec((cfg.n,) * 3, (cfg.voxel,) * 3)
+    nf = n_followup_views or cfg.followup_views
+    geom_p = ConeBeamGeometry(DSO, DSD, cfg.det, cfg.det, cfg.pitch, cfg.pitch,
+                              angles(cfg.prior_views))
+    geom_f = ConeBeamGeometry(DSO, DSD, cfg.det, cfg.det, cfg.pitch, cfg.pitch, angles(nf))
+    _, prior, follow = study(cfg_name, followup_step=followup_step)
+    Ap = ConeBeamProjector(grid, geom_p, device=device)
+    xp = Ap.volume_to_native(torch.from_numpy(prior).to(dev))
+    prior_rec = cgls_recon(ProjectionSet(geom_p, Ap.apply(xp)), grid, prior_iters, projector=Ap)
+    prior_rec = Ap.volume_from_native(prior_rec.volume).cpu().numpy()
+    del Ap, xp
+    Af = ConeBeamProjector(grid, geom_f, device=device)
+    xf = Af.volume_to_native(torch.from_numpy(follow).to(dev))
+    pf = Af.proj_from_native(Af.apply(xf)).cpu().numpy()
+    b = poisson_log(pf, cfg.i0, seed=noise_seed(cfg_name, followup_step))
+    torch.cuda.synchronize(dev)
+    return dict(cfg=cfg, grid=grid, geom=geom_f, projector=Af, prior_phantom=prior,
+                follow=follow, prior=prior_rec.astype(np.float32), b=b)

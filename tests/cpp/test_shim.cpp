@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <numbers>
 #include <random>
+#include <stdexcept>
 
 #include "kryct_b200.hpp"
 
@@ -82,6 +83,47 @@ int main() {
     const auto c_gpu = kryct_b200::cgls_recon(proj, grid, 8);
     expect(rel(c_gpu.volume.data, c_ref.volume.data) < 1e-3, "kryct_b200::cgls_recon vs cgls_recon",
            rel(c_gpu.volume.data, c_ref.volume.data));
+
+    // ReconOptions::hook: every inner iterate, in order, numbered across the
+    // outer cycles (recon.hpp:223-228; the reference's test_krylov.cpp:120-135)
+    {
+        std::vector<std::size_t> seen_ref, seen_gpu;
+        std::vector<std::vector<double>> it_ref, it_gpu;
+        ReconOptions o_ref, o_gpu;
+        o_ref.hook = [&](std::size_t it, std::span<const double> xi) {
+            seen_ref.push_back(it);
+            it_ref.emplace_back(xi.begin(), xi.end());
+        };
+        o_gpu.hook = [&](std::size_t it, std::span<const double> xi) {
+            seen_gpu.push_back(it);
+            it_gpu.emplace_back(xi.begin(), xi.end());
+        };
+        irn_piccs(proj, grid, prior, p, o_ref);
+        const auto h_gpu = kryct_b200::irn_piccs(proj, grid, prior, p, o_gpu);
+        bool order = seen_gpu == seen_ref && seen_gpu.size() == 8;
+        for (std::size_t i = 0; i < seen_gpu.size(); ++i) order = order && seen_gpu[i] == i + 1;
+        expect(order, "hook: iterations 1..8 in order, as the reference", (double)seen_gpu.size());
+        double worst = 0.0;
+        for (std::size_t i = 0; i < it_gpu.size() && i < it_ref.size(); ++i)
+            worst = std::max(worst, rel(it_gpu[i], it_ref[i]));
+        expect(worst < 1e-3 && it_gpu.size() == it_ref.size(), "hook: iterates vs reference", worst);
+        expect(it_gpu.back() == h_gpu.volume.data, "hook: last iterate == result volume", 0.0);
+        // cached handle: a repeated call is bit-identical
+        const auto again = kryct_b200::irn_piccs(proj, grid, prior, p);
+        expect(again.volume.data == h_gpu.volume.data, "cached handle: repeated call bitwise", 0.0);
+        // a throwing hook surfaces after the solve
+        ReconOptions o_bad;
+        o_bad.hook = [](std::size_t it, std::span<const double>) {
+            if (it == 2) throw std::runtime_error("hook failure");
+        };
+        bool hook_threw = false;
+        try {
+            kryct_b200::cgls_recon(proj, grid, 4, o_bad);
+        } catch (const std::runtime_error&) {
+            hook_threw = true;
+        }
+        expect(hook_threw, "hook exception propagates to the caller", 0.0);
+    }
 
     // error taxonomy (test_projector.cpp:113-120)
     bool threw = false;

@@ -166,3 +166,62 @@ def test_y_slab_auto_tau_and_float4_stencils(nz):
     for _, _, obj, res, err, tau in outs:
         assert tau == pytest.approx(ref.tau, rel=1e-12)
         np.testing.assert_allclose(obj, ref.objective_history, rtol=1e-5)
+
+
+# ---- collectives per CGLS iteration (two scalar all-reduces) -------
+def _rank_count(rank, world, port, q, mode):
+    import torch.distributed as dist
+    from paper_2509_08574_b200 import distributed
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    calls = {"scalar": 0, "vector": 0, "p2p": 0}
+    real_ar, real_p2p = dist.all_reduce, dist.batch_isend_irecv
+
+    def counting_ar(t, *a, **kw):
+        calls["scalar" if t.dtype == torch.float64 and t.numel() <= 8 else "vector"] += 1
+        return real_ar(t, *a, **kw)
+
+    def counting_p2p(ops):
+        calls["p2p"] += 1
+        return real_p2p(ops)
+    dist.all_reduce, dist.batch_isend_irecv = counting_ar, counting_p2p
+    gs, ge, prior, b = _problem()
+    proj = k.ProjectionSet(ge, b)
+    res = []
+    for inner in (2, 5):
+        for key in calls:
+            calls[key] = 0
+        params = k.RegularizationParams(alpha=0.3, outer_iters=1, inner_iters=inner, tau=1e-3)
+        if mode == "slab":
+            distributed.irn_piccs_slab(proj, gs, prior, params)
+        else:
+            local = distributed.shard_projections(proj, world, rank)
+            distributed.irn_piccs_sharded(local, gs, prior, params)
+        res.append(dict(calls))
+    q.put((rank, res))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["slab", "angles"])
+def test_collectives_per_iteration(mode):
+    """Per CGLS iteration: 2 packed fp64 scalar all-reduces (||A p||^2 and the
+    regulariser norms; ||s||^2, ||r||^2 and the error norm), 1 vector
+    all-reduce (slab: partial projections; angles: the partial A^T volume) and,
+    in slab mode, 2 neighbour halo exchanges (x and p)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    ps = [ctx.Process(target=_rank_count, args=(r, 2, port, q, mode)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = [q.get() for _ in range(2)]
+    for p in ps:
+        p.join(300)
+        assert p.exitcode == 0
+    for _, (c2, c5) in out:
+        per = {key: (c5[key] - c2[key]) / 3 for key in c2}
+        assert per["scalar"] == 2, per
+        assert per["vector"] == 1, per
+        assert per["p2p"] == (2 if mode == "slab" else 0), per

@@ -224,3 +224,105 @@ def test_float4_and_scalar_stencils_agree(monkeypatch, fn):
     assert rel_l2(vec.volume, sca.volume) < 1e-5
     np.testing.assert_allclose(vec.objective_history, sca.objective_history, rtol=1e-6)
     np.testing.assert_allclose(vec.residual_history, sca.residual_history, rtol=1e-6)
+
+
+# ---- ReconOptions.hook / wall_times / the reference's restart control flow ----
+def test_hook_sees_every_iterate_in_order(small):
+    """krylov.hpp:116 / recon.hpp:223-228 (test_krylov.cpp:120-135): the hook is
+    called once per inner iteration, 1-based across outer cycles, with the
+    iterate in the reference layout; the last one is the returned volume and
+    the error history recomputed from the hooked iterates matches the
+    device-computed one."""
+    d, gs, ge, A = small
+    seen, xs = [], []
+    opts = k.ReconOptions(ground_truth=d["truth"], hook=lambda it, x: (seen.append(it), xs.append(x)))
+    params = k.RegularizationParams(alpha=0.3, tau=1e-3, outer_iters=3, inner_iters=4)
+    rep = k.irn_piccs(k.ProjectionSet(ge, d["b"]), gs, d["prior"], params, opts, projector=A)
+    assert seen == list(range(1, 13))
+    assert all(x.dtype == np.float32 and x.size == gs.count() for x in xs)
+    np.testing.assert_array_equal(xs[-1], rep.volume)
+    truth = d["truth"].astype(np.float64)
+    err = [np.linalg.norm(x - truth) / np.linalg.norm(truth) for x in xs]
+    np.testing.assert_allclose(err, rep.error_history, rtol=1e-5)
+    # the hook does not change the solve
+    plain = k.irn_piccs(k.ProjectionSet(ge, d["b"]), gs, d["prior"], params,
+                        k.ReconOptions(ground_truth=d["truth"]), projector=A)
+    np.testing.assert_array_equal(plain.volume, rep.volume)
+    # cgls_recon: iterations 1..n (baseline_solve's hook, recon.hpp:291-295)
+    seen.clear()
+    k.cgls_recon(k.ProjectionSet(ge, d["b"]), gs, 5, k.ReconOptions(hook=lambda it, x: seen.append(it)),
+                 projector=A)
+    assert seen == [1, 2, 3, 4, 5]
+
+
+def test_hook_stops_with_the_solver():
+    """A CGLS that reaches its tolerance stops calling the hook (krylov.hpp:118-121)."""
+    gs, ge, A, truth, b = _sphere_problem()
+    seen = []
+    rep = k.cgls_recon(k.ProjectionSet(ge, b), gs, 200,
+                       k.ReconOptions(hook=lambda it, x: seen.append(it)), tolerance=1e-2,
+                       projector=A)
+    assert rep.converged
+    assert seen == list(range(1, len(rep.residual_history) + 1))
+    assert len(seen) < 200
+
+
+def test_hook_exception_propagates(small):
+    d, gs, ge, A = small
+
+    def bad(it, x):
+        if it == 2:
+            raise KeyError("boom")
+    with pytest.raises(KeyError):
+        k.cgls_recon(k.ProjectionSet(ge, d["b"]), gs, 4, k.ReconOptions(hook=bad), projector=A)
+    # the handle is usable afterwards, without the hook
+    rep = k.cgls_recon(k.ProjectionSet(ge, d["b"]), gs, 8, projector=A)
+    assert rel_l2(rep.volume, d["cgls_x"]) < RTOL
+
+
+def test_wall_times(small):
+    """SolveTrace.wall_times (krylov.hpp:40, :115): one per iteration, increasing."""
+    d, gs, ge, A = small
+    rep = k.irn_tv(k.ProjectionSet(ge, d["b"]), gs,
+                   k.RegularizationParams(alpha=0.3, tau=1e-3, outer_iters=3, inner_iters=4),
+                   projector=A)
+    w = rep.wall_times
+    assert w.size == rep.residual_history.size == 12
+    assert np.all(np.diff(w) > 0) and w[0] > 0
+    assert w[-1] <= rep.solve_seconds
+    rep = k.cgls_recon(k.ProjectionSet(ge, d["b"]), gs, 6, projector=A)
+    assert rep.wall_times.size == 6 and np.all(np.diff(rep.wall_times) > 0)
+
+
+@pytest.mark.parametrize("tag", ["tv", "piple", "piccs"])
+def test_restart_control_flow_golden(small, tag):
+    """solver_restart = 1 runs the reference's flow (fresh r = b - A x and A^T r
+    at every CGLS start, krylov.hpp:68-75; fresh A x for the objectives): same
+    golden iterates and histories as the reference at the same bar."""
+    d, gs, ge, A = small
+    params = k.RegularizationParams(alpha=0.3, tau=1e-3, outer_iters=3, inner_iters=4)
+    opts = k.ReconOptions(ground_truth=d["truth"])
+    proj = k.ProjectionSet(ge, d["b"])
+    A.set_option("solver_restart", 1)
+    try:
+        assert A.info("solver_restart") == 1
+        if tag == "tv":
+            rep = k.irn_tv(proj, gs, params, opts, projector=A)
+        else:
+            rep = getattr(k, f"irn_{tag}")(proj, gs, d["prior"], params, opts, projector=A)
+    finally:
+        A.set_option("solver_restart", 0)
+    assert rel_l2(rep.volume, d[f"{tag}_x"]) < RTOL
+    np.testing.assert_allclose(rep.objective_history, d[f"{tag}_obj"], rtol=RTOL)
+    np.testing.assert_allclose(rep.residual_history, d[f"{tag}_res"], rtol=RTOL)
+    np.testing.assert_allclose(rep.error_history, d[f"{tag}_err"], rtol=RTOL)
+
+
+def test_restart_env_default(monkeypatch):
+    monkeypatch.setenv("KCT_SOLVER_RESTART", "1")
+    gs, ge, A, truth, b = _sphere_problem(6, 4)
+    assert A.info("solver_restart") == 1
+    with pytest.raises(k.ConfigError):
+        A.set_option("solver_restart", 2)
+    with pytest.raises(k.ConfigError):
+        A.set_option("no_such_option", 1)
