@@ -119,30 +119,58 @@ def dist_env():
 # ---------------------------------------------------------------------------
 # reference arm: the reference's own CPU code (oracle/_ref) on host cores
 # ---------------------------------------------------------------------------
-def cpu_reference_gups(n_angles_sample: int, repeats: int, warmup: int = 1, threads: int = 0):
-    """fwd+adj GUPS of the unmodified reference (oracle/_ref) on a c3 angle sample."""
+def _ref_oracle(threads: int = 0):
+    """The unmodified reference compiled in place (oracle/_ref), else the C port."""
     import oracle
-    from oracle import Geometry, Grid, Oracle
+    from oracle import Oracle
     if not os.path.exists(oracle.LIBS["ref"][0]):
         try:
             oracle.build("ref")
         except Exception:
             pass
     kind = "reference" if os.path.exists(oracle.LIBS["ref"][0]) else "port"
-    o = Oracle("ref" if kind == "reference" else "ora")
     if kind == "port":
         oracle.build("ora")
+    o = Oracle("ref" if kind == "reference" else "ora")
     nthreads = threads or os.cpu_count() or 1
     o.set_threads(nthreads)
+    return o, kind, nthreads
+
+
+def host_info() -> dict:
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model or "unknown"}
+
+
+def _c3_ora(n_views: int):
+    from oracle import Geometry, Grid
     from paper_2509_08574_b200 import synth
     cfg = synth.CONFIGS["c3"]
-    sel = synth.angles(cfg.followup_views)[:: max(1, cfg.followup_views // n_angles_sample)][:n_angles_sample]
+    sel = synth.angles(cfg.followup_views)
+    if n_views < cfg.followup_views:
+        sel = sel[:: max(1, cfg.followup_views // n_views)][:n_views]
     grid = Grid(cfg.n, cfg.n, cfg.n, cfg.voxel, cfg.voxel, cfg.voxel)
     geom = Geometry(synth.DSO, synth.DSD, cfg.det, cfg.det, cfg.pitch, cfg.pitch, sel)
+    return cfg, grid, geom
+
+
+def cpu_reference_gups(n_views: int, repeats: int, warmup: int = 1, threads: int = 0):
+    """fwd+adj GUPS of the unmodified reference (oracle/_ref) on the c3 geometry
+    (all 60 views, or an evenly spaced sample of n_views)."""
+    from paper_2509_08574_b200 import synth
+    o, kind, nthreads = _ref_oracle(threads)
+    cfg, grid, geom = _c3_ora(n_views)
     _, prior, _ = synth.study("c3")
     x = prior.astype(np.float64)
     times = []
-    y = None
     for r in range(warmup + repeats):
         t0 = time.perf_counter()
         y = o.forward(grid, geom, x)
@@ -151,11 +179,55 @@ def cpu_reference_gups(n_angles_sample: int, repeats: int, warmup: int = 1, thre
         if r >= warmup:
             times.append(dt)
     m = cfg.n ** 3
-    gups = [2.0 * m * len(sel) / t / 1e9 for t in times]
-    return {"value": float(np.median(gups)), "unit": "GUPS", "cores": nthreads, "kind": kind,
-            "sample": f"c3 256^3/384^2, {len(sel)} of {cfg.followup_views} views, fwd+adj, "
-                      f"float64, median of {repeats} after {warmup} warm-up",
-            "seconds_per_step": float(np.median(times)), "all_gups": gups}
+    nv = geom.n_angles
+    total = sum(times)
+    return {"value": 2.0 * m * nv * repeats / total / 1e9, "unit": "GUPS", "cores": nthreads,
+            "kind": kind, "views": nv,
+            "sample": f"c3 256^3/384^2, {nv} of {cfg.followup_views} views, A x + A^T y "
+                      f"(project_forward + project_adjoint, float64), {repeats} timed after "
+                      f"{warmup} warm-up",
+            "seconds_per_step": total / repeats, "all_seconds": [round(t, 3) for t in times]}
+
+
+def cpu_reference_recon(threads: int = 0) -> dict:
+    """ReconReport.solve_seconds (recon.hpp:243-244) of the reference's own
+    irn_piccs (recon.hpp:267-270) at c3: 4x5 iterations, alpha = lambda = 0.5,
+    tau auto; b = the reference's forward projection of the follow-up phantom
+    (60 views) with Poisson noise I0 = 5e4; prior = the prior phantom (the
+    solve's cost does not depend on the values; no GPU on this path)."""
+    from oracle import KIND_PICCS
+    from paper_2509_08574_b200 import synth
+    o, kind, nthreads = _ref_oracle(threads)
+    cfg, grid, geom = _c3_ora(60)
+    _, prior, follow = synth.study("c3")
+    b = synth.poisson_log(o.forward(grid, geom, follow.astype(np.float64)), cfg.i0,
+                          seed=synth.noise_seed("c3"))
+    t0 = time.perf_counter()
+    _, rep = o.irn(grid, geom, KIND_PICCS, b.astype(np.float64), prior.astype(np.float64),
+                   dict(alpha=cfg.alpha, outer_iters=cfg.outer, inner_iters=cfg.inner))
+    wall = time.perf_counter() - t0
+    return {"seconds_per_recon": round(rep["solve_seconds"], 3), "wall_seconds": round(wall, 3),
+            "outer_seconds": [round(v, 3) for v in rep["outer_seconds"]],
+            "iterations": cfg.outer * cfg.inner, "outer_x_inner": f"{cfg.outer}x{cfg.inner}",
+            "threads": nthreads, "kind": kind,
+            "what": "irn_piccs c3 (256^3, 384^2, 60 views), ReconReport.solve_seconds"}
+
+
+def cpu_reference_cgls_c1(threads: int) -> dict:
+    """ReconReport.solve_seconds of the reference's cgls_recon (recon.hpp:312-315),
+    BASELINE config 1: 64^3, 96^2, 64 views, 20 iterations from zero, noiseless."""
+    from oracle import Geometry, Grid
+    from paper_2509_08574_b200 import synth
+    o, kind, nthreads = _ref_oracle(threads)
+    cfg = synth.CONFIGS["c1"]
+    grid = Grid(cfg.n, cfg.n, cfg.n, cfg.voxel, cfg.voxel, cfg.voxel)
+    geom = Geometry(synth.DSO, synth.DSD, cfg.det, cfg.det, cfg.pitch, cfg.pitch,
+                    synth.angles(cfg.followup_views))
+    _, prior, _ = synth.study("c1")
+    b = o.forward(grid, geom, prior.astype(np.float64))
+    o.cgls_recon(grid, geom, b, 2)  # warm-up (first OpenMP call)
+    _, rep = o.cgls_recon(grid, geom, b, cfg.iters)
+    return {"seconds": round(rep["solve_seconds"], 3), "threads": nthreads, "kind": kind}
 
 
 def run_reference(args):
@@ -163,17 +235,26 @@ def run_reference(args):
     if rank != 0:
         return
     steps, warmup = args.steps, args.warmup
-    res = cpu_reference_gups(args.ref_angles, steps, warmup)
+    # the whole c3 scan per step (same workload as our arm) unless K is large:
+    # then an evenly spaced angle sample keeps the run within a few minutes
+    views = 60 if steps <= 20 else max(4, 60 * 20 // steps)
+    res = cpu_reference_gups(views, steps, warmup)
     value = res["value"]
     line = {"impl": "reference", "metric": M_TAG, "value": round(value, 5), "unit": "GUPS",
             "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
             "ms_per_step": round(1e3 * res["seconds_per_step"], 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "c3: 256^3 @0.5mm, 384^2 @0.5mm, 60 views (angle sample)",
-                       "sample_views": args.ref_angles},
+            "config": {"workload": "c3: A x + A^T y, 256^3 @0.5mm, 384^2 @0.5mm, 60 views, "
+                                   "DSO 1000 / DSD 1500",
+                       "views_per_step": res["views"], "same_config": res["views"] == 60},
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": round(value, 5), "unit": "GUPS", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "host": host_info(), "all_seconds": res["all_seconds"]}
+    if not args.skip_recon:
+        line["recon"] = cpu_reference_recon()
+        line["cgls_c1"] = {"all_threads": cpu_reference_cgls_c1(0),
+                           "one_thread": cpu_reference_cgls_c1(1)}
     print(json.dumps(line), flush=True)
 
 
@@ -367,8 +448,9 @@ def run_ours(args):
 
     if rank == 0 and not args.skip_cpu:
         try:
-            out["cpu_baseline"] = {kk: v for kk, v in cpu_reference_gups(args.ref_angles, 2).items()
+            out["cpu_baseline"] = {kk: v for kk, v in cpu_reference_gups(60, 2).items()
                                    if kk in ("value", "unit", "cores", "kind", "sample")}
+            out["cpu_baseline"]["host"] = host_info()
         except Exception as e:  # report, do not fail the bench
             out["cpu_baseline"] = {"value": None, "error": str(e)}
     if ws > 1:
@@ -485,7 +567,9 @@ def run_recon(k, synth, cfg, grid, prior, follow, dev, args, ws=1, rank=0, share
                             f"angle-sharded x{ws}: partial-volume + scalar all-reduces"
                             if ws > 1 else "single GPU"),
             "setup_seconds_untimed": round(setup, 2),
-            "reference_cpu_seconds_survey_box": 329.2}
+            "reference_cpu": "the --impl reference line's recon.seconds_per_recon (same box, "
+                             "all host cores); tests/test_config_parity_gpu.py measured 151.9 s "
+                             "on 16 threads (profiles/r02_config_parity.log)"}
 
 
 def main():
@@ -494,7 +578,6 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-angles", type=int, default=16)
     ap.add_argument("--recon-steps", type=int, default=3)
     ap.add_argument("--recon-warmup", type=int, default=1)
     ap.add_argument("--skip-recon", action="store_true")

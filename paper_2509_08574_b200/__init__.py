@@ -358,6 +358,35 @@ def _ptr(out):
     return out.data_ptr() if _is_torch(out) else out.ctypes.data
 
 
+def _check_out(out, like: "_Arg", n: int, name: str = "out"):
+    """A caller-supplied output buffer must be what the C ABI will write: n
+    contiguous float32 values in the same memory kind (and device) as the
+    input — the library writes through the raw pointer (the reference checks
+    the output span's size, linear_map.hpp:52-57)."""
+    if _is_torch(out):
+        import torch
+        if not out.is_cuda:
+            raise ConfigError(f"{name}: CPU tensors are not accepted as outputs (use numpy)")
+        if like.mem != MEM_DEVICE:
+            raise ConfigError(f"{name}: device output for host input")
+        if out.device != like.keep.device:
+            raise ConfigError(f"{name}: output on {out.device}, input on {like.keep.device}")
+        if out.dtype != torch.float32 or not out.is_contiguous():
+            raise ConfigError(f"{name}: must be a contiguous float32 tensor")
+        if out.numel() != n:
+            raise ConfigError(f"{name}: expected {n} values, got {out.numel()}")
+        return out
+    if not isinstance(out, np.ndarray):
+        raise ConfigError(f"{name}: expected a numpy array or a CUDA tensor")
+    if like.mem != MEM_HOST:
+        raise ConfigError(f"{name}: host output for device input")
+    if out.dtype != np.float32 or not out.flags.c_contiguous or not out.flags.writeable:
+        raise ConfigError(f"{name}: must be a writeable C-contiguous float32 array")
+    if out.size != n:
+        raise ConfigError(f"{name}: expected {n} values, got {out.size}")
+    return out
+
+
 # ---------------------------------------------------------------------------
 # operator
 # ---------------------------------------------------------------------------
@@ -400,7 +429,7 @@ class ConeBeamProjector:
     def apply(self, x, out=None, layout=None):
         """y = A x (project_forward, projector.hpp:194-204)."""
         xa = _Arg(x, self.domain_size(), "forward: volume")
-        y = out if out is not None else _alloc_like(xa, self.range_size())
+        y = _check_out(out, xa, self.range_size()) if out is not None else _alloc_like(xa, self.range_size())
         _check(_lib.kct_forward(self._h, xa.ptr, _ptr(y), xa.mem, _layout_code(layout, xa.mem),
                                 _stream_of(xa.mem, self._dev_index(xa))))
         return y
@@ -408,7 +437,7 @@ class ConeBeamProjector:
     def apply_adjoint(self, y, out=None, layout=None):
         """x = A^T y (project_adjoint, projector.hpp:226-261)."""
         ya = _Arg(y, self.range_size(), "adjoint: projections")
-        x = out if out is not None else _alloc_like(ya, self.domain_size())
+        x = _check_out(out, ya, self.domain_size()) if out is not None else _alloc_like(ya, self.domain_size())
         _check(_lib.kct_adjoint(self._h, ya.ptr, _ptr(x), ya.mem, _layout_code(layout, ya.mem),
                                 _stream_of(ya.mem, self._dev_index(ya))))
         return x
@@ -416,7 +445,7 @@ class ConeBeamProjector:
     def fdk(self, proj, out=None, layout=None):
         """FDK reconstruction (fdk.hpp:50-139) of a full-circle scan on this geometry."""
         pa = _Arg(proj, self.range_size(), "fdk: projections")
-        x = out if out is not None else _alloc_like(pa, self.domain_size())
+        x = _check_out(out, pa, self.domain_size()) if out is not None else _alloc_like(pa, self.domain_size())
         _check(_lib.kct_fdk(self._h, pa.ptr, _ptr(x), pa.mem, _layout_code(layout, pa.mem),
                             _stream_of(pa.mem, self._dev_index(pa))))
         return x
@@ -442,28 +471,40 @@ class ConeBeamProjector:
     # layout conversions of device tensors
     def volume_to_native(self, ref, out=None):
         import torch
-        out = out if out is not None else torch.empty_like(ref)
+        a = _Arg(ref, self.domain_size(), "volume_to_native")
+        if a.mem != MEM_DEVICE:
+            raise ConfigError("volume_to_native: expects a CUDA tensor")
+        out = _check_out(out, a, self.domain_size()) if out is not None else torch.empty_like(ref)
         _check(_lib.kct_volume_to_native(self._h, ref.data_ptr(), out.data_ptr(),
                                          torch.cuda.current_stream(ref.device).cuda_stream))
         return out
 
     def volume_from_native(self, nat, out=None):
         import torch
-        out = out if out is not None else torch.empty_like(nat)
+        a = _Arg(nat, self.domain_size(), "volume_from_native")
+        if a.mem != MEM_DEVICE:
+            raise ConfigError("volume_from_native: expects a CUDA tensor")
+        out = _check_out(out, a, self.domain_size()) if out is not None else torch.empty_like(nat)
         _check(_lib.kct_volume_from_native(self._h, nat.data_ptr(), out.data_ptr(),
                                            torch.cuda.current_stream(nat.device).cuda_stream))
         return out
 
     def proj_to_native(self, ref, out=None):
         import torch
-        out = out if out is not None else torch.empty_like(ref)
+        a = _Arg(ref, self.range_size(), "proj_to_native")
+        if a.mem != MEM_DEVICE:
+            raise ConfigError("proj_to_native: expects a CUDA tensor")
+        out = _check_out(out, a, self.range_size()) if out is not None else torch.empty_like(ref)
         _check(_lib.kct_proj_to_native(self._h, ref.data_ptr(), out.data_ptr(),
                                        torch.cuda.current_stream(ref.device).cuda_stream))
         return out
 
     def proj_from_native(self, nat, out=None):
         import torch
-        out = out if out is not None else torch.empty_like(nat)
+        a = _Arg(nat, self.range_size(), "proj_from_native")
+        if a.mem != MEM_DEVICE:
+            raise ConfigError("proj_from_native: expects a CUDA tensor")
+        out = _check_out(out, a, self.range_size()) if out is not None else torch.empty_like(nat)
         _check(_lib.kct_proj_from_native(self._h, nat.data_ptr(), out.data_ptr(),
                                          torch.cuda.current_stream(nat.device).cuda_stream))
         return out
@@ -544,9 +585,7 @@ def _out_for(arg: _Arg, m: int, out):
     """The caller's output buffer (e.g. pinned host memory) or a new one."""
     if out is None:
         return _alloc_like(arg, m)
-    if (out.numel() if _is_torch(out) else np.asarray(out).size) != m:
-        raise ConfigError("output size mismatch")
-    return out
+    return _check_out(out, arg, m)
 
 
 def cgls_recon(proj: ProjectionSet, grid: GridSpec, iters: int, opts: ReconOptions | None = None,

@@ -100,7 +100,7 @@ def test_size_mismatch():
         A.apply(np.zeros(A.domain_size() + 1, dtype=np.float32))
 
 
-@pytest.mark.parametrize("cfg,n_angles", [(1, 64), (2, 8), (3, 3), (4, 1), (5, 2)])
+@pytest.mark.parametrize("cfg,n_angles", [(1, 64), (2, 45), (3, 12), (4, 6), (5, 9)])
 def test_baseline_geometry_parity(ora, cfg, n_angles):
     """Full-size BASELINE volumes/detectors, angle subsets the oracle finishes in seconds."""
     grid, geom = baseline_geometry(cfg, n_angles=n_angles)
@@ -340,3 +340,74 @@ def test_slab_paths_awkward_geometry(monkeypatch, ora):
     monkeypatch.setenv("KCT_ADJ_SLAB", "0")
     row = projector(grid, geom).apply_adjoint(y)
     assert rel_l2(slab, row) < 1e-6
+
+
+def test_out_argument_validation():
+    """Caller-supplied outputs must match what the C ABI writes:
+    exact size, contiguous float32, same memory kind / device as the input."""
+    import torch
+    grid, geom = tiny_grid(), tiny_geometry(4)
+    gs, ge = to_pkg(grid, geom)
+    A = k.ConeBeamProjector(gs, ge)
+    x = np.random.default_rng(0).uniform(0, 1, gs.count()).astype(np.float32)
+    n = ge.ray_count()
+    bad = [np.empty(n - 1, np.float32), np.empty(n, np.float64),
+           np.empty(2 * n, np.float32)[::2], torch.empty(n, device="cuda")]
+    for out in bad:
+        with pytest.raises(k.ConfigError):
+            A.apply(x, out=out)
+    xd = torch.from_numpy(x).cuda()
+    for out in (np.empty(n, np.float32), torch.empty(n, device="cuda", dtype=torch.float64),
+                torch.empty(n + 1, device="cuda")):
+        with pytest.raises(k.ConfigError):
+            A.apply(xd, out=out)
+    with pytest.raises(k.ConfigError):
+        A.apply_adjoint(np.zeros(n, np.float32), out=np.empty(gs.count() - 1, np.float32))
+    with pytest.raises(k.ConfigError):
+        A.volume_to_native(xd, out=torch.empty(3, device="cuda"))
+    good = np.empty(n, np.float32)
+    assert A.apply(x, out=good) is good
+    np.testing.assert_array_equal(good, A.apply(x))
+
+
+@pytest.mark.parametrize("cfg,n_angles", [(1, 64), (3, 6), (4, 3)])
+@pytest.mark.parametrize("how", ["KCT_ADJ_TABLE=0", "KCT_ADJ_TABLE_MB=1"])
+def test_walk_table_fallback(monkeypatch, ora, cfg, n_angles, how):
+    """Without the precomputed walk table (disabled, or over the memory budget)
+    the adjoint recomputes the walks on the fly: same parity bar, and
+    bit-identical to the table path (same walk, same deposits)."""
+    grid, geom = baseline_geometry(cfg, n_angles=n_angles)
+    y = np.random.default_rng(41).uniform(0, 1, geom.ray_count).astype(np.float32)
+    with_tab = projector(grid, geom)
+    assert with_tab.info("adj_walk_entries") > 0
+    key, val = how.split("=")
+    monkeypatch.setenv(key, val)
+    A = projector(grid, geom)
+    assert A.info("adj_walk_entries") == 0
+    got = A.apply_adjoint(y)
+    assert np.array_equal(got, A.apply_adjoint(y))
+    assert np.array_equal(got, with_tab.apply_adjoint(y))
+    assert rel_l2(got, ora.adjoint(grid, geom, y)) < TOL
+
+
+@pytest.mark.parametrize("cfg,n_angles", [(1, 64), (2, 8), (3, 4), (4, 2)])
+def test_count_nnz_matches_reference(ora, cfg, n_angles):
+    """nnz (the roofline's unit) equals the reference traverse_ray's count of
+    positive-length segments, up to segments whose float64 length is a few
+    ulps above zero (float32 walk: at most 1e-6 of nnz)."""
+    grid, geom = baseline_geometry(cfg, n_angles=n_angles)
+    got, want = projector(grid, geom).count_nnz(), ora.count_nnz(grid, geom)
+    print(f"\n[nnz c{cfg}/{n_angles} views] gpu {got} reference {want} diff {got - want}")
+    assert abs(got - want) <= max(2, 1e-6 * want)
+
+
+@pytest.mark.parametrize("n_angles", [8])
+def test_c4_slot_conflict_path(ora, n_angles):
+    """c4's row spacing can reach one slab, so the adjoint's slot-conflict
+    detection is on (adj_slab_detect) — checked against the oracle over several
+    views, not one."""
+    grid, geom = baseline_geometry(4, n_angles=n_angles)
+    A = projector(grid, geom)
+    assert A.info("adj_slab") == 1 and A.info("adj_slab_detect") == 1
+    y = np.random.default_rng(43).uniform(0, 1, geom.ray_count).astype(np.float32)
+    assert rel_l2(A.apply_adjoint(y), ora.adjoint(grid, geom, y)) < TOL

@@ -326,3 +326,28 @@ def test_restart_env_default(monkeypatch):
         A.set_option("solver_restart", 2)
     with pytest.raises(k.ConfigError):
         A.set_option("no_such_option", 1)
+
+
+@pytest.mark.slow
+def test_c4_geometry_piccs_parity(ora):
+    """BASELINE config 4 geometry (512^3 @ 0.25 mm, 768^2 @ 0.4 mm: the
+    detector overhangs the volume, the adjoint's slot-conflict detection is
+    on) at 4 views, PICCS 2x2 alpha = 0.5, seeded c4 phantoms, vs the oracle."""
+    from paper_2509_08574_b200 import synth
+    grid, geom = baseline_geometry(4, n_angles=4)
+    gs, ge = to_pkg(grid, geom)
+    _, prior, follow = synth.study("c4")
+    A = k.ConeBeamProjector(gs, ge)
+    b = synth.poisson_log(A.apply(follow), 1e5, seed=synth.noise_seed("c4"))
+    p = dict(alpha=0.5, outer_iters=2, inner_iters=2)
+    ora.set_threads(8)
+    x_ref, r_ref = ora.irn(grid, geom, KIND_PICCS, b.astype(np.float64), prior, p,
+                           ground_truth=follow)
+    rep = k.irn_piccs(k.ProjectionSet(ge, b), gs, prior,
+                      k.RegularizationParams(alpha=0.5, outer_iters=2, inner_iters=2),
+                      k.ReconOptions(ground_truth=follow), projector=A)
+    e = rel_l2(rep.volume, x_ref)
+    print(f"\n[c4 4 views 2x2] iterate rel-L2 {e:.3e}")
+    assert e < RTOL
+    np.testing.assert_allclose(rep.objective_history, r_ref["objective_history"], rtol=RTOL)
+    np.testing.assert_allclose(rep.error_history, r_ref["error_history"], rtol=RTOL)
