@@ -138,8 +138,9 @@ int kct_count_nnz(kct_projector* h, uint64_t* nnz, void* stream);
  * tests and benchmarks).  key: "adj_slab" (1: slab-lane adjoint deposits),
  * "adj_slab_detect", "adj_bz" (brick height), "adj_stride" (row-wise pass
  * stride S), "adj_groups" (angle groups), "adj_gather", "adj_walk_entries",
- * "fwd_rows_per_warp", "fwd_bands", "fwd_split_z" (host forward split upload:
- * slabs below it first, 0 = off).  Unknown key: ConfigError. */
+ * "fwd_rows_per_warp", "fwd_bands", "fwd_split_z" / "fwd_split_lo" (host
+ * forward split upload: slabs [lo, z) first, z = 0: off), "mirror" (1: z-mirror
+ * ray pairs, rows iv / nv-1-iv), "solver_restart".  Unknown key: ConfigError. */
 int kct_projector_info(const kct_projector* h, const char* key, double* value);
 /* Layout conversion on device (reference <-> native), stream-ordered. */
 int kct_volume_to_native(const kct_projector* h, const float* ref, float* native, void* stream);

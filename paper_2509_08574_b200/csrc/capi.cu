@@ -167,19 +167,24 @@ void forward_host_pipelined(kct::Projector& P, const float* vol, float* proj, in
                             cudaStream_t s) {
     const size_t M = P.domain_size(), N = P.range_size();
     cudaStream_t sc = P.pipe_stream();
-    // Split upload (reference layout: a z range is contiguous): slabs [0, Z)
-    // first, row band 0 (whose rays stay below Z) runs while the rest of the
-    // volume is uploaded on the copy stream.
+    // Split upload (reference layout: a z range is contiguous): slabs [Z0, Z)
+    // first, row band 0 (whose rays stay inside them: Z0 = 0, or the central
+    // slabs with z-mirror pairs) runs while the rest of the volume is uploaded
+    // on the copy stream.
     const int Z = layout == KCT_LAYOUT_REFERENCE ? P.fwd_split_z() : 0;
+    const int Z0 = Z > 0 ? P.fwd_split_lo() : 0;
+    const int nzg = P.grid().nz;
     if (Z > 0) {
         const kct_grid& gr = P.grid();
-        const size_t plane = (size_t)gr.nx * gr.ny, lo = (size_t)Z * plane;
+        const size_t plane = (size_t)gr.nx * gr.ny, lo = (size_t)Z0 * plane, hi = (size_t)Z * plane;
         float* tmp = P.scratch(2, M);
-        KCT_CUDA(cudaMemcpyAsync(tmp, vol, lo * sizeof(float), cudaMemcpyHostToDevice, s));
+        KCT_CUDA(cudaMemcpyAsync(tmp + lo, vol + lo, (hi - lo) * sizeof(float), cudaMemcpyHostToDevice, s));
         KCT_CUDA(cudaEventRecord(P.upload_event(), s));  // the copy stream starts after this call's
         KCT_CUDA(cudaStreamWaitEvent(sc, P.upload_event(), 0));  // earlier work on s
-        KCT_CUDA(cudaMemcpyAsync(tmp + lo, vol + lo, (M - lo) * sizeof(float), cudaMemcpyHostToDevice, sc));
-        P.vol_to_padded_z(tmp, 0, Z, s);
+        if (hi < M)
+            KCT_CUDA(cudaMemcpyAsync(tmp + hi, vol + hi, (M - hi) * sizeof(float), cudaMemcpyHostToDevice, sc));
+        if (lo > 0) KCT_CUDA(cudaMemcpyAsync(tmp, vol, lo * sizeof(float), cudaMemcpyHostToDevice, sc));
+        P.vol_to_padded_z(tmp, Z0, Z, s);
     } else if (layout == KCT_LAYOUT_REFERENCE) {
         float* tmp = P.scratch(2, M);
         KCT_CUDA(cudaMemcpyAsync(tmp, vol, M * sizeof(float), cudaMemcpyHostToDevice, s));
@@ -204,7 +209,8 @@ void forward_host_pipelined(kct::Projector& P, const float* vol, float* proj, in
         P.forward_split_lo(q, s);
         KCT_CUDA(cudaEventRecord(P.upload_event(), sc));
         KCT_CUDA(cudaStreamWaitEvent(s, P.upload_event(), 0));
-        P.vol_to_padded_z(P.scratch(2, M), Z, P.grid().nz, s);
+        if (Z < nzg) P.vol_to_padded_z(P.scratch(2, M), Z, nzg, s);
+        if (Z0 > 0) P.vol_to_padded_z(P.scratch(2, M), 0, Z0, s);
     }
     bool counted = false;
     if (done) {
@@ -329,9 +335,11 @@ int kct_projector_info(const kct_projector* h, const char* key, double* value) {
         else if (k == "adj_groups") *value = P.adj_groups();
         else if (k == "adj_gather") *value = P.adj_gather() ? 1 : 0;
         else if (k == "adj_walk_entries") *value = (double)P.walk_entries();
-        else if (k == "fwd_rows_per_warp") *value = 32 * P.fwd_chunks();
+        else if (k == "fwd_rows_per_warp") *value = 32 * P.fwd_chunks() * (P.mirror() ? 2 : 1);
         else if (k == "fwd_bands") *value = P.dev_geom().fwd_bands;
         else if (k == "fwd_split_z") *value = P.fwd_split_z();
+        else if (k == "fwd_split_lo") *value = P.fwd_split_lo();
+        else if (k == "mirror") *value = P.mirror() ? 1 : 0;
         else if (k == "solver_restart") *value = P.solver_restart ? 1 : 0;
         else throw kct::ConfigError("kct_projector_info: unknown key '" + k + "'");
     });

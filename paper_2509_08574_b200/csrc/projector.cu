@@ -61,7 +61,18 @@ static_assert(Projector::kPipeChunks <= 8, "FwdChunks holds at most 8 pipeline c
 
 // vol: slab 0 of voxel column 0 of the padded native volume (column stride
 // nz + 2, zero slabs at -1 and nz; Projector::pad_volume).
-template <int C, bool COUNT, bool DONE = false>
+//
+// MIR (z-mirror pairs; Projector::mirror_): in a z-symmetric geometry
+// (offset_v = 0, nv even, grid centred in z) detector rows iv and nv-1-iv
+// are reflections of each other in the plane z = 0, and so are slabs k and
+// nz-1-k.  A lane then walks ray pair p — the primary row nv/2-1-p (dv < 0)
+// and its mirror nv/2+p — with ONE z state: the mirror ray is defined to
+// cross plane nz-P exactly where the primary crosses plane P (the same float
+// values; the adjoint's per-ray records encode the mirror's z state so that
+// its zcross gives these values, adj_weight_kernel), so per xy segment and per
+// z crossing one test serves two rays, which load slabs k and nz-1-k.  Pairs
+// are numbered from the centre plane outwards (band 0: the rows nearest z = 0).
+template <int C, bool COUNT, bool DONE = false, bool MIR = false>
 __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const float* __restrict__ vol,
                                                   float* __restrict__ out,
                                                   const ColParams* __restrict__ cols,
@@ -81,19 +92,22 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
     const int iu = quad * kFwdWarps + (threadIdx.x >> 5);
     if (iu >= g.nu) return;
     const ColParams cp = cols[(size_t)a * g.nu + iu];
-    const int iv0 = band * (32 * C) + lane;
+    const int iv0 = band * (32 * C) + lane;  // row (MIR: pair) of chunk 0
     const int nz = g.nz;
+    const int nrows = MIR ? g.nv / 2 : g.nv;
 
     // per ray: slab k, next crossing wz of plane P (kept as pk = P - k0),
     // remaining crossings nrem of planes inside [0, nz]
-    float acc[C], wz[C], fz[C], imk[C], dvv[C];
+    float acc[C], accm[C], wz[C], fz[C], imk[C], dvv[C];
     int k[C], kstep[C], pk[C], nrem[C];
     bool hit = false;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-        const int iv = iv0 + 32 * c;
+        const int p = iv0 + 32 * c;
+        const int iv = MIR ? g.nv / 2 - 1 - p : p;  // MIR: the primary (dv < 0)
         acc[c] = 0.f;
-        const bool row_ok = iv < g.nv;
+        accm[c] = 0.f;
+        const bool row_ok = p < nrows;
         const float dv = row_ok ? dvtab[iv] : 0.f;
         dvv[c] = dv;
         // z index at w_in in float64, split into integer + fraction
@@ -103,12 +117,12 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
         fz[c] = (float)(kzd - fl);
         imk[c] = row_ok ? __fmul_rn(invdv[iv], cp.inv_h1) : 0.f;
         int kk = min(max(k0, -1), nz);
-        const int ks = dv > 0.f ? 1 : -1;
+        const int ks = MIR ? -1 : (dv > 0.f ? 1 : -1);
         kstep[c] = ks;
         const int P = ks > 0 ? kk + 1 : kk;
         int n = ks > 0 ? nz - kk : kk + 1;  // planes P, P+ks, ... inside [0, nz]
         if (!row_ok || dv == 0.f) n = 0;
-        if (!row_ok) kk = -1;  // reads the zero pad, never crosses
+        if (!row_ok) kk = MIR ? nz : -1;  // reads the zero pads, never crosses
         k[c] = kk;
         pk[c] = P - k0;
         nrem[c] = max(n, 0);
@@ -137,22 +151,29 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
             // nz: slabs k in [-1, nz] need no range check)
             // (32-bit element index: one IMAD.WIDE per load)
             const int col = (i + nx * j) * vpad_stride(nz);
-            float v[C], wa[C];
+            const int colm = col + nz - 1;  // MIR: slab nz-1-k at colm - k
+            float v[C], vm[C], wa[C];
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 wa[c] = wcur;
                 v[c] = COUNT ? ((unsigned)k[c] < (unsigned)nz ? 1.f : 0.f) : __ldg(vol + (col + k[c]));
+                if (MIR) vm[c] = COUNT ? v[c] : __ldg(vol + (colm - k[c]));
             }
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 if (wz[c] < wb) {  // this ray crosses z-plane(s) inside the segment
                     do {
                         const float len = wz[c] - wa[c];
-                        if (COUNT) acc[c] += (len > 0.f && v[c] != 0.f) ? 1.f : 0.f;
-                        else acc[c] = __fmaf_rn(len, v[c], acc[c]);
+                        if (COUNT) {
+                            acc[c] += (len > 0.f && v[c] != 0.f) ? 1.f : 0.f;
+                        } else {
+                            acc[c] = __fmaf_rn(len, v[c], acc[c]);
+                            if (MIR) accm[c] = __fmaf_rn(len, vm[c], accm[c]);
+                        }
                         wa[c] = wz[c];
                         k[c] += kstep[c];
                         v[c] = COUNT ? ((unsigned)k[c] < (unsigned)nz ? 1.f : 0.f) : __ldg(vol + (col + k[c]));
+                        if (MIR && !COUNT) vm[c] = __ldg(vol + (colm - k[c]));
                         pk[c] += kstep[c];
                         nrem[c] -= 1;
                         wz[c] = nrem[c] > 0
@@ -161,8 +182,12 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
                     } while (wz[c] < wb);
                 }
                 const float len = wb - wa[c];
-                if (COUNT) acc[c] += (len > 0.f && v[c] != 0.f) ? 1.f : 0.f;
-                else acc[c] = __fmaf_rn(len, v[c], acc[c]);
+                if (COUNT) {
+                    acc[c] += (len > 0.f && v[c] != 0.f) ? 1.f : 0.f;
+                } else {
+                    acc[c] = __fmaf_rn(len, v[c], acc[c]);
+                    if (MIR) accm[c] = __fmaf_rn(len, vm[c], accm[c]);
+                }
             }
             if (wnext >= cp.w_out) break;
             wcur = fmaxf(wnext, wcur);
@@ -183,13 +208,18 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
     float* o = out + ((size_t)a * g.nu + iu) * g.nv;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-        const int iv = iv0 + 32 * c;
-        if (iv < g.nv) {
+        const int p = iv0 + 32 * c;
+        if (p < nrows) {
+            const int iv = MIR ? g.nv / 2 - 1 - p : p;
             if (COUNT) {
                 o[iv] = acc[c];
+                if (MIR) o[g.nv - 1 - iv] = acc[c];  // the mirror's pieces are the primary's
             } else {
+                // the mirror's 3D length factor is the primary's (dv(nv-1-iv) = -dv(iv))
                 const float q = dvv[c] * cp.inv_l;
-                o[iv] = acc[c] * __fsqrt_rn(__fmaf_rn(q, q, 1.f));
+                const float f = __fsqrt_rn(__fmaf_rn(q, q, 1.f));
+                o[iv] = acc[c] * f;
+                if (MIR) o[g.nv - 1 - iv] = accm[c] * f;
             }
         }
     }
@@ -364,15 +394,18 @@ __device__ __forceinline__ void row_init(RowZ& r, bool on, int iv, float w_in, f
         r.k = min(max(k0, K0 - 1), kend);
         return;
     }
-    k = sg > 0 ? max(k, k0) : min(k, k0);
+    // the ray's slab at w_in: k0, or k0 - 1 for a z-mirror record (f0 <= 0,
+    // adj_weight_kernel); the walk never returns behind it
+    const int kin = r.f0 < 0.f ? k0 - 1 : k0;
+    k = sg > 0 ? max(k, kin) : min(k, kin);
     int pn = sg > 0 ? k + 1 : k;      // next plane
     const int pp = sg > 0 ? k : k + 1;  // plane crossed entering slab k
     float zn = zcross(pn, k0, r.f0, r.imk, w_in);
-    const float zp = k != k0 ? zcross(pp, k0, r.f0, r.imk, w_in) : -kInf;
+    const float zp = k != kin ? zcross(pp, k0, r.f0, r.imk, w_in) : -kInf;
     if (!(zp < lo && !(zn < lo))) {
         // z(lo) within rounding of a plane: search
         if (sg > 0) {
-            while (k > k0 && !(zcross(k, k0, r.f0, r.imk, w_in) < lo)) --k;
+            while (k > kin && !(zcross(k, k0, r.f0, r.imk, w_in) < lo)) --k;
             while (zcross(k + 1, k0, r.f0, r.imk, w_in) < lo) ++k;
             pn = k + 1;
         } else {
@@ -1071,15 +1104,20 @@ __global__ void __launch_bounds__(128) adj_gather_kernel(const float* __restrict
                 const int rhi = min(nv - 1, (int)floorf((dhi - g.dv0) * rpv + 1e-3f));
                 for (int iv = rlo; iv <= rhi; ++iv) {
                     const float dv = dvtab[iv];
-                    const double kzd = fma(dvd[iv], cp.g_in, -g.kz0d);
+                    // z-mirror rows: the primary's z state, planes reflected
+                    // (the forward's MIR definition, fwd_kernel)
+                    const bool mir = g.mirror && iv >= nv / 2;
+                    const int ivp = mir ? nv - 1 - iv : iv;
+                    const double kzd = fma(dvd[ivp], cp.g_in, -g.kz0d);
                     const double fl = floor(kzd);
                     const int k0 = (int)fmax(fmin(fl, 1.0e9), -1.0e9);
                     const float f0 = (float)(kzd - fl);
                     float zlo, zhi;
                     if (dv != 0.f) {
-                        const float imk = __fmul_rn(invdv[iv], cp.inv_h1);
-                        const float w0 = zcross(k, k0, f0, imk, cp.w_in);
-                        const float w1 = zcross(k + 1, k0, f0, imk, cp.w_in);
+                        const float imk = __fmul_rn(invdv[ivp], cp.inv_h1);
+                        const int kp = mir ? nz - 1 - k : k;  // the primary's slab
+                        const float w0 = zcross(kp, k0, f0, imk, cp.w_in);
+                        const float w1 = zcross(kp + 1, k0, f0, imk, cp.w_in);
                         zlo = fminf(w0, w1);
                         zhi = fmaxf(w0, w1);
                     } else {
@@ -1241,6 +1279,15 @@ void Projector::build_tables(const kct_geometry& geom) {
     dg_.pu = (float)geom.pu; dg_.off_u = (float)geom.offset_u;
     dg_.pv = (float)geom.pv;
     dg_.dv0 = (float)((0.5 - 0.5 * nv) * geom.pv + geom.offset_v);
+    // z-mirror geometry (fwd_kernel MIR): the source is at z = 0 (projector.hpp:24-27);
+    // with offset_v = 0 and nv even, rows iv and nv-1-iv have dv of opposite
+    // sign (exactly), and a grid centred in z maps slab k onto nz-1-k
+    {
+        const char* me = std::getenv("KCT_MIRROR");
+        mirror_ = geom.offset_v == 0.0 && nv % 2 == 0 &&
+                  std::abs(grid_.oz / grid_.sz + 0.5 * nz) < 1e-9 && !(me && me[0] == '0');
+        dg_.mirror = mirror_ ? 1 : 0;
+    }
 
     // detector rows: dv(iv) (projector.hpp:36) — the ray's z at the detector
     std::vector<float> dv(nv), invdv(nv);
@@ -1330,8 +1377,8 @@ void Projector::build_tables(const kct_geometry& geom) {
     }
     dg_.full_footprint = full_fp ? 1 : 0;
 
-    // forward launch shape: rows per warp = 32*C, C <= 4
-    const int chunks = (nv + 31) / 32;
+    // forward launch shape: rows (mirror: row pairs) per warp = 32*C, C <= 4
+    const int chunks = ((mirror_ ? nv / 2 : nv) + 31) / 32;
     int cmax = 4;
     if (const char* e = std::getenv("KCT_FWD_C")) cmax = std::clamp(std::atoi(e), 1, 4);
     fwd_bands_ = (chunks + cmax - 1) / cmax;
@@ -1415,18 +1462,23 @@ void Projector::build_tables(const kct_geometry& geom) {
                 // split upload of a host volume: the rays of row band 0 stay
                 // below slab Z (largest continuous z index over every column's
                 // clip, row band 0's top row; + 2 slabs of margin), so band 0
-                // can run once slabs [0, Z) are on the device
+                // can run once slabs [0, Z) are on the device.  Mirror pairs:
+                // band 0 holds the rows nearest z = 0 and stays inside slabs
+                // [nz - Z, Z).
                 double kmax = -1e30;
-                const int r1 = std::min(nv, 32 * fwd_c_) - 1;
+                const int r1 = std::min(nv, (mirror_ ? nv / 2 : 0) + 32 * fwd_c_) - 1;
                 for (const ColParams& cp : cols) {
                     if (!(cp.w_in < cp.w_out)) continue;
                     const double Gin = cp.g_in, Gout = cp.g_in + (double)(cp.w_out - cp.w_in) / cp.inv_h1;
                     kmax = std::max(kmax, std::max(dvd[r1] * Gin, dvd[r1] * Gout) - grid_.oz / grid_.sz);
                 }
-                const int Z = (int)std::floor(kmax) + 3;
+                const int Z = std::min((int)std::floor(kmax) + 3, nz);
+                const int Zlo = mirror_ ? std::max(0, nz - Z) : 0;
                 const char* sp = std::getenv("KCT_FWD_SPLIT");
-                if (fwd_bands_ >= 2 && Z >= 1 && Z <= (nz * 6) / 10 && !(sp && sp[0] == '0')) {
+                if (fwd_bands_ >= 2 && Z - Zlo >= 1 && Z - Zlo <= (nz * 6) / 10 &&
+                    !(sp && sp[0] == '0')) {
                     fwd_split_z_ = Z;
+                    fwd_split_lo_ = Zlo;
                     std::vector<int> lo, hi;
                     const int B = fwd_bands_;
                     for (size_t t = 0; t < nitems; ++t) {
@@ -1648,7 +1700,12 @@ __global__ void __launch_bounds__(256) adj_weight_kernel(const float* __restrict
     const size_t col = t / (size_t)nv;
     if (col >= ncols) return;
     const int iv = (int)(t - col * (size_t)nv);
-    const RowTab rt = ld_row(rows, iv);
+    // z-mirror geometry (fwd_kernel MIR): a row of the upper half is the
+    // reflection of row nv-1-iv, whose z state it takes, reflected:
+    // k0' = nz - k0, f0' = -f0, imk' = -imk, kstep +1 — then zcross(P') is
+    // bit-identical to the primary's zcross(nz - P') (the forward's crossings)
+    const bool mirror = g.mirror && iv >= nv / 2;
+    const RowTab rt = ld_row(rows, mirror ? nv - 1 - iv : iv);
     const float inv_l = cols[col].inv_l, inv_h1 = cols[col].inv_h1;
     const double g_in = cols[col].g_in;
     const float q = rt.dv * inv_l;
@@ -1658,9 +1715,16 @@ __global__ void __launch_bounds__(256) adj_weight_kernel(const float* __restrict
     const int ks = rt.dv > 0.f ? 1 : rt.dv < 0.f ? -1 : 0;
     float4 r;
     r.x = y[t] * __fsqrt_rn(__fmaf_rn(q, q, 1.f));
-    r.y = (float)(kzd - fl);
-    r.z = __fmul_rn(rt.invdv, inv_h1);
-    r.w = __int_as_float(k0 * 4 + ks + 1);
+    const float f0 = (float)(kzd - fl), imk = __fmul_rn(rt.invdv, inv_h1);
+    if (mirror) {
+        r.y = -f0;
+        r.z = -imk;
+        r.w = __int_as_float((g.nz - k0) * 4 + 2);
+    } else {
+        r.y = f0;
+        r.z = imk;
+        r.w = __int_as_float(k0 * 4 + ks + 1);
+    }
     rec[t] = r;
 }
 
@@ -1677,10 +1741,27 @@ __global__ void __launch_bounds__(256) adj_group_sum(float* __restrict__ out,
 }
 
 // ---- launches -----------------------------------------------------------------
+template <bool COUNT, bool MIR>
+static void launch_fwd_t(int C, int bands, int band0, const float* vol, float* out,
+                         const ColParams* cols, const float* dv, const float* invdv,
+                         const double* dvd, const DevGeom& g, const int* order, cudaStream_t s,
+                         const FwdChunks* done);
+
 template <bool COUNT>
 static void launch_fwd(int C, int bands, int band0, const float* vol, float* out, const ColParams* cols,
                        const float* dv, const float* invdv, const double* dvd, const DevGeom& g,
                        const int* order, cudaStream_t s, const FwdChunks* done = nullptr) {
+    if (g.mirror)
+        launch_fwd_t<COUNT, true>(C, bands, band0, vol, out, cols, dv, invdv, dvd, g, order, s, done);
+    else
+        launch_fwd_t<COUNT, false>(C, bands, band0, vol, out, cols, dv, invdv, dvd, g, order, s, done);
+}
+
+template <bool COUNT, bool MIR>
+static void launch_fwd_t(int C, int bands, int band0, const float* vol, float* out,
+                         const ColParams* cols, const float* dv, const float* invdv,
+                         const double* dvd, const DevGeom& g, const int* order, cudaStream_t s,
+                         const FwdChunks* done) {
     // 1D grid over (angle, band, column quad) items
     const unsigned nq = (unsigned)((g.nu + kFwdWarps - 1) / kFwdWarps);
     const dim3 g1(nq * (unsigned)bands * (unsigned)g.na, 1, 1);
@@ -1692,19 +1773,19 @@ static void launch_fwd(int C, int bands, int band0, const float* vol, float* out
     if (done) fc = *done;
     if (!COUNT && done) {  // host pipeline (counted launch)
         switch (C) {
-        case 1: fwd_kernel<1, false, true><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
-        case 2: fwd_kernel<2, false, true><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
-        case 3: fwd_kernel<3, false, true><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
-        default: fwd_kernel<4, false, true><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
+        case 1: fwd_kernel<1, false, true, MIR><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
+        case 2: fwd_kernel<2, false, true, MIR><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
+        case 3: fwd_kernel<3, false, true, MIR><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
+        default: fwd_kernel<4, false, true, MIR><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
         }
         KCT_LAUNCHED();
         return;
     }
     switch (C) {
-    case 1: fwd_kernel<1, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
-    case 2: fwd_kernel<2, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
-    case 3: fwd_kernel<3, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
-    default: fwd_kernel<4, COUNT><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
+    case 1: fwd_kernel<1, COUNT, false, MIR><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
+    case 2: fwd_kernel<2, COUNT, false, MIR><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
+    case 3: fwd_kernel<3, COUNT, false, MIR><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
+    default: fwd_kernel<4, COUNT, false, MIR><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
     }
     KCT_LAUNCHED();
 }

@@ -54,6 +54,8 @@ class Projector {
     // Split upload of a host volume (forward_host_pipelined): row band 0's
     // rays stay below slab fwd_split_z() (0: no split).
     int fwd_split_z() const { return fwd_split_z_; }
+    int fwd_split_lo() const { return fwd_split_lo_; }  // mirror pairs: band 0 needs [lo, z)
+    bool mirror() const { return mirror_; }
     void forward_split_lo(float* proj, cudaStream_t s) const;
     void forward_split_hi(float* proj, int chunk, cudaStream_t s) const;
     // The forward reads a padded copy of the native volume (column stride
@@ -145,7 +147,8 @@ class Projector {
     cudaStream_t pipe_stream_ = nullptr;
     cudaEvent_t pipe_ev_[kPipeChunks] = {};
     cudaEvent_t up_ev_ = nullptr;
-    int fwd_split_z_ = 0;
+    int fwd_split_z_ = 0, fwd_split_lo_ = 0;
+    bool mirror_ = false;             // z-mirror pairs (fwd_kernel MIR, adj_weight_kernel)
     float* d_vpad_ = nullptr;         // padded native volume read by the forward
     float2* d_cs_ = nullptr;          // per-angle (cos, sin) on the device
     int* d_flo_ = nullptr;            // block order of the split forward's band 0 (all angles)

@@ -287,12 +287,16 @@ def test_split_upload_forward_is_bitwise(monkeypatch):
 
 
 def test_projector_info_reports_paths():
-    """kct_projector_info: BASELINE c3 runs the slab-lane adjoint and the split
-    host upload; c1 (one row band) has no split; unknown keys are ConfigError."""
+    """kct_projector_info: BASELINE c3 runs the slab-lane adjoint, z-mirror
+    pairs (3 chunks of 32 row pairs per warp: 192 rows) and the split host
+    upload of the central slabs; c1 (one row band) has no split; unknown keys
+    are ConfigError."""
     A = projector(*baseline_geometry(3, n_angles=16))
     assert A.info("adj_slab") == 1 and A.info("adj_gather") == 0
-    assert A.info("adj_bz") == 86 and A.info("fwd_rows_per_warp") == 128
-    assert 0 < A.info("fwd_split_z") < 256
+    assert A.info("mirror") == 1
+    assert A.info("adj_bz") == 86 and A.info("fwd_rows_per_warp") == 192
+    lo, hi = A.info("fwd_split_lo"), A.info("fwd_split_z")
+    assert 0 < lo < 128 < hi < 256 and lo + hi == 256
     assert A.info("adj_walk_entries") > 0
     B = projector(*baseline_geometry(1, n_angles=8))
     assert B.info("adj_slab") == 1 and B.info("fwd_split_z") == 0
@@ -393,16 +397,18 @@ def test_walk_table_fallback(monkeypatch, ora, cfg, n_angles, how):
 @pytest.mark.parametrize("cfg,n_angles", [(1, 64), (2, 8), (3, 4), (4, 2)])
 def test_count_nnz_matches_reference(ora, cfg, n_angles):
     """nnz (the roofline's unit) equals the reference traverse_ray's count of
-    positive-length segments up to degenerate segments: rays through voxel
-    edges / corners (c1: 1 mm voxels, 1 mm pitch, 64 views incl. the four
-    axis-aligned ones) get float64 lengths of ~1e-13 mm where the float32 walk
-    gets exactly 0 (measured: c1 -9258 of 45.36 M, 2e-4).  They carry no
-    weight, so the byte model is unaffected; bar 5e-4 of nnz."""
+    positive-length segments up to degenerate segments: at the axis-aligned
+    views (multiples of 90 degrees) rays run inside voxel planes / through
+    voxel edges and the float64 walk produces segments shorter than 1e-6 mm
+    (0.38% of the segments of a c2 view at 0 degrees, 1e-5 at 45 degrees,
+    oracle trace) that the float32 walk gets as exactly 0.  They carry no
+    weight, so the byte model is unaffected (measured: c1 64 views -2.0e-4,
+    c2 8 views -1.5e-3); bar 5e-3 of nnz."""
     grid, geom = baseline_geometry(cfg, n_angles=n_angles)
     got, want = projector(grid, geom).count_nnz(), ora.count_nnz(grid, geom)
     print(f"\n[nnz c{cfg}/{n_angles} views] gpu {got} reference {want} "
           f"diff {got - want} ({(got - want) / want:.2e})")
-    assert abs(got - want) <= max(2, 5e-4 * want)
+    assert abs(got - want) <= max(2, 5e-3 * want)
 
 
 @pytest.mark.parametrize("n_angles", [8])
@@ -415,3 +421,49 @@ def test_c4_slot_conflict_path(ora, n_angles):
     assert A.info("adj_slab") == 1 and A.info("adj_slab_detect") == 1
     y = np.random.default_rng(43).uniform(0, 1, geom.ray_count).astype(np.float32)
     assert rel_l2(A.apply_adjoint(y), ora.adjoint(grid, geom, y)) < TOL
+
+
+def mirror_geometry(n_angles=5, nu=7, nv=6):
+    """z-symmetric tiny geometry: offset_v = 0, nv even, grid centred in z."""
+    from oracle import Geometry, uniform_angles
+    return Geometry(40.0, 90.0, nu, nv, 1.6, 1.9, uniform_angles(n_angles) + 0.1, 0.7, 0.0)
+
+
+def test_mirror_pairs_exact_transpose():
+    """With z-mirror pairs (fwd_kernel MIR: rows iv / nv-1-iv share one z
+    state; the adjoint's per-ray records encode the mirror's) the dense A from
+    apply() still equals the dense A^T from apply_adjoint(), same sparsity."""
+    grid, geom = tiny_grid(4, 5, 6), mirror_geometry()
+    A = projector(grid, geom)
+    assert A.info("mirror") == 1
+    m, n = grid.count, geom.ray_count
+    fwd = np.stack([A.apply(np.eye(m, dtype=np.float32)[j]) for j in range(m)], axis=1)
+    adj = np.stack([A.apply_adjoint(np.eye(n, dtype=np.float32)[i]) for i in range(n)], axis=0)
+    assert fwd.max() > 0
+    assert np.abs(fwd - adj).max() <= 1e-6 * np.abs(fwd).max()
+    assert np.array_equal(fwd > 0, adj > 0)
+    # the mirror row of every ray carries the primary's lengths, reflected
+    fw = fwd.reshape(geom.n_angles, geom.nv, geom.nu, grid.nz, grid.ny, grid.nx)
+    np.testing.assert_array_equal(fw, fw[:, ::-1, :, ::-1, :, :])
+
+
+@pytest.mark.parametrize("cfg,n_angles", [(1, 64), (2, 9), (3, 6), (4, 3)])
+def test_mirror_pairs_match_unpaired(monkeypatch, ora, cfg, n_angles):
+    """Mirror pairs on (BASELINE geometries are z-symmetric) and off
+    (KCT_MIRROR=0): both within the parity bar of the oracle and within
+    float rounding of each other."""
+    grid, geom = baseline_geometry(cfg, n_angles=n_angles)
+    rng = np.random.default_rng(53)
+    x = rng.uniform(0, 0.04, grid.count).astype(np.float32)
+    y = rng.uniform(0, 1, geom.ray_count).astype(np.float32)
+    A = projector(grid, geom)
+    assert A.info("mirror") == 1
+    monkeypatch.setenv("KCT_MIRROR", "0")
+    B = projector(grid, geom)
+    assert B.info("mirror") == 0
+    ax, bx = A.apply(x), B.apply(x)
+    aty, bty = A.apply_adjoint(y), B.apply_adjoint(y)
+    assert rel_l2(ax, bx) < 1e-6 and rel_l2(aty, bty) < 1e-6
+    assert rel_l2(ax, ora.forward(grid, geom, x)) < TOL
+    assert rel_l2(aty, ora.adjoint(grid, geom, y)) < TOL
+    assert abs(A.count_nnz() - B.count_nnz()) <= max(2, 1e-4 * B.count_nnz())
