@@ -292,6 +292,8 @@ struct __align__(16) Seg {
     int pad;
 };
 
+}  // namespace
+
 struct BrickCfg {
     int bz;  // slabs per brick (<= kMaxBz)
     int S;   // row stride of a pass
@@ -301,7 +303,11 @@ struct BrickCfg {
     size_t gstride;  // floats between the partial volumes of groups 1.. (group 0 -> out)
     int out_ref;     // 1: write `out` in the reference layout (x fastest) ...
     unsigned* level_done;  // ... and count finished bricks per z level (adjoint_host_ref)
+    int mirror;      // 1: z-mirror brick pairs (adj_mirror_kernel): bricks tile the lower half
+                     //    z < 0 (slabs [0, nz/2)), rows iv < nv/2
 };
+
+namespace {
 
 __device__ __forceinline__ float rcp_approx(float x) {
     float r;
@@ -470,6 +476,7 @@ __device__ __forceinline__ void row_segment(RowZ& r, const Seg& sg, unsigned col
 // adjoint and by the walk-table builder (bit-identical entries).
 struct BrickGeo {
     int I0, J0, K0, bxn, byn, bzn;
+    int rmax;  // last detector row that can cross the brick (z-mirror pairs: nv/2 - 1)
 };
 
 __device__ __forceinline__ int brick_walk(const ColParams& cp, const DevGeom& g, const BrickGeo& B,
@@ -505,7 +512,7 @@ __device__ __forceinline__ int brick_walk(const ColParams& cp, const DevGeom& g,
     const float dhi = n1 * (n1 >= 0.f ? rGlo : rGhi);
     const float rpv = 1.f / g.pv;
     const int rlo = max(0, (int)ceilf((dlo - g.dv0) * rpv - 1e-3f));
-    const int rhi = min(g.nv - 1, (int)floorf((dhi - g.dv0) * rpv + 1e-3f));
+    const int rhi = min(B.rmax, (int)floorf((dhi - g.dv0) * rpv + 1e-3f));
     if (rlo > rhi) return 0;
 
     // lane-parallel walk: lanes 0..7 take the interior x planes, 8..15 the y planes
@@ -789,7 +796,8 @@ __device__ __forceinline__ BrickGeo brick_geo(int brick, const BrickCfg& bc, con
     B.K0 = bk * bc.bz;
     B.bxn = min(BX, g.nx - B.I0);
     B.byn = min(BY, g.ny - B.J0);
-    B.bzn = min(bc.bz, g.nz - B.K0);
+    B.bzn = min(bc.bz, (bc.mirror ? g.nz / 2 : g.nz) - B.K0);
+    B.rmax = bc.mirror ? g.nv / 2 - 1 : g.nv - 1;
     return B;
 }
 
@@ -1036,6 +1044,314 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
             if (lane == 0) atomicAdd(bc.level_done + brick / (bc.nbx * bc.nby), 1u);
         }
     }
+    }
+}
+
+// ----------------------------------------------------------------------------
+// Adjoint, z-mirror brick pairs (the path every BASELINE geometry takes).
+//
+// In a z-mirror geometry (DevGeom::mirror, fwd_kernel MIR: offset_v = 0, nv
+// even, grid centred in z, here also nz even) detector row nv-1-iv is the
+// reflection of row iv in the plane z = 0 and slab nz-1-k that of slab k; the
+// mirror ray crosses plane nz-P exactly where the primary crosses plane P (the
+// same float values).  A work item is a pair of bricks: L = an xy brick's
+// voxel columns x slabs [K0, K0 + bzn) of the lower half (z < 0) and its
+// reflection U = slabs [nz - K0 - bzn, nz - K0).  Only primary rows (dv < 0,
+// iv < nv/2) cross L and exactly their mirrors cross U, so one classification
+// of the primary rows (slab_classify's, ks = -1) serves both bricks — each
+// slab slot holds the primary's and the mirror's weight — and one pass of the
+// slab lanes over the segments updates both bricks (U kept with its slabs in
+// slot order: slot j = slab nz-1-(K0 + j)).  Deposits are slab_deposits'
+// expressions in the same order: per voxel the result is the brick kernel's.
+// Per (entry, row) the fixed and the classification work are shared by two
+// rays; slots are the brick's own slabs (no guard slabs: a simple row outside
+// the brick deposits nothing into it).
+// Shared memory per warp (floats): accL[BX*BY][bz] | accU[BX*BY][bz] |
+// segs[kMaxSeg] (float4: wa, wb, L and U column addresses) | tXb[bz], tXa[bz]
+// (float4: crossing w, primary weight, mirror weight, 0) | tH[bz] (float2).
+// ----------------------------------------------------------------------------
+constexpr int kMirMaxBz = 32 * kSlabChunks;
+__host__ __device__ constexpr int adj_mir_floats(int bz) {
+    return (2 * BX * BY * bz + 4 * kMaxSeg + 10 * bz + 3) & ~3;
+}
+
+__device__ __forceinline__ float2 lds_f2(unsigned a) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+    return v;
+}
+
+// Classification of the primary rows rlo.. (nrows; records p = rec + rlo,
+// the mirrors' weights at pm = rec + (nv - 1 - rlo), descending) into the
+// slot tables; q / ym: the first chunk's record and mirror weight.  Slot j =
+// slab K0 + j, j < NS; tables all-zero on entry.
+__device__ __forceinline__ void mir_classify(const float4* __restrict__ p,
+                                             const float4* __restrict__ pm, float4 q, float ym,
+                                             int nrows, int rlo, float lo, float hi, float w_in,
+                                             float h1, int K0, int NS, int lane, const DevGeom& g,
+                                             unsigned tH, unsigned tXb, unsigned tXa) {
+    const float mid = 0.5f * (lo + hi) - w_in;
+    const unsigned tH0 = tH - 8u * (unsigned)K0;
+    const unsigned tXb0 = tXb - 16u * (unsigned)K0, tXa0 = tXa - 16u * (unsigned)K0;
+    p += lane;
+    pm -= lane;
+    float ivf = (float)(rlo + lane);
+    for (int b = lane; b < nrows + lane; b += 32) {
+        const float4 qc = q;
+        const float ymc = ym;
+        p += 32;
+        pm -= 32;
+        if (b + 32 < nrows) {  // next chunk
+            q = __ldg(p);
+            ym = __ldg(&pm->x);
+        }
+        const bool valid = b < nrows;
+        const int k0 = __float_as_int(qc.w) >> 2;  // primary rows: kstep -1
+        const float dvh = __fmul_rn(__fmaf_rn(ivf, g.pv, g.dv0), h1);
+        ivf += 32.f;
+        const int k = k0 + __float2int_rd(__fmaf_rn(mid, dvh, qc.y));
+        const float z1 = zcross(k, k0, qc.y, qc.z, w_in);
+        const float z2 = zcross(k + 1, k0, qc.y, qc.z, w_in);
+        const float wen = fminf(z1, z2), wlv = fmaxf(z1, z2);
+        const bool enter = wen > lo;
+        const bool leave = wlv < hi;
+        const bool cx = valid && (enter || leave);
+        // H: rows two apart never share a slab (two parity passes)
+        const bool hw = valid && !cx && (unsigned)(k - K0) < (unsigned)NS;
+        const unsigned ha = tH0 + 8u * (unsigned)k;
+        if (hw && !(lane & 1)) {
+            const float2 h = lds_f2(ha);
+            sts_f2(ha, make_float2(h.x + qc.x, h.y + ymc));
+        }
+        __syncwarp();
+        if (hw && (lane & 1)) {
+            const float2 h = lds_f2(ha);
+            sts_f2(ha, make_float2(h.x + qc.x, h.y + ymc));
+        }
+        if (cx) {
+            const int kb = enter ? k + 1 : k, ka = enter ? k : k - 1;
+            const float4 xv = make_float4(enter ? wen : wlv, qc.x, ymc, 0.f);
+            if ((unsigned)(kb - K0) < (unsigned)NS) sts_f4(tXb0 + 16u * (unsigned)kb, xv);
+            if ((unsigned)(ka - K0) < (unsigned)NS) sts_f4(tXa0 + 16u * (unsigned)ka, xv);
+        }
+        __syncwarp();
+    }
+}
+
+// Deposits of one entry into both bricks, lanes = slots j = lane + 32 r;
+// clears the tables.
+template <int RC>
+__device__ __forceinline__ void mir_deposits(const float4* segs, int nseg, int NS, int lane,
+                                             unsigned tH, unsigned tXb, unsigned tXa) {
+    float hL[RC], hU[RC], bw[RC], byL[RC], byU[RC], aw[RC], ayL[RC], ayU[RC];
+    unsigned off[RC];
+    bool xs[RC], on[RC];
+#pragma unroll
+    for (int r = 0; r < RC; ++r) {
+        const int j = lane + 32 * r;
+        on[r] = j < NS;
+        float2 h = make_float2(0.f, 0.f);
+        float4 xb = make_float4(0.f, 0.f, 0.f, 0.f), xa = xb;
+        if (on[r]) {
+            h = lds_f2(tH + 8u * j);
+            xb = lds_f4(tXb + 16u * j);
+            xa = lds_f4(tXa + 16u * j);
+            sts_f2(tH + 8u * j, make_float2(0.f, 0.f));
+            sts_f4(tXb + 16u * j, make_float4(0.f, 0.f, 0.f, 0.f));
+            sts_f4(tXa + 16u * j, make_float4(0.f, 0.f, 0.f, 0.f));
+        }
+        hL[r] = h.x;
+        hU[r] = h.y;
+        bw[r] = xb.x;
+        byL[r] = xb.y;
+        byU[r] = xb.z;
+        aw[r] = xa.x;
+        ayL[r] = xa.y;
+        ayU[r] = xa.z;
+        off[r] = 4u * (unsigned)j;
+        xs[r] = __any_sync(kFull, xb.y != 0.f || xa.y != 0.f || xb.z != 0.f || xa.z != 0.f);
+    }
+    for (int sgi = 0; sgi < nseg; ++sgi) {
+        const float4 sg = segs[sgi];
+        const float wa = sg.x, wb = sg.y;
+        const unsigned bL = __float_as_uint(sg.z), bU = __float_as_uint(sg.w);
+        const float d = wb - wa;
+        float vL[RC], vU[RC];
+#pragma unroll
+        for (int r = 0; r < RC; ++r) {
+            vL[r] = on[r] ? lds_f(bL + off[r]) : 0.f;
+            vU[r] = on[r] ? lds_f(bU + off[r]) : 0.f;
+        }
+#pragma unroll
+        for (int r = 0; r < RC; ++r) {
+            float dL, dU;
+            if (xs[r]) {
+                const float tb = fminf(fmaxf(bw[r], wa), wb) - wa;
+                const float ta = wb - fminf(fmaxf(aw[r], wa), wb);
+                dL = __fmaf_rn(d, hL[r], __fmaf_rn(tb, byL[r], ta * ayL[r]));
+                dU = __fmaf_rn(d, hU[r], __fmaf_rn(tb, byU[r], ta * ayU[r]));
+            } else {
+                dL = __fmul_rn(d, hL[r]);
+                dU = __fmul_rn(d, hU[r]);
+            }
+            vL[r] += dL;
+            vU[r] += dU;
+        }
+#pragma unroll
+        for (int r = 0; r < RC; ++r)
+            if (on[r]) {
+                sts_f(bL + off[r], vL[r]);
+                sts_f(bU + off[r], vU[r]);
+            }
+    }
+    __syncwarp();
+}
+
+#ifndef KCT_MIR_MINB
+#define KCT_MIR_MINB 20  // 11 KB of shared memory per warp at 64-slab bricks: <= 20 warps per SM
+#endif
+__global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
+    const float4* __restrict__ rec, float* __restrict__ out, DevGeom g, BrickCfg bc, int a0,
+    int nab, int accumulate, const int* __restrict__ order, int* queue,
+    float* __restrict__ out_part, const WalkEntry* __restrict__ tab,
+    const unsigned long long* __restrict__ off) {
+    extern __shared__ float sm[];
+    const int lane = threadIdx.x & 31;
+    const int nbricks = bc.nbx * bc.nby * bc.nbz;
+    const int CS = bc.bz;
+    const int nu = g.nu, nv = g.nv, nz = g.nz;
+    float* accL = sm;
+    float* accU = sm + BX * BY * CS;
+    float4* segs = reinterpret_cast<float4*>(sm + 2 * BX * BY * CS);
+    const unsigned accL_s = (unsigned)__cvta_generic_to_shared(accL);
+    const unsigned accU_s = accL_s + 4u * (unsigned)(BX * BY * CS);
+    const unsigned tXb = accL_s + 4u * (unsigned)(2 * BX * BY * CS + 4 * kMaxSeg);
+    const unsigned tXa = tXb + 16u * (unsigned)CS;
+    const unsigned tH = tXa + 16u * (unsigned)CS;
+    const int nitems = nbricks * bc.ngrp;
+    int ticket = queue ? 0 : blockIdx.x;
+    for (;;) {
+        int item;
+        if (queue) {
+            int tk = 0;
+            if (lane == 0) tk = atomicAdd(queue, 1);
+            tk = __shfl_sync(kFull, tk, 0);
+            if (tk >= nitems) break;
+            item = tk;
+        } else {
+            if (ticket >= nitems) break;
+            item = ticket;
+            ticket = nitems;
+        }
+        const int grp = item % bc.ngrp;
+        const int brick = queue ? order[item / bc.ngrp] : item / bc.ngrp;
+        const int a_lo = (int)((long long)nab * grp / bc.ngrp);
+        const int a_hi = (int)((long long)nab * (grp + 1) / bc.ngrp);
+        float* const dst = grp == 0 ? out : out_part + (size_t)(grp - 1) * bc.gstride;
+        const int acc_in = grp == 0 ? accumulate : 0;
+        const BrickGeo B = brick_geo(brick, bc, g);
+        const int K0 = B.K0, NS = B.bzn;
+        for (int q = lane; q < (2 * BX * BY * CS) / 4; q += 32)
+            reinterpret_cast<float4*>(sm)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int j = lane; j < CS; j += 32) {
+            sts_f2(tH + 8u * j, make_float2(0.f, 0.f));
+            sts_f4(tXb + 16u * j, make_float4(0.f, 0.f, 0.f, 0.f));
+            sts_f4(tXa + 16u * j, make_float4(0.f, 0.f, 0.f, 0.f));
+        }
+        __syncwarp();
+
+        const unsigned long long* ob = off + (size_t)brick * (g.na + 1);
+        const unsigned long long e0 = ob[a0 + a_lo], e1 = ob[a0 + a_hi];
+        const unsigned* tw = reinterpret_cast<const unsigned*>(tab);
+        constexpr int M = kNB + kNB / 4;  // first meta word
+        auto ld_entry = [&](unsigned long long e) {
+            return (e < e1 && lane < kEW) ? __ldg(tw + e * kEW + lane) : 0u;
+        };
+        const unsigned boff = (unsigned)a0 * (unsigned)nu * (unsigned)nv;
+        // the first row chunk's records (and mirror weights) of entry e
+        auto first_chunk = [&](unsigned we, unsigned long long e, float& ymo) {
+            const unsigned ro = __shfl_sync(kFull, we, M), r = __shfl_sync(kFull, we, M + 1);
+            const int rl = (int)(r & 0xffffu), n = (int)(r >> 16) - rl + 1;
+            const bool ok = e < e1 && lane < n;
+            const unsigned base = ro - boff;
+            ymo = ok ? __ldg(&rec[base + (unsigned)(nv - 1 - rl - lane)].x) : 0.f;
+            return ok ? __ldg(rec + (base + (unsigned)(rl + lane))) : make_float4(0.f, 0.f, 0.f, 0.f);
+        };
+        unsigned w = ld_entry(e0), w1 = ld_entry(e0 + 1);
+        float ym;
+        float4 q = first_chunk(w, e0, ym);
+        for (unsigned long long e = e0; e < e1; ++e) {
+            const unsigned ijw1 = __shfl_sync(kFull, w, M - 1);
+            const int nseg = (int)(ijw1 >> 24);
+            const unsigned rr = __shfl_sync(kFull, w, M + 1);
+            const float wa = __uint_as_float(__shfl_sync(kFull, w, lane & (kNB - 1)));
+            const float wb = __uint_as_float(__shfl_sync(kFull, w, (lane + 1) & (kNB - 1)));
+            const unsigned ijw = __shfl_sync(kFull, w, kNB + ((lane >> 2) & (kNB / 4 - 1)));
+            const float lo = __uint_as_float(__shfl_sync(kFull, w, 0));
+            const float hi = __uint_as_float(__shfl_sync(kFull, w, nseg & (kNB - 1)));
+            const unsigned ro = __shfl_sync(kFull, w, M);
+            const float w_in = __uint_as_float(__shfl_sync(kFull, w, M + 2));
+            const float inv_h1 = __uint_as_float(__shfl_sync(kFull, w, M + 3));
+            if (lane < nseg) {
+                const unsigned ij = (ijw >> (8 * (lane & 3))) & 0xffu;
+                const unsigned cb = 4u * ij * (unsigned)CS;
+                segs[lane] = make_float4(wa, wb, __uint_as_float(accL_s + cb), __uint_as_float(accU_s + cb));
+            }
+            const unsigned w2 = ld_entry(e + 2);
+            float ym1;
+            const float4 q1 = first_chunk(w1, e + 1, ym1);
+            __syncwarp();
+            const int rlo = (int)(rr & 0xffffu), rhi = (int)(rr >> 16);
+            const float4* rc = rec + (ro - boff);
+            mir_classify(rc + rlo, rc + (nv - 1 - rlo), q, ym, rhi - rlo + 1, rlo, lo, hi, w_in,
+                         rcp_approx(inv_h1), K0, NS, lane, g, tH, tXb, tXa);
+            switch ((NS + 31) >> 5) {
+            case 1: mir_deposits<1>(segs, nseg, NS, lane, tH, tXb, tXa); break;
+            case 2: mir_deposits<2>(segs, nseg, NS, lane, tH, tXb, tXa); break;
+            case 3: mir_deposits<3>(segs, nseg, NS, lane, tH, tXb, tXa); break;
+            default: mir_deposits<4>(segs, nseg, NS, lane, tH, tXb, tXa); break;
+            }
+            w = w1;
+            w1 = w2;
+            q = q1;
+            ym = ym1;
+        }
+        if (!bc.out_ref) {
+            // coalesced runs of the bricks' slabs per voxel column (U reversed)
+            for (int c = 0; c < B.bxn * B.byn; ++c) {
+                const int ci = c % B.bxn, cj = c / B.bxn;
+                float* o = dst + ((size_t)(B.I0 + ci) + (size_t)g.nx * (B.J0 + cj)) * nz;
+                const float* aL = accL + (ci + BX * cj) * CS;
+                const float* aU = accU + (ci + BX * cj) * CS;
+                for (int kk = lane; kk < NS; kk += 32) {
+                    float* oL = o + K0 + kk;
+                    float* oU = o + (nz - 1 - K0 - kk);
+                    *oL = acc_in ? *oL + aL[kk] : aL[kk];
+                    *oU = acc_in ? *oU + aU[kk] : aU[kk];
+                }
+            }
+            __syncwarp();
+        } else {
+            // reference layout (x fastest), lanes over the voxel columns then slabs
+            const int ncol = BX * BY;
+            for (int t = lane; t < ncol * NS; t += 32) {
+                const int c = t % ncol, kk = t / ncol;
+                const int ci = c % BX, cj = c / BX;
+                if (ci < B.bxn && cj < B.byn) {
+                    const size_t xy = (size_t)(B.I0 + ci) + (size_t)g.nx * (B.J0 + cj);
+                    const size_t plane = (size_t)g.nx * g.ny;
+                    float* oL = dst + xy + plane * (size_t)(K0 + kk);
+                    float* oU = dst + xy + plane * (size_t)(nz - 1 - K0 - kk);
+                    *oL = acc_in ? *oL + accL[c * CS + kk] : accL[c * CS + kk];
+                    *oU = acc_in ? *oU + accU[c * CS + kk] : accU[c * CS + kk];
+                }
+            }
+            if (bc.level_done) {
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) atomicAdd(bc.level_done + brick / (bc.nbx * bc.nby), 1u);
+            }
+        }
     }
 }
 
@@ -1557,7 +1873,6 @@ void Projector::build_tables(const kct_geometry& geom) {
         KCT_CUDA(cudaMalloc(&d_rows_, nv * sizeof(RowTab)));
         KCT_CUDA(cudaMemcpy(d_rows_, rt.data(), nv * sizeof(RowTab), cudaMemcpyHostToDevice));
     }
-    const size_t smem = adj_smem_bytes();
     // the attribute is per function, not per handle: set it to the largest
     // brick any projector can use, so handles with taller bricks coexist
     const int smem_max = (int)((size_t)kAdjWarps * adj_warp_floats(kMaxBz) * sizeof(float));
@@ -1565,17 +1880,40 @@ void Projector::build_tables(const kct_geometry& geom) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
     KCT_CUDA(cudaFuncSetAttribute(adj_brick_kernel<true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+    KCT_CUDA(cudaFuncSetAttribute(adj_mirror_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(adj_mir_floats(kMirMaxBz) * sizeof(float))));
 
+    // z-mirror brick pairs (adj_mirror_kernel): z-mirror geometry, slab-lane
+    // conditions, nz even; bricks of <= 64 slabs tiling the lower half
+    // (KCT_ADJ_MIR_BZ: another maximum height, <= 128; KCT_ADJ_MIRROR=0: off)
+    {
+        const char* e = std::getenv("KCT_ADJ_MIRROR");
+        adj_mir_ = mirror_ && adj_slab_ && !adj_gather_ && nz % 2 == 0 && kTabOk &&
+                   !(e && e[0] == '0');
+        int hmax = 64;
+        if (const char* h = std::getenv("KCT_ADJ_MIR_BZ")) hmax = std::clamp(std::atoi(h), 1, kMirMaxBz);
+        const int half = nz / 2, nbh = (half + hmax - 1) / std::max(1, hmax);
+        adj_mbz_ = std::max(1, (half + nbh - 1) / std::max(1, nbh));
+    }
+
+    KCT_CUDA(cudaMalloc(&d_cs_, cs_.size() * sizeof(float2)));
+    KCT_CUDA(cudaMemcpy(d_cs_, cs_.data(), cs_.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    build_walk_table();
+    if (!d_tab_) adj_mir_ = false;  // the pair kernel streams the walk table
+
+    const BrickCfg bcfg = adj_cfg();
+    const long nb = (long)bcfg.nbx * bcfg.nby * bcfg.nbz;
     // angle groups for problems with few bricks (see adj_brick_kernel); a
     // function of the problem size only, so results do not depend on the device
     {
-        const long nb = (long)((nx + BX - 1) / BX) * ((ny + BY - 1) / BY) * ((nz + adj_bz_ - 1) / adj_bz_);
         const int amax = std::min(na, kMaxAnglesPerLaunch);
         // one item per brick once the bricks fill a 148-SM B200 twice (measured:
         // c3's 12288 bricks run 3% faster undivided); otherwise ~4 items per
-        // resident warp (c2, slabs of multi-GPU shards, c1)
+        // resident warp (c2, slabs of multi-GPU shards, c1); a brick pair
+        // counts as two bricks
         constexpr long kWarpSlots = 148 * 32;
-        int G = nb >= 2 * kWarpSlots ? 1 : (int)std::min<long>(16, (4 * kWarpSlots + nb - 1) / nb);
+        const long nbw = adj_mir_ ? 2 * nb : nb;
+        int G = nbw >= 2 * kWarpSlots ? 1 : (int)std::min<long>(16, (4 * kWarpSlots + nbw - 1) / nbw);
         if (const char* e = std::getenv("KCT_ADJ_GROUPS")) G = std::max(1, std::atoi(e));
         G = std::max(1, std::min(G, amax));
         // partial volumes: (G - 1) x M floats, capped at 2 GiB
@@ -1593,36 +1931,52 @@ void Projector::build_tables(const kct_geometry& geom) {
     // distance from the mid-plane: central bricks are crossed by the most rays)
     const char* sched = std::getenv("KCT_ADJ_SCHED");
     if (!adj_gather_ && !(sched && std::string(sched) == "static")) {
-        const int nbx = (nx + BX - 1) / BX, nby = (ny + BY - 1) / BY;
-        const int nbz = (nz + adj_bz_ - 1) / adj_bz_;
-        const int nb = nbx * nby * nbz;
+        const int nbx = bcfg.nbx, nby = bcfg.nby;
         std::vector<std::pair<double, int>> key(nb);
         const char* zo = std::getenv("KCT_ADJ_ORDER");
         const bool z_major = !(zo && std::string(zo) == "radius");
-        for (int b = 0; b < nb; ++b) {
+        for (int b = 0; b < (int)nb; ++b) {
             const int bi = b % nbx, bj = (b / nbx) % nby, bk = b / (nbx * nby);
             const double cx = ox + (bi + 0.5) * BX * sx, cy = oy + (bj + 0.5) * BY * sy;
-            const double cz = grid_.oz + (bk + 0.5) * adj_bz_ * sz;
+            const double cz = grid_.oz + (bk + 0.5) * bcfg.bz * sz;
             key[b] = {std::hypot(cx, cy) + 1e-3 * std::fabs(cz), b};
             // z levels in turn: the detector rows they read stay in L2 (c4 -1%)
             if (z_major) key[b].first += 1e6 * bk;
         }
         std::stable_sort(key.begin(), key.end());
         std::vector<int> order(nb);
-        for (int b = 0; b < nb; ++b) order[b] = key[b].second;
+        for (int b = 0; b < (int)nb; ++b) order[b] = key[b].second;
         KCT_CUDA(cudaMalloc(&d_border_, nb * sizeof(int)));
         KCT_CUDA(cudaMemcpy(d_border_, order.data(), nb * sizeof(int), cudaMemcpyHostToDevice));
         KCT_CUDA(cudaMalloc(&d_queue_, sizeof(int)));
         int per_sm = 0, sms = 0;
-        KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_brick_kernel<true>,
-                                                               kAdjWarps * 32, smem));
+        if (adj_mir_)
+            KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_mirror_kernel, 32,
+                                                                   adj_smem_bytes()));
+        else
+            KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_brick_kernel<true>,
+                                                                   kAdjWarps * 32, adj_smem_bytes()));
         KCT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
         adj_ctas_ = std::max(1, per_sm) * std::max(1, sms);
     }
+}
 
-    KCT_CUDA(cudaMalloc(&d_cs_, cs_.size() * sizeof(float2)));
-    KCT_CUDA(cudaMemcpy(d_cs_, cs_.data(), cs_.size() * sizeof(float2), cudaMemcpyHostToDevice));
-    build_walk_table();
+// Brick configuration of the adjoint (and of its walk table): standard
+// bricks of adj_bz_ slabs tiling [0, nz), or (adj_mir_) z-mirror pairs whose
+// lower bricks of adj_mbz_ slabs tile [0, nz/2).
+BrickCfg Projector::adj_cfg() const {
+    BrickCfg bc{};
+    bc.mirror = adj_mir_ ? 1 : 0;
+    bc.bz = adj_mir_ ? adj_mbz_ : adj_bz_;
+    bc.S = adj_S_;
+    bc.slab = adj_slab_ ? (adj_slab_detect_ && !adj_mir_ ? 2 : 1) : 0;
+    bc.nbx = (dg_.nx + BX - 1) / BX;
+    bc.nby = (dg_.ny + BY - 1) / BY;
+    const int zext = adj_mir_ ? dg_.nz / 2 : dg_.nz;
+    bc.nbz = (zext + bc.bz - 1) / bc.bz;
+    bc.ngrp = adj_groups_;
+    bc.gstride = m_;
+    return bc;
 }
 
 // Walk table (adj_walk_build): the xy part of every (brick, angle, column) of
@@ -1640,13 +1994,7 @@ void Projector::build_walk_table() {
     KCT_CUDA(cudaMemGetInfo(&free_b, &total_b));
     size_t budget = free_b / 4;
     if (const char* e = std::getenv("KCT_ADJ_TABLE_MB")) budget = (size_t)std::atoll(e) << 20;
-    BrickCfg bc{};
-    bc.bz = adj_bz_;
-    bc.S = adj_S_;
-    bc.slab = adj_slab_ ? (adj_slab_detect_ ? 2 : 1) : 0;
-    bc.nbx = (dg_.nx + BX - 1) / BX;
-    bc.nby = (dg_.ny + BY - 1) / BY;
-    bc.nbz = (dg_.nz + adj_bz_ - 1) / adj_bz_;
+    BrickCfg bc = adj_cfg();
     bc.ngrp = 1;
     const size_t nb = (size_t)bc.nbx * bc.nby * bc.nbz;
     const size_t noff = nb * (dg_.na + 1);
@@ -1683,6 +2031,7 @@ void Projector::build_walk_table() {
 }
 
 size_t Projector::adj_smem_bytes() const {
+    if (adj_mir_) return (size_t)adj_mir_floats(adj_mbz_) * sizeof(float);
     return (size_t)kAdjWarps * adj_warp_floats(adj_bz_) * sizeof(float);
 }
 
@@ -1915,15 +2264,7 @@ void Projector::adjoint_impl(const float* proj, float* vol, int a_begin, int a_e
                              bool accumulate, bool out_ref, unsigned* level_done,
                              cudaStream_t s) const {
     AngleBatch ab;
-    BrickCfg bc;
-    bc.bz = adj_bz_;
-    bc.S = adj_S_;
-    bc.slab = adj_slab_ ? (adj_slab_detect_ ? 2 : 1) : 0;
-    bc.nbx = (dg_.nx + BX - 1) / BX;
-    bc.nby = (dg_.ny + BY - 1) / BY;
-    bc.nbz = (dg_.nz + adj_bz_ - 1) / adj_bz_;
-    bc.ngrp = adj_groups_;
-    bc.gstride = m_;
+    BrickCfg bc = adj_cfg();
     bc.out_ref = out_ref ? 1 : 0;
     bc.level_done = level_done;
     const int nctas = (bc.nbx * bc.nby * bc.nbz * bc.ngrp + kAdjWarps - 1) / kAdjWarps;
@@ -1952,7 +2293,11 @@ void Projector::adjoint_impl(const float* proj, float* vol, int a_begin, int a_e
         } else {
             if (d_queue_) KCT_CUDA(cudaMemsetAsync(d_queue_, 0, sizeof(int), s));
             const unsigned grid = d_queue_ ? std::min(nctas, adj_ctas_) : nctas;
-            if (d_tab_)
+            if (adj_mir_)
+                adj_mirror_kernel<<<grid, 32, smem, s>>>(
+                    reinterpret_cast<const float4*>(d_yw_), vol, dg_, bc, a0, nab, accum, d_border_,
+                    d_queue_, d_part_, static_cast<const WalkEntry*>(d_tab_), d_off_);
+            else if (d_tab_)
                 adj_brick_kernel<true><<<grid, kAdjWarps * 32, smem, s>>>(
                     reinterpret_cast<const float4*>(d_yw_), vol, cols, dg_, bc, d_cs_ + a0, a0, nab, accum, d_border_,
                     d_queue_, d_part_, static_cast<const WalkEntry*>(d_tab_), d_off_);
@@ -2006,7 +2351,8 @@ bool Projector::adjoint_host_ref(const float* host_proj, float* host, cudaStream
     if (e && e[0] == '0') return false;
     if (adj_gather_ || adj_groups_ > 1 || dg_.na > kMaxAnglesPerLaunch || !d_queue_ || !wait_value32())
         return false;
-    const int nbz = (dg_.nz + adj_bz_ - 1) / adj_bz_;
+    const BrickCfg bcfg = adj_cfg();
+    const int nbz = bcfg.nbz;
     const unsigned per_level =
         (unsigned)(((dg_.nx + BX - 1) / BX) * ((dg_.ny + BY - 1) / BY));
     if (!d_level_) KCT_CUDA(cudaMalloc(&d_level_, (size_t)nbz * sizeof(unsigned)));
@@ -2050,9 +2396,16 @@ bool Projector::adjoint_host_ref(const float* host_proj, float* host, cudaStream
             KCT_CUDA(cudaMemcpy(host, dev, m_ * sizeof(float), cudaMemcpyDeviceToHost));
             return true;
         }
-        const size_t k0 = (size_t)L * adj_bz_, k1 = std::min((size_t)dg_.nz, k0 + adj_bz_);
+        // level L: slabs [k0, k1) (z-mirror pairs: and their reflection)
+        const size_t zext = adj_mir_ ? dg_.nz / 2 : dg_.nz;
+        const size_t k0 = (size_t)L * bcfg.bz, k1 = std::min(zext, k0 + bcfg.bz);
         KCT_CUDA(cudaMemcpyAsync(host + k0 * plane, dev + k0 * plane, (k1 - k0) * plane * sizeof(float),
                                  cudaMemcpyDeviceToHost, sc));
+        if (adj_mir_) {
+            const size_t u0 = dg_.nz - k1;
+            KCT_CUDA(cudaMemcpyAsync(host + u0 * plane, dev + u0 * plane, (k1 - k0) * plane * sizeof(float),
+                                     cudaMemcpyDeviceToHost, sc));
+        }
     }
     KCT_CUDA(cudaStreamSynchronize(sc));
     KCT_CUDA(cudaStreamSynchronize(s));

@@ -13,6 +13,8 @@
 
 namespace kct {
 
+struct BrickCfg;  // adjoint brick configuration (projector.cu)
+
 class Projector {
   public:
     Projector(const kct_grid& grid, const kct_geometry& geom, int device);
@@ -112,12 +114,15 @@ class Projector {
     bool adj_gather() const { return adj_gather_; }
     bool adj_slab() const { return adj_slab_; }
     bool adj_slab_detect() const { return adj_slab_detect_; }
+    bool adj_mirror() const { return adj_mir_; }
+    int adj_mirror_bz() const { return adj_mbz_; }
     int adj_groups() const { return adj_groups_; }
     unsigned long long walk_entries() const { return tab_entries_; }
 
   private:
     void build_tables(const kct_geometry& geom);
     size_t adj_smem_bytes() const;
+    BrickCfg adj_cfg() const;
     void build_walk_table();
     void adjoint_impl(const float* proj, float* vol, int a_begin, int a_end, bool accumulate,
                       bool out_ref, unsigned* level_done, cudaStream_t s) const;
@@ -139,6 +144,8 @@ class Projector {
     bool adj_gather_ = false;
     bool adj_slab_ = false;           // slab-lane adjoint deposits valid (brick_rows_slab)
     bool adj_slab_detect_ = false;    // ... with crossing-slot conflict detection
+    bool adj_mir_ = false;            // z-mirror brick pairs (adj_mirror_kernel)
+    int adj_mbz_ = 64;                // ... slabs per lower brick
     int* d_border_ = nullptr;         // brick order of the adjoint queue
     int* d_forder_ = nullptr;         // forward block -> item order (longest chords first)
     int* d_fpipe_ = nullptr;          // the same per pipeline chunk (offsets pipe_off_)

@@ -294,7 +294,9 @@ def test_projector_info_reports_paths():
     A = projector(*baseline_geometry(3, n_angles=16))
     assert A.info("adj_slab") == 1 and A.info("adj_gather") == 0
     assert A.info("mirror") == 1
-    assert A.info("adj_bz") == 86 and A.info("fwd_rows_per_warp") == 192
+    # z-mirror brick pairs: lower bricks of 64 slabs tiling z < 0
+    assert A.info("adj_mirror") == 1 and A.info("adj_bz") == 64
+    assert A.info("fwd_rows_per_warp") == 192
     lo, hi = A.info("fwd_split_lo"), A.info("fwd_split_z")
     assert 0 < lo < 128 < hi < 256 and lo + hi == 256
     assert A.info("adj_walk_entries") > 0
@@ -378,19 +380,26 @@ def test_out_argument_validation():
 @pytest.mark.parametrize("how", ["KCT_ADJ_TABLE=0", "KCT_ADJ_TABLE_MB=1"])
 def test_walk_table_fallback(monkeypatch, ora, cfg, n_angles, how):
     """Without the precomputed walk table (disabled, or over the memory budget)
-    the adjoint recomputes the walks on the fly: same parity bar, and
-    bit-identical to the table path (same walk, same deposits)."""
+    the adjoint recomputes the walks on the fly (standard bricks: the brick
+    pairs stream the table): same parity bar, bit-identical to the standard
+    bricks' table path (same walk, same deposits) and within float rounding of
+    the brick-pair path."""
     grid, geom = baseline_geometry(cfg, n_angles=n_angles)
     y = np.random.default_rng(41).uniform(0, 1, geom.ray_count).astype(np.float32)
+    pairs = projector(grid, geom)
+    assert pairs.info("adj_walk_entries") > 0 and pairs.info("adj_mirror") == 1
+    monkeypatch.setenv("KCT_ADJ_MIRROR", "0")
     with_tab = projector(grid, geom)
-    assert with_tab.info("adj_walk_entries") > 0
+    assert with_tab.info("adj_walk_entries") > 0 and with_tab.info("adj_mirror") == 0
     key, val = how.split("=")
     monkeypatch.setenv(key, val)
+    monkeypatch.delenv("KCT_ADJ_MIRROR")
     A = projector(grid, geom)
-    assert A.info("adj_walk_entries") == 0
+    assert A.info("adj_walk_entries") == 0 and A.info("adj_mirror") == 0
     got = A.apply_adjoint(y)
     assert np.array_equal(got, A.apply_adjoint(y))
     assert np.array_equal(got, with_tab.apply_adjoint(y))
+    assert rel_l2(got, pairs.apply_adjoint(y)) < 1e-6
     assert rel_l2(got, ora.adjoint(grid, geom, y)) < TOL
 
 
@@ -417,9 +426,19 @@ def test_c4_slot_conflict_path(ora, n_angles):
     detection is on (adj_slab_detect) — checked against the oracle over several
     views, not one."""
     grid, geom = baseline_geometry(4, n_angles=n_angles)
-    A = projector(grid, geom)
-    assert A.info("adj_slab") == 1 and A.info("adj_slab_detect") == 1
     y = np.random.default_rng(43).uniform(0, 1, geom.ray_count).astype(np.float32)
+    # (brick pairs have no conflicts: primary and mirror rows fill separate
+    # bricks; the standard bricks detect them)
+    pairs = projector(grid, geom)
+    assert pairs.info("adj_mirror") == 1
+    assert rel_l2(pairs.apply_adjoint(y), ora.adjoint(grid, geom, y)) < TOL
+    import os
+    os.environ["KCT_ADJ_MIRROR"] = "0"
+    try:
+        A = projector(grid, geom)
+    finally:
+        del os.environ["KCT_ADJ_MIRROR"]
+    assert A.info("adj_slab") == 1 and A.info("adj_slab_detect") == 1
     assert rel_l2(A.apply_adjoint(y), ora.adjoint(grid, geom, y)) < TOL
 
 
@@ -467,3 +486,61 @@ def test_mirror_pairs_match_unpaired(monkeypatch, ora, cfg, n_angles):
     assert rel_l2(ax, ora.forward(grid, geom, x)) < TOL
     assert rel_l2(aty, ora.adjoint(grid, geom, y)) < TOL
     assert abs(A.count_nnz() - B.count_nnz()) <= max(2, 1e-4 * B.count_nnz())
+
+
+def test_mirror_brick_pairs_exact_transpose(monkeypatch):
+    """test_projector.cpp:77-85 on the z-mirror brick-pair adjoint
+    (adj_mirror_kernel: one classification of the primary rows feeds both
+    bricks of a pair): dense A^T equals dense A, same sparsity, and the mirror
+    rows carry the primary's lengths reflected."""
+    monkeypatch.setenv("KCT_ADJ_SLAB", "force")
+    grid, geom = slab_geometry(n_angles=4)
+    A = projector(grid, geom)
+    assert A.info("mirror") == 1 and A.info("adj_mirror") == 1
+    m, n = grid.count, geom.ray_count
+    fwd = np.stack([A.apply(np.eye(m, dtype=np.float32)[j]) for j in range(m)], axis=1)
+    adj = np.stack([A.apply_adjoint(np.eye(n, dtype=np.float32)[i]) for i in range(n)], axis=0)
+    assert fwd.max() > 0
+    assert np.abs(fwd - adj).max() <= 1e-6 * np.abs(fwd).max()
+    assert np.array_equal(fwd > 0, adj > 0)
+    aw = adj.reshape(geom.n_angles, geom.nv, geom.nu, grid.nz, grid.ny, grid.nx)
+    np.testing.assert_array_equal(aw, aw[:, ::-1, :, ::-1, :, :])
+
+
+@pytest.mark.parametrize("cfg,n_angles", [(1, 64), (2, 9), (3, 6), (4, 2), (5, 5)])
+@pytest.mark.parametrize("bz", ["64", "43", "128"])
+def test_mirror_brick_pairs_match_standard_bricks(monkeypatch, ora, cfg, n_angles, bz):
+    """Brick pairs (default) against the standard bricks (KCT_ADJ_MIRROR=0) and
+    the oracle, at the default and other pair heights (KCT_ADJ_MIR_BZ: 43 ->
+    uneven splits, 128 -> four slab chunks); bit-reproducible."""
+    grid, geom = baseline_geometry(cfg, n_angles=n_angles)
+    y = np.random.default_rng(61).uniform(0, 1, geom.ray_count).astype(np.float32)
+    monkeypatch.setenv("KCT_ADJ_MIR_BZ", bz)
+    A = projector(grid, geom)
+    assert A.info("adj_mirror") == 1
+    assert A.info("adj_bz") == -(-(grid.nz // 2) // -(-(grid.nz // 2) // int(bz)))
+    got = A.apply_adjoint(y)
+    assert np.array_equal(got, A.apply_adjoint(y))
+    monkeypatch.setenv("KCT_ADJ_MIRROR", "0")
+    std = projector(grid, geom).apply_adjoint(y)
+    assert rel_l2(got, std) < 1e-6
+    if bz == "64":
+        assert rel_l2(got, ora.adjoint(grid, geom, y)) < TOL
+
+
+def test_mirror_brick_pairs_host_and_groups(monkeypatch):
+    """The brick pairs' host path (reference layout written by the kernel, z
+    levels copied out pairwise) and angle groups give the device result."""
+    import torch
+    grid, geom = baseline_geometry(3, n_angles=16)
+    A = projector(grid, geom)
+    assert A.info("adj_mirror") == 1
+    y = np.random.default_rng(71).uniform(0, 1, geom.ray_count).astype(np.float32)
+    host = A.apply_adjoint(y)
+    yd = A.proj_to_native(torch.from_numpy(y).cuda())
+    dev = A.volume_from_native(A.apply_adjoint(yd)).cpu().numpy()
+    assert rel_l2(host, dev) < 1e-6
+    monkeypatch.setenv("KCT_ADJ_GROUPS", "3")
+    B = projector(grid, geom)
+    assert B.info("adj_groups") == 3
+    assert rel_l2(B.apply_adjoint(y), dev) < 1e-6
