@@ -1075,12 +1075,6 @@ __host__ __device__ constexpr int adj_mir_floats(int bz) {
     return (2 * BX * BY * bz + 4 * kMaxSeg + 10 * bz + 3) & ~3;
 }
 
-__device__ __forceinline__ float2 lds_f2(unsigned a) {
-    float2 v;
-    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
-    return v;
-}
-
 // Classification of the primary rows rlo.. (nrows; records p = rec + rlo,
 // the mirrors' weights at pm = rec + (nv - 1 - rlo), descending) into the
 // slot tables; q / ym: the first chunk's record and mirror weight.  Slot j =
@@ -1089,10 +1083,11 @@ __device__ __forceinline__ void mir_classify(const float4* __restrict__ p,
                                              const float4* __restrict__ pm, float4 q, float ym,
                                              int nrows, int rlo, float lo, float hi, float w_in,
                                              float h1, int K0, int NS, int lane, const DevGeom& g,
-                                             unsigned tH, unsigned tXb, unsigned tXa) {
+                                             float2* tH, float4* tXb, float4* tXa) {
     const float mid = 0.5f * (lo + hi) - w_in;
-    const unsigned tH0 = tH - 8u * (unsigned)K0;
-    const unsigned tXb0 = tXb - 16u * (unsigned)K0, tXa0 = tXa - 16u * (unsigned)K0;
+    tH -= K0;  // slot of slab k at tH[k]
+    tXb -= K0;
+    tXa -= K0;
     p += lane;
     pm -= lane;
     float ivf = (float)(rlo + lane);
@@ -1118,33 +1113,32 @@ __device__ __forceinline__ void mir_classify(const float4* __restrict__ p,
         const bool cx = valid && (enter || leave);
         // H: rows two apart never share a slab (two parity passes)
         const bool hw = valid && !cx && (unsigned)(k - K0) < (unsigned)NS;
-        const unsigned ha = tH0 + 8u * (unsigned)k;
         if (hw && !(lane & 1)) {
-            const float2 h = lds_f2(ha);
-            sts_f2(ha, make_float2(h.x + qc.x, h.y + ymc));
+            const float2 h = tH[k];
+            tH[k] = make_float2(h.x + qc.x, h.y + ymc);
         }
         __syncwarp();
         if (hw && (lane & 1)) {
-            const float2 h = lds_f2(ha);
-            sts_f2(ha, make_float2(h.x + qc.x, h.y + ymc));
+            const float2 h = tH[k];
+            tH[k] = make_float2(h.x + qc.x, h.y + ymc);
         }
-        if (cx) {
-            const int kb = enter ? k + 1 : k, ka = enter ? k : k - 1;
-            const float4 xv = make_float4(enter ? wen : wlv, qc.x, ymc, 0.f);
-            if ((unsigned)(kb - K0) < (unsigned)NS) sts_f4(tXb0 + 16u * (unsigned)kb, xv);
-            if ((unsigned)(ka - K0) < (unsigned)NS) sts_f4(tXa0 + 16u * (unsigned)ka, xv);
-        }
+        const int kb = enter ? k + 1 : k, ka = enter ? k : k - 1;
+        const float4 xv = make_float4(enter ? wen : wlv, qc.x, ymc, 0.f);
+        if (cx && (unsigned)(kb - K0) < (unsigned)NS) tXb[kb] = xv;
+        if (cx && (unsigned)(ka - K0) < (unsigned)NS) tXa[ka] = xv;
         __syncwarp();
     }
 }
 
 // Deposits of one entry into both bricks, lanes = slots j = lane + 32 r;
-// clears the tables.
+// clears the tables.  segs[s] = {wa, wb, float index of the L column}; the U
+// column sits UOFF floats after it.  Per voxel the pieces are added in one
+// fixed order: v + (wb - clamp(Xa.w)) Xa.y + (clamp(Xb.w) - wa) Xb.y + (wb - wa) H.
 template <int RC>
-__device__ __forceinline__ void mir_deposits(const float4* segs, int nseg, int NS, int lane,
-                                             unsigned tH, unsigned tXb, unsigned tXa) {
+__device__ __forceinline__ void mir_deposits(float* acc, const float4* segs, int nseg, int NS,
+                                             int UOFF, int lane, float2* tH, float4* tXb,
+                                             float4* tXa) {
     float hL[RC], hU[RC], bw[RC], byL[RC], byU[RC], aw[RC], ayL[RC], ayU[RC];
-    unsigned off[RC];
     bool xs[RC], on[RC];
 #pragma unroll
     for (int r = 0; r < RC; ++r) {
@@ -1153,12 +1147,12 @@ __device__ __forceinline__ void mir_deposits(const float4* segs, int nseg, int N
         float2 h = make_float2(0.f, 0.f);
         float4 xb = make_float4(0.f, 0.f, 0.f, 0.f), xa = xb;
         if (on[r]) {
-            h = lds_f2(tH + 8u * j);
-            xb = lds_f4(tXb + 16u * j);
-            xa = lds_f4(tXa + 16u * j);
-            sts_f2(tH + 8u * j, make_float2(0.f, 0.f));
-            sts_f4(tXb + 16u * j, make_float4(0.f, 0.f, 0.f, 0.f));
-            sts_f4(tXa + 16u * j, make_float4(0.f, 0.f, 0.f, 0.f));
+            h = tH[j];
+            xb = tXb[j];
+            xa = tXa[j];
+            tH[j] = make_float2(0.f, 0.f);
+            tXb[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            tXa[j] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         hL[r] = h.x;
         hU[r] = h.y;
@@ -1168,40 +1162,36 @@ __device__ __forceinline__ void mir_deposits(const float4* segs, int nseg, int N
         aw[r] = xa.x;
         ayL[r] = xa.y;
         ayU[r] = xa.z;
-        off[r] = 4u * (unsigned)j;
         xs[r] = __any_sync(kFull, xb.y != 0.f || xa.y != 0.f || xb.z != 0.f || xa.z != 0.f);
     }
     for (int sgi = 0; sgi < nseg; ++sgi) {
         const float4 sg = segs[sgi];
         const float wa = sg.x, wb = sg.y;
-        const unsigned bL = __float_as_uint(sg.z), bU = __float_as_uint(sg.w);
+        float* const a = acc + (__float_as_int(sg.z) + lane);
         const float d = wb - wa;
         float vL[RC], vU[RC];
 #pragma unroll
         for (int r = 0; r < RC; ++r) {
-            vL[r] = on[r] ? lds_f(bL + off[r]) : 0.f;
-            vU[r] = on[r] ? lds_f(bU + off[r]) : 0.f;
+            vL[r] = on[r] ? a[32 * r] : 0.f;
+            vU[r] = on[r] ? a[UOFF + 32 * r] : 0.f;
         }
 #pragma unroll
         for (int r = 0; r < RC; ++r) {
-            float dL, dU;
             if (xs[r]) {
                 const float tb = fminf(fmaxf(bw[r], wa), wb) - wa;
                 const float ta = wb - fminf(fmaxf(aw[r], wa), wb);
-                dL = __fmaf_rn(d, hL[r], __fmaf_rn(tb, byL[r], ta * ayL[r]));
-                dU = __fmaf_rn(d, hU[r], __fmaf_rn(tb, byU[r], ta * ayU[r]));
+                vL[r] = __fmaf_rn(d, hL[r], __fmaf_rn(tb, byL[r], __fmaf_rn(ta, ayL[r], vL[r])));
+                vU[r] = __fmaf_rn(d, hU[r], __fmaf_rn(tb, byU[r], __fmaf_rn(ta, ayU[r], vU[r])));
             } else {
-                dL = __fmul_rn(d, hL[r]);
-                dU = __fmul_rn(d, hU[r]);
+                vL[r] = __fmaf_rn(d, hL[r], vL[r]);
+                vU[r] = __fmaf_rn(d, hU[r], vU[r]);
             }
-            vL[r] += dL;
-            vU[r] += dU;
         }
 #pragma unroll
         for (int r = 0; r < RC; ++r)
             if (on[r]) {
-                sts_f(bL + off[r], vL[r]);
-                sts_f(bU + off[r], vU[r]);
+                a[32 * r] = vL[r];
+                a[UOFF + 32 * r] = vU[r];
             }
     }
     __syncwarp();
@@ -1210,24 +1200,27 @@ __device__ __forceinline__ void mir_deposits(const float4* segs, int nseg, int N
 #ifndef KCT_MIR_MINB
 #define KCT_MIR_MINB 20  // 11 KB of shared memory per warp at 64-slab bricks: <= 20 warps per SM
 #endif
+// CSC: the brick height as a compile-time constant (shared-memory offsets
+// become immediates), 0: bc.bz at run time.
+template <int CSC>
 __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
     const float4* __restrict__ rec, float* __restrict__ out, DevGeom g, BrickCfg bc, int a0,
     int nab, int accumulate, const int* __restrict__ order, int* queue,
     float* __restrict__ out_part, const WalkEntry* __restrict__ tab,
     const unsigned long long* __restrict__ off) {
-    extern __shared__ float sm[];
+    extern __shared__ float4 sm4[];
+    float* const sm = reinterpret_cast<float*>(sm4);
     const int lane = threadIdx.x & 31;
     const int nbricks = bc.nbx * bc.nby * bc.nbz;
-    const int CS = bc.bz;
+    const int CS = CSC ? CSC : bc.bz;
     const int nu = g.nu, nv = g.nv, nz = g.nz;
-    float* accL = sm;
-    float* accU = sm + BX * BY * CS;
-    float4* segs = reinterpret_cast<float4*>(sm + 2 * BX * BY * CS);
-    const unsigned accL_s = (unsigned)__cvta_generic_to_shared(accL);
-    const unsigned accU_s = accL_s + 4u * (unsigned)(BX * BY * CS);
-    const unsigned tXb = accL_s + 4u * (unsigned)(2 * BX * BY * CS + 4 * kMaxSeg);
-    const unsigned tXa = tXb + 16u * (unsigned)CS;
-    const unsigned tH = tXa + 16u * (unsigned)CS;
+    const int UOFF = BX * BY * CS;  // accU = accL + UOFF
+    float* const accL = sm;
+    float* const accU = sm + UOFF;
+    float4* const segs = reinterpret_cast<float4*>(sm + 2 * UOFF);
+    float4* const tXb = reinterpret_cast<float4*>(sm + 2 * UOFF + 4 * kMaxSeg);
+    float4* const tXa = tXb + CS;
+    float2* const tH = reinterpret_cast<float2*>(tXa + CS);
     const int nitems = nbricks * bc.ngrp;
     int ticket = queue ? 0 : blockIdx.x;
     for (;;) {
@@ -1251,12 +1244,11 @@ __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
         const int acc_in = grp == 0 ? accumulate : 0;
         const BrickGeo B = brick_geo(brick, bc, g);
         const int K0 = B.K0, NS = B.bzn;
-        for (int q = lane; q < (2 * BX * BY * CS) / 4; q += 32)
-            reinterpret_cast<float4*>(sm)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = lane; q < (2 * UOFF) / 4; q += 32) sm4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int j = lane; j < CS; j += 32) {
-            sts_f2(tH + 8u * j, make_float2(0.f, 0.f));
-            sts_f4(tXb + 16u * j, make_float4(0.f, 0.f, 0.f, 0.f));
-            sts_f4(tXa + 16u * j, make_float4(0.f, 0.f, 0.f, 0.f));
+            tH[j] = make_float2(0.f, 0.f);
+            tXb[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            tXa[j] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         __syncwarp();
 
@@ -1293,9 +1285,8 @@ __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
             const float w_in = __uint_as_float(__shfl_sync(kFull, w, M + 2));
             const float inv_h1 = __uint_as_float(__shfl_sync(kFull, w, M + 3));
             if (lane < nseg) {
-                const unsigned ij = (ijw >> (8 * (lane & 3))) & 0xffu;
-                const unsigned cb = 4u * ij * (unsigned)CS;
-                segs[lane] = make_float4(wa, wb, __uint_as_float(accL_s + cb), __uint_as_float(accU_s + cb));
+                const int ij = (int)((ijw >> (8 * (lane & 3))) & 0xffu);
+                segs[lane] = make_float4(wa, wb, __int_as_float(ij * CS), 0.f);
             }
             const unsigned w2 = ld_entry(e + 2);
             float ym1;
@@ -1306,10 +1297,10 @@ __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
             mir_classify(rc + rlo, rc + (nv - 1 - rlo), q, ym, rhi - rlo + 1, rlo, lo, hi, w_in,
                          rcp_approx(inv_h1), K0, NS, lane, g, tH, tXb, tXa);
             switch ((NS + 31) >> 5) {
-            case 1: mir_deposits<1>(segs, nseg, NS, lane, tH, tXb, tXa); break;
-            case 2: mir_deposits<2>(segs, nseg, NS, lane, tH, tXb, tXa); break;
-            case 3: mir_deposits<3>(segs, nseg, NS, lane, tH, tXb, tXa); break;
-            default: mir_deposits<4>(segs, nseg, NS, lane, tH, tXb, tXa); break;
+            case 1: mir_deposits<1>(sm, segs, nseg, NS, UOFF, lane, tH, tXb, tXa); break;
+            case 2: mir_deposits<2>(sm, segs, nseg, NS, UOFF, lane, tH, tXb, tXa); break;
+            case 3: mir_deposits<3>(sm, segs, nseg, NS, UOFF, lane, tH, tXb, tXa); break;
+            default: mir_deposits<4>(sm, segs, nseg, NS, UOFF, lane, tH, tXb, tXa); break;
             }
             w = w1;
             w1 = w2;
@@ -1880,8 +1871,9 @@ void Projector::build_tables(const kct_geometry& geom) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
     KCT_CUDA(cudaFuncSetAttribute(adj_brick_kernel<true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
-    KCT_CUDA(cudaFuncSetAttribute(adj_mirror_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(adj_mir_floats(kMirMaxBz) * sizeof(float))));
+    for (auto fn : {adj_mirror_kernel<0>, adj_mirror_kernel<32>, adj_mirror_kernel<64>})
+        KCT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(adj_mir_floats(kMirMaxBz) * sizeof(float))));
 
     // z-mirror brick pairs (adj_mirror_kernel): z-mirror geometry, slab-lane
     // conditions, nz even; bricks of <= 64 slabs tiling the lower half
@@ -1951,7 +1943,7 @@ void Projector::build_tables(const kct_geometry& geom) {
         KCT_CUDA(cudaMalloc(&d_queue_, sizeof(int)));
         int per_sm = 0, sms = 0;
         if (adj_mir_)
-            KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_mirror_kernel, 32,
+            KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_mirror_kernel<0>, 32,
                                                                    adj_smem_bytes()));
         else
             KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_brick_kernel<true>,
@@ -2294,7 +2286,8 @@ void Projector::adjoint_impl(const float* proj, float* vol, int a_begin, int a_e
             if (d_queue_) KCT_CUDA(cudaMemsetAsync(d_queue_, 0, sizeof(int), s));
             const unsigned grid = d_queue_ ? std::min(nctas, adj_ctas_) : nctas;
             if (adj_mir_)
-                adj_mirror_kernel<<<grid, 32, smem, s>>>(
+                (bc.bz == 64 ? adj_mirror_kernel<64> : bc.bz == 32 ? adj_mirror_kernel<32> : adj_mirror_kernel<0>)
+                    <<<grid, 32, smem, s>>>(
                     reinterpret_cast<const float4*>(d_yw_), vol, dg_, bc, a0, nab, accum, d_border_,
                     d_queue_, d_part_, static_cast<const WalkEntry*>(d_tab_), d_off_);
             else if (d_tab_)
