@@ -1075,12 +1075,12 @@ __host__ __device__ constexpr int adj_mir_floats(int bz) {
     return (2 * BX * BY * bz + 4 * kMaxSeg + 10 * bz + 3) & ~3;
 }
 
-// Classification of the primary rows rlo.. (nrows; records p = rec + rlo,
-// the mirrors' weights at pm = rec + (nv - 1 - rlo), descending) into the
+// Classification of the primary rows rlo.. (nrows; records p and the
+// mirrors' weights pm, both from row rlo on) into the
 // slot tables; q / ym: the first chunk's record and mirror weight.  Slot j =
 // slab K0 + j, j < NS; tables all-zero on entry.
 __device__ __forceinline__ void mir_classify(const float4* __restrict__ p,
-                                             const float4* __restrict__ pm, float4 q, float ym,
+                                             const float* __restrict__ pm, float4 q, float ym,
                                              int nrows, int rlo, float lo, float hi, float w_in,
                                              float h1, int K0, int NS, int lane, const DevGeom& g,
                                              float2* tH, float4* tXb, float4* tXa) {
@@ -1089,16 +1089,16 @@ __device__ __forceinline__ void mir_classify(const float4* __restrict__ p,
     tXb -= K0;
     tXa -= K0;
     p += lane;
-    pm -= lane;
+    pm += lane;
     float ivf = (float)(rlo + lane);
     for (int b = lane; b < nrows + lane; b += 32) {
         const float4 qc = q;
         const float ymc = ym;
         p += 32;
-        pm -= 32;
+        pm += 32;
         if (b + 32 < nrows) {  // next chunk
             q = __ldg(p);
-            ym = __ldg(&pm->x);
+            ym = __ldg(pm);
         }
         const bool valid = b < nrows;
         const int k0 = __float_as_int(qc.w) >> 2;  // primary rows: kstep -1
@@ -1204,10 +1204,12 @@ __device__ __forceinline__ void mir_deposits(float* acc, const float4* segs, int
 // become immediates), 0: bc.bz at run time.
 template <int CSC>
 __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
-    const float4* __restrict__ rec, float* __restrict__ out, DevGeom g, BrickCfg bc, int a0,
-    int nab, int accumulate, const int* __restrict__ order, int* queue,
-    float* __restrict__ out_part, const WalkEntry* __restrict__ tab,
+    const float4* __restrict__ rec, const float* __restrict__ ymw, float* __restrict__ out,
+    DevGeom g, BrickCfg bc, int a0, int nab, int accumulate, const int* __restrict__ order,
+    int* queue, float* __restrict__ out_part, const WalkEntry* __restrict__ tab,
     const unsigned long long* __restrict__ off) {
+    // rec / ymw: adj_weight_mir_kernel's records of the primary rows and the
+    // mirror rows' weights, [column][p], p < nv/2 (primary row p, mirror row nv-1-p)
     extern __shared__ float4 sm4[];
     float* const sm = reinterpret_cast<float*>(sm4);
     const int lane = threadIdx.x & 31;
@@ -1265,9 +1267,9 @@ __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
             const unsigned ro = __shfl_sync(kFull, we, M), r = __shfl_sync(kFull, we, M + 1);
             const int rl = (int)(r & 0xffffu), n = (int)(r >> 16) - rl + 1;
             const bool ok = e < e1 && lane < n;
-            const unsigned base = ro - boff;
-            ymo = ok ? __ldg(&rec[base + (unsigned)(nv - 1 - rl - lane)].x) : 0.f;
-            return ok ? __ldg(rec + (base + (unsigned)(rl + lane))) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const unsigned idx = ((ro - boff) >> 1) + (unsigned)(rl + lane);
+            ymo = ok ? __ldg(ymw + idx) : 0.f;
+            return ok ? __ldg(rec + idx) : make_float4(0.f, 0.f, 0.f, 0.f);
         };
         unsigned w = ld_entry(e0), w1 = ld_entry(e0 + 1);
         float ym;
@@ -1293,8 +1295,8 @@ __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
             const float4 q1 = first_chunk(w1, e + 1, ym1);
             __syncwarp();
             const int rlo = (int)(rr & 0xffffu), rhi = (int)(rr >> 16);
-            const float4* rc = rec + (ro - boff);
-            mir_classify(rc + rlo, rc + (nv - 1 - rlo), q, ym, rhi - rlo + 1, rlo, lo, hi, w_in,
+            const unsigned cb = ((ro - boff) >> 1) + (unsigned)rlo;
+            mir_classify(rec + cb, ymw + cb, q, ym, rhi - rlo + 1, rlo, lo, hi, w_in,
                          rcp_approx(inv_h1), K0, NS, lane, g, tH, tXb, tXa);
             switch ((NS + 31) >> 5) {
             case 1: mir_deposits<1>(sm, segs, nseg, NS, UOFF, lane, tH, tXb, tXa); break;
@@ -2069,6 +2071,40 @@ __global__ void __launch_bounds__(256) adj_weight_kernel(const float* __restrict
     rec[t] = r;
 }
 
+// The same records for adj_mirror_kernel, one thread per row pair: the
+// primary row p < nv/2's record (float4, [column][p]) and the weight of its
+// mirror row nv-1-p (float, [column][p]; its 3D length factor is the
+// primary's: dv(nv-1-p) = -dv(p)).
+__global__ void __launch_bounds__(256) adj_weight_mir_kernel(const float* __restrict__ y,
+                                                             float4* __restrict__ rec,
+                                                             float* __restrict__ ymw,
+                                                             const ColParams* __restrict__ cols,
+                                                             const RowTab* __restrict__ rows,
+                                                             DevGeom g, size_t ncols) {
+    const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    const int nh = g.nv / 2;
+    const size_t col = t / (size_t)nh;
+    if (col >= ncols) return;
+    const int p = (int)(t - col * (size_t)nh);
+    const RowTab rt = ld_row(rows, p);
+    const float inv_l = cols[col].inv_l, inv_h1 = cols[col].inv_h1;
+    const double g_in = cols[col].g_in;
+    const float q = rt.dv * inv_l;
+    const double kzd = fma(rt.dvd, g_in, -g.kz0d);
+    const double fl = floor(kzd);
+    const int k0 = (int)fmax(fmin(fl, (double)(1 << 28)), -(double)(1 << 28));
+    const int ks = rt.dv > 0.f ? 1 : rt.dv < 0.f ? -1 : 0;
+    const float f = __fsqrt_rn(__fmaf_rn(q, q, 1.f));
+    const float* yc = y + col * (size_t)g.nv;
+    float4 r;
+    r.x = yc[p] * f;
+    r.y = (float)(kzd - fl);
+    r.z = __fmul_rn(rt.invdv, inv_h1);
+    r.w = __int_as_float(k0 * 4 + ks + 1);
+    rec[t] = r;
+    ymw[t] = yc[g.nv - 1 - p] * f;
+}
+
 // out += part[0] + part[1] + ... (fixed order: deterministic)
 __global__ void __launch_bounds__(256) adj_group_sum(float* __restrict__ out,
                                                      const float* __restrict__ part, int nparts,
@@ -2267,10 +2303,16 @@ void Projector::adjoint_impl(const float* proj, float* vol, int a_begin, int a_e
         const int accum = (a0 > a_begin || accumulate) ? 1 : 0;
         const ColParams* cols = d_cols_ + (size_t)a0 * dg_.nu;
         const float* pr = proj + (size_t)a0 * dg_.nu * dg_.nv;
-        if (!adj_gather_) {
-            const size_t nb = (size_t)nab * dg_.nu * dg_.nv;
+        const size_t nb = (size_t)nab * dg_.nu * dg_.nv;
+        float4* const yrec = reinterpret_cast<float4*>(d_yw_);
+        float* const ymw = d_yw_ + 2 * nb;  // after the nb / 2 primary records (adj_mir_)
+        if (adj_mir_) {
+            adj_weight_mir_kernel<<<(unsigned)((nb / 2 + 255) / 256), 256, 0, s>>>(
+                pr, yrec, ymw, cols, d_rows_, dg_, (size_t)nab * dg_.nu);
+            KCT_LAUNCHED();
+        } else if (!adj_gather_) {
             adj_weight_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(
-                pr, reinterpret_cast<float4*>(d_yw_), cols, d_rows_, dg_, (size_t)nab * dg_.nu);
+                pr, yrec, cols, d_rows_, dg_, (size_t)nab * dg_.nu);
             KCT_LAUNCHED();
         }
         if (adj_gather_) {
@@ -2288,7 +2330,7 @@ void Projector::adjoint_impl(const float* proj, float* vol, int a_begin, int a_e
             if (adj_mir_)
                 (bc.bz == 64 ? adj_mirror_kernel<64> : bc.bz == 32 ? adj_mirror_kernel<32> : adj_mirror_kernel<0>)
                     <<<grid, 32, smem, s>>>(
-                    reinterpret_cast<const float4*>(d_yw_), vol, dg_, bc, a0, nab, accum, d_border_,
+                    yrec, ymw, vol, dg_, bc, a0, nab, accum, d_border_,
                     d_queue_, d_part_, static_cast<const WalkEntry*>(d_tab_), d_off_);
             else if (d_tab_)
                 adj_brick_kernel<true><<<grid, kAdjWarps * 32, smem, s>>>(
