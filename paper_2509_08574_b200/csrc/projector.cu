@@ -1067,12 +1067,13 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
 // rays; slots are the brick's own slabs (no guard slabs: a simple row outside
 // the brick deposits nothing into it).
 // Shared memory per warp (floats): accL[BX*BY][bz] | accU[BX*BY][bz] |
-// segs[kMaxSeg] (float4: wa, wb, L and U column addresses) | tXb[bz], tXa[bz]
-// (float4: crossing w, primary weight, mirror weight, 0) | tH[bz] (float2).
+// segs[kMaxSeg] (float4: wa, wb, L column index) | tX[bz + 1] (float4:
+// crossing w, primary weight, mirror weight, 0 of the row leaving slot j
+// downwards, i.e. entering slot j - 1: primary rows all fall) | tH[bz] (float2).
 // ----------------------------------------------------------------------------
 constexpr int kMirMaxBz = 32 * kSlabChunks;
 __host__ __device__ constexpr int adj_mir_floats(int bz) {
-    return (2 * BX * BY * bz + 4 * kMaxSeg + 10 * bz + 3) & ~3;
+    return (2 * BX * BY * bz + 4 * kMaxSeg + 4 * (bz + 1) + 2 * bz + 3) & ~3;
 }
 
 // Classification of the primary rows rlo.. (nrows; records p and the
@@ -1083,11 +1084,10 @@ __device__ __forceinline__ void mir_classify(const float4* __restrict__ p,
                                              const float* __restrict__ pm, float4 q, float ym,
                                              int nrows, int rlo, float lo, float hi, float w_in,
                                              float h1, int K0, int NS, int lane, const DevGeom& g,
-                                             float2* tH, float4* tXb, float4* tXa) {
+                                             float2* tH, float4* tX) {
     const float mid = 0.5f * (lo + hi) - w_in;
     tH -= K0;  // slot of slab k at tH[k]
-    tXb -= K0;
-    tXa -= K0;
+    tX -= K0;
     p += lane;
     pm += lane;
     float ivf = (float)(rlo + lane);
@@ -1122,10 +1122,11 @@ __device__ __forceinline__ void mir_classify(const float4* __restrict__ p,
             const float2 h = tH[k];
             tH[k] = make_float2(h.x + qc.x, h.y + ymc);
         }
-        const int kb = enter ? k + 1 : k, ka = enter ? k : k - 1;
-        const float4 xv = make_float4(enter ? wen : wlv, qc.x, ymc, 0.f);
-        if (cx && (unsigned)(kb - K0) < (unsigned)NS) tXb[kb] = xv;
-        if (cx && (unsigned)(ka - K0) < (unsigned)NS) tXa[ka] = xv;
+        // the slab left: entering slab k from above (k + 1) or leaving it
+        // (slot NS: the row entering the brick's top slab from above)
+        const int kb = enter ? k + 1 : k;
+        if (cx && (unsigned)(kb - K0) <= (unsigned)NS)
+            tX[kb] = make_float4(enter ? wen : wlv, qc.x, ymc, 0.f);
         __syncwarp();
     }
 }
@@ -1136,8 +1137,7 @@ __device__ __forceinline__ void mir_classify(const float4* __restrict__ p,
 // fixed order: v + (wb - clamp(Xa.w)) Xa.y + (clamp(Xb.w) - wa) Xb.y + (wb - wa) H.
 template <int RC>
 __device__ __forceinline__ void mir_deposits(float* acc, const float4* segs, int nseg, int NS,
-                                             int UOFF, int lane, float2* tH, float4* tXb,
-                                             float4* tXa) {
+                                             int UOFF, int lane, float2* tH, float4* tX) {
     float hL[RC], hU[RC], bw[RC], byL[RC], byU[RC], aw[RC], ayL[RC], ayU[RC];
     bool xs[RC], on[RC];
 #pragma unroll
@@ -1148,11 +1148,9 @@ __device__ __forceinline__ void mir_deposits(float* acc, const float4* segs, int
         float4 xb = make_float4(0.f, 0.f, 0.f, 0.f), xa = xb;
         if (on[r]) {
             h = tH[j];
-            xb = tXb[j];
-            xa = tXa[j];
+            xb = tX[j];      // the row leaving slot j
+            xa = tX[j + 1];  // the row entering slot j (leaving j + 1)
             tH[j] = make_float2(0.f, 0.f);
-            tXb[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-            tXa[j] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         hL[r] = h.x;
         hU[r] = h.y;
@@ -1164,6 +1162,12 @@ __device__ __forceinline__ void mir_deposits(float* acc, const float4* segs, int
         ayU[r] = xa.z;
         xs[r] = __any_sync(kFull, xb.y != 0.f || xa.y != 0.f || xb.z != 0.f || xa.z != 0.f);
     }
+    // clear the tables (after every lane's reads: slot j + 1 is read by lane j)
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < RC; ++r)
+        if (on[r]) tX[lane + 32 * r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (lane == 0) tX[NS] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int sgi = 0; sgi < nseg; ++sgi) {
         const float4 sg = segs[sgi];
         const float wa = sg.x, wb = sg.y;
@@ -1220,9 +1224,8 @@ __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
     float* const accL = sm;
     float* const accU = sm + UOFF;
     float4* const segs = reinterpret_cast<float4*>(sm + 2 * UOFF);
-    float4* const tXb = reinterpret_cast<float4*>(sm + 2 * UOFF + 4 * kMaxSeg);
-    float4* const tXa = tXb + CS;
-    float2* const tH = reinterpret_cast<float2*>(tXa + CS);
+    float4* const tX = reinterpret_cast<float4*>(sm + 2 * UOFF + 4 * kMaxSeg);
+    float2* const tH = reinterpret_cast<float2*>(tX + CS + 1);
     const int nitems = nbricks * bc.ngrp;
     int ticket = queue ? 0 : blockIdx.x;
     for (;;) {
@@ -1249,9 +1252,9 @@ __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
         for (int q = lane; q < (2 * UOFF) / 4; q += 32) sm4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int j = lane; j < CS; j += 32) {
             tH[j] = make_float2(0.f, 0.f);
-            tXb[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-            tXa[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            tX[j] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
+        if (lane == 0) tX[CS] = make_float4(0.f, 0.f, 0.f, 0.f);
         __syncwarp();
 
         const unsigned long long* ob = off + (size_t)brick * (g.na + 1);
@@ -1297,12 +1300,12 @@ __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
             const int rlo = (int)(rr & 0xffffu), rhi = (int)(rr >> 16);
             const unsigned cb = ((ro - boff) >> 1) + (unsigned)rlo;
             mir_classify(rec + cb, ymw + cb, q, ym, rhi - rlo + 1, rlo, lo, hi, w_in,
-                         rcp_approx(inv_h1), K0, NS, lane, g, tH, tXb, tXa);
+                         rcp_approx(inv_h1), K0, NS, lane, g, tH, tX);
             switch ((NS + 31) >> 5) {
-            case 1: mir_deposits<1>(sm, segs, nseg, NS, UOFF, lane, tH, tXb, tXa); break;
-            case 2: mir_deposits<2>(sm, segs, nseg, NS, UOFF, lane, tH, tXb, tXa); break;
-            case 3: mir_deposits<3>(sm, segs, nseg, NS, UOFF, lane, tH, tXb, tXa); break;
-            default: mir_deposits<4>(sm, segs, nseg, NS, UOFF, lane, tH, tXb, tXa); break;
+            case 1: mir_deposits<1>(sm, segs, nseg, NS, UOFF, lane, tH, tX); break;
+            case 2: mir_deposits<2>(sm, segs, nseg, NS, UOFF, lane, tH, tX); break;
+            case 3: mir_deposits<3>(sm, segs, nseg, NS, UOFF, lane, tH, tX); break;
+            default: mir_deposits<4>(sm, segs, nseg, NS, UOFF, lane, tH, tX); break;
             }
             w = w1;
             w1 = w2;
