@@ -1073,7 +1073,7 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
 // ----------------------------------------------------------------------------
 constexpr int kMirMaxBz = 32 * kSlabChunks;
 __host__ __device__ constexpr int adj_mir_floats(int bz) {
-    return (2 * BX * BY * bz + 4 * kMaxSeg + 4 * (bz + 1) + 2 * bz + 3) & ~3;
+    return 2 * BX * BY * ((bz + 1) & ~1) + 4 * kMaxSeg + 4 * (((bz + 1) & ~1) + 2) + 2 * ((bz + 1) & ~1);
 }
 
 // Classification of the primary rows rlo.. (nrows; records p and the
@@ -1131,72 +1131,75 @@ __device__ __forceinline__ void mir_classify(const float4* __restrict__ p,
     }
 }
 
-// Deposits of one entry into both bricks, lanes = slots j = lane + 32 r;
-// clears the tables.  segs[s] = {wa, wb, float index of the L column}; the U
-// column sits UOFF floats after it.  Per voxel the pieces are added in one
-// fixed order: v + (wb - clamp(Xa.w)) Xa.y + (clamp(Xb.w) - wa) Xb.y + (wb - wa) H.
+// Deposits of one entry into both bricks.  Lane l takes the slot pair
+// j = 2 l + 64 r, j + 1; the accumulators hold per voxel column CS slots of
+// float2 {L, U}, so a lane's pair is one float4 (one shared load and store per
+// segment and pair).  segs[s] = {wa, wb, float4 index of the column}.  Per
+// voxel the pieces are added in one fixed order:
+//   v + (wb - clamp(Xa.w)) Xa.y + (clamp(Xb.w) - wa) Xb.y + (wb - wa) H
+// (Xb = tX[j]: the row leaving slot j; Xa = tX[j + 1]: the row entering it).
+// Clears the tables.
 template <int RC>
-__device__ __forceinline__ void mir_deposits(float* acc, const float4* segs, int nseg, int NS,
-                                             int UOFF, int lane, float2* tH, float4* tX) {
-    float hL[RC], hU[RC], bw[RC], byL[RC], byU[RC], aw[RC], ayL[RC], ayU[RC];
+__device__ __forceinline__ void mir_deposits(float4* acc, const float4* segs, int nseg, int NS,
+                                             int lane, float2* tH, float4* tX) {
+    float4 h[RC], xA[RC], xB[RC], xC[RC];
     bool xs[RC], on[RC];
+    float4* const tH4 = reinterpret_cast<float4*>(tH);
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int r = 0; r < RC; ++r) {
-        const int j = lane + 32 * r;
+        const int j = 2 * lane + 64 * r;
         on[r] = j < NS;
-        float2 h = make_float2(0.f, 0.f);
-        float4 xb = make_float4(0.f, 0.f, 0.f, 0.f), xa = xb;
+        h[r] = xA[r] = xB[r] = xC[r] = z4;
         if (on[r]) {
-            h = tH[j];
-            xb = tX[j];      // the row leaving slot j
-            xa = tX[j + 1];  // the row entering slot j (leaving j + 1)
-            tH[j] = make_float2(0.f, 0.f);
+            h[r] = tH4[lane + 32 * r];  // {hL, hU} of slots j, j + 1
+            xA[r] = tX[j];
+            xB[r] = tX[j + 1];
+            xC[r] = tX[j + 2];
         }
-        hL[r] = h.x;
-        hU[r] = h.y;
-        bw[r] = xb.x;
-        byL[r] = xb.y;
-        byU[r] = xb.z;
-        aw[r] = xa.x;
-        ayL[r] = xa.y;
-        ayU[r] = xa.z;
-        xs[r] = __any_sync(kFull, xb.y != 0.f || xa.y != 0.f || xb.z != 0.f || xa.z != 0.f);
+        xs[r] = __any_sync(kFull, xA[r].y != 0.f || xA[r].z != 0.f || xB[r].y != 0.f ||
+                                      xB[r].z != 0.f || xC[r].y != 0.f || xC[r].z != 0.f);
     }
-    // clear the tables (after every lane's reads: slot j + 1 is read by lane j)
+    // clear the tables (after every lane's reads: tX[j + 2] is the next lane's)
     __syncwarp();
 #pragma unroll
     for (int r = 0; r < RC; ++r)
-        if (on[r]) tX[lane + 32 * r] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (lane == 0) tX[NS] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (on[r]) {
+            const int j = 2 * lane + 64 * r;
+            tH4[lane + 32 * r] = z4;
+            tX[j] = z4;
+            tX[j + 1] = z4;
+        }
+    if (lane == 0) tX[NS] = z4;
     for (int sgi = 0; sgi < nseg; ++sgi) {
         const float4 sg = segs[sgi];
         const float wa = sg.x, wb = sg.y;
-        float* const a = acc + (__float_as_int(sg.z) + lane);
+        float4* const a = acc + (__float_as_int(sg.z) + lane);
         const float d = wb - wa;
-        float vL[RC], vU[RC];
+        float4 v[RC];
 #pragma unroll
-        for (int r = 0; r < RC; ++r) {
-            vL[r] = on[r] ? a[32 * r] : 0.f;
-            vU[r] = on[r] ? a[UOFF + 32 * r] : 0.f;
-        }
+        for (int r = 0; r < RC; ++r) v[r] = on[r] ? a[32 * r] : z4;
 #pragma unroll
         for (int r = 0; r < RC; ++r) {
             if (xs[r]) {
-                const float tb = fminf(fmaxf(bw[r], wa), wb) - wa;
-                const float ta = wb - fminf(fmaxf(aw[r], wa), wb);
-                vL[r] = __fmaf_rn(d, hL[r], __fmaf_rn(tb, byL[r], __fmaf_rn(ta, ayL[r], vL[r])));
-                vU[r] = __fmaf_rn(d, hU[r], __fmaf_rn(tb, byU[r], __fmaf_rn(ta, ayU[r], vU[r])));
+                const float cA = fminf(fmaxf(xA[r].x, wa), wb);
+                const float cB = fminf(fmaxf(xB[r].x, wa), wb);
+                const float cC = fminf(fmaxf(xC[r].x, wa), wb);
+                const float tbA = cA - wa, taA = wb - cB, tbB = cB - wa, taB = wb - cC;
+                v[r].x = __fmaf_rn(d, h[r].x, __fmaf_rn(tbA, xA[r].y, __fmaf_rn(taA, xB[r].y, v[r].x)));
+                v[r].y = __fmaf_rn(d, h[r].y, __fmaf_rn(tbA, xA[r].z, __fmaf_rn(taA, xB[r].z, v[r].y)));
+                v[r].z = __fmaf_rn(d, h[r].z, __fmaf_rn(tbB, xB[r].y, __fmaf_rn(taB, xC[r].y, v[r].z)));
+                v[r].w = __fmaf_rn(d, h[r].w, __fmaf_rn(tbB, xB[r].z, __fmaf_rn(taB, xC[r].z, v[r].w)));
             } else {
-                vL[r] = __fmaf_rn(d, hL[r], vL[r]);
-                vU[r] = __fmaf_rn(d, hU[r], vU[r]);
+                v[r].x = __fmaf_rn(d, h[r].x, v[r].x);
+                v[r].y = __fmaf_rn(d, h[r].y, v[r].y);
+                v[r].z = __fmaf_rn(d, h[r].z, v[r].z);
+                v[r].w = __fmaf_rn(d, h[r].w, v[r].w);
             }
         }
 #pragma unroll
         for (int r = 0; r < RC; ++r)
-            if (on[r]) {
-                a[32 * r] = vL[r];
-                a[UOFF + 32 * r] = vU[r];
-            }
+            if (on[r]) a[32 * r] = v[r];
     }
     __syncwarp();
 }
@@ -1218,13 +1221,12 @@ __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
     float* const sm = reinterpret_cast<float*>(sm4);
     const int lane = threadIdx.x & 31;
     const int nbricks = bc.nbx * bc.nby * bc.nbz;
-    const int CS = CSC ? CSC : bc.bz;
+    const int CS = CSC ? CSC : (bc.bz + 1) & ~1;  // slots per voxel column (even)
     const int nu = g.nu, nv = g.nv, nz = g.nz;
-    const int UOFF = BX * BY * CS;  // accU = accL + UOFF
-    float* const accL = sm;
-    float* const accU = sm + UOFF;
-    float4* const segs = reinterpret_cast<float4*>(sm + 2 * UOFF);
-    float4* const tX = reinterpret_cast<float4*>(sm + 2 * UOFF + 4 * kMaxSeg);
+    // acc: [BX * BY voxel columns][CS slots] of float2 {L, U}
+    float2* const acc = reinterpret_cast<float2*>(sm);
+    float4* const segs = reinterpret_cast<float4*>(sm + 2 * BX * BY * CS);
+    float4* const tX = segs + kMaxSeg;
     float2* const tH = reinterpret_cast<float2*>(tX + CS + 1);
     const int nitems = nbricks * bc.ngrp;
     int ticket = queue ? 0 : blockIdx.x;
@@ -1249,7 +1251,7 @@ __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
         const int acc_in = grp == 0 ? accumulate : 0;
         const BrickGeo B = brick_geo(brick, bc, g);
         const int K0 = B.K0, NS = B.bzn;
-        for (int q = lane; q < (2 * UOFF) / 4; q += 32) sm4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = lane; q < BX * BY * CS / 2; q += 32) sm4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int j = lane; j < CS; j += 32) {
             tH[j] = make_float2(0.f, 0.f);
             tX[j] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1291,7 +1293,7 @@ __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
             const float inv_h1 = __uint_as_float(__shfl_sync(kFull, w, M + 3));
             if (lane < nseg) {
                 const int ij = (int)((ijw >> (8 * (lane & 3))) & 0xffu);
-                segs[lane] = make_float4(wa, wb, __int_as_float(ij * CS), 0.f);
+                segs[lane] = make_float4(wa, wb, __int_as_float(ij * (CS / 2)), 0.f);
             }
             const unsigned w2 = ld_entry(e + 2);
             float ym1;
@@ -1301,12 +1303,10 @@ __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
             const unsigned cb = ((ro - boff) >> 1) + (unsigned)rlo;
             mir_classify(rec + cb, ymw + cb, q, ym, rhi - rlo + 1, rlo, lo, hi, w_in,
                          rcp_approx(inv_h1), K0, NS, lane, g, tH, tX);
-            switch ((NS + 31) >> 5) {
-            case 1: mir_deposits<1>(sm, segs, nseg, NS, UOFF, lane, tH, tX); break;
-            case 2: mir_deposits<2>(sm, segs, nseg, NS, UOFF, lane, tH, tX); break;
-            case 3: mir_deposits<3>(sm, segs, nseg, NS, UOFF, lane, tH, tX); break;
-            default: mir_deposits<4>(sm, segs, nseg, NS, UOFF, lane, tH, tX); break;
-            }
+            if (NS > 64)  // (NS <= kMirMaxBz = 128)
+                mir_deposits<2>(sm4, segs, nseg, NS, lane, tH, tX);
+            else
+                mir_deposits<1>(sm4, segs, nseg, NS, lane, tH, tX);
             w = w1;
             w1 = w2;
             q = q1;
@@ -1317,13 +1317,13 @@ __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
             for (int c = 0; c < B.bxn * B.byn; ++c) {
                 const int ci = c % B.bxn, cj = c / B.bxn;
                 float* o = dst + ((size_t)(B.I0 + ci) + (size_t)g.nx * (B.J0 + cj)) * nz;
-                const float* aL = accL + (ci + BX * cj) * CS;
-                const float* aU = accU + (ci + BX * cj) * CS;
+                const float2* ac = acc + (ci + BX * cj) * CS;
                 for (int kk = lane; kk < NS; kk += 32) {
+                    const float2 v = ac[kk];
                     float* oL = o + K0 + kk;
                     float* oU = o + (nz - 1 - K0 - kk);
-                    *oL = acc_in ? *oL + aL[kk] : aL[kk];
-                    *oU = acc_in ? *oU + aU[kk] : aU[kk];
+                    *oL = acc_in ? *oL + v.x : v.x;
+                    *oU = acc_in ? *oU + v.y : v.y;
                 }
             }
             __syncwarp();
@@ -1338,8 +1338,9 @@ __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
                     const size_t plane = (size_t)g.nx * g.ny;
                     float* oL = dst + xy + plane * (size_t)(K0 + kk);
                     float* oU = dst + xy + plane * (size_t)(nz - 1 - K0 - kk);
-                    *oL = acc_in ? *oL + accL[c * CS + kk] : accL[c * CS + kk];
-                    *oU = acc_in ? *oU + accU[c * CS + kk] : accU[c * CS + kk];
+                    const float2 v = acc[c * CS + kk];
+                    *oL = acc_in ? *oL + v.x : v.x;
+                    *oU = acc_in ? *oU + v.y : v.y;
                 }
             }
             if (bc.level_done) {
