@@ -352,8 +352,9 @@ def run_ours(args):
     peak, peak_src = measured_peak()
     bytes_f = 4.0 * nnz_f + 4.0 * Nf
     bytes_b = 4.0 * nnz_b + 4.0 * Mb
+    adj_kernel = "adj_mirror_kernel" if A_b.info("adj_mirror") else "adj_brick_kernel"
     if mean_b >= mean_f:
-        dom = ("adjoint (adj_brick_kernel)", bytes_b, mean_b)
+        dom = (f"adjoint ({adj_kernel})", bytes_b, mean_b)
     else:
         dom = ("forward (fwd_kernel)", bytes_f, mean_f)
     achieved = dom[1] / dom[2] / 1e9
@@ -362,7 +363,7 @@ def run_ours(args):
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get("adj_brick_kernel" if "adj" in dom[0] else "fwd_kernel")
+                traffic = json.load(f).get(adj_kernel if "adj" in dom[0] else "fwd_kernel")
         except Exception:
             traffic = None
 
@@ -387,11 +388,14 @@ def run_ours(args):
                         "byte_model": "4*nnz + 4*N (A x) / 4*nnz + 4*M (A^T y), nnz = exact "
                                       "Siddon intersections counted on device"},
            "gpu_launches": launches, "clocks": clk.summary(),
-           "launches_per_step": {"forward": "fwd_kernel", "adjoint": "adj_weight_kernel + "
-                                 "adj_brick_kernel (+ adj_group_sum when angle groups > 1)"},
+           "launches_per_step": {"forward": "pad_kernel + fwd_kernel",
+                                 "adjoint": ("adj_weight_mir_kernel + adj_mirror_kernel"
+                                             if adj_kernel == "adj_mirror_kernel" else
+                                             "adj_weight_kernel + adj_brick_kernel")
+                                 + " (+ adj_group_sum when angle groups > 1)"},
            # which code paths the handles run (kct_projector_info)
-           "paths": {key: A_b.info(key) for key in ("adj_slab", "adj_bz", "adj_groups",
-                                                      "adj_walk_entries")}
+           "paths": {key: A_b.info(key) for key in ("adj_slab", "adj_mirror", "adj_bz",
+                                                      "adj_groups", "adj_walk_entries")}
            | {key: A_f.info(key) for key in ("fwd_rows_per_warp", "fwd_bands", "fwd_split_z")}}
 
     # ---- FDK (fdk.hpp:50-139) of the c3 follow-up geometry, device resident ----

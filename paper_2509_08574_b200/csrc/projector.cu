@@ -1084,10 +1084,9 @@ __device__ __forceinline__ void mir_classify(const float4* __restrict__ p,
                                              const float* __restrict__ pm, float4 q, float ym,
                                              int nrows, int rlo, float lo, float hi, float w_in,
                                              float h1, int K0, int NS, int lane, const DevGeom& g,
-                                             float2* tH, float4* tX) {
+                                             float2* tH, float4* tX, int xodd) {
     const float mid = 0.5f * (lo + hi) - w_in;
     tH -= K0;  // slot of slab k at tH[k]
-    tX -= K0;
     p += lane;
     pm += lane;
     float ivf = (float)(rlo + lane);
@@ -1125,8 +1124,9 @@ __device__ __forceinline__ void mir_classify(const float4* __restrict__ p,
         // the slab left: entering slab k from above (k + 1) or leaving it
         // (slot NS: the row entering the brick's top slab from above)
         const int kb = enter ? k + 1 : k;
-        if (cx && (unsigned)(kb - K0) <= (unsigned)NS)
-            tX[kb] = make_float4(enter ? wen : wlv, qc.x, ymc, 0.f);
+        const int sb = kb - K0;  // slot: even ones at tX[s / 2], odd ones at tX[xodd + s / 2]
+        if (cx && (unsigned)sb <= (unsigned)NS)
+            tX[(sb & 1) * xodd + (sb >> 1)] = make_float4(enter ? wen : wlv, qc.x, ymc, 0.f);
         __syncwarp();
     }
 }
@@ -1141,7 +1141,7 @@ __device__ __forceinline__ void mir_classify(const float4* __restrict__ p,
 // Clears the tables.
 template <int RC>
 __device__ __forceinline__ void mir_deposits(float4* acc, const float4* segs, int nseg, int NS,
-                                             int lane, float2* tH, float4* tX) {
+                                             int lane, float2* tH, float4* tX, int xodd) {
     float4 h[RC], xA[RC], xB[RC], xC[RC];
     bool xs[RC], on[RC];
     float4* const tH4 = reinterpret_cast<float4*>(tH);
@@ -1153,24 +1153,23 @@ __device__ __forceinline__ void mir_deposits(float4* acc, const float4* segs, in
         h[r] = xA[r] = xB[r] = xC[r] = z4;
         if (on[r]) {
             h[r] = tH4[lane + 32 * r];  // {hL, hU} of slots j, j + 1
-            xA[r] = tX[j];
-            xB[r] = tX[j + 1];
-            xC[r] = tX[j + 2];
+            xA[r] = tX[lane + 32 * r];             // slot j (even slots: conflict-free rows)
+            xB[r] = tX[xodd + lane + 32 * r];      // slot j + 1
+            xC[r] = tX[lane + 1 + 32 * r];         // slot j + 2
         }
         xs[r] = __any_sync(kFull, xA[r].y != 0.f || xA[r].z != 0.f || xB[r].y != 0.f ||
                                       xB[r].z != 0.f || xC[r].y != 0.f || xC[r].z != 0.f);
     }
-    // clear the tables (after every lane's reads: tX[j + 2] is the next lane's)
+    // clear the tables (after every lane's reads: slot j + 2 is the next lane's)
     __syncwarp();
 #pragma unroll
     for (int r = 0; r < RC; ++r)
         if (on[r]) {
-            const int j = 2 * lane + 64 * r;
             tH4[lane + 32 * r] = z4;
-            tX[j] = z4;
-            tX[j + 1] = z4;
+            tX[lane + 32 * r] = z4;
+            tX[xodd + lane + 32 * r] = z4;
         }
-    if (lane == 0) tX[NS] = z4;
+    if (lane == 0) tX[(NS & 1) * xodd + (NS >> 1)] = z4;
     for (int sgi = 0; sgi < nseg; ++sgi) {
         const float4 sg = segs[sgi];
         const float wa = sg.x, wb = sg.y;
@@ -1302,11 +1301,11 @@ __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
             const int rlo = (int)(rr & 0xffffu), rhi = (int)(rr >> 16);
             const unsigned cb = ((ro - boff) >> 1) + (unsigned)rlo;
             mir_classify(rec + cb, ymw + cb, q, ym, rhi - rlo + 1, rlo, lo, hi, w_in,
-                         rcp_approx(inv_h1), K0, NS, lane, g, tH, tX);
+                         rcp_approx(inv_h1), K0, NS, lane, g, tH, tX, CS / 2 + 1);
             if (NS > 64)  // (NS <= kMirMaxBz = 128)
-                mir_deposits<2>(sm4, segs, nseg, NS, lane, tH, tX);
+                mir_deposits<2>(sm4, segs, nseg, NS, lane, tH, tX, CS / 2 + 1);
             else
-                mir_deposits<1>(sm4, segs, nseg, NS, lane, tH, tX);
+                mir_deposits<1>(sm4, segs, nseg, NS, lane, tH, tX, CS / 2 + 1);
             w = w1;
             w1 = w2;
             q = q1;
