@@ -27,3 +27,6 @@ ncu --set full --clock-control none -k 'regex:k_reggrad|k_weights|k_normq|k_upda
     -s 40 -c 5 -o gpurun_out/prof_solver_$TAG -f python tools/recon_prof.py --reps 1 \
     > gpurun_out/prof_solver_$TAG.log 2>&1
 echo "solver ncu rc=$?"
+ncu --set full --clock-control none -k 'regex:k_weights' -s 4 -c 1 -o gpurun_out/prof_weights_$TAG -f \
+    python tools/recon_prof.py --reps 1 > gpurun_out/prof_weights_$TAG.log 2>&1
+echo "weights ncu rc=$?"
