@@ -37,9 +37,12 @@ def launches(tag, path):
             name = r[ki].split("(")[0]
             agg.setdefault(name, []).append(float(r[vi].replace(",", "")) * 1e-6)
     tot = sum(sum(v) for v in agg.values())
-    lines = [f"# ncu launch list ({tag}): gpu__time_duration.sum, --clock-control none,",
-             "# cold-cache serialised launches of `bench.py --steps 2 --warmup 3 --skip-recon",
-             "# --skip-cpu --skip-e2e --skip-fdk` (shares, not absolutes, are comparable to the bench)",
+    what = ("# cold-cache serialised launches of `tools/recon_prof.py --reps 2` (two warm 20-iteration\n"
+            "# c3 IRN-PICCS solves; shares, not absolutes, are comparable to the bench)"
+            if "solver" in tag else
+            "# cold-cache serialised launches of `bench.py --steps 2 --warmup 3 --skip-recon\n"
+            "# --skip-cpu --skip-e2e --skip-fdk` (shares, not absolutes, are comparable to the bench)")
+    lines = [f"# ncu launch list ({tag}): gpu__time_duration.sum, --clock-control none,", what,
              f"{'kernel':70s} {'n':>4s} {'total_ms':>10s} {'mean_ms':>9s} {'share':>6s}"]
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"{k[:70]:70s} {len(v):4d} {sum(v):10.3f} {sum(v) / len(v):9.3f} "
@@ -86,8 +89,11 @@ def full(tag, rep):
         except (KeyError, ValueError):
             pass
         print("\n".join(lines))
-    if traffic:
-        json.dump(traffic, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
+    if traffic:  # merged into the existing per-kernel table
+        path = os.path.join(PROF, "ncu_traffic.json")
+        allt = json.load(open(path)) if os.path.exists(path) else {}
+        allt.update(traffic)
+        json.dump(allt, open(path, "w"), indent=1)
 
 
 if __name__ == "__main__":
