@@ -1351,6 +1351,213 @@ __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
     }
 }
 
+// ---- warp-specialised brick pairs (adj_mirror_ws_kernel) ----
+// Two warps per brick pair: warp 0 (producer) decodes the walk-table entries
+// and classifies their rows into one of two table buffers, warp 1 (consumer)
+// runs the deposits of the previous entry from the other buffer into the
+// shared accumulators (and writes the bricks out).  Handshakes are shared-
+// memory mbarriers (full[b]: producer arrives, consumer waits; empty[b]: the
+// reverse), the queue ticket is handed over at a CTA barrier per item.  Same classification,
+// same deposits, same order as adj_mirror_kernel: bit-identical results; the
+// point is twice the warps per shared accumulator (the one-warp kernel is
+// held to 20 warps per SM by its 11 KB of shared memory).
+// shared-memory mbarriers (count 32: every lane of the signalling warp arrives)
+__device__ __forceinline__ void mbar_init(unsigned a, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned a) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}" ::"r"(a)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred done;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra WAIT_%=;\n\t}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+
+// one table buffer: segs[kMaxSeg] | tX[CS + 1] | tH[CS] (float2) | meta (nseg)
+__host__ __device__ constexpr int mir_buf_floats(int cs) {
+    return 4 * kMaxSeg + 4 * (cs + 1) + 2 * cs + 4;
+}
+// accumulators | 2 NP buffers | item slots [2] + 4 NP mbarriers (8 B each)
+__host__ __device__ constexpr int adj_mir_ws_floats(int bz, int np) {
+    return 2 * BX * BY * ((bz + 1) & ~1) + 2 * np * mir_buf_floats((bz + 1) & ~1) + 4 + 8 * np;
+}
+
+#ifndef KCT_MIR_NP
+#define KCT_MIR_NP 2  // producer warps per consumer warp (classification is the longer half)
+#endif
+// NP producer warps take the entries of an item in turn (global entry g ->
+// producer g % NP), each into its own two buffers (g % (2 NP)); the consumer
+// deposits them in entry order.
+template <int CSC, int NP>
+__global__ void __launch_bounds__(32 * (NP + 1), 30 / (NP + 1)) adj_mirror_ws_kernel(
+    const float4* __restrict__ rec, const float* __restrict__ ymw, float* __restrict__ out,
+    DevGeom g, BrickCfg bc, int a0, int nab, int accumulate, const int* __restrict__ order,
+    int* queue, float* __restrict__ out_part, const WalkEntry* __restrict__ tab,
+    const unsigned long long* __restrict__ off) {
+    constexpr int NB = 2 * NP;  // table buffers
+    extern __shared__ float4 sm4[];
+    float* const sm = reinterpret_cast<float*>(sm4);
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const bool producer = warp < NP;
+    const int nbricks = bc.nbx * bc.nby * bc.nbz;
+    const int CS = CSC ? CSC : (bc.bz + 1) & ~1;
+    const int nu = g.nu, nv = g.nv, nz = g.nz;
+    float2* const acc = reinterpret_cast<float2*>(sm);
+    float* const bufbase = sm + 2 * BX * BY * CS;
+    const int BF = mir_buf_floats(CS);
+    int* const s_item = reinterpret_cast<int*>(bufbase + NB * BF);  // [2]
+    // mbarriers full[0..NB), empty[0..NB) (8-byte aligned)
+    const unsigned mb = (unsigned)__cvta_generic_to_shared(bufbase + NB * BF + 4);
+    auto full_of = [&](int b) { return mb + 8u * (unsigned)b; };
+    auto empty_of = [&](int b) { return mb + 8u * (unsigned)(NB + b); };
+    auto segs_of = [&](int b) { return reinterpret_cast<float4*>(bufbase + b * BF); };
+    auto tX_of = [&](int b) { return segs_of(b) + kMaxSeg; };
+    auto tH_of = [&](int b) { return reinterpret_cast<float2*>(tX_of(b) + CS + 1); };
+    auto meta_of = [&](int b) { return reinterpret_cast<int*>(tH_of(b) + CS); };
+    const int nitems = nbricks * bc.ngrp;
+    if (producer) {  // tables start zeroed
+        for (int b = warp; b < NB; b += NP)
+            for (int j = lane; j <= CS; j += 32) {
+                tX_of(b)[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (j < CS) tH_of(b)[j] = make_float2(0.f, 0.f);
+            }
+        if (warp == 0 && lane < 2 * NB) mbar_init(mb + 8u * (unsigned)lane, 32);
+    }
+    __syncthreads();
+    unsigned gcount = 0;  // entries of earlier items (entry g: buffer g % NB)
+    int ip = 0;
+    for (;;) {
+        if (threadIdx.x == 0) s_item[ip] = atomicAdd(queue, 1);
+        __syncthreads();
+        const int item = s_item[ip];
+        ip ^= 1;
+        if (item >= nitems) break;
+        const int grp = item % bc.ngrp;
+        const int brick = order[item / bc.ngrp];
+        const int a_lo = (int)((long long)nab * grp / bc.ngrp);
+        const int a_hi = (int)((long long)nab * (grp + 1) / bc.ngrp);
+        const BrickGeo B = brick_geo(brick, bc, g);
+        const int K0 = B.K0, NS = B.bzn;
+        const unsigned long long* ob = off + (size_t)brick * (g.na + 1);
+        const unsigned long long e0 = ob[a0 + a_lo], e1 = ob[a0 + a_hi];
+        if (producer) {
+            const unsigned* tw = reinterpret_cast<const unsigned*>(tab);
+            constexpr int M = kNB + kNB / 4;
+            auto ld_entry = [&](unsigned long long e) {
+                return (e < e1 && lane < kEW) ? __ldg(tw + e * kEW + lane) : 0u;
+            };
+            const unsigned boff = (unsigned)a0 * (unsigned)nu * (unsigned)nv;
+            auto first_chunk = [&](unsigned we, unsigned long long e, float& ymo) {
+                const unsigned ro = __shfl_sync(kFull, we, M), r = __shfl_sync(kFull, we, M + 1);
+                const int rl = (int)(r & 0xffffu), n = (int)(r >> 16) - rl + 1;
+                const bool ok = e < e1 && lane < n;
+                const unsigned idx = ((ro - boff) >> 1) + (unsigned)(rl + lane);
+                ymo = ok ? __ldg(ymw + idx) : 0.f;
+                return ok ? __ldg(rec + idx) : make_float4(0.f, 0.f, 0.f, 0.f);
+            };
+            // this warp's entries: e0 + d, d = (warp - gcount) mod NP, step NP
+            const unsigned long long es = e0 + (unsigned)((warp - (int)(gcount % NP) + NP) % NP);
+            unsigned w = ld_entry(es), w1 = ld_entry(es + NP);
+            float ym;
+            float4 q = first_chunk(w, es, ym);
+            for (unsigned long long e = es; e < e1; e += NP) {
+                const unsigned gi = gcount + (unsigned)(e - e0);
+                const int b = (int)(gi % NB);
+                // the consumer is done with b (its use gi / NB - 1)
+                if (gi >= (unsigned)NB) mbar_wait(empty_of(b), (gi / NB - 1u) & 1u);
+                float4* const segs = segs_of(b);
+                const unsigned ijw1 = __shfl_sync(kFull, w, M - 1);
+                const int nseg = (int)(ijw1 >> 24);
+                const unsigned rr = __shfl_sync(kFull, w, M + 1);
+                const float wa = __uint_as_float(__shfl_sync(kFull, w, lane & (kNB - 1)));
+                const float wb = __uint_as_float(__shfl_sync(kFull, w, (lane + 1) & (kNB - 1)));
+                const unsigned ijw = __shfl_sync(kFull, w, kNB + ((lane >> 2) & (kNB / 4 - 1)));
+                const float lo = __uint_as_float(__shfl_sync(kFull, w, 0));
+                const float hi = __uint_as_float(__shfl_sync(kFull, w, nseg & (kNB - 1)));
+                const unsigned ro = __shfl_sync(kFull, w, M);
+                const float w_in = __uint_as_float(__shfl_sync(kFull, w, M + 2));
+                const float inv_h1 = __uint_as_float(__shfl_sync(kFull, w, M + 3));
+                if (lane < nseg) {
+                    const int ij = (int)((ijw >> (8 * (lane & 3))) & 0xffu);
+                    segs[lane] = make_float4(wa, wb, __int_as_float(ij * (CS / 2)), 0.f);
+                }
+                if (lane == 0) *meta_of(b) = nseg;
+                const unsigned w2 = ld_entry(e + 2 * NP);
+                float ym1;
+                const float4 q1 = first_chunk(w1, e + NP, ym1);
+                const int rlo = (int)(rr & 0xffffu), rhi = (int)(rr >> 16);
+                const unsigned cb = ((ro - boff) >> 1) + (unsigned)rlo;
+                mir_classify(rec + cb, ymw + cb, q, ym, rhi - rlo + 1, rlo, lo, hi, w_in,
+                             rcp_approx(inv_h1), K0, NS, lane, g, tH_of(b), tX_of(b), CS / 2 + 1);
+                mbar_arrive(full_of(b));  // release: the tables / segments written above
+                w = w1;
+                w1 = w2;
+                q = q1;
+                ym = ym1;
+            }
+        } else {
+            for (int q = lane; q < BX * BY * CS / 2; q += 32) sm4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            __syncwarp();
+            for (unsigned long long e = e0; e < e1; ++e) {
+                const unsigned gi = gcount + (unsigned)(e - e0);
+                const int b = (int)(gi % NB);
+                mbar_wait(full_of(b), (gi / NB) & 1u);
+                const int nseg = *meta_of(b);
+                if (NS > 64)
+                    mir_deposits<2>(sm4, segs_of(b), nseg, NS, lane, tH_of(b), tX_of(b), CS / 2 + 1);
+                else
+                    mir_deposits<1>(sm4, segs_of(b), nseg, NS, lane, tH_of(b), tX_of(b), CS / 2 + 1);
+                mbar_arrive(empty_of(b));
+            }
+            float* const dst = grp == 0 ? out : out_part + (size_t)(grp - 1) * bc.gstride;
+            const int acc_in = grp == 0 ? accumulate : 0;
+            if (!bc.out_ref) {
+                for (int c = 0; c < B.bxn * B.byn; ++c) {
+                    const int ci = c % B.bxn, cj = c / B.bxn;
+                    float* o = dst + ((size_t)(B.I0 + ci) + (size_t)g.nx * (B.J0 + cj)) * nz;
+                    const float2* ac = acc + (ci + BX * cj) * CS;
+                    for (int kk = lane; kk < NS; kk += 32) {
+                        const float2 v = ac[kk];
+                        float* oL = o + K0 + kk;
+                        float* oU = o + (nz - 1 - K0 - kk);
+                        *oL = acc_in ? *oL + v.x : v.x;
+                        *oU = acc_in ? *oU + v.y : v.y;
+                    }
+                }
+            } else {
+                const int ncol = BX * BY;
+                for (int t = lane; t < ncol * NS; t += 32) {
+                    const int c = t % ncol, kk = t / ncol;
+                    const int ci = c % BX, cj = c / BX;
+                    if (ci < B.bxn && cj < B.byn) {
+                        const size_t xy = (size_t)(B.I0 + ci) + (size_t)g.nx * (B.J0 + cj);
+                        const size_t plane = (size_t)g.nx * g.ny;
+                        float* oL = dst + xy + plane * (size_t)(K0 + kk);
+                        float* oU = dst + xy + plane * (size_t)(nz - 1 - K0 - kk);
+                        const float2 v = acc[c * CS + kk];
+                        *oL = acc_in ? *oL + v.x : v.x;
+                        *oU = acc_in ? *oU + v.y : v.y;
+                    }
+                }
+                if (bc.level_done) {
+                    __threadfence();
+                    __syncwarp();
+                    if (lane == 0) atomicAdd(bc.level_done + brick / (bc.nbx * bc.nby), 1u);
+                }
+            }
+            __syncwarp();
+        }
+        gcount += (unsigned)(e1 - e0);
+    }
+}
+
 // ----------------------------------------------------------------------------
 // Adjoint, per-voxel gather (alternative; KCT_ADJOINT=gather).  One warp = one
 // voxel column (i,j), lane owns voxels k = kbase + lane + 32c.  For each angle
@@ -1879,6 +2086,10 @@ void Projector::build_tables(const kct_geometry& geom) {
     for (auto fn : {adj_mirror_kernel<0>, adj_mirror_kernel<32>, adj_mirror_kernel<64>})
         KCT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(adj_mir_floats(kMirMaxBz) * sizeof(float))));
+    for (auto fn : {adj_mirror_ws_kernel<0, KCT_MIR_NP>, adj_mirror_ws_kernel<32, KCT_MIR_NP>,
+                    adj_mirror_ws_kernel<64, KCT_MIR_NP>})
+        KCT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(adj_mir_ws_floats(kMirMaxBz, KCT_MIR_NP) * sizeof(float))));
 
     // z-mirror brick pairs (adj_mirror_kernel): z-mirror geometry, slab-lane
     // conditions, nz even; bricks of <= 64 slabs tiling the lower half
@@ -1946,8 +2157,14 @@ void Projector::build_tables(const kct_geometry& geom) {
         KCT_CUDA(cudaMalloc(&d_border_, nb * sizeof(int)));
         KCT_CUDA(cudaMemcpy(d_border_, order.data(), nb * sizeof(int), cudaMemcpyHostToDevice));
         KCT_CUDA(cudaMalloc(&d_queue_, sizeof(int)));
+        // warp-specialised brick pairs (adj_mirror_ws_kernel; KCT_ADJ_WS=0: one warp per pair)
+        const char* ws = std::getenv("KCT_ADJ_WS");
+        adj_ws_ = adj_mir_ && !(ws && ws[0] == '0');
         int per_sm = 0, sms = 0;
-        if (adj_mir_)
+        if (adj_ws_)
+            KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, adj_mirror_ws_kernel<0, KCT_MIR_NP>, 32 * (KCT_MIR_NP + 1), adj_smem_bytes()));
+        else if (adj_mir_)
             KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_mirror_kernel<0>, 32,
                                                                    adj_smem_bytes()));
         else
@@ -2028,6 +2245,7 @@ void Projector::build_walk_table() {
 }
 
 size_t Projector::adj_smem_bytes() const {
+    if (adj_ws_) return (size_t)adj_mir_ws_floats(adj_mbz_, KCT_MIR_NP) * sizeof(float);
     if (adj_mir_) return (size_t)adj_mir_floats(adj_mbz_) * sizeof(float);
     return (size_t)kAdjWarps * adj_warp_floats(adj_bz_) * sizeof(float);
 }
@@ -2330,7 +2548,13 @@ void Projector::adjoint_impl(const float* proj, float* vol, int a_begin, int a_e
         } else {
             if (d_queue_) KCT_CUDA(cudaMemsetAsync(d_queue_, 0, sizeof(int), s));
             const unsigned grid = d_queue_ ? std::min(nctas, adj_ctas_) : nctas;
-            if (adj_mir_)
+            if (adj_ws_)
+                (bc.bz == 64 ? adj_mirror_ws_kernel<64, KCT_MIR_NP>
+                 : bc.bz == 32 ? adj_mirror_ws_kernel<32, KCT_MIR_NP> : adj_mirror_ws_kernel<0, KCT_MIR_NP>)
+                    <<<grid, 32 * (KCT_MIR_NP + 1), smem, s>>>(
+                    yrec, ymw, vol, dg_, bc, a0, nab, accum, d_border_,
+                    d_queue_, d_part_, static_cast<const WalkEntry*>(d_tab_), d_off_);
+            else if (adj_mir_)
                 (bc.bz == 64 ? adj_mirror_kernel<64> : bc.bz == 32 ? adj_mirror_kernel<32> : adj_mirror_kernel<0>)
                     <<<grid, 32, smem, s>>>(
                     yrec, ymw, vol, dg_, bc, a0, nab, accum, d_border_,

@@ -115,6 +115,7 @@ class Projector {
     bool adj_slab() const { return adj_slab_; }
     bool adj_slab_detect() const { return adj_slab_detect_; }
     bool adj_mirror() const { return adj_mir_; }
+    bool adj_ws() const { return adj_ws_; }
     int adj_mirror_bz() const { return adj_mbz_; }
     int adj_groups() const { return adj_groups_; }
     unsigned long long walk_entries() const { return tab_entries_; }
@@ -145,6 +146,7 @@ class Projector {
     bool adj_slab_ = false;           // slab-lane adjoint deposits valid (brick_rows_slab)
     bool adj_slab_detect_ = false;    // ... with crossing-slot conflict detection
     bool adj_mir_ = false;            // z-mirror brick pairs (adj_mirror_kernel)
+    bool adj_ws_ = false;             // ... warp-specialised (adj_mirror_ws_kernel)
     int adj_mbz_ = 64;                // ... slabs per lower brick
     int* d_border_ = nullptr;         // brick order of the adjoint queue
     int* d_forder_ = nullptr;         // forward block -> item order (longest chords first)

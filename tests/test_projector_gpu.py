@@ -544,3 +544,19 @@ def test_mirror_brick_pairs_host_and_groups(monkeypatch):
     B = projector(grid, geom)
     assert B.info("adj_groups") == 3
     assert rel_l2(B.apply_adjoint(y), dev) < 1e-6
+
+
+@pytest.mark.parametrize("cfg,n_angles", [(1, 64), (2, 9), (3, 6), (4, 2)])
+def test_warp_specialised_pairs_bitwise(monkeypatch, cfg, n_angles):
+    """adj_mirror_ws_kernel (producer warp classifies, consumer warp deposits,
+    named-barrier handshakes) computes exactly what the one-warp brick-pair
+    kernel computes (KCT_ADJ_WS=0): same bits, also on the host path."""
+    grid, geom = baseline_geometry(cfg, n_angles=n_angles)
+    y = np.random.default_rng(81).uniform(0, 1, geom.ray_count).astype(np.float32)
+    A = projector(grid, geom)
+    assert A.info("adj_mirror") == 1 and A.info("adj_ws") == 1
+    ws = A.apply_adjoint(y)
+    monkeypatch.setenv("KCT_ADJ_WS", "0")
+    B = projector(grid, geom)
+    assert B.info("adj_ws") == 0
+    assert np.array_equal(ws, B.apply_adjoint(y))
