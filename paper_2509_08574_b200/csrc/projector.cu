@@ -1373,9 +1373,9 @@ __device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity) {
     asm volatile(
         "{\n\t.reg .pred done;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1, %2;\n\t"
         "@!done bra WAIT_%=;\n\t}" ::"r"(a),
-        "r"(parity)
+        "r"(parity), "r"(0x989680u)  // suspend-time hint: sleep (no spinning) until the phase flips
         : "memory");
 }
 
