@@ -272,11 +272,14 @@ __device__ __forceinline__ void footprint(const DevGeom& g, float cth, float sth
 // one warp and its contributions are added in a fixed (angle, column, pass,
 // row group, segment, piece) order: deterministic, no atomics, exactly A^T.
 // ----------------------------------------------------------------------------
-// Brick shape: tall narrow bricks (4x4 voxel columns x ~128 slabs, two rows
-// per lane) measured best at c3 (tools/adj_sweep.sh).
+// Brick shape: 5x5 voxel columns (x 64-slab pairs with the warp-specialised
+// z-mirror kernel; measured against 4x4, 6x5, 6x6, 8x4, 4x8 at c1-c5,
+// DESIGN.md §3).  The slab-lane condition bounds the xy size: a row's z-span
+// over the brick's chord must stay below the row spacing (c4: 6x6 is the
+// largest square that passes, 7x6 fails at c3).
 #ifndef KCT_BX
-#define KCT_BX 4
-#define KCT_BY 4
+#define KCT_BX 5
+#define KCT_BY 5
 #endif
 #ifndef KCT_ADJ_WARPS
 #define KCT_ADJ_WARPS 1  // one-warp CTAs: the warp's shared-memory base is CTA-uniform (uniform registers)
@@ -624,8 +627,10 @@ __device__ __forceinline__ void brick_rows(const Seg* segs, int nseg, const RowC
 constexpr int kSlabChunks = 4;  // slab table slots (bz + 2) <= 32 * kSlabChunks
 
 // floats of one warp's shared memory in adj_brick_kernel (16-byte multiple)
+// (the accumulators padded to a 16-byte multiple: Seg / float4 tables follow)
+__host__ __device__ constexpr int adj_acc_floats(int bz) { return (BX * BY * (bz + 2) + 3) & ~3; }
 __host__ __device__ constexpr int adj_warp_floats(int bz) {
-    return (BX * BY * (bz + 2) + 4 * kMaxSeg + 2 * (kMaxSeg + 2) + 5 * (bz + 2) + 3) & ~3;
+    return (adj_acc_floats(bz) + 4 * kMaxSeg + 2 * (kMaxSeg + 2) + 5 * (bz + 2) + 3) & ~3;
 }
 
 // Row classification of one entry into the slab tables: tH[j] = H (4 B),
@@ -869,11 +874,12 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
     const int CS = BZ + 2;
     const int wfloats = adj_warp_floats(BZ);
     float* acc = sm + warp * wfloats;
-    Seg* segs = reinterpret_cast<Seg*>(acc + BX * BY * CS);
-    float* bnd = acc + BX * BY * CS + 4 * kMaxSeg;
+    const int ACCF = adj_acc_floats(BZ);
+    Seg* segs = reinterpret_cast<Seg*>(acc + ACCF);
+    float* bnd = acc + ACCF + 4 * kMaxSeg;
     int* axis = reinterpret_cast<int*>(bnd + kMaxSeg + 2);
     const unsigned acc_s = (unsigned)__cvta_generic_to_shared(acc);
-    const unsigned tX = acc_s + 4u * (unsigned)(BX * BY * CS + 4 * kMaxSeg + 2 * (kMaxSeg + 2));
+    const unsigned tX = acc_s + 4u * (unsigned)(ACCF + 4 * kMaxSeg + 2 * (kMaxSeg + 2));
     const unsigned tH = tX + 16u * (unsigned)CS;
     const int S = bc.S;
 

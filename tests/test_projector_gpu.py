@@ -333,7 +333,7 @@ def test_slab_paths_awkward_geometry(monkeypatch, ora):
     from tests._util import Geometry, Grid
     grid = Grid(37, 29, 53, 0.9, 1.1, 1.3)
     angles = np.sort(np.random.default_rng(5).uniform(0, 2 * np.pi, 24))
-    geom = Geometry(300.0, 450.0, 61, 75, 1.2, 1.25, angles, 0.7, -0.9)
+    geom = Geometry(600.0, 900.0, 61, 75, 1.2, 1.25, angles, 0.7, -0.9)
     rng = np.random.default_rng(6)
     x = rng.uniform(0, 1, grid.count).astype(np.float32)
     y = rng.uniform(0, 1, geom.ray_count).astype(np.float32)
@@ -560,3 +560,23 @@ def test_warp_specialised_pairs_bitwise(monkeypatch, cfg, n_angles):
     B = projector(grid, geom)
     assert B.info("adj_ws") == 0
     assert np.array_equal(ws, B.apply_adjoint(y))
+
+
+def test_mirror_pairs_awkward_geometry(monkeypatch, ora):
+    """Brick pairs on awkward sizes: partial 5x5 bricks in x and y, a lower
+    half (27 slabs) that is an odd brick height, anisotropic voxels, a detector
+    u offset and non-uniform angles (z-mirror: offset_v = 0, nv even) —
+    against the oracle, the standard bricks and the one-warp pair kernel."""
+    from tests._util import Geometry, Grid
+    grid = Grid(37, 29, 54, 0.9, 1.1, 1.3)
+    angles = np.sort(np.random.default_rng(7).uniform(0, 2 * np.pi, 24))
+    geom = Geometry(600.0, 900.0, 61, 76, 1.2, 1.25, angles, 0.7, 0.0)
+    y = np.random.default_rng(8).uniform(0, 1, geom.ray_count).astype(np.float32)
+    A = projector(grid, geom)
+    assert A.info("adj_mirror") == 1 and A.info("adj_ws") == 1 and A.info("adj_bz") == 27
+    ws = A.apply_adjoint(y)
+    assert rel_l2(ws, ora.adjoint(grid, geom, y)) < TOL
+    monkeypatch.setenv("KCT_ADJ_WS", "0")
+    assert np.array_equal(projector(grid, geom).apply_adjoint(y), ws)
+    monkeypatch.setenv("KCT_ADJ_MIRROR", "0")
+    assert rel_l2(projector(grid, geom).apply_adjoint(y), ws) < 1e-6
