@@ -26,42 +26,59 @@ struct FdkGeom {
     float scale;                 // 0.5 * 2 pi / na (fdk.hpp:96-97)
 };
 
-// Stage 1+2 (fdk.hpp:65-86): one CTA = one angle x 32 detector rows; the
-// cosine-weighted rows are staged in shared memory, lane = row, warps stride
-// over the output columns.  Input / output in the native v-fastest layout.
+// Stage 1+2 (fdk.hpp:65-86): one CTA = one angle x R detector rows; the
+// cosine-weighted rows are staged in shared memory ([nu][R]), a lane takes row
+// lane % R of output column phase lane / R, warps stride over the output
+// columns.  R = 32 while the tile fits (nu <= ~1700 columns at 227 KB), fewer
+// rows per CTA for wider detectors (R = 1 reaches nu ~ 19000; the reference's
+// FFT filter has no width limit).  Input / output in the native v-fastest layout.
+template <int R>
 __global__ void __launch_bounds__(256) k_fdk_filter(const float* __restrict__ proj,
                                                     float* __restrict__ out, FdkGeom f) {
-    extern __shared__ float sm[];
-    float* tile = sm;                       // [nu][32]
-    float* h = sm + (size_t)f.nu * 32;      // [nu] kernel taps by distance
-    const int a = blockIdx.y, iv0 = blockIdx.x * 32;
+    constexpr int CP = 32 / R;              // column phases per warp
+    extern __shared__ double smd[];
+    double* h = smd;                                      // [nu] kernel taps by distance
+    float* tile = reinterpret_cast<float*>(smd + f.nu);  // [nu][R]
+    const int a = blockIdx.y, iv0 = blockIdx.x * R;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-    const int iv = iv0 + lane;
+    const int row = lane % R, cph = lane / R;
+    const int iv = iv0 + row;
     const bool row_ok = iv < f.nv;
     const float* pa = proj + (size_t)a * f.nu * f.nv;
     const double v = f.v0 + iv * f.dv;
-    for (int iu = warp; iu < f.nu; iu += nwarp) {
+    for (int iu = warp * CP + cph; iu < f.nu; iu += nwarp * CP) {
         float w = 0.f;
         if (row_ok) {
             const double u = f.u0 + iu * f.du;
             const double cosw = f.dso / sqrt(f.dso * f.dso + u * u + v * v);
             w = (float)(pa[(size_t)iu * f.nv + iv] * cosw);
         }
-        tile[iu * 32 + lane] = w;
+        tile[iu * R + row] = w;
     }
     const double inv = 1.0 / (f.du * f.du);
     for (int d = threadIdx.x; d < f.nu; d += blockDim.x)
-        h[d] = d == 0 ? (float)(0.25 * inv)
-                      : ((d & 1) ? (float)(-inv / (M_PI * M_PI * (double)d * (double)d)) : 0.f);
+        h[d] = d == 0 ? 0.25 * inv : ((d & 1) ? -inv / (M_PI * M_PI * (double)d * (double)d) : 0.0);
     __syncthreads();
     float* po = out + (size_t)a * f.nu * f.nv;
-    for (int iu = warp; iu < f.nu; iu += nwarp) {
-        float acc = h[0] * tile[iu * 32 + lane];
+    for (int iu = warp * CP + cph; iu < f.nu; iu += nwarp * CP) {
+        // float64 taps and sum: the ramp filter of a smooth row is a small
+        // residual of large cancelling terms (float32 sums lose ~1e-4 relative
+        // at a few thousand columns; the reference filters in float64)
+        double acc = h[0] * tile[iu * R + row];
         // odd distances only: iu' = iu -/+ 1, 3, 5, ...
-        for (int d = 1; d <= iu; d += 2) acc = fmaf(h[d], tile[(iu - d) * 32 + lane], acc);
-        for (int d = 1; iu + d < f.nu; d += 2) acc = fmaf(h[d], tile[(iu + d) * 32 + lane], acc);
+        for (int d = 1; d <= iu; d += 2) acc = fma(h[d], (double)tile[(iu - d) * R + row], acc);
+        for (int d = 1; iu + d < f.nu; d += 2) acc = fma(h[d], (double)tile[(iu + d) * R + row], acc);
         if (row_ok) po[(size_t)iu * f.nv + iv] = (float)(acc * f.du);
     }
+}
+
+template <int R>
+void launch_fdk_filter(const float* proj, float* filt, const FdkGeom& f, cudaStream_t s) {
+    const size_t smem = (size_t)f.nu * R * sizeof(float) + (size_t)f.nu * sizeof(double);
+    KCT_CUDA(cudaFuncSetAttribute(k_fdk_filter<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const dim3 g1((f.nv + R - 1) / R, f.na);
+    k_fdk_filter<R><<<g1, 256, smem, s>>>(proj, filt, f);
+    KCT_LAUNCHED();
 }
 
 // Stage 3 (fdk.hpp:88-138): a warp owns 32*KZ consecutive slabs of one voxel
@@ -151,11 +168,19 @@ void Projector::fdk(const float* proj, float* vol, float* filt, cudaStream_t s) 
     f.ox = grid_.ox; f.oy = grid_.oy; f.oz = grid_.oz;
     f.sx = grid_.sx; f.sy = grid_.sy; f.sz = grid_.sz;
     f.scale = (float)(0.5 * (2.0 * M_PI / (double)f.na));
-    const size_t smem = ((size_t)f.nu * 32 + f.nu) * sizeof(float);
-    KCT_CUDA(cudaFuncSetAttribute(k_fdk_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dim3 g1((f.nv + 31) / 32, f.na);
-    k_fdk_filter<<<g1, 256, smem, s>>>(proj, filt, f);
-    KCT_LAUNCHED();
+    // rows per filter CTA: the most that fit the shared-memory tile
+    int smem_max = 0;
+    KCT_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device_));
+    const auto fits = [&](int R) {
+        return (size_t)f.nu * R * sizeof(float) + (size_t)f.nu * sizeof(double) <= (size_t)smem_max;
+    };
+    if (fits(32)) launch_fdk_filter<32>(proj, filt, f, s);
+    else if (fits(16)) launch_fdk_filter<16>(proj, filt, f, s);
+    else if (fits(8)) launch_fdk_filter<8>(proj, filt, f, s);
+    else if (fits(4)) launch_fdk_filter<4>(proj, filt, f, s);
+    else if (fits(2)) launch_fdk_filter<2>(proj, filt, f, s);
+    else if (fits(1)) launch_fdk_filter<1>(proj, filt, f, s);
+    else throw ConfigError("fdk: detector too wide for the shared-memory row filter");
     AngleBatch ab;
     const size_t warps = (size_t)f.nx * f.ny * ((f.nz + 32 * kFdkKZ - 1) / (32 * kFdkKZ));
     const unsigned blocks = (unsigned)((warps * 32 + 255) / 256);

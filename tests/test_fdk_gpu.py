@@ -35,3 +35,24 @@ def test_fdk_needs_two_angles():
     gs, ge = to_pkg(grid, geom)
     with pytest.raises(k.ConfigError):
         k.ConeBeamProjector(gs, ge).fdk(np.zeros(ge.ray_count(), dtype=np.float32))
+
+
+@pytest.mark.parametrize("nu", [1024, 2048, 4100])
+def test_fdk_wide_detector(nu):
+    """detectors wider than one 32-row shared-memory tile (33 nu
+    floats > 227 KB from nu ~ 1760) filter with fewer rows per CTA; same
+    result as the oracle on projections of a random volume (nu = 1024: the
+    32-row path on the same kind of data)."""
+    import oracle
+    from oracle import Geometry, Grid, uniform_angles
+    oracle.build("ora")
+    ora = Oracle("ora")
+    grid = Grid(48, 48, 8, 1.0, 1.0, 1.0)
+    geom = Geometry(1000.0, 1500.0, nu, 12, 100.0 / nu, 1.0, uniform_angles(16))
+    gs, ge = to_pkg(grid, geom)
+    A = k.ConeBeamProjector(gs, ge)
+    x = np.random.default_rng(9).uniform(0, 0.04, gs.count()).astype(np.float32)
+    p = A.apply(x)
+    err = rel_l2(A.fdk(p), ora.fdk(grid, geom, p))
+    print(f"\n[fdk nu={nu}] rel err {err:.2e}")
+    assert err < 1e-4
