@@ -352,7 +352,8 @@ def run_ours(args):
     peak, peak_src = measured_peak()
     bytes_f = 4.0 * nnz_f + 4.0 * Nf
     bytes_b = 4.0 * nnz_b + 4.0 * Mb
-    adj_kernel = "adj_mirror_kernel" if A_b.info("adj_mirror") else "adj_brick_kernel"
+    adj_kernel = ("adj_mirror_ws_kernel" if A_b.info("adj_ws") else "adj_mirror_kernel") \
+        if A_b.info("adj_mirror") else "adj_brick_kernel"
     if mean_b >= mean_f:
         dom = (f"adjoint ({adj_kernel})", bytes_b, mean_b)
     else:
@@ -389,12 +390,12 @@ def run_ours(args):
                                       "Siddon intersections counted on device"},
            "gpu_launches": launches, "clocks": clk.summary(),
            "launches_per_step": {"forward": "pad_kernel + fwd_kernel",
-                                 "adjoint": ("adj_weight_mir_kernel + adj_mirror_kernel"
-                                             if adj_kernel == "adj_mirror_kernel" else
+                                 "adjoint": (f"adj_weight_mir_kernel + {adj_kernel}"
+                                             if "mirror" in adj_kernel else
                                              "adj_weight_kernel + adj_brick_kernel")
                                  + " (+ adj_group_sum when angle groups > 1)"},
            # which code paths the handles run (kct_projector_info)
-           "paths": {key: A_b.info(key) for key in ("adj_slab", "adj_mirror", "adj_bz",
+           "paths": {key: A_b.info(key) for key in ("adj_slab", "adj_mirror", "adj_ws", "adj_bz",
                                                       "adj_groups", "adj_walk_entries")}
            | {key: A_f.info(key) for key in ("fwd_rows_per_warp", "fwd_bands", "fwd_split_z")}}
 

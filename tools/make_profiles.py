@@ -70,7 +70,7 @@ def full(tag, rep):
     for r in rows[2:]:
         d = dict(zip(h, r))
         name = d["Kernel Name"].split("(")[0]
-        short = next((k for k in ("fwd_kernel", "adj_mirror_kernel", "adj_brick_kernel") if k in name),
+        short = next((k for k in ("fwd_kernel", "adj_mirror_ws_kernel", "adj_mirror_kernel", "adj_brick_kernel") if k in name),
                      name.split("::")[-1].split("<")[0])
         lines = [f"# ncu --set full --clock-control none ({tag}): {name}",
                  "# c3 workload (tools/kprof.py): 256^3 @0.5 mm, 384^2 @0.5 mm, 60 views"]
