@@ -163,8 +163,64 @@ namespace {
 // Host-buffer forward, pipelined: the projections of angle chunk c leave the
 // device (layout transpose + D2H on the copy stream) while chunk c + 1 is
 // computed.  Same kernels and results as the unpipelined path.
+// Staged host forward (reference layouts): the volume goes up stage range by
+// stage range on the copy stream (slabs [z_lo, z_hi) of stage s, centre out),
+// the main stream transposes each range into the padded volume and runs
+// stage s's rows as soon as its range is in; the last stage is counted per
+// pipeline chunk of angles and each chunk's projections go down as they finish.
+bool forward_host_staged(kct::Projector& P, const float* vol, float* proj, cudaStream_t s) {
+    const auto& st = P.fwd_stages();
+    const int S = (int)st.size();
+    if (S < 2 || S > kct::Projector::kPipeChunks || !P.fwd_done()) return false;
+    const size_t M = P.domain_size(), N = P.range_size();
+    const kct_grid& gr = P.grid();
+    const size_t plane = (size_t)gr.nx * gr.ny;
+    cudaStream_t sc = P.pipe_stream();
+    float* tmp = P.scratch(2, M);
+    float* q = P.scratch(1, N);
+    float* qr = P.scratch(3, N);
+    unsigned* done = P.fwd_done();
+    const int K = P.pipe_chunks();
+    KCT_CUDA(cudaMemsetAsync(done, 0, K * sizeof(unsigned), s));
+    KCT_CUDA(cudaEventRecord(P.upload_event(), s));  // the copy stream starts after this call's
+    KCT_CUDA(cudaStreamWaitEvent(sc, P.upload_event(), 0));  // earlier work and sees the reset
+    if (!P.stream_wait_geq(sc, done, 0u)) return false;  // probe: stream memory ops available
+    // uploads: the new slabs of each stage (below and above the previous range)
+    int lo = st[0].z_lo, hi = st[0].z_lo;
+    std::vector<std::pair<int, int>> pieces[kct::Projector::kPipeChunks];
+    for (int k = 0; k < S; ++k) {
+        if (st[k].z_lo < lo) pieces[k].push_back({st[k].z_lo, lo});
+        if (st[k].z_hi > hi) pieces[k].push_back({hi, st[k].z_hi});
+        lo = std::min(lo, st[k].z_lo);
+        hi = std::max(hi, st[k].z_hi);
+        for (auto& pc : pieces[k])
+            KCT_CUDA(cudaMemcpyAsync(tmp + pc.first * plane, vol + pc.first * plane,
+                                     (size_t)(pc.second - pc.first) * plane * sizeof(float),
+                                     cudaMemcpyHostToDevice, sc));
+        KCT_CUDA(cudaEventRecord(P.pipe_event(k), sc));
+    }
+    for (int k = 0; k < S; ++k) {
+        KCT_CUDA(cudaStreamWaitEvent(s, P.pipe_event(k), 0));
+        for (auto& pc : pieces[k]) P.vol_to_padded_z(tmp, pc.first, pc.second, s);
+        P.forward_stage(k, q, k + 1 == S ? done : nullptr, s);
+    }
+    const size_t per = N / (size_t)P.n_angles();
+    for (int c = 0; c < K; ++c) {
+        const int a0 = P.pipe_angle(c), a1 = P.pipe_angle(c + 1);
+        if (!P.stream_wait_geq(sc, done + c, (unsigned)((a1 - a0) * P.dev_geom().nu)))
+            throw kct::CudaError("forward: stream wait failed");
+        P.proj_from_native_range(q, qr, a0, a1, sc);
+        KCT_CUDA(cudaMemcpyAsync(proj + a0 * per, qr + a0 * per, (a1 - a0) * per * sizeof(float),
+                                 cudaMemcpyDeviceToHost, sc));
+    }
+    KCT_CUDA(cudaStreamSynchronize(sc));
+    KCT_CUDA(cudaStreamSynchronize(s));
+    return true;
+}
+
 void forward_host_pipelined(kct::Projector& P, const float* vol, float* proj, int layout,
                             cudaStream_t s) {
+    if (layout == KCT_LAYOUT_REFERENCE && forward_host_staged(P, vol, proj, s)) return;
     const size_t M = P.domain_size(), N = P.range_size();
     cudaStream_t sc = P.pipe_stream();
     // Split upload (reference layout: a z range is contiguous): slabs [Z0, Z)
@@ -341,6 +397,7 @@ int kct_projector_info(const kct_projector* h, const char* key, double* value) {
         else if (k == "fwd_bands") *value = P.dev_geom().fwd_bands;
         else if (k == "fwd_split_z") *value = P.fwd_split_z();
         else if (k == "fwd_split_lo") *value = P.fwd_split_lo();
+        else if (k == "fwd_stages") *value = (double)P.fwd_stages().size();
         else if (k == "mirror") *value = P.mirror() ? 1 : 0;
         else if (k == "solver_restart") *value = P.solver_restart ? 1 : 0;
         else throw kct::ConfigError("kct_projector_info: unknown key '" + k + "'");

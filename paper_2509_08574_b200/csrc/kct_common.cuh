@@ -116,6 +116,7 @@ struct DevGeom {
     int full_footprint;    // 1: some voxel square is not fully in front of a source
     int fwd_bands;         // forward row bands (32*C rows each) in this launch
     int fwd_band0;         // first row band of this launch
+    int fwd_row0;          // row (mirror: row pair) of band 0's first lane (staged host forward)
     int mirror;            // 1: z-mirror geometry, rows iv / nv-1-iv walked as pairs (fwd_kernel MIR)
 };
 

@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
     const int iu = quad * kFwdWarps + (threadIdx.x >> 5);
     if (iu >= g.nu) return;
     const ColParams cp = cols[(size_t)a * g.nu + iu];
-    const int iv0 = band * (32 * C) + lane;  // row (MIR: pair) of chunk 0
+    const int iv0 = g.fwd_row0 + band * (32 * C) + lane;  // row (MIR: pair) of chunk 0
     const int nz = g.nz;
     const int nrows = MIR ? g.nv / 2 : g.nv;
 
@@ -305,7 +305,8 @@ struct BrickCfg {
     int slab;      // slab-lane deposits (brick_rows_slab): 0 off, 1 on, 2 on with slot-conflict detection
     size_t gstride;  // floats between the partial volumes of groups 1.. (group 0 -> out)
     int out_ref;     // 1: write `out` in the reference layout (x fastest) ...
-    unsigned* level_done;  // ... and count finished bricks per z level (adjoint_host_ref)
+    unsigned* level_done;  // ... and count finished bricks per (z level, y part) (adjoint_host_ref)
+    int nparts;            // y parts per z level of those counters (brick row bj -> bj * nparts / nby)
     int mirror;      // 1: z-mirror brick pairs (adj_mirror_kernel): bricks tile the lower half
                      //    z < 0 (slabs [0, nz/2)), rows iv < nv/2
 };
@@ -806,6 +807,12 @@ __device__ __forceinline__ BrickGeo brick_geo(int brick, const BrickCfg& bc, con
     return B;
 }
 
+// counter of a finished brick in adjoint_host_ref: (z level, y part)
+__device__ __forceinline__ int progress_slot(int brick, const BrickCfg& bc) {
+    const int plane = bc.nbx * bc.nby, bj = (brick / bc.nbx) % bc.nby;
+    return (brick / plane) * bc.nparts + bj * bc.nparts / bc.nby;
+}
+
 // FILL = false: count entries per (brick, angle) into off[b (na + 1) + a];
 // FILL = true: write them from off[] (exclusive prefix sums).  One warp per brick.
 template <bool FILL>
@@ -1047,7 +1054,7 @@ __global__ void __launch_bounds__(kAdjWarps * 32, KCT_ADJ_MINB) adj_brick_kernel
         if (bc.level_done) {
             __threadfence();
             __syncwarp();
-            if (lane == 0) atomicAdd(bc.level_done + brick / (bc.nbx * bc.nby), 1u);
+            if (lane == 0) atomicAdd(bc.level_done + progress_slot(brick, bc), 1u);
         }
     }
     }
@@ -1351,7 +1358,7 @@ __global__ void __launch_bounds__(32, KCT_MIR_MINB) adj_mirror_kernel(
             if (bc.level_done) {
                 __threadfence();
                 __syncwarp();
-                if (lane == 0) atomicAdd(bc.level_done + brick / (bc.nbx * bc.nby), 1u);
+                if (lane == 0) atomicAdd(bc.level_done + progress_slot(brick, bc), 1u);
             }
         }
     }
@@ -1555,7 +1562,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 30 / (NP + 1)) adj_mirror_ws_ke
                 if (bc.level_done) {
                     __threadfence();
                     __syncwarp();
-                    if (lane == 0) atomicAdd(bc.level_done + brick / (bc.nbx * bc.nby), 1u);
+                    if (lane == 0) atomicAdd(bc.level_done + progress_slot(brick, bc), 1u);
                 }
             }
             __syncwarp();
@@ -1766,6 +1773,7 @@ Projector::~Projector() {
     cudaFree(d_vpad_);
     cudaFree(d_cs_);
     cudaFree(d_fhi_);
+    cudaFree(d_fstage_);
     if (pipe_stream_) {
         for (auto e : pipe_ev_) cudaEventDestroy(e);
         cudaEventDestroy(up_ev_);
@@ -2031,6 +2039,71 @@ void Projector::build_tables(const kct_geometry& geom) {
             }
         }
     }
+    // staged host forward (forward_host_staged): row stages of 1, 2, 3, 4, 4,
+    // ... chunks of 32 rows (z-mirror: row pairs) from z = 0 outwards; stage s
+    // runs once the slabs its rays reach are uploaded (centre out), so the
+    // upload of the outer slabs overlaps the inner rows' projection
+    if (pipe_chunks_ > 1) {
+        const char* se = std::getenv("KCT_FWD_STAGED");
+        const int rows = mirror_ ? nv / 2 : nv, T = (rows + 31) / 32;
+        std::vector<int> sizes;
+        for (int t = 0, c = 1; t < T; c = std::min(c + 1, 4)) {
+            sizes.push_back(std::min(c, T - t));
+            t += sizes.back();
+        }
+        auto zrange = [&](int r_end, int& lo, int& hi) {  // slabs of rows (pairs) [0, r_end)
+            const int r1 = std::min(nv, (mirror_ ? nv / 2 : 0) + r_end) - 1;
+            double kmax = -1e30;
+            for (const ColParams& cp : cols) {
+                if (!(cp.w_in < cp.w_out)) continue;
+                const double Gin = cp.g_in, Gout = cp.g_in + (double)(cp.w_out - cp.w_in) / cp.inv_h1;
+                kmax = std::max(kmax, std::max(dvd[r1] * Gin, dvd[r1] * Gout) - grid_.oz / grid_.sz);
+            }
+            hi = std::clamp((int)std::floor(kmax) + 3, 1, nz);
+            lo = mirror_ ? std::max(0, nz - hi) : 0;
+        };
+        int lo0 = 0, hi0 = nz;
+        if (sizes.size() >= 2) zrange(32 * sizes[0], lo0, hi0);
+        if (sizes.size() >= 2 && hi0 - lo0 <= (nz * 6) / 10 && !(se && se[0] == '0')) {
+            const int nq = (nu + kFwdWarps - 1) / kFwdWarps;
+            std::vector<float> chord((size_t)nq * na, 0.f);
+            for (int a = 0; a < na; ++a)
+                for (int iu = 0; iu < nu; ++iu) {
+                    const ColParams& cp = cols[(size_t)a * nu + iu];
+                    chord[(size_t)a * nq + iu / kFwdWarps] += std::max(0.f, cp.w_out - cp.w_in);
+                }
+            std::vector<int> orders;
+            int row0 = 0;
+            for (size_t st = 0; st < sizes.size(); ++st) {
+                const bool last = st + 1 == sizes.size();
+                FwdStage f{};
+                f.row0 = row0;
+                f.C = sizes[st];
+                row0 += 32 * f.C;
+                if (last) { f.z_lo = 0; f.z_hi = nz; }
+                else zrange(row0, f.z_lo, f.z_hi);
+                if (!fstages_.empty()) {  // cumulative ranges
+                    f.z_lo = std::min(f.z_lo, fstages_.back().z_lo);
+                    f.z_hi = std::max(f.z_hi, fstages_.back().z_hi);
+                }
+                f.order_off = orders.size();
+                // items quad + nq * a, longest chords first (last stage: per
+                // pipeline chunk of angles, so chunks finish in turn)
+                std::vector<std::pair<double, int>> key((size_t)nq * na);
+                for (int a = 0; a < na; ++a)
+                    for (int qd = 0; qd < nq; ++qd) {
+                        int ck = 0;
+                        while (last && ck + 1 < pipe_chunks_ && a >= pipe_angle(ck + 1)) ++ck;
+                        key[(size_t)a * nq + qd] = {1e9 * ck - chord[(size_t)a * nq + qd], qd + nq * a};
+                    }
+                std::stable_sort(key.begin(), key.end());
+                for (auto& kv : key) orders.push_back(kv.second);
+                fstages_.push_back(f);
+            }
+            KCT_CUDA(cudaMalloc(&d_fstage_, orders.size() * sizeof(int)));
+            KCT_CUDA(cudaMemcpy(d_fstage_, orders.data(), orders.size() * sizeof(int), cudaMemcpyHostToDevice));
+        }
+    }
     const int kc = (nz + 31) / 32;
     adj_k_ = kc <= 1 ? 1 : kc <= 2 ? 2 : kc <= 4 ? 4 : 8;
 
@@ -2110,6 +2183,15 @@ void Projector::build_tables(const kct_geometry& geom) {
         adj_mbz_ = std::max(1, (half + nbh - 1) / std::max(1, nbh));
     }
 
+    // y parts per z level whose completion the host path tracks separately
+    // (adjoint_host_ref copies a (level, part) out as soon as it is final:
+    // the last level's copy is then mostly overlapped too)
+    {
+        adj_parts_ = 4;
+        if (const char* e = std::getenv("KCT_ADJ_PARTS")) adj_parts_ = std::max(1, std::atoi(e));
+        adj_parts_ = std::min(adj_parts_, (ny + BY - 1) / BY);
+    }
+
     KCT_CUDA(cudaMalloc(&d_cs_, cs_.size() * sizeof(float2)));
     KCT_CUDA(cudaMemcpy(d_cs_, cs_.data(), cs_.size() * sizeof(float2), cudaMemcpyHostToDevice));
     build_walk_table();
@@ -2157,11 +2239,23 @@ void Projector::build_tables(const kct_geometry& geom) {
             // z levels in turn: the detector rows they read stay in L2 (c4 -1%)
             if (z_major) key[b].first += 1e6 * bk;
         }
+        std::vector<std::pair<double, int>> hkey = key;
         std::stable_sort(key.begin(), key.end());
         std::vector<int> order(nb);
         for (int b = 0; b < (int)nb; ++b) order[b] = key[b].second;
-        KCT_CUDA(cudaMalloc(&d_border_, nb * sizeof(int)));
+        KCT_CUDA(cudaMalloc(&d_border_, 2 * nb * sizeof(int)));
         KCT_CUDA(cudaMemcpy(d_border_, order.data(), nb * sizeof(int), cudaMemcpyHostToDevice));
+        // the host path's order: within a level the y parts in turn (it copies
+        // a (level, part) out as soon as it is final), heaviest first in a
+        // part (measured: costs the kernel itself 3%, so device calls keep
+        // the order above)
+        for (int b = 0; b < (int)nb; ++b) {
+            const int bj = (b / nbx) % nby;
+            hkey[b].first += 1e4 * (double)(bj * adj_parts_ / nby);
+        }
+        std::stable_sort(hkey.begin(), hkey.end());
+        for (int b = 0; b < (int)nb; ++b) order[b] = hkey[b].second;
+        KCT_CUDA(cudaMemcpy(d_border_ + nb, order.data(), nb * sizeof(int), cudaMemcpyHostToDevice));
         KCT_CUDA(cudaMalloc(&d_queue_, sizeof(int)));
         // warp-specialised brick pairs (adj_mirror_ws_kernel; KCT_ADJ_WS=0: one warp per pair)
         const char* ws = std::getenv("KCT_ADJ_WS");
@@ -2196,6 +2290,7 @@ BrickCfg Projector::adj_cfg() const {
     bc.nbz = (zext + bc.bz - 1) / bc.bz;
     bc.ngrp = adj_groups_;
     bc.gstride = m_;
+    bc.nparts = adj_parts_;
     return bc;
 }
 
@@ -2431,6 +2526,22 @@ void Projector::forward_counted(float* proj, int band0, unsigned* done, cudaStre
     launch_fwd<false>(fwd_c_, fwd_bands_ - band0, band0, d_vpad_ + kVOff, proj, d_cols_, d_dv_,
                       d_invdv_, d_dvd_, dg_, band0 ? d_fcnt_hi_ : d_fcnt_all_, s, &fc);
 }
+// Stage `stage` of the staged host forward (one band: C chunks from row0),
+// counted per pipeline chunk when `done` is set.
+void Projector::forward_stage(int stage, float* proj, unsigned* done, cudaStream_t s) const {
+    const FwdStage& f = fstages_[stage];
+    DevGeom g = dg_;
+    g.fwd_row0 = f.row0;
+    FwdChunks fc{};
+    if (done) {
+        fc.count = done;
+        fc.n = pipe_chunks_;
+        for (int c = 0; c <= pipe_chunks_; ++c) fc.cb[c] = pipe_angle(c);
+    }
+    launch_fwd<false>(f.C, 1, 0, d_vpad_ + kVOff, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, g,
+                      d_fstage_ + f.order_off, s, done ? &fc : nullptr);
+}
+
 unsigned Projector::fwd_chunk_columns(int c, int band0) const {
     return (unsigned)((pipe_angle(c + 1) - pipe_angle(c)) * dg_.nu * (fwd_bands_ - band0));
 }
@@ -2523,6 +2634,9 @@ void Projector::adjoint_impl(const float* proj, float* vol, int a_begin, int a_e
     bc.out_ref = out_ref ? 1 : 0;
     bc.level_done = level_done;
     const int nctas = (bc.nbx * bc.nby * bc.nbz * bc.ngrp + kAdjWarps - 1) / kAdjWarps;
+    // the host path's brick order (y parts in turn within a z level) when it
+    // tracks progress
+    const int* border = d_border_ && level_done ? d_border_ + (size_t)bc.nbx * bc.nby * bc.nbz : d_border_;
     const size_t smem = adj_smem_bytes();
     for (int a0 = a_begin; a0 < a_end; a0 += kMaxAnglesPerLaunch) {
         const int nab = std::min(kMaxAnglesPerLaunch, a_end - a0);
@@ -2558,20 +2672,20 @@ void Projector::adjoint_impl(const float* proj, float* vol, int a_begin, int a_e
                 (bc.bz == 64 ? adj_mirror_ws_kernel<64, KCT_MIR_NP>
                  : bc.bz == 32 ? adj_mirror_ws_kernel<32, KCT_MIR_NP> : adj_mirror_ws_kernel<0, KCT_MIR_NP>)
                     <<<grid, 32 * (KCT_MIR_NP + 1), smem, s>>>(
-                    yrec, ymw, vol, dg_, bc, a0, nab, accum, d_border_,
+                    yrec, ymw, vol, dg_, bc, a0, nab, accum, border,
                     d_queue_, d_part_, static_cast<const WalkEntry*>(d_tab_), d_off_);
             else if (adj_mir_)
                 (bc.bz == 64 ? adj_mirror_kernel<64> : bc.bz == 32 ? adj_mirror_kernel<32> : adj_mirror_kernel<0>)
                     <<<grid, 32, smem, s>>>(
-                    yrec, ymw, vol, dg_, bc, a0, nab, accum, d_border_,
+                    yrec, ymw, vol, dg_, bc, a0, nab, accum, border,
                     d_queue_, d_part_, static_cast<const WalkEntry*>(d_tab_), d_off_);
             else if (d_tab_)
                 adj_brick_kernel<true><<<grid, kAdjWarps * 32, smem, s>>>(
-                    reinterpret_cast<const float4*>(d_yw_), vol, cols, dg_, bc, d_cs_ + a0, a0, nab, accum, d_border_,
+                    reinterpret_cast<const float4*>(d_yw_), vol, cols, dg_, bc, d_cs_ + a0, a0, nab, accum, border,
                     d_queue_, d_part_, static_cast<const WalkEntry*>(d_tab_), d_off_);
             else
                 adj_brick_kernel<false><<<grid, kAdjWarps * 32, smem, s>>>(
-                    reinterpret_cast<const float4*>(d_yw_), vol, cols, dg_, bc, d_cs_ + a0, a0, nab, accum, d_border_,
+                    reinterpret_cast<const float4*>(d_yw_), vol, cols, dg_, bc, d_cs_ + a0, a0, nab, accum, border,
                     d_queue_, d_part_, nullptr, nullptr);
             if (bc.ngrp > 1) {
                 KCT_LAUNCHED();
@@ -2620,10 +2734,8 @@ bool Projector::adjoint_host_ref(const float* host_proj, float* host, cudaStream
     if (adj_gather_ || adj_groups_ > 1 || dg_.na > kMaxAnglesPerLaunch || !d_queue_ || !wait_value32())
         return false;
     const BrickCfg bcfg = adj_cfg();
-    const int nbz = bcfg.nbz;
-    const unsigned per_level =
-        (unsigned)(((dg_.nx + BX - 1) / BX) * ((dg_.ny + BY - 1) / BY));
-    if (!d_level_) KCT_CUDA(cudaMalloc(&d_level_, (size_t)nbz * sizeof(unsigned)));
+    const int nbz = bcfg.nbz, NP = bcfg.nparts, nslots = nbz * NP;
+    if (!d_level_) KCT_CUDA(cudaMalloc(&d_level_, (size_t)nslots * sizeof(unsigned)));
     const size_t per = (size_t)dg_.nu * dg_.nv;
     float* tmp = scratch(2, n_);  // reference-layout projections
     float* q = scratch(1, n_);    // native projections
@@ -2640,7 +2752,7 @@ bool Projector::adjoint_host_ref(const float* host_proj, float* host, cudaStream
                       ? std::max(1, dg_.na / KCT_ADJ_FIRST_PART)
                       : dg_.na;
     KCT_CUDA(cudaMemcpyAsync(tmp, host_proj, H * per * sizeof(float), cudaMemcpyHostToDevice, s));
-    KCT_CUDA(cudaMemsetAsync(d_level_, 0, (size_t)nbz * sizeof(unsigned), s));
+    KCT_CUDA(cudaMemsetAsync(d_level_, 0, (size_t)nslots * sizeof(unsigned), s));
     KCT_CUDA(cudaEventRecord(pipe_ev_[0], s));  // copy stream: after this call's earlier work
     KCT_CUDA(cudaStreamWaitEvent(sc, pipe_ev_[0], 0));  // and sees the reset counters
     if (H < dg_.na)
@@ -2655,24 +2767,35 @@ bool Projector::adjoint_host_ref(const float* host_proj, float* host, cudaStream
     }
     adjoint_impl(q, dev, H < dg_.na ? H : 0, dg_.na, H < dg_.na, true, d_level_, s);
     const size_t plane = (size_t)dg_.nx * dg_.ny;
+    // (level L, y part q): brick rows bj with bj * NP / nby == q, i.e. voxel
+    // rows [J0, J1) of slabs [k0, k1) (and, with z-mirror pairs, of their
+    // reflection): one strided copy per z range
+    const int nby = bcfg.nby;
+    const size_t zext = adj_mir_ ? dg_.nz / 2 : dg_.nz;
     for (int L = 0; L < nbz; ++L) {
-        const CUresult r = wait_value32()((CUstream)sc, (CUdeviceptr)(d_level_ + L), per_level,
-                                          CU_STREAM_WAIT_VALUE_GEQ);
-        if (r != CUDA_SUCCESS) {  // fall back: whole volume after the kernel
-            KCT_CUDA(cudaStreamSynchronize(s));
-            KCT_CUDA(cudaStreamSynchronize(sc));
-            KCT_CUDA(cudaMemcpy(host, dev, m_ * sizeof(float), cudaMemcpyDeviceToHost));
-            return true;
-        }
-        // level L: slabs [k0, k1) (z-mirror pairs: and their reflection)
-        const size_t zext = adj_mir_ ? dg_.nz / 2 : dg_.nz;
-        const size_t k0 = (size_t)L * bcfg.bz, k1 = std::min(zext, k0 + bcfg.bz);
-        KCT_CUDA(cudaMemcpyAsync(host + k0 * plane, dev + k0 * plane, (k1 - k0) * plane * sizeof(float),
-                                 cudaMemcpyDeviceToHost, sc));
-        if (adj_mir_) {
-            const size_t u0 = dg_.nz - k1;
-            KCT_CUDA(cudaMemcpyAsync(host + u0 * plane, dev + u0 * plane, (k1 - k0) * plane * sizeof(float),
-                                     cudaMemcpyDeviceToHost, sc));
+        for (int q = 0; q < NP; ++q) {
+            const int bj0 = (q * nby + NP - 1) / NP, bj1 = ((q + 1) * nby + NP - 1) / NP;
+            if (bj1 <= bj0) continue;
+            const unsigned want = (unsigned)(bcfg.nbx * (bj1 - bj0));
+            const CUresult r = wait_value32()((CUstream)sc, (CUdeviceptr)(d_level_ + L * NP + q), want,
+                                              CU_STREAM_WAIT_VALUE_GEQ);
+            if (r != CUDA_SUCCESS) {  // fall back: whole volume after the kernel
+                KCT_CUDA(cudaStreamSynchronize(s));
+                KCT_CUDA(cudaStreamSynchronize(sc));
+                KCT_CUDA(cudaMemcpy(host, dev, m_ * sizeof(float), cudaMemcpyDeviceToHost));
+                return true;
+            }
+            const size_t J0 = (size_t)bj0 * BY, J1 = std::min((size_t)dg_.ny, (size_t)bj1 * BY);
+            const size_t k0 = (size_t)L * bcfg.bz, k1 = std::min(zext, k0 + bcfg.bz);
+            const size_t row0 = J0 * dg_.nx, width = (J1 - J0) * dg_.nx * sizeof(float);
+            const size_t pitch = plane * sizeof(float);
+            KCT_CUDA(cudaMemcpy2DAsync(host + k0 * plane + row0, pitch, dev + k0 * plane + row0, pitch,
+                                       width, k1 - k0, cudaMemcpyDeviceToHost, sc));
+            if (adj_mir_) {
+                const size_t u0 = dg_.nz - k1;
+                KCT_CUDA(cudaMemcpy2DAsync(host + u0 * plane + row0, pitch, dev + u0 * plane + row0,
+                                           pitch, width, k1 - k0, cudaMemcpyDeviceToHost, sc));
+            }
         }
     }
     KCT_CUDA(cudaStreamSynchronize(sc));

@@ -72,6 +72,17 @@ class Projector {
     void forward_counted(float* proj, int band0, unsigned* done, cudaStream_t s) const;
     unsigned fwd_chunk_columns(int chunk, int band0) const;
     unsigned* fwd_done() const { return d_fdone_; }
+    // Staged host forward (capi.cu forward_host_staged): stage s covers rows
+    // (z-mirror: row pairs) [row0, row0 + 32 C) of every angle, whose rays stay
+    // inside slabs [z_lo, z_hi); the volume is uploaded stage range by stage
+    // range (centre out) and stage s runs as soon as its slabs are in; the last
+    // stage is counted per pipeline chunk (fwd_done(), (a1 - a0) nu columns).
+    struct FwdStage {
+        int row0, C, z_lo, z_hi;
+        size_t order_off;  // its block order in d_fstage_
+    };
+    const std::vector<FwdStage>& fwd_stages() const { return fstages_; }
+    void forward_stage(int stage, float* proj, unsigned* done, cudaStream_t s) const;
     // enqueue on `sc`: wait until *addr >= value (cuStreamWaitValue32); false
     // when stream memory operations are unavailable (nothing enqueued)
     bool stream_wait_geq(cudaStream_t sc, const unsigned* addr, unsigned value) const;
@@ -148,6 +159,7 @@ class Projector {
     bool adj_mir_ = false;            // z-mirror brick pairs (adj_mirror_kernel)
     bool adj_ws_ = false;             // ... warp-specialised (adj_mirror_ws_kernel)
     int adj_mbz_ = 64;                // ... slabs per lower brick
+    int adj_parts_ = 1;               // y parts per z level of the host path's progress counters
     int* d_border_ = nullptr;         // brick order of the adjoint queue
     int* d_forder_ = nullptr;         // forward block -> item order (longest chords first)
     int* d_fpipe_ = nullptr;          // the same per pipeline chunk (offsets pipe_off_)
@@ -157,6 +169,8 @@ class Projector {
     cudaEvent_t pipe_ev_[kPipeChunks] = {};
     cudaEvent_t up_ev_ = nullptr;
     int fwd_split_z_ = 0, fwd_split_lo_ = 0;
+    std::vector<FwdStage> fstages_;   // staged host forward (empty: not used)
+    int* d_fstage_ = nullptr;         // block orders of the stages
     bool mirror_ = false;             // z-mirror pairs (fwd_kernel MIR, adj_weight_kernel)
     float* d_vpad_ = nullptr;         // padded native volume read by the forward
     float2* d_cs_ = nullptr;          // per-angle (cos, sin) on the device
