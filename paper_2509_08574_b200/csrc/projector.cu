@@ -2047,9 +2047,21 @@ void Projector::build_tables(const kct_geometry& geom) {
         const char* se = std::getenv("KCT_FWD_STAGED");
         const int rows = mirror_ ? nv / 2 : nv, T = (rows + 31) / 32;
         std::vector<int> sizes;
-        for (int t = 0, c = 1; t < T; c = std::min(c + 1, 4)) {
-            sizes.push_back(std::min(c, T - t));
-            t += sizes.back();
+        if (const char* ss = std::getenv("KCT_FWD_STAGE_SIZES")) {  // e.g. "2,4" (sweeps)
+            int t = 0;
+            for (const char* c = ss; *c && t < T;) {
+                const int v = std::clamp(std::atoi(c), 1, 4);
+                sizes.push_back(std::min(v, T - t));
+                t += sizes.back();
+                while (*c && *c != ',') ++c;
+                if (*c == ',') ++c;
+            }
+            while (t < T) sizes.push_back(std::min(4, T - t)), t += sizes.back();
+        } else {
+            for (int t = 0, c = 1; t < T; c = std::min(c + 1, 4)) {
+                sizes.push_back(std::min(c, T - t));
+                t += sizes.back();
+            }
         }
         auto zrange = [&](int r_end, int& lo, int& hi) {  // slabs of rows (pairs) [0, r_end)
             const int r1 = std::min(nv, (mirror_ ? nv / 2 : 0) + r_end) - 1;
