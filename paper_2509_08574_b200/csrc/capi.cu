@@ -398,6 +398,7 @@ int kct_projector_info(const kct_projector* h, const char* key, double* value) {
         else if (k == "fwd_split_z") *value = P.fwd_split_z();
         else if (k == "fwd_split_lo") *value = P.fwd_split_lo();
         else if (k == "fwd_stages") *value = (double)P.fwd_stages().size();
+        else if (k == "fwd_table_segments") *value = (double)P.fwd_table_segments();
         else if (k == "mirror") *value = P.mirror() ? 1 : 0;
         else if (k == "solver_restart") *value = P.solver_restart ? 1 : 0;
         else throw kct::ConfigError("kct_projector_info: unknown key '" + k + "'");

@@ -59,6 +59,73 @@ struct FwdChunks {
 };
 static_assert(Projector::kPipeChunks <= 8, "FwdChunks holds at most 8 pipeline chunks");
 
+// The xy Siddon walk of one (angle, column) through the padded volume's
+// voxel columns: seg(wa, wb, col) for every segment [wa, wb] of voxel column
+// col = (i + nx j) * vpad_stride(nz), in ray order (projector.hpp:116-129
+// restricted to the x / y planes).  Shared by the forward and its walk table.
+template <class F>
+__device__ __forceinline__ void xy_walk(const ColParams& cp, const DevGeom& g, F&& seg) {
+    const int nx = g.nx, ny = g.ny;
+    int i = cp.i0, j = cp.j0;
+    const int stx = cp.dx > 0.0 ? 1 : -1, sty = cp.dy > 0.0 ? 1 : -1;
+    int px = cp.dx > 0.0 ? i + 1 : i;
+    int py = cp.dy > 0.0 ? j + 1 : j;
+    float wnx = cp.dx != 0.0 ? xcross(cp, px) : kInf;
+    float wny = cp.dy != 0.0 ? ycross(cp, py) : kInf;
+    float wcur = cp.w_in;
+    for (;;) {
+        const bool stepx = wnx <= wny;
+        const float wnext = stepx ? wnx : wny;
+        const float wb = fmaxf(fminf(wnext, cp.w_out), wcur);
+        // the column's slab 0 in the padded volume (zero slabs at -1 and nz:
+        // slabs k in [-1, nz] need no range check; 32-bit element index)
+        seg(wcur, wb, (i + nx * j) * vpad_stride(g.nz));
+        if (wnext >= cp.w_out) break;
+        wcur = fmaxf(wnext, wcur);
+        if (stepx) {
+            i += stx;
+            if ((unsigned)i >= (unsigned)nx) break;
+            px += stx;
+            wnx = xcross(cp, px);
+        } else {
+            j += sty;
+            if ((unsigned)j >= (unsigned)ny) break;
+            py += sty;
+            wny = ycross(cp, py);
+        }
+    }
+}
+
+// Forward walk table (TAB): per (angle, column) the segments of xy_walk as
+// {bits of wb, col}, segment s of column (a, iu) at seg[off[a nu + iu] + s]
+// (a segment starts where the previous one ends; the first at w_in).
+}  // namespace
+struct FwdTab {
+    const unsigned* off;
+    const int2* seg;
+};
+namespace {
+
+// FILL = false: segment counts per column into cnt; true: write them at off.
+template <bool FILL>
+__global__ void __launch_bounds__(128) fwd_tab_build(const ColParams* __restrict__ cols, DevGeom g,
+                                                     unsigned* __restrict__ cnt,
+                                                     const unsigned* __restrict__ off,
+                                                     int2* __restrict__ seg) {
+    const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (t >= (size_t)g.na * g.nu) return;
+    const ColParams cp = cols[t];
+    unsigned n = 0;
+    if (cp.w_in < cp.w_out) {
+        int2* o = FILL ? seg + off[t] : nullptr;
+        xy_walk(cp, g, [&](float, float wb, int col) {
+            if (FILL) o[n] = make_int2(__float_as_int(wb), col);
+            ++n;
+        });
+    }
+    if (!FILL) cnt[t] = n;
+}
+
 // vol: slab 0 of voxel column 0 of the padded native volume (column stride
 // nz + 2, zero slabs at -1 and nz; Projector::pad_volume).
 //
@@ -72,7 +139,7 @@ static_assert(Projector::kPipeChunks <= 8, "FwdChunks holds at most 8 pipeline c
 // its zcross gives these values, adj_weight_kernel), so per xy segment and per
 // z crossing one test serves two rays, which load slabs k and nz-1-k.  Pairs
 // are numbered from the centre plane outwards (band 0: the rows nearest z = 0).
-template <int C, bool COUNT, bool DONE = false, bool MIR = false>
+template <int C, bool COUNT, bool DONE = false, bool MIR = false, bool TAB = false>
 __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const float* __restrict__ vol,
                                                   float* __restrict__ out,
                                                   const ColParams* __restrict__ cols,
@@ -80,7 +147,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
                                                   const float* __restrict__ invdv,
                                                   const double* __restrict__ dvd, DevGeom g,
                                                   const int* __restrict__ order,
-                                                  FwdChunks done) {
+                                                  FwdChunks done, FwdTab tab) {
     // blocks are dispatched in index order; `order` maps them to (angle, row
     // band, column quad) items longest-chord first, so the last wave holds
     // the shortest rays (no long tail, notably with few angles per GPU)
@@ -135,22 +202,8 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
     // rows that all pass above / below the volume (detector overhang, c4)
     // skip the walk: their line integrals are 0
     if (cp.w_in < cp.w_out && __any_sync(kFull, hit)) {
-        const int nx = g.nx, ny = g.ny;
-        int i = cp.i0, j = cp.j0;
-        const int stx = cp.dx > 0.0 ? 1 : -1, sty = cp.dy > 0.0 ? 1 : -1;
-        int px = cp.dx > 0.0 ? i + 1 : i;
-        int py = cp.dy > 0.0 ? j + 1 : j;
-        float wnx = cp.dx != 0.0 ? xcross(cp, px) : kInf;
-        float wny = cp.dy != 0.0 ? ycross(cp, py) : kInf;
-        float wcur = cp.w_in;
-        for (;;) {
-            const bool stepx = wnx <= wny;
-            const float wnext = stepx ? wnx : wny;
-            const float wb = fmaxf(fminf(wnext, cp.w_out), wcur);
-            // the column's slab 0 in the padded volume (zero slabs at -1 and
-            // nz: slabs k in [-1, nz] need no range check)
-            // (32-bit element index: one IMAD.WIDE per load)
-            const int col = (i + nx * j) * vpad_stride(nz);
+        // one xy segment [wcur, wb] of padded voxel column col, all rows
+        auto segment = [&](float wcur, float wb, int col) {
             const int colm = col + nz - 1;  // MIR: slab nz-1-k at colm - k
             float v[C], vm[C], wa[C];
 #pragma unroll
@@ -189,19 +242,23 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
                     if (MIR) accm[c] = __fmaf_rn(len, vm[c], accm[c]);
                 }
             }
-            if (wnext >= cp.w_out) break;
-            wcur = fmaxf(wnext, wcur);
-            if (stepx) {
-                i += stx;
-                if ((unsigned)i >= (unsigned)nx) break;
-                px += stx;
-                wnx = xcross(cp, px);
-            } else {
-                j += sty;
-                if ((unsigned)j >= (unsigned)ny) break;
-                py += sty;
-                wny = ycross(cp, py);
+        };
+        if (TAB) {
+            // the column's walk from the table (fwd_tab_build: the segments
+            // xy_walk produces), 32 segments per coalesced load, broadcast
+            const unsigned s0 = tab.off[(size_t)a * g.nu + iu], s1 = tab.off[(size_t)a * g.nu + iu + 1];
+            float wcur = cp.w_in;
+            for (unsigned sb = s0; sb < s1; sb += 32) {
+                const int2 e = sb + lane < s1 ? __ldg(tab.seg + sb + lane) : make_int2(0, 0);
+                const int ns = (int)min(32u, s1 - sb);
+                for (int t = 0; t < ns; ++t) {
+                    const float wb = __int_as_float(__shfl_sync(kFull, e.x, t));
+                    segment(wcur, wb, __shfl_sync(kFull, e.y, t));
+                    wcur = wb;
+                }
             }
+        } else {
+            xy_walk(cp, g, segment);
         }
     }
 
@@ -1774,6 +1831,8 @@ Projector::~Projector() {
     cudaFree(d_cs_);
     cudaFree(d_fhi_);
     cudaFree(d_fstage_);
+    cudaFree(d_ftab_off_);
+    cudaFree(d_ftab_);
     if (pipe_stream_) {
         for (auto e : pipe_ev_) cudaEventDestroy(e);
         cudaEventDestroy(up_ev_);
@@ -2208,6 +2267,7 @@ void Projector::build_tables(const kct_geometry& geom) {
     KCT_CUDA(cudaMemcpy(d_cs_, cs_.data(), cs_.size() * sizeof(float2), cudaMemcpyHostToDevice));
     build_walk_table();
     if (!d_tab_) adj_mir_ = false;  // the pair kernel streams the walk table
+    build_fwd_table();
 
     const BrickCfg bcfg = adj_cfg();
     const long nb = (long)bcfg.nbx * bcfg.nby * bcfg.nbz;
@@ -2357,6 +2417,46 @@ void Projector::build_walk_table() {
     tab_entries_ = tot;
 }
 
+// Forward walk table (fwd_tab_build): every (angle, column)'s xy segments,
+// 8 bytes each (c3: 8.2 M segments = 66 MB), built once per projector; the
+// forward then loads 32 segments per coalesced load instead of stepping the
+// walk (plane crossings in float64, voxel indices, exits) per segment.
+// Skipped (on-the-fly walks) with KCT_FWD_TABLE=0, or above the budget
+// KCT_FWD_TABLE_MB (default an eighth of the free device memory).
+void Projector::build_fwd_table() {
+    const char* en = std::getenv("KCT_FWD_TABLE");
+    if (en && en[0] == '0') return;
+    const size_t ncol = (size_t)dg_.na * dg_.nu;
+    unsigned* cnt = nullptr;
+    KCT_CUDA(cudaMalloc(&cnt, ncol * sizeof(unsigned)));
+    const unsigned blocks = (unsigned)((ncol + 127) / 128);
+    fwd_tab_build<false><<<blocks, 128>>>(d_cols_, dg_, cnt, nullptr, nullptr);
+    KCT_LAUNCHED();
+    std::vector<unsigned> c(ncol);
+    KCT_CUDA(cudaMemcpy(c.data(), cnt, ncol * sizeof(unsigned), cudaMemcpyDeviceToHost));
+    cudaFree(cnt);
+    std::vector<unsigned> off(ncol + 1);
+    unsigned long long tot = 0;
+    for (size_t t = 0; t < ncol; ++t) {
+        off[t] = (unsigned)tot;
+        tot += c[t];
+    }
+    off[ncol] = (unsigned)tot;
+    size_t free_b = 0, total_b = 0;
+    KCT_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    size_t budget = free_b / 8;
+    if (const char* e = std::getenv("KCT_FWD_TABLE_MB")) budget = (size_t)std::atoll(e) << 20;
+    if (tot == 0 || tot >= (1ull << 32) || tot * sizeof(int2) > budget) return;
+    KCT_CUDA(cudaMalloc(&d_ftab_off_, (ncol + 1) * sizeof(unsigned)));
+    KCT_CUDA(cudaMemcpy(d_ftab_off_, off.data(), (ncol + 1) * sizeof(unsigned), cudaMemcpyHostToDevice));
+    KCT_CUDA(cudaMalloc(&d_ftab_, tot * sizeof(int2)));
+    fwd_tab_build<true><<<blocks, 128>>>(d_cols_, dg_, nullptr, d_ftab_off_,
+                                         static_cast<int2*>(d_ftab_));
+    KCT_LAUNCHED();
+    KCT_CUDA(cudaDeviceSynchronize());
+    ftab_segs_ = tot;
+}
+
 size_t Projector::adj_smem_bytes() const {
     if (adj_ws_) return (size_t)adj_mir_ws_floats(adj_mbz_, KCT_MIR_NP) * sizeof(float);
     if (adj_mir_) return (size_t)adj_mir_floats(adj_mbz_) * sizeof(float);
@@ -2452,27 +2552,27 @@ __global__ void __launch_bounds__(256) adj_group_sum(float* __restrict__ out,
 }
 
 // ---- launches -----------------------------------------------------------------
-template <bool COUNT, bool MIR>
-static void launch_fwd_t(int C, int bands, int band0, const float* vol, float* out,
+template <bool COUNT, bool MIR, bool DONE, bool TAB>
+static void launch_fwd_c(int C, dim3 g1, int th, cudaStream_t s, const float* vol, float* out,
                          const ColParams* cols, const float* dv, const float* invdv,
-                         const double* dvd, const DevGeom& g, const int* order, cudaStream_t s,
-                         const FwdChunks* done);
-
-template <bool COUNT>
-static void launch_fwd(int C, int bands, int band0, const float* vol, float* out, const ColParams* cols,
-                       const float* dv, const float* invdv, const double* dvd, const DevGeom& g,
-                       const int* order, cudaStream_t s, const FwdChunks* done = nullptr) {
-    if (g.mirror)
-        launch_fwd_t<COUNT, true>(C, bands, band0, vol, out, cols, dv, invdv, dvd, g, order, s, done);
-    else
-        launch_fwd_t<COUNT, false>(C, bands, band0, vol, out, cols, dv, invdv, dvd, g, order, s, done);
+                         const double* dvd, const DevGeom& gg, const int* order, const FwdChunks& fc,
+                         const FwdTab& tab) {
+    switch (C) {
+    case 1: fwd_kernel<1, COUNT, DONE, MIR, TAB><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc, tab); break;
+    case 2: fwd_kernel<2, COUNT, DONE, MIR, TAB><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc, tab); break;
+    case 3: fwd_kernel<3, COUNT, DONE, MIR, TAB><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc, tab); break;
+    default: fwd_kernel<4, COUNT, DONE, MIR, TAB><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc, tab); break;
+    }
+    KCT_LAUNCHED();
 }
 
+// tab.off == nullptr: walk the columns on the fly; tab.off / cols point at
+// the launch's first angle.
 template <bool COUNT, bool MIR>
 static void launch_fwd_t(int C, int bands, int band0, const float* vol, float* out,
                          const ColParams* cols, const float* dv, const float* invdv,
                          const double* dvd, const DevGeom& g, const int* order, cudaStream_t s,
-                         const FwdChunks* done) {
+                         const FwdChunks* done, const FwdTab& tab) {
     // 1D grid over (angle, band, column quad) items
     const unsigned nq = (unsigned)((g.nu + kFwdWarps - 1) / kFwdWarps);
     const dim3 g1(nq * (unsigned)bands * (unsigned)g.na, 1, 1);
@@ -2482,23 +2582,31 @@ static void launch_fwd_t(int C, int bands, int band0, const float* vol, float* o
     gg.fwd_band0 = band0;
     FwdChunks fc{};
     if (done) fc = *done;
+    const bool tb = !COUNT && tab.off;
     if (!COUNT && done) {  // host pipeline (counted launch)
-        switch (C) {
-        case 1: fwd_kernel<1, false, true, MIR><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
-        case 2: fwd_kernel<2, false, true, MIR><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
-        case 3: fwd_kernel<3, false, true, MIR><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
-        default: fwd_kernel<4, false, true, MIR><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
-        }
-        KCT_LAUNCHED();
+        if (tb) launch_fwd_c<false, MIR, true, true>(C, g1, th, s, vol, out, cols, dv, invdv, dvd, gg, order, fc, tab);
+        else launch_fwd_c<false, MIR, true, false>(C, g1, th, s, vol, out, cols, dv, invdv, dvd, gg, order, fc, tab);
         return;
     }
-    switch (C) {
-    case 1: fwd_kernel<1, COUNT, false, MIR><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
-    case 2: fwd_kernel<2, COUNT, false, MIR><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
-    case 3: fwd_kernel<3, COUNT, false, MIR><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
-    default: fwd_kernel<4, COUNT, false, MIR><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc); break;
-    }
-    KCT_LAUNCHED();
+    if (tb) launch_fwd_c<false, MIR, false, true>(C, g1, th, s, vol, out, cols, dv, invdv, dvd, gg, order, fc, tab);
+    else launch_fwd_c<COUNT, MIR, false, false>(C, g1, th, s, vol, out, cols, dv, invdv, dvd, gg, order, fc, tab);
+}
+
+template <bool COUNT>
+static void launch_fwd(int C, int bands, int band0, const float* vol, float* out, const ColParams* cols,
+                       const float* dv, const float* invdv, const double* dvd, const DevGeom& g,
+                       const int* order, cudaStream_t s, const FwdChunks* done = nullptr,
+                       const FwdTab& tab = FwdTab{nullptr, nullptr}) {
+    if (g.mirror)
+        launch_fwd_t<COUNT, true>(C, bands, band0, vol, out, cols, dv, invdv, dvd, g, order, s, done, tab);
+    else
+        launch_fwd_t<COUNT, false>(C, bands, band0, vol, out, cols, dv, invdv, dvd, g, order, s, done, tab);
+}
+
+// the forward walk table from angle a on (none: FwdTab{} -> on-the-fly walks)
+FwdTab Projector::ftab(int a) const {
+    if (!d_ftab_off_) return FwdTab{nullptr, nullptr};
+    return FwdTab{d_ftab_off_ + (size_t)a * dg_.nu, reinterpret_cast<const int2*>(d_ftab_)};
 }
 
 void Projector::forward(const float* vol, float* proj, cudaStream_t s) const {
@@ -2516,7 +2624,8 @@ void Projector::forward_range(const float* vol, float* proj, int a_begin, int a_
 // stay below slab fwd_split_z_) for all angles, or bands 1.. for angles
 // [a_begin, a_end) — with the block orders built for these launches.
 void Projector::forward_split_lo(float* proj, cudaStream_t s) const {
-    launch_fwd<false>(fwd_c_, 1, 0, d_vpad_ + kVOff, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_, d_flo_, s);
+    launch_fwd<false>(fwd_c_, 1, 0, d_vpad_ + kVOff, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, dg_, d_flo_, s,
+                      nullptr, ftab(0));
 }
 void Projector::forward_split_hi(float* proj, int c, cudaStream_t s) const {
     const int a0 = pipe_angle(c), a1 = pipe_angle(c + 1);
@@ -2524,7 +2633,7 @@ void Projector::forward_split_hi(float* proj, int c, cudaStream_t s) const {
     g.na = a1 - a0;
     launch_fwd<false>(fwd_c_, fwd_bands_ - 1, 1, d_vpad_ + kVOff, proj + (size_t)a0 * dg_.nu * dg_.nv,
                       d_cols_ + (size_t)a0 * dg_.nu, d_dv_, d_invdv_, d_dvd_, g,
-                      d_fhi_ + fhi_off_[c], s);
+                      d_fhi_ + fhi_off_[c], s, nullptr, ftab(a0));
 }
 // Host pipeline, one launch: bands band0.. of every angle in chunk-major
 // block order, counting finished columns per pipeline chunk into `done`
@@ -2536,7 +2645,7 @@ void Projector::forward_counted(float* proj, int band0, unsigned* done, cudaStre
     fc.n = pipe_chunks_;
     for (int c = 0; c <= pipe_chunks_; ++c) fc.cb[c] = pipe_angle(c);
     launch_fwd<false>(fwd_c_, fwd_bands_ - band0, band0, d_vpad_ + kVOff, proj, d_cols_, d_dv_,
-                      d_invdv_, d_dvd_, dg_, band0 ? d_fcnt_hi_ : d_fcnt_all_, s, &fc);
+                      d_invdv_, d_dvd_, dg_, band0 ? d_fcnt_hi_ : d_fcnt_all_, s, &fc, ftab(0));
 }
 // Stage `stage` of the staged host forward (one band: C chunks from row0),
 // counted per pipeline chunk when `done` is set.
@@ -2551,7 +2660,7 @@ void Projector::forward_stage(int stage, float* proj, unsigned* done, cudaStream
         for (int c = 0; c <= pipe_chunks_; ++c) fc.cb[c] = pipe_angle(c);
     }
     launch_fwd<false>(f.C, 1, 0, d_vpad_ + kVOff, proj, d_cols_, d_dv_, d_invdv_, d_dvd_, g,
-                      d_fstage_ + f.order_off, s, done ? &fc : nullptr);
+                      d_fstage_ + f.order_off, s, done ? &fc : nullptr, ftab(0));
 }
 
 unsigned Projector::fwd_chunk_columns(int c, int band0) const {
@@ -2606,7 +2715,8 @@ void Projector::forward_padded(float* proj, int a_begin, int a_end, cudaStream_t
     DevGeom g = dg_;
     g.na = a_end - a_begin;
     launch_fwd<false>(fwd_c_, fwd_bands_, 0, d_vpad_ + kVOff, proj + (size_t)a_begin * dg_.nu * dg_.nv,
-                      d_cols_ + (size_t)a_begin * dg_.nu, d_dv_, d_invdv_, d_dvd_, g, order, s);
+                      d_cols_ + (size_t)a_begin * dg_.nu, d_dv_, d_invdv_, d_dvd_, g, order, s, nullptr,
+                      ftab(a_begin));
 }
 
 cudaStream_t Projector::pipe_stream() {

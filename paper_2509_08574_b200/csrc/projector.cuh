@@ -14,6 +14,7 @@
 namespace kct {
 
 struct BrickCfg;  // adjoint brick configuration (projector.cu)
+struct FwdTab;    // forward walk table view (projector.cu)
 
 class Projector {
   public:
@@ -130,12 +131,15 @@ class Projector {
     int adj_mirror_bz() const { return adj_mbz_; }
     int adj_groups() const { return adj_groups_; }
     unsigned long long walk_entries() const { return tab_entries_; }
+    unsigned long long fwd_table_segments() const { return ftab_segs_; }
 
   private:
     void build_tables(const kct_geometry& geom);
     size_t adj_smem_bytes() const;
     BrickCfg adj_cfg() const;
     void build_walk_table();
+    void build_fwd_table();
+    FwdTab ftab(int a) const;
     void adjoint_impl(const float* proj, float* vol, int a_begin, int a_end, bool accumulate,
                       bool out_ref, unsigned* level_done, cudaStream_t s) const;
 
@@ -170,6 +174,9 @@ class Projector {
     cudaEvent_t up_ev_ = nullptr;
     int fwd_split_z_ = 0, fwd_split_lo_ = 0;
     std::vector<FwdStage> fstages_;   // staged host forward (empty: not used)
+    unsigned* d_ftab_off_ = nullptr;  // forward walk table: segment offsets [angle][column + 1]
+    void* d_ftab_ = nullptr;          // ... segments (int2: bits of wb, padded column)
+    unsigned long long ftab_segs_ = 0;
     int* d_fstage_ = nullptr;         // block orders of the stages
     bool mirror_ = false;             // z-mirror pairs (fwd_kernel MIR, adj_weight_kernel)
     float* d_vpad_ = nullptr;         // padded native volume read by the forward

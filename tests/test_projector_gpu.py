@@ -622,3 +622,35 @@ def test_staged_host_forward_is_bitwise(monkeypatch, cfg, n_angles):
     B = projector(grid, geom)
     assert B.info("fwd_stages") == 0
     assert np.array_equal(B.apply(x2), staged)
+
+
+@pytest.mark.parametrize("cfg,n_angles", [(1, 64), (2, 9), (3, 6), (4, 2), (5, 5)])
+def test_forward_walk_table_bitwise(monkeypatch, cfg, n_angles):
+    """The forward's xy walks from the precomputed walk table (fwd_tab_build:
+    the same xy_walk, stored) give the on-the-fly walk's bits
+    (KCT_FWD_TABLE=0), device-resident and through the host pipeline."""
+    grid, geom = baseline_geometry(cfg, n_angles=n_angles)
+    x = np.random.default_rng(57).uniform(0, 0.04, grid.count).astype(np.float32)
+    A = projector(grid, geom)
+    assert A.info("fwd_table_segments") > 0
+    tab = A.apply(x)
+    monkeypatch.setenv("KCT_FWD_TABLE", "0")
+    B = projector(grid, geom)
+    assert B.info("fwd_table_segments") == 0
+    assert np.array_equal(B.apply(x), tab)
+
+
+def test_forward_walk_table_awkward(monkeypatch, ora):
+    """Walk table on the awkward geometry (partial columns, offsets, odd sizes,
+    a non-mirror detector): oracle parity and the on-the-fly walk's bits."""
+    from tests._util import Geometry, Grid
+    grid = Grid(37, 29, 53, 0.9, 1.1, 1.3)
+    angles = np.sort(np.random.default_rng(5).uniform(0, 2 * np.pi, 24))
+    geom = Geometry(600.0, 900.0, 61, 75, 1.2, 1.25, angles, 0.7, -0.9)
+    x = np.random.default_rng(6).uniform(0, 1, grid.count).astype(np.float32)
+    A = projector(grid, geom)
+    assert A.info("fwd_table_segments") > 0
+    tab = A.apply(x)
+    assert rel_l2(tab, ora.forward(grid, geom, x)) < TOL
+    monkeypatch.setenv("KCT_FWD_TABLE", "0")
+    assert np.array_equal(projector(grid, geom).apply(x), tab)
