@@ -1273,6 +1273,77 @@ __device__ __forceinline__ void mir_deposits(float4* acc, const float4* segs, in
     __syncwarp();
 }
 
+// Zero one table buffer (tX: CS + 1 float4, tH: CS float2).
+__device__ __forceinline__ void mir_clear(float2* tH, float4* tX, int CS, int lane) {
+    for (int j = lane; j <= CS; j += 32) {
+        tX[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j < CS) tH[j] = make_float2(0.f, 0.f);
+    }
+    __syncwarp();
+}
+
+// mir_deposits for NC consumer warps of the warp-specialised kernel:
+// consumer c0 owns the voxel columns ij with ij % NC == c0 and takes the
+// segments in them (so consumers never touch one column, even when one runs
+// an entry ahead of another, and each column's deposits keep entry order);
+// the tables are read only (the producer clears a buffer before refilling
+// it).  Same arithmetic per voxel.
+template <int RC>
+__device__ __forceinline__ void mir_deposits_nc(float4* acc, const float4* segs, int nseg, int NS,
+                                                int lane, const float2* tH, const float4* tX,
+                                                int xodd, int c0, int NC) {
+    float4 h[RC], xA[RC], xB[RC], xC[RC];
+    bool xs[RC], on[RC];
+    const float4* const tH4 = reinterpret_cast<const float4*>(tH);
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < RC; ++r) {
+        const int j = 2 * lane + 64 * r;
+        on[r] = j < NS;
+        h[r] = xA[r] = xB[r] = xC[r] = z4;
+        if (on[r]) {
+            h[r] = tH4[lane + 32 * r];
+            xA[r] = tX[lane + 32 * r];
+            xB[r] = tX[xodd + lane + 32 * r];
+            xC[r] = tX[lane + 1 + 32 * r];
+        }
+        xs[r] = __any_sync(kFull, xA[r].y != 0.f || xA[r].z != 0.f || xB[r].y != 0.f ||
+                                      xB[r].z != 0.f || xC[r].y != 0.f || xC[r].z != 0.f);
+    }
+    for (int sgi = 0; sgi < nseg; ++sgi) {
+        const float4 sg = segs[sgi];
+        if (__float_as_int(sg.w) % NC != c0) continue;
+        const float wa = sg.x, wb = sg.y;
+        float4* const a = acc + (__float_as_int(sg.z) + lane);
+        const float d = wb - wa;
+        float4 v[RC];
+#pragma unroll
+        for (int r = 0; r < RC; ++r) v[r] = on[r] ? a[32 * r] : z4;
+#pragma unroll
+        for (int r = 0; r < RC; ++r) {
+            if (xs[r]) {
+                const float cA = fminf(fmaxf(xA[r].x, wa), wb);
+                const float cB = fminf(fmaxf(xB[r].x, wa), wb);
+                const float cC = fminf(fmaxf(xC[r].x, wa), wb);
+                const float tbA = cA - wa, taA = wb - cB, tbB = cB - wa, taB = wb - cC;
+                v[r].x = __fmaf_rn(d, h[r].x, __fmaf_rn(tbA, xA[r].y, __fmaf_rn(taA, xB[r].y, v[r].x)));
+                v[r].y = __fmaf_rn(d, h[r].y, __fmaf_rn(tbA, xA[r].z, __fmaf_rn(taA, xB[r].z, v[r].y)));
+                v[r].z = __fmaf_rn(d, h[r].z, __fmaf_rn(tbB, xB[r].y, __fmaf_rn(taB, xC[r].y, v[r].z)));
+                v[r].w = __fmaf_rn(d, h[r].w, __fmaf_rn(tbB, xB[r].z, __fmaf_rn(taB, xC[r].z, v[r].w)));
+            } else {
+                v[r].x = __fmaf_rn(d, h[r].x, v[r].x);
+                v[r].y = __fmaf_rn(d, h[r].y, v[r].y);
+                v[r].z = __fmaf_rn(d, h[r].z, v[r].z);
+                v[r].w = __fmaf_rn(d, h[r].w, v[r].w);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < RC; ++r)
+            if (on[r]) a[32 * r] = v[r];
+    }
+    __syncwarp();
+}
+
 #ifndef KCT_MIR_MINB
 #define KCT_MIR_MINB 20  // 11 KB of shared memory per warp at 64-slab bricks: <= 20 warps per SM
 #endif
@@ -1459,13 +1530,19 @@ __host__ __device__ constexpr int adj_mir_ws_floats(int bz, int np) {
 }
 
 #ifndef KCT_MIR_NP
-#define KCT_MIR_NP 2  // producer warps per consumer warp (classification is the longer half)
+#define KCT_MIR_NP 2  // producer warps (decode + classification)
+#endif
+#ifndef KCT_MIR_NC
+#define KCT_MIR_NC 1  // consumer warps (deposits; 2 / 3 measured slower: 2.51 / 3.14 ms at c3)
 #endif
 // NP producer warps take the entries of an item in turn (global entry g ->
-// producer g % NP), each into its own two buffers (g % (2 NP)); the consumer
-// deposits them in entry order.
-template <int CSC, int NP>
-__global__ void __launch_bounds__(32 * (NP + 1), 30 / (NP + 1)) adj_mirror_ws_kernel(
+// producer g % NP), each into its own two buffers (g % (2 NP)) which it
+// clears before refilling; the NC consumer warps deposit every entry in
+// entry order, consumer c the segments in its voxel columns (ij % NC == c),
+// and share the bricks' clear and write-out (a named barrier between the
+// consumers orders them around the deposits).
+template <int CSC, int NP, int NC>
+__global__ void __launch_bounds__(32 * (NP + NC), 32 / (NP + NC)) adj_mirror_ws_kernel(
     const float4* __restrict__ rec, const float* __restrict__ ymw, float* __restrict__ out,
     DevGeom g, BrickCfg bc, int a0, int nab, int accumulate, const int* __restrict__ order,
     int* queue, float* __restrict__ out_part, const WalkEntry* __restrict__ tab,
@@ -1476,11 +1553,16 @@ __global__ void __launch_bounds__(32 * (NP + 1), 30 / (NP + 1)) adj_mirror_ws_ke
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const bool producer = warp < NP;
+    const int cw = warp - NP;  // consumer index (>= 0)
     const int nbricks = bc.nbx * bc.nby * bc.nbz;
     const int CS = CSC ? CSC : (bc.bz + 1) & ~1;
     const int nu = g.nu, nv = g.nv, nz = g.nz;
     float2* const acc = reinterpret_cast<float2*>(sm);
     float* const bufbase = sm + 2 * BX * BY * CS;
+    auto consumers_sync = [&]() {  // named barrier 1: the NC consumer warps
+        if (NC > 1) asm volatile("bar.sync 1, %0;" ::"n"(32 * NC) : "memory");
+        else __syncwarp();
+    };
     const int BF = mir_buf_floats(CS);
     int* const s_item = reinterpret_cast<int*>(bufbase + NB * BF);  // [2]
     // mbarriers full[0..NB), empty[0..NB) (8-byte aligned)
@@ -1498,7 +1580,8 @@ __global__ void __launch_bounds__(32 * (NP + 1), 30 / (NP + 1)) adj_mirror_ws_ke
                 tX_of(b)[j] = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (j < CS) tH_of(b)[j] = make_float2(0.f, 0.f);
             }
-        if (warp == 0 && lane < 2 * NB) mbar_init(mb + 8u * (unsigned)lane, 32);
+        // full[b]: the producer's 32 lanes arrive; empty[b]: every consumer's
+        if (warp == 0 && lane < 2 * NB) mbar_init(mb + 8u * (unsigned)lane, lane < NB ? 32 : 32 * NC);
     }
     __syncthreads();
     unsigned gcount = 0;  // entries of earlier items (entry g: buffer g % NB)
@@ -1541,7 +1624,10 @@ __global__ void __launch_bounds__(32 * (NP + 1), 30 / (NP + 1)) adj_mirror_ws_ke
                 const unsigned gi = gcount + (unsigned)(e - e0);
                 const int b = (int)(gi % NB);
                 // the consumer is done with b (its use gi / NB - 1)
-                if (gi >= (unsigned)NB) mbar_wait(empty_of(b), (gi / NB - 1u) & 1u);
+                if (gi >= (unsigned)NB) {
+                    mbar_wait(empty_of(b), (gi / NB - 1u) & 1u);
+                    if (NC > 1) mir_clear(tH_of(b), tX_of(b), CS, lane);
+                }
                 float4* const segs = segs_of(b);
                 const unsigned ijw1 = __shfl_sync(kFull, w, M - 1);
                 const int nseg = (int)(ijw1 >> 24);
@@ -1556,7 +1642,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 30 / (NP + 1)) adj_mirror_ws_ke
                 const float inv_h1 = __uint_as_float(__shfl_sync(kFull, w, M + 3));
                 if (lane < nseg) {
                     const int ij = (int)((ijw >> (8 * (lane & 3))) & 0xffu);
-                    segs[lane] = make_float4(wa, wb, __int_as_float(ij * (CS / 2)), 0.f);
+                    segs[lane] = make_float4(wa, wb, __int_as_float(ij * (CS / 2)), __int_as_float(ij));
                 }
                 if (lane == 0) *meta_of(b) = nseg;
                 const unsigned w2 = ld_entry(e + 2 * NP);
@@ -1573,23 +1659,32 @@ __global__ void __launch_bounds__(32 * (NP + 1), 30 / (NP + 1)) adj_mirror_ws_ke
                 ym = ym1;
             }
         } else {
-            for (int q = lane; q < BX * BY * CS / 2; q += 32) sm4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-            __syncwarp();
+            for (int q = lane + 32 * cw; q < BX * BY * CS / 2; q += 32 * NC)
+                sm4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            consumers_sync();
             for (unsigned long long e = e0; e < e1; ++e) {
                 const unsigned gi = gcount + (unsigned)(e - e0);
                 const int b = (int)(gi % NB);
                 mbar_wait(full_of(b), (gi / NB) & 1u);
                 const int nseg = *meta_of(b);
-                if (NS > 64)
-                    mir_deposits<2>(sm4, segs_of(b), nseg, NS, lane, tH_of(b), tX_of(b), CS / 2 + 1);
-                else
-                    mir_deposits<1>(sm4, segs_of(b), nseg, NS, lane, tH_of(b), tX_of(b), CS / 2 + 1);
+                if (NC > 1) {
+                    if (CSC ? CSC > 64 : NS > 64)
+                        mir_deposits_nc<2>(sm4, segs_of(b), nseg, NS, lane, tH_of(b), tX_of(b), CS / 2 + 1, cw, NC);
+                    else
+                        mir_deposits_nc<1>(sm4, segs_of(b), nseg, NS, lane, tH_of(b), tX_of(b), CS / 2 + 1, cw, NC);
+                } else {
+                    if (CSC ? CSC > 64 : NS > 64)
+                        mir_deposits<2>(sm4, segs_of(b), nseg, NS, lane, tH_of(b), tX_of(b), CS / 2 + 1);
+                    else
+                        mir_deposits<1>(sm4, segs_of(b), nseg, NS, lane, tH_of(b), tX_of(b), CS / 2 + 1);
+                }
                 mbar_arrive(empty_of(b));
             }
+            consumers_sync();  // every consumer's deposits are in before the write-out
             float* const dst = grp == 0 ? out : out_part + (size_t)(grp - 1) * bc.gstride;
             const int acc_in = grp == 0 ? accumulate : 0;
             if (!bc.out_ref) {
-                for (int c = 0; c < B.bxn * B.byn; ++c) {
+                for (int c = cw; c < B.bxn * B.byn; c += NC) {
                     const int ci = c % B.bxn, cj = c / B.bxn;
                     float* o = dst + ((size_t)(B.I0 + ci) + (size_t)g.nx * (B.J0 + cj)) * nz;
                     const float2* ac = acc + (ci + BX * cj) * CS;
@@ -1603,7 +1698,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 30 / (NP + 1)) adj_mirror_ws_ke
                 }
             } else {
                 const int ncol = BX * BY;
-                for (int t = lane; t < ncol * NS; t += 32) {
+                for (int t = lane + 32 * cw; t < ncol * NS; t += 32 * NC) {
                     const int c = t % ncol, kk = t / ncol;
                     const int ci = c % BX, cj = c / BX;
                     if (ci < B.bxn && cj < B.byn) {
@@ -1618,8 +1713,8 @@ __global__ void __launch_bounds__(32 * (NP + 1), 30 / (NP + 1)) adj_mirror_ws_ke
                 }
                 if (bc.level_done) {
                     __threadfence();
-                    __syncwarp();
-                    if (lane == 0) atomicAdd(bc.level_done + progress_slot(brick, bc), 1u);
+                    consumers_sync();
+                    if (cw == 0 && lane == 0) atomicAdd(bc.level_done + progress_slot(brick, bc), 1u);
                 }
             }
             __syncwarp();
@@ -2236,8 +2331,8 @@ void Projector::build_tables(const kct_geometry& geom) {
     for (auto fn : {adj_mirror_kernel<0>, adj_mirror_kernel<32>, adj_mirror_kernel<64>})
         KCT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(adj_mir_floats(kMirMaxBz) * sizeof(float))));
-    for (auto fn : {adj_mirror_ws_kernel<0, KCT_MIR_NP>, adj_mirror_ws_kernel<32, KCT_MIR_NP>,
-                    adj_mirror_ws_kernel<64, KCT_MIR_NP>})
+    for (auto fn : {adj_mirror_ws_kernel<0, KCT_MIR_NP, KCT_MIR_NC>, adj_mirror_ws_kernel<32, KCT_MIR_NP, KCT_MIR_NC>,
+                    adj_mirror_ws_kernel<64, KCT_MIR_NP, KCT_MIR_NC>})
         KCT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(adj_mir_ws_floats(kMirMaxBz, KCT_MIR_NP) * sizeof(float))));
 
@@ -2335,7 +2430,7 @@ void Projector::build_tables(const kct_geometry& geom) {
         int per_sm = 0, sms = 0;
         if (adj_ws_)
             KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &per_sm, adj_mirror_ws_kernel<0, KCT_MIR_NP>, 32 * (KCT_MIR_NP + 1), adj_smem_bytes()));
+                &per_sm, adj_mirror_ws_kernel<0, KCT_MIR_NP, KCT_MIR_NC>, 32 * (KCT_MIR_NP + KCT_MIR_NC), adj_smem_bytes()));
         else if (adj_mir_)
             KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_mirror_kernel<0>, 32,
                                                                    adj_smem_bytes()));
@@ -2791,9 +2886,9 @@ void Projector::adjoint_impl(const float* proj, float* vol, int a_begin, int a_e
             if (d_queue_) KCT_CUDA(cudaMemsetAsync(d_queue_, 0, sizeof(int), s));
             const unsigned grid = d_queue_ ? std::min(nctas, adj_ctas_) : nctas;
             if (adj_ws_)
-                (bc.bz == 64 ? adj_mirror_ws_kernel<64, KCT_MIR_NP>
-                 : bc.bz == 32 ? adj_mirror_ws_kernel<32, KCT_MIR_NP> : adj_mirror_ws_kernel<0, KCT_MIR_NP>)
-                    <<<grid, 32 * (KCT_MIR_NP + 1), smem, s>>>(
+                (bc.bz == 64 ? adj_mirror_ws_kernel<64, KCT_MIR_NP, KCT_MIR_NC>
+                 : bc.bz == 32 ? adj_mirror_ws_kernel<32, KCT_MIR_NP, KCT_MIR_NC> : adj_mirror_ws_kernel<0, KCT_MIR_NP, KCT_MIR_NC>)
+                    <<<grid, 32 * (KCT_MIR_NP + KCT_MIR_NC), smem, s>>>(
                     yrec, ymw, vol, dg_, bc, a0, nab, accum, border,
                     d_queue_, d_part_, static_cast<const WalkEntry*>(d_tab_), d_off_);
             else if (adj_mir_)
