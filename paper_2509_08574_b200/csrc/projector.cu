@@ -2965,8 +2965,10 @@ bool Projector::adjoint_host_ref(const float* host_proj, float* host, cudaStream
 // 1/2 .. 1/30: 1/8 best, host adjoint 5.02 -> 4.81 ms)
 #define KCT_ADJ_FIRST_PART 8
 #endif
+    int first_part = KCT_ADJ_FIRST_PART;
+    if (const char* fp = std::getenv("KCT_ADJ_FIRST_PART")) first_part = std::max(1, std::atoi(fp));
     const int H = (dg_.na >= 4 * kPipeMinAngles && !(sp && sp[0] == '0'))
-                      ? std::max(1, dg_.na / KCT_ADJ_FIRST_PART)
+                      ? std::max(1, dg_.na / first_part)
                       : dg_.na;
     KCT_CUDA(cudaMemcpyAsync(tmp, host_proj, H * per * sizeof(float), cudaMemcpyHostToDevice, s));
     KCT_CUDA(cudaMemsetAsync(d_level_, 0, (size_t)nslots * sizeof(unsigned), s));
