@@ -2961,9 +2961,10 @@ bool Projector::adjoint_host_ref(const float* host_proj, float* host, cudaStream
     const char* sp = std::getenv("KCT_ADJ_SPLIT");
 #ifndef KCT_ADJ_FIRST_PART
 // the first launch takes 1 / KCT_ADJ_FIRST_PART of the angles, so that it
-// lasts about as long as the rest's upload (c3: 0.52 ms vs 0.56 ms; measured
-// 1/2 .. 1/30: 1/8 best, host adjoint 5.02 -> 4.81 ms)
-#define KCT_ADJ_FIRST_PART 8
+// lasts about as long as the rest's upload (round 1, 4 ms kernel: 1/8 best;
+// round 2, 2 ms kernel, c3 host adjoint over 1/2 .. 1/12: 3.12 / 2.91 / 2.82 /
+// 2.86 / 2.97 / 3.03 ms -> 1/4)
+#define KCT_ADJ_FIRST_PART 4
 #endif
     int first_part = KCT_ADJ_FIRST_PART;
     if (const char* fp = std::getenv("KCT_ADJ_FIRST_PART")) first_part = std::max(1, std::atoi(fp));
