@@ -112,6 +112,12 @@ int kct_abi_version(void);
 /* Number of CUDA kernels the library has launched in this process (all
  * handles, all devices) — lets a caller verify which work ran on the GPU. */
 unsigned long long kct_launch_count(void);
+/* Page-locked host staging memory (cudaMallocHost): host buffers passed with
+ * KCT_MEM_HOST that live here are copied asynchronously at full PCIe rate
+ * and overlap the kernels.  No reference counterpart: the C++ shim
+ * (kryct_b200.hpp) converts the reference's double spans into such buffers. */
+int kct_host_alloc(size_t bytes, void** out);
+int kct_host_free(void* ptr);
 
 /* ---- operator: ConeBeamProjector (projector.hpp:264-291) --------------- */
 /* ctor: validate grid + geometry, reject a source inside the volume

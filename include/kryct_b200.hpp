@@ -29,8 +29,10 @@
 #include <kryct/recon.hpp>
 #include <kryct/types.hpp>
 
+#include <cmath>
 #include <cstdlib>
 #include <exception>
+#include <future>
 #include <list>
 #include <memory>
 #include <mutex>
@@ -66,6 +68,45 @@ inline kct_geometry to_geom(const kryct::ConeBeamGeometry& g) {
 
 inline std::vector<float> to_f32(std::span<const double> v) {
     return std::vector<float>(v.begin(), v.end());
+}
+
+// Page-locked float staging buffers (kct_host_alloc) per slot, grown on
+// demand and kept for the process: the solver's host copies then run
+// asynchronously at full PCIe rate.  Conversions double <-> float run on all
+// OpenMP threads when the caller compiles with OpenMP (as the reference does).
+struct Pinned {
+    std::mutex mu;
+    float* ptr[4] = {nullptr, nullptr, nullptr, nullptr};
+    std::size_t cap[4] = {0, 0, 0, 0};
+    float* get(int slot, std::size_t n) {
+        if (cap[slot] < n) {
+            if (ptr[slot]) kct_host_free(ptr[slot]);
+            ptr[slot] = nullptr;
+            cap[slot] = 0;
+            void* p = nullptr;
+            if (kct_host_alloc(n * sizeof(float), &p) != KCT_OK) return nullptr;
+            ptr[slot] = static_cast<float*>(p);
+            cap[slot] = n;
+        }
+        return ptr[slot];
+    }
+};
+inline Pinned& pinned() {
+    static Pinned p;
+    return p;
+}
+
+// double -> float; returns false if any value is not finite (the caller
+// throws the reference's ConfigError: types.hpp Volume/ProjectionSet::validate)
+inline bool to_f32(std::span<const double> v, float* out) {
+    const std::ptrdiff_t n = static_cast<std::ptrdiff_t>(v.size());
+    int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+    for (std::ptrdiff_t i = 0; i < n; ++i) {
+        bad |= std::isfinite(v[i]) ? 0 : 1;
+        out[i] = static_cast<float>(v[i]);
+    }
+    return bad == 0;
 }
 
 struct Handle {
@@ -206,19 +247,37 @@ inline kryct::ReconReport run(int kind, const kryct::ProjectionSet& proj,
                               const kryct::GridSpec& grid, const kryct::Volume* prior,
                               const kryct::RegularizationParams* params, std::size_t iters,
                               double tol, const kryct::ReconOptions& opts) {
-    proj.validate();
+    // ProjectionSet::validate (types.hpp:180-186) with the finiteness scan
+    // fused into the conversion below
+    proj.geometry.validate();
+    if (proj.data.size() != proj.geometry.ray_count())
+        throw kryct::ConfigError("projection data length does not match geometry");
     grid.validate();
     CheckedOut co(grid, proj.geometry);
     const GpuConeBeamProjector& A = *co.h;
     HookCtx hc{&opts.hook, nullptr, {}};
     if (opts.hook) check(kct_set_iterate_hook(A.handle(), hook_trampoline, &hc));
     const std::size_t m = grid.dims.count();
-    auto b = to_f32(proj.data);
-    std::vector<float> pr, x0, gt, x(m);
+    // the large buffers go through the page-locked staging slots (one caller
+    // at a time holds them; a concurrent call falls back to plain vectors)
+    std::unique_lock<std::mutex> plk(pinned().mu, std::try_to_lock);
+    std::vector<float> b_v, pr_v, x_v;
+    float* b = plk.owns_lock() ? pinned().get(0, proj.data.size()) : nullptr;
+    float* pr_p = nullptr;
+    float* x = plk.owns_lock() ? pinned().get(2, m) : nullptr;
+    if (!b) b = (b_v.resize(proj.data.size()), b_v.data());
+    if (!x) x = (x_v.resize(m), x_v.data());
+    if (!to_f32(proj.data, b)) throw kryct::ConfigError("projections contain non-finite values");
+    // the result's double vector is allocated (and its pages touched) by a
+    // helper thread while the device solves
+    auto result = std::async(std::launch::async, [m] { return std::vector<double>(m); });
+    std::vector<float> x0, gt;
     if (prior) {
         if (!(prior->dims == grid.dims))
             throw kryct::ConfigError("prior volume does not match the reconstruction grid");
-        pr = to_f32(prior->data);
+        pr_p = plk.owns_lock() ? pinned().get(1, m) : nullptr;
+        if (!pr_p) pr_p = (pr_v.resize(m), pr_v.data());
+        if (!to_f32(prior->data, pr_p)) throw kryct::ConfigError("volume contains non-finite values");
     }
     if (opts.initial) {
         if (!(opts.initial->dims == grid.dims))
@@ -247,15 +306,23 @@ inline kryct::ReconReport run(int kind, const kryct::ProjectionSet& proj,
         const kct_reg_params p{params->alpha,       params->lambda,          params->tau,
                                params->outer_iters, params->inner_iters,    params->inner_tolerance,
                                params->warm_start ? 1 : 0};
-        check(kct_irn(A.handle(), kind, b.data(), pr.empty() ? nullptr : pr.data(), px0, pgt, &p,
-                      x.data(), &rep, KCT_MEM_HOST, KCT_LAYOUT_REFERENCE, nullptr));
+        check(kct_irn(A.handle(), kind, b, pr_p, px0, pgt, &p, x, &rep, KCT_MEM_HOST,
+                      KCT_LAYOUT_REFERENCE, nullptr));
     } else {
-        check(kct_cgls_recon(A.handle(), b.data(), iters, px0, pgt, tol, x.data(), &rep,
-                             KCT_MEM_HOST, KCT_LAYOUT_REFERENCE, nullptr));
+        check(kct_cgls_recon(A.handle(), b, iters, px0, pgt, tol, x, &rep, KCT_MEM_HOST,
+                             KCT_LAYOUT_REFERENCE, nullptr));
     }
     kryct::ReconReport r;
-    r.volume = kryct::Volume(grid);
-    r.volume.data.assign(x.begin(), x.end());
+    r.volume.dims = grid.dims;
+    r.volume.spacing = grid.spacing;
+    r.volume.origin = grid.origin;
+    r.volume.data = result.get();
+    {
+        double* dst = r.volume.data.data();
+        const std::ptrdiff_t mm = static_cast<std::ptrdiff_t>(m);
+#pragma omp parallel for schedule(static)
+        for (std::ptrdiff_t i = 0; i < mm; ++i) dst[i] = x[i];
+    }
     r.objective_history.assign(obj.begin(), obj.begin() + rep.objective_count);
     r.residual_history.assign(res.begin(), res.begin() + rep.residual_count);
     r.error_history.assign(err.begin(), err.begin() + rep.error_count);

@@ -102,6 +102,8 @@ _SIGS = {
     "kct_last_error": ([], C.c_char_p),
     "kct_abi_version": ([], C.c_int),
     "kct_launch_count": ([], C.c_ulonglong),
+    "kct_host_alloc": ([C.c_size_t, C.POINTER(_P)], C.c_int),
+    "kct_host_free": ([_P], C.c_int),
     "kct_set_slab": ([_P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P], C.c_int),  # typed by distributed.install_slab
     "kct_projector_create": ([C.POINTER(_Grid), C.POINTER(_Geom), C.c_int, C.POINTER(_P)], C.c_int),
     "kct_projector_destroy": ([_P], C.c_int),

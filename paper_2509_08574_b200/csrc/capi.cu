@@ -126,6 +126,20 @@ int kct_abi_version(void) { return KCT_ABI_VERSION; }
 
 unsigned long long kct_launch_count(void) { return kct::g_launches.load(std::memory_order_relaxed); }
 
+int kct_host_alloc(size_t bytes, void** out) {
+    return guarded([&] {
+        if (!out) throw kct::ConfigError("null argument");
+        *out = nullptr;
+        KCT_CUDA(cudaMallocHost(out, bytes ? bytes : 1));
+    });
+}
+
+int kct_host_free(void* ptr) {
+    return guarded([&] {
+        if (ptr) KCT_CUDA(cudaFreeHost(ptr));
+    });
+}
+
 int kct_projector_create(const kct_grid* grid, const kct_geometry* geom, int device,
                          kct_projector** out) {
     return guarded([&] {
