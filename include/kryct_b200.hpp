@@ -140,15 +140,34 @@ class GpuConeBeamProjector final : public kryct::LinearMap {
     void apply(std::span<const double> x, std::span<double> out) const override {
         check_domain(x.size());
         check_range(out.size());
-        detail::check(kct_forward_f64(h_->h, x.data(), out.data()));
+        if (!staged(x, out, true)) detail::check(kct_forward_f64(h_->h, x.data(), out.data()));
     }
     void apply_adjoint(std::span<const double> y, std::span<double> out) const override {
         check_range(y.size());
         check_domain(out.size());
-        detail::check(kct_adjoint_f64(h_->h, y.data(), out.data()));
+        if (!staged(y, out, false)) detail::check(kct_adjoint_f64(h_->h, y.data(), out.data()));
     }
 
   private:
+    // through the page-locked float staging slots (the host pipelines of
+    // kct_forward / kct_adjoint then overlap their copies with the kernels);
+    // false when another call holds the slots
+    bool staged(std::span<const double> in, std::span<double> out, bool fwd) const {
+        std::unique_lock<std::mutex> lk(detail::pinned().mu, std::try_to_lock);
+        if (!lk.owns_lock()) return false;
+        float* fi = detail::pinned().get(1, in.size());
+        float* fo = detail::pinned().get(0, out.size());
+        if (!fi || !fo) return false;
+        detail::to_f32(in, fi);
+        detail::check(fwd ? kct_forward(h_->h, fi, fo, KCT_MEM_HOST, KCT_LAYOUT_REFERENCE, nullptr)
+                          : kct_adjoint(h_->h, fi, fo, KCT_MEM_HOST, KCT_LAYOUT_REFERENCE, nullptr));
+        const std::ptrdiff_t n = static_cast<std::ptrdiff_t>(out.size());
+        double* o = out.data();
+#pragma omp parallel for schedule(static)
+        for (std::ptrdiff_t i = 0; i < n; ++i) o[i] = fo[i];
+        return true;
+    }
+
     kryct::GridSpec grid_;
     kryct::ConeBeamGeometry geom_;
     std::shared_ptr<detail::Handle> h_;
