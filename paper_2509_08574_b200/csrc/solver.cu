@@ -27,6 +27,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+
 #include "solver.cuh"
 
 namespace kct {
@@ -386,6 +388,192 @@ __global__ void __launch_bounds__(kBlock, KCT_STENCIL_MINB) k_reggrad4(const flo
     write_partials(part, 0, ts, sm);
     write_partials(part, 1, t1, sm);
     write_partials(part, 2, t2, sm);
+}
+
+// a thread's 4-slab quad of a field with its k-1 / k+4 neighbours
+struct Q4 {
+    float4 c;      // slabs k .. k+3
+    float km, kp;  // slab k-1, slab k+4
+};
+__device__ __forceinline__ float4 sub4(float4 a, float4 b) {
+    return make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
+}
+// D^T W^2 D of the quad F (neighbours fip, fim, fjp, fjm) with weights W
+// (centre, i-1, j-1, k-1): dtwd's arithmetic
+__device__ __forceinline__ void dtwd_m(const Q4& F, float4 fip, float4 fim, float4 fjp, float4 fjm,
+                                       const Q4& W, float4 wim, float4 wjm, int k, bool hasip,
+                                       bool hasim, bool hasjp, bool hasjm, int nz, float g[4],
+                                       float g2[4]) {
+    const float f[6] = {F.km, F.c.x, F.c.y, F.c.z, F.c.w, F.kp};
+    const float w[5] = {W.km, W.c.x, W.c.y, W.c.z, W.c.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const float fv = f[q + 1];
+        const float gx = hasip ? q4(fip, q) - fv : 0.f;
+        const float gy = hasjp ? q4(fjp, q) - fv : 0.f;
+        const float gz = k + q + 1 < nz ? f[q + 2] - fv : 0.f;
+        const float wv = w[q + 1], wv2 = wv * wv;
+        float t = -wv2 * (gx + gy + gz);
+        if (hasim) { const float ww = q4(wim, q); t += ww * ww * (fv - q4(fim, q)); }
+        if (hasjm) { const float ww = q4(wjm, q); t += ww * ww * (fv - q4(fjm, q)); }
+        if (k + q > 0) { const float ww = w[q]; t += ww * ww * (fv - f[q]); }
+        g[q] = t;
+        g2[q] = wv2 * (gx * gx + gy * gy + gz * gz);
+    }
+}
+
+// ---- k_reggrad4 on TMA tiles (PICCS / TV, x != nullptr) ------------------
+// A CTA takes tiles of 64 slabs x 8 x-columns x 4 y-rows; the halo'd tiles of
+// x, x_p, W1, W2 (72 x 10 x 6 floats each: slabs k0-4 .. k0+67, columns
+// i0-1 .. i0+8, rows j0-1 .. j0+4) arrive in shared memory by four TMA
+// tensor loads (cp.async.bulk.tensor.3d, zero fill outside the volume /
+// slab, completion on an mbarrier), so every voxel value is read from DRAM
+// about once and all the stencil's neighbour reads are shared-memory loads.
+// Per voxel the arithmetic of k_reggrad4 (dtwd); the CTA's partial sums add
+// in (tile, thread, quad) order: deterministic.
+#ifndef KCT_TMA_TY
+#define KCT_TMA_TY 2
+#endif
+constexpr int kTZ = 64, kTX = 8, kTY = KCT_TMA_TY;          // voxels per tile
+constexpr int kBZ = kTZ + 8, kBX = kTX + 2, kBY = kTY + 2;  // TMA box (z padded to 16 B)
+constexpr int kTile = kBZ * kBX * kBY;                      // floats per tensor tile
+constexpr int kStages = 2;  // tile buffers: the next tile's loads overlap this tile's math
+
+__device__ __forceinline__ void tma_load3(float* dst, const CUtensorMap* tm, int z, int x, int y,
+                                          unsigned mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"((unsigned)__cvta_generic_to_shared(dst)), "l"(reinterpret_cast<unsigned long long>(tm)),
+        "r"(z), "r"(x), "r"(y), "r"(mbar)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(kBlock, 2) k_reggrad4t(
+    const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_xp,
+    const __grid_constant__ CUtensorMap tm_w1, const __grid_constant__ CUtensorMap tm_w2,
+    const float* __restrict__ sA, float* __restrict__ s, RegCfg c, int yoff, double* part) {
+    extern __shared__ __align__(1024) float tsm[];  // [kStages][4][kTile]
+    __shared__ __align__(8) unsigned long long mbar_s[kStages];
+    __shared__ double red[32];
+    const bool w1on = c.use_w1, m2 = c.mode2 == 1, m3 = c.mode2 == 2;
+    const int ntz = (c.nz + kTZ - 1) / kTZ, ntx = (c.nx + kTX - 1) / kTX, nty = (c.ny + kTY - 1) / kTY;
+    const int ntiles = ntz * ntx * nty;
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < kStages; ++st)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                             (unsigned)__cvta_generic_to_shared(&mbar_s[st]))
+                         : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const unsigned bytes = (unsigned)(kTile * sizeof(float)) * ((w1on || m2 || m3 ? 1u : 0u) +
+                                                                 (m2 || m3 ? 1u : 0u) +
+                                                                 (w1on ? 1u : 0u) + (m2 ? 1u : 0u));
+    // thread 0: this CTA's n-th tile into stage n % kStages
+    auto issue = [&](int tile, int n) {
+        const int tz = tile % ntz, rest = tile / ntz, txi = rest % ntx, tyi = rest / ntx;
+        const int k0 = tz * kTZ, i0 = txi * kTX, j0 = tyi * kTY;
+        float* const T = tsm + (size_t)(n % kStages) * 4 * kTile;
+        const unsigned mbar = (unsigned)__cvta_generic_to_shared(&mbar_s[n % kStages]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes)
+                     : "memory");
+        // tensor coordinates (z, x, y); y shifted by the slab's halo plane
+        if (w1on || m2 || m3) tma_load3(T, &tm_x, k0 - 4, i0 - 1, j0 - 1 + yoff, mbar);
+        if (m2 || m3) tma_load3(T + kTile, &tm_xp, k0 - 4, i0 - 1, j0 - 1 + yoff, mbar);
+        if (w1on) tma_load3(T + 2 * kTile, &tm_w1, k0 - 4, i0 - 1, j0 - 1 + yoff, mbar);
+        if (m2) tma_load3(T + 3 * kTile, &tm_w2, k0 - 4, i0 - 1, j0 - 1 + yoff, mbar);
+    };
+    // thread -> z quad (16 per 64 slabs) x column (8) x rows (kTY / 2 each)
+    constexpr int RPT = kTY * kTX * (kTZ / 4) / kBlock;  // quads (rows) per thread
+    const int qz = threadIdx.x & 15, col = threadIdx.x >> 4;
+    const int tx = col & 7, ty0 = (col >> 3) * RPT;
+    const size_t si = c.nz;
+    double ts = 0.0, t1 = 0.0, t2 = 0.0;
+    if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    int n = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++n) {
+        if (threadIdx.x == 0 && tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, n + 1);
+        const int tz = tile % ntz, rest = tile / ntz, txi = rest % ntx, tyi = rest / ntx;
+        const int k0 = tz * kTZ, i0 = txi * kTX, j0 = tyi * kTY;
+        const float* const TX = tsm + (size_t)(n % kStages) * 4 * kTile;
+        const float* const TP = TX + kTile;
+        const float* const T1 = TX + 2 * kTile;
+        const float* const T2 = TX + 3 * kTile;
+        // wait for this tile (use n / kStages of its stage's mbarrier)
+        asm volatile(
+            "{\n\t.reg .pred done;\n"
+            "TMAWAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1;\n\t"
+            "@!done bra TMAWAIT_%=;\n\t}" ::"r"((unsigned)__cvta_generic_to_shared(&mbar_s[n % kStages])),
+            "r"((unsigned)((n / kStages) & 1))
+            : "memory");
+        const int k = k0 + 4 * qz, i = i0 + tx;
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            const int ty = ty0 + r, j = j0 + ty;
+            const bool ok = k < c.nz && i < c.nx && j < c.ny;
+            // tile offset of the quad: slab kk = 4 + 4 qz, column tx + 1, row ty + 1
+            const int o = ((ty + 1) * kBX + (tx + 1)) * kBZ + 4 + 4 * qz;
+            const size_t v = ok ? (size_t)k + si * ((size_t)i + (size_t)c.nx * j) : 0;
+            const float4 a = ok ? __ldg(reinterpret_cast<const float4*>(sA + v)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            float sv[4] = {a.x, a.y, a.z, a.w};
+            const int jg = j + c.j0;
+            const bool hasip = i + 1 < c.nx, hasim = i > 0, hasjp = jg + 1 < c.nyg, hasjm = jg > 0;
+            auto ld4s = [&](const float* T, int off) { return *reinterpret_cast<const float4*>(T + off); };
+            float g[4], gg[4];
+            if (w1on) {
+                Q4 X, W;
+                X.c = ld4s(TX, o);
+                X.km = TX[o - 1];
+                X.kp = TX[o + 4];
+                W.c = ld4s(T1, o);
+                W.km = T1[o - 1];
+                dtwd_m(X, ld4s(TX, o + kBZ), ld4s(TX, o - kBZ), ld4s(TX, o + kBZ * kBX),
+                       ld4s(TX, o - kBZ * kBX), W, ld4s(T1, o - kBZ), ld4s(T1, o - kBZ * kBX), k,
+                       hasip, hasim, hasjp, hasjm, c.nz, g, gg);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    sv[q] -= c.alpha2 * g[q];
+                    if (ok) t1 += (double)gg[q];
+                }
+            }
+            if (m2) {
+                auto d4 = [&](int off) { return sub4(ld4s(TX, off), ld4s(TP, off)); };
+                Q4 D, W;
+                D.c = d4(o);
+                D.km = TX[o - 1] - TP[o - 1];
+                D.kp = TX[o + 4] - TP[o + 4];
+                W.c = ld4s(T2, o);
+                W.km = T2[o - 1];
+                dtwd_m(D, d4(o + kBZ), d4(o - kBZ), d4(o + kBZ * kBX), d4(o - kBZ * kBX), W,
+                       ld4s(T2, o - kBZ), ld4s(T2, o - kBZ * kBX), k, hasip, hasim, hasjp, hasjm,
+                       c.nz, g, gg);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    sv[q] -= c.lambda2 * g[q];
+                    if (ok) t2 += (double)gg[q];
+                }
+            } else if (m3) {
+                const float4 xv = ld4s(TX, o), pv = ld4s(TP, o);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float dv = q4(xv, q) - q4(pv, q);
+                    sv[q] -= c.lambda2 * dv;
+                    if (ok) t2 += (double)dv * (double)dv;
+                }
+            }
+            if (ok) {
+                *reinterpret_cast<float4*>(s + v) = make_float4(sv[0], sv[1], sv[2], sv[3]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) ts += (double)sv[q] * (double)sv[q];
+            }
+        }
+        __syncthreads();  // this stage is free for the tile after next
+    }
+    write_partials(part, 0, ts, red);
+    write_partials(part, 1, t1, red);
+    write_partials(part, 2, t2, red);
 }
 
 __global__ void __launch_bounds__(kBlock) k_normq4(const float* __restrict__ q, size_t n,
@@ -824,6 +1012,40 @@ void CUDART_CB hook_trampoline(void* arg) {
     c->fn(c->ctx, ++*c->counter, c->x, c->m);
 }
 
+// cuTensorMapEncodeTiled (driver API), resolved at run time through the
+// runtime's entry-point query (no -lcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+    static const EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// 3D tensor map of a native-layout volume vector (z, x, y[+ halo planes]) with
+// the k_reggrad4t box
+bool volume_tmap(CUtensorMap& tm, const float* v, const RegCfg& rc, size_t halo) {
+    const EncodeTiledFn enc = encode_tiled();
+    if (!enc) return false;
+    const int hy = halo ? 1 : 0;
+    const cuuint64_t dims[3] = {(cuuint64_t)rc.nz, (cuuint64_t)rc.nx, (cuuint64_t)(rc.ny + 2 * hy)};
+    const cuuint64_t strides[2] = {(cuuint64_t)rc.nz * sizeof(float),
+                                   (cuuint64_t)rc.nz * rc.nx * sizeof(float)};
+    const cuuint32_t box[3] = {(cuuint32_t)kBZ, (cuuint32_t)kBX, (cuuint32_t)kBY};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(v - halo), dims, strides,
+               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 struct Engine {
     Projector& P;
     Workspace& w;
@@ -967,8 +1189,29 @@ struct Engine {
 
     // out <- in - regulariser gradient (in == out allowed), norms into slots 0..2
     // (with_err: slot 5 of the preceding k_update_xr joins the same all-reduce)
+    // k_reggrad4t: x present, nz a multiple of 4, the volume at least one
+    // tile deep (KCT_TMA_STENCIL=0: the grid-stride kernel)
+    bool reggrad_tma(const float* in, float* out, const float* xv) {
+        const char* e = std::getenv("KCT_TMA_STENCIL");
+        if ((e && e[0] == '0') || !use4() || !xv || rc.nz < kTZ || rc.nx < kTX || rc.ny < kTY)
+            return false;
+        CUtensorMap tx, tp, t1, t2;
+        const float* xp = w.prior ? w.prior : xv;
+        const float* w1 = w.w1 ? w.w1 : xv;
+        const float* w2 = w.w2 ? w.w2 : xv;
+        if (!volume_tmap(tx, xv, rc, w.halo) || !volume_tmap(tp, xp, rc, w.halo) ||
+            !volume_tmap(t1, w1, rc, w.halo) || !volume_tmap(t2, w2, rc, w.halo))
+            return false;
+        const int smem = kStages * 4 * kTile * (int)sizeof(float);
+        KCT_CUDA(cudaFuncSetAttribute(k_reggrad4t, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        k_reggrad4t<<<kGrid, kBlock, smem, stream>>>(tx, tp, t1, t2, in, out, rc, w.halo ? 1 : 0, w.part);
+        KCT_LAUNCHED();
+        return true;
+    }
+
     void reggrad(const float* in, float* out, const float* xv, bool with_err = false) {
-        if (use4()) KCT_LAUNCH(k_reggrad4, in, xv, w.prior, w.w1, w.w2, out, rc, w.part);
+        if (reggrad_tma(in, out, xv)) {
+        } else if (use4()) KCT_LAUNCH(k_reggrad4, in, xv, w.prior, w.w1, w.w2, out, rc, w.part);
         else KCT_LAUNCH(k_reggrad, in, xv, w.prior, w.w1, w.w2, out, rc, w.part);
         if (with_err) vol_slots({0, 1, 2, 5});
         else vol_slots({0, 1, 2});

@@ -218,12 +218,15 @@ def test_float4_and_scalar_stencils_agree(monkeypatch, fn):
             return k.irn_tv(proj, gs, params, projector=A)
         return getattr(k, fn)(proj, gs, prior, params, projector=A)
 
-    vec = run()
+    vec = run()  # TMA-tiled k_reggrad4t (c1: 64^3)
+    monkeypatch.setenv("KCT_TMA_STENCIL", "0")
+    grid4 = run()  # grid-stride float4 kernels
     monkeypatch.setenv("KCT_SCALAR_STENCILS", "1")
     sca = run()
-    assert rel_l2(vec.volume, sca.volume) < 1e-5
-    np.testing.assert_allclose(vec.objective_history, sca.objective_history, rtol=1e-6)
-    np.testing.assert_allclose(vec.residual_history, sca.residual_history, rtol=1e-6)
+    for other in (grid4, sca):
+        assert rel_l2(vec.volume, other.volume) < 1e-5
+        np.testing.assert_allclose(vec.objective_history, other.objective_history, rtol=1e-6)
+        np.testing.assert_allclose(vec.residual_history, other.residual_history, rtol=1e-6)
 
 
 # ---- ReconOptions.hook / wall_times / the reference's restart control flow ----
