@@ -576,6 +576,180 @@ __global__ void __launch_bounds__(kBlock, 2) k_reggrad4t(
     write_partials(part, 2, t2, red);
 }
 
+// ---- k_weights4 / k_normq4 on TMA tiles ---------------------------------
+// The same tiles and two-stage pipeline as k_reggrad4t for the forward-
+// difference stencils: k_weights4t reads tiles of x and x_p (TV weights,
+// smoothed-TV sums), k_normq4t tiles of p (||W1 D p||^2, ||W2 D p||^2) with
+// W1 / W2 read directly (each voxel once).  Per voxel the arithmetic of
+// k_weights4 / k_normq4.
+template <class Body>
+__device__ __forceinline__ void tma_tiles(const CUtensorMap* tmA, const CUtensorMap* tmB, int ntile_maps,
+                                          const RegCfg& c, int yoff, float* tsm,
+                                          unsigned long long* mbar_s, Body&& body) {
+    const int ntz = (c.nz + kTZ - 1) / kTZ, ntx = (c.nx + kTX - 1) / kTX, nty = (c.ny + kTY - 1) / kTY;
+    const int ntiles = ntz * ntx * nty;
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < kStages; ++st)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                             (unsigned)__cvta_generic_to_shared(&mbar_s[st]))
+                         : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const unsigned bytes = (unsigned)(kTile * sizeof(float)) * (unsigned)ntile_maps;
+    auto issue = [&](int tile, int n) {
+        const int tz = tile % ntz, rest = tile / ntz, txi = rest % ntx, tyi = rest / ntx;
+        float* const T = tsm + (size_t)(n % kStages) * 2 * kTile;
+        const unsigned mbar = (unsigned)__cvta_generic_to_shared(&mbar_s[n % kStages]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes)
+                     : "memory");
+        tma_load3(T, tmA, tz * kTZ - 4, txi * kTX - 1, tyi * kTY - 1 + yoff, mbar);
+        if (ntile_maps > 1) tma_load3(T + kTile, tmB, tz * kTZ - 4, txi * kTX - 1, tyi * kTY - 1 + yoff, mbar);
+    };
+    if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    int n = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++n) {
+        if (threadIdx.x == 0 && tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, n + 1);
+        asm volatile(
+            "{\n\t.reg .pred done;\n"
+            "TMAWAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1;\n\t"
+            "@!done bra TMAWAIT_%=;\n\t}" ::"r"((unsigned)__cvta_generic_to_shared(&mbar_s[n % kStages])),
+            "r"((unsigned)((n / kStages) & 1))
+            : "memory");
+        const int tz = tile % ntz, rest = tile / ntz, txi = rest % ntx, tyi = rest / ntx;
+        const float* const T = tsm + (size_t)(n % kStages) * 2 * kTile;
+        // thread -> z quad x column x row (one quad per thread and tile)
+        const int qz = threadIdx.x & 15, col = threadIdx.x >> 4;
+        const int tx = col & 7, ty = col >> 3;
+        const int k = tz * kTZ + 4 * qz, i = txi * kTX + tx, j = tyi * kTY + ty;
+        const int o = ((ty + 1) * kBX + (tx + 1)) * kBZ + 4 + 4 * qz;
+        body(T, T + kTile, o, k, i, j, k < c.nz && i < c.nx && j < c.ny);
+        __syncthreads();
+    }
+}
+static_assert(kTY * kTX * (kTZ / 4) == kBlock, "one quad per thread and tile");
+
+__global__ void __launch_bounds__(kBlock, 3) k_weights4t(const __grid_constant__ CUtensorMap tm_x,
+                                                         const __grid_constant__ CUtensorMap tm_xp,
+                                                         float* __restrict__ w1, float* __restrict__ w2,
+                                                         RegCfg c, int yoff, int write_w, double* part) {
+    extern __shared__ __align__(1024) float tsm[];  // [kStages][2][kTile]
+    __shared__ __align__(8) unsigned long long mbar_s[kStages];
+    __shared__ double red[32];
+    const size_t si = c.nz;
+    double t1 = 0.0, t2 = 0.0;
+    const bool m2 = c.mode2 == 1, m3 = c.mode2 == 2;
+    tma_tiles(&tm_x, &tm_xp, m2 || m3 ? 2 : 1, c, yoff, tsm, mbar_s,
+              [&](const float* TX, const float* TP, int o, int k, int i, int j, bool ok) {
+        const int jg = j + c.j0;
+        const bool hasip = i + 1 < c.nx, hasjp = jg + 1 < c.nyg;
+        const float4 xc = *reinterpret_cast<const float4*>(TX + o);
+        const float4 xip = *reinterpret_cast<const float4*>(TX + o + kBZ);
+        const float4 xjp = *reinterpret_cast<const float4*>(TX + o + kBZ * kBX);
+        const float xf[5] = {xc.x, xc.y, xc.z, xc.w, TX[o + 4]};
+        float o1[4], o2[4];
+        float4 pc = make_float4(0.f, 0.f, 0.f, 0.f), pip = pc, pjp = pc;
+        float pk4 = 0.f;
+        if (m2 || m3) {
+            pc = *reinterpret_cast<const float4*>(TP + o);
+            pip = *reinterpret_cast<const float4*>(TP + o + kBZ);
+            pjp = *reinterpret_cast<const float4*>(TP + o + kBZ * kBX);
+            pk4 = TP[o + 4];
+        }
+        const float pf[5] = {pc.x, pc.y, pc.z, pc.w, pk4};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float xv = xf[q];
+            if (c.use_w1) {
+                const float gx = hasip ? q4(xip, q) - xv : 0.f;
+                const float gy = hasjp ? q4(xjp, q) - xv : 0.f;
+                const float gz = k + q + 1 < c.nz ? xf[q + 1] - xv : 0.f;
+                const float r = sqrtf(gx * gx + gy * gy + gz * gz + c.tau2);
+                if (ok) t1 += (double)r;
+                o1[q] = 1.f / sqrtf(r);
+            }
+            if (m2) {
+                const float dv = xv - pf[q];
+                const float gx = hasip ? (q4(xip, q) - q4(pip, q)) - dv : 0.f;
+                const float gy = hasjp ? (q4(xjp, q) - q4(pjp, q)) - dv : 0.f;
+                const float gz = k + q + 1 < c.nz ? (xf[q + 1] - pf[q + 1]) - dv : 0.f;
+                const float r = sqrtf(gx * gx + gy * gy + gz * gz + c.tau2);
+                if (ok) t2 += (double)r;
+                o2[q] = 1.f / sqrtf(r);
+            } else if (m3) {
+                const double d = (double)xv - (double)pf[q];
+                if (ok) t2 += d * d;
+            }
+        }
+        if (ok && write_w) {
+            const size_t v = (size_t)k + si * ((size_t)i + (size_t)c.nx * j);
+            if (c.use_w1) *reinterpret_cast<float4*>(w1 + v) = make_float4(o1[0], o1[1], o1[2], o1[3]);
+            if (m2) *reinterpret_cast<float4*>(w2 + v) = make_float4(o2[0], o2[1], o2[2], o2[3]);
+        }
+    });
+    write_partials(part, 1, t1, red);
+    write_partials(part, 2, t2, red);
+}
+
+__global__ void __launch_bounds__(kBlock, 3) k_normq4t(const float* __restrict__ q, size_t n,
+                                                       const __grid_constant__ CUtensorMap tm_p,
+                                                       const float* __restrict__ pv0,
+                                                       const float* __restrict__ w1,
+                                                       const float* __restrict__ w2, RegCfg c,
+                                                       int yoff, const Ctl* ctl, double* part) {
+    if (ctl->stop) return;
+    extern __shared__ __align__(1024) float tsm[];
+    __shared__ __align__(8) unsigned long long mbar_s[kStages];
+    __shared__ double red[32];
+    double tq = 0.0, t1 = 0.0, t2 = 0.0;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    // ||q||^2 with float4 loads (four values per thread and step, k order)
+    {
+        const size_t n4 = n / 4;
+        const float4* q4p = reinterpret_cast<const float4*>(q);
+        for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n4; v += stride) {
+            const float4 a = __ldg(q4p + v);
+            tq += (double)a.x * a.x + (double)a.y * a.y + (double)a.z * a.z + (double)a.w * a.w;
+        }
+        for (size_t v = 4 * n4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n; v += stride) {
+            const double qv = q[v];
+            tq += qv * qv;
+        }
+    }
+    const size_t si = c.nz;
+    tma_tiles(&tm_p, &tm_p, 1, c, yoff, tsm, mbar_s,
+              [&](const float* TPn, const float*, int o, int k, int i, int j, bool ok) {
+        const int jg = j + c.j0;
+        const bool hasip = i + 1 < c.nx, hasjp = jg + 1 < c.nyg;
+        const float4 pc = *reinterpret_cast<const float4*>(TPn + o);
+        const float4 pip = *reinterpret_cast<const float4*>(TPn + o + kBZ);
+        const float4 pjp = *reinterpret_cast<const float4*>(TPn + o + kBZ * kBX);
+        const float pf[5] = {pc.x, pc.y, pc.z, pc.w, TPn[o + 4]};
+        const size_t v = ok ? (size_t)k + si * ((size_t)i + (size_t)c.nx * j) : 0;
+        const float4 a1 = (ok && c.use_w1) ? __ldg(reinterpret_cast<const float4*>(w1 + v)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 a2 = (ok && c.mode2 == 1) ? __ldg(reinterpret_cast<const float4*>(w2 + v)) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+            const float pvv = pf[qq];
+            if (c.mode2 == 2 && ok) t2 += (double)pvv * (double)pvv;
+            if (c.use_w1 || c.mode2 == 1) {
+                const float gx = hasip ? q4(pip, qq) - pvv : 0.f;
+                const float gy = hasjp ? q4(pjp, qq) - pvv : 0.f;
+                const float gz = k + qq + 1 < c.nz ? pf[qq + 1] - pvv : 0.f;
+                const float g2 = gx * gx + gy * gy + gz * gz;
+                if (c.use_w1 && ok) { const float w = q4(a1, qq); t1 += (double)(w * w * g2); }
+                if (c.mode2 == 1 && ok) { const float w = q4(a2, qq); t2 += (double)(w * w * g2); }
+            }
+        }
+    });
+    (void)pv0;
+    write_partials(part, 0, tq, red);
+    write_partials(part, 1, t1, red);
+    write_partials(part, 2, t2, red);
+}
+
 __global__ void __launch_bounds__(kBlock) k_normq4(const float* __restrict__ q, size_t n,
                                                    const float* __restrict__ p,
                                                    const float* __restrict__ w1,
@@ -1112,7 +1286,8 @@ struct Engine {
         if (!rc.use_w1 && !rc.mode2) {
             KCT_CUDA(cudaMemsetAsync(w.part + 1 * kGrid, 0, 2 * kGrid * sizeof(double), stream));
         } else {
-            if (use4()) KCT_LAUNCH(k_weights4, w.x, w.prior, w.w1, w.w2, rc, write ? 1 : 0, w.part);
+            if (weights_tma(write)) {
+            } else if (use4()) KCT_LAUNCH(k_weights4, w.x, w.prior, w.w1, w.w2, rc, write ? 1 : 0, w.part);
             else KCT_LAUNCH(k_weights, w.x, w.prior, w.w1, w.w2, rc, write ? 1 : 0, w.part);
             vol_slots({1, 2});
             if (write) {
@@ -1209,6 +1384,36 @@ struct Engine {
         return true;
     }
 
+    bool tma_ok() const {
+        const char* e = std::getenv("KCT_TMA_STENCIL");
+        return !(e && e[0] == '0') && use4() && rc.nz >= kTZ && rc.nx >= kTX && rc.ny >= kTY &&
+               encode_tiled();
+    }
+    bool weights_tma(bool write) {
+        if (!tma_ok() || !w.x) return false;
+        CUtensorMap tx, tp;
+        if (!volume_tmap(tx, w.x, rc, w.halo) ||
+            !volume_tmap(tp, w.prior ? w.prior : w.x, rc, w.halo))
+            return false;
+        const int smem = kStages * 2 * kTile * (int)sizeof(float);
+        KCT_CUDA(cudaFuncSetAttribute(k_weights4t, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        k_weights4t<<<kGrid, kBlock, smem, stream>>>(tx, tp, w.w1, w.w2, rc, w.halo ? 1 : 0,
+                                                    write ? 1 : 0, w.part);
+        KCT_LAUNCHED();
+        return true;
+    }
+    bool normq_tma() {
+        if (!tma_ok() || !(rc.use_w1 || rc.mode2)) return false;
+        CUtensorMap tp;
+        if (!volume_tmap(tp, w.p, rc, w.halo)) return false;
+        const int smem = kStages * 2 * kTile * (int)sizeof(float);
+        KCT_CUDA(cudaFuncSetAttribute(k_normq4t, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        k_normq4t<<<kGrid, kBlock, smem, stream>>>(w.q, w.n, tp, w.p, w.w1, w.w2, rc, w.halo ? 1 : 0,
+                                                  w.ctl, w.part);
+        KCT_LAUNCHED();
+        return true;
+    }
+
     void reggrad(const float* in, float* out, const float* xv, bool with_err = false) {
         if (reggrad_tma(in, out, xv)) {
         } else if (use4()) KCT_LAUNCH(k_reggrad4, in, xv, w.prior, w.w1, w.w2, out, rc, w.part);
@@ -1220,7 +1425,8 @@ struct Engine {
     // One CGLS iteration (krylov.hpp:98-125).
     void iterate(double* res, double* err, bool with_gt) {
         forward(w.p, w.q);
-        if (use4()) KCT_LAUNCH(k_normq4, w.q, w.n, w.p, w.w1, w.w2, rc, w.ctl, w.part);
+        if (normq_tma()) {
+        } else if (use4()) KCT_LAUNCH(k_normq4, w.q, w.n, w.p, w.w1, w.w2, rc, w.ctl, w.part);
         else KCT_LAUNCH(k_normq, w.q, w.n, w.p, w.w1, w.w2, rc, w.ctl, w.part);
         proj_slots({0});
         vol_slots({1, 2});
