@@ -143,6 +143,7 @@ int kct_host_free(void* ptr) {
 int kct_projector_create(const kct_grid* grid, const kct_geometry* geom, int device,
                          kct_projector** out) {
     return guarded([&] {
+        kct::NvtxRange nvtx("kct_projector_create");
         if (!grid || !geom || !out) throw kct::ConfigError("null argument");
         *out = nullptr;
         auto* h = new kct_projector{nullptr};
@@ -334,6 +335,7 @@ bool pipelined(const kct::Projector& P, int mem) {
 int kct_forward(kct_projector* h, const float* vol, float* proj, int mem, int layout,
                 void* stream) {
     return guarded([&] {
+        kct::NvtxRange nvtx("kct_forward");
         auto& P = get(h);
         check_mem_layout(mem, layout);
         if (!vol || !proj) throw kct::ConfigError("forward: null buffer");
@@ -352,6 +354,7 @@ int kct_forward(kct_projector* h, const float* vol, float* proj, int mem, int la
 int kct_adjoint(kct_projector* h, const float* proj, float* vol, int mem, int layout,
                 void* stream) {
     return guarded([&] {
+        kct::NvtxRange nvtx("kct_adjoint");
         auto& P = get(h);
         check_mem_layout(mem, layout);
         if (!vol || !proj) throw kct::ConfigError("adjoint: null buffer");
@@ -469,6 +472,7 @@ int kct_proj_from_native(const kct_projector* h, const float* native, float* ref
 
 int kct_fdk(kct_projector* h, const float* proj, float* vol, int mem, int layout, void* stream) {
     return guarded([&] {
+        kct::NvtxRange nvtx("kct_fdk");
         auto& P = get(h);
         check_mem_layout(mem, layout);
         if (!vol || !proj) throw kct::ConfigError("fdk: null buffer");
@@ -541,6 +545,7 @@ int kct_cgls_recon(kct_projector* h, const float* b, size_t iters, const float* 
                    const float* ground_truth, double tolerance, float* x_out,
                    kct_report* report, int mem, int layout, void* stream) {
     return guarded([&] {
+        kct::NvtxRange nvtx("kct_cgls_recon");
         auto& P = get(h);
         check_mem_layout(mem, layout);
         DeviceGuard dg(P.device());
@@ -553,6 +558,7 @@ int kct_irn(kct_projector* h, int kind, const float* b, const float* prior, cons
             const float* ground_truth, const kct_reg_params* params, float* x_out,
             kct_report* report, int mem, int layout, void* stream) {
     return guarded([&] {
+        kct::NvtxRange nvtx("kct_irn");
         auto& P = get(h);
         check_mem_layout(mem, layout);
         if (!params) throw kct::ConfigError("null params");

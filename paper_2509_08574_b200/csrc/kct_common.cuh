@@ -12,6 +12,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <stdexcept>
@@ -37,6 +38,15 @@ struct CudaError : std::runtime_error {
         if (e_ != cudaSuccess)                                                          \
             throw ::kct::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
+
+// NVTX range around a library phase (header-only NVTX v3: free unless a
+// profiler such as Nsight Systems injects its tool library).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Every kernel launch of the library is counted (kct_launch_count): evidence
 // of which work ran on the device, read by bench.py around its timed region.

@@ -1724,6 +1724,7 @@ void irn_solve(Projector& P, int kind, const float* b, const float* prior, const
     e.mark_start();
     std::vector<size_t> wall_keep;  // event indices of the iterations that ran
     for (size_t cycle = 0; cycle < outer; ++cycle) {
+        NvtxRange nvtx("irn outer cycle");  // (host enqueue; the device runs behind)
         const double t_cycle = now_s();
         e.weights(true);
         if (p.warm_start) {
