@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define KCT_ABI_VERSION 2
+#define KCT_ABI_VERSION 3
 
 enum kct_status {
     KCT_OK = 0,
@@ -49,6 +49,12 @@ enum kct_status {
 enum kct_mem { KCT_MEM_HOST = 0, KCT_MEM_DEVICE = 1 };
 enum kct_layout { KCT_LAYOUT_REFERENCE = 0, KCT_LAYOUT_NATIVE = 1 };
 enum kct_kind { KCT_KIND_TV = 0, KCT_KIND_PIPLE = 1, KCT_KIND_PICCS = 2 };
+/* Row-block maps of a caller-assembled stack (kct_cgls_stack). */
+enum kct_map {
+    KCT_MAP_PROJECTOR = 0, /* the handle's cone-beam projector, range N (projector.hpp:264-291) */
+    KCT_MAP_DIFF = 1,      /* DiffOperator, range 3M [dx; dy; dz] (diffreg.hpp:20-81) */
+    KCT_MAP_IDENTITY = 2   /* IdentityMap, range M (linear_map.hpp:59-80) */
+};
 
 /* GridSpec (types.hpp:56-80): dims, spacing [mm], origin = min corner of voxel (0,0,0). */
 typedef struct kct_grid {
@@ -230,6 +236,34 @@ int kct_irn(kct_projector* h, int kind, const float* b, const float* prior, cons
 int kct_irn_piccs(kct_projector* h, const float* b, const float* prior, const float* x0,
                   const float* ground_truth, const kct_reg_params* params, float* x_out,
                   kct_report* report, int mem, int layout, void* stream);
+
+/* One row block of a vertically stacked system (ScaledBlock, linear_map.hpp:152-157):
+ * scale * diag(weights) * map.  `weights` is the DiagonalMap a caller composes
+ * on the left of the map (compose(DiagonalMap(w), map), linear_map.hpp:82-150;
+ * recon.hpp:211-217 builds the reweighted TV blocks this way); range-sized,
+ * same mem / layout as the other arrays; NULL = no diagonal.  (ABI 3) */
+typedef struct kct_stack_block {
+    int map;      /* enum kct_map */
+    double scale;
+    const float* weights;
+} kct_stack_block;
+
+/* cgls(const LinearMap&, b, x0, KrylovConfig) (krylov.hpp:59-127) on a
+ * caller-assembled StackedMap (linear_map.hpp:159-216), device-resident: the
+ * iteration vectors never leave the GPU (the alternative, driving the
+ * reference's own cgls through kct_forward_f64 / kct_adjoint_f64, pays two
+ * PCIe copies and two float64 conversions per operator application).
+ * b: the concatenated right-hand side, block by block (N / 3M / M floats);
+ * x0: M floats or NULL (zeros); x_out: M floats.  Volume-shaped pieces (x0,
+ * x_out, each of a DIFF block's three components, IDENTITY blocks, and the
+ * weights of those blocks) use `layout`'s volume order, PROJECTOR blocks its
+ * projection order.  report: residual_history / wall_times (capacity
+ * max_iters), residual_count = SolveTrace::iterations, converged, breakdown.
+ * The per-iteration hook (kct_set_iterate_hook) is served as in the drivers.
+ * Single-process only (KCT_ERR_CONFIG in the sharded solver modes). */
+int kct_cgls_stack(kct_projector* h, const kct_stack_block* blocks, size_t n_blocks,
+                   const float* b, const float* x0, size_t max_iters, double tolerance,
+                   float* x_out, kct_report* report, int mem, int layout, void* stream);
 
 /* resolve_tau (recon.hpp:60-66) over a float32 host array (NULL/0 = empty). */
 double kct_resolve_tau(double tau, const float* reference, size_t n);

@@ -6,6 +6,11 @@
 //   kryct_b200::GpuConeBeamProjector : kryct::LinearMap   (projector.hpp:264-291)
 //   kryct_b200::cgls_recon(proj, grid, iters, opts, tol)   (recon.hpp:312-315)
 //   kryct_b200::irn_tv / irn_piple / irn_piccs             (recon.hpp:252-270)
+//   kryct_b200::cgls(A, b, x0, cfg)                        (krylov.hpp:59-127)
+//     device-resident CGLS over a caller-assembled kryct::StackedMap whose
+//     blocks are a GpuConeBeamProjector, kryct::DiffOperator or
+//     kryct::IdentityMap, each optionally under compose(DiagonalMap, .) —
+//     the stacks recon.hpp:211-221 assembles (kct_cgls_stack)
 // so existing callers switch by namespace, and the reference's own generic
 // solvers (kryct::cgls, kryct::StackedMap, ...) can drive the GPU operator.
 // Values cross the boundary as float32 (the reference reads float32 files,
@@ -25,6 +30,8 @@
 // to a concurrent call (that call builds its own).
 #pragma once
 
+#include <kryct/diffreg.hpp>
+#include <kryct/krylov.hpp>
 #include <kryct/linear_map.hpp>
 #include <kryct/recon.hpp>
 #include <kryct/types.hpp>
@@ -118,6 +125,11 @@ struct Handle {
 
 }  // namespace detail
 
+// The operator lives in an inner namespace so that an unqualified
+// `cgls(gpu_projector, ...)` in caller code (argument-dependent lookup) keeps
+// resolving to kryct::cgls alone, not also to kryct_b200::cgls below.
+namespace ops {
+
 /// ConeBeamProjector on one CUDA device (projector.hpp:264-291).
 class GpuConeBeamProjector final : public kryct::LinearMap {
   public:
@@ -172,6 +184,9 @@ class GpuConeBeamProjector final : public kryct::LinearMap {
     kryct::ConeBeamGeometry geom_;
     std::shared_ptr<detail::Handle> h_;
 };
+
+}  // namespace ops
+using ops::GpuConeBeamProjector;
 
 namespace detail {
 
@@ -356,6 +371,140 @@ inline kryct::ReconReport run(int kind, const kryct::ProjectionSet& proj,
 }
 
 }  // namespace detail
+
+namespace detail {
+
+// kryct::ComposedMap keeps its operands private and has no accessors
+// (linear_map.hpp:146-149).  Reading them through an explicit template
+// instantiation (which may name private members) lets the drop-in take the
+// caller's unmodified compose(DiagonalMap, map) blocks; a maintainer adopting
+// the shim would add outer() / inner() accessors instead.
+template <class Tag, typename Tag::type Member>
+struct MemberOf {
+    friend typename Tag::type member_ptr(Tag) { return Member; }
+};
+struct ComposedOuter {
+    using type = std::shared_ptr<const kryct::LinearMap> kryct::ComposedMap::*;
+    friend type member_ptr(ComposedOuter);
+};
+struct ComposedInner {
+    using type = std::shared_ptr<const kryct::LinearMap> kryct::ComposedMap::*;
+    friend type member_ptr(ComposedInner);
+};
+template struct MemberOf<ComposedOuter, &kryct::ComposedMap::outer_>;
+template struct MemberOf<ComposedInner, &kryct::ComposedMap::inner_>;
+
+struct FlatBlock {
+    int map;
+    double scale;
+    const std::vector<double>* weights;  // nullptr = no diagonal
+    std::size_t len;
+};
+
+// One block: [DiagonalMap o] {GpuConeBeamProjector | DiffOperator | IdentityMap}
+inline FlatBlock flatten_block(const kryct::LinearMap& m, double scale,
+                               const GpuConeBeamProjector*& projector) {
+    const kryct::LinearMap* map = &m;
+    const std::vector<double>* w = nullptr;
+    if (const auto* cm = dynamic_cast<const kryct::ComposedMap*>(map)) {
+        const auto& outer = cm->*member_ptr(ComposedOuter{});
+        const auto& inner = cm->*member_ptr(ComposedInner{});
+        const auto* dm = dynamic_cast<const kryct::DiagonalMap*>(outer.get());
+        if (!dm) throw kryct::ConfigError("kryct_b200::cgls: a composed block must be DiagonalMap o map");
+        w = &dm->weights();
+        map = inner.get();
+    }
+    int code;
+    if (const auto* gp = dynamic_cast<const GpuConeBeamProjector*>(map)) {
+        if (projector && projector->handle() != gp->handle())
+            throw kryct::ConfigError("kryct_b200::cgls: blocks must share one projector");
+        projector = gp;
+        code = KCT_MAP_PROJECTOR;
+    } else if (dynamic_cast<const kryct::DiffOperator*>(map)) {
+        code = KCT_MAP_DIFF;
+    } else if (dynamic_cast<const kryct::IdentityMap*>(map)) {
+        code = KCT_MAP_IDENTITY;
+    } else {
+        throw kryct::ConfigError(
+            "kryct_b200::cgls: unsupported block (GpuConeBeamProjector, DiffOperator or IdentityMap, "
+            "optionally under a DiagonalMap; other maps: kryct::cgls drives the GPU operator)");
+    }
+    return FlatBlock{code, scale, w, map->range_size()};
+}
+
+}  // namespace detail
+
+/// krylov.hpp:59-127 — cgls on a caller-assembled stack with every iteration
+/// vector resident on the device.  Same signature, error behaviour and trace
+/// as kryct::cgls; values cross the boundary as float32.
+inline kryct::SolveResult cgls(const kryct::LinearMap& A, std::span<const double> b,
+                               std::span<const double> x0, const kryct::KrylovConfig& cfg = {}) {
+    if (b.size() != A.range_size()) throw kryct::ConfigError("cgls: rhs size mismatch");
+    if (x0.size() != A.domain_size()) throw kryct::ConfigError("cgls: x0 size mismatch");
+    const GpuConeBeamProjector* P = nullptr;
+    std::vector<detail::FlatBlock> flat;
+    if (const auto* st = dynamic_cast<const kryct::StackedMap*>(&A)) {
+        for (std::size_t i = 0; i < st->block_count(); ++i)
+            flat.push_back(detail::flatten_block(*st->block(i).map, st->block(i).scale, P));
+    } else {
+        flat.push_back(detail::flatten_block(A, 1.0, P));
+    }
+    if (!P) throw kryct::ConfigError("kryct_b200::cgls: the stack needs a GpuConeBeamProjector block");
+    const std::size_t m = P->domain_size();
+    for (const auto& f : flat) {
+        const std::size_t want =
+            f.map == KCT_MAP_PROJECTOR ? P->range_size() : (f.map == KCT_MAP_DIFF ? 3 * m : m);
+        if (f.len != want) throw kryct::ConfigError("kryct_b200::cgls: block size does not match the grid");
+    }
+    // DiffOperator dims must be the projector grid's (its range alone does not say so)
+    if (const auto* st = dynamic_cast<const kryct::StackedMap*>(&A))
+        for (std::size_t i = 0; i < st->block_count(); ++i) {
+            const kryct::LinearMap* mp = st->block(i).map.get();
+            if (const auto* cm = dynamic_cast<const kryct::ComposedMap*>(mp))
+                mp = (cm->*member_ptr(detail::ComposedInner{})).get();
+            if (const auto* d = dynamic_cast<const kryct::DiffOperator*>(mp))
+                if (!(d->dims() == P->grid().dims))
+                    throw kryct::ConfigError("kryct_b200::cgls: DiffOperator dims do not match the grid");
+        }
+
+    std::vector<float> bf(b.size()), xf(m), out(m);
+    detail::to_f32(b, bf.data());  // non-finite data surfaces as SolverError from the device (krylov.hpp:75)
+    detail::to_f32(x0, xf.data());
+    std::vector<std::vector<float>> wf(flat.size());
+    std::vector<kct_stack_block> blocks(flat.size());
+    for (std::size_t i = 0; i < flat.size(); ++i) {
+        if (flat[i].weights) {
+            wf[i].resize(flat[i].weights->size());
+            detail::to_f32(*flat[i].weights, wf[i].data());
+        }
+        blocks[i] = kct_stack_block{flat[i].map, flat[i].scale, flat[i].weights ? wf[i].data() : nullptr};
+    }
+    bool x_zero = true;
+    for (double v : x0) x_zero = x_zero && v == 0.0;
+    detail::HookCtx hc{&cfg.hook, nullptr, {}};
+    struct HookGuard {
+        kct_projector* h;
+        ~HookGuard() { kct_set_iterate_hook(h, nullptr, nullptr); }
+    } guard{P->handle()};
+    if (cfg.hook) detail::check(kct_set_iterate_hook(P->handle(), detail::hook_trampoline, &hc));
+    const std::size_t cap = cfg.max_iters > 0 ? cfg.max_iters : 1;
+    std::vector<double> res(cap), wall(cap);
+    kct_report rep{};
+    rep.residual_history = res.data();
+    rep.wall_times = wall.data();
+    detail::check(kct_cgls_stack(P->handle(), blocks.data(), blocks.size(), bf.data(),
+                                 x_zero ? nullptr : xf.data(), cfg.max_iters, cfg.tolerance, out.data(),
+                                 &rep, KCT_MEM_HOST, KCT_LAYOUT_REFERENCE, nullptr));
+    if (hc.err) std::rethrow_exception(hc.err);
+    kryct::SolveResult r;
+    r.x.assign(out.begin(), out.end());
+    r.trace.iterations = rep.residual_count;
+    r.trace.converged = rep.converged != 0;
+    r.trace.breakdown = rep.breakdown != 0;
+    r.trace.residual_norms.assign(res.begin(), res.begin() + rep.residual_count);
+    r.trace.wall_times.assign(wall.begin(), wall.begin() + rep.wall_count);
+    return r;
+}
 
 /// Drop the cached projector handles (frees their device memory).
 inline void clear_handle_cache() { detail::handle_cache().clear(); }

@@ -175,6 +175,10 @@ class Oracle:
         self._cgls = g("cgls_recon")
         self._cgls.argtypes = [gp, gg, P(C.c_double), C.c_size_t, P(C.c_double), P(C.c_double),
                                C.c_double, P(C.c_double), P(KctReport)]
+        self._cgls_stack = g("cgls_stack")
+        self._cgls_stack.argtypes = [gp, gg, C.c_size_t, P(C.c_int), P(C.c_double),
+                                     P(P(C.c_double)), P(C.c_double), P(C.c_double), C.c_size_t,
+                                     C.c_double, P(C.c_double), P(C.c_size_t), P(C.c_int), P(C.c_int)]
         self._irn = g("irn")
         self._irn.argtypes = [gp, gg, C.c_int, P(C.c_double), P(C.c_double), P(C.c_double),
                               P(C.c_double), P(KctRegParams), P(C.c_double), P(KctReport)]
@@ -296,6 +300,29 @@ class Oracle:
         self._check(self._cgls(C.byref(gc), C.byref(ge), _dp(bb), iters, _dp(x0a), _dp(gta),
                                tol, _dp(out), C.byref(rep)))
         return out, self._unpack(rep, bufs)
+
+    def cgls_stack(self, grid, geom, blocks, b, iters, x0=None, tol=0.0):
+        """cgls (krylov.hpp:59-127) on a caller-assembled StackedMap
+        (linear_map.hpp:159-216).  blocks: [(map, scale, weights | None), ...] with map
+        0 projector / 1 DiffOperator / 2 IdentityMap.  Returns (x, info dict)."""
+        m, n = grid.count, geom.ray_count
+        lens = [n if mp == 0 else (3 * m if mp == 1 else m) for mp, _, _ in blocks]
+        bb = self._f64(b, sum(lens))
+        nb = len(blocks)
+        maps = (C.c_int * nb)(*[int(mp) for mp, _, _ in blocks])
+        scales = (C.c_double * nb)(*[float(sc) for _, sc, _ in blocks])
+        keep = [None if w is None else self._f64(w, ln) for (_, _, w), ln in zip(blocks, lens)]
+        wts = (C.POINTER(C.c_double) * nb)(*[
+            C.cast(None, C.POINTER(C.c_double)) if w is None else _dp(w) for w in keep])
+        x = np.zeros(m) if x0 is None else self._f64(x0, m).copy()
+        res = np.zeros(max(int(iters), 1))
+        its, conv, brk = C.c_size_t(0), C.c_int(0), C.c_int(0)
+        gc, ge = grid.c(), geom.c()
+        self._check(self._cgls_stack(C.byref(gc), C.byref(ge), nb, maps, scales, wts, _dp(bb), _dp(x),
+                                     int(iters), float(tol), _dp(res), C.byref(its), C.byref(conv),
+                                     C.byref(brk)))
+        return x, dict(iterations=its.value, converged=bool(conv.value), breakdown=bool(brk.value),
+                       residual_history=res[:its.value].copy())
 
     def irn(self, grid, geom, kind, b, prior, params: dict, x0=None, ground_truth=None):
         bb = self._f64(b, geom.ray_count)

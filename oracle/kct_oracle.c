@@ -369,9 +369,24 @@ typedef struct {
     int identity;     /* piple: lambda*I block */
     double* tmp3;     /* 3M scratch */
     double* tmpm;     /* M scratch */
+    /* caller-assembled stack (ora_cgls_stack): nblk > 0 replaces the fixed layout above */
+    size_t nblk;
+    const int* maps;            /* enum kct_map */
+    const double* scales;       /* ScaledBlock::scale */
+    const double* const* wts;   /* DiagonalMap composed on the left, NULL = none */
+    double* tmpn;               /* N scratch */
 } stack_op;
 
+static size_t block_len(const stack_op* s, size_t i) {
+    return s->maps[i] == KCT_MAP_PROJECTOR ? s->n : (s->maps[i] == KCT_MAP_DIFF ? 3 * s->m : s->m);
+}
+
 static size_t stack_range(const stack_op* s) {
+    if (s->nblk) {
+        size_t t = 0;
+        for (size_t i = 0; i < s->nblk; ++i) t += block_len(s, i);
+        return t;
+    }
     size_t r = s->n;
     if (s->w1) r += 3 * s->m;
     if (s->identity) r += s->m;
@@ -383,8 +398,47 @@ static void scale(double c, double* x, size_t n) {
     for (size_t i = 0; i < n; ++i) x[i] *= c;
 }
 
+/* StackedMap::apply :185-193 over caller blocks; a weighted block is
+ * ComposedMap(DiagonalMap(w), map) (:82-150): map first, then diag(w) */
+static void gstack_apply(const stack_op* s, const double* x, double* out) {
+    const kct_grid* gr = s->grid;
+    size_t off = 0;
+    for (size_t b = 0; b < s->nblk; ++b) {
+        const size_t len = block_len(s, b);
+        double* o = out + off;
+        if (s->maps[b] == KCT_MAP_PROJECTOR) ora_forward(gr, s->g, x, o);
+        else if (s->maps[b] == KCT_MAP_DIFF) ora_diff(gr->nx, gr->ny, gr->nz, x, o);
+        else for (size_t i = 0; i < len; ++i) o[i] = x[i];
+        if (s->wts[b]) for (size_t i = 0; i < len; ++i) o[i] = s->wts[b][i] * o[i];
+        if (s->scales[b] != 1.0) scale(s->scales[b], o, len);
+        off += len;
+    }
+}
+
+/* StackedMap::apply_adjoint :195-205 */
+static void gstack_adjoint(const stack_op* s, const double* y, double* out) {
+    const kct_grid* gr = s->grid;
+    memset(out, 0, s->m * sizeof(double));
+    size_t off = 0;
+    for (size_t b = 0; b < s->nblk; ++b) {
+        const size_t len = block_len(s, b);
+        const double* in = y + off;
+        if (s->wts[b]) {
+            double* t = s->maps[b] == KCT_MAP_PROJECTOR ? s->tmpn : s->tmp3;
+            for (size_t i = 0; i < len; ++i) t[i] = s->wts[b][i] * in[i];
+            in = t;
+        }
+        if (s->maps[b] == KCT_MAP_PROJECTOR) ora_adjoint(gr, s->g, in, s->tmpm);
+        else if (s->maps[b] == KCT_MAP_DIFF) ora_diff_adjoint(gr->nx, gr->ny, gr->nz, in, s->tmpm);
+        else memcpy(s->tmpm, in, len * sizeof(double));
+        axpy(s->scales[b], s->tmpm, out, s->m);
+        off += len;
+    }
+}
+
 /* StackedMap::apply :185-193 with ComposedMap(DiagonalMap, D) blocks */
 static void stack_apply(const stack_op* s, const double* x, double* out) {
+    if (s->nblk) { gstack_apply(s, x, out); return; }
     const kct_grid* gr = s->grid;
     ora_forward(gr, s->g, x, out);
     size_t off = s->n;
@@ -406,6 +460,7 @@ static void stack_apply(const stack_op* s, const double* x, double* out) {
 
 /* StackedMap::apply_adjoint :195-205 */
 static void stack_adjoint(const stack_op* s, const double* y, double* out) {
+    if (s->nblk) { gstack_adjoint(s, y, out); return; }
     const kct_grid* gr = s->grid;
     memset(out, 0, s->m * sizeof(double));
     ora_adjoint(gr, s->g, y, s->tmpm);
@@ -502,6 +557,40 @@ static int cgls(const stack_op* A, const double* b, double* x, size_t max_iters,
     }
 out:
     free(r); free(q); free(s); free(p);
+    return rc;
+}
+
+/* cgls (krylov.hpp:59-127) on a caller-assembled StackedMap (linear_map.hpp:159-216).
+ * x: in = x0, out = the solution; res_hist: capacity max_iters. */
+int ora_cgls_stack(const kct_grid* grid, const kct_geometry* g, size_t n_blocks, const int* maps,
+                   const double* scales, const double* const* weights, const double* b, double* x,
+                   size_t max_iters, double tol, double* res_hist, size_t* iterations,
+                   int* converged, int* breakdown) {
+    int rc = validate(grid, g);
+    if (rc) return rc;
+    if (n_blocks == 0) return fail(2, "stack: needs at least one block");
+    for (size_t i = 0; i < n_blocks; ++i)
+        if (maps[i] != KCT_MAP_PROJECTOR && maps[i] != KCT_MAP_DIFF && maps[i] != KCT_MAP_IDENTITY)
+            return fail(2, "stack: unknown block map");
+    stack_op A = {0};
+    A.grid = grid;
+    A.g = g;
+    A.m = (size_t)grid->nx * grid->ny * grid->nz;
+    A.n = (size_t)g->n_angles * g->nu * g->nv;
+    A.nblk = n_blocks;
+    A.maps = maps;
+    A.scales = scales;
+    A.wts = weights;
+    A.tmp3 = (double*)malloc(3 * A.m * sizeof(double));
+    A.tmpm = (double*)malloc(A.m * sizeof(double));
+    A.tmpn = (double*)malloc(A.n * sizeof(double));
+    cgls_trace tr = {0};
+    tr.res_hist = res_hist;
+    rc = cgls(&A, b, x, max_iters, tol, &tr);
+    if (iterations) *iterations = tr.iterations;
+    if (converged) *converged = tr.converged;
+    if (breakdown) *breakdown = tr.breakdown;
+    free(A.tmp3); free(A.tmpm); free(A.tmpn);
     return rc;
 }
 

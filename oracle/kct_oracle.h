@@ -54,6 +54,14 @@ double ora_resolve_tau(double tau, const double* ref, size_t n);
 int ora_cgls_recon(const kct_grid* grid, const kct_geometry* g, const double* b, size_t iters,
                    const double* x0, const double* ground_truth, double tol, double* x_out,
                    kct_report* rep);
+/* cgls (krylov.hpp:59-127) on a caller-assembled StackedMap (linear_map.hpp:159-216):
+ * block i = scales[i] * diag(weights[i]) * map(maps[i]) (enum kct_map; weights[i] NULL = none).
+ * x: in x0, out solution (M); b: concatenated rhs; res_hist capacity max_iters. */
+int ora_cgls_stack(const kct_grid* grid, const kct_geometry* g, size_t n_blocks, const int* maps,
+                   const double* scales, const double* const* weights, const double* b, double* x,
+                   size_t max_iters, double tol, double* res_hist, size_t* iterations,
+                   int* converged, int* breakdown);
+
 int ora_irn(const kct_grid* grid, const kct_geometry* g, int kind, const double* b,
             const double* prior, const double* x0, const double* ground_truth,
             const kct_reg_params* p, double* x_out, kct_report* rep);

@@ -292,4 +292,43 @@ int ref_irn(const kct_grid* grid, const kct_geometry* g, int kind, const double*
     });
 }
 
+// cgls (krylov.hpp:59-127) on a StackedMap the caller assembles (linear_map.hpp:159-216):
+// block i = ScaledBlock{scales[i], compose(DiagonalMap(weights[i]), map_i)} (plain map_i
+// without weights), map_i the reference's ConeBeamProjector / DiffOperator / IdentityMap.
+int ref_cgls_stack(const kct_grid* grid, const kct_geometry* g, size_t n_blocks, const int* maps,
+                   const double* scales, const double* const* weights, const double* b, double* x,
+                   size_t max_iters, double tol, double* res_hist, size_t* iterations,
+                   int* converged, int* breakdown) {
+    return guarded([&] {
+        const auto gs = to_grid(grid);
+        const auto ge = to_geom(g);
+        const std::size_t m = gs.dims.count();
+        std::vector<kryct::ScaledBlock> blocks;
+        for (size_t i = 0; i < n_blocks; ++i) {
+            std::shared_ptr<const kryct::LinearMap> map;
+            if (maps[i] == KCT_MAP_PROJECTOR) map = std::make_shared<kryct::ConeBeamProjector>(gs, ge);
+            else if (maps[i] == KCT_MAP_DIFF) map = kryct::make_diff(gs.dims);
+            else if (maps[i] == KCT_MAP_IDENTITY) map = std::make_shared<kryct::IdentityMap>(m);
+            else throw kryct::ConfigError("stack: unknown block map");
+            if (weights[i]) {
+                std::vector<double> w(weights[i], weights[i] + map->range_size());
+                map = kryct::compose(std::make_shared<kryct::DiagonalMap>(std::move(w)), map);
+            }
+            blocks.push_back({scales[i], map});
+        }
+        const auto A = kryct::stack_maps(std::move(blocks));
+        kryct::KrylovConfig cfg;
+        cfg.max_iters = max_iters;
+        cfg.tolerance = tol;
+        const auto r = kryct::cgls(*A, std::span<const double>(b, A->range_size()),
+                                   std::span<const double>(x, m), cfg);
+        std::memcpy(x, r.x.data(), m * sizeof(double));
+        if (res_hist)
+            for (size_t i = 0; i < r.trace.residual_norms.size(); ++i) res_hist[i] = r.trace.residual_norms[i];
+        if (iterations) *iterations = r.trace.iterations;
+        if (converged) *converged = r.trace.converged ? 1 : 0;
+        if (breakdown) *breakdown = r.trace.breakdown ? 1 : 0;
+    });
+}
+
 }  // extern "C"

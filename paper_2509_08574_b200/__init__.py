@@ -34,6 +34,8 @@ __all__ = [
     "ConeBeamProjector", "RegularizationParams", "ReconOptions", "ReconReport", "cgls_recon",
     "irn_tv", "irn_piple", "irn_piccs", "fdk", "resolve_tau", "uniform_angles", "load_library",
     "subsample_indices", "subsample_angles", "LIB_PATH", "shard",
+    "DiffOperator", "IdentityMap", "DiagonalMap", "ComposedMap", "compose", "ScaledBlock",
+    "StackedMap", "stack_maps", "KrylovConfig", "SolveTrace", "SolveResult", "cgls",
 ]
 
 LIB_PATH = os.environ.get("KCT_LIB_PATH", _build.LIB)
@@ -82,6 +84,10 @@ class _Reg(C.Structure):
                 ("inner_tolerance", C.c_double), ("warm_start", C.c_int)]
 
 
+class _StackBlock(C.Structure):
+    _fields_ = [("map", C.c_int), ("scale", C.c_double), ("weights", C.c_void_p)]
+
+
 class _Report(C.Structure):
     _fields_ = [("objective_history", C.POINTER(C.c_double)), ("objective_count", C.c_size_t),
                 ("residual_history", C.POINTER(C.c_double)), ("residual_count", C.c_size_t),
@@ -120,6 +126,8 @@ _SIGS = {
     "kct_proj_from_native": ([_P, _P, _P, _P], C.c_int),
     "kct_cgls_recon": ([_P, _P, C.c_size_t, _P, _P, C.c_double, _P, C.POINTER(_Report), C.c_int,
                         C.c_int, _P], C.c_int),
+    "kct_cgls_stack": ([_P, C.POINTER(_StackBlock), C.c_size_t, _P, _P, C.c_size_t, C.c_double, _P,
+                        C.POINTER(_Report), C.c_int, C.c_int, _P], C.c_int),
     "kct_irn": ([_P, C.c_int, _P, _P, _P, _P, C.POINTER(_Reg), _P, C.POINTER(_Report), C.c_int,
                  C.c_int, _P], C.c_int),
     "kct_irn_piccs": ([_P, _P, _P, _P, _P, C.POINTER(_Reg), _P, C.POINTER(_Report), C.c_int,
@@ -610,6 +618,200 @@ def cgls_recon(proj: ProjectionSet, grid: GridSpec, iters: int, opts: ReconOptio
                                    C.byref(rep), mem, _layout_code(layout, mem),
                                    _stream_of(mem, b.keep.device.index if mem == MEM_DEVICE else None)))
     return _unpack(rep, bufs, out)
+
+
+# ---------------------------------------------------------------------------
+# caller-assembled stacks: the LinearMap algebra (linear_map.hpp) as block
+# descriptors, solved on the device by kct_cgls_stack
+# ---------------------------------------------------------------------------
+MAP_PROJECTOR, MAP_DIFF, MAP_IDENTITY = 0, 1, 2
+
+
+class DiffOperator:
+    """DiffOperator (diffreg.hpp:20-81): forward differences [dx; dy; dz], 3M values."""
+
+    def __init__(self, dims):
+        self.dims = tuple(int(d) for d in dims)
+        if min(self.dims) < 1:
+            raise ConfigError("diff operator: dims must be positive")
+
+    def domain_size(self) -> int:
+        return self.dims[0] * self.dims[1] * self.dims[2]
+
+    def range_size(self) -> int:
+        return 3 * self.domain_size()
+
+
+class IdentityMap:
+    """IdentityMap (linear_map.hpp:59-80)."""
+
+    def __init__(self, n: int):
+        self.n = int(n)
+
+    def domain_size(self) -> int:
+        return self.n
+
+    def range_size(self) -> int:
+        return self.n
+
+
+class DiagonalMap:
+    """DiagonalMap (linear_map.hpp:82-106): multiplication by diag(weights)."""
+
+    def __init__(self, weights):
+        self.weights = weights
+
+    def domain_size(self) -> int:
+        w = self.weights
+        return int(w.numel()) if _is_torch(w) else int(np.asarray(w).size)
+
+    range_size = domain_size
+
+
+class ComposedMap:
+    """ComposedMap (linear_map.hpp:108-150): outer after inner."""
+
+    def __init__(self, outer, inner):
+        if outer is None or inner is None:
+            raise ConfigError("compose: null operand")
+        if outer.domain_size() != inner.range_size():
+            raise ConfigError("compose: inner range must match outer domain")
+        self.outer, self.inner = outer, inner
+
+    def domain_size(self) -> int:
+        return self.inner.domain_size()
+
+    def range_size(self) -> int:
+        return self.outer.range_size()
+
+
+def compose(outer, inner) -> ComposedMap:
+    return ComposedMap(outer, inner)
+
+
+@dataclass
+class ScaledBlock:
+    """linear_map.hpp:152-157."""
+    scale: float = 1.0
+    map: object = None
+
+
+class StackedMap:
+    """StackedMap (linear_map.hpp:159-216): [c1 A1; c2 A2; ...] over one domain."""
+
+    def __init__(self, blocks):
+        self.blocks = [b if isinstance(b, ScaledBlock) else ScaledBlock(*b) for b in blocks]
+        if not self.blocks:
+            raise ConfigError("stack: needs at least one block")
+        if any(b.map is None for b in self.blocks):
+            raise ConfigError("stack: null block")
+        self._domain = self.blocks[0].map.domain_size()
+        if any(b.map.domain_size() != self._domain for b in self.blocks):
+            raise ConfigError("stack: all blocks must share the domain")
+
+    def domain_size(self) -> int:
+        return self._domain
+
+    def range_size(self) -> int:
+        return sum(b.map.range_size() for b in self.blocks)
+
+    def block_count(self) -> int:
+        return len(self.blocks)
+
+
+def stack_maps(blocks) -> StackedMap:
+    return StackedMap(blocks)
+
+
+@dataclass
+class KrylovConfig:
+    """krylov.hpp:25-33."""
+    max_iters: int = 100
+    tolerance: float = 0.0
+    hook: object = None
+
+
+@dataclass
+class SolveTrace:
+    """krylov.hpp:35-41."""
+    iterations: int = 0
+    converged: bool = False
+    breakdown: bool = False
+    residual_norms: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    wall_times: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+
+@dataclass
+class SolveResult:
+    """krylov.hpp:43-46."""
+    x: object = None
+    trace: SolveTrace = field(default_factory=SolveTrace)
+
+
+def _flatten_stack(A):
+    """A LinearMap expression -> (projector, [(map code, scale, weights | None)]).
+    Accepted shapes (what recon.hpp:211-221 assembles, and plain maps): a
+    ConeBeamProjector / DiffOperator / IdentityMap, compose(DiagonalMap, one
+    of those), or a StackedMap of such blocks with exactly one projector
+    handle among them.  Anything else is a ConfigError: there is no CPU path."""
+    blocks = A.blocks if isinstance(A, StackedMap) else [ScaledBlock(1.0, A)]
+    projector, out = None, []
+    for blk in blocks:
+        mp, w = blk.map, None
+        if isinstance(mp, ComposedMap) and isinstance(mp.outer, DiagonalMap):
+            w, mp = mp.outer.weights, mp.inner
+        if isinstance(mp, ConeBeamProjector):
+            if projector is not None and projector is not mp:
+                raise ConfigError("stack: blocks must share one projector handle")
+            projector, code = mp, MAP_PROJECTOR
+        elif isinstance(mp, DiffOperator):
+            code = MAP_DIFF
+        elif isinstance(mp, IdentityMap):
+            code = MAP_IDENTITY
+        else:
+            raise ConfigError(f"stack: unsupported block {type(mp).__name__} "
+                              "(projector, DiffOperator, IdentityMap, optionally under a DiagonalMap)")
+        out.append((code, float(blk.scale), w, mp))
+    if projector is None:
+        raise ConfigError("stack: needs a ConeBeamProjector block (it owns the device)")
+    m = projector.domain_size()
+    for code, _, _, mp in out:
+        if code == MAP_DIFF and (mp.domain_size() != m or tuple(mp.dims) != tuple(projector.grid.dims)):
+            raise ConfigError("stack: DiffOperator dims must match the projector grid")
+        if mp.domain_size() != m:
+            raise ConfigError("stack: all blocks must share the domain")
+    return projector, out
+
+
+def cgls(A, b, x0=None, cfg: KrylovConfig | None = None, layout=None, out=None) -> SolveResult:
+    """cgls (krylov.hpp:59-127) over a caller-assembled stack, device-resident
+    (kct_cgls_stack).  `b` is the concatenated right-hand side (block order),
+    `x0` the start (None = zeros); numpy arrays or CUDA tensors, all of one kind."""
+    cfg = cfg or KrylovConfig()
+    P, blocks = _flatten_stack(A)
+    m, n = P.domain_size(), P.range_size()
+    lens = [n if c == MAP_PROJECTOR else (3 * m if c == MAP_DIFF else m) for c, _, _, _ in blocks]
+    if (b.numel() if _is_torch(b) else np.asarray(b).size) != sum(lens):
+        raise ConfigError("cgls: rhs size mismatch")
+    bb = _Arg(b, sum(lens), "rhs")
+    xx = _Arg(x0, m, "x0") if x0 is not None else None
+    ws = [_Arg(w, ln, "weights") if w is not None else None for (_, _, w, _), ln in zip(blocks, lens)]
+    mem = _same_mem([bb, xx] + ws)
+    out = _out_for(bb, m, out)
+    arr = (_StackBlock * len(blocks))()
+    for i, ((code, scale, _, _), w) in enumerate(zip(blocks, ws)):
+        arr[i].map, arr[i].scale, arr[i].weights = code, scale, (w.ptr if w else None)
+    iters = int(cfg.max_iters)
+    rep, bufs = _report_buffers(1, iters, 1)
+    with _HookInstall(P, cfg.hook):
+        _check(_lib.kct_cgls_stack(P.handle, arr, len(blocks), bb.ptr, xx.ptr if xx else None, iters,
+                                   float(cfg.tolerance), _ptr(out), C.byref(rep), mem,
+                                   _layout_code(layout, mem),
+                                   _stream_of(mem, bb.keep.device.index if mem == MEM_DEVICE else None)))
+    return SolveResult(x=out, trace=SolveTrace(
+        iterations=int(rep.residual_count), converged=bool(rep.converged),
+        breakdown=bool(rep.breakdown), residual_norms=bufs["res"][:rep.residual_count].copy(),
+        wall_times=bufs["wall"][:rep.wall_count].copy()))
 
 
 def _irn(kind, proj, grid, prior, params, opts, projector, layout, out=None):

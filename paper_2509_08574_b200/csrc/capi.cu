@@ -554,6 +554,19 @@ int kct_cgls_recon(kct_projector* h, const float* b, size_t iters, const float* 
     });
 }
 
+int kct_cgls_stack(kct_projector* h, const kct_stack_block* blocks, size_t n_blocks,
+                   const float* b, const float* x0, size_t max_iters, double tolerance,
+                   float* x_out, kct_report* report, int mem, int layout, void* stream) {
+    return guarded([&] {
+        kct::NvtxRange nvtx("kct_cgls_stack");
+        auto& P = get(h);
+        check_mem_layout(mem, layout);
+        DeviceGuard dg(P.device());
+        kct::cgls_stack(P, blocks, n_blocks, b, x0, max_iters, tolerance, x_out, report, mem,
+                        layout, static_cast<cudaStream_t>(stream));
+    });
+}
+
 int kct_irn(kct_projector* h, int kind, const float* b, const float* prior, const float* x0,
             const float* ground_truth, const kct_reg_params* params, float* x_out,
             kct_report* report, int mem, int layout, void* stream) {

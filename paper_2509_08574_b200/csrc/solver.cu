@@ -1015,6 +1015,8 @@ struct Workspace {
     double* gath = nullptr;  // y-slab mode: [2 * world] gather-by-sum buffer
     double* red = nullptr;   // multi-process: packed fp64 slots of one all-reduce
     size_t cap = 0, cap_obj = 0;
+    float* stack = nullptr;  // kct_cgls_stack: r | q | weights of the caller's stack
+    size_t stack_cap = 0;
     std::vector<void*> allocs;
     // per-iteration hook: reference-layout device copy of x, pinned host copy,
     // side stream, events (x copied / host copy done)
@@ -1030,7 +1032,7 @@ struct Workspace {
     ~Workspace() {
         if (hook_stream) cudaStreamSynchronize(hook_stream);
         for (void* ptr : allocs) cudaFree(ptr);
-        for (void* ptr : {(void*)hist, (void*)obj}) cudaFree(ptr);
+        for (void* ptr : {(void*)hist, (void*)obj, (void*)stack}) cudaFree(ptr);
         if (hook_host) cudaFreeHost(hook_host);
         if (hook_stop) cudaFreeHost(hook_stop);
         if (hook_stream) cudaStreamDestroy(hook_stream);
@@ -1785,6 +1787,300 @@ void irn_solve(Projector& P, int kind, const float* b, const float* prior, const
                 if (rep->wall_times) rep->wall_times[rep->wall_count] = all[idx - 1];
                 ++rep->wall_count;
             }
+    }
+    KCT_CUDA(cudaStreamSynchronize(stream));
+}
+
+// ---- caller-assembled stacks -------------------------------------------------
+// cgls (krylov.hpp:59-127) over a StackedMap (linear_map.hpp:159-216) whose row
+// blocks are scale * diag(w) * {projector, DiffOperator, IdentityMap}, all
+// vectors resident on the device in the native layouts (a volume-shaped piece
+// is z-fastest, a DIFF block [dx; dy; dz] of three such pieces).  Unlike the
+// IRN drivers above, the regulariser residual blocks are materialised (the
+// caller's right-hand side is arbitrary), so this is the reference's algorithm
+// vector for vector: float32 storage, fp64 fixed-order reductions.
+namespace {
+
+// partial sums accumulate over the kernels of one phase (same block index,
+// stream order: deterministic)
+__device__ __forceinline__ void add_partials(double* part, int slot, double v, double* sm,
+                                             int acc) {
+    const double t = block_sum(v, sm);
+    if (threadIdx.x == 0) {
+        double* dst = part + slot * kGrid + blockIdx.x;
+        *dst = acc ? *dst + t : t;
+    }
+}
+
+// q = c * w .* (D p)  (diffreg.hpp:34-49); slot0 (+)= ||q||^2
+__global__ void __launch_bounds__(kBlock) k_stack_diff(const float* __restrict__ p,
+                                                       const float* __restrict__ w, float c,
+                                                       float* __restrict__ q, RegCfg g,
+                                                       double* part, int acc) {
+    __shared__ double sm[32];
+    const size_t m = (size_t)g.nx * g.ny * g.nz, si = g.nz, sj = (size_t)g.nz * g.nx;
+    double t = 0.0;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < m;
+         v += (size_t)gridDim.x * blockDim.x) {
+        int k, i, j;
+        decode(v, g, k, i, j);
+        float gx, gy, gz;
+        fdiff(p, v, k, i, j, g, si, sj, p[v], gx, gy, gz);
+        if (w) { gx *= w[v]; gy *= w[m + v]; gz *= w[2 * m + v]; }
+        gx *= c; gy *= c; gz *= c;
+        q[v] = gx; q[m + v] = gy; q[2 * m + v] = gz;
+        t += (double)gx * gx + (double)gy * gy + (double)gz * gz;
+    }
+    add_partials(part, 0, t, sm, acc);
+}
+
+// s (+)= c * D^T (w .* r)  (diffreg.hpp:51-76, as a gather: one owner per voxel)
+__global__ void __launch_bounds__(kBlock) k_stack_diff_adj(const float* __restrict__ r,
+                                                           const float* __restrict__ w, float c,
+                                                           float* __restrict__ s, RegCfg g,
+                                                           int acc) {
+    const size_t m = (size_t)g.nx * g.ny * g.nz, si = g.nz, sj = (size_t)g.nz * g.nx;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < m;
+         v += (size_t)gridDim.x * blockDim.x) {
+        int k, i, j;
+        decode(v, g, k, i, j);
+        auto y = [&](size_t u) { return w ? r[u] * w[u] : r[u]; };
+        float a = 0.f;
+        if (i + 1 < g.nx) a -= y(v);
+        if (i > 0) a += y(v - si);
+        if (j + 1 < g.ny) a -= y(m + v);
+        if (j > 0) a += y(m + v - sj);
+        if (k + 1 < g.nz) a -= y(2 * m + v);
+        if (k > 0) a += y(2 * m + v - 1);
+        s[v] = acc ? fmaf(c, a, s[v]) : c * a;
+    }
+}
+
+// q = c * w .* src (src == q allowed: the projector block after its forward;
+// src = p: an identity block); slot0 (+)= ||q||^2
+__global__ void __launch_bounds__(kBlock) k_stack_scale(const float* src, const float* __restrict__ w,
+                                                        float c, float* q, size_t n, double* part,
+                                                        int acc) {
+    __shared__ double sm[32];
+    double t = 0.0;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n;
+         v += (size_t)gridDim.x * blockDim.x) {
+        float a = src[v];
+        if (w) a *= w[v];
+        a *= c;
+        q[v] = a;
+        t += (double)a * a;
+    }
+    add_partials(part, 0, t, sm, acc);
+}
+
+// s (+)= c * w .* r
+__global__ void __launch_bounds__(kBlock) k_stack_axpy(const float* __restrict__ r,
+                                                       const float* __restrict__ w, float c,
+                                                       float* s, size_t n, int acc) {
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n;
+         v += (size_t)gridDim.x * blockDim.x) {
+        const float a = w ? r[v] * w[v] : r[v];
+        s[v] = acc ? fmaf(c, a, s[v]) : c * a;
+    }
+}
+
+// r -= q; slot0 = ||r||^2
+__global__ void __launch_bounds__(kBlock) k_stack_sub(float* __restrict__ r,
+                                                      const float* __restrict__ q, size_t n,
+                                                      double* part) {
+    __shared__ double sm[32];
+    double t = 0.0;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n;
+         v += (size_t)gridDim.x * blockDim.x) {
+        const float rv = r[v] - q[v];
+        r[v] = rv;
+        t += (double)rv * rv;
+    }
+    write_partials(part, 0, t, sm);
+}
+
+struct StackBlock {
+    int map;
+    float scale;
+    size_t off, len;          // position in the concatenated range
+    const float* w = nullptr;  // device, native layout (nullptr: no diagonal)
+};
+
+struct Stack {
+    Projector& P;
+    Workspace& w;
+    cudaStream_t stream;
+    RegCfg rc{};
+    std::vector<StackBlock> blocks;
+    size_t range = 0;
+
+    // q = A v  (StackedMap::apply, linear_map.hpp:185-193); slot0 = ||q||^2
+    void apply(const float* v, float* q) {
+        int acc = 0;
+        for (const StackBlock& b : blocks) {
+            float* qb = q + b.off;
+            switch (b.map) {
+            case KCT_MAP_PROJECTOR:
+                P.forward(v, qb, stream);
+                KCT_LAUNCH(k_stack_scale, qb, b.w, b.scale, qb, b.len, w.part, acc);
+                break;
+            case KCT_MAP_DIFF:
+                KCT_LAUNCH(k_stack_diff, v, b.w, b.scale, qb, rc, w.part, acc);
+                break;
+            default:
+                KCT_LAUNCH(k_stack_scale, v, b.w, b.scale, qb, b.len, w.part, acc);
+            }
+            acc = 1;
+        }
+    }
+
+    // s = A^T y  (StackedMap::apply_adjoint, linear_map.hpp:195-205); slot0 = ||s||^2
+    void adjoint(const float* y, float* s) {
+        int acc = 0;
+        for (const StackBlock& b : blocks) {
+            const float* yb = y + b.off;
+            switch (b.map) {
+            case KCT_MAP_PROJECTOR: {
+                const float* in = yb;
+                if (b.w) {  // diag(w) first (ComposedMap::apply_adjoint, linear_map.hpp:134-140)
+                    KCT_LAUNCH(k_stack_axpy, yb, b.w, 1.f, w.q, b.len, 0);
+                    in = w.q;
+                }
+                if (!acc && b.scale == 1.f) {
+                    P.adjoint(in, s, stream);
+                } else {
+                    P.adjoint(in, w.atr, stream);
+                    KCT_LAUNCH(k_stack_axpy, w.atr, nullptr, b.scale, s, w.m, acc);
+                }
+                break;
+            }
+            case KCT_MAP_DIFF:
+                KCT_LAUNCH(k_stack_diff_adj, yb, b.w, b.scale, s, rc, acc);
+                break;
+            default:
+                KCT_LAUNCH(k_stack_axpy, yb, b.w, b.scale, s, b.len, acc);
+            }
+            acc = 1;
+        }
+        KCT_LAUNCH(k_stats, s, w.m, w.part);
+    }
+};
+
+}  // namespace
+
+void cgls_stack(Projector& P, const kct_stack_block* blocks, size_t n_blocks, const float* b,
+                const float* x0, size_t iters, double tol, float* x_out, kct_report* rep, int mem,
+                int layout, cudaStream_t stream) {
+    if (!blocks || n_blocks == 0) throw ConfigError("stack: needs at least one block");
+    if (!b || !x_out) throw ConfigError("cgls: null buffer");
+    if (P.slab_mode() || P.comm_fn)
+        throw ConfigError("kct_cgls_stack runs in a single process (sharded modes are set)");
+    reset_report(rep);
+    Workspace& w = workspace(P, std::max<size_t>(iters, 1), 1);
+    Stack st{P, w, stream};
+    set_grid(st.rc, P);
+    size_t n_weights = 0;
+    for (size_t i = 0; i < n_blocks; ++i) {
+        StackBlock sb;
+        sb.map = blocks[i].map;
+        if (sb.map != KCT_MAP_PROJECTOR && sb.map != KCT_MAP_DIFF && sb.map != KCT_MAP_IDENTITY)
+            throw ConfigError("stack: unknown block map");
+        if (!std::isfinite(blocks[i].scale)) throw ConfigError("stack: block scale must be finite");
+        sb.scale = (float)blocks[i].scale;
+        sb.len = sb.map == KCT_MAP_PROJECTOR ? w.n : (sb.map == KCT_MAP_DIFF ? 3 * w.m : w.m);
+        sb.off = st.range;
+        st.range += sb.len;
+        if (blocks[i].weights) n_weights += sb.len;
+        st.blocks.push_back(sb);
+    }
+    const size_t R = st.range;
+    const size_t need = 2 * R + n_weights;
+    if (w.stack_cap < need) {
+        cudaFree(w.stack);
+        w.stack = nullptr;
+        w.stack_cap = 0;
+        KCT_CUDA(cudaMalloc(&w.stack, need * sizeof(float)));
+        w.stack_cap = need;
+    }
+    float* r = w.stack;
+    float* q = r + R;
+    float* wts = q + R;
+    // the right-hand side goes straight into r; volume-shaped pieces one by one
+    auto load_block = [&](float* dst, const float* src, const StackBlock& sb) {
+        if (sb.map == KCT_MAP_PROJECTOR) {
+            load(P, dst, src, sb.len, false, mem, layout, stream);
+        } else {
+            for (size_t c = 0; c < sb.len / w.m; ++c)
+                load(P, dst + c * w.m, src + c * w.m, w.m, true, mem, layout, stream);
+        }
+    };
+    for (size_t i = 0; i < n_blocks; ++i) {
+        StackBlock& sb = st.blocks[i];
+        load_block(r + sb.off, b + sb.off, sb);
+        if (blocks[i].weights) {
+            load_block(wts, blocks[i].weights, sb);
+            sb.w = wts;
+            wts += sb.len;
+        }
+    }
+    if (x0) load(P, w.x, x0, w.m, true, mem, layout, stream);
+    else KCT_CUDA(cudaMemsetAsync(w.x, 0, w.m * sizeof(float), stream));
+    KCT_CUDA(cudaMemsetAsync(w.part, 0, (size_t)kSlots * kGrid * sizeof(double), stream));
+    init_ctl(w, 0.0, 0.0, stream);
+    Engine e{P, w, stream};  // hook copies and the wall-time events
+    set_grid(e.rc, P);
+    KCT_CUDA(cudaStreamSynchronize(stream));
+
+    HookScope hooks(e);
+    const double t0 = now_s();
+    e.mark_start();
+    // krylov.hpp:66-96
+    if (tol > 0.0 && x0) {
+        KCT_LAUNCH(k_stats, w.x, w.m, w.part);
+        k_set_nonzero<<<1, kBlock, 0, stream>>>(w.ctl, w.part);
+        KCT_LAUNCHED();
+        st.adjoint(r, w.p);  // A^T b, the tolerance reference of a warm start (:81-88)
+        launch_scalar(w, S_REF, stream);
+    }
+    if (x0) {
+        st.apply(w.x, q);
+        KCT_LAUNCH(k_stack_sub, r, q, R, w.part);
+    }
+    st.adjoint(r, w.s);
+    launch_scalar(w, S_INIT, stream, tol);
+    KCT_LAUNCH(k_update_p, w.p, w.s, w.m, w.ctl, 1);
+    Ctl c{};
+    bool stopped = false;
+    if (tol > 0.0) stopped = (c = read_ctl(w, stream)).stop != 0;
+    // krylov.hpp:98-125
+    for (size_t it = 0; it < iters && !stopped; ++it) {
+        st.apply(w.p, q);
+        launch_scalar(w, S_DELTA, stream);
+        KCT_LAUNCH(k_update_xr, w.x, w.p, w.m, r, q, R, nullptr, w.ctl, w.part);
+        e.hook_copy();
+        st.adjoint(r, w.s);
+        launch_scalar(w, S_GAMMA, stream, 0.0, w.hist, nullptr);
+        KCT_LAUNCH(k_update_p, w.p, w.s, w.m, w.ctl, 0);
+        if (e.n_wall < w.wall_ev.size()) KCT_CUDA(cudaEventRecord(w.wall_ev[e.n_wall++], stream));
+        // an early stop (tolerance) is noticed within a few iterations
+        if (tol > 0.0 && (it & 3) == 3) stopped = (c = read_ctl(w, stream)).stop != 0;
+    }
+    c = read_ctl(w, stream);
+    const double secs = now_s() - t0;
+    e.hook_drain();
+    throw_solver(c);
+    stage_out(P, w.x, x_out, w.m, true, mem, layout, 2, stream);
+    if (rep) {
+        const size_t n = (size_t)c.iters;
+        copy_hist(rep->residual_history, w.hist, n, stream);
+        KCT_CUDA(cudaStreamSynchronize(stream));
+        rep->residual_count = n;
+        rep->solve_seconds = secs;
+        rep->converged = c.converged;
+        rep->breakdown = c.breakdown;
+        write_wall(e, rep);
+        if (rep->wall_count > n) rep->wall_count = n;
     }
     KCT_CUDA(cudaStreamSynchronize(stream));
 }

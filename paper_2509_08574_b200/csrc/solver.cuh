@@ -20,6 +20,11 @@ void irn_solve(Projector& P, int kind, const float* b, const float* prior, const
                const float* gt, const kct_reg_params& params, float* x_out, kct_report* rep,
                int mem, int layout, cudaStream_t s);
 
+// cgls over a caller-assembled StackedMap (krylov.hpp:59-127, linear_map.hpp:159-216)
+void cgls_stack(Projector& P, const kct_stack_block* blocks, size_t n_blocks, const float* b,
+                const float* x0, size_t iters, double tol, float* x_out, kct_report* rep, int mem,
+                int layout, cudaStream_t s);
+
 // Staging helpers shared with capi.cu.
 const float* stage_in(Projector& P, const float* src, size_t n, bool is_vol, int mem, int layout,
                       int slot, int tmp_slot, cudaStream_t s);

@@ -2,6 +2,7 @@
 // the unmodified reference.  Compiled against /root/reference headers by
 // oracle/Makefile (target `shim`) into oracle/_ref/test_shim; run on a GPU box by
 // tests/test_shim_gpu.py.  Exit code 0 = all checks passed.
+#include <kryct/diffreg.hpp>
 #include <kryct/krylov.hpp>
 #include <kryct/projector.hpp>
 #include <kryct/recon.hpp>
@@ -61,6 +62,68 @@ int main() {
     const auto r_gpu = cgls(gpu, bf, x0, {.max_iters = 10});
     expect(rel(r_gpu.x, r_ref.x) < 1e-3, "kryct::cgls(GpuConeBeamProjector) vs reference",
            rel(r_gpu.x, r_ref.x));
+
+    // device-resident cgls over a caller-assembled stack (krylov.hpp:59-127 on
+    // linear_map.hpp:159-216): the reweighted system recon.hpp:211-221 builds,
+    // assembled with the reference's own compose / DiagonalMap / stack_maps
+    {
+        auto gpu_sp = std::make_shared<kryct_b200::GpuConeBeamProjector>(grid, g);
+        auto ref_sp = std::make_shared<ConeBeamProjector>(grid, g);
+        auto D = make_diff(grid.dims);
+        const auto w1 = tv_weights(D->apply(x), 1e-3);
+        std::vector<double> xs(x.size());
+        for (size_t i = 0; i < x.size(); ++i) xs[i] = static_cast<float>(0.1 * x[i]);
+        auto w2 = tv_weights(D->apply(xs), 1e-3);
+        std::vector<double> w1f(w1.size()), w2f(w2.size()), wi(x.size());
+        for (size_t i = 0; i < w1.size(); ++i) w1f[i] = static_cast<float>(w1[i]);
+        for (size_t i = 0; i < w2.size(); ++i) w2f[i] = static_cast<float>(w2[i]);
+        for (size_t i = 0; i < wi.size(); ++i) wi[i] = static_cast<float>(0.5 + 10.0 * x[i]);
+        auto mk = [&](std::shared_ptr<const LinearMap> A) {
+            return stack_maps({{1.0, A},
+                               {0.01, compose(std::make_shared<DiagonalMap>(w1f), D)},
+                               {0.02, compose(std::make_shared<DiagonalMap>(w2f), D)},
+                               {0.05, compose(std::make_shared<DiagonalMap>(wi),
+                                              std::make_shared<IdentityMap>(x.size()))}});
+        };
+        const auto S_gpu = mk(gpu_sp);
+        const auto S_ref = mk(ref_sp);
+        std::vector<double> rhs(S_ref->range_size(), 0.0);
+        std::copy(bf.begin(), bf.end(), rhs.begin());
+        for (size_t i = 0; i < x.size(); ++i)
+            rhs[S_ref->block_offset(3) + i] = static_cast<float>(0.05 * wi[i] * 0.9 * x[i]);
+        const auto s_ref = cgls(*S_ref, rhs, x0, {.max_iters = 8});
+        std::vector<size_t> seen;
+        KrylovConfig kc;
+        kc.max_iters = 8;
+        kc.hook = [&](std::size_t it, std::span<const double>) { seen.push_back(it); };
+        const auto s_gpu = kryct_b200::cgls(*S_gpu, rhs, x0, kc);
+        expect(rel(s_gpu.x, s_ref.x) < 1e-3, "kryct_b200::cgls(stack) vs kryct::cgls(stack)",
+               rel(s_gpu.x, s_ref.x));
+        expect(s_gpu.trace.iterations == s_ref.trace.iterations &&
+                   rel(s_gpu.trace.residual_norms, s_ref.trace.residual_norms) < 1e-3,
+               "stack cgls: residual norms", rel(s_gpu.trace.residual_norms, s_ref.trace.residual_norms));
+        expect(seen.size() == 8 && seen.front() == 1 && seen.back() == 8 &&
+                   s_gpu.trace.wall_times.size() == 8,
+               "stack cgls: hook order + wall_times", (double)seen.size());
+        // warm start with a tolerance (krylov.hpp:81-96)
+        const auto t_ref = cgls(*S_ref, rhs, xs, {.max_iters = 30, .tolerance = 0.05});
+        const auto t_gpu = kryct_b200::cgls(*S_gpu, rhs, xs, {.max_iters = 30, .tolerance = 0.05});
+        expect(t_gpu.trace.converged == t_ref.trace.converged &&
+                   t_gpu.trace.iterations == t_ref.trace.iterations && rel(t_gpu.x, t_ref.x) < 1e-3,
+               "stack cgls: warm start + tolerance", rel(t_gpu.x, t_ref.x));
+        bool bad_rhs = false, bad_map = false;
+        try {
+            kryct_b200::cgls(*S_gpu, bf, x0, {.max_iters = 2});
+        } catch (const ConfigError&) {
+            bad_rhs = true;
+        }
+        try {   // a CPU projector block is not something the device solver can run
+            kryct_b200::cgls(*S_ref, rhs, x0, {.max_iters = 2});
+        } catch (const ConfigError&) {
+            bad_map = true;
+        }
+        expect(bad_rhs && bad_map, "stack cgls: ConfigError on size / unsupported block", 0.0);
+    }
 
     // solver entry points with the reference signatures
     ProjectionSet proj(g);

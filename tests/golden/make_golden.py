@@ -97,13 +97,56 @@ def fdk_case(ref, name, grid, geom, seed):
                         **grid_dict(grid), **geom_dict(geom))
 
 
+def stack_inputs(ref, grid, geom, seed):
+    """Two caller-assembled stacks (linear_map.hpp:159-216) on the recon_small problem:
+    A = [A; 0.3 W1 D; 0.4 W2 D; 0.2 Wi I] from zero (the reweighted PICCS system of
+    recon.hpp:195-221 plus a weighted identity block), B = [0.7 Wp A; 0.5 D] warm-started
+    with a tolerance.  Returns float32-representable inputs."""
+    rng = np.random.default_rng(seed)
+    m, n = grid.count, geom.ray_count
+    dims = (grid.nx, grid.ny, grid.nz)
+    truth = f32(sphere(grid, 0.6, 0.8) + 0.05 * rng.uniform(0, 1, m))
+    prior = f32(0.9 * truth)
+    b = f32(ref.forward(grid, geom, truth) + 0.01 * rng.standard_normal(n))
+    xr = f32(truth + 0.02 * rng.standard_normal(m))
+    w1 = f32(ref.tv_weights(ref.diff(dims, xr), 1e-2))
+    w2 = f32(ref.tv_weights(ref.diff(dims, xr - prior), 1e-2))
+    wi = f32(rng.uniform(0.5, 1.5, m))
+    wp = f32(rng.uniform(0.5, 1.5, n))
+    rhs_a = np.concatenate([b, np.zeros(3 * m), f32(0.4 * w2 * ref.diff(dims, prior)),
+                            f32(0.2 * wi * prior)])
+    rhs_b = np.concatenate([f32(0.7 * wp * b), np.zeros(3 * m)])
+    return dict(truth=truth, prior=prior, b=b, w1=w1, w2=w2, wi=wi, wp=wp, rhs_a=rhs_a, rhs_b=rhs_b)
+
+
+def stack_blocks(d):
+    a = [(0, 1.0, None), (1, 0.3, d["w1"]), (1, 0.4, d["w2"]), (2, 0.2, d["wi"])]
+    b = [(0, 0.7, d["wp"]), (1, 0.5, None)]
+    return a, b
+
+
+def stack_case(ref, name, grid, geom, seed):
+    """cgls (krylov.hpp:59-127) over caller-assembled StackedMaps, by the reference."""
+    d = stack_inputs(ref, grid, geom, seed)
+    blk_a, blk_b = stack_blocks(d)
+    xa, ta = ref.cgls_stack(grid, geom, blk_a, d["rhs_a"], 6)
+    xb, tb = ref.cgls_stack(grid, geom, blk_b, d["rhs_b"], 12, x0=d["prior"], tol=2e-2)
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d, xa=xa, res_a=ta["residual_history"],
+                        xb=xb, res_b=tb["residual_history"], iters_b=tb["iterations"],
+                        converged_b=tb["converged"], **grid_dict(grid), **geom_dict(geom))
+
+
 def main():
     ref = Oracle("ref")
+    if len(sys.argv) > 1 and sys.argv[1] == "stack":   # add the stack fixture only
+        stack_case(ref, "stack_small", Grid(8, 8, 8), recon_geometry(6), 106)
+        return
     op_case(ref, "op_tiny", Grid(4, 4, 4, 1.0, 1.1, 0.9), tiny_geometry(8, 10, 9), 101)
     op_case(ref, "op_tiny_odd", Grid(5, 6, 4, 1.0, 1.1, 0.9), tiny_geometry(7, 9, 8), 102)
     op_case(ref, "op_c1_small", Grid(16, 16, 16, 4.0, 4.0, 4.0),
             Geometry(1000.0, 1500.0, 24, 24, 4.0, 4.0, uniform_angles(16)), 103)
     recon_case(ref, "recon_small", Grid(8, 8, 8), recon_geometry(6), 104)
+    stack_case(ref, "stack_small", Grid(8, 8, 8), recon_geometry(6), 106)
     fdk_case(ref, "fdk_small", Grid(24, 24, 16, 2.0, 2.0, 2.0),
              Geometry(1000.0, 1500.0, 48, 32, 2.0, 2.0, uniform_angles(36), 0.5, -0.7), 105)
     print("golden fixtures written to", OUT)

@@ -57,6 +57,50 @@ def test_recon_golden(ora):
     assert rel_l2(x, d["piccs_auto_x"]) < 1e-12
 
 
+def _stack_blocks(d):
+    a = [(0, 1.0, None), (1, 0.3, d["w1"]), (1, 0.4, d["w2"]), (2, 0.2, d["wi"])]
+    b = [(0, 0.7, d["wp"]), (1, 0.5, None)]
+    return a, b
+
+
+def test_stack_cgls_golden(ora):
+    """cgls (krylov.hpp:59-127) over caller-assembled StackedMaps
+    (linear_map.hpp:159-216): the restatement against the reference's own run."""
+    d = load_golden("stack_small")
+    grid, geom = grid_from(d), geom_from(d)
+    blk_a, blk_b = _stack_blocks(d)
+    xa, ta = ora.cgls_stack(grid, geom, blk_a, d["rhs_a"], 6)
+    assert rel_l2(xa, d["xa"]) < 1e-12
+    np.testing.assert_allclose(ta["residual_history"], d["res_a"], rtol=1e-12)
+    xb, tb = ora.cgls_stack(grid, geom, blk_b, d["rhs_b"], 12, x0=d["prior"], tol=2e-2)
+    assert rel_l2(xb, d["xb"]) < 1e-12
+    np.testing.assert_allclose(tb["residual_history"], d["res_b"], rtol=1e-12)
+    assert tb["iterations"] == int(d["iters_b"]) and tb["converged"] == bool(d["converged_b"])
+
+
+def test_stack_cgls_reduces_to_irn_cycle(ora):
+    """One outer cycle of irn_piccs is cgls on [A; a W1 D; l W2 D] with the rhs
+    [b; 0; l W2 D x_p] (recon.hpp:195-232) — the stack API reproduces it."""
+    d = load_golden("recon_small")
+    grid, geom = grid_from(d), geom_from(d)
+    dims, m = (grid.nx, grid.ny, grid.nz), grid.count
+    tau, a, lam = 1e-3, 0.3, 0.3
+    w1 = ora.tv_weights(ora.diff(dims, np.zeros(m)), tau)
+    w2 = ora.tv_weights(ora.diff(dims, -d["prior"]), tau)
+    rhs = np.concatenate([d["b"], np.zeros(3 * m), lam * w2 * ora.diff(dims, d["prior"])])
+    x, _ = ora.cgls_stack(grid, geom, [(0, 1.0, None), (1, a, w1), (1, lam, w2)], rhs, 4)
+    xi, _ = ora.irn(grid, geom, KIND_PICCS, d["b"], d["prior"],
+                    dict(alpha=a, outer_iters=1, inner_iters=4, tau=tau))
+    assert rel_l2(x, xi) < 1e-12
+
+
+def test_stack_errors(ora):
+    d = load_golden("stack_small")
+    grid, geom = grid_from(d), geom_from(d)
+    with pytest.raises(Exception):
+        ora.cgls_stack(grid, geom, [(7, 1.0, None)], np.zeros(geom.ray_count), 2)
+
+
 def test_fdk_golden(ora):
     """fdk.hpp:50-139 restated (radix-2 FFT ramp filter) reproduces the reference."""
     d = load_golden("fdk_small")
