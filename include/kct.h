@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define KCT_ABI_VERSION 3
+#define KCT_ABI_VERSION 4
 
 enum kct_status {
     KCT_OK = 0,
@@ -217,6 +217,50 @@ typedef int (*kct_halo_fn)(void* ctx, const void* lo_plane, const void* hi_plane
                            void* hi_halo, size_t count, void* stream);
 int kct_set_slab(kct_projector* h, int rank, int world, int j0, int ny_global, kct_halo_fn fn,
                  void* ctx);
+
+/* Library-owned NCCL communicator (ABI 4): the two hooks above served by
+ * NCCL itself — ncclAllReduce for the sums, one grouped ncclSend / ncclRecv
+ * pair per neighbour for the halo planes — enqueued on the solver's stream
+ * with no host synchronisation and no callback into the caller's runtime, so
+ * a C++ host (kryct_b200.hpp) runs multi-GPU solves without Python.  One
+ * process per GPU; NCCL is bound at run time (the libnccl.so.2 already loaded
+ * in the process, else the system's; KCT_NCCL_LIB overrides), the library
+ * itself does not link it.  Not part of the reference (single-process,
+ * OpenMP only: projector.hpp:178-181).
+ *   kct_comm_unique_id  fill `id` (KCT_COMM_ID_BYTES) on one rank; the caller
+ *                       distributes it (file, MPI, torch.distributed, ...)
+ *   kct_comm_create     join as `rank` of `world` on CUDA device `device`, which
+ *                       becomes the calling thread's current device (< 0: stay
+ *                       on the current device); collective over the ranks
+ *   kct_comm_allreduce  in-place sum (dtype 0 = float32, 1 = float64) or,
+ *                       op = 1, maximum, of a device buffer over the ranks
+ *   kct_comm_allreduce_host  the same for a host buffer, staged through a
+ *                       temporary device buffer (joining the ranks' result
+ *                       slabs once per solve; not for the iteration path)
+ *   kct_use_comm        kct_set_allreduce with the communicator's all-reduce
+ *                       (angle-sharded mode); comm = NULL: single-process
+ *   kct_use_comm_slab   kct_set_allreduce + kct_set_slab (rank and world from
+ *                       the communicator) with the communicator's exchange */
+#define KCT_COMM_ID_BYTES 128
+typedef struct kct_comm kct_comm;
+int kct_comm_unique_id(void* id);
+int kct_comm_create(int rank, int world, const void* id, int device, kct_comm** out);
+int kct_comm_destroy(kct_comm* c);
+int kct_comm_rank(const kct_comm* c);
+int kct_comm_world(const kct_comm* c);
+int kct_comm_allreduce(kct_comm* c, void* buf, size_t count, int dtype, int op, void* stream);
+int kct_comm_allreduce_host(kct_comm* c, void* buf, size_t count, int dtype, int op);
+int kct_use_comm(kct_projector* h, kct_comm* c);
+int kct_use_comm_slab(kct_projector* h, kct_comm* c, int j0, int ny_global);
+
+/* Work-balanced y-slab boundaries for `world` ranks (world + 1 ints, bounds[0]
+ * = 0, bounds[world] = ny): contiguous y-plane ranges of about equal
+ * backprojection work — the number of (voxel column, angle) pairs of a plane
+ * that project onto the detector's u extent, counted over a full circle of 64
+ * views of this system so that every scan of one system gets the same slabs —
+ * interior boundaries on multiples of 4 planes (whole adjoint bricks).  Host
+ * arithmetic only. */
+int kct_slab_bounds(const kct_grid* grid, const kct_geometry* geom, int world, int* bounds);
 
 /* ---- solvers ---------------------------------------------------------- */
 /* cgls_recon (recon.hpp:312-315 -> baseline_solve :274-307 -> cgls krylov.hpp:59-127).

@@ -11,6 +11,9 @@
 //     blocks are a GpuConeBeamProjector, kryct::DiffOperator or
 //     kryct::IdentityMap, each optionally under compose(DiagonalMap, .) —
 //     the stacks recon.hpp:211-221 assembles (kct_cgls_stack)
+//   kryct_b200::Communicator + the same drivers with a communicator first:
+//     one process per GPU, y-slab-sharded solves over the library's own NCCL
+//     communicator (kct_comm_*; no reference counterpart)
 // so existing callers switch by namespace, and the reference's own generic
 // solvers (kryct::cgls, kryct::StackedMap, ...) can drive the GPU operator.
 // Values cross the boundary as float32 (the reference reads float32 files,
@@ -36,7 +39,11 @@
 #include <kryct/recon.hpp>
 #include <kryct/types.hpp>
 
+#include <algorithm>
+#include <array>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <exception>
 #include <future>
@@ -45,6 +52,8 @@
 #include <mutex>
 #include <span>
 #include <string>
+#include <thread>
+#include <utility>
 #include <vector>
 
 #include "kct.h"
@@ -537,6 +546,248 @@ inline kryct::ReconReport irn_piccs(const kryct::ProjectionSet& proj, const kryc
                                     const kryct::RegularizationParams& params,
                                     const kryct::ReconOptions& opts = {}) {
     return detail::run(KCT_KIND_PICCS, proj, grid, &prior, &params, 0, 0.0, opts);
+}
+
+// ---- multi-GPU: one process per GPU, y-slab-sharded solves ------------------
+// The reference is single-process (OpenMP only, projector.hpp:178-181); these
+// entry points are the B200 library's scale-out of the same solvers (SURVEY
+// §8e: volume vectors partitioned in slabs, NCCL over NVLink for the partial
+// projections, the halo planes and the Krylov scalars).  Every rank calls
+// with the SAME arguments (all projections, full-size prior / initial /
+// ground truth) and gets the same report; the library's own NCCL
+// communicator (kct_comm_*) carries the collectives, no MPI or Python needed.
+
+/// RAII handle of the library's NCCL communicator.
+class Communicator {
+  public:
+    using Id = std::array<unsigned char, KCT_COMM_ID_BYTES>;
+    static Id unique_id() {
+        Id id{};
+        detail::check(kct_comm_unique_id(id.data()));
+        return id;
+    }
+    /// Join as `rank` of `world` (collective); `device` >= 0 becomes the
+    /// calling thread's CUDA device.
+    Communicator(int rank, int world, const Id& id, int device = -1) {
+        kct_comm* c = nullptr;
+        detail::check(kct_comm_create(rank, world, id.data(), device, &c));
+        c_ = std::shared_ptr<kct_comm>(c, [](kct_comm* p) { kct_comm_destroy(p); });
+    }
+    /// From a launcher's environment (torchrun / mpirun / srun): rank = RANK |
+    /// OMPI_COMM_WORLD_RANK | PMI_RANK | SLURM_PROCID, world = WORLD_SIZE | ...,
+    /// device = LOCAL_RANK | OMPI_COMM_WORLD_LOCAL_RANK | SLURM_LOCALID (else
+    /// rank).  The unique id travels through `id_file` (default
+    /// $KCT_COMM_ID_FILE; a path on a file system all ranks see, fresh per
+    /// job): rank 0 writes it atomically and removes it once every rank has
+    /// joined, the others poll for it ($KCT_COMM_TIMEOUT seconds, default 120).
+    static Communicator from_env(std::string id_file = {}) {
+        auto env_int = [](std::initializer_list<const char*> names, int dflt) {
+            for (const char* n : names)
+                if (const char* v = std::getenv(n)) return std::atoi(v);
+            return dflt;
+        };
+        const int rank = env_int({"RANK", "OMPI_COMM_WORLD_RANK", "PMI_RANK", "SLURM_PROCID"}, 0);
+        const int world = env_int({"WORLD_SIZE", "OMPI_COMM_WORLD_SIZE", "PMI_SIZE", "SLURM_NTASKS"}, 1);
+        const int device =
+            env_int({"LOCAL_RANK", "OMPI_COMM_WORLD_LOCAL_RANK", "SLURM_LOCALID"}, rank);
+        if (id_file.empty())
+            if (const char* f = std::getenv("KCT_COMM_ID_FILE")) id_file = f;
+        Id id{};
+        if (world > 1 && id_file.empty())
+            throw kryct::ConfigError("Communicator::from_env: no id file (KCT_COMM_ID_FILE)");
+        if (rank == 0) {
+            id = unique_id();
+            if (world > 1) {
+                const std::string tmp = id_file + ".tmp";
+                std::FILE* f = std::fopen(tmp.c_str(), "wb");
+                if (!f || std::fwrite(id.data(), 1, id.size(), f) != id.size())
+                    throw kryct::ConfigError("Communicator: cannot write " + tmp);
+                std::fclose(f);
+                if (std::rename(tmp.c_str(), id_file.c_str()) != 0)
+                    throw kryct::ConfigError("Communicator: cannot create " + id_file);
+            }
+        } else {
+            const char* t = std::getenv("KCT_COMM_TIMEOUT");
+            const double limit = t ? std::atof(t) : 120.0;
+            const auto t0 = std::chrono::steady_clock::now();
+            for (;;) {
+                if (std::FILE* f = std::fopen(id_file.c_str(), "rb")) {
+                    const std::size_t n = std::fread(id.data(), 1, id.size(), f);
+                    std::fclose(f);
+                    if (n == id.size()) break;
+                }
+                if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit)
+                    throw kryct::ConfigError("Communicator: timed out waiting for " + id_file);
+                std::this_thread::sleep_for(std::chrono::milliseconds(20));
+            }
+        }
+        Communicator c(rank, world, id, device);
+        if (rank == 0 && world > 1) std::remove(id_file.c_str());  // every rank has joined
+        return c;
+    }
+    int rank() const { return kct_comm_rank(c_.get()); }
+    int world() const { return kct_comm_world(c_.get()); }
+    kct_comm* handle() const { return c_.get(); }
+    /// In-place sum (or maximum) of a host array over the ranks.
+    void all_reduce(std::span<double> v, bool max = false) const {
+        detail::check(kct_comm_allreduce_host(c_.get(), v.data(), v.size(), 1, max ? 1 : 0));
+    }
+
+  private:
+    std::shared_ptr<kct_comm> c_;
+};
+
+/// This rank's y-plane range [j0, j1) of `grid` (kct_slab_bounds: balanced by
+/// backprojection work, the same on every rank and for every scan of a system).
+inline std::pair<int, int> slab_range(const Communicator& comm, const kryct::GridSpec& grid,
+                                      const kryct::ConeBeamGeometry& geom) {
+    std::vector<int> bounds(static_cast<std::size_t>(comm.world()) + 1);
+    const kct_grid g = detail::to_grid(grid);
+    const kct_geometry ge = detail::to_geom(geom);
+    detail::check(kct_slab_bounds(&g, &ge, comm.world(), bounds.data()));
+    return {bounds[comm.rank()], bounds[comm.rank() + 1]};
+}
+
+namespace detail {
+
+// planes [j0, j1) of a reference-layout (x-fastest) volume, as float32
+inline std::vector<float> y_slab_f32(std::span<const double> v, const kryct::Dims3& d, int j0,
+                                     int j1, const char* what) {
+    const std::size_t nx = d.nx, ny = d.ny, nz = d.nz, sy = static_cast<std::size_t>(j1 - j0);
+    std::vector<float> out(nx * sy * nz);
+    bool ok = true;
+    for (std::size_t k = 0; k < nz; ++k)
+        for (std::size_t j = 0; j < sy; ++j) {
+            const double* src = v.data() + nx * (j0 + j + ny * k);
+            float* dst = out.data() + nx * (j + sy * k);
+            for (std::size_t i = 0; i < nx; ++i) {
+                ok = ok && std::isfinite(src[i]);
+                dst[i] = static_cast<float>(src[i]);
+            }
+        }
+    if (!ok) throw kryct::ConfigError(std::string(what) + " contains non-finite values");
+    return out;
+}
+
+inline kryct::ReconReport run_slab(const Communicator& comm, int kind,
+                                   const kryct::ProjectionSet& proj, const kryct::GridSpec& grid,
+                                   const kryct::Volume* prior,
+                                   const kryct::RegularizationParams* params, std::size_t iters,
+                                   double tol, const kryct::ReconOptions& opts) {
+    proj.geometry.validate();
+    if (proj.data.size() != proj.geometry.ray_count())
+        throw kryct::ConfigError("projection data length does not match geometry");
+    grid.validate();
+    if (opts.hook)
+        throw kryct::ConfigError("ReconOptions::hook is not served by the slab-sharded solves "
+                                 "(each rank holds a slab of the iterate)");
+    const auto [j0, j1] = slab_range(comm, grid, proj.geometry);
+    kryct::GridSpec sg = grid;
+    sg.dims.ny = j1 - j0;
+    sg.origin.y = grid.origin.y + j0 * grid.spacing.y;
+    CheckedOut co(sg, proj.geometry);
+    const GpuConeBeamProjector& A = *co.h;
+    check(kct_use_comm_slab(A.handle(), comm.handle(), j0, grid.dims.ny));
+    struct Leave {  // a cached handle goes back in single-process mode
+        kct_projector* h;
+        ~Leave() { kct_use_comm_slab(h, nullptr, 0, 0); }
+    } leave{A.handle()};
+    std::vector<float> b(proj.data.size());
+    if (!to_f32(proj.data, b.data()))
+        throw kryct::ConfigError("projections contain non-finite values");
+    auto slab_of = [&](const kryct::Volume& v, const char* what) {
+        if (!(v.dims == grid.dims))
+            throw kryct::ConfigError(std::string(what) + " does not match the reconstruction grid");
+        return y_slab_f32(v.data, grid.dims, j0, j1, what);
+    };
+    std::vector<float> pr, x0, gt;
+    if (prior) pr = slab_of(*prior, "prior volume");
+    if (opts.initial) x0 = slab_of(*opts.initial, "initial volume");
+    if (opts.ground_truth) gt = slab_of(*opts.ground_truth, "ground truth");
+    const std::size_t ms = sg.dims.count(), m = grid.dims.count();
+    std::vector<float> x(ms);
+    const std::size_t outer = params ? params->outer_iters : 1;
+    const std::size_t inner = params ? params->inner_iters : iters;
+    std::vector<double> obj(outer * inner + outer + 1), res(outer * inner), err(outer * inner),
+        secs(outer + 1);
+    std::vector<uint64_t> bnd(outer + 1);
+    kct_report rep{};
+    rep.objective_history = obj.data();
+    rep.residual_history = res.data();
+    rep.error_history = err.data();
+    rep.outer_boundaries = bnd.data();
+    rep.outer_seconds = secs.data();
+    const float* ppr = pr.empty() ? nullptr : pr.data();
+    const float* px0 = x0.empty() ? nullptr : x0.data();
+    const float* pgt = gt.empty() ? nullptr : gt.data();
+    if (params) {
+        const kct_reg_params p{params->alpha,       params->lambda,       params->tau,
+                               params->outer_iters, params->inner_iters, params->inner_tolerance,
+                               params->warm_start ? 1 : 0};
+        check(kct_irn(A.handle(), kind, b.data(), ppr, px0, pgt, &p, x.data(), &rep, KCT_MEM_HOST,
+                      KCT_LAYOUT_REFERENCE, nullptr));
+    } else {
+        check(kct_cgls_recon(A.handle(), b.data(), iters, px0, pgt, tol, x.data(), &rep,
+                             KCT_MEM_HOST, KCT_LAYOUT_REFERENCE, nullptr));
+    }
+    // join the slabs: every rank places its planes in a zero volume; the sum
+    // over the ranks (x + 0 + ... + 0, exact) is the whole iterate everywhere
+    std::vector<float> full(comm.world() > 1 ? m : 0);
+    const float* whole = x.data();
+    if (comm.world() > 1) {
+        const std::size_t nx = grid.dims.nx, ny = grid.dims.ny, nz = grid.dims.nz,
+                          sy = static_cast<std::size_t>(j1 - j0);
+        for (std::size_t k = 0; k < nz; ++k)
+            for (std::size_t j = 0; j < sy; ++j)
+                std::copy_n(x.data() + nx * (j + sy * k), nx, full.data() + nx * (j0 + j + ny * k));
+        check(kct_comm_allreduce_host(comm.handle(), full.data(), m, 0, 0));
+        whole = full.data();
+    }
+    kryct::ReconReport r;
+    r.volume.dims = grid.dims;
+    r.volume.spacing = grid.spacing;
+    r.volume.origin = grid.origin;
+    r.volume.data.assign(whole, whole + m);
+    r.objective_history.assign(obj.begin(), obj.begin() + rep.objective_count);
+    r.residual_history.assign(res.begin(), res.begin() + rep.residual_count);
+    r.error_history.assign(err.begin(), err.begin() + rep.error_count);
+    for (std::size_t i = 0; i < rep.outer_count; ++i) {
+        r.outer_boundaries.push_back(bnd[i]);
+        r.outer_seconds.push_back(secs[i]);
+    }
+    r.solve_seconds = rep.solve_seconds;
+    r.converged = rep.converged != 0;
+    return r;
+}
+
+}  // namespace detail
+
+/// cgls_recon (recon.hpp:312-315) over the communicator's GPUs.
+inline kryct::ReconReport cgls_recon(const Communicator& comm, const kryct::ProjectionSet& proj,
+                                     const kryct::GridSpec& grid, std::size_t iters,
+                                     const kryct::ReconOptions& opts = {}, double tolerance = 0.0) {
+    return detail::run_slab(comm, KCT_KIND_TV, proj, grid, nullptr, nullptr, iters, tolerance, opts);
+}
+/// irn_tv (recon.hpp:252-255) over the communicator's GPUs.
+inline kryct::ReconReport irn_tv(const Communicator& comm, const kryct::ProjectionSet& proj,
+                                 const kryct::GridSpec& grid,
+                                 const kryct::RegularizationParams& params,
+                                 const kryct::ReconOptions& opts = {}) {
+    return detail::run_slab(comm, KCT_KIND_TV, proj, grid, nullptr, &params, 0, 0.0, opts);
+}
+/// irn_piple (recon.hpp:260-263) over the communicator's GPUs.
+inline kryct::ReconReport irn_piple(const Communicator& comm, const kryct::ProjectionSet& proj,
+                                    const kryct::GridSpec& grid, const kryct::Volume& prior,
+                                    const kryct::RegularizationParams& params,
+                                    const kryct::ReconOptions& opts = {}) {
+    return detail::run_slab(comm, KCT_KIND_PIPLE, proj, grid, &prior, &params, 0, 0.0, opts);
+}
+/// irn_piccs (recon.hpp:267-270) over the communicator's GPUs.
+inline kryct::ReconReport irn_piccs(const Communicator& comm, const kryct::ProjectionSet& proj,
+                                    const kryct::GridSpec& grid, const kryct::Volume& prior,
+                                    const kryct::RegularizationParams& params,
+                                    const kryct::ReconOptions& opts = {}) {
+    return detail::run_slab(comm, KCT_KIND_PICCS, proj, grid, &prior, &params, 0, 0.0, opts);
 }
 
 }  // namespace kryct_b200

@@ -134,6 +134,16 @@ _SIGS = {
                        C.c_int, _P], C.c_int),
     "kct_resolve_tau": ([C.c_double, _P, C.c_size_t], C.c_double),
     "kct_set_allreduce": ([_P, _P, _P], C.c_int),  # typed by distributed.install_allreduce
+    "kct_comm_unique_id": ([_P], C.c_int),
+    "kct_comm_create": ([C.c_int, C.c_int, _P, C.c_int, C.POINTER(_P)], C.c_int),
+    "kct_comm_destroy": ([_P], C.c_int),
+    "kct_comm_rank": ([_P], C.c_int),
+    "kct_comm_world": ([_P], C.c_int),
+    "kct_comm_allreduce": ([_P, _P, C.c_size_t, C.c_int, C.c_int, _P], C.c_int),
+    "kct_comm_allreduce_host": ([_P, _P, C.c_size_t, C.c_int, C.c_int], C.c_int),
+    "kct_use_comm": ([_P, _P], C.c_int),
+    "kct_use_comm_slab": ([_P, _P, C.c_int, C.c_int], C.c_int),
+    "kct_slab_bounds": ([C.POINTER(_Grid), C.POINTER(_Geom), C.c_int, C.POINTER(C.c_int)], C.c_int),
     "kct_fdk": ([_P, _P, _P, C.c_int, C.c_int, _P], C.c_int),
     "kct_set_option": ([_P, C.c_char_p, C.c_double], C.c_int),
     "kct_set_iterate_hook": ([_P, _ITER_HOOK, _P], C.c_int),

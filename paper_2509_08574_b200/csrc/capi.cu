@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -76,6 +77,9 @@ __global__ void sum_counts_kernel(const float* __restrict__ c, size_t n, unsigne
 }  // namespace
 
 namespace kct {
+
+// comm.cu's entry points share the status mapping and the last-error slot
+int guard_call(const std::function<void()>& f) { return guarded(f); }
 
 std::atomic<unsigned long long> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }

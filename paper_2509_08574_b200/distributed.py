@@ -54,11 +54,84 @@ def _on_stream(stream, device):
     return torch.cuda.stream(torch.cuda.ExternalStream(stream, device=device))
 
 
-def install_allreduce(projector: ConeBeamProjector, group=None) -> None:
-    """Put `projector` in angle-sharded mode, summing over `group` (torch.distributed)."""
+class NativeComm:
+    """The library's own NCCL communicator (`kct_comm_*`, include/kct.h): the
+    solver's sums and halo exchanges become ncclAllReduce / grouped ncclSend +
+    ncclRecv enqueued on the solver's stream by the library itself — no Python
+    trampoline and no host synchronisation per collective.  Join with an
+    explicit (rank, world, id) or bootstrap over a torch.distributed group
+    (`NativeComm.from_group`: rank 0's unique id is broadcast as an object)."""
+
+    def __init__(self, rank: int, world: int, uid: bytes):
+        lib = load_library()
+        if len(uid) != ID_BYTES:
+            raise ValueError(f"unique id must be {ID_BYTES} bytes")
+        h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(uid), ID_BYTES)
+        _check(lib.kct_comm_create(int(rank), int(world), buf, -1, C.byref(h)))
+        self.handle, self.rank, self.world = h, int(rank), int(world)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(ID_BYTES)
+        _check(load_library().kct_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_group(cls, group=None) -> "NativeComm":
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        box = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0 if group is None else dist.get_global_rank(group, 0),
+                                   group=group)
+        return cls(rank, world, box[0])
+
+    def all_reduce(self, tensor, op: str = "sum", stream=None) -> None:
+        """In-place sum / max of a contiguous float32 / float64 CUDA tensor."""
+        import torch
+        dt = {torch.float32: 0, torch.float64: 1}[tensor.dtype]
+        assert tensor.is_cuda and tensor.is_contiguous()
+        s = torch.cuda.current_stream().cuda_stream if stream is None else stream
+        _check(load_library().kct_comm_allreduce(self.handle, tensor.data_ptr(), tensor.numel(), dt,
+                                                 {"sum": 0, "max": 1}[op], s))
+
+    def close(self) -> None:
+        if self.handle:
+            load_library().kct_comm_destroy(self.handle)
+            self.handle = None
+
+
+ID_BYTES = 128  # KCT_COMM_ID_BYTES
+_native_comms: dict = {}
+
+
+def native_comm(group=None):
+    """The cached NativeComm of `group`, or None when the solves should go
+    through the torch.distributed hooks: any backend but nccl (the gloo tests),
+    or KCT_NATIVE_COMM=0."""
+    import os
+
+    import torch.distributed as dist
+    if os.environ.get("KCT_NATIVE_COMM", "1") == "0" or dist.get_backend(group) != "nccl":
+        return None
+    key = id(group) if group is not None else None
+    if key not in _native_comms:
+        _native_comms[key] = NativeComm.from_group(group)
+    return _native_comms[key]
+
+
+def install_allreduce(projector: ConeBeamProjector, group=None, comm=None) -> None:
+    """Put `projector` in angle-sharded mode, summing over `group`: through
+    the library's NCCL communicator (`comm`, or the group's `native_comm`) when
+    there is one, else through a torch.distributed all-reduce hook."""
     import torch
     import torch.distributed as dist
     lib = load_library()
+    comm = comm if comm is not None else native_comm(group)
+    if comm is not None:
+        _check(lib.kct_use_comm(projector.handle, comm.handle))
+        projector._comm = comm  # keep the communicator alive with the handle
+        return
     device = torch.device("cuda", torch.cuda.current_device())
 
     def hook(ctx, buf, count, dtype, stream):
@@ -121,14 +194,23 @@ def cgls_recon_sharded(proj_local, grid, iters, opts=None, tolerance=0.0, group=
 # y-slab-sharded solves
 # ---------------------------------------------------------------------------
 def install_slab(projector: ConeBeamProjector, rank: int, world: int, j0: int, ny_global: int,
-                 group=None) -> None:
+                 group=None, comm=None) -> None:
     """Put `projector` (built on this rank's y-slab grid) in slab mode: the
     all-reduce hook plus a neighbour exchange of boundary y planes (P2P
-    send / recv with ranks r - 1 and r + 1; CPU staging under gloo)."""
+    send / recv with ranks r - 1 and r + 1) — both by the library's NCCL
+    communicator when there is one (`comm` / `native_comm(group)`), else by
+    torch.distributed hooks (CPU staging under gloo)."""
     import torch
     import torch.distributed as dist
-    install_allreduce(projector, group)
     lib = load_library()
+    comm = comm if comm is not None else native_comm(group)
+    if comm is not None:
+        if (comm.rank, comm.world) != (rank, world):
+            raise ValueError("communicator rank / world differ from the slab's")
+        _check(lib.kct_use_comm_slab(projector.handle, comm.handle, j0, ny_global))
+        projector._comm = comm
+        return
+    install_allreduce(projector, group)
     device = torch.device("cuda", torch.cuda.current_device())
     cpu = dist.get_backend(group) == "gloo"
 

@@ -9,6 +9,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <numbers>
 #include <random>
 #include <stdexcept>
@@ -186,6 +187,44 @@ int main() {
             hook_threw = true;
         }
         expect(hook_threw, "hook exception propagates to the caller", 0.0);
+    }
+
+    // multi-GPU entry points on the library's own NCCL communicator, world
+    // size 1 (one GPU here; NCCL refuses two ranks on one device): the
+    // y-slab-sharded drivers reduce to the single-process solves bit for bit
+    {
+        kryct_b200::Communicator comm(0, 1, kryct_b200::Communicator::unique_id());
+        expect(comm.rank() == 0 && comm.world() == 1, "Communicator: rank 0 of 1", 0.0);
+        const auto range = kryct_b200::slab_range(comm, grid, g);
+        expect(range.first == 0 && range.second == grid.dims.ny, "slab_range: whole grid", 0.0);
+        std::vector<double> v{1.0, 2.5, -3.0};
+        comm.all_reduce(v);
+        comm.all_reduce(v, true);
+        expect(v == std::vector<double>{1.0, 2.5, -3.0}, "Communicator::all_reduce (sum, max)", 0.0);
+        const auto s_gpu = kryct_b200::irn_piccs(comm, proj, grid, prior, p);
+        expect(s_gpu.volume.data == a_gpu.volume.data, "irn_piccs(comm, ...) == irn_piccs(...) bitwise",
+               rel(s_gpu.volume.data, a_gpu.volume.data));
+        expect(s_gpu.objective_history == a_gpu.objective_history, "slab objective history bitwise", 0.0);
+        const auto sc = kryct_b200::cgls_recon(comm, proj, grid, 8);
+        expect(sc.volume.data == c_gpu.volume.data, "cgls_recon(comm, ...) bitwise", 0.0);
+        // from_env with the launcher's variables of a 1-rank job
+        setenv("RANK", "0", 1);
+        setenv("WORLD_SIZE", "1", 1);
+        setenv("LOCAL_RANK", "0", 1);
+        auto env_comm = kryct_b200::Communicator::from_env();
+        expect(env_comm.world() == 1, "Communicator::from_env", 0.0);
+        // a handle that served a slab solve goes back to the cache single-process
+        const auto after = kryct_b200::irn_piccs(proj, grid, prior, p);
+        expect(after.volume.data == a_gpu.volume.data, "cached handle after a slab solve", 0.0);
+        bool rejected = false;
+        try {
+            ReconOptions o;
+            o.hook = [](std::size_t, std::span<const double>) {};
+            kryct_b200::cgls_recon(comm, proj, grid, 2, o);
+        } catch (const ConfigError&) {
+            rejected = true;
+        }
+        expect(rejected, "slab solves reject ReconOptions::hook (ConfigError)", 0.0);
     }
 
     // error taxonomy (test_projector.cpp:113-120)

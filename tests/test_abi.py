@@ -25,7 +25,7 @@ def test_library_loads_and_exports_header():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(k._SIGS), "python bindings must cover the header exactly"
-    assert lib.kct_abi_version() == 3
+    assert lib.kct_abi_version() == 4
 
 
 def test_library_is_sm100a():

@@ -225,3 +225,93 @@ def test_collectives_per_iteration(mode):
         assert per["scalar"] == 2, per
         assert per["vector"] == 1, per
         assert per["p2p"] == (2 if mode == "slab" else 0), per
+
+
+# ---- the library's own NCCL communicator (kct_comm_*, ABI 4) -----------------
+def _native_rank(q, mode):
+    """One rank on cuda:0 with a real NCCL communicator of world size 1 (more
+    ranks need more GPUs: NCCL refuses two ranks on one device)."""
+    from paper_2509_08574_b200 import distributed
+    torch.cuda.set_device(0)
+    out = {}
+    if mode == "torch":  # bootstrap over torch.distributed's nccl backend
+        import torch.distributed as dist
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+        dist.init_process_group("nccl", rank=0, world_size=1)
+        comm = distributed.native_comm()
+        assert comm is not None and (comm.rank, comm.world) == (0, 1)
+    else:  # no torch.distributed at all: explicit id
+        comm = distributed.NativeComm(0, 1, distributed.NativeComm.unique_id())
+    t = torch.arange(5, dtype=torch.float64, device="cuda")
+    comm.all_reduce(t, "sum")
+    comm.all_reduce(t, "max")
+    f = torch.full((7,), 2.5, dtype=torch.float32, device="cuda")
+    with torch.cuda.stream(torch.cuda.Stream()):  # a non-default current stream
+        comm.all_reduce(f)
+        torch.cuda.current_stream().synchronize()
+    out["reduce"] = (t.cpu().numpy(), f.cpu().numpy())
+    gs, ge, prior, b = _problem(8)
+    proj = k.ProjectionSet(ge, b)
+    params = k.RegularizationParams(**dict(PARAMS, tau=0.0))
+    ref = k.irn_piccs(proj, gs, prior, params)
+    # y-slab mode: the whole volume is rank 0's slab
+    A = k.ConeBeamProjector(gs, ge)
+    distributed.install_slab(A, 0, 1, 0, gs.dims[1], comm=comm)
+    n0 = k.launch_count()
+    rep = k.irn_piccs(proj, gs, prior, params, projector=A)
+    out["slab"] = (np.array_equal(rep.volume, ref.volume),
+                   rep.objective_history == ref.objective_history, rep.tau == ref.tau,
+                   k.launch_count() - n0)
+    # angle-sharded mode
+    A2 = k.ConeBeamProjector(gs, ge)
+    distributed.install_allreduce(A2, comm=comm)
+    rep2 = k.irn_piccs(proj, gs, prior, params, projector=A2)
+    out["angles"] = (np.array_equal(rep2.volume, ref.volume),
+                     rep2.residual_history == ref.residual_history)
+    if mode == "torch":  # the public entry picks the native communicator by itself
+        rep3 = distributed.irn_piccs_slab(proj, gs, prior, params)
+        out["auto"] = np.array_equal(rep3.volume, ref.volume)
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    comm.close()
+    q.put(out)
+
+
+@pytest.mark.parametrize("mode", ["explicit", "torch"])
+def test_native_nccl_comm_world1(mode):
+    """kct_comm_* with NCCL itself (run-time bound): sums and maxima on the
+    caller's stream, and slab / angle-sharded solves through the native hooks
+    bit-identical to the single-process solve at world size 1."""
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    p = ctx.Process(target=_native_rank, args=(q, mode))
+    p.start()
+    while q.empty() and p.is_alive():  # a crashed rank must fail the test, not hang it
+        p.join(0.2)
+    assert not q.empty(), f"rank exited with {p.exitcode}"
+    out = q.get()
+    p.join(300)
+    assert p.exitcode == 0
+    t, f = out["reduce"]
+    np.testing.assert_array_equal(t, np.arange(5.0))
+    np.testing.assert_array_equal(f, np.full(7, 2.5, np.float32))
+    assert out["slab"][:3] == (True, True, True) and out["slab"][3] > 0, out["slab"]
+    assert out["angles"] == (True, True), out["angles"]
+    if mode == "torch":
+        assert out["auto"]
+
+
+def test_native_comm_argument_errors():
+    """ConfigError before any NCCL work: bad rank / world, null id, null handle."""
+    import ctypes as C
+    lib = k.load_library()
+    h = C.c_void_p()
+    buf = C.create_string_buffer(128)
+    assert lib.kct_comm_create(2, 2, buf, -1, C.byref(h)) == 2
+    assert lib.kct_comm_create(0, 0, buf, -1, C.byref(h)) == 2
+    assert lib.kct_comm_create(0, 1, None, -1, C.byref(h)) == 2
+    assert lib.kct_comm_allreduce(None, None, 0, 0, 0, None) == 2
+    assert lib.kct_comm_rank(None) == -1 and lib.kct_comm_world(None) == 0
+    gs, ge, prior, b = _problem(8)
+    A = k.ConeBeamProjector(gs, ge)
+    assert lib.kct_use_comm(A.handle, None) == 0  # NULL: back to single-process

@@ -164,3 +164,30 @@ def test_slab_bounds_same_for_every_scan_of_a_system():
     assert b == distributed.slab_bounds(grid, g360, 8)
     sizes = np.diff(b)
     assert sizes[0] > sizes[3] and sizes[-1] > sizes[4]
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("dims,nu,pu,off", [((64, 64, 8), 96, 1.0, 0.0), ((48, 80, 4), 40, 1.7, 3.0),
+                                            ((256, 256, 4), 384, 0.5, 0.0), ((10, 9, 3), 12, 1.3, -0.4)])
+def test_native_slab_bounds_match_python(world, dims, nu, pu, off):
+    """kct_slab_bounds (the C++ host's slab split, include/kct.h) is the same
+    function as distributed.slab_bounds."""
+    import ctypes as C
+    from paper_2509_08574_b200 import distributed
+    sp = 1.0 if dims[0] != 256 else 0.5
+    grid = k.GridSpec(dims, (sp, sp, sp))
+    geom = k.ConeBeamGeometry(1000.0, 1500.0, nu, 16, pu, pu, k.uniform_angles(7), off, 0.0)
+    want = distributed.slab_bounds(grid, geom, world)
+    got = (C.c_int * (world + 1))()
+    g, ge = grid._c(), geom._c()
+    assert k.load_library().kct_slab_bounds(C.byref(g), C.byref(ge), world, got) == 0
+    assert list(got) == list(want)
+
+
+def test_native_slab_bounds_rejects_too_many_ranks():
+    import ctypes as C
+    grid = k.GridSpec((8, 4, 8))
+    geom = k.ConeBeamGeometry(100.0, 150.0, 12, 12, 1.0, 1.0, k.uniform_angles(4))
+    got = (C.c_int * 6)()
+    g, ge = grid._c(), geom._c()
+    assert k.load_library().kct_slab_bounds(C.byref(g), C.byref(ge), 5, got) == 2
