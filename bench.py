@@ -591,6 +591,10 @@ def run_recon(k, synth, cfg, grid, prior, follow, dev, args, ws=1, rank=0, share
                             "halo planes" if slab else
                             f"angle-sharded x{ws}: partial-volume + scalar all-reduces"
                             if ws > 1 else "single GPU"),
+            "collectives": (None if ws == 1 else
+                            "library NCCL communicator (kct_comm_*: ncclAllReduce / ncclSend+Recv "
+                            "on the solver's stream)" if getattr(A, "_comm", None) is not None
+                            else "torch.distributed hooks"),
             "setup_seconds_untimed": round(setup, 2),
             "reference_cpu": "the --impl reference line's recon.seconds_per_recon (same box, "
                              "all host cores); tests/test_config_parity_gpu.py measured 151.9 s "

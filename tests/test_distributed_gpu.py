@@ -259,18 +259,19 @@ def _native_rank(q, mode):
     distributed.install_slab(A, 0, 1, 0, gs.dims[1], comm=comm)
     n0 = k.launch_count()
     rep = k.irn_piccs(proj, gs, prior, params, projector=A)
-    out["slab"] = (np.array_equal(rep.volume, ref.volume),
-                   rep.objective_history == ref.objective_history, rep.tau == ref.tau,
+    out["slab"] = (bool(np.array_equal(rep.volume, ref.volume)),
+                   bool(np.array_equal(rep.objective_history, ref.objective_history)),
+                   bool(rep.tau == ref.tau),
                    k.launch_count() - n0)
     # angle-sharded mode
     A2 = k.ConeBeamProjector(gs, ge)
     distributed.install_allreduce(A2, comm=comm)
     rep2 = k.irn_piccs(proj, gs, prior, params, projector=A2)
-    out["angles"] = (np.array_equal(rep2.volume, ref.volume),
-                     rep2.residual_history == ref.residual_history)
+    out["angles"] = (bool(np.array_equal(rep2.volume, ref.volume)),
+                     bool(np.array_equal(rep2.residual_history, ref.residual_history)))
     if mode == "torch":  # the public entry picks the native communicator by itself
         rep3 = distributed.irn_piccs_slab(proj, gs, prior, params)
-        out["auto"] = np.array_equal(rep3.volume, ref.volume)
+        out["auto"] = bool(np.array_equal(rep3.volume, ref.volume))
         import torch.distributed as dist
         dist.destroy_process_group()
     comm.close()
