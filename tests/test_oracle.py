@@ -217,3 +217,18 @@ def test_lambda_zero_collapses_to_tv(ora):
     x_pc, _ = ora.irn(grid, geom, KIND_PICCS, b, 0.9 * truth, p)
     x_pl, _ = ora.irn(grid, geom, KIND_PIPLE, b, 0.9 * truth, p)
     assert np.array_equal(x_tv, x_pc) and np.array_equal(x_tv, x_pl)
+
+
+def test_uniform_volume_row_sums_are_box_chords():
+    """A 1 = the ray's chord through the volume box (test_projector.cpp:54-69):
+    the oracle's Siddon sums against the closed-form slab clip used by the
+    full-size GPU property test (tests/test_fullsize_gpu.py)."""
+    from tests._util import baseline_geometry, tiny_geometry, tiny_grid
+    from oracle import build
+    from tests.test_fullsize_gpu import box_chords
+    build("ora")
+    ora = Oracle("ora")
+    for grid, geom in [(tiny_grid(6, 5, 7), tiny_geometry(5, 8, 9)), baseline_geometry(1, 3)]:
+        want = ora.forward(grid, geom, np.ones(grid.count))
+        got = box_chords(grid, geom)
+        assert np.abs(got - want).max() < 1e-10
