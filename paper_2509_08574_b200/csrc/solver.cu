@@ -576,6 +576,234 @@ __global__ void __launch_bounds__(kBlock, 2) k_reggrad4t(
     write_partials(part, 2, t2, red);
 }
 
+// ---- k_reggrad4m: the same stencil on a y-marching TMA ring ---------------
+// k_reggrad4t reloads every tile's halo (72 x 10 x 4 floats for 64 x 8 x 2
+// voxels: 2.8x the voxels in L2 -> shared traffic, and the 16-byte z halos
+// cost a whole DRAM sector each: 446 MB read per launch for 335 MB of
+// operands).  Here a CTA owns a contiguous range of the flattened (column
+// tile, y) rows — a column tile is the WHOLE z extent (up to 256 slabs; no z
+// halo at all, the volume faces are the stencil's own boundary rules) x mx
+// x-columns — and marches along y: every step loads ONE row plane (zbox x
+// (mx + 2) floats per tensor, one cp.async.bulk.tensor.3d box {zbox, mx + 2,
+// 1} each) into a ring of kMR slots and computes the row whose three planes
+// (y - 1, y, y + 1) are resident, so a plane is loaded once per CTA and the
+// halo costs (mx + 2) / mx in x plus two planes per run.  kMR - 3 planes are
+// in flight ahead of the one being waited for.  kMarch CTAs (one per SM, 512
+// threads) carry the work; the other blocks of the fixed partial-sum grid
+// write zero partials.  Per voxel the arithmetic of k_reggrad4 (dtwd);
+// partial sums in (row, thread, quad) order.
+constexpr int kMR = 5;           // ring slots
+constexpr int kMarch = 148;      // CTAs that carry work (fixed: deterministic sums)
+constexpr int kMBlock = 512;     // threads per march CTA
+constexpr int kMZ = 248;         // z tile when nz > 256 (box = tile + 8 <= 256)
+constexpr int kMPlaneMax = 2560; // floats per tensor row plane (10 KB)
+static_assert(kMarch <= kGrid, "march CTAs within the partial-sum grid");
+
+struct MarchCfg {
+    int zt;     // z extent of a column tile (multiple of 4)
+    int zbox;   // TMA box z extent (zt + 2 zo)
+    int zo;     // z halo on each side (0: the tile is the whole z extent)
+    int nzq;    // z quads per tile
+    int mx;     // x columns per tile
+    int ntz, ntx;
+    int plane;  // floats per tensor row plane in shared memory (128-byte multiple)
+};
+
+inline MarchCfg march_cfg(const RegCfg& c) {
+    MarchCfg m{};
+    if (c.nz <= 256) {
+        m.ntz = 1;
+        m.zt = c.nz;
+        m.zo = 0;
+    } else {
+        m.ntz = (c.nz + kMZ - 1) / kMZ;
+        m.zt = (((c.nz + m.ntz - 1) / m.ntz) + 3) & ~3;
+        m.zo = 4;
+    }
+    m.zbox = m.zt + 2 * m.zo;
+    m.nzq = m.zt / 4;
+    m.mx = std::max(1, std::min({kMBlock / m.nzq, kMPlaneMax / m.zbox - 2, 254}));
+    m.ntx = (c.nx + m.mx - 1) / m.mx;
+    m.plane = (m.zbox * (m.mx + 2) + 31) & ~31;
+    return m;
+}
+
+// Walks the row planes a CTA loads, run by run: the CTA's rows [g0, g1) of
+// the flattened (column tile, y) space split into runs inside one column
+// tile; a run [ja, jb) loads planes ja - 1 .. jb.
+struct MarchRuns {
+    long g, g1;   // next unvisited flattened row / end of the CTA's range
+    int ny;
+    int col, j, jb;  // current run: column tile, next plane, last plane (inclusive)
+    bool done;
+    __device__ void init(long g0, long g1_, int ny_) {
+        g = g0; g1 = g1_; ny = ny_;
+        done = g0 >= g1_;
+        if (!done) start();
+    }
+    __device__ void start() {
+        col = (int)(g / ny);
+        const int ja = (int)(g - (long)col * ny);
+        const long left = g1 - g;
+        jb = (int)(left < (long)(ny - ja) ? ja + left : ny);
+        j = ja - 1;
+        g += jb - ja;
+    }
+    // advance past plane j of the current run
+    __device__ void next() {
+        if (++j > jb) {
+            if (g >= g1) done = true;
+            else start();
+        }
+    }
+};
+
+__global__ void __launch_bounds__(kMBlock, 1) k_reggrad4m(
+    const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_xp,
+    const __grid_constant__ CUtensorMap tm_w1, const __grid_constant__ CUtensorMap tm_w2,
+    const float* __restrict__ sA, float* __restrict__ s, RegCfg c, MarchCfg mc, int yoff,
+    double* part) {
+    extern __shared__ __align__(1024) float tsm[];  // [kMR][4][mc.plane]
+    __shared__ __align__(8) unsigned long long mbar_s[kMR];
+    __shared__ double red[32];
+    double ts = 0.0, t1 = 0.0, t2 = 0.0;
+    if (blockIdx.x < kMarch) {
+        const bool w1on = c.use_w1, m2 = c.mode2 == 1, m3 = c.mode2 == 2;
+        const int ntz = mc.ntz, P = mc.plane, ZB = mc.zbox;
+        const long total = (long)ntz * mc.ntx * c.ny;
+        const long g0 = total * blockIdx.x / kMarch, g1 = total * (blockIdx.x + 1) / kMarch;
+        if (threadIdx.x == 0) {
+            for (int st = 0; st < kMR; ++st)
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                                 (unsigned)__cvta_generic_to_shared(&mbar_s[st]))
+                             : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        const unsigned bytes = (unsigned)(ZB * (mc.mx + 2) * sizeof(float)) *  // the boxes, not the padded planes
+                               ((w1on || m2 || m3 ? 1u : 0u) + (m2 || m3 ? 1u : 0u) +
+                                (w1on ? 1u : 0u) + (m2 ? 1u : 0u));
+        MarchRuns ld;  // thread 0: the planes still to load
+        int issued = 0;
+        ld.init(g0, g1, c.ny);
+        auto issue = [&]() {
+            const int tz = ld.col % ntz, txi = ld.col / ntz;
+            float* const T = tsm + (size_t)(issued % kMR) * 4 * P;
+            const unsigned mbar = (unsigned)__cvta_generic_to_shared(&mbar_s[issued % kMR]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes)
+                         : "memory");
+            const int z = tz * mc.zt - mc.zo, x = txi * mc.mx - 1, y = ld.j + yoff;
+            if (w1on || m2 || m3) tma_load3(T, &tm_x, z, x, y, mbar);
+            if (m2 || m3) tma_load3(T + P, &tm_xp, z, x, y, mbar);
+            if (w1on) tma_load3(T + 2 * P, &tm_w1, z, x, y, mbar);
+            if (m2) tma_load3(T + 3 * P, &tm_w2, z, x, y, mbar);
+            ++issued;
+            ld.next();
+        };
+        auto wait = [&](int n) {
+            asm volatile(
+                "{\n\t.reg .pred done;\n"
+                "MARCHWAIT_%=:\n\t"
+                "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1;\n\t"
+                "@!done bra MARCHWAIT_%=;\n\t}" ::"r"((unsigned)__cvta_generic_to_shared(&mbar_s[n % kMR])),
+                "r"((unsigned)((n / kMR) & 1))
+                : "memory");
+        };
+        if (threadIdx.x == 0)
+            while (issued < kMR && !ld.done) issue();
+        const int qz = threadIdx.x % mc.nzq, tx = threadIdx.x / mc.nzq;
+        const bool mine = tx < mc.mx;
+        const int o = (tx + 1) * ZB + mc.zo + 4 * qz;
+        const size_t si = c.nz;
+        MarchRuns cr;  // all threads: the runs being computed
+        cr.init(g0, g1, c.ny);
+        int n = 0;  // load index of the current run's first plane (ja - 1)
+        while (!cr.done) {
+            const int col = cr.col, ja = cr.j + 1, jb = cr.jb;
+            const int tz = col % ntz, txi = col / ntz;
+            const int k = tz * mc.zt + 4 * qz, i = txi * mc.mx + tx;
+            const bool ok = mine && k < c.nz && k < (tz + 1) * mc.zt && i < c.nx;
+            const bool hasip = i + 1 < c.nx, hasim = i > 0;
+            wait(n);
+            wait(n + 1);
+            for (int j = ja; j < jb; ++j) {
+                const int nn = n + 2 + (j - ja);  // load index of plane j + 1
+                wait(nn);
+                if (ok) {
+                    const float* const Tm = tsm + (size_t)((nn - 2) % kMR) * 4 * P;
+                    const float* const Tc = tsm + (size_t)((nn - 1) % kMR) * 4 * P;
+                    const float* const Tp = tsm + (size_t)(nn % kMR) * 4 * P;
+                    const size_t v = (size_t)k + si * ((size_t)i + (size_t)c.nx * j);
+                    const float4 a = __ldg(reinterpret_cast<const float4*>(sA + v));
+                    float sv[4] = {a.x, a.y, a.z, a.w};
+                    const int jg = j + c.j0;
+                    const bool hasjp = jg + 1 < c.nyg, hasjm = jg > 0;
+                    auto ld4s = [&](const float* T, int off) { return *reinterpret_cast<const float4*>(T + off); };
+                    float g[4], gg[4];
+                    if (w1on) {
+                        const float* const T1 = Tc + 2 * P;
+                        Q4 X, W;
+                        X.c = ld4s(Tc, o);
+                        X.km = Tc[o - 1];
+                        X.kp = Tc[o + 4];
+                        W.c = ld4s(T1, o);
+                        W.km = T1[o - 1];
+                        dtwd_m(X, ld4s(Tc, o + ZB), ld4s(Tc, o - ZB), ld4s(Tp, o), ld4s(Tm, o), W,
+                               ld4s(T1, o - ZB), ld4s(Tm + 2 * P, o), k, hasip, hasim, hasjp, hasjm,
+                               c.nz, g, gg);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            sv[q] -= c.alpha2 * g[q];
+                            t1 += (double)gg[q];
+                        }
+                    }
+                    if (m2) {
+                        const float* const T2 = Tc + 3 * P;
+                        auto d4 = [&](const float* T, int off) { return sub4(ld4s(T, off), ld4s(T + P, off)); };
+                        Q4 D, W;
+                        D.c = d4(Tc, o);
+                        D.km = Tc[o - 1] - Tc[P + o - 1];
+                        D.kp = Tc[o + 4] - Tc[P + o + 4];
+                        W.c = ld4s(T2, o);
+                        W.km = T2[o - 1];
+                        dtwd_m(D, d4(Tc, o + ZB), d4(Tc, o - ZB), d4(Tp, o), d4(Tm, o), W,
+                               ld4s(T2, o - ZB), ld4s(Tm + 3 * P, o), k, hasip, hasim, hasjp, hasjm,
+                               c.nz, g, gg);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            sv[q] -= c.lambda2 * g[q];
+                            t2 += (double)gg[q];
+                        }
+                    } else if (m3) {
+                        const float4 xv = ld4s(Tc, o), pv = ld4s(Tc + P, o);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const float dv = q4(xv, q) - q4(pv, q);
+                            sv[q] -= c.lambda2 * dv;
+                            t2 += (double)dv * (double)dv;
+                        }
+                    }
+                    *reinterpret_cast<float4*>(s + v) = make_float4(sv[0], sv[1], sv[2], sv[3]);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) ts += (double)sv[q] * (double)sv[q];
+                }
+                __syncthreads();  // plane j - 1's slot is free
+                // planes up to (next needed) + kMR - 3 may be in flight
+                const int next_needed = j + 1 < jb ? nn + 1 : nn + 3;
+                if (threadIdx.x == 0)
+                    while (issued < next_needed + kMR - 2 && !ld.done) issue();
+            }
+            n += jb - ja + 2;
+            cr.j = cr.jb;  // the run is consumed
+            cr.next();
+        }
+    }
+    write_partials(part, 0, ts, red);
+    write_partials(part, 1, t1, red);
+    write_partials(part, 2, t2, red);
+}
+
 // ---- k_weights4 / k_normq4 on TMA tiles ---------------------------------
 // The same tiles and two-stage pipeline as k_reggrad4t for the forward-
 // difference stencils: k_weights4t reads tiles of x and x_p (TV weights,
@@ -1208,14 +1436,15 @@ EncodeTiledFn encode_tiled() {
 
 // 3D tensor map of a native-layout volume vector (z, x, y[+ halo planes]) with
 // the k_reggrad4t box
-bool volume_tmap(CUtensorMap& tm, const float* v, const RegCfg& rc, size_t halo) {
+bool volume_tmap(CUtensorMap& tm, const float* v, const RegCfg& rc, size_t halo, int bz = kBZ,
+                 int bx = kBX, int by = kBY) {
     const EncodeTiledFn enc = encode_tiled();
     if (!enc) return false;
     const int hy = halo ? 1 : 0;
     const cuuint64_t dims[3] = {(cuuint64_t)rc.nz, (cuuint64_t)rc.nx, (cuuint64_t)(rc.ny + 2 * hy)};
     const cuuint64_t strides[2] = {(cuuint64_t)rc.nz * sizeof(float),
                                    (cuuint64_t)rc.nz * rc.nx * sizeof(float)};
-    const cuuint32_t box[3] = {(cuuint32_t)kBZ, (cuuint32_t)kBX, (cuuint32_t)kBY};
+    const cuuint32_t box[3] = {(cuuint32_t)bz, (cuuint32_t)bx, (cuuint32_t)by};
     const cuuint32_t estr[3] = {1, 1, 1};
     return enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(v - halo), dims, strides,
                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1376,6 +1605,22 @@ struct Engine {
         const float* xp = w.prior ? w.prior : xv;
         const float* w1 = w.w1 ? w.w1 : xv;
         const float* w2 = w.w2 ? w.w2 : xv;
+        // KCT_TMA_MARCH=1: the y-marching ring (measured at c3: same time as the
+        // tiles, 108.9 vs 107.3 us, with 412 instead of 446 MB of DRAM reads —
+        // both kernels are issue-bound, not traffic-bound)
+        const char* me = std::getenv("KCT_TMA_MARCH");
+        const MarchCfg mc = march_cfg(rc);
+        if (me && me[0] == '1' && volume_tmap(tx, xv, rc, w.halo, mc.zbox, mc.mx + 2, 1) &&
+            volume_tmap(tp, xp, rc, w.halo, mc.zbox, mc.mx + 2, 1) &&
+            volume_tmap(t1, w1, rc, w.halo, mc.zbox, mc.mx + 2, 1) &&
+            volume_tmap(t2, w2, rc, w.halo, mc.zbox, mc.mx + 2, 1)) {
+            const int smem = kMR * 4 * mc.plane * (int)sizeof(float);
+            KCT_CUDA(cudaFuncSetAttribute(k_reggrad4m, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            k_reggrad4m<<<kGrid, kMBlock, smem, stream>>>(tx, tp, t1, t2, in, out, rc, mc, w.halo ? 1 : 0,
+                                                         w.part);
+            KCT_LAUNCHED();
+            return true;
+        }
         if (!volume_tmap(tx, xv, rc, w.halo) || !volume_tmap(tp, xp, rc, w.halo) ||
             !volume_tmap(t1, w1, rc, w.halo) || !volume_tmap(t2, w2, rc, w.halo))
             return false;

@@ -229,6 +229,41 @@ def test_float4_and_scalar_stencils_agree(monkeypatch, fn):
         np.testing.assert_allclose(vec.residual_history, other.residual_history, rtol=1e-6)
 
 
+@pytest.mark.parametrize("fn", ["irn_tv", "irn_piple", "irn_piccs"])
+@pytest.mark.parametrize("dims", [(40, 36, 72), (16, 5, 64), (50, 130, 132)])
+def test_march_tile_and_grid_stride_stencils_agree(monkeypatch, fn, dims):
+    """k_reggrad4m (y-marching TMA ring), k_reggrad4t (TMA tiles) and the
+    grid-stride float4 kernel on grids that are no multiple of any tile (partial
+    z / x tiles, short and long y runs, CTA ranges spanning several column
+    tiles): same regulariser terms up to the partial-sum order."""
+    from oracle import Geometry, Grid, uniform_angles
+    grid = Grid(*dims, 1.0, 1.0, 1.0)
+    geom = Geometry(600.0, 900.0, 48, 56, 2.5, 2.5, uniform_angles(6))
+    gs, ge = to_pkg(grid, geom)
+    A = k.ConeBeamProjector(gs, ge)
+    rng = np.random.default_rng(5)
+    x = rng.uniform(0, 0.04, grid.count).astype(np.float32)
+    prior = (x * rng.uniform(0.9, 1.1, grid.count)).astype(np.float32)
+    proj = k.ProjectionSet(ge, A.apply(x))
+    params = k.RegularizationParams(alpha=0.2, tau=1e-3, outer_iters=2, inner_iters=3)
+
+    def run():
+        if fn == "irn_tv":
+            return k.irn_tv(proj, gs, params, projector=A)
+        return getattr(k, fn)(proj, gs, prior, params, projector=A)
+
+    monkeypatch.setenv("KCT_TMA_MARCH", "1")
+    march = run()
+    monkeypatch.delenv("KCT_TMA_MARCH")
+    tiles = run()
+    monkeypatch.setenv("KCT_TMA_STENCIL", "0")
+    plain = run()
+    for other in (tiles, plain):
+        assert rel_l2(march.volume, other.volume) < 1e-5
+        np.testing.assert_allclose(march.objective_history, other.objective_history, rtol=1e-6)
+        np.testing.assert_allclose(march.residual_history, other.residual_history, rtol=1e-6)
+
+
 # ---- ReconOptions.hook / wall_times / the reference's restart control flow ----
 def test_hook_sees_every_iterate_in_order(small):
     """krylov.hpp:116 / recon.hpp:223-228 (test_krylov.cpp:120-135): the hook is
