@@ -395,7 +395,7 @@ def run_ours(args):
                                              "adj_weight_kernel + adj_brick_kernel")
                                  + " (+ adj_group_sum when angle groups > 1)"},
            # which code paths the handles run (kct_projector_info)
-           "paths": {key: A_b.info(key) for key in ("adj_slab", "adj_mirror", "adj_ws", "adj_bz",
+           "paths": {key: A_b.info(key) for key in ("adj_slab", "adj_mirror", "adj_ws", "adj_np", "adj_bz",
                                                       "adj_groups", "adj_walk_entries")}
            | {key: A_f.info(key) for key in ("fwd_rows_per_warp", "fwd_bands", "fwd_split_z")}}
 

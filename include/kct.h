@@ -148,7 +148,8 @@ int kct_adjoint_f64(kct_projector* h, const double* proj, double* vol);
 int kct_count_nnz(kct_projector* h, uint64_t* nnz, void* stream);
 /* Which code paths this handle runs (no reference counterpart; evidence for
  * tests and benchmarks).  key: "adj_slab" (1: slab-lane adjoint deposits),
- * "adj_slab_detect", "adj_bz" (brick height), "adj_stride" (row-wise pass
+ * "adj_slab_detect", "adj_bz" (brick height), "adj_np" (producer warps per consumer of the
+ * warp-specialised adjoint, 0: another kernel), "adj_stride" (row-wise pass
  * stride S), "adj_groups" (angle groups), "adj_gather", "adj_walk_entries",
  * "fwd_rows_per_warp", "fwd_bands", "fwd_split_z" / "fwd_split_lo" (host
  * forward split upload: slabs [lo, z) first, z = 0: off), "mirror" (1: z-mirror

@@ -410,6 +410,7 @@ int kct_projector_info(const kct_projector* h, const char* key, double* value) {
         else if (k == "adj_bz") *value = P.adj_mirror() ? P.adj_mirror_bz() : P.adj_bz();
         else if (k == "adj_mirror") *value = P.adj_mirror() ? 1 : 0;
         else if (k == "adj_ws") *value = P.adj_ws() ? 1 : 0;
+        else if (k == "adj_np") *value = P.adj_ws() ? P.adj_np() : 0;
         else if (k == "adj_stride") *value = P.adj_stride();
         else if (k == "adj_groups") *value = P.adj_groups();
         else if (k == "adj_gather") *value = P.adj_gather() ? 1 : 0;

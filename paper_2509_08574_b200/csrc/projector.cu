@@ -1209,6 +1209,9 @@ __device__ __forceinline__ void mir_classify(const float4* __restrict__ p,
 //   v + (wb - clamp(Xa.w)) Xa.y + (clamp(Xb.w) - wa) Xb.y + (wb - wa) H
 // (Xb = tX[j]: the row leaving slot j; Xa = tX[j + 1]: the row entering it).
 // Clears the tables.
+#ifndef KCT_MIR_UNROLL
+#define KCT_MIR_UNROLL 2  // c3 adjoint with 3 producers: 2.04 (1) / 1.96 (2) / 1.98 (3) / 2.20 ms (4)
+#endif
 template <int RC>
 __device__ __forceinline__ void mir_deposits(float4* acc, const float4* segs, int nseg, int NS,
                                              int lane, float2* tH, float4* tX, int xodd) {
@@ -1240,7 +1243,57 @@ __device__ __forceinline__ void mir_deposits(float4* acc, const float4* segs, in
             tX[xodd + lane + 32 * r] = z4;
         }
     if (lane == 0) tX[(NS & 1) * xodd + (NS >> 1)] = z4;
-    for (int sgi = 0; sgi < nseg; ++sgi) {
+    int sgi = 0;
+#if KCT_MIR_UNROLL > 1
+    // KCT_MIR_UNROLL segments per step: an entry's segments lie in distinct
+    // voxel columns (the xy walk never revisits one), so the later segments'
+    // accumulator loads need not wait for the earlier ones' stores
+    constexpr int U = KCT_MIR_UNROLL;
+    for (; sgi + U <= nseg; sgi += U) {
+        float4 sg[U];
+        float4* a[U];
+        float4 v[U][RC];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            sg[u] = segs[sgi + u];
+            a[u] = acc + (__float_as_int(sg[u].z) + lane);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int r = 0; r < RC; ++r) v[u][r] = on[r] ? a[u][32 * r] : z4;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const float wa = sg[u].x, wb = sg[u].y;
+            const float d = wb - wa;
+#pragma unroll
+            for (int r = 0; r < RC; ++r) {
+                float4& w = v[u][r];
+                if (xs[r]) {
+                    const float cA = fminf(fmaxf(xA[r].x, wa), wb);
+                    const float cB = fminf(fmaxf(xB[r].x, wa), wb);
+                    const float cC = fminf(fmaxf(xC[r].x, wa), wb);
+                    const float tbA = cA - wa, taA = wb - cB, tbB = cB - wa, taB = wb - cC;
+                    w.x = __fmaf_rn(d, h[r].x, __fmaf_rn(tbA, xA[r].y, __fmaf_rn(taA, xB[r].y, w.x)));
+                    w.y = __fmaf_rn(d, h[r].y, __fmaf_rn(tbA, xA[r].z, __fmaf_rn(taA, xB[r].z, w.y)));
+                    w.z = __fmaf_rn(d, h[r].z, __fmaf_rn(tbB, xB[r].y, __fmaf_rn(taB, xC[r].y, w.z)));
+                    w.w = __fmaf_rn(d, h[r].w, __fmaf_rn(tbB, xB[r].z, __fmaf_rn(taB, xC[r].z, w.w)));
+                } else {
+                    w.x = __fmaf_rn(d, h[r].x, w.x);
+                    w.y = __fmaf_rn(d, h[r].y, w.y);
+                    w.z = __fmaf_rn(d, h[r].z, w.z);
+                    w.w = __fmaf_rn(d, h[r].w, w.w);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int r = 0; r < RC; ++r)
+                if (on[r]) a[u][32 * r] = v[u][r];
+    }
+#endif
+    for (; sgi < nseg; ++sgi) {
         const float4 sg = segs[sgi];
         const float wa = sg.x, wb = sg.y;
         float4* const a = acc + (__float_as_int(sg.z) + lane);
@@ -1555,9 +1608,6 @@ __host__ __device__ constexpr int adj_mir_ws_floats(int bz, int np) {
     return 2 * BX * BY * ((bz + 1) & ~1) + 2 * np * mir_buf_floats((bz + 1) & ~1) + 4 + 8 * np;
 }
 
-#ifndef KCT_MIR_NP
-#define KCT_MIR_NP 2  // producer warps (decode + classification)
-#endif
 #ifndef KCT_MIR_NC
 #define KCT_MIR_NC 1  // consumer warps (deposits; 2 / 3 measured slower: 2.51 / 3.14 ms at c3)
 #endif
@@ -1747,6 +1797,18 @@ __global__ void __launch_bounds__(32 * (NP + NC), 32 / (NP + NC)) adj_mirror_ws_
         }
         gcount += (unsigned)(e1 - e0);
     }
+}
+
+// The warp-specialised kernel by (brick height, producer warps): handles pick
+// 2 or 3 producers per consumer at creation (Projector::tune_adjoint).
+using AdjWsFn = void (*)(const float4*, const float*, float*, DevGeom, BrickCfg, int, int, int,
+                         const int*, int*, float*, const WalkEntry*, const unsigned long long*);
+static AdjWsFn adj_ws_fn(int bz, int np) {
+    if (np == 3)
+        return bz == 64 ? adj_mirror_ws_kernel<64, 3, KCT_MIR_NC>
+               : bz == 32 ? adj_mirror_ws_kernel<32, 3, KCT_MIR_NC> : adj_mirror_ws_kernel<0, 3, KCT_MIR_NC>;
+    return bz == 64 ? adj_mirror_ws_kernel<64, 2, KCT_MIR_NC>
+           : bz == 32 ? adj_mirror_ws_kernel<32, 2, KCT_MIR_NC> : adj_mirror_ws_kernel<0, 2, KCT_MIR_NC>;
 }
 
 // ----------------------------------------------------------------------------
@@ -2357,10 +2419,10 @@ void Projector::build_tables(const kct_geometry& geom) {
     for (auto fn : {adj_mirror_kernel<0>, adj_mirror_kernel<32>, adj_mirror_kernel<64>})
         KCT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(adj_mir_floats(kMirMaxBz) * sizeof(float))));
-    for (auto fn : {adj_mirror_ws_kernel<0, KCT_MIR_NP, KCT_MIR_NC>, adj_mirror_ws_kernel<32, KCT_MIR_NP, KCT_MIR_NC>,
-                    adj_mirror_ws_kernel<64, KCT_MIR_NP, KCT_MIR_NC>})
-        KCT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(adj_mir_ws_floats(kMirMaxBz, KCT_MIR_NP) * sizeof(float))));
+    for (int np : {2, 3})
+        for (int bz : {0, 32, 64})
+            KCT_CUDA(cudaFuncSetAttribute(adj_ws_fn(bz, np), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(adj_mir_ws_floats(kMirMaxBz, np) * sizeof(float))));
 
     // z-mirror brick pairs (adj_mirror_kernel): z-mirror geometry, slab-lane
     // conditions, nz even; bricks of <= 64 slabs tiling the lower half
@@ -2454,18 +2516,24 @@ void Projector::build_tables(const kct_geometry& geom) {
         const char* ws = std::getenv("KCT_ADJ_WS");
         adj_ws_ = adj_mir_ && !(ws && ws[0] == '0');
         int per_sm = 0, sms = 0;
-        if (adj_ws_)
-            KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &per_sm, adj_mirror_ws_kernel<0, KCT_MIR_NP, KCT_MIR_NC>, 32 * (KCT_MIR_NP + KCT_MIR_NC), adj_smem_bytes()));
-        else if (adj_mir_)
+        KCT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+        if (adj_ws_) {
+            for (int np : {2, 3}) {
+                KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                    &per_sm, adj_ws_fn(0, np), 32 * (np + KCT_MIR_NC),
+                    (size_t)adj_mir_ws_floats(adj_mbz_, np) * sizeof(float)));
+                adj_ctas_np_[np - 2] = std::max(1, per_sm) * std::max(1, sms);
+            }
+            per_sm = adj_ctas_np_[adj_np_ - 2] / std::max(1, sms);
+        } else if (adj_mir_)
             KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_mirror_kernel<0>, 32,
                                                                    adj_smem_bytes()));
         else
             KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_brick_kernel<true>,
                                                                    kAdjWarps * 32, adj_smem_bytes()));
-        KCT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
         adj_ctas_ = std::max(1, per_sm) * std::max(1, sms);
     }
+    tune_adjoint();
 }
 
 // Brick configuration of the adjoint (and of its walk table): standard
@@ -2579,7 +2647,7 @@ void Projector::build_fwd_table() {
 }
 
 size_t Projector::adj_smem_bytes() const {
-    if (adj_ws_) return (size_t)adj_mir_ws_floats(adj_mbz_, KCT_MIR_NP) * sizeof(float);
+    if (adj_ws_) return (size_t)adj_mir_ws_floats(adj_mbz_, adj_np_) * sizeof(float);
     if (adj_mir_) return (size_t)adj_mir_floats(adj_mbz_) * sizeof(float);
     return (size_t)kAdjWarps * adj_warp_floats(adj_bz_) * sizeof(float);
 }
@@ -2910,11 +2978,11 @@ void Projector::adjoint_impl(const float* proj, float* vol, int a_begin, int a_e
             }
         } else {
             if (d_queue_) KCT_CUDA(cudaMemsetAsync(d_queue_, 0, sizeof(int), s));
-            const unsigned grid = d_queue_ ? std::min(nctas, adj_ctas_) : nctas;
+            const unsigned grid = d_queue_ ? std::min(nctas, adj_ws_ ? adj_ctas_np_[adj_np_ - 2] : adj_ctas_)
+                                           : nctas;
             if (adj_ws_)
-                (bc.bz == 64 ? adj_mirror_ws_kernel<64, KCT_MIR_NP, KCT_MIR_NC>
-                 : bc.bz == 32 ? adj_mirror_ws_kernel<32, KCT_MIR_NP, KCT_MIR_NC> : adj_mirror_ws_kernel<0, KCT_MIR_NP, KCT_MIR_NC>)
-                    <<<grid, 32 * (KCT_MIR_NP + KCT_MIR_NC), smem, s>>>(
+                adj_ws_fn(bc.bz == 64 || bc.bz == 32 ? bc.bz : 0, adj_np_)
+                    <<<grid, 32 * (adj_np_ + KCT_MIR_NC), smem, s>>>(
                     yrec, ymw, vol, dg_, bc, a0, nab, accum, border,
                     d_queue_, d_part_, static_cast<const WalkEntry*>(d_tab_), d_off_);
             else if (adj_mir_)
@@ -2937,6 +3005,56 @@ void Projector::adjoint_impl(const float* proj, float* vol, int a_begin, int a_e
         }
         KCT_LAUNCHED();
     }
+}
+
+// Producer warps per consumer of the warp-specialised adjoint: 2 or 3,
+// whichever runs this handle's geometry faster (c3: 3 producers 1.96 vs 2.02
+// ms, c4: 2 producers 13.2 vs 13.9 ms, c2: 2).  Timed once at creation on the
+// first <= 24 angles with non-zero readings (both variants are bit-identical,
+// so a noisy choice changes time, never results).  KCT_ADJ_NP=2|3 forces the
+// choice, KCT_ADJ_TUNE=0 keeps 2.
+void Projector::tune_adjoint() {
+    if (!adj_ws_ || !d_queue_) return;
+    if (const char* e = std::getenv("KCT_ADJ_NP")) {
+        adj_np_ = std::atoi(e) == 3 ? 3 : 2;
+        return;
+    }
+    const char* te = std::getenv("KCT_ADJ_TUNE");
+    if (te && te[0] == '0') return;
+    const int na_t = std::min(dg_.na, 24);
+    const size_t n_t = (size_t)na_t * dg_.nu * dg_.nv;
+    if ((double)n_t * dg_.nz < 2e8) return;  // small problems: launch-bound either way
+    float *y = nullptr, *v = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (cudaMalloc(&y, n_t * sizeof(float)) != cudaSuccess || cudaMalloc(&v, m_ * sizeof(float)) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(y);
+        return;  // no room to tune: keep the default
+    }
+    KCT_CUDA(cudaMemset(y, 0x3c, n_t * sizeof(float)));  // 0x3c3c3c3c = 0.0115f everywhere
+    KCT_CUDA(cudaEventCreate(&e0));
+    KCT_CUDA(cudaEventCreate(&e1));
+    float best = 0.f;
+    int best_np = adj_np_;
+    for (int np : {2, 3}) {
+        adj_np_ = np;
+        adjoint_impl(y, v, 0, na_t, false, false, nullptr, nullptr);  // warm (table in L2 / TLB)
+        KCT_CUDA(cudaEventRecord(e0, nullptr));
+        for (int r = 0; r < 2; ++r) adjoint_impl(y, v, 0, na_t, false, false, nullptr, nullptr);
+        KCT_CUDA(cudaEventRecord(e1, nullptr));
+        KCT_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        KCT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        if (np == 2 || ms < 0.99f * best) {  // 3 producers must win by 1%
+            best = ms;
+            best_np = np;
+        }
+    }
+    adj_np_ = best_np;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(y);
+    cudaFree(v);
 }
 
 // cuStreamWaitValue32 (driver API, MemOp v2: supported by default since CUDA

@@ -128,6 +128,7 @@ class Projector {
     bool adj_slab_detect() const { return adj_slab_detect_; }
     bool adj_mirror() const { return adj_mir_; }
     bool adj_ws() const { return adj_ws_; }
+    int adj_np() const { return adj_np_; }
     int adj_mirror_bz() const { return adj_mbz_; }
     int adj_groups() const { return adj_groups_; }
     unsigned long long walk_entries() const { return tab_entries_; }
@@ -138,6 +139,7 @@ class Projector {
     size_t adj_smem_bytes() const;
     BrickCfg adj_cfg() const;
     void build_walk_table();
+    void tune_adjoint();
     void build_fwd_table();
     FwdTab ftab(int a) const;
     void adjoint_impl(const float* proj, float* vol, int a_begin, int a_end, bool accumulate,
@@ -189,6 +191,8 @@ class Projector {
     unsigned* d_fdone_ = nullptr;     // finished columns per pipeline chunk
     int* d_queue_ = nullptr;          // adjoint brick queue counter
     int adj_ctas_ = 0;                // resident CTAs of the persistent adjoint grid
+    int adj_ctas_np_[2] = {0, 0};     // ... of the warp-specialised kernel with 2 / 3 producers
+    int adj_np_ = 2;                  // producer warps per consumer (tune_adjoint)
     int adj_groups_ = 1;              // angle groups of the adjoint (small problems)
     float* d_part_ = nullptr;         // (adj_groups_ - 1) partial volumes
     float* d_yw_ = nullptr;           // adjoint per-ray records (float4, one angle batch)

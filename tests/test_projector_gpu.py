@@ -7,6 +7,7 @@ uniform-volume chords, bit-identical reruns, size checks) on the CUDA path.
 """
 import numpy as np
 import pytest
+import torch
 
 import paper_2509_08574_b200 as k
 from oracle import Oracle
@@ -556,9 +557,21 @@ def test_warp_specialised_pairs_bitwise(monkeypatch, cfg, n_angles):
     A = projector(grid, geom)
     assert A.info("adj_mirror") == 1 and A.info("adj_ws") == 1
     ws = A.apply_adjoint(y)
+    # 2 or 3 producer warps per consumer (picked by timing at creation;
+    # forced here): the same entries in the same order, bit-identical
+    assert A.info("adj_np") in (2, 3)
+    for np_forced in ("2", "3"):
+        monkeypatch.setenv("KCT_ADJ_NP", np_forced)
+        C = projector(grid, geom)
+        assert C.info("adj_np") == int(np_forced)
+        assert np.array_equal(ws, C.apply_adjoint(y))
+        x_dev = C.apply_adjoint(torch.from_numpy(C.proj_to_native(y) if False else y).cuda(),
+                                layout="reference")
+        assert np.array_equal(ws, x_dev.cpu().numpy())
+    monkeypatch.delenv("KCT_ADJ_NP")
     monkeypatch.setenv("KCT_ADJ_WS", "0")
     B = projector(grid, geom)
-    assert B.info("adj_ws") == 0
+    assert B.info("adj_ws") == 0 and B.info("adj_np") == 0
     assert np.array_equal(ws, B.apply_adjoint(y))
 
 
