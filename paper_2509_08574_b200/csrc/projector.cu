@@ -1209,10 +1209,14 @@ __device__ __forceinline__ void mir_classify(const float4* __restrict__ p,
 //   v + (wb - clamp(Xa.w)) Xa.y + (clamp(Xb.w) - wa) Xb.y + (wb - wa) H
 // (Xb = tX[j]: the row leaving slot j; Xa = tX[j + 1]: the row entering it).
 // Clears the tables.
+#ifndef KCT_MIR_PCLEAR
+#define KCT_MIR_PCLEAR 0  // 1: the producers clear a table buffer before refilling it (measured slower:
+                          // c3 1.96 -> 2.02 ms, c4 13.2 -> 13.8 ms; the consumer clears only the live slots)
+#endif
 #ifndef KCT_MIR_UNROLL
 #define KCT_MIR_UNROLL 2  // c3 adjoint with 3 producers: 2.04 (1) / 1.96 (2) / 1.98 (3) / 2.20 ms (4)
 #endif
-template <int RC>
+template <int RC, bool CLR = true>
 __device__ __forceinline__ void mir_deposits(float4* acc, const float4* segs, int nseg, int NS,
                                              int lane, float2* tH, float4* tX, int xodd) {
     float4 h[RC], xA[RC], xB[RC], xC[RC];
@@ -1234,15 +1238,17 @@ __device__ __forceinline__ void mir_deposits(float4* acc, const float4* segs, in
                                       xB[r].z != 0.f || xC[r].y != 0.f || xC[r].z != 0.f);
     }
     // clear the tables (after every lane's reads: slot j + 2 is the next lane's)
-    __syncwarp();
+    if (CLR) {
+        __syncwarp();
 #pragma unroll
-    for (int r = 0; r < RC; ++r)
-        if (on[r]) {
-            tH4[lane + 32 * r] = z4;
-            tX[lane + 32 * r] = z4;
-            tX[xodd + lane + 32 * r] = z4;
-        }
-    if (lane == 0) tX[(NS & 1) * xodd + (NS >> 1)] = z4;
+        for (int r = 0; r < RC; ++r)
+            if (on[r]) {
+                tH4[lane + 32 * r] = z4;
+                tX[lane + 32 * r] = z4;
+                tX[xodd + lane + 32 * r] = z4;
+            }
+        if (lane == 0) tX[(NS & 1) * xodd + (NS >> 1)] = z4;
+    }
     int sgi = 0;
 #if KCT_MIR_UNROLL > 1
     // KCT_MIR_UNROLL segments per step: an entry's segments lie in distinct
@@ -1702,7 +1708,7 @@ __global__ void __launch_bounds__(32 * (NP + NC), 32 / (NP + NC)) adj_mirror_ws_
                 // the consumer is done with b (its use gi / NB - 1)
                 if (gi >= (unsigned)NB) {
                     mbar_wait(empty_of(b), (gi / NB - 1u) & 1u);
-                    if (NC > 1) mir_clear(tH_of(b), tX_of(b), CS, lane);
+                    if (NC > 1 || KCT_MIR_PCLEAR) mir_clear(tH_of(b), tX_of(b), CS, lane);
                 }
                 float4* const segs = segs_of(b);
                 const unsigned ijw1 = __shfl_sync(kFull, w, M - 1);
@@ -1750,9 +1756,9 @@ __global__ void __launch_bounds__(32 * (NP + NC), 32 / (NP + NC)) adj_mirror_ws_
                         mir_deposits_nc<1>(sm4, segs_of(b), nseg, NS, lane, tH_of(b), tX_of(b), CS / 2 + 1, cw, NC);
                 } else {
                     if (CSC ? CSC > 64 : NS > 64)
-                        mir_deposits<2>(sm4, segs_of(b), nseg, NS, lane, tH_of(b), tX_of(b), CS / 2 + 1);
+                        mir_deposits<2, !KCT_MIR_PCLEAR>(sm4, segs_of(b), nseg, NS, lane, tH_of(b), tX_of(b), CS / 2 + 1);
                     else
-                        mir_deposits<1>(sm4, segs_of(b), nseg, NS, lane, tH_of(b), tX_of(b), CS / 2 + 1);
+                        mir_deposits<1, !KCT_MIR_PCLEAR>(sm4, segs_of(b), nseg, NS, lane, tH_of(b), tX_of(b), CS / 2 + 1);
                 }
                 mbar_arrive(empty_of(b));
             }
@@ -1804,6 +1810,9 @@ __global__ void __launch_bounds__(32 * (NP + NC), 32 / (NP + NC)) adj_mirror_ws_
 using AdjWsFn = void (*)(const float4*, const float*, float*, DevGeom, BrickCfg, int, int, int,
                          const int*, int*, float*, const WalkEntry*, const unsigned long long*);
 static AdjWsFn adj_ws_fn(int bz, int np) {
+    if (np == 1)
+        return bz == 64 ? adj_mirror_ws_kernel<64, 1, KCT_MIR_NC>
+               : bz == 32 ? adj_mirror_ws_kernel<32, 1, KCT_MIR_NC> : adj_mirror_ws_kernel<0, 1, KCT_MIR_NC>;
     if (np == 3)
         return bz == 64 ? adj_mirror_ws_kernel<64, 3, KCT_MIR_NC>
                : bz == 32 ? adj_mirror_ws_kernel<32, 3, KCT_MIR_NC> : adj_mirror_ws_kernel<0, 3, KCT_MIR_NC>;
@@ -2419,7 +2428,7 @@ void Projector::build_tables(const kct_geometry& geom) {
     for (auto fn : {adj_mirror_kernel<0>, adj_mirror_kernel<32>, adj_mirror_kernel<64>})
         KCT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(adj_mir_floats(kMirMaxBz) * sizeof(float))));
-    for (int np : {2, 3})
+    for (int np : {1, 2, 3})
         for (int bz : {0, 32, 64})
             KCT_CUDA(cudaFuncSetAttribute(adj_ws_fn(bz, np), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)(adj_mir_ws_floats(kMirMaxBz, np) * sizeof(float))));
@@ -2518,13 +2527,13 @@ void Projector::build_tables(const kct_geometry& geom) {
         int per_sm = 0, sms = 0;
         KCT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
         if (adj_ws_) {
-            for (int np : {2, 3}) {
+            for (int np : {1, 2, 3}) {
                 KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                     &per_sm, adj_ws_fn(0, np), 32 * (np + KCT_MIR_NC),
                     (size_t)adj_mir_ws_floats(adj_mbz_, np) * sizeof(float)));
-                adj_ctas_np_[np - 2] = std::max(1, per_sm) * std::max(1, sms);
+                adj_ctas_np_[np - 1] = std::max(1, per_sm) * std::max(1, sms);
             }
-            per_sm = adj_ctas_np_[adj_np_ - 2] / std::max(1, sms);
+            per_sm = adj_ctas_np_[adj_np_ - 1] / std::max(1, sms);
         } else if (adj_mir_)
             KCT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adj_mirror_kernel<0>, 32,
                                                                    adj_smem_bytes()));
@@ -2978,7 +2987,7 @@ void Projector::adjoint_impl(const float* proj, float* vol, int a_begin, int a_e
             }
         } else {
             if (d_queue_) KCT_CUDA(cudaMemsetAsync(d_queue_, 0, sizeof(int), s));
-            const unsigned grid = d_queue_ ? std::min(nctas, adj_ws_ ? adj_ctas_np_[adj_np_ - 2] : adj_ctas_)
+            const unsigned grid = d_queue_ ? std::min(nctas, adj_ws_ ? adj_ctas_np_[adj_np_ - 1] : adj_ctas_)
                                            : nctas;
             if (adj_ws_)
                 adj_ws_fn(bc.bz == 64 || bc.bz == 32 ? bc.bz : 0, adj_np_)
@@ -3009,14 +3018,15 @@ void Projector::adjoint_impl(const float* proj, float* vol, int a_begin, int a_e
 
 // Producer warps per consumer of the warp-specialised adjoint: 2 or 3,
 // whichever runs this handle's geometry faster (c3: 3 producers 1.96 vs 2.02
-// ms, c4: 2 producers 13.2 vs 13.9 ms, c2: 2).  Timed once at creation on the
+// ms, c4: 2 producers 13.2 vs 13.9 ms, c2: 2; one producer is slower
+// everywhere: c3 2.55, c4 15.6 ms).  Timed once at creation on the
 // first <= 24 angles with non-zero readings (both variants are bit-identical,
 // so a noisy choice changes time, never results).  KCT_ADJ_NP=2|3 forces the
 // choice, KCT_ADJ_TUNE=0 keeps 2.
 void Projector::tune_adjoint() {
     if (!adj_ws_ || !d_queue_) return;
     if (const char* e = std::getenv("KCT_ADJ_NP")) {
-        adj_np_ = std::atoi(e) == 3 ? 3 : 2;
+        adj_np_ = std::clamp(std::atoi(e), 1, 3);
         return;
     }
     const char* te = std::getenv("KCT_ADJ_TUNE");

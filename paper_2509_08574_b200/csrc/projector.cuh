@@ -191,7 +191,7 @@ class Projector {
     unsigned* d_fdone_ = nullptr;     // finished columns per pipeline chunk
     int* d_queue_ = nullptr;          // adjoint brick queue counter
     int adj_ctas_ = 0;                // resident CTAs of the persistent adjoint grid
-    int adj_ctas_np_[2] = {0, 0};     // ... of the warp-specialised kernel with 2 / 3 producers
+    int adj_ctas_np_[3] = {0, 0, 0};  // ... of the warp-specialised kernel with 1 / 2 / 3 producers
     int adj_np_ = 2;                  // producer warps per consumer (tune_adjoint)
     int adj_groups_ = 1;              // angle groups of the adjoint (small problems)
     float* d_part_ = nullptr;         // (adj_groups_ - 1) partial volumes
