@@ -108,8 +108,11 @@ struct Pinned {
     }
 };
 inline Pinned& pinned() {
-    static Pinned p;
-    return p;
+    // never destroyed: its buffers belong to the CUDA context, which may be
+    // gone by the time static destructors run at process exit (the page-locked
+    // memory goes with the process)
+    static Pinned* const p = new Pinned;
+    return *p;
 }
 
 // double -> float; returns false if any value is not finite (the caller
@@ -252,8 +255,11 @@ struct HandleCache {
 };
 
 inline HandleCache& handle_cache() {
-    static HandleCache c;
-    return c;
+    // never destroyed (see pinned()): cached handles are released by
+    // clear_handle_cache() or with the process, never by a static destructor
+    // racing the CUDA runtime's own teardown
+    static HandleCache* const c = new HandleCache;
+    return *c;
 }
 
 struct CheckedOut {
