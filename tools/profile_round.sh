@@ -14,8 +14,9 @@ echo "c5 rc=$?"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
     python bench.py --steps 2 --warmup 3 --skip-recon --skip-cpu --skip-e2e --skip-fdk > /dev/null 2>&1
 echo "launches rc=$?"
-# full sections of the two operator kernels (second rep of tools/kprof.py)
-ncu --set full --clock-control none --import-source on -k 'regex:fwd_kernel|adj_brick|adj_mirror' -s 2 -c 2 \
+# full sections of the two operator kernels (second rep of tools/kprof.py; the first 6 adjoint
+# launches are the handle's producer-count tuning, Projector::tune_adjoint)
+ncu --set full --clock-control none --import-source on -k 'regex:fwd_kernel|adj_brick|adj_mirror' -s 8 -c 2 \
     -o gpurun_out/prof_$TAG -f python tools/kprof.py --reps 2 > gpurun_out/prof_$TAG.log 2>&1
 echo "ncu rc=$?"
 # launch list of one warm 20-iteration PICCS (tools/recon_prof.py, second solve)
