@@ -2,6 +2,7 @@
 // host<->device staging, exception -> status-code mapping.  All compute is in
 // projector.cu / solver.cu.
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -179,6 +180,44 @@ int kct_projector_sizes(const kct_projector* h, size_t* domain, size_t* range) {
 
 namespace {
 
+// KCT_TRACE=1: device timeline of the host pipelines (events on both streams,
+// printed to stderr after the call; diagnostics only)
+struct Trace {
+    bool on = false;
+    cudaEvent_t t0 = nullptr;
+    std::vector<std::pair<std::string, cudaEvent_t>> ev;
+    explicit Trace(cudaStream_t s) {
+        const char* e = std::getenv("KCT_TRACE");
+        on = e && e[0] == '1';
+        if (on) {
+            cudaEventCreate(&t0);
+            cudaEventRecord(t0, s);
+        }
+    }
+    void mark(const std::string& name, cudaStream_t s) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        ev.emplace_back(name, e);
+    }
+    void dump(const char* what) {
+        if (!on) return;
+        std::string line = std::string("[kct trace] ") + what + ":";
+        for (auto& [name, e] : ev) {
+            float ms = 0.f;
+            cudaEventSynchronize(e);
+            cudaEventElapsedTime(&ms, t0, e);
+            char buf[64];
+            std::snprintf(buf, sizeof buf, " %s=%.3f", name.c_str(), ms);
+            line += buf;
+            cudaEventDestroy(e);
+        }
+        cudaEventDestroy(t0);
+        std::fprintf(stderr, "%s\n", line.c_str());
+    }
+};
+
 // Host-buffer forward, pipelined: the projections of angle chunk c leave the
 // device (layout transpose + D2H on the copy stream) while chunk c + 1 is
 // computed.  Same kernels and results as the unpipelined path.
@@ -200,6 +239,7 @@ bool forward_host_staged(kct::Projector& P, const float* vol, float* proj, cudaS
     float* qr = P.scratch(3, N);
     unsigned* done = P.fwd_done();
     const int K = P.pipe_chunks();
+    Trace tr(s);
     KCT_CUDA(cudaMemsetAsync(done, 0, K * sizeof(unsigned), s));
     KCT_CUDA(cudaEventRecord(P.upload_event(), s));  // the copy stream starts after this call's
     KCT_CUDA(cudaStreamWaitEvent(sc, P.upload_event(), 0));  // earlier work and sees the reset
@@ -217,13 +257,60 @@ bool forward_host_staged(kct::Projector& P, const float* vol, float* proj, cudaS
                                      (size_t)(pc.second - pc.first) * plane * sizeof(float),
                                      cudaMemcpyHostToDevice, sc));
         KCT_CUDA(cudaEventRecord(P.pipe_event(k), sc));
+        tr.mark("up" + std::to_string(k), sc);
+    }
+    const size_t per = N / (size_t)P.n_angles();
+    if (P.fwd_rowstages()) {
+        // every stage's rows (all angles) leave the device as soon as the
+        // stage is done: native -> reference transpose of the stage's row
+        // band(s) and one strided copy per band on the copy stream, so only
+        // the last stage's share of the projections is left when the kernels end
+        const int nv = P.dev_geom().nv, nu = P.dev_geom().nu, na = P.n_angles();
+        const bool mir = P.mirror();
+        for (int k = 0; k < S; ++k) {
+            KCT_CUDA(cudaStreamWaitEvent(s, P.pipe_event(k), 0));
+            for (auto& pc : pieces[k]) P.vol_to_padded_z(tmp, pc.first, pc.second, s);
+            tr.mark("pad" + std::to_string(k), s);
+            P.forward_stage(k, q, nullptr, s);
+            tr.mark("stage" + std::to_string(k), s);
+            KCT_CUDA(cudaEventRecord(P.pipe_event(k), s));  // (its upload wait is already enqueued)
+            KCT_CUDA(cudaStreamWaitEvent(sc, P.pipe_event(k), 0));
+            const int r0 = st[k].row0, r1 = st[k].row0 + 32 * st[k].C;
+            std::pair<int, int> bands[2];
+            int nb = 0;
+            if (mir) {  // pairs [r0, r1): rows nv/2 - r1 .. nv/2 - r0 and their mirrors
+                const int h = nv / 2;
+                if (r0 == 0) bands[nb++] = {std::max(0, h - r1), std::min(nv, h + r1)};
+                else {
+                    bands[nb++] = {std::max(0, h - r1), h - r0};
+                    bands[nb++] = {h + r0, std::min(nv, h + r1)};
+                }
+            } else {
+                bands[nb++] = {r0, std::min(nv, r1)};
+            }
+            for (int b = 0; b < nb; ++b) {
+                const int v0 = bands[b].first, v1 = bands[b].second;
+                if (v1 <= v0) continue;
+                P.proj_rows_from_native(q, qr, v0, v1, sc);
+                KCT_CUDA(cudaMemcpy2DAsync(proj + (size_t)v0 * nu, per * sizeof(float),
+                                           qr + (size_t)v0 * nu, per * sizeof(float),
+                                           (size_t)(v1 - v0) * nu * sizeof(float), na,
+                                           cudaMemcpyDeviceToHost, sc));
+            }
+            tr.mark("down" + std::to_string(k), sc);
+        }
+        KCT_CUDA(cudaStreamSynchronize(sc));
+        KCT_CUDA(cudaStreamSynchronize(s));
+        tr.dump("forward_host_staged (row stages)");
+        return true;
     }
     for (int k = 0; k < S; ++k) {
         KCT_CUDA(cudaStreamWaitEvent(s, P.pipe_event(k), 0));
         for (auto& pc : pieces[k]) P.vol_to_padded_z(tmp, pc.first, pc.second, s);
+        tr.mark("pad" + std::to_string(k), s);
         P.forward_stage(k, q, k + 1 == S ? done : nullptr, s);
+        tr.mark("stage" + std::to_string(k), s);
     }
-    const size_t per = N / (size_t)P.n_angles();
     for (int c = 0; c < K; ++c) {
         const int a0 = P.pipe_angle(c), a1 = P.pipe_angle(c + 1);
         if (!P.stream_wait_geq(sc, done + c, (unsigned)((a1 - a0) * P.dev_geom().nu)))
@@ -231,9 +318,11 @@ bool forward_host_staged(kct::Projector& P, const float* vol, float* proj, cudaS
         P.proj_from_native_range(q, qr, a0, a1, sc);
         KCT_CUDA(cudaMemcpyAsync(proj + a0 * per, qr + a0 * per, (a1 - a0) * per * sizeof(float),
                                  cudaMemcpyDeviceToHost, sc));
+        tr.mark("down" + std::to_string(c), sc);
     }
     KCT_CUDA(cudaStreamSynchronize(sc));
     KCT_CUDA(cudaStreamSynchronize(s));
+    tr.dump("forward_host_staged");
     return true;
 }
 

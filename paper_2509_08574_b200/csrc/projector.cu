@@ -1942,6 +1942,24 @@ __global__ void transpose_kernel(const float* __restrict__ in, float* __restrict
     }
 }
 
+// Sub-block transpose with leading dimensions and batch strides:
+// in[b * bsi + r * ldi + c] -> out[b * bso + c * ldo + r], r < R, c < Cc.
+__global__ void transpose_sub_kernel(const float* __restrict__ in, float* __restrict__ out, int R,
+                                     int Cc, int ldi, int ldo, size_t bsi, size_t bso) {
+    __shared__ float tile[32][33];
+    const size_t boff = (size_t)blockIdx.z * bsi, ooff = (size_t)blockIdx.z * bso;
+    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int r = r0 + dy, c = c0 + threadIdx.x;
+        if (r < R && c < Cc) tile[dy][threadIdx.x] = in[boff + (size_t)r * ldi + c];
+    }
+    __syncthreads();
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int c = c0 + dy, r = r0 + threadIdx.x;
+        if (r < R && c < Cc) out[ooff + (size_t)c * ldo + r] = tile[threadIdx.x][dy];
+    }
+}
+
 // in[b][r][c] -> out[b][c][r] (row stride of out: ldo >= R)
 void launch_transpose(const float* in, float* out, int B, int R, int Cc, cudaStream_t s,
                       int ldo = 0) {
@@ -2296,6 +2314,15 @@ void Projector::build_tables(const kct_geometry& geom) {
     // upload of the outer slabs overlaps the inner rows' projection
     if (pipe_chunks_ > 1) {
         const char* se = std::getenv("KCT_FWD_STAGED");
+        // KCT_FWD_ROWSTAGES=1: every stage's rows leave the device as soon as
+        // the stage is done (default: only the last stage streams out, per
+        // pipeline chunk of angles).  Measured slower at c3 (2.84 vs 2.66 ms
+        // with stages 1,2,3; 3.06 ms with six one-chunk stages): a stage of C
+        // row chunks shares one xy walk between C rows per lane, so small
+        // stages redo the walk — the kernels of 1,1,1,1,1,1 sum to 2.29 ms
+        // against 1.71 ms in one launch.
+        const char* rs = std::getenv("KCT_FWD_ROWSTAGES");
+        fwd_rowstages_ = rs && rs[0] == '1';
         const int rows = mirror_ ? nv / 2 : nv, T = (rows + 31) / 32;
         std::vector<int> sizes;
         if (const char* ss = std::getenv("KCT_FWD_STAGE_SIZES")) {  // e.g. "2,4" (sweeps)
@@ -2356,7 +2383,7 @@ void Projector::build_tables(const kct_geometry& geom) {
                 for (int a = 0; a < na; ++a)
                     for (int qd = 0; qd < nq; ++qd) {
                         int ck = 0;
-                        while (last && ck + 1 < pipe_chunks_ && a >= pipe_angle(ck + 1)) ++ck;
+                        while (last && !fwd_rowstages_ && ck + 1 < pipe_chunks_ && a >= pipe_angle(ck + 1)) ++ck;
                         key[(size_t)a * nq + qd] = {1e9 * ck - chord[(size_t)a * nq + qd], qd + nq * a};
                     }
                 std::stable_sort(key.begin(), key.end());
@@ -3125,7 +3152,23 @@ bool Projector::adjoint_host_ref(const float* host_proj, float* host, cudaStream
     const int H = (dg_.na >= 4 * kPipeMinAngles && !(sp && sp[0] == '0'))
                       ? std::max(1, dg_.na / first_part)
                       : dg_.na;
+    const char* tre = std::getenv("KCT_TRACE");
+    const bool trace = tre && tre[0] == '1';
+    std::vector<std::pair<std::string, cudaEvent_t>> tev;
+    cudaEvent_t tr0 = nullptr;
+    auto mark = [&](const std::string& name, cudaStream_t st) {
+        if (!trace) return;
+        cudaEvent_t ev;
+        cudaEventCreate(&ev);
+        cudaEventRecord(ev, st);
+        tev.emplace_back(name, ev);
+    };
+    if (trace) {
+        cudaEventCreate(&tr0);
+        cudaEventRecord(tr0, s);
+    }
     KCT_CUDA(cudaMemcpyAsync(tmp, host_proj, H * per * sizeof(float), cudaMemcpyHostToDevice, s));
+    mark("up0", s);
     KCT_CUDA(cudaMemsetAsync(d_level_, 0, (size_t)nslots * sizeof(unsigned), s));
     KCT_CUDA(cudaEventRecord(pipe_ev_[0], s));  // copy stream: after this call's earlier work
     KCT_CUDA(cudaStreamWaitEvent(sc, pipe_ev_[0], 0));  // and sees the reset counters
@@ -3133,13 +3176,16 @@ bool Projector::adjoint_host_ref(const float* host_proj, float* host, cudaStream
         KCT_CUDA(cudaMemcpyAsync(tmp + H * per, host_proj + H * per, (dg_.na - H) * per * sizeof(float),
                                  cudaMemcpyHostToDevice, sc));
     KCT_CUDA(cudaEventRecord(up_ev_, sc));
+    mark("up1", sc);
     proj_to_native_range(tmp, q, 0, H, s);
     if (H < dg_.na) {
         adjoint_impl(q, dev, 0, H, false, true, nullptr, s);
+        mark("adj0", s);
         KCT_CUDA(cudaStreamWaitEvent(s, up_ev_, 0));
         proj_to_native_range(tmp, q, H, dg_.na, s);
     }
     adjoint_impl(q, dev, H < dg_.na ? H : 0, dg_.na, H < dg_.na, true, d_level_, s);
+    mark("adj1", s);
     const size_t plane = (size_t)dg_.nx * dg_.ny;
     // (level L, y part q): brick rows bj with bj * NP / nby == q, i.e. voxel
     // rows [J0, J1) of slabs [k0, k1) (and, with z-mirror pairs, of their
@@ -3170,10 +3216,25 @@ bool Projector::adjoint_host_ref(const float* host_proj, float* host, cudaStream
                 KCT_CUDA(cudaMemcpy2DAsync(host + u0 * plane + row0, pitch, dev + u0 * plane + row0,
                                            pitch, width, k1 - k0, cudaMemcpyDeviceToHost, sc));
             }
+            mark("L" + std::to_string(L) + "p" + std::to_string(q), sc);
         }
     }
     KCT_CUDA(cudaStreamSynchronize(sc));
     KCT_CUDA(cudaStreamSynchronize(s));
+    if (trace) {
+        std::string line = "[kct trace] adjoint_host_ref:";
+        for (auto& [name, ev] : tev) {
+            float ms = 0.f;
+            cudaEventSynchronize(ev);
+            cudaEventElapsedTime(&ms, tr0, ev);
+            char buf[64];
+            std::snprintf(buf, sizeof buf, " %s=%.3f", name.c_str(), ms);
+            line += buf;
+            cudaEventDestroy(ev);
+        }
+        cudaEventDestroy(tr0);
+        std::fprintf(stderr, "%s\n", line.c_str());
+    }
     return true;
 }
 
@@ -3195,6 +3256,16 @@ void Projector::proj_to_native_range(const float* ref, float* nat, int a0, int a
                                      cudaStream_t s) const {
     const size_t off = (size_t)a0 * dg_.nu * dg_.nv;
     launch_transpose(ref + off, nat + off, a1 - a0, dg_.nv, dg_.nu, s);
+}
+// detector rows [v0, v1) of every angle: native [a][iu][iv] -> reference [a][iv][iu]
+void Projector::proj_rows_from_native(const float* nat, float* ref, int v0, int v1,
+                                      cudaStream_t s) const {
+    if (v1 <= v0) return;
+    const size_t per = (size_t)dg_.nu * dg_.nv;
+    dim3 grid((v1 - v0 + 31) / 32, (dg_.nu + 31) / 32, dg_.na);
+    transpose_sub_kernel<<<grid, dim3(32, 8), 0, s>>>(nat + v0, ref + (size_t)v0 * dg_.nu, dg_.nu,
+                                                     v1 - v0, dg_.nv, dg_.nu, per, per);
+    KCT_LAUNCHED();
 }
 void Projector::proj_from_native_range(const float* nat, float* ref, int a0, int a1,
                                        cudaStream_t s) const {

@@ -83,6 +83,7 @@ class Projector {
         size_t order_off;  // its block order in d_fstage_
     };
     const std::vector<FwdStage>& fwd_stages() const { return fstages_; }
+    bool fwd_rowstages() const { return fwd_rowstages_; }
     void forward_stage(int stage, float* proj, unsigned* done, cudaStream_t s) const;
     // enqueue on `sc`: wait until *addr >= value (cuStreamWaitValue32); false
     // when stream memory operations are unavailable (nothing enqueued)
@@ -99,6 +100,7 @@ class Projector {
     void proj_from_native(const float* nat, float* ref, cudaStream_t s) const;
     void proj_to_native_range(const float* ref, float* nat, int a0, int a1, cudaStream_t s) const;
     void proj_from_native_range(const float* nat, float* ref, int a0, int a1, cudaStream_t s) const;
+    void proj_rows_from_native(const float* nat, float* ref, int v0, int v1, cudaStream_t s) const;
 
     // Lazily allocated scratch used by the C-ABI for host / reference-layout calls.
     float* scratch(int slot, size_t n);
@@ -176,6 +178,7 @@ class Projector {
     cudaEvent_t up_ev_ = nullptr;
     int fwd_split_z_ = 0, fwd_split_lo_ = 0;
     std::vector<FwdStage> fstages_;   // staged host forward (empty: not used)
+    bool fwd_rowstages_ = false;      // ... every stage's rows are copied out as the stage ends (opt-in)
     unsigned* d_ftab_off_ = nullptr;  // forward walk table: segment offsets [angle][column + 1]
     void* d_ftab_ = nullptr;          // ... segments (int2: bits of wb, padded column)
     unsigned long long ftab_segs_ = 0;

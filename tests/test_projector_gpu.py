@@ -631,10 +631,38 @@ def test_staged_host_forward_is_bitwise(monkeypatch, cfg, n_angles):
     staged = A.apply(x2)
     dev = A.proj_from_native(A.apply(A.volume_to_native(torch.from_numpy(x2).cuda()))).cpu().numpy()
     assert np.array_equal(staged, dev)
+    # every stage's rows streaming out as the stage ends (opt-in), other stage sizes
+    monkeypatch.setenv("KCT_FWD_ROWSTAGES", "1")
+    assert np.array_equal(projector(grid, geom).apply(x2), staged)
+    for sizes in ("1,1,1,1,1,1", "2,1,3", "1,4"):
+        monkeypatch.setenv("KCT_FWD_STAGE_SIZES", sizes)
+        assert np.array_equal(projector(grid, geom).apply(x2), staged), sizes
+    monkeypatch.delenv("KCT_FWD_ROWSTAGES")
+    assert np.array_equal(projector(grid, geom).apply(x2), staged)
+    monkeypatch.delenv("KCT_FWD_STAGE_SIZES")
     monkeypatch.setenv("KCT_FWD_STAGED", "0")
     B = projector(grid, geom)
     assert B.info("fwd_stages") == 0
     assert np.array_equal(B.apply(x2), staged)
+
+
+def test_staged_host_forward_without_mirror_symmetry(monkeypatch):
+    """A detector offset in v breaks the z-mirror symmetry: the staged host
+    forward then walks single rows (one row band per stage) — same bits as the
+    device-resident forward."""
+    import torch
+    from oracle import Geometry, Grid, uniform_angles
+    grid = Grid(128, 128, 128, 0.8, 0.8, 0.8)
+    geom = Geometry(1000.0, 1500.0, 192, 200, 0.8, 0.8, uniform_angles(24), 0.0, 3.3)
+    gs, ge = to_pkg(grid, geom)
+    x = np.random.default_rng(52).uniform(0, 0.04, grid.count).astype(np.float32)
+    for rowstages in ("0", "1"):
+        monkeypatch.setenv("KCT_FWD_ROWSTAGES", rowstages)
+        A = k.ConeBeamProjector(gs, ge)
+        assert A.info("mirror") == 0
+        host = A.apply(x)
+        dev = A.proj_from_native(A.apply(A.volume_to_native(torch.from_numpy(x).cuda()))).cpu().numpy()
+        assert np.array_equal(host, dev)
 
 
 @pytest.mark.parametrize("cfg,n_angles", [(1, 64), (2, 9), (3, 6), (4, 2), (5, 5)])
