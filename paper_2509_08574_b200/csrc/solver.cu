@@ -92,6 +92,10 @@ __device__ __forceinline__ void write_partials(double* part, int slot, double v,
 
 // ---- weights + smoothed-TV sums (tv_weights diffreg.hpp:142-156; ----------
 // smoothed_tv :118-126; the PIPLE quadratic of recon.hpp:107-114) ----------
+// w = r^(-1/2) with r = sqrt(|grad|^2 + tau^2): r by the IEEE square root (it
+// also enters the smoothed-TV sums), w by rsqrtf (<= 2 ulp; a second square
+// root and a division measured 94 vs 73 us per launch of the issue-bound
+// tile kernel at c3) — the same expression in all three weight kernels.
 __global__ void __launch_bounds__(kBlock) k_weights(const float* __restrict__ x,
                                                     const float* __restrict__ xp,
                                                     float* __restrict__ w1, float* __restrict__ w2,
@@ -110,7 +114,7 @@ __global__ void __launch_bounds__(kBlock) k_weights(const float* __restrict__ x,
             const float m2 = gx * gx + gy * gy + gz * gz + c.tau2;
             const float r = sqrtf(m2);
             t1 += (double)r;
-            if (write_w) w1[v] = 1.f / sqrtf(r);
+            if (write_w) w1[v] = rsqrtf(r);
         }
         if (c.mode2 == 1) {
             const float dv = xv - xp[v];
@@ -119,7 +123,7 @@ __global__ void __launch_bounds__(kBlock) k_weights(const float* __restrict__ x,
             const float gz = k + 1 < c.nz ? (x[v + 1] - xp[v + 1]) - dv : 0.f;
             const float r = sqrtf(gx * gx + gy * gy + gz * gz + c.tau2);
             t2 += (double)r;
-            if (write_w) w2[v] = 1.f / sqrtf(r);
+            if (write_w) w2[v] = rsqrtf(r);
         } else if (c.mode2 == 2) {
             const double d = (double)xv - (double)xp[v];
             t2 += d * d;
@@ -275,7 +279,7 @@ __global__ void __launch_bounds__(kBlock) k_weights4(const float* __restrict__ x
                 const float gz = k + q + 1 < c.nz ? X.f[q + 2] - xv : 0.f;
                 const float r = sqrtf(gx * gx + gy * gy + gz * gz + c.tau2);
                 if (ok) t1 += (double)r;
-                o1[q] = 1.f / sqrtf(r);
+                o1[q] = rsqrtf(r);
             }
             if (c.mode2 == 1) {
                 const float dv = xv - P.f[q + 1];
@@ -284,7 +288,7 @@ __global__ void __launch_bounds__(kBlock) k_weights4(const float* __restrict__ x
                 const float gz = k + q + 1 < c.nz ? (X.f[q + 2] - P.f[q + 2]) - dv : 0.f;
                 const float r = sqrtf(gx * gx + gy * gy + gz * gz + c.tau2);
                 if (ok) t2 += (double)r;
-                o2[q] = 1.f / sqrtf(r);
+                o2[q] = rsqrtf(r);
             } else if (c.mode2 == 2) {
                 const double d = (double)xv - (double)P.f[q + 1];
                 if (ok) t2 += d * d;
@@ -896,7 +900,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_weights4t(const __grid_constant__
                 const float gz = k + q + 1 < c.nz ? xf[q + 1] - xv : 0.f;
                 const float r = sqrtf(gx * gx + gy * gy + gz * gz + c.tau2);
                 if (ok) t1 += (double)r;
-                o1[q] = 1.f / sqrtf(r);
+                o1[q] = rsqrtf(r);
             }
             if (m2) {
                 const float dv = xv - pf[q];
@@ -905,7 +909,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_weights4t(const __grid_constant__
                 const float gz = k + q + 1 < c.nz ? (xf[q + 1] - pf[q + 1]) - dv : 0.f;
                 const float r = sqrtf(gx * gx + gy * gy + gz * gz + c.tau2);
                 if (ok) t2 += (double)r;
-                o2[q] = 1.f / sqrtf(r);
+                o2[q] = rsqrtf(r);
             } else if (m3) {
                 const double d = (double)xv - (double)pf[q];
                 if (ok) t2 += d * d;
