@@ -2179,9 +2179,11 @@ void Projector::build_tables(const kct_geometry& geom) {
     }
     dg_.full_footprint = full_fp ? 1 : 0;
 
-    // forward launch shape: rows (mirror: row pairs) per warp = 32*C, C <= 4
+    // forward launch shape: rows (mirror: row pairs) per warp = 32*C, C <= 3
+    // (C = 4 costs registers and occupancy: c4 with 12 chunks, 3 bands of 4
+    // 12.59 ms, 4 bands of 3 11.56 ms, 6 bands of 2 12.33 ms; KCT_FWD_C: up to 4)
     const int chunks = ((mirror_ ? nv / 2 : nv) + 31) / 32;
-    int cmax = 4;
+    int cmax = 3;
     if (const char* e = std::getenv("KCT_FWD_C")) cmax = std::clamp(std::atoi(e), 1, 4);
     fwd_bands_ = (chunks + cmax - 1) / cmax;
     fwd_c_ = (chunks + fwd_bands_ - 1) / fwd_bands_;
