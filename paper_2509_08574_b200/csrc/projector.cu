@@ -2323,8 +2323,15 @@ void Projector::build_tables(const kct_geometry& geom) {
         // row chunks shares one xy walk between C rows per lane, so small
         // stages redo the walk — the kernels of 1,1,1,1,1,1 sum to 2.29 ms
         // against 1.71 ms in one launch.
+        // Tall detectors (more than 6 row chunks; c4: 12) do take it: their
+        // outermost stage mostly misses the volume and ends at once, so the
+        // angle-chunk scheme leaves the whole download exposed (c4 host
+        // forward 22.1 ms; row stages of 1,2,3,4,2 chunks 20.0 ms, of
+        // 2,3,3,2,2 chunks 18.7 ms — a short first stage to start early,
+        // 3-chunk stages in the middle, short ones last for a short tail).
         const char* rs = std::getenv("KCT_FWD_ROWSTAGES");
         fwd_rowstages_ = rs && rs[0] == '1';
+        const bool rows_auto = !rs && ((mirror_ ? nv / 2 : nv) + 31) / 32 > 6;
         const int rows = mirror_ ? nv / 2 : nv, T = (rows + 31) / 32;
         std::vector<int> sizes;
         if (const char* ss = std::getenv("KCT_FWD_STAGE_SIZES")) {  // e.g. "2,4" (sweeps)
@@ -2338,7 +2345,20 @@ void Projector::build_tables(const kct_geometry& geom) {
             }
             while (t < T) sizes.push_back(std::min(4, T - t)), t += sizes.back();
         } else {
-            for (int t = 0, c = 1; t < T; c = std::min(c + 1, 4)) {
+            if (rows_auto) {
+                std::vector<int> cand = {2};
+                int rem = T - 6;
+                for (; rem >= 3; rem -= 3) cand.push_back(3);
+                if (rem > 0) cand.push_back(rem);
+                cand.push_back(2);
+                cand.push_back(2);
+                if ((int)cand.size() <= kPipeChunks) {
+                    sizes = cand;
+                    fwd_rowstages_ = true;
+                }
+            }
+            const bool have = !sizes.empty();
+            for (int t = 0, c = 1; !have && t < T; c = std::min(c + 1, 4)) {
                 sizes.push_back(std::min(c, T - t));
                 t += sizes.back();
             }
