@@ -62,13 +62,16 @@ class NativeComm:
     explicit (rank, world, id) or bootstrap over a torch.distributed group
     (`NativeComm.from_group`: rank 0's unique id is broadcast as an object)."""
 
-    def __init__(self, rank: int, world: int, uid: bytes):
+    def __init__(self, rank: int, world: int, uid: bytes, device: int | None = None):
         lib = load_library()
         if len(uid) != ID_BYTES:
             raise ValueError(f"unique id must be {ID_BYTES} bytes")
+        if device is None:  # torch's current device, named explicitly
+            import torch
+            device = torch.cuda.current_device()
         h = C.c_void_p()
         buf = C.create_string_buffer(bytes(uid), ID_BYTES)
-        _check(lib.kct_comm_create(int(rank), int(world), buf, -1, C.byref(h)))
+        _check(lib.kct_comm_create(int(rank), int(world), buf, int(device), C.byref(h)))
         self.handle, self.rank, self.world = h, int(rank), int(world)
 
     @staticmethod
