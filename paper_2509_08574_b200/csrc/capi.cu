@@ -260,6 +260,10 @@ bool forward_host_staged(kct::Projector& P, const float* vol, float* proj, cudaS
         tr.mark("up" + std::to_string(k), sc);
     }
     const size_t per = N / (size_t)P.n_angles();
+    // the stages write the reference layout themselves (KCT_FWD_REFOUT=0: native
+    // layout + a transpose kernel per output piece on the copy stream)
+    const char* ro = std::getenv("KCT_FWD_REFOUT");
+    const bool refout = !(ro && ro[0] == '0');
     if (P.fwd_rowstages()) {
         // every stage's rows (all angles) leave the device as soon as the
         // stage is done: native -> reference transpose of the stage's row
@@ -271,7 +275,7 @@ bool forward_host_staged(kct::Projector& P, const float* vol, float* proj, cudaS
             KCT_CUDA(cudaStreamWaitEvent(s, P.pipe_event(k), 0));
             for (auto& pc : pieces[k]) P.vol_to_padded_z(tmp, pc.first, pc.second, s);
             tr.mark("pad" + std::to_string(k), s);
-            P.forward_stage(k, q, nullptr, s);
+            P.forward_stage(k, refout ? qr : q, nullptr, s, refout);
             tr.mark("stage" + std::to_string(k), s);
             KCT_CUDA(cudaEventRecord(P.pipe_event(k), s));  // (its upload wait is already enqueued)
             KCT_CUDA(cudaStreamWaitEvent(sc, P.pipe_event(k), 0));
@@ -291,7 +295,7 @@ bool forward_host_staged(kct::Projector& P, const float* vol, float* proj, cudaS
             for (int b = 0; b < nb; ++b) {
                 const int v0 = bands[b].first, v1 = bands[b].second;
                 if (v1 <= v0) continue;
-                P.proj_rows_from_native(q, qr, v0, v1, sc);
+                if (!refout) P.proj_rows_from_native(q, qr, v0, v1, sc);
                 KCT_CUDA(cudaMemcpy2DAsync(proj + (size_t)v0 * nu, per * sizeof(float),
                                            qr + (size_t)v0 * nu, per * sizeof(float),
                                            (size_t)(v1 - v0) * nu * sizeof(float), na,
@@ -308,14 +312,14 @@ bool forward_host_staged(kct::Projector& P, const float* vol, float* proj, cudaS
         KCT_CUDA(cudaStreamWaitEvent(s, P.pipe_event(k), 0));
         for (auto& pc : pieces[k]) P.vol_to_padded_z(tmp, pc.first, pc.second, s);
         tr.mark("pad" + std::to_string(k), s);
-        P.forward_stage(k, q, k + 1 == S ? done : nullptr, s);
+        P.forward_stage(k, refout ? qr : q, k + 1 == S ? done : nullptr, s, refout);
         tr.mark("stage" + std::to_string(k), s);
     }
     for (int c = 0; c < K; ++c) {
         const int a0 = P.pipe_angle(c), a1 = P.pipe_angle(c + 1);
         if (!P.stream_wait_geq(sc, done + c, (unsigned)((a1 - a0) * P.dev_geom().nu)))
             throw kct::CudaError("forward: stream wait failed");
-        P.proj_from_native_range(q, qr, a0, a1, sc);
+        if (!refout) P.proj_from_native_range(q, qr, a0, a1, sc);
         KCT_CUDA(cudaMemcpyAsync(proj + a0 * per, qr + a0 * per, (a1 - a0) * per * sizeof(float),
                                  cudaMemcpyDeviceToHost, sc));
         tr.mark("down" + std::to_string(c), sc);

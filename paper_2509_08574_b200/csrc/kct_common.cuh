@@ -128,6 +128,7 @@ struct DevGeom {
     int fwd_band0;         // first row band of this launch
     int fwd_row0;          // row (mirror: row pair) of band 0's first lane (staged host forward)
     int mirror;            // 1: z-mirror geometry, rows iv / nv-1-iv walked as pairs (fwd_kernel MIR)
+    int out_ref;           // 1: the forward writes the reference layout [a][iv][iu] (staged host forward)
 };
 
 // ---- deterministic fp64 block reduction ----------------------------------

@@ -35,7 +35,9 @@ constexpr unsigned kFull = 0xffffffffu;
 // overlapping voxel columns are served from L1.
 // ----------------------------------------------------------------------------
 #ifndef KCT_FWD_MINB
-#define KCT_FWD_MINB 6  // <= 80 registers: 6 CTAs of 4 warps per SM
+#define KCT_FWD_MINB 8  // 64 registers, 8 CTAs of 4 warps per SM (re-swept with the walk table and row
+                        // pairs: 6 / 8 / 9 / 10 / 12 -> c3 1.709 / 1.666 / 1.672 / 1.728 / 2.121 ms, c4 11.55 /
+                        // 10.81 / 10.61 / 10.78 ms, c2 0.187 / 0.173 / 0.179 ms; 9 and up spill)
 #endif
 #ifndef KCT_FWD_WARPS
 #define KCT_FWD_WARPS 4  // adjacent detector columns per CTA (shared voxel columns in L1)
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(128) fwd_tab_build(const ColParams* __restrict
 // its zcross gives these values, adj_weight_kernel), so per xy segment and per
 // z crossing one test serves two rays, which load slabs k and nz-1-k.  Pairs
 // are numbered from the centre plane outwards (band 0: the rows nearest z = 0).
-template <int C, bool COUNT, bool DONE = false, bool MIR = false, bool TAB = false>
+template <int C, bool COUNT, bool DONE = false, bool MIR = false, bool TAB = false, bool REF = false>
 __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const float* __restrict__ vol,
                                                   float* __restrict__ out,
                                                   const ColParams* __restrict__ cols,
@@ -262,21 +264,28 @@ __global__ void __launch_bounds__(kFwdWarps * 32, KCT_FWD_MINB) fwd_kernel(const
         }
     }
 
-    float* o = out + ((size_t)a * g.nu + iu) * g.nv;
+    // native layout [a][iu][iv] (a warp's rows are contiguous), or — REF, the
+    // staged host forward — the reference layout [a][iv][iu] directly: the
+    // strided stores merge in L2 (the projections fit) and the copy stream
+    // needs no transpose kernel, which had to squeeze in between the forward's
+    // blocks (a template flag: as a run-time flag it cost the device-resident
+    // forward 1.6-2%)
+    float* o = REF ? out + (size_t)a * g.nu * g.nv + iu : out + ((size_t)a * g.nu + iu) * g.nv;
+    const size_t os = REF ? (size_t)g.nu : 1;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
         const int p = iv0 + 32 * c;
         if (p < nrows) {
             const int iv = MIR ? g.nv / 2 - 1 - p : p;
             if (COUNT) {
-                o[iv] = acc[c];
-                if (MIR) o[g.nv - 1 - iv] = acc[c];  // the mirror's pieces are the primary's
+                o[iv * os] = acc[c];
+                if (MIR) o[(g.nv - 1 - iv) * os] = acc[c];  // the mirror's pieces are the primary's
             } else {
                 // the mirror's 3D length factor is the primary's (dv(nv-1-iv) = -dv(iv))
                 const float q = dvv[c] * cp.inv_l;
                 const float f = __fsqrt_rn(__fmaf_rn(q, q, 1.f));
-                o[iv] = acc[c] * f;
-                if (MIR) o[g.nv - 1 - iv] = accm[c] * f;
+                o[iv * os] = acc[c] * f;
+                if (MIR) o[(g.nv - 1 - iv) * os] = accm[c] * f;
             }
         }
     }
@@ -2799,16 +2808,16 @@ __global__ void __launch_bounds__(256) adj_group_sum(float* __restrict__ out,
 }
 
 // ---- launches -----------------------------------------------------------------
-template <bool COUNT, bool MIR, bool DONE, bool TAB>
+template <bool COUNT, bool MIR, bool DONE, bool TAB, bool REF = false>
 static void launch_fwd_c(int C, dim3 g1, int th, cudaStream_t s, const float* vol, float* out,
                          const ColParams* cols, const float* dv, const float* invdv,
                          const double* dvd, const DevGeom& gg, const int* order, const FwdChunks& fc,
                          const FwdTab& tab) {
     switch (C) {
-    case 1: fwd_kernel<1, COUNT, DONE, MIR, TAB><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc, tab); break;
-    case 2: fwd_kernel<2, COUNT, DONE, MIR, TAB><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc, tab); break;
-    case 3: fwd_kernel<3, COUNT, DONE, MIR, TAB><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc, tab); break;
-    default: fwd_kernel<4, COUNT, DONE, MIR, TAB><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc, tab); break;
+    case 1: fwd_kernel<1, COUNT, DONE, MIR, TAB, REF><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc, tab); break;
+    case 2: fwd_kernel<2, COUNT, DONE, MIR, TAB, REF><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc, tab); break;
+    case 3: fwd_kernel<3, COUNT, DONE, MIR, TAB, REF><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc, tab); break;
+    default: fwd_kernel<4, COUNT, DONE, MIR, TAB, REF><<<g1, th, 0, s>>>(vol, out, cols, dv, invdv, dvd, gg, order, fc, tab); break;
     }
     KCT_LAUNCHED();
 }
@@ -2830,6 +2839,16 @@ static void launch_fwd_t(int C, int bands, int band0, const float* vol, float* o
     FwdChunks fc{};
     if (done) fc = *done;
     const bool tb = !COUNT && tab.off;
+    if (!COUNT && gg.out_ref) {  // staged host forward: reference-layout output
+        if (done) {
+            if (tb) launch_fwd_c<false, MIR, true, true, true>(C, g1, th, s, vol, out, cols, dv, invdv, dvd, gg, order, fc, tab);
+            else launch_fwd_c<false, MIR, true, false, true>(C, g1, th, s, vol, out, cols, dv, invdv, dvd, gg, order, fc, tab);
+        } else {
+            if (tb) launch_fwd_c<false, MIR, false, true, true>(C, g1, th, s, vol, out, cols, dv, invdv, dvd, gg, order, fc, tab);
+            else launch_fwd_c<false, MIR, false, false, true>(C, g1, th, s, vol, out, cols, dv, invdv, dvd, gg, order, fc, tab);
+        }
+        return;
+    }
     if (!COUNT && done) {  // host pipeline (counted launch)
         if (tb) launch_fwd_c<false, MIR, true, true>(C, g1, th, s, vol, out, cols, dv, invdv, dvd, gg, order, fc, tab);
         else launch_fwd_c<false, MIR, true, false>(C, g1, th, s, vol, out, cols, dv, invdv, dvd, gg, order, fc, tab);
@@ -2896,10 +2915,12 @@ void Projector::forward_counted(float* proj, int band0, unsigned* done, cudaStre
 }
 // Stage `stage` of the staged host forward (one band: C chunks from row0),
 // counted per pipeline chunk when `done` is set.
-void Projector::forward_stage(int stage, float* proj, unsigned* done, cudaStream_t s) const {
+void Projector::forward_stage(int stage, float* proj, unsigned* done, cudaStream_t s,
+                              bool ref_out) const {
     const FwdStage& f = fstages_[stage];
     DevGeom g = dg_;
     g.fwd_row0 = f.row0;
+    g.out_ref = ref_out ? 1 : 0;
     FwdChunks fc{};
     if (done) {
         fc.count = done;

@@ -84,7 +84,8 @@ class Projector {
     };
     const std::vector<FwdStage>& fwd_stages() const { return fstages_; }
     bool fwd_rowstages() const { return fwd_rowstages_; }
-    void forward_stage(int stage, float* proj, unsigned* done, cudaStream_t s) const;
+    void forward_stage(int stage, float* proj, unsigned* done, cudaStream_t s,
+                       bool ref_out = false) const;
     // enqueue on `sc`: wait until *addr >= value (cuStreamWaitValue32); false
     // when stream memory operations are unavailable (nothing enqueued)
     bool stream_wait_geq(cudaStream_t sc, const unsigned* addr, unsigned value) const;

@@ -631,6 +631,10 @@ def test_staged_host_forward_is_bitwise(monkeypatch, cfg, n_angles):
     staged = A.apply(x2)
     dev = A.proj_from_native(A.apply(A.volume_to_native(torch.from_numpy(x2).cuda()))).cpu().numpy()
     assert np.array_equal(staged, dev)
+    # native-layout stages + transpose kernels on the copy stream
+    monkeypatch.setenv("KCT_FWD_REFOUT", "0")
+    assert np.array_equal(projector(grid, geom).apply(x2), staged)
+    monkeypatch.delenv("KCT_FWD_REFOUT")
     # every stage's rows streaming out as the stage ends (opt-in), other stage sizes
     monkeypatch.setenv("KCT_FWD_ROWSTAGES", "1")
     assert np.array_equal(projector(grid, geom).apply(x2), staged)
