@@ -1623,6 +1623,10 @@ __host__ __device__ constexpr int adj_mir_ws_floats(int bz, int np) {
     return 2 * BX * BY * ((bz + 1) & ~1) + 2 * np * mir_buf_floats((bz + 1) & ~1) + 4 + 8 * np;
 }
 
+#ifndef KCT_MIR_WARPS
+#define KCT_MIR_WARPS 32  // resident warps per SM the register allocation aims at (64 registers; 28 / 36 / 40:
+                          // 72 / 56 / 48 registers, c3 2.06 / 2.03 / 2.31 ms against 1.96 ms)
+#endif
 #ifndef KCT_MIR_NC
 #define KCT_MIR_NC 1  // consumer warps (deposits; 2 / 3 measured slower: 2.51 / 3.14 ms at c3)
 #endif
@@ -1633,7 +1637,7 @@ __host__ __device__ constexpr int adj_mir_ws_floats(int bz, int np) {
 // and share the bricks' clear and write-out (a named barrier between the
 // consumers orders them around the deposits).
 template <int CSC, int NP, int NC>
-__global__ void __launch_bounds__(32 * (NP + NC), 32 / (NP + NC)) adj_mirror_ws_kernel(
+__global__ void __launch_bounds__(32 * (NP + NC), KCT_MIR_WARPS / (NP + NC)) adj_mirror_ws_kernel(
     const float4* __restrict__ rec, const float* __restrict__ ymw, float* __restrict__ out,
     DevGeom g, BrickCfg bc, int a0, int nab, int accumulate, const int* __restrict__ order,
     int* queue, float* __restrict__ out_part, const WalkEntry* __restrict__ tab,
