@@ -1067,6 +1067,10 @@ __global__ void __launch_bounds__(kBlock) k_normq(const float* __restrict__ q, s
 }
 
 // ---- x += a p ; r0 -= a q ; slot4 = ||r0||^2, slot5 = ||x - gt||^2 ---------
+__device__ __forceinline__ bool aligned16(const void* a, const void* b, const void* c = nullptr) {
+    return ((reinterpret_cast<size_t>(a) | reinterpret_cast<size_t>(b) | reinterpret_cast<size_t>(c)) & 15) == 0;
+}
+
 __global__ void __launch_bounds__(kBlock) k_update_xr(float* __restrict__ x,
                                                       const float* __restrict__ p, size_t m,
                                                       float* __restrict__ r,
@@ -1077,13 +1081,41 @@ __global__ void __launch_bounds__(kBlock) k_update_xr(float* __restrict__ x,
     __shared__ double sm[32];
     const float a = (float)ctl->a;
     const size_t stride = (size_t)gridDim.x * blockDim.x;
+    const size_t t0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     double tr = 0.0, te = 0.0;
-    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < m; v += stride) {
+    // four values per thread and step when the buffers allow 16-byte accesses
+    const size_t m4 = aligned16(x, p, gt) ? m / 4 : 0, n4 = aligned16(r, q) ? n / 4 : 0;
+    for (size_t v = t0; v < m4; v += stride) {
+        const float4 pv = __ldg(reinterpret_cast<const float4*>(p) + v);
+        float4 xv = reinterpret_cast<float4*>(x)[v];
+        xv.x = fmaf(a, pv.x, xv.x);
+        xv.y = fmaf(a, pv.y, xv.y);
+        xv.z = fmaf(a, pv.z, xv.z);
+        xv.w = fmaf(a, pv.w, xv.w);
+        reinterpret_cast<float4*>(x)[v] = xv;
+        if (gt) {
+            const float4 g = __ldg(reinterpret_cast<const float4*>(gt) + v);
+            const double d0 = (double)xv.x - (double)g.x, d1 = (double)xv.y - (double)g.y,
+                         d2 = (double)xv.z - (double)g.z, d3 = (double)xv.w - (double)g.w;
+            te += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+        }
+    }
+    for (size_t v = 4 * m4 + t0; v < m; v += stride) {
         const float xv = fmaf(a, p[v], x[v]);
         x[v] = xv;
         if (gt) { const double d = (double)xv - (double)gt[v]; te += d * d; }
     }
-    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n; v += stride) {
+    for (size_t v = t0; v < n4; v += stride) {
+        const float4 qv = __ldg(reinterpret_cast<const float4*>(q) + v);
+        float4 rv = reinterpret_cast<float4*>(r)[v];
+        rv.x = fmaf(-a, qv.x, rv.x);
+        rv.y = fmaf(-a, qv.y, rv.y);
+        rv.z = fmaf(-a, qv.z, rv.z);
+        rv.w = fmaf(-a, qv.w, rv.w);
+        reinterpret_cast<float4*>(r)[v] = rv;
+        tr += (double)rv.x * rv.x + (double)rv.y * rv.y + (double)rv.z * rv.z + (double)rv.w * rv.w;
+    }
+    for (size_t v = 4 * n4 + t0; v < n; v += stride) {
         const float rv = fmaf(-a, q[v], r[v]);
         r[v] = rv;
         tr += (double)rv * (double)rv;
@@ -1091,16 +1123,27 @@ __global__ void __launch_bounds__(kBlock) k_update_xr(float* __restrict__ x,
     write_partials(part, 4, tr, sm);
     write_partials(part, 5, te, sm);
 }
-
-// ---- p = s + beta p (init: p = s) ----------------------------------------
 __global__ void __launch_bounds__(kBlock) k_update_p(float* __restrict__ p,
                                                      const float* __restrict__ s, size_t m,
                                                      const Ctl* ctl, int init) {
     if (ctl->stop) return;
     const float beta = (float)ctl->beta;
-    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < m;
-         v += (size_t)gridDim.x * blockDim.x)
-        p[v] = init ? s[v] : fmaf(beta, p[v], s[v]);
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    const size_t t0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    const size_t m4 = aligned16(p, s) ? m / 4 : 0;
+    for (size_t v = t0; v < m4; v += stride) {
+        const float4 sv = __ldg(reinterpret_cast<const float4*>(s) + v);
+        float4 pv = sv;
+        if (!init) {
+            pv = reinterpret_cast<float4*>(p)[v];
+            pv.x = fmaf(beta, pv.x, sv.x);
+            pv.y = fmaf(beta, pv.y, sv.y);
+            pv.z = fmaf(beta, pv.z, sv.z);
+            pv.w = fmaf(beta, pv.w, sv.w);
+        }
+        reinterpret_cast<float4*>(p)[v] = pv;
+    }
+    for (size_t v = 4 * m4 + t0; v < m; v += stride) p[v] = init ? s[v] : fmaf(beta, p[v], s[v]);
 }
 
 // ---- misc reductions -------------------------------------------------------
