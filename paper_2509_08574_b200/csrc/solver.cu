@@ -1178,31 +1178,30 @@ __global__ void __launch_bounds__(kBlock) k_stats(const float* __restrict__ f, s
     }
 }
 
-__device__ __forceinline__ double slot_sum(const double* part, int slot, double* sm) {
-    double t = 0.0;
-    for (int b = threadIdx.x; b < kGrid; b += blockDim.x) t += part[slot * kGrid + b];
-    const double r = block_sum(t, sm);
-    __syncthreads();
-    return r;  // valid in thread 0
-}
 
 // One-block scalar step: reduces the partials of the preceding kernel(s) in a
 // fixed order and runs the CGLS scalar recurrence (krylov.hpp:68-125).
 __global__ void __launch_bounds__(kBlock) k_scalar(Ctl* ctl, const double* part, int mode,
                                                    double tol, double* res_hist, double* err_hist,
                                                    double* obj_out, int obj_kind) {
-    __shared__ double sm[32];
-    const double s0 = slot_sum(part, 0, sm);
-    double s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0, s5 = 0.0;
-    if (mode == S_TV || mode == S_DELTA || mode == S_GAMMA) {
-        s1 = slot_sum(part, 1, sm);
-        s2 = slot_sum(part, 2, sm);
+    // the slots a mode needs, one warp per slot, all at once (fixed order:
+    // lane l adds partials l, l + 32, ..., then the shuffle tree)
+    __shared__ double ss[8];
+    {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const bool m12 = mode == S_TV || mode == S_DELTA || mode == S_GAMMA;
+        const bool need = warp == 0 || ((warp == 1 || warp == 2) && m12) ||
+                          (warp == 3 && mode == S_REF) || ((warp == 4 || warp == 5) && mode == S_GAMMA);
+        if (warp < 6) {
+            double t = 0.0;
+            if (need)
+                for (int b = lane; b < kGrid; b += 32) t += part[warp * kGrid + b];
+            t = warp_sum(t);
+            if (lane == 0) ss[warp] = t;
+        }
+        __syncthreads();
     }
-    if (mode == S_REF) s3 = slot_sum(part, 3, sm);
-    if (mode == S_GAMMA) {
-        s4 = slot_sum(part, 4, sm);
-        s5 = slot_sum(part, 5, sm);
-    }
+    const double s0 = ss[0], s1 = ss[1], s2 = ss[2], s3 = ss[3], s4 = ss[4], s5 = ss[5];
     if (threadIdx.x != 0) return;
     Ctl& c = *ctl;
     switch (mode) {
