@@ -2512,7 +2512,7 @@ void Projector::build_tables(const kct_geometry& geom) {
     // (adjoint_host_ref copies a (level, part) out as soon as it is final:
     // the last level's copy is then mostly overlapped too)
     {
-        adj_parts_ = 4;
+        adj_parts_ = 6;  // re-swept with the 1.96 ms kernel: 2 / 4 / 6 / 8 -> host adjoint 2.86 / 2.75 / 2.72 / 2.72 ms
         if (const char* e = std::getenv("KCT_ADJ_PARTS")) adj_parts_ = std::max(1, std::atoi(e));
         adj_parts_ = std::min(adj_parts_, (ny + BY - 1) / BY);
     }
@@ -3191,8 +3191,8 @@ bool Projector::adjoint_host_ref(const float* host_proj, float* host, cudaStream
 // the first launch takes 1 / KCT_ADJ_FIRST_PART of the angles, so that it
 // lasts about as long as the rest's upload (round 1, 4 ms kernel: 1/8 best;
 // round 2, 2 ms kernel, c3 host adjoint over 1/2 .. 1/12: 3.12 / 2.91 / 2.82 /
-// 2.86 / 2.97 / 3.03 ms -> 1/4)
-#define KCT_ADJ_FIRST_PART 4
+// 2.86 / 2.97 / 3.03 ms -> 1/4; end of round 2 -> 1/5, below)
+#define KCT_ADJ_FIRST_PART 5  // 1.96 ms kernel, 6 y parts: 1/3 .. 1/8 -> 2.84 / 2.76 / 2.72 / 2.79 / 2.89 ms
 #endif
     int first_part = KCT_ADJ_FIRST_PART;
     if (const char* fp = std::getenv("KCT_ADJ_FIRST_PART")) first_part = std::max(1, std::atoi(fp));
