@@ -7,8 +7,12 @@ angles only and sums, over the ranks, the partial adjoint volume and the
 projection-domain reductions (||A p||^2, ||r0||^2, the objective's data term)
 — NCCL all-reduces over NVLink when torch.distributed runs the nccl backend.
 The regulariser terms are computed redundantly (identical on every rank).
-The collective is injected through the C ABI hook `kct_set_allreduce`
-(include/kct.h); the library itself stays free of any communication runtime.
+The collectives reach the solver through the C ABI hooks `kct_set_allreduce`
+/ `kct_set_slab` (include/kct.h).  Under torch's nccl backend they are served
+by the library's own NCCL communicator (`NativeComm`, `kct_comm_*`: NCCL bound
+at run time, collectives enqueued on the solver's stream without a Python
+trampoline); under gloo (the CPU-side multi-rank tests) or with
+KCT_NATIVE_COMM=0 by torch.distributed callbacks.
 
 y-slab-sharded mode (SURVEY §8e's volume-partitioned variant, `*_slab`):
 rank r holds the y planes [j0, j1) of every volume vector (one halo plane on
